@@ -1,0 +1,234 @@
+/*
+ * reseq_cuda.h -- C ABI of the B200 (sm_100a) backend for the `reseq` hot path:
+ * suffix-array construction over sentinel-joined read sets, the data-parallel
+ * primitives it is made of, SA-driven prefix-range / overlap queries, and the host
+ * greedy superstring merge.
+ *
+ * Every entry point replaces one reference interface (cited as
+ * proj/include/reseq/<file>:<line>, relative to the reference root).  The reference
+ * is a header-only C++ library with no FFI of its own; its extension points are the
+ * `const executor&` argument and `fragment_index::builder`.  INTEGRATION.md shows the
+ * binding a reference maintainer would add (a `builder::cuda` enumerator and an
+ * executor backend that forward to these symbols).
+ *
+ * Conventions
+ *   - plain pointers + sizes; no C++/torch types; no exception crosses this boundary.
+ *   - every function returns an int status (RESEQ_OK == 0); reseq_cuda_last_error()
+ *     gives the message of the calling thread's most recent failure.
+ *   - "host" entry points take HOST buffers and perform H2D / D2H internally
+ *     (pinned buffers are copied at full PCIe rate; pageable ones work too).
+ *   - "_device" entry points take DEVICE pointers (HBM-resident data) and enqueue on
+ *     the context's stream; call reseq_cuda_ctx_synchronize() before reading results.
+ *   - outputs are pre-sized by the caller (value semantics of the reference's
+ *     std::vector returns are provided by the C++ shim in include/reseq_b200/).
+ *   - empty inputs are valid and produce empty outputs (suffix_array.hpp:66,
+ *     scan.hpp:35, radix_sort.hpp:146).
+ *   - one host thread per context at a time (executor.hpp:39-40 has the same rule);
+ *     a finished index is immutable and may be queried concurrently from several
+ *     contexts.
+ *   - there is NO CPU fallback: without a CUDA device every compute entry point
+ *     fails with RESEQ_NO_DEVICE.
+ */
+#ifndef RESEQ_CUDA_H
+#define RESEQ_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The C++ shim maps them back to the reference's exception types
+ * (errors.hpp:9-11,54-61; radix_sort.hpp:171-172). */
+enum reseq_status {
+    RESEQ_OK = 0,
+    RESEQ_INVALID_ARGUMENT = 1, /* std::invalid_argument (e.g. digit_bits not in 1..8) */
+    RESEQ_TEXT_TOO_LARGE = 2,   /* reseq::text_too_large_error */
+    RESEQ_SCAN_OVERFLOW = 3,    /* reseq::scan_overflow_error */
+    RESEQ_CUDA_ERROR = 4,       /* reseq::error carrying the CUDA message */
+    RESEQ_OUT_OF_MEMORY = 5,
+    RESEQ_NO_DEVICE = 6
+};
+
+/* Largest text the device path accepts.  The reference caps at 2^31-1
+ * (suffix_array.hpp:64, sequence.hpp:113-114); positions and rank+1 are u32, so the
+ * device path relaxes the cap to 2^32-2 (needed for the 3 Gbp configuration). */
+#define RESEQ_CUDA_MAX_TEXT 0xFFFFFFFEull
+
+typedef struct reseq_cuda_ctx reseq_cuda_ctx;     /* device + stream + workspace arena */
+typedef struct reseq_cuda_index reseq_cuda_index; /* device-resident fragment index */
+
+/* ---- context ------------------------------------------------------------------ */
+
+/* Replaces: executor construction, executor.hpp:28-37 (the BSP thread pool becomes a
+ * device + stream; `workers`/`chunk_size` have no device meaning). */
+int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out);
+void reseq_cuda_ctx_destroy(reseq_cuda_ctx* ctx);
+/* Launch on an externally owned cudaStream_t (e.g. torch's current stream) so callers
+ * can bracket work with their own events.  NULL restores the context's own stream. */
+int reseq_cuda_ctx_set_stream(reseq_cuda_ctx* ctx, void* cuda_stream);
+int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx);
+/* Number of kernels this context has launched since creation (bench `gpu_launches`). */
+uint64_t reseq_cuda_ctx_launch_count(const reseq_cuda_ctx* ctx);
+/* Bytes currently held by the context's workspace arena. */
+size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
+const char* reseq_cuda_last_error(void);
+const char* reseq_cuda_version(void);
+
+/* ---- L0 primitives ------------------------------------------------------------ */
+
+/* Replaces exclusive_scan, scan.hpp:32-56: out[i] = sum(values[0..i)).  A grand total
+ * above 0xFFFFFFFF returns RESEQ_SCAN_OVERFLOW (scan.hpp:38) and leaves `out`
+ * unspecified. */
+int reseq_cuda_exclusive_scan(reseq_cuda_ctx* ctx, const uint32_t* values, size_t n,
+                              uint32_t* out);
+int reseq_cuda_exclusive_scan_device(reseq_cuda_ctx* ctx, const uint32_t* d_values, size_t n,
+                                     uint32_t* d_out, uint64_t* total_out /* host, nullable */);
+
+/* Replaces split_by_bit, radix_sort.hpp:126-139: stable partition, bit==0 first.
+ * `payload`/`payload_out` may both be NULL (key_array without payload,
+ * radix_sort.hpp:16-23).  bit > 31 is RESEQ_INVALID_ARGUMENT. */
+int reseq_cuda_split_by_bit(reseq_cuda_ctx* ctx, const uint32_t* keys, const uint32_t* payload,
+                            size_t n, unsigned bit, uint32_t* keys_out, uint32_t* payload_out);
+
+/* Replaces radix_sort, radix_sort.hpp:143-161: stable ascending sort on keys, payload
+ * carried.  Implemented as an 8-bit-digit LSD "onesweep" radix sort; passes whose
+ * digit is constant over the whole array are skipped (the analogue of the
+ * reference's sortedness early-exit, radix_sort.hpp:151). */
+int reseq_cuda_radix_sort(reseq_cuda_ctx* ctx, const uint32_t* keys, const uint32_t* payload,
+                          size_t n, uint32_t* keys_out, uint32_t* payload_out);
+int reseq_cuda_radix_sort_device(reseq_cuda_ctx* ctx, const uint32_t* d_keys,
+                                 const uint32_t* d_payload, size_t n, uint32_t* d_keys_out,
+                                 uint32_t* d_payload_out);
+
+/* Replaces chunked_radix_sort, radix_sort.hpp:169-303: same result as radix_sort;
+ * `digit_bits` selects the radix width of the device passes and must be in 1..8,
+ * otherwise RESEQ_INVALID_ARGUMENT (radix_sort.hpp:171-172). */
+int reseq_cuda_chunked_radix_sort(reseq_cuda_ctx* ctx, const uint32_t* keys,
+                                  const uint32_t* payload, size_t n, unsigned digit_bits,
+                                  uint32_t* keys_out, uint32_t* payload_out);
+
+/* ---- L1 suffix array ---------------------------------------------------------- */
+
+/* Per-build statistics (all optional output). */
+typedef struct reseq_sa_stats {
+    uint32_t alphabet;      /* 0 = 2-bit DNA path (bytes in {0,A,C,G,T}), 1 = generic bytes */
+    uint32_t init_symbols;  /* symbols ranked by the initial k-mer sort */
+    uint32_t rounds;        /* prefix-doubling rounds executed */
+    uint32_t sort_passes;   /* radix digit passes executed in total */
+    uint64_t kernel_launches;
+    uint64_t refined_tile;  /* elements re-sorted by the shared-memory group-refine kernel */
+    uint64_t refined_global;/* elements re-sorted by the global radix fallback */
+} reseq_sa_stats;
+
+/* Replaces build_parallel, suffix_array.hpp:61-124 (and therefore build_naive,
+ * :45-54, whose result it equals): sa = suffix positions in the total order of
+ * suffix_less (:28-41), rank = inverse permutation.  n == 0 is valid.
+ * n > RESEQ_CUDA_MAX_TEXT returns RESEQ_TEXT_TOO_LARGE.  `rank` may be NULL. */
+int reseq_cuda_build_sa(reseq_cuda_ctx* ctx, const uint8_t* text, size_t n, uint32_t* sa,
+                        uint32_t* rank, reseq_sa_stats* stats /* nullable */);
+int reseq_cuda_build_sa_device(reseq_cuda_ctx* ctx, const uint8_t* d_text, size_t n,
+                               uint32_t* d_sa, uint32_t* d_rank,
+                               reseq_sa_stats* stats /* nullable, filled after sync */);
+
+/* FNV-1a-64 over the little-endian bytes of a device u32 array == bench::checksum_u32,
+ * bench.hpp:31-48 (host-side fold of per-block partials is exact: FNV is sequential, so
+ * this copies the array back in chunks and folds on the host; a parity fingerprint, not
+ * a timed operator). */
+int reseq_cuda_checksum_u32_device(reseq_cuda_ctx* ctx, const uint32_t* d_v, size_t n,
+                                   uint64_t* out);
+
+/* ---- L2 fragment index -------------------------------------------------------- */
+
+/* Replaces fragment_index::fragment_index(set, builder::scan_radix, exec),
+ * fragment_index.hpp:34-56.  `concat` is fragment_set::concat() (f0 \0 f1 \0 ...,
+ * sequence.hpp:60-92), `starts` fragment_set::starts().  The index owns device copies
+ * of the text (raw + 2-bit packed when DNA), SA, rank, start_rank_list and a k-mer
+ * directory over the SA.  Host inputs need not outlive the call. */
+int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n,
+                            const uint32_t* starts, size_t k, reseq_cuda_index** out);
+void reseq_cuda_index_destroy(reseq_cuda_index* ix);
+size_t reseq_cuda_index_text_len(const reseq_cuda_index* ix);
+size_t reseq_cuda_index_fragments(const reseq_cuda_index* ix);
+/* Copies of fragment_index::sa().sa / .rank / start_rank_list() (fragment_index.hpp:59-61);
+ * any pointer may be NULL. */
+int reseq_cuda_index_get(const reseq_cuda_index* ix, uint32_t* sa, uint32_t* rank,
+                         uint32_t* start_rank_list);
+/* Device pointers to the same arrays (valid until destroy). */
+int reseq_cuda_index_device_ptrs(const reseq_cuda_index* ix, const uint32_t** d_sa,
+                                 const uint32_t** d_rank, const uint32_t** d_start_rank_list);
+
+/* Replaces q calls of fragment_index::locate_prefix_range, fragment_index.hpp:65-70 (the
+ * binary searches of narrow(), :114-148).  Pattern i is pats[pat_off[i] .. pat_off[i+1]);
+ * patterns must be non-empty and free of byte 0.  lo[i], hi[i] receive the half-open SA
+ * interval; an absent pattern yields lo == hi at the lower-bound insertion point. */
+int reseq_cuda_index_locate_batch(reseq_cuda_index* ix, const uint8_t* pats,
+                                  const uint64_t* pat_off, size_t q, uint32_t* lo, uint32_t* hi);
+
+/* Same query where every pattern is a suffix of a fragment already in the text:
+ * pattern i = fragment frag[i] from offset off[i] to its end (a `residual`,
+ * sequence.hpp:96-101).  Nothing but (frag, off) crosses PCIe. */
+int reseq_cuda_index_locate_residuals(reseq_cuda_index* ix, const uint32_t* frag,
+                                      const uint32_t* off, size_t q, uint32_t* lo, uint32_t* hi);
+
+/* Replaces q calls of fragment_index::prefix_related, fragment_index.hpp:72-109, for
+ * patterns given as residuals (the assembler's use, assembler.hpp:74-78,117).  Results are
+ * CSR: list i of each kind occupies [*_off[i], *_off[i+1]) of the malloc'ed id arrays
+ * (each list ascending by id, fragment_index.hpp:105-107).  Free with
+ * reseq_cuda_free_host(). */
+typedef struct reseq_prefix_relations {
+    size_t q;
+    uint64_t *prefixes_off, *extensions_off, *exact_off; /* q+1 each */
+    uint32_t *prefixes, *extensions, *exact;
+} reseq_prefix_relations;
+int reseq_cuda_index_prefix_related_batch(reseq_cuda_index* ix, const uint32_t* frag,
+                                          const uint32_t* off, size_t q,
+                                          reseq_prefix_relations* out);
+void reseq_cuda_prefix_relations_free(reseq_prefix_relations* r);
+
+/* The sparse overlap graph: every (i, j, w) with i != j and
+ * w = overlap_weight(f_i, f_j) >= min_overlap (overlap.hpp:16-23, :35-45 restricted to
+ * non-zero entries), sorted by (i, j).  One query per (fragment, offset) pair with
+ * remaining length >= min_overlap.  Also reports, per fragment, whether
+ * detail::absorb_contained (overlap.hpp:51-67) would drop it.  Arrays are malloc'ed;
+ * free with reseq_cuda_overlaps_free(). */
+typedef struct reseq_overlaps {
+    uint64_t count;       /* number of (i, j, w) triples */
+    uint32_t *i, *j, *w;  /* count entries each, sorted by (i, j) */
+    uint8_t* contained;   /* k flags */
+    uint64_t queries;     /* number of locate-equivalent queries executed */
+    double device_ms;     /* device time of the query + enumeration kernels */
+} reseq_overlaps;
+int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_overlaps* out);
+void reseq_cuda_overlaps_free(reseq_overlaps* o);
+
+/* ---- L3 host merge (stays on the host by design) -------------------------------- */
+
+/* Replaces greedy_superstring_with_order, overlap.hpp:80-113, at scale: consumes the
+ * sparse overlap list (>= min_overlap) and the containment flags from
+ * reseq_cuda_index_overlaps, finishes sub-threshold overlaps among the surviving contigs
+ * exactly, and returns the same superstring and id order the reference's O(k^3) loop
+ * produces.  `superstring` must hold sum(lens) bytes, `order` k entries.  Pure host code;
+ * needs no device. */
+int reseq_greedy_superstring(const uint8_t* concat, size_t n, const uint32_t* starts, size_t k,
+                             const reseq_overlaps* ov, uint32_t min_overlap,
+                             uint8_t* superstring, size_t* superstring_len, uint32_t* order,
+                             size_t* order_len);
+
+/* ---- synthetic workloads (bench.hpp:54-72, shotgun.hpp:20-27) - */
+
+/* genome = "ACGT"[mt19937_64(genome_seed)() & 3] per base. */
+void reseq_synth_random_dna(size_t n, uint64_t seed, uint8_t* out);
+/* keys[i] = (uint32_t) mt19937_64(seed)(), payload[i] = i. */
+void reseq_synth_random_keys(size_t n, uint64_t seed, uint32_t* keys, uint32_t* payload);
+/* k reads of length L drawn forward-strand, error-free, start = bounded rejection draw
+ * from mt19937_64(read_seed); out receives k*(L+1) bytes: read, 0, read, 0, ...;
+ * starts (nullable) receives the k fragment offsets. */
+int reseq_synth_read_text(size_t genome_len, size_t read_len, size_t k, uint64_t genome_seed,
+                          uint64_t read_seed, uint8_t* out, uint32_t* starts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RESEQ_CUDA_H */

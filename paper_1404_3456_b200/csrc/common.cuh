@@ -1,0 +1,121 @@
+// Shared plumbing for the sm_100a backend: context, workspace arena, error handling,
+// small device helpers.  Internal to the library (nothing here is ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "reseq_cuda.h"
+
+namespace rsq {
+
+using u8 = uint8_t;
+using u32 = uint32_t;
+using u64 = uint64_t;
+
+constexpr int kSmCount = 148;  // B200: 2 dies x 74 SMs; grids are sized in multiples of it
+
+void set_last_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define RSQ_CUDA(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return ::rsq::fail(_e == cudaErrorMemoryAllocation ? RESEQ_OUT_OF_MEMORY       \
+                                                               : RESEQ_CUDA_ERROR,         \
+                               std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+    } while (0)
+
+#define RSQ_TRY(expr)                  \
+    do {                               \
+        int _s = (expr);               \
+        if (_s != RESEQ_OK) return _s; \
+    } while (0)
+
+}  // namespace rsq
+
+// The opaque context of the C ABI.
+struct reseq_cuda_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int sm_count = rsq::kSmCount;
+    uint64_t launches = 0;
+
+    // Grow-only bump arena.  begin() rewinds it; alloc() carves 256-byte aligned
+    // blocks.  If the arena is too small the whole block is re-allocated *before* any
+    // carve of the current operation (ops call reserve() with their total first).
+    char* arena = nullptr;
+    size_t arena_cap = 0;
+    size_t arena_used = 0;
+
+    // pinned staging word for small D2H reads (round-termination flags etc.)
+    uint64_t* pinned = nullptr;
+
+    int reserve(size_t bytes);
+    void begin() { arena_used = 0; }
+    template <typename T>
+    T* alloc(size_t count) {
+        size_t bytes = (count * sizeof(T) + 255) & ~size_t{255};
+        if (arena_used + bytes > arena_cap) return nullptr;
+        T* p = reinterpret_cast<T*>(arena + arena_used);
+        arena_used += bytes;
+        return p;
+    }
+    static size_t padded(size_t bytes) { return (bytes + 255) & ~size_t{255}; }
+};
+
+namespace rsq {
+
+// ---- device helpers --------------------------------------------------------------
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Streaming 128-bit global accesses: data touched once per pass should not displace the
+// (small, hot) look-back descriptors and histograms from L1.
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
+    u64 v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled look-back descriptor: status in the top two bits, value below; one 64-bit
+// word so a single relaxed store publishes both atomically.
+constexpr u64 kDescAggregate = 1ull << 62;
+constexpr u64 kDescInclusive = 2ull << 62;
+constexpr u64 kDescValueMask = (1ull << 62) - 1;
+
+inline unsigned bit_width_u64(u64 v) {
+    unsigned b = 0;
+    while (v) {
+        ++b;
+        v >>= 1;
+    }
+    return b;
+}
+
+}  // namespace rsq

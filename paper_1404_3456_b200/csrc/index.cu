@@ -1,0 +1,783 @@
+// Device-resident fragment index and the batched SA binary-search / overlap kernels.
+//
+// Replaces fragment_index (fragment_index.hpp:30-167):
+//   ctor (:34-56)              -> reseq_cuda_index_create: SA by build_sa_device, start
+//                                 ranks by one radix sort of (rank[start(id)], id), plus
+//                                 a k-mer DIRECTORY over the SA that the reference does
+//                                 not have (below)
+//   locate_prefix_range (:65)  -> locate kernels: one thread per pattern, lower/upper
+//   narrow (:114-148)             bound by binary search over SA with packed 32-base
+//                                 compares; the search starts from the directory bucket
+//                                 instead of [0, n)
+//   start_rank_list lower_bound (:95-96) -> same two lower bounds, started from a second
+//                                 directory over the fragment-start suffixes
+//
+// Directory.  For D bases, dir[x] = number of suffixes smaller than the D-base pattern x,
+// x in [0, 4^D].  Every pattern P with |P| >= D and D-prefix x has its whole SA interval,
+// and its lower-bound insertion point when absent, inside [dir[x], dir[x+1]]; so the
+// directory replaces the top ~2D levels of both binary searches by two adjacent loads from
+// an L2-sized table ("staging the top of the search tree on chip").  It is built without
+// the SA: a suffix s is below pattern x iff code(s) <= x, where code(s) = (first D bases,
+// zero padded at a terminator) + (1 if no terminator within D symbols); one histogram over
+// positions and one exclusive scan.  sdir is the same table counted over fragment-start
+// suffixes only, indexing start_rank_list.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "radix.cuh"
+#include "sa.cuh"
+#include "scan.cuh"
+
+using namespace rsq;
+
+struct reseq_cuda_index {
+    reseq_cuda_ctx* ctx = nullptr;
+    size_t n = 0, k = 0;
+    bool dna = false;
+    int dir_bases = 0;
+    u8* d_text = nullptr;
+    u64* d_packed = nullptr;
+    u64* d_sent = nullptr;
+    u32* d_sa = nullptr;
+    u32* d_rank = nullptr;
+    u32* d_starts = nullptr;
+    u32* d_lens = nullptr;
+    u32* d_start_rank = nullptr;  // start_rank_list
+    u32* d_start_frag = nullptr;  // fragment id of each start_rank_list entry
+    u32* d_dir = nullptr;         // 4^D + 1 entries (+1 leading scan slot)
+    u32* d_sdir = nullptr;
+    u32 max_len = 0;
+    std::vector<void*> owned;
+};
+
+namespace {
+
+template <typename T>
+int dev_alloc(reseq_cuda_index* ix, T** p, size_t count) {
+    *p = nullptr;
+    void* raw = nullptr;
+    cudaError_t e = cudaMalloc(&raw, std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RESEQ_OUT_OF_MEMORY, "cudaMalloc failed while building the index");
+    }
+    ix->owned.push_back(raw);
+    *p = static_cast<T*>(raw);
+    return RESEQ_OK;
+}
+
+unsigned grid_1d(const reseq_cuda_ctx* ctx, size_t items, int block, int waves = 16) {
+    size_t want = (items + block - 1) / block;
+    const size_t cap = static_cast<size_t>(ctx->sm_count) * waves;
+    if (want < 1) want = 1;
+    return static_cast<unsigned>(want < cap ? want : cap);
+}
+
+// ---- packed-text access (layout documented in sa.cu) ---------------------------------
+
+__device__ __forceinline__ u64 base_window(const u64* __restrict__ packed, u64 pos) {
+    const u64 w = pos >> 5;
+    const unsigned s = static_cast<unsigned>(pos & 31) * 2;
+    const u64 hi = packed[w], lo = packed[w + 1];
+    return s ? (hi << s) | (lo >> (64 - s)) : hi;
+}
+__device__ __forceinline__ u64 sent_window(const u64* __restrict__ sent, u64 pos) {
+    const u64 w = pos >> 6;
+    const unsigned s = static_cast<unsigned>(pos & 63);
+    const u64 hi = sent[w], lo = sent[w + 1];
+    return s ? (hi << s) | (lo >> (64 - s)) : hi;
+}
+
+struct TextView {
+    const u8* text;
+    const u64* packed;
+    const u64* sent;
+    u64 n;
+};
+
+// Sign of (suffix at `spos`) vs (pattern = text[ppos .. ppos+m)), both read from the packed
+// text, 32 bases per step -- the cmp lambda of fragment_index.hpp:118-128.  A suffix that
+// reaches a sentinel or the end of the text before the pattern is exhausted is smaller.
+__device__ __forceinline__ int cmp_packed(const TextView& tv, u64 spos, u64 ppos, u32 m) {
+    for (u32 c = 0; c < m; c += 32) {
+        const u64 sp = spos + c;
+        if (sp >= tv.n) return -1;
+        const u32 chunk = m - c < 32u ? m - c : 32u;
+        const u32 sw = static_cast<u32>(sent_window(tv.sent, sp) >> 32);
+        u32 valid = sw ? static_cast<u32>(__clz(sw)) : 32u;
+        const u64 rem = tv.n - sp;
+        if (rem < valid) valid = static_cast<u32>(rem);
+        const u32 len = valid < chunk ? valid : chunk;
+        if (len) {
+            const u64 a = base_window(tv.packed, sp);
+            const u64 b = base_window(tv.packed, ppos + c);
+            const u64 diff = (a ^ b) >> (64 - 2 * len);  // only the first `len` bases
+            if (diff) {
+                const int j = (__clzll(diff) - (64 - 2 * static_cast<int>(len))) >> 1;
+                const u32 ca = static_cast<u32>(a >> (62 - 2 * j)) & 3u;
+                const u32 cb = static_cast<u32>(b >> (62 - 2 * j)) & 3u;
+                return ca < cb ? -1 : 1;
+            }
+        }
+        if (valid < chunk) return -1;
+    }
+    return 0;
+}
+
+// Byte-wise form of the same comparison for generic alphabets and host-supplied patterns.
+__device__ __forceinline__ int cmp_bytes(const TextView& tv, u64 spos, const u8* __restrict__ pat, u32 m) {
+    for (u32 t = 0; t < m; ++t) {
+        if (spos + t >= tv.n) return -1;
+        const u32 sc = tv.text[spos + t], pc = pat[t];
+        if (sc != pc) return sc < pc ? -1 : 1;
+    }
+    return 0;
+}
+
+// Lower and upper bound of the pattern inside [l0, r0) -- fragment_index.hpp:129-147.
+template <typename Cmp>
+__device__ __forceinline__ void bounds(const u32* __restrict__ sa, u32 l0, u32 r0, Cmp cmp, u32* lo, u32* hi) {
+    u32 l = l0, r = r0;
+    while (l < r) {
+        const u32 mid = l + ((r - l) >> 1);
+        if (cmp(sa[mid]) < 0) l = mid + 1;
+        else r = mid;
+    }
+    *lo = l;
+    r = r0;
+    while (l < r) {
+        const u32 mid = l + ((r - l) >> 1);
+        if (cmp(sa[mid]) <= 0) l = mid + 1;
+        else r = mid;
+    }
+    *hi = l;
+}
+
+__device__ __forceinline__ u32 lower_bound_u32(const u32* __restrict__ v, u32 l, u32 r, u32 x) {
+    while (l < r) {
+        const u32 mid = l + ((r - l) >> 1);
+        if (v[mid] < x) l = mid + 1;
+        else r = mid;
+    }
+    return l;
+}
+
+// ---- index construction kernels ----------------------------------------------------
+
+__global__ void lens_kernel(const u32* __restrict__ starts, u64 k, u64 n, u32* __restrict__ lens,
+                            const u32* __restrict__ rank, u32* __restrict__ keys, u32* __restrict__ ids,
+                            u32* __restrict__ max_len) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    u32 local_max = 0;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const u64 end = (i + 1 < k ? starts[i + 1] : n) - 1;  // sequence.hpp:78-83
+        const u32 len = static_cast<u32>(end - starts[i]);
+        lens[i] = len;
+        keys[i] = rank[starts[i]];
+        ids[i] = static_cast<u32>(i);
+        local_max = max(local_max, len);
+    }
+    for (int o = 16; o > 0; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+    if (lane_id() == 0 && local_max) atomicMax(max_len, local_max);
+}
+
+// code(s) of the header comment; D <= 16.
+__device__ __forceinline__ u32 dir_code(const u64* __restrict__ packed, const u64* __restrict__ sent,
+                                        u64 n, u64 pos, int D) {
+    const u32 bases = static_cast<u32>(base_window(packed, pos) >> (64 - 2 * D));
+    const u32 sw = static_cast<u32>(sent_window(sent, pos) >> (64 - D));
+    const u32 t = sw ? static_cast<u32>(__clz(sw)) - (32 - D) : D;
+    const u64 rem = n - pos;
+    u32 len = t;
+    if (rem < len) len = static_cast<u32>(rem);
+    if (len >= static_cast<u32>(D)) return bases + 1u;
+    return bases & ~((1u << (2 * (D - len))) - 1u);
+}
+
+// Histogram of code(s) over all positions (positions == nullptr) or over a position list.
+__global__ void dir_hist_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n,
+                                const u32* __restrict__ positions, u64 count, int D,
+                                u32* __restrict__ hist) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const u64 pos = positions ? positions[i] : i;
+        atomicAdd(hist + dir_code(packed, sent, n, pos, D), 1u);
+    }
+}
+
+// ---- query kernels --------------------------------------------------------------------
+
+struct IndexView {
+    TextView tv;
+    const u32* sa;
+    const u32* starts;
+    const u32* lens;
+    const u32* start_rank;
+    const u32* start_frag;
+    const u32* dir;   // dir[x] = lower bound of D-base pattern x; nullptr when absent
+    const u32* sdir;
+    int D;
+    u32 k;
+};
+
+// SA interval of the pattern text[ppos .. ppos+m) (a residual).
+__device__ __forceinline__ void locate_residual(const IndexView& iv, u64 ppos, u32 m, u32* lo, u32* hi,
+                                                u32* s_first, u32* s_last) {
+    u32 l0 = 0, r0 = static_cast<u32>(iv.tv.n), f0 = 0, f1 = iv.k;
+    if (iv.tv.packed) {
+        if (iv.dir && m >= static_cast<u32>(iv.D)) {
+            const u32 x = static_cast<u32>(base_window(iv.tv.packed, ppos) >> (64 - 2 * iv.D));
+            l0 = iv.dir[x];
+            r0 = iv.dir[x + 1];
+            f0 = iv.sdir[x];
+            f1 = iv.sdir[x + 1];
+        }
+        bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_packed(iv.tv, spos, ppos, m); }, lo, hi);
+    } else {
+        const u8* pat = iv.tv.text + ppos;
+        bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_bytes(iv.tv, spos, pat, m); }, lo, hi);
+    }
+    // fragment_index.hpp:95-96
+    *s_first = lower_bound_u32(iv.start_rank, f0, f1, *lo);
+    *s_last = lower_bound_u32(iv.start_rank, *s_first, f1, *hi);
+}
+
+__global__ void __launch_bounds__(256)
+locate_residuals_kernel(IndexView iv, const u32* __restrict__ frag, const u32* __restrict__ off, u64 q,
+                        u32* __restrict__ lo, u32* __restrict__ hi) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < q; i += stride) {
+        const u32 f = frag[i], o = off[i];
+        u32 l, h, sf, sl;
+        locate_residual(iv, static_cast<u64>(iv.starts[f]) + o, iv.lens[f] - o, &l, &h, &sf, &sl);
+        lo[i] = l;
+        hi[i] = h;
+    }
+}
+
+// Host-supplied byte patterns.  A DNA index still narrows through the directory when the
+// first D pattern bytes are bases; the comparisons are byte-wise so that patterns holding
+// bytes outside the alphabet land on the reference's insertion point.
+__global__ void __launch_bounds__(256)
+locate_patterns_kernel(IndexView iv, const u8* __restrict__ pats, const u64* __restrict__ pat_off, u64 q,
+                       u32* __restrict__ lo, u32* __restrict__ hi) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < q; i += stride) {
+        const u8* pat = pats + pat_off[i];
+        const u32 m = static_cast<u32>(pat_off[i + 1] - pat_off[i]);
+        u32 l0 = 0, r0 = static_cast<u32>(iv.tv.n);
+        if (iv.dir && m >= static_cast<u32>(iv.D)) {
+            u32 x = 0;
+            bool ok = true;
+            for (int t = 0; t < iv.D; ++t) {
+                const u32 c = pat[t];
+                ok &= (c == 'A' || c == 'C' || c == 'G' || c == 'T');
+                x = (x << 2) | (((c >> 1) ^ (c >> 2)) & 3u);
+            }
+            if (ok) {
+                l0 = iv.dir[x];
+                r0 = iv.dir[x + 1];
+            }
+        }
+        u32 l, h;
+        bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_bytes(iv.tv, spos, pat, m); }, &l, &h);
+        lo[i] = l;
+        hi[i] = h;
+    }
+}
+
+// Overlap pass 1: one warp per fragment, lanes stride over the offsets.  Query (i, o) =
+// pattern f_i[o..]; every fragment-start suffix inside its SA interval is a fragment j
+// whose prefix equals that pattern, i.e. overlap_weight(f_i, f_j) >= |f_i| - o
+// (overlap.hpp:16-23).  Stores, per query, the start-list interval; per fragment, the
+// absorb_contained verdict (overlap.hpp:51-67) from the o = 0 query.
+__global__ void __launch_bounds__(256)
+overlap_count_kernel(IndexView iv, u32 min_ov, const u64* __restrict__ qoff, u32* __restrict__ q_first,
+                     u32* __restrict__ q_count, u8* __restrict__ contained) {
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < iv.k; i += warps) {
+        const u32 len = iv.lens[i];
+        const u64 start = iv.starts[i];
+        const u64 qbase = qoff[i];
+        const u32 nq = static_cast<u32>(qoff[i + 1] - qbase);  // offsets 0 .. len - min_ov
+        // a fragment shorter than min_ov still runs its o = 0 query for the containment flag
+        const u32 steps = nq ? nq : 1u;
+        for (u32 o = lane; o < steps; o += 32) {
+            const u32 m = len - o;
+            u32 lo, hi, sf, sl;
+            locate_residual(iv, start + o, m, &lo, &hi, &sf, &sl);
+            u32 cnt = sl - sf;
+            if (o == 0) {
+                // the o = 0 interval contains f_i's own start suffix: not an overlap
+                cnt -= 1;
+                u32 exact = 0, min_id = 0xFFFFFFFFu;
+                for (u32 t = sf; t < sl; ++t) {
+                    const u32 id = iv.start_frag[t];
+                    if (iv.lens[id] == m) {
+                        ++exact;
+                        min_id = min(min_id, id);
+                    }
+                }
+                contained[i] = (hi - lo > exact) || (min_id < static_cast<u32>(i));
+            }
+            if (o < nq) {
+                q_first[qbase + o] = sf;
+                q_count[qbase + o] = cnt;
+            }
+        }
+    }
+}
+
+// Overlap pass 2: writes the raw (i<<32 | j, w) records at the scanned offsets, in
+// (i, o ascending) order so that after a STABLE sort on (i, j) the first record of every
+// pair carries its maximum w.
+__global__ void __launch_bounds__(256)
+overlap_fill_kernel(IndexView iv, const u64* __restrict__ qoff, const u32* __restrict__ q_first,
+                    const u32* __restrict__ q_count, const u32* __restrict__ q_out, u64* __restrict__ keys,
+                    u32* __restrict__ w) {
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < iv.k; i += warps) {
+        const u32 len = iv.lens[i];
+        const u64 qbase = qoff[i];
+        const u32 nq = static_cast<u32>(qoff[i + 1] - qbase);
+        for (u32 o = lane; o < nq; o += 32) {
+            const u32 cnt = q_count[qbase + o];
+            if (!cnt) continue;
+            u32 out = q_out[qbase + o];
+            const u32 sf = q_first[qbase + o];
+            const u32 span = cnt + (o == 0 ? 1u : 0u);
+            for (u32 t = 0; t < span; ++t) {
+                const u32 j = iv.start_frag[sf + t];
+                if (j == static_cast<u32>(i)) continue;
+                keys[out] = (static_cast<u64>(i) << 32) | j;
+                w[out] = len - o;
+                ++out;
+            }
+        }
+    }
+}
+
+__global__ void unique_flag_kernel(const u64* __restrict__ keys, u64 m, u32* __restrict__ flag) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 t = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; t < m; t += stride)
+        flag[t] = (t == 0 || keys[t] != keys[t - 1]) ? 1u : 0u;
+}
+
+__global__ void unique_compact_kernel(const u64* __restrict__ keys, const u32* __restrict__ w,
+                                      const u32* __restrict__ flag, const u32* __restrict__ dst, u64 m,
+                                      u32* __restrict__ oi, u32* __restrict__ oj, u32* __restrict__ ow) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 t = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; t < m; t += stride)
+        if (flag[t]) {
+            const u32 d = dst[t];
+            oi[d] = static_cast<u32>(keys[t] >> 32);
+            oj[d] = static_cast<u32>(keys[t]);
+            ow[d] = w[t];
+        }
+}
+
+IndexView view_of(const reseq_cuda_index* ix) {
+    IndexView iv{};
+    iv.tv = TextView{ix->d_text, ix->dna ? ix->d_packed : nullptr, ix->dna ? ix->d_sent : nullptr, ix->n};
+    iv.sa = ix->d_sa;
+    iv.starts = ix->d_starts;
+    iv.lens = ix->d_lens;
+    iv.start_rank = ix->d_start_rank;
+    iv.start_frag = ix->d_start_frag;
+    iv.dir = ix->dna && ix->d_dir ? ix->d_dir + 1 : nullptr;
+    iv.sdir = ix->dna && ix->d_sdir ? ix->d_sdir + 1 : nullptr;
+    iv.D = ix->dir_bases;
+    iv.k = static_cast<u32>(ix->k);
+    return iv;
+}
+
+int choose_dir_bases(size_t n) {
+    // aim at ~16 suffixes per bucket, table between 4^6 and 4^13 entries (<= 256 MiB)
+    int D = 6;
+    while (D < 13 && (size_t{1} << (2 * D)) * 16 < n) ++D;
+    return D;
+}
+
+// Exclusive scan of a u32 histogram of `count` entries whose total is < 2^32.
+int scan_table(reseq_cuda_ctx* ctx, const u32* hist, u32* out, size_t count) {
+    u64* d_total = ctx->alloc<u64>(1);
+    if (!d_total) return fail(RESEQ_OUT_OF_MEMORY, "directory scan workspace");
+    return exclusive_scan_device(ctx, hist, out, count, d_total);
+}
+
+}  // namespace
+
+extern "C" {
+
+int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n, const uint32_t* starts,
+                            size_t k, reseq_cuda_index** out) {
+    if (!out) return fail(RESEQ_INVALID_ARGUMENT, "null out pointer");
+    *out = nullptr;
+    if (!ctx) return fail(RESEQ_INVALID_ARGUMENT, "null context");
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    if (n > RESEQ_CUDA_MAX_TEXT)
+        return fail(RESEQ_TEXT_TOO_LARGE, "text of length " + std::to_string(n) + " exceeds 2^32-2");
+    if (n == 0 || k == 0 || !concat || !starts)
+        return fail(RESEQ_INVALID_ARGUMENT, "an index needs at least one fragment");
+    if (concat[n - 1] != 0)
+        return fail(RESEQ_INVALID_ARGUMENT, "concat must end with the separator byte (sequence.hpp:60-62)");
+
+    auto* ix = new reseq_cuda_index();
+    ix->ctx = ctx;
+    ix->n = n;
+    ix->k = k;
+    auto bail = [&](int code) {
+        reseq_cuda_index_destroy(ix);
+        return code;
+    };
+#define IX_TRY(expr)                            \
+    do {                                        \
+        int _s = (expr);                        \
+        if (_s != RESEQ_OK) return bail(_s);    \
+    } while (0)
+#define IX_CUDA(expr)                                                                        \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return bail(fail(RESEQ_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e))); \
+    } while (0)
+
+    cudaStream_t s = ctx->stream;
+    IX_TRY(dev_alloc(ix, &ix->d_text, n));
+    IX_TRY(dev_alloc(ix, &ix->d_sa, n));
+    IX_TRY(dev_alloc(ix, &ix->d_rank, n));
+    IX_TRY(dev_alloc(ix, &ix->d_starts, k));
+    IX_TRY(dev_alloc(ix, &ix->d_lens, k));
+    IX_TRY(dev_alloc(ix, &ix->d_start_rank, k));
+    IX_TRY(dev_alloc(ix, &ix->d_start_frag, k));
+    IX_TRY(dev_alloc(ix, &ix->d_packed, n / 32 + 8));
+    IX_TRY(dev_alloc(ix, &ix->d_sent, n / 64 + 8));
+    IX_CUDA(cudaMemcpyAsync(ix->d_text, concat, n, cudaMemcpyHostToDevice, s));
+    IX_CUDA(cudaMemcpyAsync(ix->d_starts, starts, sizeof(u32) * k, cudaMemcpyHostToDevice, s));
+
+    // suffix array (fragment_index.hpp:37)
+    IX_TRY(ctx->reserve(sa_workspace_bytes(n)));
+    ctx->begin();
+    reseq_sa_stats st{};
+    IX_TRY(build_sa_device(ctx, ix->d_text, n, ix->d_sa, ix->d_rank, &st));
+    ix->dna = st.alphabet == 0;
+
+    // lengths, start ranks (fragment_index.hpp:40-48), directories
+    const int D = choose_dir_bases(n);
+    const size_t dir_entries = (size_t{1} << (2 * D)) + 2;
+    const size_t need = 4 * reseq_cuda_ctx::padded(sizeof(u32) * k) + sort_workspace_bytes(k) +
+                        reseq_cuda_ctx::padded(sizeof(u32) * dir_entries) + scan_workspace_bytes(dir_entries) +
+                        8192;
+    IX_TRY(ctx->reserve(need));
+    ctx->begin();
+    u32* keys_a = ctx->alloc<u32>(k);
+    u32* keys_b = ctx->alloc<u32>(k);
+    u32* ids_a = ctx->alloc<u32>(k);
+    u32* ids_b = ctx->alloc<u32>(k);
+    u32* counters = ctx->alloc<u32>(64);
+    u32* hist = ctx->alloc<u32>(dir_entries);
+    if (!keys_a || !keys_b || !ids_a || !ids_b || !counters || !hist)
+        return bail(fail(RESEQ_OUT_OF_MEMORY, "index workspace"));
+    IX_CUDA(cudaMemsetAsync(counters, 0, 256, s));
+    lens_kernel<<<grid_1d(ctx, k, 256), 256, 0, s>>>(ix->d_starts, k, n, ix->d_lens, ix->d_rank, keys_a,
+                                                     ids_a, counters);
+    ++ctx->launches;
+    IX_CUDA(cudaGetLastError());
+    if (k > 1) {
+        SortWorkspace ws;
+        IX_TRY(sort_workspace_carve(ctx, k, &ws));
+        bool in_b = false;
+        const PassTable pt = make_passes(0, static_cast<int>(bit_width_u64(n)));
+        IX_TRY(onesweep_sort<u32>(ctx, keys_a, keys_b, ids_a, ids_b, k, pt, ws, false, 0, &in_b));
+        IX_CUDA(cudaMemcpyAsync(ix->d_start_rank, in_b ? keys_b : keys_a, sizeof(u32) * k,
+                                cudaMemcpyDeviceToDevice, s));
+        IX_CUDA(cudaMemcpyAsync(ix->d_start_frag, in_b ? ids_b : ids_a, sizeof(u32) * k,
+                                cudaMemcpyDeviceToDevice, s));
+    } else {
+        IX_CUDA(cudaMemcpyAsync(ix->d_start_rank, keys_a, sizeof(u32), cudaMemcpyDeviceToDevice, s));
+        IX_CUDA(cudaMemcpyAsync(ix->d_start_frag, ids_a, sizeof(u32), cudaMemcpyDeviceToDevice, s));
+    }
+    IX_CUDA(cudaMemcpyAsync(ctx->pinned, counters, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    IX_CUDA(cudaStreamSynchronize(s));
+    ix->max_len = *reinterpret_cast<volatile u32*>(ctx->pinned);
+
+    if (ix->dna) {
+        bool is_dna = true;
+        IX_TRY(pack_dna_device(ctx, ix->d_text, n, ix->d_packed, ix->d_sent, counters + 8, &is_dna));
+        ix->dir_bases = D;
+        IX_TRY(dev_alloc(ix, &ix->d_dir, dir_entries));
+        IX_TRY(dev_alloc(ix, &ix->d_sdir, dir_entries));
+        for (int which = 0; which < 2; ++which) {
+            IX_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * dir_entries, s));
+            const size_t count = which == 0 ? n : k;
+            dir_hist_kernel<<<grid_1d(ctx, count, 256), 256, 0, s>>>(
+                ix->d_packed, ix->d_sent, n, which == 0 ? nullptr : ix->d_starts, count, D, hist);
+            ++ctx->launches;
+            IX_CUDA(cudaGetLastError());
+            IX_TRY(scan_table(ctx, hist, which == 0 ? ix->d_dir : ix->d_sdir, dir_entries));
+        }
+    }
+    IX_CUDA(cudaStreamSynchronize(s));
+#undef IX_TRY
+#undef IX_CUDA
+    *out = ix;
+    return RESEQ_OK;
+}
+
+void reseq_cuda_index_destroy(reseq_cuda_index* ix) {
+    if (!ix) return;
+    if (ix->ctx) {
+        cudaSetDevice(ix->ctx->device);
+        cudaStreamSynchronize(ix->ctx->stream);
+    }
+    for (void* p : ix->owned) cudaFree(p);
+    delete ix;
+}
+
+size_t reseq_cuda_index_text_len(const reseq_cuda_index* ix) { return ix ? ix->n : 0; }
+size_t reseq_cuda_index_fragments(const reseq_cuda_index* ix) { return ix ? ix->k : 0; }
+
+int reseq_cuda_index_get(const reseq_cuda_index* ix, uint32_t* sa, uint32_t* rank, uint32_t* start_rank_list) {
+    if (!ix) return fail(RESEQ_INVALID_ARGUMENT, "null index");
+    RSQ_CUDA(cudaSetDevice(ix->ctx->device));
+    cudaStream_t s = ix->ctx->stream;
+    if (sa) RSQ_CUDA(cudaMemcpyAsync(sa, ix->d_sa, sizeof(u32) * ix->n, cudaMemcpyDeviceToHost, s));
+    if (rank) RSQ_CUDA(cudaMemcpyAsync(rank, ix->d_rank, sizeof(u32) * ix->n, cudaMemcpyDeviceToHost, s));
+    if (start_rank_list)
+        RSQ_CUDA(cudaMemcpyAsync(start_rank_list, ix->d_start_rank, sizeof(u32) * ix->k, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    return RESEQ_OK;
+}
+
+int reseq_cuda_index_device_ptrs(const reseq_cuda_index* ix, const uint32_t** d_sa, const uint32_t** d_rank,
+                                 const uint32_t** d_start_rank_list) {
+    if (!ix) return fail(RESEQ_INVALID_ARGUMENT, "null index");
+    if (d_sa) *d_sa = ix->d_sa;
+    if (d_rank) *d_rank = ix->d_rank;
+    if (d_start_rank_list) *d_start_rank_list = ix->d_start_rank;
+    return RESEQ_OK;
+}
+
+int reseq_cuda_index_locate_batch(reseq_cuda_index* ix, const uint8_t* pats, const uint64_t* pat_off, size_t q,
+                                  uint32_t* lo, uint32_t* hi) {
+    if (!ix) return fail(RESEQ_INVALID_ARGUMENT, "null index");
+    if (q == 0) return RESEQ_OK;
+    if (!pats || !pat_off || !lo || !hi) return fail(RESEQ_INVALID_ARGUMENT, "null buffer");
+    for (size_t i = 0; i < q; ++i)
+        if (pat_off[i + 1] <= pat_off[i])
+            return fail(RESEQ_INVALID_ARGUMENT, "patterns must be non-empty (fragment_index.hpp:63-64)");
+    reseq_cuda_ctx* ctx = ix->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t bytes = pat_off[q];
+    auto pad = reseq_cuda_ctx::padded;
+    RSQ_TRY(ctx->reserve(pad(bytes) + pad(sizeof(u64) * (q + 1)) + 2 * pad(sizeof(u32) * q) + 4096));
+    ctx->begin();
+    u8* d_pats = ctx->alloc<u8>(bytes);
+    u64* d_off = ctx->alloc<u64>(q + 1);
+    u32* d_lo = ctx->alloc<u32>(q);
+    u32* d_hi = ctx->alloc<u32>(q);
+    RSQ_CUDA(cudaMemcpyAsync(d_pats, pats, bytes, cudaMemcpyHostToDevice, s));
+    RSQ_CUDA(cudaMemcpyAsync(d_off, pat_off, sizeof(u64) * (q + 1), cudaMemcpyHostToDevice, s));
+    locate_patterns_kernel<<<grid_1d(ctx, q, 256), 256, 0, s>>>(view_of(ix), d_pats, d_off, q, d_lo, d_hi);
+    ++ctx->launches;
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(lo, d_lo, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(hi, d_hi, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    return RESEQ_OK;
+}
+
+int reseq_cuda_index_locate_residuals(reseq_cuda_index* ix, const uint32_t* frag, const uint32_t* off, size_t q,
+                                      uint32_t* lo, uint32_t* hi) {
+    if (!ix) return fail(RESEQ_INVALID_ARGUMENT, "null index");
+    if (q == 0) return RESEQ_OK;
+    if (!frag || !off || !lo || !hi) return fail(RESEQ_INVALID_ARGUMENT, "null buffer");
+    reseq_cuda_ctx* ctx = ix->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    // residual_view's bounds check (sequence.hpp:127-131) needs the lengths on the host
+    std::vector<u32> lens(ix->k);
+    RSQ_CUDA(cudaMemcpyAsync(lens.data(), ix->d_lens, sizeof(u32) * ix->k, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < q; ++i)
+        if (frag[i] >= ix->k || off[i] >= lens[frag[i]])
+            return fail(RESEQ_INVALID_ARGUMENT, "residual offset out of range (sequence.hpp:128-129)");
+    auto pad = reseq_cuda_ctx::padded;
+    RSQ_TRY(ctx->reserve(4 * pad(sizeof(u32) * q) + 4096));
+    ctx->begin();
+    u32* d_frag = ctx->alloc<u32>(q);
+    u32* d_offs = ctx->alloc<u32>(q);
+    u32* d_lo = ctx->alloc<u32>(q);
+    u32* d_hi = ctx->alloc<u32>(q);
+    RSQ_CUDA(cudaMemcpyAsync(d_frag, frag, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
+    RSQ_CUDA(cudaMemcpyAsync(d_offs, off, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
+    locate_residuals_kernel<<<grid_1d(ctx, q, 256), 256, 0, s>>>(view_of(ix), d_frag, d_offs, q, d_lo, d_hi);
+    ++ctx->launches;
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(lo, d_lo, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(hi, d_hi, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    return RESEQ_OK;
+}
+
+int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_overlaps* out) {
+    if (!ix || !out) return fail(RESEQ_INVALID_ARGUMENT, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    if (min_overlap < 1) min_overlap = 1;
+    reseq_cuda_ctx* ctx = ix->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t k = ix->k;
+    auto pad = reseq_cuda_ctx::padded;
+
+    // -- per-fragment query counts -> query offsets (host prefix sum; k entries) -----------
+    std::vector<u32> lens(k);
+    RSQ_CUDA(cudaMemcpyAsync(lens.data(), ix->d_lens, sizeof(u32) * k, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    std::vector<u64> qoff(k + 1, 0);
+    for (size_t i = 0; i < k; ++i) qoff[i + 1] = qoff[i] + (lens[i] >= min_overlap ? lens[i] - min_overlap + 1 : 0);
+    const u64 Q = qoff[k];
+    out->queries = Q;
+    out->contained = static_cast<uint8_t*>(std::calloc(k, 1));
+    if (!out->contained) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
+    if (Q > 0xFFFFFFF0ull) return fail(RESEQ_INVALID_ARGUMENT, "more than 2^32 overlap queries in one call");
+
+    cudaEvent_t ev0, ev1;
+    RSQ_CUDA(cudaEventCreate(&ev0));
+    RSQ_CUDA(cudaEventCreate(&ev1));
+
+    size_t need = pad(sizeof(u64) * (k + 1)) + 3 * pad(sizeof(u32) * (Q + 1)) + pad(k) +
+                  scan_workspace_bytes(Q + 1) + 8192;
+    RSQ_TRY(ctx->reserve(need));
+    ctx->begin();
+    u64* d_qoff = ctx->alloc<u64>(k + 1);
+    u32* q_first = ctx->alloc<u32>(Q + 1);
+    u32* q_count = ctx->alloc<u32>(Q + 1);
+    u32* q_out = ctx->alloc<u32>(Q + 1);
+    u8* d_contained = ctx->alloc<u8>(k);
+    u64* d_total = ctx->alloc<u64>(1);
+    if (!d_qoff || !q_first || !q_count || !q_out || !d_contained || !d_total)
+        return fail(RESEQ_OUT_OF_MEMORY, "overlap workspace");
+    RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (k + 1), cudaMemcpyHostToDevice, s));
+    RSQ_CUDA(cudaMemsetAsync(d_contained, 0, k, s));
+    RSQ_CUDA(cudaMemsetAsync(q_count + Q, 0, sizeof(u32), s));
+    const IndexView iv = view_of(ix);
+
+    RSQ_CUDA(cudaEventRecord(ev0, s));
+    u64 raw = 0;
+    if (Q > 0) {
+        const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+        overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, d_qoff, q_first, q_count, d_contained);
+        ++ctx->launches;
+        RSQ_CUDA(cudaGetLastError());
+        RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
+        RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total, sizeof(u64), cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaStreamSynchronize(s));
+        raw = *reinterpret_cast<volatile u64*>(ctx->pinned);
+    }
+    RSQ_CUDA(cudaMemcpyAsync(out->contained, d_contained, k, cudaMemcpyDeviceToHost, s));
+    if (raw > 0xFFFFFFF0ull) return fail(RESEQ_INVALID_ARGUMENT, "more than 2^32 raw overlap records");
+
+    u64 uniq = 0;
+    if (raw > 0) {
+        // The query arrays stay where they are; the record buffers follow them in the arena.
+        const size_t used_before = ctx->arena_used;
+        const size_t more = 2 * pad(sizeof(u64) * raw) + 4 * pad(sizeof(u32) * raw) + 3 * pad(sizeof(u32) * raw) +
+                            sort_workspace_bytes(raw) + scan_workspace_bytes(raw) + 8192;
+        if (ctx->arena_cap < used_before + more) {
+            // grow: the arena is re-allocated, so redo pass 1 state in the new block
+            RSQ_TRY(ctx->reserve(used_before + more));
+            ctx->begin();
+            d_qoff = ctx->alloc<u64>(k + 1);
+            q_first = ctx->alloc<u32>(Q + 1);
+            q_count = ctx->alloc<u32>(Q + 1);
+            q_out = ctx->alloc<u32>(Q + 1);
+            d_contained = ctx->alloc<u8>(k);
+            d_total = ctx->alloc<u64>(1);
+            RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (k + 1), cudaMemcpyHostToDevice, s));
+            RSQ_CUDA(cudaMemsetAsync(q_count + Q, 0, sizeof(u32), s));
+            const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+            overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, d_qoff, q_first, q_count, d_contained);
+            ++ctx->launches;
+            RSQ_CUDA(cudaGetLastError());
+            RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
+        }
+        u64* keys_a = ctx->alloc<u64>(raw);
+        u64* keys_b = ctx->alloc<u64>(raw);
+        u32* w_a = ctx->alloc<u32>(raw);
+        u32* w_b = ctx->alloc<u32>(raw);
+        u32* flag = ctx->alloc<u32>(raw);
+        u32* dst = ctx->alloc<u32>(raw);
+        u32* oi = ctx->alloc<u32>(raw);
+        u32* oj = ctx->alloc<u32>(raw);
+        u32* ow = ctx->alloc<u32>(raw);
+        u64* d_total2 = ctx->alloc<u64>(1);
+        if (!keys_a || !keys_b || !w_a || !w_b || !flag || !dst || !oi || !oj || !ow || !d_total2)
+            return fail(RESEQ_OUT_OF_MEMORY, "overlap record workspace");
+        {
+            const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+            overlap_fill_kernel<<<grid, 256, 0, s>>>(iv, d_qoff, q_first, q_count, q_out, keys_a, w_a);
+            ++ctx->launches;
+            RSQ_CUDA(cudaGetLastError());
+        }
+        // stable sort on (i, j): j digits then i digits
+        const int kb = static_cast<int>(bit_width_u64(k));
+        PassTable pt = make_passes(0, kb);
+        const PassTable hi_pt = make_passes(32, 32 + kb);
+        for (int p = 0; p < hi_pt.count; ++p) {
+            pt.shift[pt.count] = hi_pt.shift[p];
+            pt.bits[pt.count] = hi_pt.bits[p];
+            ++pt.count;
+        }
+        SortWorkspace ws;
+        RSQ_TRY(sort_workspace_carve(ctx, raw, &ws));
+        bool in_b = false;
+        RSQ_TRY(onesweep_sort<u64>(ctx, keys_a, keys_b, w_a, w_b, raw, pt, ws, false, 0, &in_b));
+        const u64* sk = in_b ? keys_b : keys_a;
+        const u32* sw = in_b ? w_b : w_a;
+        unique_flag_kernel<<<grid_1d(ctx, raw, 256), 256, 0, s>>>(sk, raw, flag);
+        ++ctx->launches;
+        RSQ_CUDA(cudaGetLastError());
+        RSQ_TRY(exclusive_scan_device(ctx, flag, dst, raw, d_total2));
+        unique_compact_kernel<<<grid_1d(ctx, raw, 256), 256, 0, s>>>(sk, sw, flag, dst, raw, oi, oj, ow);
+        ++ctx->launches;
+        RSQ_CUDA(cudaGetLastError());
+        RSQ_CUDA(cudaEventRecord(ev1, s));
+        RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total2, sizeof(u64), cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaStreamSynchronize(s));
+        uniq = *reinterpret_cast<volatile u64*>(ctx->pinned);
+        out->i = static_cast<uint32_t*>(std::malloc(sizeof(u32) * uniq));
+        out->j = static_cast<uint32_t*>(std::malloc(sizeof(u32) * uniq));
+        out->w = static_cast<uint32_t*>(std::malloc(sizeof(u32) * uniq));
+        if (!out->i || !out->j || !out->w) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
+        RSQ_CUDA(cudaMemcpyAsync(out->i, oi, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaMemcpyAsync(out->j, oj, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaMemcpyAsync(out->w, ow, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
+    } else {
+        RSQ_CUDA(cudaEventRecord(ev1, s));
+    }
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    RSQ_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    out->device_ms = ms;
+    out->count = uniq;
+    return RESEQ_OK;
+}
+
+void reseq_cuda_overlaps_free(reseq_overlaps* o) {
+    if (!o) return;
+    std::free(o->i);
+    std::free(o->j);
+    std::free(o->w);
+    std::free(o->contained);
+    std::memset(o, 0, sizeof(*o));
+}
+
+}  // extern "C"

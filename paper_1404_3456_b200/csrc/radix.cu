@@ -1,0 +1,123 @@
+// Host driver of the onesweep radix sort (kernels in radix.cuh).
+#include "radix.cuh"
+
+namespace rsq {
+
+// One block per pass: exclusive scan of the 256 digit counts.
+__global__ void __launch_bounds__(kRadix)
+digit_base_kernel(const u32* __restrict__ g_hist, u32* __restrict__ g_base) {
+    __shared__ u32 s_warp[kRadix / 32];
+    const int d = threadIdx.x;
+    const u32 c = g_hist[blockIdx.x * kRadix + d];
+    u32 inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (static_cast<int>(lane_id()) >= o) inc += t;
+    }
+    if (lane_id() == 31) s_warp[d >> 5] = inc;
+    __syncthreads();
+    u32 add = 0;
+    for (int w = 0; w < (d >> 5); ++w) add += s_warp[w];
+    g_base[blockIdx.x * kRadix + d] = add + inc - c;
+}
+
+template <> struct SortTuning<u32, false> { static constexpr int kBlock = 256, kItems = 16; };
+template <> struct SortTuning<u32, true>  { static constexpr int kBlock = 256, kItems = 16; };
+template <> struct SortTuning<u64, true>  { static constexpr int kBlock = 256, kItems = 16; };
+template <> struct SortTuning<u64, false> { static constexpr int kBlock = 256, kItems = 16; };
+
+// The smallest tile among the tunings bounds the look-back array.
+static constexpr size_t kMinTile = 256 * 16;
+
+size_t sort_workspace_bytes(size_t n) {
+    const size_t tiles = (n + kMinTile - 1) / kMinTile + 1;
+    return reseq_cuda_ctx::padded(sizeof(u32) * kMaxPasses * kRadix) * 2 +
+           reseq_cuda_ctx::padded(sizeof(u32) * kMaxPasses) +
+           reseq_cuda_ctx::padded(sizeof(u64) * tiles * kRadix);
+}
+
+int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws) {
+    const size_t tiles = (n + kMinTile - 1) / kMinTile + 1;
+    ws->hist = ctx->alloc<u32>(kMaxPasses * kRadix);
+    ws->base = ctx->alloc<u32>(kMaxPasses * kRadix);
+    ws->tickets = ctx->alloc<u32>(kMaxPasses);
+    ws->lookback = ctx->alloc<u64>(tiles * kRadix);
+    ws->lookback_bytes = sizeof(u64) * tiles * kRadix;
+    if (!ws->hist || !ws->base || !ws->tickets || !ws->lookback)
+        return fail(RESEQ_OUT_OF_MEMORY, "sort workspace does not fit the reserved arena");
+    return RESEQ_OK;
+}
+
+template <typename KeyT, bool HAS_VAL>
+static int launch_pass(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u32* vin, u32* vout,
+                       size_t n, int shift, u32 mask, const u32* base, u64* lookback,
+                       u32* ticket) {
+    using T = SortTuning<KeyT, HAS_VAL>;
+    using Cfg = OnesweepCfg<KeyT, HAS_VAL, T::kBlock, T::kItems>;
+    auto kern = onesweep_kernel<KeyT, HAS_VAL, T::kBlock, T::kItems>;
+    static bool configured = false;
+    if (!configured) {
+        RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Cfg::kSmem)));
+        configured = true;
+    }
+    const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
+    kern<<<static_cast<unsigned>(tiles), T::kBlock, Cfg::kSmem, ctx->stream>>>(
+        kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+    ++ctx->launches;
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
+}
+
+template <typename KeyT>
+int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, u32* vals_b,
+                  size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
+                  u32 skip_mask, bool* in_b) {
+    *in_b = false;
+    if (n == 0 || pt.count == 0) return RESEQ_OK;
+    const bool has_val = vals_a != nullptr;
+    RSQ_CUDA(cudaMemsetAsync(ws.tickets, 0, sizeof(u32) * kMaxPasses, ctx->stream));
+    if (!hist_ready) {
+        RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * pt.count * kRadix, ctx->stream));
+        const int block = 512;
+        size_t want = (n + block * 8 - 1) / (block * 8);
+        const unsigned grid = static_cast<unsigned>(want < static_cast<size_t>(ctx->sm_count) * 4 ? (want ? want : 1) : ctx->sm_count * 4);
+        hist_kernel<KeyT><<<grid, block, sizeof(u32) * pt.count * kRadix, ctx->stream>>>(
+            keys_a, n, pt, ws.hist);
+        ++ctx->launches;
+        RSQ_CUDA(cudaGetLastError());
+    }
+    digit_base_kernel<<<pt.count, kRadix, 0, ctx->stream>>>(ws.hist, ws.base);
+    ++ctx->launches;
+    RSQ_CUDA(cudaGetLastError());
+
+    KeyT* kin = keys_a;
+    KeyT* kout = keys_b;
+    u32* vin = vals_a;
+    u32* vout = vals_b;
+    bool flipped = false;
+    for (int p = 0; p < pt.count; ++p) {
+        if (skip_mask & (1u << p)) continue;
+        RSQ_CUDA(cudaMemsetAsync(ws.lookback, 0, ws.lookback_bytes, ctx->stream));
+        if (has_val)
+            RSQ_TRY((launch_pass<KeyT, true>(ctx, kin, kout, vin, vout, n, pt.shift[p], pt.mask(p),
+                                             ws.base + p * kRadix, ws.lookback, ws.tickets + p)));
+        else
+            RSQ_TRY((launch_pass<KeyT, false>(ctx, kin, kout, nullptr, nullptr, n, pt.shift[p],
+                                              pt.mask(p), ws.base + p * kRadix, ws.lookback,
+                                              ws.tickets + p)));
+        KeyT* tk = kin; kin = kout; kout = tk;
+        u32* tv = vin; vin = vout; vout = tv;
+        flipped = !flipped;
+    }
+    *in_b = flipped;
+    return RESEQ_OK;
+}
+
+template int onesweep_sort<u32>(reseq_cuda_ctx*, u32*, u32*, u32*, u32*, size_t, const PassTable&,
+                                const SortWorkspace&, bool, u32, bool*);
+template int onesweep_sort<u64>(reseq_cuda_ctx*, u64*, u64*, u32*, u32*, size_t, const PassTable&,
+                                const SortWorkspace&, bool, u32, bool*);
+
+}  // namespace rsq

@@ -1,0 +1,473 @@
+// Suffix-array construction on sm_100a: 2-bit packing, k-mer initial ranking, prefix
+// doubling over (rank[i], rank[i+h]) pairs.
+//
+// Replaces build_parallel, suffix_array.hpp:61-124.  Same mathematical result -- the
+// unique permutation sorted by suffix_less (suffix_array.hpp:28-41) and its inverse --
+// reached with far fewer, far fatter phases:
+//
+//   reference                                   here
+//   ---------------------------------------     ------------------------------------------
+//   1-byte initial ranks (:68-87)               13-base (DNA, 2-bit packed) or 3-byte
+//                                               (generic) sentinel-aware initial ranks:
+//                                               one 31-bit key per suffix, 4 digit passes
+//   h = 1, 2, 4, ... (:90)                      h = 13, 26, 52, ... (3 rounds at L=100,
+//                                               4 at L=150 instead of 7 / 8)
+//   two 32-pass 1-bit radix sorts per round     one LSD sort of the packed
+//   (:97,:99)                                   (rank[i] << b | rank[i+h]+1) key,
+//                                               ceil(2b/8) onesweep digit passes
+//   diff by 4 rank gathers (:101-111)           adjacent compare of the sorted keys
+//   dense ranks by exclusive_scan (:112-113)    group-head ranks (index of the first
+//                                               suffix of the group) by a max-scan with
+//                                               decoupled look-back, scatter fused
+//   inverse permutation phase (:118-122)        free: with all groups singletons the
+//                                               group-head rank array IS the inverse
+//
+// Sentinel semantics (suffix_array.hpp:16-20): every byte 0 is its own symbol, ordered
+// by text position, below every other byte; end of text is below everything.  A suffix
+// whose first k symbols contain a terminator is therefore already unique after the
+// initial sort: its key is (symbols before the terminator, zero padded | 2*len + kind)
+// where kind 0 = end of text, 1 = sentinel, and equal keys keep position order because
+// the sort is stable and starts from the identity permutation.
+#include "radix.cuh"
+#include "sa.cuh"
+#include "scan.cuh"
+
+#include <type_traits>
+
+namespace rsq {
+
+namespace {
+
+// ---- 2-bit packing ----------------------------------------------------------------
+// packed: u64 words, 32 bases each, base p in bits [63-2(p%32)-1, 63-2(p%32)] so that a
+// window's integer order equals its lexicographic order.  sent: u64 words, 64 flags
+// each, position p at bit 63-(p%64).  Both arrays carry >= 2 zero words of padding.
+
+__device__ __forceinline__ u32 dna_code(u32 c) { return ((c >> 1) ^ (c >> 2)) & 3u; }
+__device__ __forceinline__ bool is_dna_or_zero(u32 c) {
+    return c == 0u || c == 'A' || c == 'C' || c == 'G' || c == 'T';
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256)
+pack_dna_kernel(const u8* __restrict__ text, u64 n, u64* __restrict__ packed,
+                u64* __restrict__ sent, u32* __restrict__ bad_flag) {
+    const u64 words = (n + 63) >> 6;  // one thread per 64 positions
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    bool bad = false;
+    for (u64 w = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) {
+        const u64 base = w << 6;
+        u64 p0 = 0, p1 = 0, s = 0;
+        if (VEC && base + 64 <= n) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = ld_stream_v4(text + base + 16 * q);
+                const u32 word[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const u32 c = (word[t >> 2] >> (8 * (t & 3))) & 0xFFu;
+                    bad |= !is_dna_or_zero(c);
+                    const int p = 16 * q + t;
+                    const u64 code = dna_code(c) & (c ? 3u : 0u);
+                    if (p < 32) p0 |= code << (62 - 2 * p);
+                    else p1 |= code << (62 - 2 * (p - 32));
+                    s |= static_cast<u64>(c == 0u) << (63 - p);
+                }
+            }
+        } else {
+            for (int p = 0; p < 64; ++p) {
+                if (base + p >= n) break;
+                const u32 c = text[base + p];
+                bad |= !is_dna_or_zero(c);
+                const u64 code = dna_code(c) & (c ? 3u : 0u);
+                if (p < 32) p0 |= code << (62 - 2 * p);
+                else p1 |= code << (62 - 2 * (p - 32));
+                s |= static_cast<u64>(c == 0u) << (63 - p);
+            }
+        }
+        packed[2 * w] = p0;
+        packed[2 * w + 1] = p1;
+        sent[w] = s;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(bad_flag, 1u);
+}
+
+__device__ __forceinline__ u64 base_window(const u64* __restrict__ packed, u64 pos) {
+    const u64 w = pos >> 5;
+    const unsigned s = static_cast<unsigned>(pos & 31) * 2;
+    const u64 hi = packed[w], lo = packed[w + 1];
+    return s ? (hi << s) | (lo >> (64 - s)) : hi;
+}
+__device__ __forceinline__ u64 sent_window(const u64* __restrict__ sent, u64 pos) {
+    const u64 w = pos >> 6;
+    const unsigned s = static_cast<unsigned>(pos & 63);
+    const u64 hi = sent[w], lo = sent[w + 1];
+    return s ? (hi << s) | (lo >> (64 - s)) : hi;
+}
+
+// ---- initial keys --------------------------------------------------------------------
+
+constexpr int kDnaK = 13;       // bases per initial key: 26 bits + 5-bit terminator field
+constexpr int kDnaFieldBits = 5;
+constexpr int kByteK = 3;       // bytes per initial key: 24 bits + 3-bit terminator field
+constexpr int kByteFieldBits = 3;
+
+__global__ void __launch_bounds__(256)
+initkey_dna_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n,
+                   u32* __restrict__ keys, u32* __restrict__ vals, PassTable pt,
+                   u32* __restrict__ g_hist) {
+    extern __shared__ u32 s_hist[];
+    for (int i = threadIdx.x; i < pt.count * kRadix; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    const u64 rounds = (n + stride - 1) / stride;
+    u64 pos = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (u64 r = 0; r < rounds; ++r, pos += stride) {
+        const bool in = pos < n;
+        u32 key = 0;
+        if (in) {
+            const u32 bases = static_cast<u32>(base_window(packed, pos) >> (64 - 2 * kDnaK));
+            const u32 sw = static_cast<u32>(sent_window(sent, pos) >> (64 - kDnaK));
+            const u32 t = sw ? static_cast<u32>(__clz(sw)) - (32 - kDnaK) : kDnaK;
+            const u64 rem = n - pos;
+            const u32 lim = rem < kDnaK ? static_cast<u32>(rem) : kDnaK;
+            u32 len, field;
+            if (t < lim) { len = t; field = 2 * t + 1; }          // sentinel after `t` bases
+            else if (lim < kDnaK) { len = lim; field = 2 * lim; } // text ends after `lim`
+            else { len = kDnaK; field = 2 * kDnaK; }              // k full bases
+            const u32 kept = bases & ~((1u << (2 * (kDnaK - len))) - 1u);
+            key = (kept << kDnaFieldBits) | field;
+            keys[pos] = key;
+            vals[pos] = static_cast<u32>(pos);
+        }
+        for (int p = 0; p < pt.count; ++p)
+            hist_add(s_hist + p * kRadix, key_digit(key, pt.shift[p], pt.mask(p)), in);
+    }
+    __syncthreads();
+    hist_flush(s_hist, g_hist, pt.count);
+}
+
+__global__ void __launch_bounds__(256)
+initkey_bytes_kernel(const u8* __restrict__ text, u64 n, u32* __restrict__ keys,
+                     u32* __restrict__ vals, PassTable pt, u32* __restrict__ g_hist) {
+    extern __shared__ u32 s_hist[];
+    for (int i = threadIdx.x; i < pt.count * kRadix; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    const u64 rounds = (n + stride - 1) / stride;
+    u64 pos = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (u64 r = 0; r < rounds; ++r, pos += stride) {
+        const bool in = pos < n;
+        u32 key = 0;
+        if (in) {
+            u32 sym = 0, len = 0, field = 2 * kByteK;
+            for (int t = 0; t < kByteK; ++t) {
+                if (pos + t >= n) { field = 2 * len; break; }
+                const u32 c = text[pos + t];
+                if (c == 0u) { field = 2 * len + 1; break; }
+                sym |= c << (8 * (kByteK - 1 - t));
+                ++len;
+            }
+            key = (sym << kByteFieldBits) | field;
+            keys[pos] = key;
+            vals[pos] = static_cast<u32>(pos);
+        }
+        for (int p = 0; p < pt.count; ++p)
+            hist_add(s_hist + p * kRadix, key_digit(key, pt.shift[p], pt.mask(p)), in);
+    }
+    __syncthreads();
+    hist_flush(s_hist, g_hist, pt.count);
+}
+
+// ---- re-ranking ------------------------------------------------------------------------
+// After a sort, suffix sa[idx] starts a new group iff its key differs from its left
+// neighbour's (or, for initial keys, carries a terminator: those are unique by
+// construction).  rank = index of the group's first suffix ("group-head rank"): an
+// inclusive max-scan of (head ? idx+1 : 0).  A tile containing any head needs no
+// look-back (heads increase with idx), so the chain is only walked inside groups that
+// span whole tiles.
+
+constexpr int kRankBlock = 256;
+constexpr int kRankItems = 8;
+constexpr int kRankTile = kRankBlock * kRankItems;
+
+template <typename KeyT>
+__global__ void __launch_bounds__(kRankBlock)
+rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, u32 uniq_mask,
+              u32 uniq_full, u32* __restrict__ rank, u32* __restrict__ head_of,
+              u64* __restrict__ desc, u32* __restrict__ ticket, u32* __restrict__ num_heads) {
+    __shared__ u32 s_tile;
+    __shared__ u32 s_warp[kRankBlock / 32];
+    __shared__ u32 s_count[kRankBlock / 32];
+    __shared__ u32 s_prefix;
+    __shared__ KeyT s_last[kRankBlock];
+
+    const int tid = threadIdx.x;
+    const unsigned lane = lane_id();
+    const int warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 base = static_cast<u64>(tile) * kRankTile + static_cast<u64>(tid) * kRankItems;
+
+    KeyT k[kRankItems];
+#pragma unroll
+    for (int j = 0; j < kRankItems; ++j) k[j] = base + j < n ? keys[base + j] : KeyT(0);
+    s_last[tid] = k[kRankItems - 1];
+    __syncthreads();
+    KeyT prev;
+    if (tid > 0) prev = s_last[tid - 1];
+    else prev = base > 0 && base <= n ? keys[base - 1] : KeyT(0);
+
+    u32 m[kRankItems];
+    u32 run = 0, heads = 0;
+#pragma unroll
+    for (int j = 0; j < kRankItems; ++j) {
+        const u64 idx = base + j;
+        const bool head = idx < n && (idx == 0 || k[j] != prev ||
+                                      (static_cast<u32>(k[j]) & uniq_mask) != uniq_full);
+        prev = k[j];
+        heads += head;
+        if (head) run = static_cast<u32>(idx) + 1u;
+        m[j] = run;  // thread-local inclusive max (0 = no head yet in this thread)
+    }
+    u32 inc = run;
+    u32 hsum = heads;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (static_cast<int>(lane) >= o) inc = max(inc, t);
+        hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+    }
+    u32 before = __shfl_up_sync(0xffffffffu, inc, 1);  // max over earlier lanes
+    if (lane == 0) before = 0;
+    if (lane == 31) s_warp[warp] = inc;
+    if (lane == 0) s_count[warp] = hsum;
+    __syncthreads();
+    u32 wmax = 0, tile_max = 0, tile_heads = 0;
+#pragma unroll
+    for (int w = 0; w < kRankBlock / 32; ++w) {
+        if (w < warp) wmax = max(wmax, s_warp[w]);
+        tile_max = max(tile_max, s_warp[w]);
+        tile_heads += s_count[w];
+    }
+    if (tid == 0) {
+        u32 excl = 0;
+        if (tile_max != 0 || tile == 0) {
+            st_relaxed_u64(desc + tile, kDescInclusive | tile_max);
+        } else {
+            st_relaxed_u64(desc + tile, kDescAggregate | 0u);
+            long long t = static_cast<long long>(tile) - 1;
+            for (;;) {
+                const u64 d = ld_relaxed_u64(desc + t);
+                if ((d >> 62) == 0) continue;
+                excl = max(excl, static_cast<u32>(d));
+                if (d & kDescInclusive) break;
+                --t;
+            }
+            st_relaxed_u64(desc + tile, kDescInclusive | excl);
+        }
+        // tiles with a head never read s_prefix for elements after it; elements before the
+        // first head of the tile need the previous tiles' maximum:
+        if (tile_max != 0 && tile > 0) {
+            long long t = static_cast<long long>(tile) - 1;
+            for (;;) {
+                const u64 d = ld_relaxed_u64(desc + t);
+                if ((d >> 62) == 0) continue;
+                excl = max(excl, static_cast<u32>(d));
+                if (d & kDescInclusive) break;
+                --t;
+            }
+        }
+        s_prefix = excl;
+        if (tile_heads) atomicAdd(num_heads, tile_heads);
+    }
+    __syncthreads();
+    const u32 carry = max(max(s_prefix, wmax), before);
+#pragma unroll
+    for (int j = 0; j < kRankItems; ++j) {
+        const u64 idx = base + j;
+        if (idx < n) {
+            const u32 h = max(m[j], carry) - 1u;
+            head_of[idx] = h;
+            rank[sa[idx]] = h;
+        }
+    }
+}
+
+// ---- doubling round: build the pair keys --------------------------------------------
+
+__global__ void __launch_bounds__(256)
+pair_key_kernel(const u32* __restrict__ sa, const u32* __restrict__ head_of,
+                const u32* __restrict__ rank, u64 n, u64 h, int rank_bits,
+                u64* __restrict__ keys, PassTable pt, u32* __restrict__ g_hist) {
+    extern __shared__ u32 s_hist[];
+    for (int i = threadIdx.x; i < pt.count * kRadix; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    const u64 rounds = (n + stride - 1) / stride;
+    u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (u64 r = 0; r < rounds; ++r, idx += stride) {
+        const bool in = idx < n;
+        u64 key = 0;
+        if (in) {
+            const u64 p = static_cast<u64>(sa[idx]) + h;
+            // suffix_array.hpp:93-96: rank of the suffix h further on, +1, 0 past the end
+            const u64 k2 = p < n ? static_cast<u64>(rank[p]) + 1u : 0u;
+            key = (static_cast<u64>(head_of[idx]) << rank_bits) | k2;
+            keys[idx] = key;
+        }
+        for (int p = 0; p < pt.count; ++p)
+            hist_add(s_hist + p * kRadix, key_digit(key, pt.shift[p], pt.mask(p)), in);
+    }
+    __syncthreads();
+    hist_flush(s_hist, g_hist, pt.count);
+}
+
+unsigned grid_for(const reseq_cuda_ctx* ctx, size_t n, int block, int per_thread, int waves) {
+    size_t want = (n + static_cast<size_t>(block) * per_thread - 1) /
+                  (static_cast<size_t>(block) * per_thread);
+    const size_t cap = static_cast<size_t>(ctx->sm_count) * waves;
+    if (want < 1) want = 1;
+    return static_cast<unsigned>(want < cap ? want : cap);
+}
+
+}  // namespace
+
+int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed, u64* sent,
+                    u32* d_flag, bool* is_dna) {
+    cudaStream_t s = ctx->stream;
+    RSQ_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(u32), s));
+    RSQ_CUDA(cudaMemsetAsync(packed + (n / 64) * 2, 0,
+                             sizeof(u64) * ((n / 32 + 8) - (n / 64) * 2), s));
+    RSQ_CUDA(cudaMemsetAsync(sent + n / 64, 0, sizeof(u64) * ((n / 64 + 8) - n / 64), s));
+    const unsigned grid = grid_for(ctx, (n + 63) / 64, 256, 1, 8);
+    if (reinterpret_cast<uintptr_t>(d_text) % 16 == 0)
+        pack_dna_kernel<true><<<grid, 256, 0, s>>>(d_text, n, packed, sent, d_flag);
+    else
+        pack_dna_kernel<false><<<grid, 256, 0, s>>>(d_text, n, packed, sent, d_flag);
+    ++ctx->launches;
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_flag, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    *is_dna = (*reinterpret_cast<volatile u32*>(ctx->pinned)) == 0;
+    return RESEQ_OK;
+}
+
+size_t sa_workspace_bytes(size_t n) {
+    auto pad = reseq_cuda_ctx::padded;
+    size_t total = 0;
+    total += pad(sizeof(u64) * (n / 32 + 8));        // packed bases
+    total += pad(sizeof(u64) * (n / 64 + 8));        // sentinel bitmap
+    total += 2 * pad(sizeof(u64) * n);               // key buffers a / b
+    total += 2 * pad(sizeof(u32) * n);               // payload buffer b, head_of
+    total += pad(sizeof(u32) * n);                   // rank when the caller wants none
+    total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
+    total += pad(1024);                              // counters
+    total += sort_workspace_bytes(n);
+    return total + 4096;
+}
+
+int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, u32* d_rank,
+                    reseq_sa_stats* stats) {
+    reseq_sa_stats st{};
+    const uint64_t launches0 = ctx->launches;
+    if (n > RESEQ_CUDA_MAX_TEXT)
+        return fail(RESEQ_TEXT_TOO_LARGE, "text of length " + std::to_string(n) + " exceeds 2^32-2");
+    if (n == 0) {
+        if (stats) *stats = st;
+        return RESEQ_OK;
+    }
+    cudaStream_t s = ctx->stream;
+
+    u64* packed = ctx->alloc<u64>(n / 32 + 8);
+    u64* sent = ctx->alloc<u64>(n / 64 + 8);
+    u64* keys_a = ctx->alloc<u64>(n);
+    u64* keys_b = ctx->alloc<u64>(n);
+    u32* vals_b = ctx->alloc<u32>(n);
+    u32* head_of = ctx->alloc<u32>(n);
+    u32* rank = d_rank ? d_rank : ctx->alloc<u32>(n);
+    const size_t rank_tiles = (n + kRankTile - 1) / kRankTile;
+    u64* desc = ctx->alloc<u64>(rank_tiles + 4);
+    u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads
+    SortWorkspace ws;
+    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters)
+        return fail(RESEQ_OUT_OF_MEMORY, "suffix-array workspace does not fit the reserved arena");
+    RSQ_TRY(sort_workspace_carve(ctx, n, &ws));
+
+    // -- pack, decide the alphabet ----------------------------------------------------
+    RSQ_CUDA(cudaMemsetAsync(counters, 0, 1024, s));
+    bool dna = false;
+    RSQ_TRY(pack_dna_device(ctx, d_text, n, packed, sent, counters, &dna));
+    st.alphabet = dna ? 0 : 1;
+
+    // -- initial keys + their digit histograms, 32-bit LSD sort --------------------------
+    u32* k32_a = reinterpret_cast<u32*>(keys_a);
+    u32* k32_b = reinterpret_cast<u32*>(keys_b);
+    const int key_bits = dna ? 2 * kDnaK + kDnaFieldBits : 8 * kByteK + kByteFieldBits;
+    const PassTable pt0 = make_passes(0, key_bits);
+    RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * pt0.count * kRadix, s));
+    {
+        const unsigned grid = grid_for(ctx, n, 256, 8, 8);
+        const size_t smem = sizeof(u32) * pt0.count * kRadix;
+        if (dna)
+            initkey_dna_kernel<<<grid, 256, smem, s>>>(packed, sent, n, k32_a, d_sa, pt0, ws.hist);
+        else
+            initkey_bytes_kernel<<<grid, 256, smem, s>>>(d_text, n, k32_a, d_sa, pt0, ws.hist);
+        ++ctx->launches;
+        RSQ_CUDA(cudaGetLastError());
+    }
+    bool in_b = false;
+    RSQ_TRY(onesweep_sort<u32>(ctx, k32_a, k32_b, d_sa, vals_b, n, pt0, ws, true, 0, &in_b));
+    st.sort_passes += pt0.count;
+    st.init_symbols = dna ? kDnaK : kByteK;
+    u32* sa_cur = in_b ? vals_b : d_sa;
+    u32* sa_alt = in_b ? d_sa : vals_b;
+
+    auto rerank = [&](auto* keys, u32 uniq_mask, u32 uniq_full) -> int {
+        RSQ_CUDA(cudaMemsetAsync(desc, 0, sizeof(u64) * (rank_tiles + 4), s));
+        RSQ_CUDA(cudaMemsetAsync(counters + 1, 0, 2 * sizeof(u32), s));
+        using K = std::remove_pointer_t<decltype(keys)>;
+        rerank_kernel<K><<<static_cast<unsigned>(rank_tiles), kRankBlock, 0, s>>>(
+            keys, sa_cur, n, uniq_mask, uniq_full, rank, head_of, desc, counters + 1, counters + 2);
+        ++ctx->launches;
+        RSQ_CUDA(cudaGetLastError());
+        RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 2, sizeof(u32), cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaStreamSynchronize(s));
+        return RESEQ_OK;
+    };
+
+    const u32 field_mask = (1u << (dna ? kDnaFieldBits : kByteFieldBits)) - 1u;
+    const u32 field_full = 2u * (dna ? kDnaK : kByteK);
+    RSQ_TRY(rerank(in_b ? k32_b : k32_a, field_mask, field_full));
+    u64 heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
+
+    // -- prefix doubling ------------------------------------------------------------------
+    const int b = static_cast<int>(bit_width_u64(n));
+    const PassTable pt = make_passes(0, 2 * b);
+    for (u64 h = st.init_symbols; heads < n && h < n; h <<= 1) {
+        RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * pt.count * kRadix, s));
+        {
+            const unsigned grid = grid_for(ctx, n, 256, 8, 8);
+            pair_key_kernel<<<grid, 256, sizeof(u32) * pt.count * kRadix, s>>>(
+                sa_cur, head_of, rank, n, h, b, keys_a, pt, ws.hist);
+            ++ctx->launches;
+            RSQ_CUDA(cudaGetLastError());
+        }
+        RSQ_TRY(onesweep_sort<u64>(ctx, keys_a, keys_b, sa_cur, sa_alt, n, pt, ws, true, 0, &in_b));
+        st.sort_passes += pt.count;
+        if (in_b) { u32* t = sa_cur; sa_cur = sa_alt; sa_alt = t; }
+        RSQ_TRY(rerank(in_b ? keys_b : keys_a, 0u, 0u));
+        heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
+        ++st.rounds;
+        st.refined_global += n;
+    }
+
+    if (sa_cur != d_sa)
+        RSQ_CUDA(cudaMemcpyAsync(d_sa, sa_cur, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
+    st.kernel_launches = ctx->launches - launches0;
+    if (stats) *stats = st;
+    return RESEQ_OK;
+}
+
+}  // namespace rsq

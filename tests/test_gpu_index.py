@@ -1,0 +1,172 @@
+"""Parity of the device fragment index (locate / start ranks / overlaps / greedy) with the
+oracle -- the cases of proj/tests/test_fragment_index.cpp plus the overlap result contract
+(overlap.hpp), through the C ABI."""
+import numpy as np
+import pytest
+
+from tests.oracle_lib import concat_of
+
+pytestmark = pytest.mark.gpu
+
+WORKED = [b"GATT", b"ACA", b"GGT", b"GA", b"TTAC", b"AGGT"]
+PAPER5 = [b"abthatb", b"hatbpaab", b"tbabhhatbpaa", b"paabtabh", b"bhaabtpb"]
+
+
+def random_frags(rng, k, lo, hi, alphabet=(65, 67, 71, 84), probs=None):
+    return [bytes(rng.choice(alphabet, int(rng.integers(lo, hi + 1)), p=probs).astype(np.uint8)) for _ in range(k)]
+
+
+def shotgun(rng, G, k, lo, hi, alphabet=(65, 67, 71, 84)):
+    genome = rng.choice(alphabet, G).astype(np.uint8)
+    out = []
+    for _ in range(k):
+        ln = min(G, int(rng.integers(lo, hi + 1)))
+        s = int(rng.integers(0, G - ln + 1))
+        out.append(bytes(genome[s:s + ln]))
+    return out
+
+
+def test_locate_on_the_worked_instance(rq, ex):
+    # test_fragment_index.cpp:33-45
+    ix = rq.FragmentIndex(rq.make_fragment_set(WORKED, "dna"), ex)
+    lo, hi = ix.locate_prefix_range(b"GA")
+    assert hi - lo == 2
+    assert sorted(ix.sa()[lo:hi].tolist()) == [0, 13]
+    lo, hi = ix.locate_prefix_range(b"QQ")
+    assert lo == hi
+
+
+def test_single_fragment_exact(rq, ex):
+    # test_fragment_index.cpp:47-53
+    ix = rq.FragmentIndex(rq.make_fragment_set([b"GATT"], "dna"), ex)
+    lo, hi = ix.locate_prefix_range(b"GATT")
+    assert hi - lo == 1 and ix.sa()[lo] == 0
+
+
+def test_structure_matches_oracle_on_paper_fragments(rq, ex, oracle):
+    # test_fragment_index.cpp:129-138
+    fs = rq.make_fragment_set(PAPER5, "generic_byte")
+    ix = rq.FragmentIndex(fs, ex)
+    wsa, wrank = oracle.build_sa(fs.concat)
+    assert np.array_equal(ix.sa(), wsa) and np.array_equal(ix.rank(), wrank)
+    assert np.array_equal(ix.start_rank_list(), oracle.start_rank_list(wrank, fs.starts))
+
+
+def test_intervals_equal_the_oracle_binary_search(rq, ex, oracle):
+    # test_fragment_index.cpp:55-80 (maximality) strengthened to exact equality, incl. absent
+    # patterns (insertion point) and patterns with bytes outside the alphabet
+    rng = np.random.default_rng(51)
+    for it in range(60):
+        dna = it % 2 == 0
+        alpha = (65, 67, 71, 84) if dna else (97, 98)
+        frags = random_frags(rng, 1 + int(rng.integers(0, 8)), 1, 6 if not dna else 30, alpha)
+        fs = rq.make_fragment_set(frags, "dna" if dna else "generic_byte")
+        ix = rq.FragmentIndex(fs, ex)
+        sa = ix.sa()
+        pats = [bytes(rng.choice(alpha, 1 + int(rng.integers(0, 4))).astype(np.uint8)) for _ in range(12)]
+        pats += [b"QQ", b"B", b"AQ", b"z", b"!"]
+        pats += [f[int(rng.integers(0, len(f))):] for f in frags]
+        lo, hi = ix.locate_batch(pats)
+        for p, l, h in zip(pats, lo, hi):
+            assert (int(l), int(h)) == oracle.locate(fs.concat, sa, p), (frags, p)
+
+
+def test_locate_with_directory_on_read_sets(rq, ex, oracle):
+    rng = np.random.default_rng(52)
+    frags = shotgun(rng, 20_000, 4_000, 40, 120)
+    fs = rq.make_fragment_set(frags, "dna")
+    ix = rq.FragmentIndex(fs, ex)
+    sa = ix.sa()
+    assert oracle.verify_sa(fs.concat, sa) == 0
+    pats, fr, of = [], [], []
+    for _ in range(3000):
+        f = int(rng.integers(0, len(frags)))
+        o = int(rng.integers(0, len(frags[f])))
+        fr.append(f); of.append(o)
+        pats.append(frags[f][o:])
+    absent = [bytes(rng.choice([65, 67, 71, 84], int(rng.integers(1, 40))).astype(np.uint8)) for _ in range(500)]
+    lo, hi = ix.locate_batch(pats + absent)
+    rlo, rhi = ix.locate_residuals(fr, of)
+    for t, p in enumerate(pats + absent):
+        want = oracle.locate(fs.concat, sa, p)
+        assert (int(lo[t]), int(hi[t])) == want
+        if t < len(pats):
+            assert (int(rlo[t]), int(rhi[t])) == want
+    with pytest.raises(rq.OffsetOutOfRangeError):
+        ix.locate_residuals([0], [len(frags[0])])
+
+
+def _check_overlaps(rq, ex, oracle, frags, alphabet, min_ov):
+    fs = rq.make_fragment_set(frags, alphabet)
+    ix = rq.FragmentIndex(fs, ex)
+    ov = ix.overlaps(min_ov)
+    lens = fs.lengths()
+    wi, wj, ww = oracle.overlap_list(fs.concat, fs.starts, lens, min_ov)
+    assert np.array_equal(ov.i, wi) and np.array_equal(ov.j, wj) and np.array_equal(ov.w, ww), frags
+    keep = oracle.absorb_contained(fs.concat, fs.starts, lens)
+    assert np.array_equal(np.flatnonzero(ov.contained == 0).astype(np.uint32), keep), frags
+    assert ov.queries == int(np.maximum(lens.astype(np.int64) - min_ov + 1, 0).sum())
+    return fs, ix, ov
+
+
+def test_overlap_lists_equal_the_dense_graph(rq, ex, oracle):
+    """overlap.hpp:35-45: every non-zero weight, tau = 1, on adversarial small sets (tiny
+    alphabets, duplicates, contained reads, mixed lengths)."""
+    rng = np.random.default_rng(53)
+    for it in range(120):
+        if it % 3 == 0:
+            frags = shotgun(rng, int(rng.integers(20, 80)), int(rng.integers(4, 16)), 3, 12, (65, 67))
+        elif it % 3 == 1:
+            frags = shotgun(rng, int(rng.integers(20, 80)), int(rng.integers(4, 16)), 5, 5)
+        else:
+            frags = random_frags(rng, int(rng.integers(2, 12)), 1, 9, (65, 67, 71, 84), [.6, .2, .1, .1])
+        fs, ix, ov = _check_overlaps(rq, ex, oracle, frags, "dna", 1)
+        dense = oracle.overlap_graph(fs.concat, fs.starts, fs.lengths())
+        assert np.array_equal(ov.dense(len(frags)), dense)
+    for it in range(30):  # generic alphabet
+        frags = shotgun(rng, 40, int(rng.integers(3, 12)), 2, 10, (97, 98, 104))
+        _check_overlaps(rq, ex, oracle, frags, "generic_byte", 1)
+
+
+def test_overlap_lists_on_read_sets(rq, ex, oracle):
+    rng = np.random.default_rng(54)
+    _check_overlaps(rq, ex, oracle, shotgun(rng, 30_000, 6_000, 100, 100), "dna", 20)
+    _check_overlaps(rq, ex, oracle, shotgun(rng, 8_000, 3_000, 30, 150), "dna", 16)
+    _check_overlaps(rq, ex, oracle, shotgun(rng, 3_000, 2_000, 60, 60), "dna", 5)     # duplicates, deep coverage
+    _check_overlaps(rq, ex, oracle, [b"ACGT" * 10] * 5 + [b"CGTA" * 10, b"A" * 30, b"A" * 31], "dna", 3)
+
+
+def test_greedy_reconstruction_matches_the_oracle(rq, ex, oracle):
+    """overlap.hpp:80-113 end to end: device overlaps + host merge == the reference loop."""
+    # the paper's example: SPEC.md:300
+    fs = rq.make_fragment_set(PAPER5, "generic_byte")
+    sup, order = rq.greedy_superstring_with_order(fs, exec=ex)
+    assert sup == b"abthatbabhhatbpaabtabhaabtpb" and order.tolist() == [0, 2, 1, 3, 4]
+    rng = np.random.default_rng(55)
+    for it in range(150):
+        if it % 2:
+            frags = shotgun(rng, int(rng.integers(20, 80)), int(rng.integers(4, 16)), 4, 14, (65, 67))
+        else:
+            frags = shotgun(rng, int(rng.integers(30, 120)), int(rng.integers(4, 20)), 8, 25)
+        fs = rq.make_fragment_set(frags, "dna")
+        ix = rq.FragmentIndex(fs, ex)
+        want = oracle.greedy(fs.concat, fs.starts, fs.lengths())
+        for tau in (1, 4):
+            sup, order = rq.greedy_superstring_with_order(fs, ix, tau)
+            assert sup == want[0] and order.tolist() == want[1].tolist(), (frags, tau)
+
+
+def test_reconstruction_at_config1_scale_properties(rq, ex):
+    """Config 1: every read is a substring of the reconstructed sequence, the order is a
+    permutation of the kept reads, and a second run is byte-identical."""
+    text, starts = rq.synth_read_text(200_000, 100, 20_000)
+    fs = rq.fragment_set_from_text(text, starts)
+    ix = rq.FragmentIndex(fs, ex)
+    ov = ix.overlaps(20)
+    sup, order = rq.greedy_superstring_from_overlaps(fs, ov)
+    sup2, order2 = rq.greedy_superstring_from_overlaps(fs, ix.overlaps(20))
+    assert sup == sup2 and np.array_equal(order, order2)
+    kept = np.flatnonzero(ov.contained == 0)
+    assert sorted(order.tolist()) == kept.tolist()
+    for i in range(0, len(starts), 97):
+        assert fs.bytes(i) in sup

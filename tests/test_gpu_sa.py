@@ -1,0 +1,176 @@
+"""Parity of the device suffix-array builder with the oracle -- the cases of
+proj/tests/test_suffix_array.cpp plus read-set shaped and adversarial texts, through
+reseq_cuda_build_sa."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def check(rq, ex, oracle, text):
+    got = rq.build_parallel(text, ex)
+    wsa, wrank = oracle.build_sa(text)
+    assert np.array_equal(got.sa, wsa), f"sa differs for text of length {len(text)}"
+    assert np.array_equal(got.rank, wrank)
+    return got
+
+
+def test_classic_inputs(rq, ex, oracle):
+    # test_suffix_array.cpp:10-14
+    assert rq.build_parallel(b"banana", ex).sa.tolist() == [5, 3, 1, 0, 4, 2]
+    assert rq.build_parallel(b"aaa", ex).sa.tolist() == [2, 1, 0]
+    r = rq.build_parallel(b"", ex)
+    assert r.sa.size == 0 and r.rank.size == 0
+    assert rq.build_parallel(b"x", ex).sa.tolist() == [0]
+
+
+def test_rank_is_the_inverse_of_sa(rq, ex):
+    # test_suffix_array.cpp:16-21
+    r = rq.build_parallel(b"mississippi", ex)
+    assert np.array_equal(r.rank[r.sa], np.arange(r.sa.size, dtype=np.uint32))
+
+
+def test_exhaustive_ab_strings(rq, ex, oracle):
+    # test_suffix_array.cpp:23-36: all 510 strings over {a,b} of length 1..8
+    for length in range(1, 9):
+        for mask in range(1 << length):
+            s = bytes(ord("b") if (mask >> i) & 1 else ord("a") for i in range(length))
+            check(rq, ex, oracle, s)
+
+
+def test_sentinel_ties_break_by_position(rq, ex, oracle):
+    # test_suffix_array.cpp:38-44
+    got = check(rq, ex, oracle, b"GA\0TT\0")
+    assert got.sa.tolist() == [2, 5, 1, 0, 4, 3]
+    assert got.stats.alphabet == 0  # the 2-bit DNA path
+
+
+def test_random_sentinel_joined_texts(rq, ex, oracle):
+    # test_suffix_array.cpp:46-61 (own RNG: the property, not the stream, is what matters)
+    rng = np.random.default_rng(41)
+    for _ in range(150):
+        parts = []
+        for _f in range(1 + int(rng.integers(0, 5))):
+            ln = 1 + int(rng.integers(0, 6))
+            parts.append(bytes(rng.choice([97, 98], ln).astype(np.uint8)) + b"\0")
+        check(rq, ex, oracle, b"".join(parts))
+    for _ in range(100):  # the same with the DNA alphabet (2-bit path)
+        parts = []
+        for _f in range(1 + int(rng.integers(0, 6))):
+            ln = 1 + int(rng.integers(0, 40))
+            parts.append(bytes(rng.choice([65, 67, 71, 84], ln, p=[.7, .1, .1, .1]).astype(np.uint8)) + b"\0")
+        check(rq, ex, oracle, b"".join(parts))
+
+
+def test_random_dna_4096(rq, ex, oracle):
+    # test_suffix_array.cpp:63-72
+    rng = np.random.default_rng(43)
+    check(rq, ex, oracle, bytes(rng.choice([65, 67, 71, 84], 4096).astype(np.uint8)))
+
+
+@pytest.mark.parametrize("n", [2, 3, 12, 13, 14, 25, 26, 27, 63, 64, 65, 2047, 2048, 2049, 4095, 4096, 4097,
+                               8193, 100_003])
+def test_sizes_around_tile_and_kmer_boundaries(rq, ex, oracle, n):
+    rng = np.random.default_rng(n)
+    check(rq, ex, oracle, bytes(rng.choice([65, 67, 71, 84], n).astype(np.uint8)))       # no sentinel at all
+    t = rng.choice([65, 67, 71, 84, 0], n, p=[.24, .24, .24, .24, .04]).astype(np.uint8)  # ragged reads
+    check(rq, ex, oracle, bytes(t))
+    t[-1] = 0
+    check(rq, ex, oracle, bytes(t))
+
+
+def test_adversarial_repeats(rq, ex, oracle):
+    check(rq, ex, oracle, b"A" * 5000)                       # one run: log2(n) doubling rounds
+    check(rq, ex, oracle, b"A" * 3000 + b"\0")
+    check(rq, ex, oracle, (b"A" * 150 + b"\0") * 300)        # identical reads: ties only by sentinel position
+    check(rq, ex, oracle, (b"ACGT" * 40 + b"\0") * 200)      # periodic reads
+    check(rq, ex, oracle, b"\0" * 1000)                      # only sentinels
+    check(rq, ex, oracle, b"\0\0A\0\0\0CC\0" * 50)
+    check(rq, ex, oracle, b"AC" * 4000)
+    rng = np.random.default_rng(5)
+    unit = bytes(rng.choice([65, 67, 71, 84], 700).astype(np.uint8))
+    check(rq, ex, oracle, unit * 12)                         # long exact repeats, no sentinel
+
+
+def test_generic_byte_texts(rq, ex, oracle):
+    got = check(rq, ex, oracle, b"abthatb\0hatbpaab\0tbabhhatbpaa\0paabtabh\0bhaabtpb\0")
+    assert got.stats.alphabet == 1
+    rng = np.random.default_rng(6)
+    check(rq, ex, oracle, bytes(rng.integers(1, 256, 20_000).astype(np.uint8)))
+    check(rq, ex, oracle, bytes(rng.integers(0, 4, 30_000).astype(np.uint8)))    # bytes 0..3, many sentinels
+    check(rq, ex, oracle, bytes(rng.choice([65, 67, 71, 84, 78], 50_000).astype(np.uint8)))  # DNA with N
+    check(rq, ex, oracle, b"ab" * 3000 + b"\0" + b"ba" * 1000)
+    check(rq, ex, oracle, bytes([255]) * 4000)
+
+
+@pytest.mark.parametrize("G,L,k", [(5_000, 100, 500), (50_000, 100, 5_000), (100_000, 150, 6_000)])
+def test_read_sets_against_the_oracle(rq, ex, oracle, G, L, k):
+    text, _ = rq.synth_read_text(G, L, k)
+    got = check(rq, ex, oracle, text)
+    assert got.stats.alphabet == 0 and got.stats.init_symbols == 13
+    assert got.stats.rounds <= 4
+
+
+def test_reference_bench_input_fingerprint(rq, ex, oracle):
+    """make_random_dna(1<<20, 1): checksum_u32(sa) == 7546189330682201289 (BASELINE.md section 2,
+    the reference's own build_parallel and build_naive)."""
+    text = rq.synth_random_dna(1 << 20, 1)
+    got = rq.build_parallel(text, ex)
+    assert oracle.checksum_u32(got.sa) == 7546189330682201289
+    assert oracle.verify_sa(text, got.sa) == 0
+    assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
+
+
+def test_config1_full_size_fingerprint_and_proof(rq, ex, oracle):
+    """BASELINE config 1 (1 Mbp genome, 100 bp reads, 10x; n = 10 100 000): the reference's
+    build_parallel == build_naive gave checksum_u32(sa) = 11642757783061468293; the
+    permutation + adjacent-order verifier is a proof of equality at this size."""
+    text, _ = rq.synth_read_text(1_000_000, 100, 100_000)
+    got = rq.build_parallel(text, ex)
+    assert got.stats.rounds == 3
+    assert oracle.checksum_u32(got.sa) == 11642757783061468293
+    assert oracle.verify_sa(text, got.sa) == 0
+    assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
+
+
+def test_config2_full_size_proof(rq, ex, oracle):
+    """BASELINE config 2 (4.6 Mbp, 150 bp, 30x; n = 138 920 000): size-independent proof."""
+    text, _ = rq.synth_read_text(4_600_000, 150, 920_000)
+    got = rq.build_parallel(text, ex)
+    assert got.stats.rounds == 4
+    assert oracle.verify_sa(text, got.sa, threads=32) == 0
+    assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
+
+
+def test_text_too_large_is_rejected_before_any_work(rq, ex):
+    lib = rq._lib.load()
+    dummy = np.zeros(16, np.uint8)
+    out = np.zeros(16, np.uint32)
+    st = lib.reseq_cuda_build_sa(ex.handle, dummy.ctypes.data_as(C.c_void_p), C.c_size_t(0xFFFFFFFF),
+                                 out.ctypes.data_as(C.c_void_p), None, None)
+    assert st == rq._lib.TEXT_TOO_LARGE
+    with pytest.raises(rq.TextTooLargeError):
+        rq._lib.check(st)
+
+
+def test_device_resident_entry_point(rq, ex, oracle):
+    import torch
+    text, _ = rq.synth_read_text(30_000, 100, 3_000)
+    d_text = torch.from_numpy(text).cuda()
+    d_sa = torch.empty(text.size, dtype=torch.int32, device="cuda")
+    d_rank = torch.empty(text.size, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    lib = rq._lib.load()
+    st = rq.SaStats()
+    rq._lib.check(lib.reseq_cuda_build_sa_device(ex.handle, C.c_void_p(d_text.data_ptr()), text.size,
+                                                 C.c_void_p(d_sa.data_ptr()), C.c_void_p(d_rank.data_ptr()),
+                                                 C.byref(st)))
+    ex.synchronize()
+    wsa, wrank = oracle.build_sa(text)
+    assert np.array_equal(d_sa.cpu().numpy().view(np.uint32), wsa)
+    assert np.array_equal(d_rank.cpu().numpy().view(np.uint32), wrank)
+    h = C.c_uint64()
+    rq._lib.check(lib.reseq_cuda_checksum_u32_device(ex.handle, C.c_void_p(d_sa.data_ptr()), text.size, C.byref(h)))
+    assert h.value == oracle.checksum_u32(wsa)
