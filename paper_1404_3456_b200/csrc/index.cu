@@ -46,6 +46,7 @@ struct reseq_cuda_index {
     u32* d_lens = nullptr;
     u32* d_start_rank = nullptr;  // start_rank_list
     u32* d_start_frag = nullptr;  // fragment id of each start_rank_list entry
+    u32* d_start_inv = nullptr;   // position of each fragment in start_rank_list
     u32* d_dir = nullptr;         // 4^D + 1 entries (+1 leading scan slot)
     u32* d_sdir = nullptr;
     u32 max_len = 0;
@@ -183,6 +184,12 @@ __global__ void lens_kernel(const u32* __restrict__ starts, u64 k, u64 n, u32* _
     if (lane_id() == 0 && local_max) atomicMax(max_len, local_max);
 }
 
+__global__ void invert_kernel(const u32* __restrict__ start_frag, u64 k, u32* __restrict__ start_inv) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 t = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; t < k; t += stride)
+        start_inv[start_frag[t]] = static_cast<u32>(t);
+}
+
 // code(s) of the header comment; D <= 16.
 __device__ __forceinline__ u32 dir_code(const u64* __restrict__ packed, const u64* __restrict__ sent,
                                         u64 n, u64 pos, int D) {
@@ -216,6 +223,7 @@ struct IndexView {
     const u32* lens;
     const u32* start_rank;
     const u32* start_frag;
+    const u32* start_inv;
     const u32* dir;   // dir[x] = lower bound of D-base pattern x; nullptr when absent
     const u32* sdir;
     int D;
@@ -309,10 +317,12 @@ overlap_count_kernel(IndexView iv, u32 min_ov, const u64* __restrict__ qoff, u32
             const u32 m = len - o;
             u32 lo, hi, sf, sl;
             locate_residual(iv, start + o, m, &lo, &hi, &sf, &sl);
-            u32 cnt = sl - sf;
+            // f_i's own start suffix lies in the interval at o = 0, and at o > 0 whenever f_i
+            // overlaps itself; the diagonal is zero by convention (overlap.hpp:26,41)
+            const u32 self = iv.start_inv[i];
+            const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
+            const u32 cnt = sl - sf - self_in;
             if (o == 0) {
-                // the o = 0 interval contains f_i's own start suffix: not an overlap
-                cnt -= 1;
                 u32 exact = 0, min_id = 0xFFFFFFFFu;
                 for (u32 t = sf; t < sl; ++t) {
                     const u32 id = iv.start_frag[t];
@@ -324,7 +334,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, const u64* __restrict__ qoff, u32
                 contained[i] = (hi - lo > exact) || (min_id < static_cast<u32>(i));
             }
             if (o < nq) {
-                q_first[qbase + o] = sf;
+                q_first[qbase + o] = sf | (self_in << 31);  // k < 2^31: a fragment takes >= 2 bytes
                 q_count[qbase + o] = cnt;
             }
         }
@@ -348,8 +358,8 @@ overlap_fill_kernel(IndexView iv, const u64* __restrict__ qoff, const u32* __res
             const u32 cnt = q_count[qbase + o];
             if (!cnt) continue;
             u32 out = q_out[qbase + o];
-            const u32 sf = q_first[qbase + o];
-            const u32 span = cnt + (o == 0 ? 1u : 0u);
+            const u32 sf = q_first[qbase + o] & 0x7FFFFFFFu;
+            const u32 span = cnt + (q_first[qbase + o] >> 31);
             for (u32 t = 0; t < span; ++t) {
                 const u32 j = iv.start_frag[sf + t];
                 if (j == static_cast<u32>(i)) continue;
@@ -388,6 +398,7 @@ IndexView view_of(const reseq_cuda_index* ix) {
     iv.lens = ix->d_lens;
     iv.start_rank = ix->d_start_rank;
     iv.start_frag = ix->d_start_frag;
+    iv.start_inv = ix->d_start_inv;
     iv.dir = ix->dna && ix->d_dir ? ix->d_dir + 1 : nullptr;
     iv.sdir = ix->dna && ix->d_sdir ? ix->d_sdir + 1 : nullptr;
     iv.D = ix->dir_bases;
@@ -454,6 +465,7 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     IX_TRY(dev_alloc(ix, &ix->d_lens, k));
     IX_TRY(dev_alloc(ix, &ix->d_start_rank, k));
     IX_TRY(dev_alloc(ix, &ix->d_start_frag, k));
+    IX_TRY(dev_alloc(ix, &ix->d_start_inv, k));
     IX_TRY(dev_alloc(ix, &ix->d_packed, n / 32 + 8));
     IX_TRY(dev_alloc(ix, &ix->d_sent, n / 64 + 8));
     IX_CUDA(cudaMemcpyAsync(ix->d_text, concat, n, cudaMemcpyHostToDevice, s));
@@ -501,6 +513,9 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
         IX_CUDA(cudaMemcpyAsync(ix->d_start_rank, keys_a, sizeof(u32), cudaMemcpyDeviceToDevice, s));
         IX_CUDA(cudaMemcpyAsync(ix->d_start_frag, ids_a, sizeof(u32), cudaMemcpyDeviceToDevice, s));
     }
+    invert_kernel<<<grid_1d(ctx, k, 256), 256, 0, s>>>(ix->d_start_frag, k, ix->d_start_inv);
+    ++ctx->launches;
+    IX_CUDA(cudaGetLastError());
     IX_CUDA(cudaMemcpyAsync(ctx->pinned, counters, sizeof(u32), cudaMemcpyDeviceToHost, s));
     IX_CUDA(cudaStreamSynchronize(s));
     ix->max_len = *reinterpret_cast<volatile u32*>(ctx->pinned);
