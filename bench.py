@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: suffix-array build (Msuffixes/s) + overlap queries/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c1|c2|c3]
+
+One "step" = one complete SA build (2-bit pack, k-mer initial sort, prefix-doubling rounds)
+over the synthetic read text of the named BASELINE.json configuration.  Prints ONE JSON line.
+
+  value    : n_suffixes * steps / device time, text already resident in HBM (CUDA events on
+             the launching stream, max over ranks)
+  e2e      : the same build through the host-buffer C-ABI call reseq_cuda_build_sa (pinned
+             host text in, sa + rank out to pinned host buffers; H2D and D2H inside the timed
+             region)
+  roofline : the dominant kernel (one onesweep digit pass over (u64 key, u32 position) pairs),
+             timed live with CUDA events around every launch inside the timed region
+  cpu_baseline : the reference's own build_parallel (oracle/_ref) on a bounded prefix of the
+             same text, on this box's host cores
+  overlap  : the batched SA binary-search job (queries/s), measured once after the timed steps
+
+`--impl reference` times the reference CPU implementation only (no GPU work).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (genome bases, read length, reads) -- SURVEY.md section 8(d) / BASELINE.md section 3
+    "c1": (1_000_000, 100, 100_000),
+    "c2": (4_600_000, 150, 920_000),
+    "c3": (10_000_000, 150, 666_666),
+    "c4": (100_000_000, 150, 6_666_666),
+}
+DESCRIPTION = {
+    "c1": "config[0]: 1 Mbp genome, 100-bp reads, 10x (n=10.1M suffixes)",
+    "c2": "config[1]: 4.6 Mbp genome, 150-bp reads, 30x (n=138.92M suffixes)",
+    "c3": "config[2]: 100 Mbp concatenated read text (n=100.67M suffixes)",
+    "c4": "config[3]: 1 Gbp read set (n=1.0067G suffixes)",
+}
+METRIC = "sa_build_msuffixes_per_s"
+UNIT = "Msuffixes/s"
+
+
+def bytes_alg_per_suffix(n: int, read_len: int) -> tuple[float, int, int]:
+    """80 + R16*(44 + 24*P) + 8 with P = ceil(2*ceil(log2(n+2))/8)."""
+    b = int(np.ceil(np.log2(n + 2)))
+    P = -(-2 * b // 8)
+    R16 = int(np.ceil(np.log2(np.ceil((read_len + 1) / 16))))
+    return 80 + R16 * (44 + 24 * P) + 8, P, R16
+
+
+def measured_peak() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._pump, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- reference / CPU baseline ------------------------------------------------------------
+
+def _load_cpu_lib():
+    """oracle/_ref (the real reference) if present, else the oracle port.  The only place
+    bench.py touches oracle/: the CPU baseline, never the measured product path."""
+    ref = ROOT / "oracle" / "_ref" / "libreseq_ref.so"
+    if ref.exists():
+        try:
+            return C.CDLL(str(ref)), "reference"
+        except OSError:
+            pass
+    port = ROOT / "oracle" / "liboracle.so"
+    if not port.exists():
+        subprocess.run(["make", "-C", str(ROOT / "oracle"), "liboracle.so"], check=True,
+                       stdout=subprocess.DEVNULL)
+    return C.CDLL(str(port)), "port"
+
+
+def cpu_build(lib, kind: str, text: np.ndarray, workers: int) -> float:
+    """One reference build_parallel (or oracle build) of `text`; returns seconds."""
+    n = text.size
+    sa = np.empty(n, np.uint32)
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        st = lib.ref_build_parallel(vp(text), C.c_size_t(n), C.c_uint(workers), C.c_size_t(1 << 15), vp(sa), None)
+    else:
+        st = lib.orc_build_sa(vp(text), C.c_size_t(n), vp(sa), None)
+    dt = time.perf_counter() - t0
+    if st != 0:
+        raise RuntimeError("CPU baseline build failed")
+    return dt
+
+
+def cpu_sample(text: np.ndarray, read_len: int, target_bytes: int) -> np.ndarray:
+    reads = max(1, min(text.size, target_bytes) // (read_len + 1))
+    return np.ascontiguousarray(text[: reads * (read_len + 1)])
+
+
+def run_reference(args, text, read_len, workload):
+    lib, kind = _load_cpu_lib()
+    cores = os.cpu_count() or 1
+    workers = cores if kind == "reference" else 1
+    steps, warmup = args.steps, args.warmup
+    # calibrate the sample so that (steps + warmup) builds end within ~150 s
+    probe = cpu_sample(text, read_len, 1 << 17)
+    t_probe = cpu_build(lib, kind, probe, workers)
+    rate = probe.size / t_probe  # suffixes / s, roughly flat in n for this code
+    budget = 150.0 / max(1, steps + warmup)
+    target = int(min(1 << 20, max(1 << 16, rate * budget)))
+    sample = cpu_sample(text, read_len, target)
+    for _ in range(warmup):
+        cpu_build(lib, kind, sample, workers)
+    t = [cpu_build(lib, kind, sample, workers) for _ in range(steps)]
+    total = float(sum(t))
+    value = sample.size * steps / total / 1e6
+    desc = (f"first {sample.size // (read_len + 1)} reads ({sample.size} suffixes) of the {workload} text; "
+            f"{'reference build_parallel (suffix_array.hpp:61), executor{workers=' + str(workers) + ', chunk=32768}' if kind == 'reference' else 'oracle port (std::sort on suffix order), 1 thread'}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warmup, "ms_per_step": total / steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": DESCRIPTION[workload], "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+# ---- main arm ----------------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-overlap", action="store_true", help="skip the overlap-query measurement")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    workload = args.workload or "c2"
+    G, L, k = WORKLOADS[workload]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import paper_1404_3456_b200._lib as lib_mod  # synthetic generator only (host code)
+        lib = lib_mod.load()
+        # the reference arm needs only a prefix of the text: generate 2^20 bytes' worth of reads
+        kk = min(k, (1 << 20) // (L + 1) + 1)
+        text = np.empty(kk * (L + 1), np.uint8)
+        lib.reseq_synth_read_text(G, L, kk, 1, 2, text.ctypes.data_as(C.c_void_p), None)
+        run_reference(args, text, L, workload)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1404_3456_b200 as rq
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device; the reseq B200 backend has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    if world > 1:
+        from paper_1404_3456_b200 import sharded
+        sharded.bench_main(args, workload, rank, world, local_rank)
+        return
+
+    # ---- inputs: RNG-exact synthetic read text, pinned on the host, resident in HBM -----------
+    text, starts = rq.synth_read_text(G, L, k, 1, 2, pinned=True)
+    n = int(text.size)
+    ex = rq.Executor(local_rank)
+    stream = torch.cuda.current_stream()
+    ex.set_stream(stream.cuda_stream)
+    lib = rq._lib.load()
+    d_text = torch.from_numpy(text).cuda()
+    d_sa = torch.empty(n, dtype=torch.int32, device="cuda")
+    d_rank = torch.empty(n, dtype=torch.int32, device="cuda")
+    st = rq.SaStats()
+
+    def step_device():
+        rq._lib.check(lib.reseq_cuda_build_sa_device(ex.handle, C.c_void_p(d_text.data_ptr()), n,
+                                                     C.c_void_p(d_sa.data_ptr()), C.c_void_p(d_rank.data_ptr()),
+                                                     C.byref(st)))
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    ex.profile(True)
+    launches0 = ex.launch_count
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = ex.launch_count - launches0
+    prof = ex.profile_read()
+    ex.profile(False)
+    ms_per_step = ms_total / args.steps
+    value = n / (ms_per_step * 1e-3) / 1e6
+
+    # parity fingerprint of what was just built (size-independent proof runs in tests/)
+    sa_host = d_sa.cpu().numpy().view(np.uint32)
+    # rank[sa[i]] == i for every i  <=>  sa is a permutation and rank its inverse
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    perm_ok = bool(torch.equal((d_rank[(d_sa.to(torch.int64) & 0xFFFFFFFF)].to(torch.int64) & 0xFFFFFFFF), idx))
+    del idx
+
+    # ---- roofline of the dominant kernel ------------------------------------------------------
+    peak, peak_src = measured_peak()
+    per_suffix, P, R16 = bytes_alg_per_suffix(n, L)
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (0, 0.0))
+    dom_name, (dom_launches, dom_ms) = dom
+    pass_bytes = {"onesweep_u64_pairs": 24.0, "onesweep_u32_pairs": 16.0, "onesweep_u32_keys": 8.0}.get(dom_name, 0.0)
+    if dom_launches and pass_bytes:
+        achieved = pass_bytes * n / (dom_ms / dom_launches * 1e-3) / 1e9
+    else:
+        achieved = 0.0
+    kernel_ms = sum(v[1] for v in prof.values()) / args.steps
+    roofline = {
+        "bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak if peak else None, "traffic": None,
+        "peak_source": peak_src,
+        "alg_bytes_per_launch": pass_bytes * n, "launches_per_step": dom_launches / args.steps,
+        "avg_launch_ms": dom_ms / dom_launches if dom_launches else None,
+        "kernel_share_of_step": (dom_ms / args.steps) / ms_per_step,
+        "build": {"alg_bytes_per_suffix": per_suffix, "P": P, "R16": R16,
+                  "achieved_gbs": per_suffix * n / (ms_per_step * 1e-3) / 1e9,
+                  "frac": per_suffix * n / (ms_per_step * 1e-3) / 1e9 / peak},
+        "per_kernel_ms_per_step": {kname: v[1] / args.steps for kname, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "sum_kernel_ms_per_step": kernel_ms,
+    }
+
+    # ---- e2e: host buffers through the C ABI -----------------------------------------------------
+    h_sa = torch.empty(n, dtype=torch.int32).pin_memory()
+    h_rank = torch.empty(n, dtype=torch.int32).pin_memory()
+
+    def step_host():
+        rq._lib.check(lib.reseq_cuda_build_sa(ex.handle, C.c_void_p(text.ctypes.data), n,
+                                              C.c_void_p(h_sa.data_ptr()), C.c_void_p(h_rank.data_ptr()), None))
+
+    step_host()
+    e2e_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_host()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    same = bool(np.array_equal(h_sa.numpy().view(np.uint32), sa_host))
+    e2e = {"value": n / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": n, "d2h_bytes_per_step": 8 * n,
+           "ms_per_step": e2e_s * 1e3, "steps": e2e_steps, "matches_device_run": same}
+
+    # ---- overlap queries -------------------------------------------------------------------------
+    overlap = None
+    if not args.no_overlap:
+        del h_rank
+        fset = rq.fragment_set_from_text(text, starts)
+        t0 = time.perf_counter()
+        ix = rq.FragmentIndex(fset, ex)
+        torch.cuda.synchronize()
+        t_index = time.perf_counter() - t0
+        ix.overlaps(20)  # warm-up (arena growth)
+        t0 = time.perf_counter()
+        ov = ix.overlaps(20)
+        t_ov = time.perf_counter() - t0
+        overlap = {"metric": "overlap_queries_per_s", "min_overlap": 20, "queries": ov.queries,
+                   "value": ov.queries / (ov.device_ms * 1e-3) / 1e6, "unit": "Mqueries/s",
+                   "device_ms": ov.device_ms, "e2e_ms": t_ov * 1e3,
+                   "e2e_value": ov.queries / t_ov / 1e6, "overlaps_found": int(ov.i.size),
+                   "contained_reads": int(ov.contained.sum()), "index_build_ms": t_index * 1e3,
+                   "alg_bytes_per_query": 2 * int(np.ceil(np.log2(n))) * 64 + 64}
+        overlap["alg_frac_of_peak"] = overlap["alg_bytes_per_query"] * ov.queries / (ov.device_ms * 1e-3) / 1e9 / peak
+        ix.close()
+
+    # ---- CPU baseline -------------------------------------------------------------------------------
+    cpu = None
+    if not args.no_cpu:
+        cpu_lib, kind = _load_cpu_lib()
+        cores = os.cpu_count() or 1
+        workers = cores if kind == "reference" else 1
+        probe = cpu_sample(text, L, 1 << 17)
+        rate = probe.size / cpu_build(cpu_lib, kind, probe, workers)
+        sample = cpu_sample(text, L, int(min(1 << 20, max(1 << 17, rate * 15.0))))
+        dt = cpu_build(cpu_lib, kind, sample, workers)
+        cpu = {"value": sample.size / dt / 1e6, "unit": UNIT, "cores": workers, "kind": kind,
+               "sample": f"first {sample.size // (L + 1)} reads ({sample.size} suffixes) of the same text, 1 build, "
+                         f"{dt:.1f} s; reference build_parallel with executor{{workers={workers}}}" if kind == "reference"
+               else f"first {sample.size} suffixes, oracle port, 1 thread, {dt:.1f} s"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic",
+        "config": {"workload": DESCRIPTION[workload], "genome_bp": G, "read_len": L, "reads": k, "suffixes": n,
+                   "l2_policy": "inputs larger than L2 (text 139 MB, key/rank arrays >= 556 MB each vs 126 MB L2)"
+                   if n > 64_000_000 else "working set exceeds L2 only partly; no flush",
+                   "rounds": int(st.rounds), "init_symbols": int(st.init_symbols),
+                   "sort_passes": int(st.sort_passes), "alphabet": "dna-2bit" if st.alphabet == 0 else "bytes"},
+        "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
+        "roofline": roofline, "cpu_baseline": cpu, "overlap": overlap,
+        "checks": {"rank_is_inverse_of_sa": perm_ok, "host_run_equals_device_run": same},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -73,6 +73,17 @@ int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx);
 uint64_t reseq_cuda_ctx_launch_count(const reseq_cuda_ctx* ctx);
 /* Bytes currently held by the context's workspace arena. */
 size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
+/* Per-kernel device timing, measured with CUDA events recorded on the launching stream
+ * around every launch while enabled.  reseq_cuda_ctx_profile(ctx, 1) clears and starts,
+ * (ctx, 0) stops; reseq_cuda_ctx_profile_read synchronises the stream and writes up to
+ * `cap` per-kernel-name aggregates, returning how many names exist. */
+typedef struct reseq_kernel_profile {
+    char name[48];
+    uint64_t launches;
+    double total_ms;
+} reseq_kernel_profile;
+int reseq_cuda_ctx_profile(reseq_cuda_ctx* ctx, int enable);
+size_t reseq_cuda_ctx_profile_read(reseq_cuda_ctx* ctx, reseq_kernel_profile* out, size_t cap);
 const char* reseq_cuda_last_error(void);
 const char* reseq_cuda_version(void);
 

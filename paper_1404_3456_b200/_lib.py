@@ -44,6 +44,10 @@ class SaStats(C.Structure):
     ]
 
 
+class KernelProfile(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("launches", C.c_uint64), ("total_ms", C.c_double)]
+
+
 class Overlaps(C.Structure):
     _fields_ = [
         ("count", C.c_uint64),
@@ -70,6 +74,8 @@ SIGNATURES = {
     "reseq_cuda_ctx_synchronize": (C.c_int, [_vp]),
     "reseq_cuda_ctx_launch_count": (C.c_uint64, [_vp]),
     "reseq_cuda_ctx_workspace_bytes": (C.c_size_t, [_vp]),
+    "reseq_cuda_ctx_profile": (C.c_int, [_vp, C.c_int]),
+    "reseq_cuda_ctx_profile_read": (C.c_size_t, [_vp, C.POINTER(KernelProfile), C.c_size_t]),
     "reseq_cuda_last_error": (C.c_char_p, []),
     "reseq_cuda_version": (C.c_char_p, []),
     "reseq_cuda_exclusive_scan": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),

@@ -84,6 +84,16 @@ class Executor:
     def workspace_bytes(self) -> int:
         return int(self._lib.reseq_cuda_ctx_workspace_bytes(self._h))
 
+    def profile(self, enable: bool) -> None:
+        """Start (and clear) or stop per-kernel event timing."""
+        _lib.check(self._lib.reseq_cuda_ctx_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{kernel name: (launches, total device ms)} since profile(True)."""
+        buf = (_lib.KernelProfile * 64)()
+        m = int(self._lib.reseq_cuda_ctx_profile_read(self._h, buf, 64))
+        return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(min(m, 64))}
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._lib.reseq_cuda_ctx_destroy(self._h)

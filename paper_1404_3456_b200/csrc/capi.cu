@@ -45,6 +45,17 @@ int reseq_cuda_ctx::reserve(size_t bytes) {
     return RESEQ_OK;
 }
 
+cudaEvent_t reseq_cuda_ctx::take_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
 namespace {
 
 int check_ctx(reseq_cuda_ctx* ctx) {
@@ -69,8 +80,9 @@ int sort_u32(reseq_cuda_ctx* ctx, u32* ka, u32* kb, u32* va, u32* vb, size_t n, 
         size_t want = (n + block * 8 - 1) / (block * 8);
         const size_t cap = static_cast<size_t>(ctx->sm_count) * 4;
         const unsigned grid = static_cast<unsigned>(want < cap ? (want ? want : 1) : cap);
+        RSQ_LAUNCH_BEGIN(ctx, "hist_kernel");
         hist_kernel<u32><<<grid, block, sizeof(u32) * pt.count * kRadix, ctx->stream>>>(ka, n, pt, ws.hist);
-        ++ctx->launches;
+        RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
     }
     std::vector<u32> hist(static_cast<size_t>(pt.count) * kRadix);
@@ -151,6 +163,11 @@ void reseq_cuda_ctx_destroy(reseq_cuda_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (auto& r : ctx->profile) {
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -166,6 +183,45 @@ int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx) {
     RSQ_TRY(check_ctx(ctx));
     RSQ_CUDA(cudaStreamSynchronize(ctx->stream));
     return RESEQ_OK;
+}
+
+int reseq_cuda_ctx_profile(reseq_cuda_ctx* ctx, int enable) {
+    RSQ_TRY(check_ctx(ctx));
+    RSQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (enable) {
+        for (auto& r : ctx->profile) {
+            ctx->event_pool.push_back(r.e0);
+            ctx->event_pool.push_back(r.e1);
+        }
+        ctx->profile.clear();
+    }
+    ctx->profiling = enable != 0;
+    return RESEQ_OK;
+}
+
+size_t reseq_cuda_ctx_profile_read(reseq_cuda_ctx* ctx, reseq_kernel_profile* out, size_t cap) {
+    if (!ctx) return 0;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    std::vector<reseq_kernel_profile> agg;
+    for (const auto& r : ctx->profile) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        size_t t = 0;
+        while (t < agg.size() && std::strncmp(agg[t].name, r.name, sizeof(agg[t].name)) != 0) ++t;
+        if (t == agg.size()) {
+            reseq_kernel_profile p{};
+            std::strncpy(p.name, r.name, sizeof(p.name) - 1);
+            agg.push_back(p);
+        }
+        agg[t].launches += 1;
+        agg[t].total_ms += ms;
+    }
+    for (size_t t = 0; t < agg.size() && t < cap; ++t) out[t] = agg[t];
+    return agg.size();
 }
 
 uint64_t reseq_cuda_ctx_launch_count(const reseq_cuda_ctx* ctx) { return ctx ? ctx->launches : 0; }

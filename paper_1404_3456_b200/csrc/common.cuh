@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "reseq_cuda.h"
 
@@ -56,6 +57,17 @@ struct reseq_cuda_ctx {
     // pinned staging word for small D2H reads (round-termination flags etc.)
     uint64_t* pinned = nullptr;
 
+    // Optional per-launch timing with CUDA events on the launching stream (bench.py's
+    // live roofline).  Off by default; see reseq_cuda_ctx_profile().
+    struct ProfileRec {
+        const char* name;
+        cudaEvent_t e0, e1;
+    };
+    bool profiling = false;
+    std::vector<ProfileRec> profile;
+    std::vector<cudaEvent_t> event_pool;
+    cudaEvent_t take_event();
+
     int reserve(size_t bytes);
     void begin() { arena_used = 0; }
     template <typename T>
@@ -70,6 +82,20 @@ struct reseq_cuda_ctx {
 };
 
 namespace rsq {
+
+// Bracket one kernel launch: counts it, and records events around it when profiling.
+inline void launch_begin(reseq_cuda_ctx* ctx, const char* name) {
+    ++ctx->launches;
+    if (!ctx->profiling) return;
+    reseq_cuda_ctx::ProfileRec r{name, ctx->take_event(), ctx->take_event()};
+    cudaEventRecord(r.e0, ctx->stream);
+    ctx->profile.push_back(r);
+}
+inline void launch_end(reseq_cuda_ctx* ctx) {
+    if (ctx->profiling) cudaEventRecord(ctx->profile.back().e1, ctx->stream);
+}
+#define RSQ_LAUNCH_BEGIN(ctx, name) ::rsq::launch_begin((ctx), (name))
+#define RSQ_LAUNCH_END(ctx) ::rsq::launch_end((ctx))
 
 // ---- device helpers --------------------------------------------------------------
 

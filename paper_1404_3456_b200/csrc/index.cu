@@ -495,9 +495,10 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     if (!keys_a || !keys_b || !ids_a || !ids_b || !counters || !hist)
         return bail(fail(RESEQ_OUT_OF_MEMORY, "index workspace"));
     IX_CUDA(cudaMemsetAsync(counters, 0, 256, s));
+    RSQ_LAUNCH_BEGIN(ctx, "lens_kernel");
     lens_kernel<<<grid_1d(ctx, k, 256), 256, 0, s>>>(ix->d_starts, k, n, ix->d_lens, ix->d_rank, keys_a,
                                                      ids_a, counters);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     IX_CUDA(cudaGetLastError());
     if (k > 1) {
         SortWorkspace ws;
@@ -513,8 +514,9 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
         IX_CUDA(cudaMemcpyAsync(ix->d_start_rank, keys_a, sizeof(u32), cudaMemcpyDeviceToDevice, s));
         IX_CUDA(cudaMemcpyAsync(ix->d_start_frag, ids_a, sizeof(u32), cudaMemcpyDeviceToDevice, s));
     }
+    RSQ_LAUNCH_BEGIN(ctx, "invert_kernel");
     invert_kernel<<<grid_1d(ctx, k, 256), 256, 0, s>>>(ix->d_start_frag, k, ix->d_start_inv);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     IX_CUDA(cudaGetLastError());
     IX_CUDA(cudaMemcpyAsync(ctx->pinned, counters, sizeof(u32), cudaMemcpyDeviceToHost, s));
     IX_CUDA(cudaStreamSynchronize(s));
@@ -529,9 +531,10 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
         for (int which = 0; which < 2; ++which) {
             IX_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * dir_entries, s));
             const size_t count = which == 0 ? n : k;
+            RSQ_LAUNCH_BEGIN(ctx, "dir_hist_kernel");
             dir_hist_kernel<<<grid_1d(ctx, count, 256), 256, 0, s>>>(
                 ix->d_packed, ix->d_sent, n, which == 0 ? nullptr : ix->d_starts, count, D, hist);
-            ++ctx->launches;
+            RSQ_LAUNCH_END(ctx);
             IX_CUDA(cudaGetLastError());
             IX_TRY(scan_table(ctx, hist, which == 0 ? ix->d_dir : ix->d_sdir, dir_entries));
         }
@@ -598,8 +601,9 @@ int reseq_cuda_index_locate_batch(reseq_cuda_index* ix, const uint8_t* pats, con
     u32* d_hi = ctx->alloc<u32>(q);
     RSQ_CUDA(cudaMemcpyAsync(d_pats, pats, bytes, cudaMemcpyHostToDevice, s));
     RSQ_CUDA(cudaMemcpyAsync(d_off, pat_off, sizeof(u64) * (q + 1), cudaMemcpyHostToDevice, s));
+    RSQ_LAUNCH_BEGIN(ctx, "locate_patterns_kernel");
     locate_patterns_kernel<<<grid_1d(ctx, q, 256), 256, 0, s>>>(view_of(ix), d_pats, d_off, q, d_lo, d_hi);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(lo, d_lo, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaMemcpyAsync(hi, d_hi, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
@@ -631,8 +635,9 @@ int reseq_cuda_index_locate_residuals(reseq_cuda_index* ix, const uint32_t* frag
     u32* d_hi = ctx->alloc<u32>(q);
     RSQ_CUDA(cudaMemcpyAsync(d_frag, frag, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
     RSQ_CUDA(cudaMemcpyAsync(d_offs, off, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
+    RSQ_LAUNCH_BEGIN(ctx, "locate_residuals_kernel");
     locate_residuals_kernel<<<grid_1d(ctx, q, 256), 256, 0, s>>>(view_of(ix), d_frag, d_offs, q, d_lo, d_hi);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(lo, d_lo, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaMemcpyAsync(hi, d_hi, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
@@ -687,8 +692,9 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
     u64 raw = 0;
     if (Q > 0) {
         const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+        RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
         overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, d_qoff, q_first, q_count, d_contained);
-        ++ctx->launches;
+        RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
         RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total, sizeof(u64), cudaMemcpyDeviceToHost, s));
@@ -717,8 +723,9 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
             RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (k + 1), cudaMemcpyHostToDevice, s));
             RSQ_CUDA(cudaMemsetAsync(q_count + Q, 0, sizeof(u32), s));
             const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+            RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
             overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, d_qoff, q_first, q_count, d_contained);
-            ++ctx->launches;
+            RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
             RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
         }
@@ -736,8 +743,9 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
             return fail(RESEQ_OUT_OF_MEMORY, "overlap record workspace");
         {
             const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+            RSQ_LAUNCH_BEGIN(ctx, "overlap_fill_kernel");
             overlap_fill_kernel<<<grid, 256, 0, s>>>(iv, d_qoff, q_first, q_count, q_out, keys_a, w_a);
-            ++ctx->launches;
+            RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
         }
         // stable sort on (i, j): j digits then i digits
@@ -755,12 +763,14 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
         RSQ_TRY(onesweep_sort<u64>(ctx, keys_a, keys_b, w_a, w_b, raw, pt, ws, false, 0, &in_b));
         const u64* sk = in_b ? keys_b : keys_a;
         const u32* sw = in_b ? w_b : w_a;
+        RSQ_LAUNCH_BEGIN(ctx, "unique_flag_kernel");
         unique_flag_kernel<<<grid_1d(ctx, raw, 256), 256, 0, s>>>(sk, raw, flag);
-        ++ctx->launches;
+        RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
         RSQ_TRY(exclusive_scan_device(ctx, flag, dst, raw, d_total2));
+        RSQ_LAUNCH_BEGIN(ctx, "unique_compact_kernel");
         unique_compact_kernel<<<grid_1d(ctx, raw, 256), 256, 0, s>>>(sk, sw, flag, dst, raw, oi, oj, ow);
-        ++ctx->launches;
+        RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
         RSQ_CUDA(cudaEventRecord(ev1, s));
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total2, sizeof(u64), cudaMemcpyDeviceToHost, s));

@@ -63,9 +63,11 @@ static int launch_pass(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u
         configured = true;
     }
     const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
+    RSQ_LAUNCH_BEGIN(ctx, sizeof(KeyT) == 8 ? (HAS_VAL ? "onesweep_u64_pairs" : "onesweep_u64_keys")
+                                           : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys"));
     kern<<<static_cast<unsigned>(tiles), T::kBlock, Cfg::kSmem, ctx->stream>>>(
         kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
 }
@@ -83,13 +85,15 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
         const int block = 512;
         size_t want = (n + block * 8 - 1) / (block * 8);
         const unsigned grid = static_cast<unsigned>(want < static_cast<size_t>(ctx->sm_count) * 4 ? (want ? want : 1) : ctx->sm_count * 4);
+        RSQ_LAUNCH_BEGIN(ctx, "hist_kernel");
         hist_kernel<KeyT><<<grid, block, sizeof(u32) * pt.count * kRadix, ctx->stream>>>(
             keys_a, n, pt, ws.hist);
-        ++ctx->launches;
+        RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
     }
+    RSQ_LAUNCH_BEGIN(ctx, "digit_base_kernel");
     digit_base_kernel<<<pt.count, kRadix, 0, ctx->stream>>>(ws.hist, ws.base);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
 
     KeyT* kin = keys_a;

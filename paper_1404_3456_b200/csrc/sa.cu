@@ -342,11 +342,12 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
                              sizeof(u64) * ((n / 32 + 8) - (n / 64) * 2), s));
     RSQ_CUDA(cudaMemsetAsync(sent + n / 64, 0, sizeof(u64) * ((n / 64 + 8) - n / 64), s));
     const unsigned grid = grid_for(ctx, (n + 63) / 64, 256, 1, 8);
+    RSQ_LAUNCH_BEGIN(ctx, "pack_dna_kernel");
     if (reinterpret_cast<uintptr_t>(d_text) % 16 == 0)
         pack_dna_kernel<true><<<grid, 256, 0, s>>>(d_text, n, packed, sent, d_flag);
     else
         pack_dna_kernel<false><<<grid, 256, 0, s>>>(d_text, n, packed, sent, d_flag);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_flag, sizeof(u32), cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaStreamSynchronize(s));
@@ -410,11 +411,12 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     {
         const unsigned grid = grid_for(ctx, n, 256, 8, 8);
         const size_t smem = sizeof(u32) * pt0.count * kRadix;
+        RSQ_LAUNCH_BEGIN(ctx, dna ? "initkey_dna_kernel" : "initkey_bytes_kernel");
         if (dna)
             initkey_dna_kernel<<<grid, 256, smem, s>>>(packed, sent, n, k32_a, d_sa, pt0, ws.hist);
         else
             initkey_bytes_kernel<<<grid, 256, smem, s>>>(d_text, n, k32_a, d_sa, pt0, ws.hist);
-        ++ctx->launches;
+        RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
     }
     bool in_b = false;
@@ -428,9 +430,10 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         RSQ_CUDA(cudaMemsetAsync(desc, 0, sizeof(u64) * (rank_tiles + 4), s));
         RSQ_CUDA(cudaMemsetAsync(counters + 1, 0, 2 * sizeof(u32), s));
         using K = std::remove_pointer_t<decltype(keys)>;
+        RSQ_LAUNCH_BEGIN(ctx, "rerank_kernel");
         rerank_kernel<K><<<static_cast<unsigned>(rank_tiles), kRankBlock, 0, s>>>(
             keys, sa_cur, n, uniq_mask, uniq_full, rank, head_of, desc, counters + 1, counters + 2);
-        ++ctx->launches;
+        RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 2, sizeof(u32), cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaStreamSynchronize(s));
@@ -449,9 +452,10 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * pt.count * kRadix, s));
         {
             const unsigned grid = grid_for(ctx, n, 256, 8, 8);
+            RSQ_LAUNCH_BEGIN(ctx, "pair_key_kernel");
             pair_key_kernel<<<grid, 256, sizeof(u32) * pt.count * kRadix, s>>>(
                 sa_cur, head_of, rank, n, h, b, keys_a, pt, ws.hist);
-            ++ctx->launches;
+            RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
         }
         RSQ_TRY(onesweep_sort<u64>(ctx, keys_a, keys_b, sa_cur, sa_alt, n, pt, ws, true, 0, &in_b));

@@ -137,13 +137,14 @@ int exclusive_scan_device(reseq_cuda_ctx* ctx, const u32* d_in, u32* d_out, size
     RSQ_CUDA(cudaMemsetAsync(ticket, 0, 256, ctx->stream));
     const bool vec = (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(d_out) % 16 == 0);
+    RSQ_LAUNCH_BEGIN(ctx, "scan_kernel");
     if (vec)
         scan_kernel<true><<<static_cast<unsigned>(tiles), kScanBlock, 0, ctx->stream>>>(
             d_in, d_out, n, desc, ticket, d_total);
     else
         scan_kernel<false><<<static_cast<unsigned>(tiles), kScanBlock, 0, ctx->stream>>>(
             d_in, d_out, n, desc, ticket, d_total);
-    ++ctx->launches;
+    RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
 }
