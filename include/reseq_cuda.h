@@ -73,6 +73,11 @@ int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx);
 uint64_t reseq_cuda_ctx_launch_count(const reseq_cuda_ctx* ctx);
 /* Bytes currently held by the context's workspace arena. */
 size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
+/* Tuning / test knobs.  "sa_text_rounds": maximum number of shared-memory group-refinement
+ * rounds (keys fetched from the packed text) the DNA suffix-array path runs before handing
+ * over to prefix doubling; 0 forces pure prefix doubling.  Unknown names are
+ * RESEQ_INVALID_ARGUMENT.  Results never depend on these options. */
+int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long value);
 /* Per-kernel device timing, measured with CUDA events recorded on the launching stream
  * around every launch while enabled.  reseq_cuda_ctx_profile(ctx, 1) clears and starts,
  * (ctx, 0) stops; reseq_cuda_ctx_profile_read synchronises the stream and writes up to

@@ -74,6 +74,7 @@ SIGNATURES = {
     "reseq_cuda_ctx_synchronize": (C.c_int, [_vp]),
     "reseq_cuda_ctx_launch_count": (C.c_uint64, [_vp]),
     "reseq_cuda_ctx_workspace_bytes": (C.c_size_t, [_vp]),
+    "reseq_cuda_ctx_set_option": (C.c_int, [_vp, C.c_char_p, C.c_longlong]),
     "reseq_cuda_ctx_profile": (C.c_int, [_vp, C.c_int]),
     "reseq_cuda_ctx_profile_read": (C.c_size_t, [_vp, C.POINTER(KernelProfile), C.c_size_t]),
     "reseq_cuda_last_error": (C.c_char_p, []),

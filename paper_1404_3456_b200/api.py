@@ -84,6 +84,9 @@ class Executor:
     def workspace_bytes(self) -> int:
         return int(self._lib.reseq_cuda_ctx_workspace_bytes(self._h))
 
+    def set_option(self, name: str, value: int) -> None:
+        _lib.check(self._lib.reseq_cuda_ctx_set_option(self._h, name.encode(), int(value)))
+
     def profile(self, enable: bool) -> None:
         """Start (and clear) or stop per-kernel event timing."""
         _lib.check(self._lib.reseq_cuda_ctx_profile(self._h, 1 if enable else 0))

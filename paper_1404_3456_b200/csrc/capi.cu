@@ -185,6 +185,16 @@ int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx) {
     return RESEQ_OK;
 }
 
+int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long value) {
+    if (!ctx || !name) return fail(RESEQ_INVALID_ARGUMENT, "null argument");
+    if (std::strcmp(name, "sa_text_rounds") == 0) {
+        if (value < 0 || value > 1024) return fail(RESEQ_INVALID_ARGUMENT, "sa_text_rounds must be in 0..1024");
+        ctx->opt_text_rounds = static_cast<int>(value);
+        return RESEQ_OK;
+    }
+    return fail(RESEQ_INVALID_ARGUMENT, std::string("unknown option ") + name);
+}
+
 int reseq_cuda_ctx_profile(reseq_cuda_ctx* ctx, int enable) {
     RSQ_TRY(check_ctx(ctx));
     RSQ_CUDA(cudaStreamSynchronize(ctx->stream));

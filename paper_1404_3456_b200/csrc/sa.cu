@@ -191,7 +191,7 @@ constexpr int kRankBlock = 256;
 constexpr int kRankItems = 8;
 constexpr int kRankTile = kRankBlock * kRankItems;
 
-template <typename KeyT>
+template <typename KeyT, bool FLAGS_ONLY>
 __global__ void __launch_bounds__(kRankBlock)
 rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, u32 uniq_mask,
               u32 uniq_full, u32* __restrict__ rank, u32* __restrict__ head_of,
@@ -224,8 +224,10 @@ rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, 
 #pragma unroll
     for (int j = 0; j < kRankItems; ++j) {
         const u64 idx = base + j;
-        const bool head = idx < n && (idx == 0 || k[j] != prev ||
-                                      (static_cast<u32>(k[j]) & uniq_mask) != uniq_full);
+        // FLAGS_ONLY: the "keys" are 0/1 head flags expanded from a head bitmap
+        const bool head = idx < n && (FLAGS_ONLY ? (idx == 0 || k[j] != KeyT(0))
+                                                 : (idx == 0 || k[j] != prev ||
+                                                    (static_cast<u32>(k[j]) & uniq_mask) != uniq_full));
         prev = k[j];
         heads += head;
         if (head) run = static_cast<u32>(idx) + 1u;
@@ -293,6 +295,194 @@ rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, 
             rank[sa[idx]] = h;
         }
     }
+}
+
+// ---- group refinement from L2-resident text windows ----------------------------------
+//
+// After the initial sort the suffixes are grouped by their first `depth` symbols; groups
+// are contiguous in sa and delimited by a head bitmap (bit idx set <=> sa[idx] starts a
+// group).  On B200 the 2-bit packed text (n/4 bytes: 35 MB at 4.6 Mbp x 30) fits the 126 MB
+// L2 while the 4n-byte rank array does not, so the next 29 symbols of every still-tied
+// suffix are fetched straight from the packed text (an L2 hit) instead of through
+// rank[pos + h] (a DRAM sector per suffix, plus a DRAM read-modify-write per suffix to
+// scatter the new ranks).  Each CTA owns the groups that START inside its 2048-suffix tile,
+// stages them in shared memory, ranks every tied suffix inside its group by enumeration
+// (groups of a shotgun read set hold ~coverage suffixes), writes the refined order back in
+// place and ORs the new group heads into the next bitmap.  No global sort, no rank array.
+//
+// A group that does not fit the CTA's shared-memory window (more than kRefExt suffixes past
+// the tile) is left untouched and reported; the host then switches to the general
+// prefix-doubling rounds below, which have no size limit.
+
+constexpr int kRefBlock = 256;
+constexpr int kRefTile = 2048;
+constexpr int kRefExt = 2048;
+constexpr int kRefCap = kRefTile + kRefExt;
+constexpr int kRefWords = kRefCap / 32 + 2;
+constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * (kRefCap + 2 * kRefWords);
+constexpr int kTextK = 29;          // bases per refinement key: 58 bits + 6-bit terminator field
+constexpr int kTextFieldBits = 6;
+
+__device__ __forceinline__ u64 text_key(const u64* __restrict__ packed, const u64* __restrict__ sent,
+                                        u64 n, u64 pos) {
+    if (pos >= n) return 0;  // the text ends exactly here: end-of-text after 0 symbols
+    const u64 bases = base_window(packed, pos) >> (64 - 2 * kTextK);
+    const u32 sw = static_cast<u32>(sent_window(sent, pos) >> (64 - kTextK));
+    const u32 t = sw ? static_cast<u32>(__clz(sw)) - (32 - kTextK) : kTextK;
+    const u64 rem = n - pos;
+    const u32 lim = rem < kTextK ? static_cast<u32>(rem) : kTextK;
+    u32 len, field;
+    if (t < lim) { len = t; field = 2 * t + 1; }
+    else if (lim < kTextK) { len = lim; field = 2 * lim; }
+    else { len = kTextK; field = 2 * kTextK; }
+    const u64 kept = len == kTextK ? bases : bases & ~((1ull << (2 * (kTextK - len))) - 1ull);
+    return (kept << kTextFieldBits) | field;
+}
+
+// Head bitmap from the sorted initial keys: a suffix starts a group iff its key differs
+// from its left neighbour's or carries a terminator (unique by construction).
+__global__ void __launch_bounds__(256)
+headbits_kernel(const u32* __restrict__ keys, u64 n, u32 uniq_mask, u32 uniq_full,
+                u32* __restrict__ bits, u32* __restrict__ counters) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    const u64 rounds = (n + stride - 1) / stride;
+    u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    u32 nonheads = 0;
+    for (u64 r = 0; r < rounds; ++r, idx += stride) {
+        const bool in = idx < n;
+        bool head = false;
+        if (in) {
+            const u32 k = keys[idx];
+            head = idx == 0 || k != keys[idx - 1] || (k & uniq_mask) != uniq_full;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, head);
+        const unsigned act = __ballot_sync(0xffffffffu, in);
+        if (lane_id() == 0 && act) {
+            bits[idx >> 5] = b;
+            nonheads += __popc(act & ~b);
+        }
+    }
+    if (nonheads) atomicAdd(counters, nonheads);
+}
+
+__global__ void __launch_bounds__(kRefBlock)
+refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n,
+                   u32* __restrict__ sa, const u32* __restrict__ bits_old, u32* __restrict__ bits_new,
+                   u32 depth, u32* __restrict__ counters) {
+    extern __shared__ __align__(16) unsigned char ref_smem[];
+    u64* s_key = reinterpret_cast<u64*>(ref_smem);
+    u32* s_pos = reinterpret_cast<u32*>(s_key + kRefCap);
+    u32* s_bits = s_pos + kRefCap;
+    u32* s_new = s_bits + kRefWords;
+    __shared__ int s_first, s_end, s_last;
+    __shared__ u32 s_nonheads;
+
+    const int tid = threadIdx.x;
+    const u64 t0 = static_cast<u64>(blockIdx.x) * kRefTile;
+    const u64 w0 = t0 >> 5;
+    const int lim = static_cast<int>(n - t0 < static_cast<u64>(kRefTile) ? n - t0 : kRefTile);
+    const u64 total_words = (n + 31) >> 5;
+
+    if (tid == 0) { s_first = 0x7fffffff; s_end = 0x7fffffff; s_last = -1; s_nonheads = 0; }
+    for (int j = tid; j < kRefWords; j += kRefBlock) {
+        s_bits[j] = w0 + j < total_words ? bits_old[w0 + j] : 0u;
+        s_new[j] = 0;
+    }
+    __syncthreads();
+    // position n acts as a head so that the last group has an end
+    if (tid == 0 && n - t0 < static_cast<u64>(kRefWords) * 32) s_bits[(n - t0) >> 5] |= 1u << ((n - t0) & 31);
+    __syncthreads();
+
+    // first head inside the tile, last head inside the tile, first head at or after its end
+    for (int j = tid; j < kRefWords; j += kRefBlock) {
+        const u32 w = s_bits[j];
+        if (!w) continue;
+        const int base = j * 32;
+        u32 lo_mask = base + 32 <= lim ? 0xffffffffu : (base >= lim ? 0u : ((1u << (lim - base)) - 1u));
+        const u32 lo = w & lo_mask, hi = w & ~lo_mask;
+        if (lo) {
+            atomicMin(&s_first, base + __ffs(lo) - 1);
+            atomicMax(&s_last, base + 31 - __clz(lo));
+        }
+        if (hi) atomicMin(&s_end, base + __ffs(hi) - 1);
+    }
+    __syncthreads();
+    const int first = s_first;
+    if (first == 0x7fffffff) return;  // no group starts in this tile
+    int end = s_end;
+    if (end > kRefCap) {              // the tile's last group overruns the window
+        if (tid == 0) atomicOr(counters + 1, 1u);
+        end = s_last;                 // leave that group alone
+    }
+    const int m = end - first;
+    if (m <= 1) return;
+
+    auto bit = [&](int a) { return (s_bits[a >> 5] >> (a & 31)) & 1u; };
+
+    // anything still tied in [first, end)?
+    bool tied = false;
+    for (int i = tid; i < m; i += kRefBlock) tied |= !bit(first + i);
+    if (!__syncthreads_or(tied)) return;
+
+    // phase 1: stage positions; fetch the next 29 symbols of every tied suffix
+    for (int i = tid; i < m; i += kRefBlock) {
+        const int a = first + i;
+        const u32 pos = sa[t0 + a];
+        s_pos[i] = pos;
+        const bool single = bit(a) && bit(a + 1);
+        s_key[i] = single ? 0ull : text_key(packed, sent, n, static_cast<u64>(pos) + depth);
+    }
+    __syncthreads();
+
+    // phase 2: rank every tied suffix inside its group
+    u32 nonheads = 0;
+    constexpr u32 kFull = 2 * kTextK;
+    for (int i = tid; i < m; i += kRefBlock) {
+        const int a = first + i;
+        if (bit(a) && bit(a + 1)) continue;
+        // group start: last head at or before a; group end: first head after a
+        int gs = a, ge = a + 1;
+        {
+            int w = gs >> 5;
+            u32 word = s_bits[w] & (0xffffffffu >> (31 - (gs & 31)));
+            while (!word) word = s_bits[--w];
+            gs = w * 32 + 31 - __clz(word);
+            w = ge >> 5;
+            word = s_bits[w] & (0xffffffffu << (ge & 31));
+            while (!word) word = s_bits[++w];
+            ge = w * 32 + __ffs(word) - 1;
+        }
+        const u64 ki = s_key[i];
+        u32 less = 0, eq_before = 0;
+        for (int j = gs - first; j < ge - first; ++j) {
+            const u64 kj = s_key[j];
+            less += kj < ki;
+            eq_before += (kj == ki) & (j < i);
+        }
+        const int dst = gs + static_cast<int>(less + eq_before);
+        sa[t0 + dst] = s_pos[i];
+        const bool head = eq_before == 0 || (static_cast<u32>(ki) & ((1u << kTextFieldBits) - 1u)) != kFull;
+        if (head) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
+        else ++nonheads;
+    }
+    for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
+    if (lane_id() == 0 && nonheads) atomicAdd(&s_nonheads, nonheads);
+    __syncthreads();
+    for (int j = tid; j < kRefWords; j += kRefBlock)
+        if (s_new[j]) atomicOr(bits_new + w0 + j, s_new[j]);
+    if (tid == 0 && s_nonheads) atomicAdd(counters, s_nonheads);
+}
+
+__global__ void inverse_kernel(const u32* __restrict__ sa, u64 n, u32* __restrict__ rank) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        rank[sa[i]] = static_cast<u32>(i);
+}
+
+__global__ void expand_bits_kernel(const u32* __restrict__ bits, u64 n, u32* __restrict__ flags) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        flags[i] = (bits[i >> 5] >> (i & 31)) & 1u;
 }
 
 // ---- doubling round: build the pair keys --------------------------------------------
@@ -365,6 +555,7 @@ size_t sa_workspace_bytes(size_t n) {
     total += pad(sizeof(u32) * n);                   // rank when the caller wants none
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
+    total += 2 * pad(sizeof(u32) * (n / 32 + 8));    // head bitmaps
     total += sort_workspace_bytes(n);
     return total + 4096;
 }
@@ -390,9 +581,11 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     u32* rank = d_rank ? d_rank : ctx->alloc<u32>(n);
     const size_t rank_tiles = (n + kRankTile - 1) / kRankTile;
     u64* desc = ctx->alloc<u64>(rank_tiles + 4);
-    u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads
+    u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads, [4..5] refine
+    u32* bits_0 = ctx->alloc<u32>(n / 32 + 8);
+    u32* bits_1 = ctx->alloc<u32>(n / 32 + 8);
     SortWorkspace ws;
-    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters)
+    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !bits_0 || !bits_1)
         return fail(RESEQ_OUT_OF_MEMORY, "suffix-array workspace does not fit the reserved arena");
     RSQ_TRY(sort_workspace_carve(ctx, n, &ws));
 
@@ -426,12 +619,12 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     u32* sa_cur = in_b ? vals_b : d_sa;
     u32* sa_alt = in_b ? d_sa : vals_b;
 
-    auto rerank = [&](auto* keys, u32 uniq_mask, u32 uniq_full) -> int {
+    auto rerank = [&](auto* keys, auto flags_only, u32 uniq_mask, u32 uniq_full) -> int {
         RSQ_CUDA(cudaMemsetAsync(desc, 0, sizeof(u64) * (rank_tiles + 4), s));
         RSQ_CUDA(cudaMemsetAsync(counters + 1, 0, 2 * sizeof(u32), s));
         using K = std::remove_pointer_t<decltype(keys)>;
         RSQ_LAUNCH_BEGIN(ctx, "rerank_kernel");
-        rerank_kernel<K><<<static_cast<unsigned>(rank_tiles), kRankBlock, 0, s>>>(
+        rerank_kernel<K, decltype(flags_only)::value><<<static_cast<unsigned>(rank_tiles), kRankBlock, 0, s>>>(
             keys, sa_cur, n, uniq_mask, uniq_full, rank, head_of, desc, counters + 1, counters + 2);
         RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
@@ -442,13 +635,83 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
 
     const u32 field_mask = (1u << (dna ? kDnaFieldBits : kByteFieldBits)) - 1u;
     const u32 field_full = 2u * (dna ? kDnaK : kByteK);
-    RSQ_TRY(rerank(in_b ? k32_b : k32_a, field_mask, field_full));
-    u64 heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
+    u64 heads = 0;
+    u64 h = st.init_symbols;
+    bool ranked = false;  // rank / head_of valid for the current order
 
-    // -- prefix doubling ------------------------------------------------------------------
+    // -- DNA fast path: refine groups from L2-resident text windows -------------------------
+    if (dna && ctx->opt_text_rounds > 0) {
+        const size_t words = (n + 31) / 32 + 4;
+        u32* bits_a = bits_0;
+        u32* bits_b = bits_1;
+        static bool configured = false;
+        if (!configured) {
+            RSQ_CUDA(cudaFuncSetAttribute(refine_text_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kRefSmem)));
+            configured = true;
+        }
+        RSQ_CUDA(cudaMemsetAsync(bits_a, 0, sizeof(u32) * words, s));
+        RSQ_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * sizeof(u32), s));
+        RSQ_LAUNCH_BEGIN(ctx, "headbits_kernel");
+        headbits_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(in_b ? k32_b : k32_a, n, field_mask,
+                                                                     field_full, bits_a, counters + 4);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_CUDA(cudaGetLastError());
+        RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 4, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaStreamSynchronize(s));
+        u32 tied = reinterpret_cast<volatile u32*>(ctx->pinned)[0];
+        bool oversize = false;
+        const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
+        int text_rounds = 0;
+        while (tied > 0 && !oversize && text_rounds < ctx->opt_text_rounds) {
+            RSQ_CUDA(cudaMemcpyAsync(bits_b, bits_a, sizeof(u32) * words, cudaMemcpyDeviceToDevice, s));
+            RSQ_CUDA(cudaMemsetAsync(counters + 4, 0, 2 * sizeof(u32), s));
+            RSQ_LAUNCH_BEGIN(ctx, "refine_text_kernel");
+            refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sa_cur, bits_a, bits_b,
+                                                          static_cast<u32>(h), counters + 4);
+            RSQ_LAUNCH_END(ctx);
+            RSQ_CUDA(cudaGetLastError());
+            RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 4, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+            RSQ_CUDA(cudaStreamSynchronize(s));
+            st.refined_tile += tied;
+            tied = reinterpret_cast<volatile u32*>(ctx->pinned)[0];
+            oversize = reinterpret_cast<volatile u32*>(ctx->pinned)[1] != 0;
+            u32* t = bits_a; bits_a = bits_b; bits_b = t;
+            // a skipped (oversize) group is still tied at the old depth: prefix doubling must
+            // resume from the smallest depth any group is known to share
+            if (!oversize) h += kTextK;
+            ++text_rounds;
+            ++st.rounds;
+        }
+        if (tied == 0 && !oversize) {
+            // every group is a singleton: sa is final and rank is its inverse
+            RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
+            inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa_cur, n, rank);
+            RSQ_LAUNCH_END(ctx);
+            RSQ_CUDA(cudaGetLastError());
+            heads = n;
+            ranked = true;
+        } else {
+            // hand over to prefix doubling: group-head ranks from the bitmap
+            u32* flags = reinterpret_cast<u32*>(keys_b);  // the initial keys are no longer needed
+            RSQ_LAUNCH_BEGIN(ctx, "expand_bits_kernel");
+            expand_bits_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(bits_a, n, flags);
+            RSQ_LAUNCH_END(ctx);
+            RSQ_CUDA(cudaGetLastError());
+            RSQ_TRY(rerank(flags, std::true_type{}, 0u, 0u));
+            heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
+            ranked = true;
+        }
+    }
+    if (!ranked) {
+        RSQ_TRY(rerank(in_b ? k32_b : k32_a, std::false_type{}, field_mask, field_full));
+        heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
+    }
+
+    // -- prefix doubling (general engine: any alphabet, any group size, any LCP) --------------
     const int b = static_cast<int>(bit_width_u64(n));
     const PassTable pt = make_passes(0, 2 * b);
-    for (u64 h = st.init_symbols; heads < n && h < n; h <<= 1) {
+    for (; heads < n && h < n; h <<= 1) {
         RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * pt.count * kRadix, s));
         {
             const unsigned grid = grid_for(ctx, n, 256, 8, 8);
@@ -461,7 +724,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         RSQ_TRY(onesweep_sort<u64>(ctx, keys_a, keys_b, sa_cur, sa_alt, n, pt, ws, true, 0, &in_b));
         st.sort_passes += pt.count;
         if (in_b) { u32* t = sa_cur; sa_cur = sa_alt; sa_alt = t; }
-        RSQ_TRY(rerank(in_b ? keys_b : keys_a, 0u, 0u));
+        RSQ_TRY(rerank(in_b ? keys_b : keys_a, std::false_type{}, 0u, 0u));
         heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
         ++st.rounds;
         st.refined_global += n;

@@ -9,11 +9,29 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+_doubling = {}
+
+
+def doubling_executor(rq):
+    """A second context forced onto pure prefix doubling (sa_text_rounds = 0), so both
+    engines of the builder are checked on every small case."""
+    if "ex" not in _doubling:
+        e = rq.Executor(0)
+        e.set_option("sa_text_rounds", 0)
+        _doubling["ex"] = e
+    return _doubling["ex"]
+
+
 def check(rq, ex, oracle, text):
     got = rq.build_parallel(text, ex)
     wsa, wrank = oracle.build_sa(text)
     assert np.array_equal(got.sa, wsa), f"sa differs for text of length {len(text)}"
     assert np.array_equal(got.rank, wrank)
+    if len(text) <= 300_000:
+        alt = rq.build_parallel(text, doubling_executor(rq))
+        assert alt.stats.refined_tile == 0
+        assert np.array_equal(alt.sa, wsa), f"prefix-doubling sa differs for text of length {len(text)}"
+        assert np.array_equal(alt.rank, wrank)
     return got
 
 
@@ -110,7 +128,7 @@ def test_read_sets_against_the_oracle(rq, ex, oracle, G, L, k):
     text, _ = rq.synth_read_text(G, L, k)
     got = check(rq, ex, oracle, text)
     assert got.stats.alphabet == 0 and got.stats.init_symbols == 13
-    assert got.stats.rounds <= 4
+    assert got.stats.rounds <= 5 and got.stats.refined_global == 0  # 13 + 29 r >= L + 1
 
 
 def test_reference_bench_input_fingerprint(rq, ex, oracle):
@@ -129,7 +147,7 @@ def test_config1_full_size_fingerprint_and_proof(rq, ex, oracle):
     permutation + adjacent-order verifier is a proof of equality at this size."""
     text, _ = rq.synth_read_text(1_000_000, 100, 100_000)
     got = rq.build_parallel(text, ex)
-    assert got.stats.rounds == 3
+    assert got.stats.rounds == 4 and got.stats.refined_global == 0  # 13 + 29*3 = 100 < 101 <= 129
     assert oracle.checksum_u32(got.sa) == 11642757783061468293
     assert oracle.verify_sa(text, got.sa) == 0
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
@@ -139,7 +157,7 @@ def test_config2_full_size_proof(rq, ex, oracle):
     """BASELINE config 2 (4.6 Mbp, 150 bp, 30x; n = 138 920 000): size-independent proof."""
     text, _ = rq.synth_read_text(4_600_000, 150, 920_000)
     got = rq.build_parallel(text, ex)
-    assert got.stats.rounds == 4
+    assert got.stats.rounds == 5 and got.stats.refined_global == 0
     assert oracle.verify_sa(text, got.sa, threads=32) == 0
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
 
@@ -174,3 +192,23 @@ def test_device_resident_entry_point(rq, ex, oracle):
     h = C.c_uint64()
     rq._lib.check(lib.reseq_cuda_checksum_u32_device(ex.handle, C.c_void_p(d_sa.data_ptr()), text.size, C.byref(h)))
     assert h.value == oracle.checksum_u32(wsa)
+
+
+def test_oversize_groups_hand_over_to_prefix_doubling(rq, ex, oracle):
+    """Groups larger than the refine kernel's shared-memory window (identical / low-complexity
+    reads) must be finished by the global prefix-doubling rounds."""
+    text = (b"ACGTACGTAC" * 12 + b"\0") * 3000          # 3000 identical reads: groups of 3000
+    got = check(rq, ex, oracle, text)
+    assert got.stats.refined_global > 0
+    rng = np.random.default_rng(8)
+    unit = bytes(rng.choice([65, 67, 71, 84], 100).astype(np.uint8))
+    text = b"".join(unit[int(o):] + unit[:int(o)] + b"\0" for o in rng.integers(0, 100, 2500))  # rotations
+    got = check(rq, ex, oracle, text)
+
+
+def test_doubling_only_mode_on_config1(rq, oracle):
+    e = doubling_executor(rq)
+    text, _ = rq.synth_read_text(1_000_000, 100, 100_000)
+    got = rq.build_parallel(text, e)
+    assert got.stats.rounds == 3 and got.stats.refined_tile == 0   # h = 13, 26, 52 -> 104 >= 101
+    assert oracle.checksum_u32(got.sa) == 11642757783061468293
