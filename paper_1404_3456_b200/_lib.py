@@ -48,6 +48,14 @@ class KernelProfile(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("launches", C.c_uint64), ("total_ms", C.c_double)]
 
 
+class PrefixRelations(C.Structure):
+    _fields_ = [("q", C.c_size_t),
+                ("prefixes_off", C.POINTER(C.c_uint64)), ("extensions_off", C.POINTER(C.c_uint64)),
+                ("exact_off", C.POINTER(C.c_uint64)),
+                ("prefixes", C.POINTER(C.c_uint32)), ("extensions", C.POINTER(C.c_uint32)),
+                ("exact", C.POINTER(C.c_uint32))]
+
+
 class Overlaps(C.Structure):
     _fields_ = [
         ("count", C.c_uint64),
@@ -96,6 +104,8 @@ SIGNATURES = {
     "reseq_cuda_index_device_ptrs": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
     "reseq_cuda_index_locate_batch": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "reseq_cuda_index_locate_residuals": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
+    "reseq_cuda_index_prefix_related_batch": (C.c_int, [_vp, _vp, _vp, C.c_size_t, C.POINTER(PrefixRelations)]),
+    "reseq_cuda_prefix_relations_free": (None, [C.POINTER(PrefixRelations)]),
     "reseq_cuda_index_overlaps": (C.c_int, [_vp, C.c_uint32, C.POINTER(Overlaps)]),
     "reseq_cuda_overlaps_free": (None, [C.POINTER(Overlaps)]),
     "reseq_greedy_superstring": (C.c_int, [_vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(Overlaps), C.c_uint32,

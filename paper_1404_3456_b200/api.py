@@ -363,6 +363,36 @@ class FragmentIndex:
             raise OffsetOutOfRangeError(str(e)) from None
         return lo, hi
 
+    def prefix_related_batch(self, frag, off):
+        """fragment_index::prefix_related (fragment_index.hpp:72-109) for a batch of residuals.
+        Returns a list of (prefixes_of, extensions_of, exact_matches) id arrays, each
+        ascending by id."""
+        f, o = _u32(frag, "frag"), _u32(off, "off")
+        if f.size != o.size:
+            raise ValueError("frag and off must have the same length")
+        rel = _lib.PrefixRelations()
+        try:
+            try:
+                _lib.check(self._lib.reseq_cuda_index_prefix_related_batch(self._h, _ptr(f), _ptr(o), f.size,
+                                                                           C.byref(rel)))
+            except ValueError as e:
+                raise OffsetOutOfRangeError(str(e)) from None
+            out = []
+            for i in range(f.size):
+                row = []
+                for offp, idp in ((rel.prefixes_off, rel.prefixes), (rel.extensions_off, rel.extensions),
+                                  (rel.exact_off, rel.exact)):
+                    a, b = int(offp[i]), int(offp[i + 1])
+                    row.append(np.array([idp[t] for t in range(a, b)], np.uint32))
+                out.append(tuple(row))
+            return out
+        finally:
+            self._lib.reseq_cuda_prefix_relations_free(C.byref(rel))
+
+    def prefix_related(self, frag: int, off: int = 0):
+        """prefix_related(residual{frag, off}) (fragment_index.hpp:78-80)."""
+        return self.prefix_related_batch([frag], [off])[0]
+
     def overlaps(self, min_overlap: int = 1) -> OverlapList:
         ov = _lib.Overlaps()
         _lib.check(self._lib.reseq_cuda_index_overlaps(self._h, int(min_overlap), C.byref(ov)))

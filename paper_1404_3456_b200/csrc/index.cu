@@ -50,6 +50,8 @@ struct reseq_cuda_index {
     u32* d_dir = nullptr;         // 4^D + 1 entries (+1 leading scan slot)
     u32* d_sdir = nullptr;
     u32 max_len = 0;
+    u32* d_lengths = nullptr;     // distinct fragment lengths, ascending (lengths_, fragment_index.hpp:52-55)
+    u32 n_lengths = 0;
     std::vector<void*> owned;
 };
 
@@ -371,6 +373,62 @@ overlap_fill_kernel(IndexView iv, const u64* __restrict__ qoff, const u32* __res
     }
 }
 
+// prefix_related (fragment_index.hpp:82-109) for residual patterns, one thread per query.
+// The sweep over the distinct fragment lengths below |pattern| collects the fragments that
+// are proper prefixes of the pattern (start suffixes of exactly that length inside the
+// interval of the pattern's prefix); the final interval yields extensions and exact
+// matches.  MODE 0 counts, MODE 1 fills the CSR arrays at the scanned offsets.  For a
+// residual every prefix of the pattern occurs in the text, so the early return of
+// fragment_index.hpp:91 cannot trigger.  Lists leave in start-rank order; the host sorts
+// each by id (fragment_index.hpp:105-107).
+template <int MODE>
+__global__ void __launch_bounds__(256)
+prefix_related_kernel(IndexView iv, const u32* __restrict__ lengths, u32 n_lengths,
+                      const u32* __restrict__ frag, const u32* __restrict__ off, u64 q,
+                      u32* __restrict__ cnt_pre, u32* __restrict__ cnt_ext, u32* __restrict__ cnt_exact,
+                      const u32* __restrict__ off_pre, const u32* __restrict__ off_ext,
+                      const u32* __restrict__ off_exact, u32* __restrict__ out_pre,
+                      u32* __restrict__ out_ext, u32* __restrict__ out_exact) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < q; i += stride) {
+        const u32 f = frag[i], o = off[i];
+        const u64 ppos = static_cast<u64>(iv.starts[f]) + o;
+        const u32 m = iv.lens[f] - o;
+        u32 np = 0, ne = 0, nx = 0;
+        u32 wp = MODE ? off_pre[i] : 0, we = MODE ? off_ext[i] : 0, wx = MODE ? off_exact[i] : 0;
+        u32 lo, hi, sf, sl;
+        for (u32 t = 0; t < n_lengths; ++t) {
+            const u32 len = lengths[t];
+            if (len >= m) break;
+            locate_residual(iv, ppos, len, &lo, &hi, &sf, &sl);
+            for (u32 u = sf; u < sl; ++u) {
+                const u32 id = iv.start_frag[u];
+                if (iv.lens[id] == len) {
+                    if (MODE) out_pre[wp++] = id;
+                    ++np;
+                }
+            }
+        }
+        locate_residual(iv, ppos, m, &lo, &hi, &sf, &sl);
+        for (u32 u = sf; u < sl; ++u) {
+            const u32 id = iv.start_frag[u];
+            const u32 len = iv.lens[id];
+            if (len > m) {
+                if (MODE) out_ext[we++] = id;
+                ++ne;
+            } else if (len == m) {
+                if (MODE) out_exact[wx++] = id;
+                ++nx;
+            }
+        }
+        if (!MODE) {
+            cnt_pre[i] = np;
+            cnt_ext[i] = ne;
+            cnt_exact[i] = nx;
+        }
+    }
+}
+
 __global__ void unique_flag_kernel(const u64* __restrict__ keys, u64 m, u32* __restrict__ flag) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 t = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; t < m; t += stride)
@@ -521,6 +579,15 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     IX_CUDA(cudaMemcpyAsync(ctx->pinned, counters, sizeof(u32), cudaMemcpyDeviceToHost, s));
     IX_CUDA(cudaStreamSynchronize(s));
     ix->max_len = *reinterpret_cast<volatile u32*>(ctx->pinned);
+    {
+        std::vector<u32> lens(k);
+        IX_CUDA(cudaMemcpy(lens.data(), ix->d_lens, sizeof(u32) * k, cudaMemcpyDeviceToHost));
+        std::sort(lens.begin(), lens.end());
+        lens.erase(std::unique(lens.begin(), lens.end()), lens.end());
+        ix->n_lengths = static_cast<u32>(lens.size());
+        IX_TRY(dev_alloc(ix, &ix->d_lengths, lens.size()));
+        IX_CUDA(cudaMemcpy(ix->d_lengths, lens.data(), sizeof(u32) * lens.size(), cudaMemcpyHostToDevice));
+    }
 
     if (ix->dna) {
         bool is_dna = true;
@@ -642,6 +709,103 @@ int reseq_cuda_index_locate_residuals(reseq_cuda_index* ix, const uint32_t* frag
     RSQ_CUDA(cudaMemcpyAsync(lo, d_lo, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaMemcpyAsync(hi, d_hi, sizeof(u32) * q, cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaStreamSynchronize(s));
+    return RESEQ_OK;
+}
+
+void reseq_cuda_prefix_relations_free(reseq_prefix_relations* r) {
+    if (!r) return;
+    std::free(r->prefixes_off);
+    std::free(r->extensions_off);
+    std::free(r->exact_off);
+    std::free(r->prefixes);
+    std::free(r->extensions);
+    std::free(r->exact);
+    std::memset(r, 0, sizeof(*r));
+}
+
+int reseq_cuda_index_prefix_related_batch(reseq_cuda_index* ix, const uint32_t* frag, const uint32_t* off,
+                                          size_t q, reseq_prefix_relations* out) {
+    if (!ix || !out) return fail(RESEQ_INVALID_ARGUMENT, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    out->q = q;
+    reseq_cuda_ctx* ctx = ix->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    uint64_t** offs[3] = {&out->prefixes_off, &out->extensions_off, &out->exact_off};
+    uint32_t** ids[3] = {&out->prefixes, &out->extensions, &out->exact};
+    for (auto* o : offs) {
+        *o = static_cast<uint64_t*>(std::calloc(q + 1, sizeof(uint64_t)));
+        if (!*o) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
+    }
+    if (q == 0) return RESEQ_OK;
+    if (!frag || !off) return fail(RESEQ_INVALID_ARGUMENT, "null buffer");
+    std::vector<u32> lens(ix->k);
+    RSQ_CUDA(cudaMemcpyAsync(lens.data(), ix->d_lens, sizeof(u32) * ix->k, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < q; ++i)
+        if (frag[i] >= ix->k || off[i] >= lens[frag[i]])
+            return fail(RESEQ_INVALID_ARGUMENT, "residual offset out of range (sequence.hpp:128-129)");
+    auto pad = reseq_cuda_ctx::padded;
+    RSQ_TRY(ctx->reserve(8 * pad(sizeof(u32) * (q + 1)) + 3 * scan_workspace_bytes(q + 1) + 8192));
+    ctx->begin();
+    u32* d_frag = ctx->alloc<u32>(q);
+    u32* d_offs = ctx->alloc<u32>(q);
+    u32* cnt[3];
+    u32* pos[3];
+    u64* d_tot[3];
+    for (int t = 0; t < 3; ++t) {
+        cnt[t] = ctx->alloc<u32>(q + 1);
+        pos[t] = ctx->alloc<u32>(q + 1);
+        d_tot[t] = ctx->alloc<u64>(1);
+        RSQ_CUDA(cudaMemsetAsync(cnt[t] + q, 0, sizeof(u32), s));
+    }
+    RSQ_CUDA(cudaMemcpyAsync(d_frag, frag, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
+    RSQ_CUDA(cudaMemcpyAsync(d_offs, off, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
+    const IndexView iv = view_of(ix);
+    RSQ_LAUNCH_BEGIN(ctx, "prefix_related_kernel");
+    prefix_related_kernel<0><<<grid_1d(ctx, q, 256), 256, 0, s>>>(iv, ix->d_lengths, ix->n_lengths, d_frag, d_offs, q,
+                                                                  cnt[0], cnt[1], cnt[2], nullptr, nullptr, nullptr,
+                                                                  nullptr, nullptr, nullptr);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    u64 totals[3];
+    std::vector<u32> host_pos(q + 1);
+    for (int t = 0; t < 3; ++t) {
+        RSQ_TRY(exclusive_scan_device(ctx, cnt[t], pos[t], q + 1, d_tot[t]));
+        RSQ_CUDA(cudaMemcpyAsync(host_pos.data(), pos[t], sizeof(u32) * (q + 1), cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_tot[t], sizeof(u64), cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaStreamSynchronize(s));
+        totals[t] = *reinterpret_cast<volatile u64*>(ctx->pinned);
+        if (totals[t] > 0xFFFFFFF0ull) return fail(RESEQ_INVALID_ARGUMENT, "more than 2^32 relation entries");
+        for (size_t i = 0; i <= q; ++i) (*offs[t])[i] = host_pos[i];
+    }
+    // the id arrays follow the query arrays in the arena; grow it if the totals need more
+    const size_t used = ctx->arena_used;
+    const size_t more = pad(sizeof(u32) * (totals[0] + 1)) + pad(sizeof(u32) * (totals[1] + 1)) +
+                        pad(sizeof(u32) * (totals[2] + 1)) + 1024;
+    if (ctx->arena_cap < used + more) {
+        // re-run from scratch in a larger arena
+        RSQ_TRY(ctx->reserve(used + more + 8192));
+        reseq_cuda_prefix_relations_free(out);
+        return reseq_cuda_index_prefix_related_batch(ix, frag, off, q, out);
+    }
+    u32* d_out[3];
+    for (int t = 0; t < 3; ++t) d_out[t] = ctx->alloc<u32>(totals[t] + 1);
+    RSQ_LAUNCH_BEGIN(ctx, "prefix_related_kernel");
+    prefix_related_kernel<1><<<grid_1d(ctx, q, 256), 256, 0, s>>>(iv, ix->d_lengths, ix->n_lengths, d_frag, d_offs, q,
+                                                                  nullptr, nullptr, nullptr, pos[0], pos[1], pos[2],
+                                                                  d_out[0], d_out[1], d_out[2]);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    for (int t = 0; t < 3; ++t) {
+        *ids[t] = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (totals[t] + 1)));
+        if (!*ids[t]) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
+        RSQ_CUDA(cudaMemcpyAsync(*ids[t], d_out[t], sizeof(u32) * totals[t], cudaMemcpyDeviceToHost, s));
+    }
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    for (int t = 0; t < 3; ++t)  // each list ascending by id (fragment_index.hpp:105-107)
+        for (size_t i = 0; i < q; ++i)
+            std::sort(*ids[t] + (*offs[t])[i], *ids[t] + (*offs[t])[i + 1]);
     return RESEQ_OK;
 }
 

@@ -316,10 +316,11 @@ rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, 
 
 constexpr int kRefBlock = 256;
 constexpr int kRefTile = 2048;
-constexpr int kRefExt = 2048;
+constexpr int kRefExt = 1024;
 constexpr int kRefCap = kRefTile + kRefExt;
 constexpr int kRefWords = kRefCap / 32 + 2;
-constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * (kRefCap + 2 * kRefWords);
+constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 2 * sizeof(unsigned short) * kRefCap +
+                            sizeof(u32) * (3 * kRefWords + 16);
 constexpr int kTextK = 29;          // bases per refinement key: 58 bits + 6-bit terminator field
 constexpr int kTextFieldBits = 6;
 
@@ -365,25 +366,35 @@ headbits_kernel(const u32* __restrict__ keys, u64 n, u32 uniq_mask, u32 uniq_ful
     if (nonheads) atomicAdd(counters, nonheads);
 }
 
+// One CTA refines every group that starts in its tile to completion: the key of a tied
+// suffix depends only on (position, depth), never on another group, so all rounds run
+// back to back in shared memory and the tile goes back to HBM once.  Every round first
+// compacts the still-tied suffixes into a dense list (order preserving, so a group stays
+// contiguous) -- late rounds, where few suffixes are tied, then cost in proportion to what
+// is left instead of dragging 32-wide warps through one or two live lanes.
 __global__ void __launch_bounds__(kRefBlock)
 refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n,
                    u32* __restrict__ sa, const u32* __restrict__ bits_old, u32* __restrict__ bits_new,
-                   u32 depth, u32* __restrict__ counters) {
+                   u32 depth, int max_rounds, u32* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char ref_smem[];
-    u64* s_key = reinterpret_cast<u64*>(ref_smem);
-    u32* s_pos = reinterpret_cast<u32*>(s_key + kRefCap);
-    u32* s_bits = s_pos + kRefCap;
-    u32* s_new = s_bits + kRefWords;
+    u64* s_key = reinterpret_cast<u64*>(ref_smem);               // [cap] keys of the round ...
+    u32* s_pos2 = reinterpret_cast<u32*>(ref_smem);              // ... then the permuted positions
+    u32* s_pos = reinterpret_cast<u32*>(s_key + kRefCap);        // [cap] suffix positions, sa order
+    unsigned short* s_list = reinterpret_cast<unsigned short*>(s_pos + kRefCap);  // [cap] tied slots
+    unsigned short* s_dst = s_list + kRefCap;                    // [cap] new slot | head << 15
+    u32* s_bits = reinterpret_cast<u32*>(s_dst + kRefCap);       // [words] head bits of the window
+    u32* s_new = s_bits + kRefWords;                             // [words] heads created this round
+    u32* s_cnt = s_new + kRefWords;                              // [words + 1] tied-count scan
     __shared__ int s_first, s_end, s_last;
-    __shared__ u32 s_nonheads;
 
     const int tid = threadIdx.x;
+    const unsigned lane = lane_id();
     const u64 t0 = static_cast<u64>(blockIdx.x) * kRefTile;
     const u64 w0 = t0 >> 5;
     const int lim = static_cast<int>(n - t0 < static_cast<u64>(kRefTile) ? n - t0 : kRefTile);
     const u64 total_words = (n + 31) >> 5;
 
-    if (tid == 0) { s_first = 0x7fffffff; s_end = 0x7fffffff; s_last = -1; s_nonheads = 0; }
+    if (tid == 0) { s_first = 0x7fffffff; s_end = 0x7fffffff; s_last = -1; }
     for (int j = tid; j < kRefWords; j += kRefBlock) {
         s_bits[j] = w0 + j < total_words ? bits_old[w0 + j] : 0u;
         s_new[j] = 0;
@@ -393,12 +404,12 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
     if (tid == 0 && n - t0 < static_cast<u64>(kRefWords) * 32) s_bits[(n - t0) >> 5] |= 1u << ((n - t0) & 31);
     __syncthreads();
 
-    // first head inside the tile, last head inside the tile, first head at or after its end
+    // first / last head inside the tile, first head at or after its end
     for (int j = tid; j < kRefWords; j += kRefBlock) {
         const u32 w = s_bits[j];
         if (!w) continue;
         const int base = j * 32;
-        u32 lo_mask = base + 32 <= lim ? 0xffffffffu : (base >= lim ? 0u : ((1u << (lim - base)) - 1u));
+        const u32 lo_mask = base + 32 <= lim ? 0xffffffffu : (base >= lim ? 0u : ((1u << (lim - base)) - 1u));
         const u32 lo = w & lo_mask, hi = w & ~lo_mask;
         if (lo) {
             atomicMin(&s_first, base + __ffs(lo) - 1);
@@ -414,63 +425,138 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
         if (tid == 0) atomicOr(counters + 1, 1u);
         end = s_last;                 // leave that group alone
     }
-    const int m = end - first;
-    if (m <= 1) return;
+    if (end - first <= 1) return;
 
-    auto bit = [&](int a) { return (s_bits[a >> 5] >> (a & 31)) & 1u; };
+    // Tied slots of window word j, restricted to [first, end): slot a is tied unless it is a
+    // head whose successor is a head too.
+    auto tied_word = [&](int j) -> u32 {
+        const int base = j * 32;
+        if (base + 32 <= first || base >= end) return 0u;
+        const u32 w = s_bits[j];
+        const u32 next = (w >> 1) | (s_bits[j + 1] << 31);
+        u32 t = ~(w & next);
+        if (base < first) t &= 0xffffffffu << (first - base);
+        if (base + 32 > end) t &= (1u << (end - base)) - 1u;
+        return t;
+    };
 
-    // anything still tied in [first, end)?
-    bool tied = false;
-    for (int i = tid; i < m; i += kRefBlock) tied |= !bit(first + i);
-    if (!__syncthreads_or(tied)) return;
-
-    // phase 1: stage positions; fetch the next 29 symbols of every tied suffix
-    for (int i = tid; i < m; i += kRefBlock) {
-        const int a = first + i;
-        const u32 pos = sa[t0 + a];
-        s_pos[i] = pos;
-        const bool single = bit(a) && bit(a + 1);
-        s_key[i] = single ? 0ull : text_key(packed, sent, n, static_cast<u64>(pos) + depth);
-    }
-    __syncthreads();
-
-    // phase 2: rank every tied suffix inside its group
-    u32 nonheads = 0;
+    constexpr u32 kFieldMask = (1u << kTextFieldBits) - 1u;
     constexpr u32 kFull = 2 * kTextK;
-    for (int i = tid; i < m; i += kRefBlock) {
-        const int a = first + i;
-        if (bit(a) && bit(a + 1)) continue;
-        // group start: last head at or before a; group end: first head after a
-        int gs = a, ge = a + 1;
-        {
-            int w = gs >> 5;
-            u32 word = s_bits[w] & (0xffffffffu >> (31 - (gs & 31)));
-            while (!word) word = s_bits[--w];
-            gs = w * 32 + 31 - __clz(word);
-            w = ge >> 5;
-            word = s_bits[w] & (0xffffffffu << (ge & 31));
-            while (!word) word = s_bits[++w];
-            ge = w * 32 + __ffs(word) - 1;
+    bool loaded = false;
+    int rounds = 0;
+    for (; rounds < max_rounds; ++rounds, depth += kTextK) {
+        // -- compact the tied slots, in order ------------------------------------------------
+        u32 tw = 0, c = 0;
+        if (tid < kRefWords) {
+            tw = tied_word(tid);
+            c = __popc(tw);
         }
-        const u64 ki = s_key[i];
-        u32 less = 0, eq_before = 0;
-        for (int j = gs - first; j < ge - first; ++j) {
-            const u64 kj = s_key[j];
-            less += kj < ki;
-            eq_before += (kj == ki) & (j < i);
+        u32 inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (static_cast<int>(lane) >= o) inc += t;
         }
-        const int dst = gs + static_cast<int>(less + eq_before);
-        sa[t0 + dst] = s_pos[i];
-        const bool head = eq_before == 0 || (static_cast<u32>(ki) & ((1u << kTextFieldBits) - 1u)) != kFull;
-        if (head) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
-        else ++nonheads;
+        if (lane == 31) s_cnt[kRefWords + 1 + (tid >> 5)] = inc;   // warp totals
+        __syncthreads();
+        u32 before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kRefBlock / 32; ++w) {
+            const u32 v = s_cnt[kRefWords + 1 + w];
+            if (w < (tid >> 5)) before += v;
+            total += v;
+        }
+        if (total == 0) break;
+        if (tid < kRefWords) {
+            u32 at = before + inc - c;
+            while (tw) {
+                const int b = __ffs(tw) - 1;
+                tw &= tw - 1;
+                s_list[at++] = static_cast<unsigned short>(tid * 32 + b);
+            }
+        }
+        if (!loaded) {
+            for (int a = first + tid; a < end; a += kRefBlock) s_pos[a] = sa[t0 + a];
+            loaded = true;
+        }
+        __syncthreads();
+        const int cnt = static_cast<int>(total);
+
+        // -- fetch the next 29 symbols of every tied suffix (an L2 hit) -----------------------
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            s_key[a] = text_key(packed, sent, n, static_cast<u64>(s_pos[a]) + depth);
+        }
+        __syncthreads();
+
+        // -- rank inside the group: #smaller keys + #equal keys before it ----------------------
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            int gs, ge;
+            {
+                int w = a >> 5;
+                u32 word = s_bits[w] & (0xffffffffu >> (31 - (a & 31)));
+                while (!word) word = s_bits[--w];
+                gs = w * 32 + 31 - __clz(word);
+                w = (a + 1) >> 5;
+                word = s_bits[w] & (0xffffffffu << ((a + 1) & 31));
+                while (!word) word = s_bits[++w];
+                ge = w * 32 + __ffs(word) - 1;
+            }
+            const u64 ki = s_key[a];
+            u32 le = 0, lt = 0;
+            for (int j = gs; j < a; ++j) {      // earlier members: ties count
+                const u64 kj = s_key[j];
+                le += kj <= ki;
+                lt += kj < ki;
+            }
+            u32 after = 0;
+            for (int j = a + 1; j < ge; ++j) after += s_key[j] < ki;   // later members: only smaller keys
+            const int dst = gs + static_cast<int>(le + after);
+            const bool head = le == lt || (static_cast<u32>(ki) & kFieldMask) != kFull;
+            s_dst[u] = static_cast<unsigned short>(dst | (head ? 0x8000 : 0));
+        }
+        __syncthreads();
+
+        // -- permute (the key buffer is dead: it receives the new order) -----------------------
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            const int d = s_dst[u];
+            const int dst = d & 0x7fff;
+            s_pos2[dst] = s_pos[a];
+            if (d & 0x8000) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
+        }
+        __syncthreads();
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            s_pos[a] = s_pos2[a];
+        }
+        if (tid < kRefWords) {
+            s_bits[tid] |= s_new[tid];
+            s_new[tid] = 0;
+        }
+        __syncthreads();
+    }
+    if (!loaded) return;  // nothing was tied in this tile
+
+    // write the tile back once; publish the new heads; count what is still tied
+    u32 nonheads = 0;
+    for (int a = first + tid; a < end; a += kRefBlock) {
+        sa[t0 + a] = s_pos[a];
+        nonheads += !((s_bits[a >> 5] >> (a & 31)) & 1u);
+    }
+    const int n_local = n - t0 < static_cast<u64>(kRefWords) * 32 ? static_cast<int>(n - t0) : kRefWords * 32;
+    for (int j = tid; j < kRefWords; j += kRefBlock) {
+        const int base = j * 32;
+        if (base >= n_local || base >= end) break;
+        u32 w = s_bits[j];
+        if (base + 32 > n_local) w &= (1u << (n_local - base)) - 1u;  // drop the artificial end bit
+        if (base + 32 > end) w &= (1u << (end - base)) - 1u;
+        if (w) atomicOr(bits_new + w0 + j, w);
     }
     for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
-    if (lane_id() == 0 && nonheads) atomicAdd(&s_nonheads, nonheads);
-    __syncthreads();
-    for (int j = tid; j < kRefWords; j += kRefBlock)
-        if (s_new[j]) atomicOr(bits_new + w0 + j, s_new[j]);
-    if (tid == 0 && s_nonheads) atomicAdd(counters, s_nonheads);
+    if (lane == 0 && nonheads) atomicAdd(counters, nonheads);
+    if (tid == 0) atomicMax(counters + 2, static_cast<u32>(rounds));
 }
 
 __global__ void inverse_kernel(const u32* __restrict__ sa, u64 n, u32* __restrict__ rank) {
@@ -661,27 +747,27 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         RSQ_CUDA(cudaStreamSynchronize(s));
         u32 tied = reinterpret_cast<volatile u32*>(ctx->pinned)[0];
         bool oversize = false;
-        const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
-        int text_rounds = 0;
-        while (tied > 0 && !oversize && text_rounds < ctx->opt_text_rounds) {
+        if (tied > 0) {
+            const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
             RSQ_CUDA(cudaMemcpyAsync(bits_b, bits_a, sizeof(u32) * words, cudaMemcpyDeviceToDevice, s));
-            RSQ_CUDA(cudaMemsetAsync(counters + 4, 0, 2 * sizeof(u32), s));
+            RSQ_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * sizeof(u32), s));
             RSQ_LAUNCH_BEGIN(ctx, "refine_text_kernel");
             refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sa_cur, bits_a, bits_b,
-                                                          static_cast<u32>(h), counters + 4);
+                                                                   static_cast<u32>(h), ctx->opt_text_rounds,
+                                                                   counters + 4);
             RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
-            RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 4, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+            RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 4, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
             RSQ_CUDA(cudaStreamSynchronize(s));
             st.refined_tile += tied;
             tied = reinterpret_cast<volatile u32*>(ctx->pinned)[0];
             oversize = reinterpret_cast<volatile u32*>(ctx->pinned)[1] != 0;
+            st.rounds += reinterpret_cast<volatile u32*>(ctx->pinned)[2];
             u32* t = bits_a; bits_a = bits_b; bits_b = t;
-            // a skipped (oversize) group is still tied at the old depth: prefix doubling must
-            // resume from the smallest depth any group is known to share
-            if (!oversize) h += kTextK;
-            ++text_rounds;
-            ++st.rounds;
+            // Groups still tied after the kernel share at least h + 29 * max_rounds symbols --
+            // unless one was skipped as oversize: that one is still tied at depth h, and prefix
+            // doubling must resume from the smallest depth any group is known to share.
+            if (!oversize) h += static_cast<u64>(kTextK) * ctx->opt_text_rounds;
         }
         if (tied == 0 && !oversize) {
             // every group is a singleton: sa is final and rank is its inverse
