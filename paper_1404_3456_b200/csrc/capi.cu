@@ -1,5 +1,6 @@
 // C-ABI entry points (include/reseq_cuda.h) for the context, the L0 primitives and the
 // suffix-array builder.  Index entry points live in index.cu; host-only ones in host/.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -153,6 +154,8 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     RSQ_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     RSQ_CUDA(cudaMallocHost(&ctx->pinned, 4096));
+    if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
+    if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);
     *out = ctx;
     return RESEQ_OK;
 }
@@ -190,6 +193,11 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     if (std::strcmp(name, "sa_text_rounds") == 0) {
         if (value < 0 || value > 1024) return fail(RESEQ_INVALID_ARGUMENT, "sa_text_rounds must be in 0..1024");
         ctx->opt_text_rounds = static_cast<int>(value);
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "sort_cfg") == 0) {
+        if (value < 0 || value > 7) return fail(RESEQ_INVALID_ARGUMENT, "sort_cfg must be in 0..7");
+        ctx->opt_sort_cfg = static_cast<int>(value);
         return RESEQ_OK;
     }
     return fail(RESEQ_INVALID_ARGUMENT, std::string("unknown option ") + name);

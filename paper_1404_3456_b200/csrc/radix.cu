@@ -23,12 +23,12 @@ digit_base_kernel(const u32* __restrict__ g_hist, u32* __restrict__ g_base) {
 }
 
 template <> struct SortTuning<u32, false> { static constexpr int kBlock = 256, kItems = 16; };
-template <> struct SortTuning<u32, true>  { static constexpr int kBlock = 256, kItems = 16; };
+template <> struct SortTuning<u32, true>  { static constexpr int kBlock = 384, kItems = 12; };
 template <> struct SortTuning<u64, true>  { static constexpr int kBlock = 256, kItems = 16; };
 template <> struct SortTuning<u64, false> { static constexpr int kBlock = 256, kItems = 16; };
 
 // The smallest tile among the tunings bounds the look-back array.
-static constexpr size_t kMinTile = 256 * 16;
+static constexpr size_t kMinTile = 256 * 8;
 
 size_t sort_workspace_bytes(size_t n) {
     const size_t tiles = (n + kMinTile - 1) / kMinTile + 1;
@@ -49,13 +49,11 @@ int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws) {
     return RESEQ_OK;
 }
 
-template <typename KeyT, bool HAS_VAL>
-static int launch_pass(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u32* vin, u32* vout,
-                       size_t n, int shift, u32 mask, const u32* base, u64* lookback,
-                       u32* ticket) {
-    using T = SortTuning<KeyT, HAS_VAL>;
-    using Cfg = OnesweepCfg<KeyT, HAS_VAL, T::kBlock, T::kItems>;
-    auto kern = onesweep_kernel<KeyT, HAS_VAL, T::kBlock, T::kItems>;
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS>
+static int launch_pass_cfg(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u32* vin, u32* vout,
+                           size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket) {
+    using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
+    auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS>;
     static bool configured = false;
     if (!configured) {
         RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -65,11 +63,31 @@ static int launch_pass(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u
     const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
     RSQ_LAUNCH_BEGIN(ctx, sizeof(KeyT) == 8 ? (HAS_VAL ? "onesweep_u64_pairs" : "onesweep_u64_keys")
                                            : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys"));
-    kern<<<static_cast<unsigned>(tiles), T::kBlock, Cfg::kSmem, ctx->stream>>>(
+    kern<<<static_cast<unsigned>(tiles), BLOCK, Cfg::kSmem, ctx->stream>>>(
         kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
+}
+
+template <typename KeyT, bool HAS_VAL>
+static int launch_pass(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u32* vin, u32* vout,
+                       size_t n, int shift, u32 mask, const u32* base, u64* lookback,
+                       u32* ticket) {
+    // "sort_cfg" picks a tile shape (tuning knob; every shape gives the same result)
+    switch (ctx->opt_sort_cfg) {
+        case 1: return launch_pass_cfg<KeyT, HAS_VAL, 512, 8>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 2: return launch_pass_cfg<KeyT, HAS_VAL, 512, 12>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 3: return launch_pass_cfg<KeyT, HAS_VAL, 256, 12>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 4: return launch_pass_cfg<KeyT, HAS_VAL, 256, 8>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 5: return launch_pass_cfg<KeyT, HAS_VAL, 384, 12>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 6: return launch_pass_cfg<KeyT, HAS_VAL, 1024, 4>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 7: return launch_pass_cfg<KeyT, HAS_VAL, 512, 16>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        default: break;
+    }
+    using T = SortTuning<KeyT, HAS_VAL>;
+    return launch_pass_cfg<KeyT, HAS_VAL, T::kBlock, T::kItems>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+                                                               lookback, ticket);
 }
 
 template <typename KeyT>
@@ -116,6 +134,32 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
         flipped = !flipped;
     }
     *in_b = flipped;
+    return RESEQ_OK;
+}
+
+int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out, u32* idx_out, size_t n,
+                            int shift, int bits, const SortWorkspace& ws) {
+    if (n == 0) return RESEQ_OK;
+    using T = SortTuning<u32, true>;
+    using Cfg = OnesweepCfg<u32, true, T::kBlock, T::kItems>;
+    auto kern = onesweep_kernel<u32, true, T::kBlock, T::kItems, true>;
+    static bool configured = false;
+    if (!configured) {
+        RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem)));
+        configured = true;
+    }
+    RSQ_CUDA(cudaMemsetAsync(ws.tickets, 0, sizeof(u32) * kMaxPasses, ctx->stream));
+    RSQ_CUDA(cudaMemsetAsync(ws.lookback, 0, ws.lookback_bytes, ctx->stream));
+    RSQ_LAUNCH_BEGIN(ctx, "digit_base_kernel");
+    digit_base_kernel<<<1, kRadix, 0, ctx->stream>>>(ws.hist, ws.base);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
+    RSQ_LAUNCH_BEGIN(ctx, "onesweep_u32_partition");
+    kern<<<static_cast<unsigned>(tiles), T::kBlock, Cfg::kSmem, ctx->stream>>>(
+        keys, keys_out, nullptr, idx_out, n, shift, (1u << bits) - 1u, ws.base, ws.lookback, ws.tickets);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
 }
 

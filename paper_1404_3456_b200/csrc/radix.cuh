@@ -94,6 +94,22 @@ hist_kernel(const KeyT* __restrict__ keys, u64 n, PassTable pt, u32* __restrict_
 
 // ---- one digit pass -----------------------------------------------------------------
 
+// Lanes of the warp holding the same digit.  Built from one ballot per digit bit: on
+// sm_100a eight VOTE + LOP3 pairs sustain a far higher rate than one MATCH.ANY, whose issue
+// rate (not latency) capped the ranking loop at ~1.5 TB/s of key traffic (ncu: the BREV
+// consuming the match result held 38 % of the stall samples, profiles/r1_onesweep_match.txt).
+__device__ __forceinline__ unsigned warp_match_digit(u32 d, u32 mask) {
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+        if ((mask >> b) & 1u) {  // warp-uniform: the last pass of a key may be narrower
+            const unsigned vote = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? vote : ~vote;
+        }
+    }
+    return peers;
+}
+
 template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS>
 struct OnesweepCfg {
     static constexpr int kWarps = BLOCK / 32;
@@ -102,7 +118,8 @@ struct OnesweepCfg {
                                     sizeof(u32) * (kWarps * kRadix + 2 * kRadix + 32 + 4);
 };
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS>
+// IOTA_VAL: the payload of element i is i itself (no payload array is read).
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, bool IOTA_VAL = false>
 __global__ void __launch_bounds__(BLOCK)
 onesweep_kernel(const KeyT* __restrict__ keys_in, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,
@@ -142,35 +159,45 @@ onesweep_kernel(const KeyT* __restrict__ keys_in, KeyT* __restrict__ keys_out,
         for (int j = 0; j < ITEMS; ++j) key[j] = keys_in[tile_base + wbase + j * 32];
         if (HAS_VAL) {
 #pragma unroll
-            for (int j = 0; j < ITEMS; ++j) val[j] = vals_in[tile_base + wbase + j * 32];
+            for (int j = 0; j < ITEMS; ++j)
+                val[j] = IOTA_VAL ? static_cast<u32>(tile_base + wbase + j * 32) : vals_in[tile_base + wbase + j * 32];
         }
     } else {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
             const u32 li = wbase + j * 32;
             key[j] = li < valid ? keys_in[tile_base + li] : ~KeyT(0);  // pads rank last
-            if (HAS_VAL) val[j] = li < valid ? vals_in[tile_base + li] : 0u;
+            if (HAS_VAL) val[j] = li < valid ? (IOTA_VAL ? static_cast<u32>(tile_base + li) : vals_in[tile_base + li]) : 0u;
         }
     }
 
-    // -- rank inside the warp: match.any groups equal digits; the lowest lane of each
-    //    group bumps the warp's private counter once for the whole group ---------------
+    // -- rank inside the warp: match.any groups equal digits; the lowest lane of each group
+    //    bumps the warp's private counter once for the whole group.  The bump is a shared
+    //    atomicAdd whose old value is consumed only after a batch of them has been issued:
+    //    successive steps of one warp are then independent instructions in flight instead of
+    //    a load -> add -> store chain that exposes the shared-memory latency 16 times. --------
     u32* wh = s_whist + warp * kRadix;
     unsigned short rnk[ITEMS];
     const unsigned lt = lanemask_lt();
+    constexpr int kBatch = ITEMS % 8 == 0 ? 8 : (ITEMS % 4 == 0 ? 4 : 1);
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const u32 d = key_digit(key[j], shift, mask);
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const int leader = __ffs(peers) - 1;
-        u32 base = 0;
-        if (static_cast<int>(lane) == leader) {
-            base = wh[d];
-            wh[d] = base + __popc(peers);
+    for (int j0 = 0; j0 < ITEMS; j0 += kBatch) {
+        unsigned peers[kBatch];
+        u32 base[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b)
+            peers[b] = warp_match_digit(key_digit(key[j0 + b], shift, mask), mask);
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            base[b] = 0;
+            if ((peers[b] & lt) == 0)  // lowest lane of its group
+                base[b] = atomicAdd(wh + key_digit(key[j0 + b], shift, mask), __popc(peers[b]));
         }
-        base = __shfl_sync(0xffffffffu, base, leader);
-        rnk[j] = static_cast<unsigned short>(base + __popc(peers & lt));
-        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const u32 first = __shfl_sync(0xffffffffu, base[b], __ffs(peers[b]) - 1);
+            rnk[j0 + b] = static_cast<unsigned short>(first + __popc(peers[b] & lt));
+        }
     }
     __syncthreads();
 
@@ -266,5 +293,10 @@ template <typename KeyT>
 int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, u32* vals_b,
                   size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
                   u32 skip_mask, bool* in_b);
+
+// One stable partition pass of (keys[i], i) on key bits [shift, shift + bits): keys_out /
+// idx_out receive the pairs grouped by digit.  ws.hist[0..255] must hold the digit counts.
+int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out, u32* idx_out, size_t n,
+                            int shift, int bits, const SortWorkspace& ws);
 
 }  // namespace rsq

@@ -319,14 +319,20 @@ constexpr int kRefTile = 2048;
 constexpr int kRefExt = 1024;
 constexpr int kRefCap = kRefTile + kRefExt;
 constexpr int kRefWords = kRefCap / 32 + 2;
-constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 2 * sizeof(unsigned short) * kRefCap +
+constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 3 * sizeof(unsigned short) * kRefCap +
                             sizeof(u32) * (3 * kRefWords + 16);
-constexpr int kTextK = 29;          // bases per refinement key: 58 bits + 6-bit terminator field
-constexpr int kTextFieldBits = 6;
+constexpr int kTextK = 23;          // bases per refinement round
+constexpr int kTextFieldBits = 6;   // terminator field: 2*len + kind, 2*kTextK = "no terminator"
+constexpr int kTextSlotBits = 12;   // window slot of the suffix: makes every key of a round unique
+static_assert(kRefCap <= (1 << kTextSlotBits), "window slots must fit the key's slot field");
+static_assert(2 * kTextK + kTextFieldBits + kTextSlotBits == 64, "refinement key layout");
 
+// Key of one round for the suffix in window slot `slot`: the next 23 symbols from `pos`
+// (zero padded at a terminator) | terminator field | slot.  Keys of equal content keep
+// their slot order, so the order of the full 64-bit keys IS the stable refined order.
 __device__ __forceinline__ u64 text_key(const u64* __restrict__ packed, const u64* __restrict__ sent,
-                                        u64 n, u64 pos) {
-    if (pos >= n) return 0;  // the text ends exactly here: end-of-text after 0 symbols
+                                        u64 n, u64 pos, u32 slot) {
+    if (pos >= n) return slot;  // the text ends exactly here: end-of-text after 0 symbols
     const u64 bases = base_window(packed, pos) >> (64 - 2 * kTextK);
     const u32 sw = static_cast<u32>(sent_window(sent, pos) >> (64 - kTextK));
     const u32 t = sw ? static_cast<u32>(__clz(sw)) - (32 - kTextK) : kTextK;
@@ -337,7 +343,7 @@ __device__ __forceinline__ u64 text_key(const u64* __restrict__ packed, const u6
     else if (lim < kTextK) { len = lim; field = 2 * lim; }
     else { len = kTextK; field = 2 * kTextK; }
     const u64 kept = len == kTextK ? bases : bases & ~((1ull << (2 * (kTextK - len))) - 1ull);
-    return (kept << kTextFieldBits) | field;
+    return (((kept << kTextFieldBits) | field) << kTextSlotBits) | slot;
 }
 
 // Head bitmap from the sorted initial keys: a suffix starts a group iff its key differs
@@ -381,8 +387,9 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
     u32* s_pos2 = reinterpret_cast<u32*>(ref_smem);              // ... then the permuted positions
     u32* s_pos = reinterpret_cast<u32*>(s_key + kRefCap);        // [cap] suffix positions, sa order
     unsigned short* s_list = reinterpret_cast<unsigned short*>(s_pos + kRefCap);  // [cap] tied slots
-    unsigned short* s_dst = s_list + kRefCap;                    // [cap] new slot | head << 15
-    u32* s_bits = reinterpret_cast<u32*>(s_dst + kRefCap);       // [words] head bits of the window
+    unsigned short* s_dst = s_list + kRefCap;                    // [cap] new slot of list entry u
+    unsigned short* s_src = s_dst + kRefCap;                     // [cap] old slot of new slot d
+    u32* s_bits = reinterpret_cast<u32*>(s_src + kRefCap);       // [words] head bits of the window
     u32* s_new = s_bits + kRefWords;                             // [words] heads created this round
     u32* s_cnt = s_new + kRefWords;                              // [words + 1] tied-count scan
     __shared__ int s_first, s_end, s_last;
@@ -482,14 +489,14 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
         __syncthreads();
         const int cnt = static_cast<int>(total);
 
-        // -- fetch the next 29 symbols of every tied suffix (an L2 hit) -----------------------
+        // -- fetch the next 23 symbols of every tied suffix (an L2 hit) -----------------------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
-            s_key[a] = text_key(packed, sent, n, static_cast<u64>(s_pos[a]) + depth);
+            s_key[a] = text_key(packed, sent, n, static_cast<u64>(s_pos[a]) + depth, static_cast<u32>(a));
         }
         __syncthreads();
 
-        // -- rank inside the group: #smaller keys + #equal keys before it ----------------------
+        // -- rank inside the group: the keys are unique, so rank = #smaller keys -----------------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
             int gs, ge;
@@ -504,28 +511,36 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
                 ge = w * 32 + __ffs(word) - 1;
             }
             const u64 ki = s_key[a];
-            u32 le = 0, lt = 0;
-            for (int j = gs; j < a; ++j) {      // earlier members: ties count
-                const u64 kj = s_key[j];
-                le += kj <= ki;
-                lt += kj < ki;
+            u32 r0 = 0, r1 = 0;
+            int j = gs;
+            for (; j + 1 < ge; j += 2) {   // every member of the group runs the same trip count
+                r0 += s_key[j] < ki;
+                r1 += s_key[j + 1] < ki;
             }
-            u32 after = 0;
-            for (int j = a + 1; j < ge; ++j) after += s_key[j] < ki;   // later members: only smaller keys
-            const int dst = gs + static_cast<int>(le + after);
-            const bool head = le == lt || (static_cast<u32>(ki) & kFieldMask) != kFull;
-            s_dst[u] = static_cast<unsigned short>(dst | (head ? 0x8000 : 0));
+            if (j < ge) r0 += s_key[j] < ki;
+            const int dst = gs + static_cast<int>(r0 + r1);
+            s_dst[u] = static_cast<unsigned short>(dst);
+            s_src[dst] = static_cast<unsigned short>(a);
+        }
+        __syncthreads();
+
+        // -- new heads: a suffix starts a group iff its content differs from its predecessor's
+        //    in the new order, or it carries a terminator (unique by construction) ---------------
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            const int dst = s_dst[u];
+            const u64 ki = s_key[a] >> kTextSlotBits;
+            bool head = (static_cast<u32>(ki) & kFieldMask) != kFull;
+            // slot dst-1 belongs to the same group unless dst opens it (then its bit is already set
+            // and s_src[dst - 1] is not this round's)
+            if (!head && !((s_bits[dst >> 5] >> (dst & 31)) & 1u))
+                head = (s_key[s_src[dst - 1]] >> kTextSlotBits) != ki;
+            if (head) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
         }
         __syncthreads();
 
         // -- permute (the key buffer is dead: it receives the new order) -----------------------
-        for (int u = tid; u < cnt; u += kRefBlock) {
-            const int a = s_list[u];
-            const int d = s_dst[u];
-            const int dst = d & 0x7fff;
-            s_pos2[dst] = s_pos[a];
-            if (d & 0x8000) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
-        }
+        for (int u = tid; u < cnt; u += kRefBlock) s_pos2[s_dst[u]] = s_pos[s_list[u]];
         __syncthreads();
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
@@ -557,6 +572,25 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
     for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
     if (lane == 0 && nonheads) atomicAdd(counters, nonheads);
     if (tid == 0) atomicMax(counters + 2, static_cast<u32>(rounds));
+}
+
+// rank = inverse permutation of sa.  A direct scatter rank[sa[i]] = i is n random 4-byte
+// writes, each a DRAM read-modify-write of a whole sector (measured 5.9 ms at n = 139 M).
+// Instead the (sa[i], i) pairs are first partitioned by the top 8 bits of sa[i] -- one
+// streaming onesweep pass -- so that consecutive pairs target one n/256-entry window of
+// rank; the scatter then hits in L2 and DRAM only sees whole lines written once.
+__global__ void perm_digit_hist_kernel(u64 n, int shift, u32* __restrict__ hist) {
+    // sa is a permutation of [0, n): the number of values with top digit d is known
+    const u64 d = threadIdx.x;
+    const u64 lo = d << shift, hi = (d + 1) << shift;
+    hist[d] = static_cast<u32>((hi < n ? hi : n) - (lo < n ? lo : n));
+}
+
+__global__ void scatter_pairs_kernel(const u32* __restrict__ pos, const u32* __restrict__ idx, u64 n,
+                                     u32* __restrict__ rank) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        rank[pos[i]] = idx[i];
 }
 
 __global__ void inverse_kernel(const u32* __restrict__ sa, u64 n, u32* __restrict__ rank) {
@@ -771,9 +805,23 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         }
         if (tied == 0 && !oversize) {
             // every group is a singleton: sa is final and rank is its inverse
-            RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
-            inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa_cur, n, rank);
-            RSQ_LAUNCH_END(ctx);
+            const int nb = static_cast<int>(bit_width_u64(n - 1));
+            if (n >= (size_t{1} << 22)) {
+                const int shift = nb - 8;
+                u32* part_pos = reinterpret_cast<u32*>(keys_a);
+                u32* part_idx = part_pos + n;
+                RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
+                perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, ws.hist);
+                RSQ_LAUNCH_END(ctx);
+                RSQ_TRY(onesweep_partition_iota(ctx, sa_cur, part_pos, part_idx, n, shift, 8, ws));
+                RSQ_LAUNCH_BEGIN(ctx, "scatter_pairs_kernel");
+                scatter_pairs_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(part_pos, part_idx, n, rank);
+                RSQ_LAUNCH_END(ctx);
+            } else {  // the whole rank array is L2-resident: scatter directly
+                RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
+                inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa_cur, n, rank);
+                RSQ_LAUNCH_END(ctx);
+            }
             RSQ_CUDA(cudaGetLastError());
             heads = n;
             ranked = true;
