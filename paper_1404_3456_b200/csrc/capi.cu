@@ -155,6 +155,7 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     ctx->stream = ctx->own_stream;
     RSQ_CUDA(cudaMallocHost(&ctx->pinned, 4096));
     if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
+    if (const char* e = std::getenv("RESEQ_INVERSE_LO_BITS")) ctx->opt_inverse_lo_bits = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);
     *out = ctx;
     return RESEQ_OK;

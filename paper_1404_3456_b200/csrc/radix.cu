@@ -137,12 +137,13 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
     return RESEQ_OK;
 }
 
-int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out, u32* idx_out, size_t n,
-                            int shift, int bits, const SortWorkspace& ws) {
+template <bool IOTA>
+static int partition_impl(reseq_cuda_ctx* ctx, const u32* keys, const u32* vals, u32* keys_out, u32* vals_out,
+                          size_t n, int shift, int bits, const SortWorkspace& ws) {
     if (n == 0) return RESEQ_OK;
     using T = SortTuning<u32, true>;
     using Cfg = OnesweepCfg<u32, true, T::kBlock, T::kItems>;
-    auto kern = onesweep_kernel<u32, true, T::kBlock, T::kItems, true>;
+    auto kern = onesweep_kernel<u32, true, T::kBlock, T::kItems, IOTA>;
     static bool configured = false;
     if (!configured) {
         RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem)));
@@ -157,10 +158,20 @@ int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out,
     const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
     RSQ_LAUNCH_BEGIN(ctx, "onesweep_u32_partition");
     kern<<<static_cast<unsigned>(tiles), T::kBlock, Cfg::kSmem, ctx->stream>>>(
-        keys, keys_out, nullptr, idx_out, n, shift, (1u << bits) - 1u, ws.base, ws.lookback, ws.tickets);
+        keys, keys_out, vals, vals_out, n, shift, (1u << bits) - 1u, ws.base, ws.lookback, ws.tickets);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
+}
+
+int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out, u32* idx_out, size_t n,
+                            int shift, int bits, const SortWorkspace& ws) {
+    return partition_impl<true>(ctx, keys, nullptr, keys_out, idx_out, n, shift, bits, ws);
+}
+
+int onesweep_partition_pairs(reseq_cuda_ctx* ctx, const u32* keys, const u32* vals, u32* keys_out, u32* vals_out,
+                             size_t n, int shift, int bits, const SortWorkspace& ws) {
+    return partition_impl<false>(ctx, keys, vals, keys_out, vals_out, n, shift, bits, ws);
 }
 
 template int onesweep_sort<u32>(reseq_cuda_ctx*, u32*, u32*, u32*, u32*, size_t, const PassTable&,

@@ -298,5 +298,8 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
 // idx_out receive the pairs grouped by digit.  ws.hist[0..255] must hold the digit counts.
 int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out, u32* idx_out, size_t n,
                             int shift, int bits, const SortWorkspace& ws);
+// The same for explicit (key, payload) pairs.
+int onesweep_partition_pairs(reseq_cuda_ctx* ctx, const u32* keys, const u32* vals, u32* keys_out, u32* vals_out,
+                             size_t n, int shift, int bits, const SortWorkspace& ws);
 
 }  // namespace rsq

@@ -579,11 +579,16 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
 // Instead the (sa[i], i) pairs are first partitioned by the top 8 bits of sa[i] -- one
 // streaming onesweep pass -- so that consecutive pairs target one n/256-entry window of
 // rank; the scatter then hits in L2 and DRAM only sees whole lines written once.
-__global__ void perm_digit_hist_kernel(u64 n, int shift, u32* __restrict__ hist) {
-    // sa is a permutation of [0, n): the number of values with top digit d is known
+__global__ void perm_digit_hist_kernel(u64 n, int shift, int bits, u32* __restrict__ hist) {
+    // sa is a permutation of [0, n): the number of values v with digit (v >> shift) & mask == d
+    // is known in closed form -- count of such v below n
     const u64 d = threadIdx.x;
-    const u64 lo = d << shift, hi = (d + 1) << shift;
-    hist[d] = static_cast<u32>((hi < n ? hi : n) - (lo < n ? lo : n));
+    const u64 period = 1ull << (shift + bits), span = 1ull << shift;
+    if (d >= (1ull << bits)) { hist[d] = 0; return; }
+    const u64 full = n / period, rem = n % period;
+    const u64 lo = d * span;
+    const u64 part = rem > lo ? (rem - lo < span ? rem - lo : span) : 0;
+    hist[d] = static_cast<u32>(full * span + part);
 }
 
 __global__ void scatter_pairs_kernel(const u32* __restrict__ pos, const u32* __restrict__ idx, u64 n,
@@ -591,6 +596,23 @@ __global__ void scatter_pairs_kernel(const u32* __restrict__ pos, const u32* __r
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
         rank[pos[i]] = idx[i];
+}
+
+// After the partition passes every aligned window of 2^win_bits rank entries has all of its
+// (pos, idx) pairs in the same index range of the pair arrays (sa is a permutation, so the
+// buckets are exactly window-sized).  One CTA per window: scatter in shared memory, store the
+// window with full-width coalesced writes -- 139 M single-sector L2 write transactions become
+// 4.3 M full lines.
+__global__ void __launch_bounds__(512)
+window_scatter_kernel(const u32* __restrict__ pos, const u32* __restrict__ idx, u64 n, int win_bits,
+                      u32* __restrict__ rank) {
+    extern __shared__ u32 s_win[];
+    const u64 base = static_cast<u64>(blockIdx.x) << win_bits;
+    const u32 size = static_cast<u32>(n - base < (1ull << win_bits) ? n - base : (1ull << win_bits));
+    const u32 mask = (1u << win_bits) - 1u;
+    for (u32 t = threadIdx.x; t < size; t += blockDim.x) s_win[pos[base + t] & mask] = idx[base + t];
+    __syncthreads();
+    for (u32 t = threadIdx.x; t < size; t += blockDim.x) rank[base + t] = s_win[t];
 }
 
 __global__ void inverse_kernel(const u32* __restrict__ sa, u64 n, u32* __restrict__ rank) {
@@ -807,16 +829,51 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
             // every group is a singleton: sa is final and rank is its inverse
             const int nb = static_cast<int>(bit_width_u64(n - 1));
             if (n >= (size_t{1} << 22)) {
+                // two stable passes (low 5 bits of the top 13, then the top 8): windows of
+                // n / 8192 rank entries
                 const int shift = nb - 8;
+                int lo_bits = shift - 13;  // aim at windows of 8192 entries (32 KB of shared memory)
+                if (lo_bits < 0) lo_bits = 0;
+                if (lo_bits > 8) lo_bits = 8;
+                if (ctx->opt_inverse_lo_bits >= 0) lo_bits = ctx->opt_inverse_lo_bits;
+                const int win_bits = shift - lo_bits;
                 u32* part_pos = reinterpret_cast<u32*>(keys_a);
                 u32* part_idx = part_pos + n;
-                RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
-                perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, ws.hist);
-                RSQ_LAUNCH_END(ctx);
-                RSQ_TRY(onesweep_partition_iota(ctx, sa_cur, part_pos, part_idx, n, shift, 8, ws));
-                RSQ_LAUNCH_BEGIN(ctx, "scatter_pairs_kernel");
-                scatter_pairs_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(part_pos, part_idx, n, rank);
-                RSQ_LAUNCH_END(ctx);
+                const u32* src_pos = sa_cur;
+                if (lo_bits > 0) {
+                    u32* p0 = reinterpret_cast<u32*>(keys_b);
+                    u32* i0 = p0 + n;
+                    RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
+                    perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift - lo_bits, lo_bits, ws.hist);
+                    RSQ_LAUNCH_END(ctx);
+                    RSQ_TRY(onesweep_partition_iota(ctx, sa_cur, p0, i0, n, shift - lo_bits, lo_bits, ws));
+                    RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
+                    perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
+                    RSQ_LAUNCH_END(ctx);
+                    RSQ_TRY(onesweep_partition_pairs(ctx, p0, i0, part_pos, part_idx, n, shift, 8, ws));
+                } else {
+                    RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
+                    perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
+                    RSQ_LAUNCH_END(ctx);
+                    RSQ_TRY(onesweep_partition_iota(ctx, src_pos, part_pos, part_idx, n, shift, 8, ws));
+                }
+                if (win_bits <= 14) {
+                    static bool configured = false;
+                    if (!configured) {
+                        RSQ_CUDA(cudaFuncSetAttribute(window_scatter_kernel,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+                        configured = true;
+                    }
+                    const unsigned windows = static_cast<unsigned>((n + (size_t{1} << win_bits) - 1) >> win_bits);
+                    RSQ_LAUNCH_BEGIN(ctx, "window_scatter_kernel");
+                    window_scatter_kernel<<<windows, 512, sizeof(u32) << win_bits, s>>>(part_pos, part_idx, n,
+                                                                                        win_bits, rank);
+                    RSQ_LAUNCH_END(ctx);
+                } else {
+                    RSQ_LAUNCH_BEGIN(ctx, "scatter_pairs_kernel");
+                    scatter_pairs_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(part_pos, part_idx, n, rank);
+                    RSQ_LAUNCH_END(ctx);
+                }
             } else {  // the whole rank array is L2-resident: scatter directly
                 RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
                 inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa_cur, n, rank);
