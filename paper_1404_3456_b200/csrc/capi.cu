@@ -156,6 +156,7 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     RSQ_CUDA(cudaMallocHost(&ctx->pinned, 4096));
     if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
     if (const char* e = std::getenv("RESEQ_INVERSE_LO_BITS")) ctx->opt_inverse_lo_bits = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_SA_SHORTCUT")) ctx->opt_shortcut = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);
     *out = ctx;
     return RESEQ_OK;
@@ -194,6 +195,10 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     if (std::strcmp(name, "sa_text_rounds") == 0) {
         if (value < 0 || value > 1024) return fail(RESEQ_INVALID_ARGUMENT, "sa_text_rounds must be in 0..1024");
         ctx->opt_text_rounds = static_cast<int>(value);
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "sa_shortcut") == 0) {
+        ctx->opt_shortcut = value != 0;
         return RESEQ_OK;
     }
     if (std::strcmp(name, "sort_cfg") == 0) {

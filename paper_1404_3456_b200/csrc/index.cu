@@ -591,7 +591,7 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
 
     if (ix->dna) {
         bool is_dna = true;
-        IX_TRY(pack_dna_device(ctx, ix->d_text, n, ix->d_packed, ix->d_sent, counters + 8, &is_dna));
+        IX_TRY(pack_dna_device(ctx, ix->d_text, n, ix->d_packed, ix->d_sent, counters + 8, &is_dna, nullptr));
         ix->dir_bases = D;
         IX_TRY(dev_alloc(ix, &ix->d_dir, dir_entries));
         IX_TRY(dev_alloc(ix, &ix->d_sdir, dir_entries));

@@ -55,6 +55,7 @@ pack_dna_kernel(const u8* __restrict__ text, u64 n, u64* __restrict__ packed,
     const u64 words = (n + 63) >> 6;  // one thread per 64 positions
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     bool bad = false;
+    u32 n_sent = 0;
     for (u64 w = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) {
         const u64 base = w << 6;
         u64 p0 = 0, p1 = 0, s = 0;
@@ -88,8 +89,11 @@ pack_dna_kernel(const u8* __restrict__ text, u64 n, u64* __restrict__ packed,
         packed[2 * w] = p0;
         packed[2 * w + 1] = p1;
         sent[w] = s;
+        n_sent += __popcll(s);
     }
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(bad_flag, 1u);
+    for (int o = 16; o > 0; o >>= 1) n_sent += __shfl_xor_sync(0xffffffffu, n_sent, o);
+    if (lane_id() == 0 && n_sent) atomicAdd(bad_flag + 1, n_sent);  // number of separator bytes
 }
 
 __device__ __forceinline__ u64 base_window(const u64* __restrict__ packed, u64 pos) {
@@ -320,9 +324,10 @@ constexpr int kRefExt = 1024;
 constexpr int kRefCap = kRefTile + kRefExt;
 constexpr int kRefWords = kRefCap / 32 + 2;
 constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 3 * sizeof(unsigned short) * kRefCap +
-                            sizeof(u32) * (3 * kRefWords + 16);
+                            sizeof(u32) * (4 * kRefWords + 16);
 constexpr int kTextK = 23;          // bases per refinement round
 constexpr int kTextFieldBits = 6;   // terminator field: 2*len + kind, 2*kTextK = "no terminator"
+constexpr u32 kDistCap = 4095;      // farthest sentinel the distance shortcut looks for
 constexpr int kTextSlotBits = 12;   // window slot of the suffix: makes every key of a round unique
 static_assert(kRefCap <= (1 << kTextSlotBits), "window slots must fit the key's slot field");
 static_assert(2 * kTextK + kTextFieldBits + kTextSlotBits == 64, "refinement key layout");
@@ -381,7 +386,7 @@ headbits_kernel(const u32* __restrict__ keys, u64 n, u32 uniq_mask, u32 uniq_ful
 __global__ void __launch_bounds__(kRefBlock)
 refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n,
                    u32* __restrict__ sa, const u32* __restrict__ bits_old, u32* __restrict__ bits_new,
-                   u32 depth, int max_rounds, u32* __restrict__ counters) {
+                   u32 depth, int max_rounds, bool use_shortcut, u32* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char ref_smem[];
     u64* s_key = reinterpret_cast<u64*>(ref_smem);               // [cap] keys of the round ...
     u32* s_pos2 = reinterpret_cast<u32*>(ref_smem);              // ... then the permuted positions
@@ -391,7 +396,8 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
     unsigned short* s_src = s_dst + kRefCap;                     // [cap] old slot of new slot d
     u32* s_bits = reinterpret_cast<u32*>(s_src + kRefCap);       // [words] head bits of the window
     u32* s_new = s_bits + kRefWords;                             // [words] heads created this round
-    u32* s_cnt = s_new + kRefWords;                              // [words + 1] tied-count scan
+    u32* s_fail = s_new + kRefWords;                             // [words] groups the shortcut gave up on
+    u32* s_cnt = s_fail + kRefWords;                             // [words + 1] tied-count scan
     __shared__ int s_first, s_end, s_last;
 
     const int tid = threadIdx.x;
@@ -449,14 +455,37 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
 
     constexpr u32 kFieldMask = (1u << kTextFieldBits) - 1u;
     constexpr u32 kFull = 2 * kTextK;
+    constexpr u32 kNoDist = kDistCap + 1;  // "no sentinel within reach": the shortcut does not apply
+
+    // group start of window slot a: the last head at or before it
+    auto group_start = [&](int a) {
+        int w = a >> 5;
+        u32 word = s_bits[w] & (0xffffffffu >> (31 - (a & 31)));
+        while (!word) word = s_bits[--w];
+        return w * 32 + 31 - __clz(word);
+    };
+    auto group_end = [&](int a) {  // the first head after it
+        int w = (a + 1) >> 5;
+        u32 word = s_bits[w] & (0xffffffffu << ((a + 1) & 31));
+        while (!word) word = s_bits[++w];
+        return w * 32 + __ffs(word) - 1;
+    };
+
     bool loaded = false;
     int rounds = 0;
-    for (; rounds < max_rounds; ++rounds, depth += kTextK) {
+    // Steps alternate: a SHORTCUT step (below) on everything tied, then a TEXT step (the next
+    // 23 symbols) on what the shortcut could not settle.
+    for (int step = 0;; ++step) {
+        const bool shortcut = use_shortcut && (step & 1) == 0;
+        if (!shortcut && rounds >= max_rounds) break;
+        if (!use_shortcut && (step & 1) == 0) continue;
+
         // -- compact the tied slots, in order ------------------------------------------------
         u32 tw = 0, c = 0;
         if (tid < kRefWords) {
             tw = tied_word(tid);
             c = __popc(tw);
+            s_fail[tid] = 0;
         }
         u32 inc = c;
 #pragma unroll
@@ -489,27 +518,37 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
         __syncthreads();
         const int cnt = static_cast<int>(total);
 
-        // -- fetch the next 23 symbols of every tied suffix (an L2 hit) -----------------------
+        // -- keys.  TEXT: the next 23 symbols (an L2 hit).  SHORTCUT: the distance from the
+        //    current depth to the suffix's sentinel.  In a read set the members of a group are
+        //    reads over one locus: each is a prefix of the longer ones, so their order is
+        //    (distance, position) -- provided that really holds, which the verify pass below
+        //    checks base by base on neighbours in the new order (prefix-of is transitive along
+        //    the sorted chain).  A verified group is completely ordered in ONE step instead of
+        //    ceil(length / 23). ----------------------------------------------------------------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
-            s_key[a] = text_key(packed, sent, n, static_cast<u64>(s_pos[a]) + depth, static_cast<u32>(a));
+            const u64 q = static_cast<u64>(s_pos[a]) + depth;
+            if (shortcut) {
+                u32 dist = kNoDist;
+                for (u32 c0 = 0; c0 <= kDistCap && q + c0 < n; c0 += 64) {
+                    const u64 w = sent_window(sent, q + c0);
+                    if (w) {
+                        dist = c0 + static_cast<u32>(__clzll(w));
+                        break;
+                    }
+                }
+                if (dist > kDistCap) dist = kNoDist;
+                s_key[a] = (static_cast<u64>(dist) << kTextSlotBits) | static_cast<u32>(a);
+            } else {
+                s_key[a] = text_key(packed, sent, n, q, static_cast<u32>(a));
+            }
         }
         __syncthreads();
 
         // -- rank inside the group: the keys are unique, so rank = #smaller keys -----------------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
-            int gs, ge;
-            {
-                int w = a >> 5;
-                u32 word = s_bits[w] & (0xffffffffu >> (31 - (a & 31)));
-                while (!word) word = s_bits[--w];
-                gs = w * 32 + 31 - __clz(word);
-                w = (a + 1) >> 5;
-                word = s_bits[w] & (0xffffffffu << ((a + 1) & 31));
-                while (!word) word = s_bits[++w];
-                ge = w * 32 + __ffs(word) - 1;
-            }
+            const int gs = group_start(a), ge = group_end(a);
             const u64 ki = s_key[a];
             u32 r0 = 0, r1 = 0;
             int j = gs;
@@ -524,25 +563,56 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
         }
         __syncthreads();
 
-        // -- new heads: a suffix starts a group iff its content differs from its predecessor's
-        //    in the new order, or it carries a terminator (unique by construction) ---------------
+        // -- new heads -------------------------------------------------------------------------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
             const int dst = s_dst[u];
-            const u64 ki = s_key[a] >> kTextSlotBits;
-            bool head = (static_cast<u32>(ki) & kFieldMask) != kFull;
-            // slot dst-1 belongs to the same group unless dst opens it (then its bit is already set
-            // and s_src[dst - 1] is not this round's)
-            if (!head && !((s_bits[dst >> 5] >> (dst & 31)) & 1u))
-                head = (s_key[s_src[dst - 1]] >> kTextSlotBits) != ki;
-            if (head) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
+            const bool opens = (s_bits[dst >> 5] >> (dst & 31)) & 1u;  // slot dst starts the group
+            if (shortcut) {
+                // verify: the predecessor in the new order must be a prefix of this suffix
+                const u32 dist = static_cast<u32>(s_key[a] >> kTextSlotBits);
+                bool ok = dist != kNoDist;
+                if (ok && !opens) {
+                    const int pa = s_src[dst - 1];
+                    const u32 pd = static_cast<u32>(s_key[pa] >> kTextSlotBits);  // <= dist
+                    const u64 qa = static_cast<u64>(s_pos[a]) + depth, qp = static_cast<u64>(s_pos[pa]) + depth;
+                    for (u32 c0 = 0; c0 < pd && ok; c0 += 32) {
+                        const u32 len = pd - c0 < 32u ? pd - c0 : 32u;
+                        ok = ((base_window(packed, qa + c0) ^ base_window(packed, qp + c0)) >> (64 - 2 * len)) == 0;
+                    }
+                }
+                if (!ok) {
+                    const int gs = group_start(a);
+                    atomicOr(&s_fail[gs >> 5], 1u << (gs & 31));
+                }
+            } else {
+                // a suffix starts a group iff its content differs from its predecessor's in the
+                // new order, or it carries a terminator (unique by construction)
+                const u64 ki = s_key[a] >> kTextSlotBits;
+                bool head = (static_cast<u32>(ki) & kFieldMask) != kFull;
+                if (!head && !opens) head = (s_key[s_src[dst - 1]] >> kTextSlotBits) != ki;
+                if (head) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
+            }
         }
         __syncthreads();
 
         // -- permute (the key buffer is dead: it receives the new order) -----------------------
-        for (int u = tid; u < cnt; u += kRefBlock) s_pos2[s_dst[u]] = s_pos[s_list[u]];
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            int dst = s_dst[u];
+            if (shortcut) {
+                const int gs = group_start(a);
+                if ((s_fail[gs >> 5] >> (gs & 31)) & 1u) {
+                    s_dst[u] = 0xffff;  // group left as it was
+                    continue;
+                }
+                atomicOr(&s_new[dst >> 5], 1u << (dst & 31));  // verified: every member is final
+            }
+            s_pos2[dst] = s_pos[a];
+        }
         __syncthreads();
         for (int u = tid; u < cnt; u += kRefBlock) {
+            if (s_dst[u] == 0xffff) continue;
             const int a = s_list[u];
             s_pos[a] = s_pos2[a];
         }
@@ -551,6 +621,10 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
             s_new[tid] = 0;
         }
         __syncthreads();
+        if (!shortcut) {
+            ++rounds;
+            depth += kTextK;
+        }
     }
     if (!loaded) return;  // nothing was tied in this tile
 
@@ -667,9 +741,9 @@ unsigned grid_for(const reseq_cuda_ctx* ctx, size_t n, int block, int per_thread
 }  // namespace
 
 int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed, u64* sent,
-                    u32* d_flag, bool* is_dna) {
+                    u32* d_flag, bool* is_dna, u64* n_separators) {
     cudaStream_t s = ctx->stream;
-    RSQ_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(u32), s));
+    RSQ_CUDA(cudaMemsetAsync(d_flag, 0, 2 * sizeof(u32), s));
     RSQ_CUDA(cudaMemsetAsync(packed + (n / 64) * 2, 0,
                              sizeof(u64) * ((n / 32 + 8) - (n / 64) * 2), s));
     RSQ_CUDA(cudaMemsetAsync(sent + n / 64, 0, sizeof(u64) * ((n / 64 + 8) - n / 64), s));
@@ -681,9 +755,10 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
         pack_dna_kernel<false><<<grid, 256, 0, s>>>(d_text, n, packed, sent, d_flag);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
-    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_flag, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_flag, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaStreamSynchronize(s));
-    *is_dna = (*reinterpret_cast<volatile u32*>(ctx->pinned)) == 0;
+    *is_dna = reinterpret_cast<volatile u32*>(ctx->pinned)[0] == 0;
+    if (n_separators) *n_separators = reinterpret_cast<volatile u32*>(ctx->pinned)[1];
     return RESEQ_OK;
 }
 
@@ -734,7 +809,11 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     // -- pack, decide the alphabet ----------------------------------------------------
     RSQ_CUDA(cudaMemsetAsync(counters, 0, 1024, s));
     bool dna = false;
-    RSQ_TRY(pack_dna_device(ctx, d_text, n, packed, sent, counters, &dna));
+    u64 n_separators = 0;
+    RSQ_TRY(pack_dna_device(ctx, d_text, n, packed, sent, counters + 16, &dna, &n_separators));
+    // The sentinel-distance shortcut pays off on read sets (a sentinel every <= 1024 symbols on
+    // average); on sentinel-free texts every probe would scan to its cap for nothing.
+    const bool use_shortcut = ctx->opt_shortcut != 0 && n_separators * 1024 >= n;
     st.alphabet = dna ? 0 : 1;
 
     // -- initial keys + their digit histograms, 32-bit LSD sort --------------------------
@@ -810,7 +889,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
             RSQ_LAUNCH_BEGIN(ctx, "refine_text_kernel");
             refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sa_cur, bits_a, bits_b,
                                                                    static_cast<u32>(h), ctx->opt_text_rounds,
-                                                                   counters + 4);
+                                                                   use_shortcut, counters + 4);
             RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
             RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 4, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));

@@ -17,6 +17,6 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
 // 2-bit packing of a DNA text (shared with the index): returns false through *is_dna when
 // a byte outside {0,A,C,G,T} is present.  packed needs n/32+8 u64, sent n/64+8 u64.
 int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed, u64* sent,
-                    u32* d_flag, bool* is_dna);
+                    u32* d_flag /* 2 words */, bool* is_dna, u64* n_separators /* nullable */);
 
 }  // namespace rsq
