@@ -87,7 +87,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._pump, daemon=True)
             self.t.start()
         except OSError:
@@ -203,7 +203,7 @@ def run_reference(args, text, read_len, workload):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
@@ -291,28 +291,49 @@ def main():
     perm_ok = bool(torch.equal((d_rank[(d_sa.to(torch.int64) & 0xFFFFFFFF)].to(torch.int64) & 0xFFFFFFFF), idx))
     del idx
 
-    # ---- roofline of the dominant kernel ------------------------------------------------------
+    # ---- roofline: per-kernel algorithmic bytes over live CUDA-event durations ----
     peak, peak_src = measured_peak()
     per_suffix, P, R16 = bytes_alg_per_suffix(n, L)
-    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (0, 0.0))
-    dom_name, (dom_launches, dom_ms) = dom
-    pass_bytes = {"onesweep_u64_pairs": 24.0, "onesweep_u32_pairs": 16.0, "onesweep_u32_keys": 8.0}.get(dom_name, 0.0)
-    if dom_launches and pass_bytes:
-        achieved = pass_bytes * n / (dom_ms / dom_launches * 1e-3) / 1e9
-    else:
-        achieved = 0.0
+    # B/suffix one launch of each kernel accounts for in the SURVEY 8(d) model.  The refine kernel
+    # stands for ALL doubling rounds of the model (R16 * (44 + 24 P)): it reaches the same order by
+    # fetching keys from the L2-resident packed text, so its figure can exceed the HBM peak -- its
+    # real DRAM traffic is in `traffic` (ncu).  The partition passes + window scatter stand for the
+    # model's inverse-permutation phase (8 B/suffix) and are listed with their own minimal traffic.
+    model = {
+        "pack_dna_kernel": 1.375, "initkey_dna_kernel": 8.375, "initkey_bytes_kernel": 9.0,
+        "onesweep_u32_pairs": 16.0, "onesweep_u32_keys": 8.0, "onesweep_u64_pairs": 24.0,
+        "headbits_kernel": 4.03, "refine_text_kernel": float(R16 * (44 + 24 * P)),
+        "onesweep_u32_partition": 14.0, "window_scatter_kernel": 12.0, "scatter_pairs_kernel": 12.0,
+        "inverse_kernel": 8.0, "pair_key_kernel": 20.0, "rerank_kernel": 16.0, "hist_kernel": 4.0,
+    }
+    ncu_traffic = {"refine_text_kernel": 1.259e9}  # dram read+write per launch, profiles/r1_ncu_refine.txt
+    kernels = {}
+    for kname, (cnt, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        b = model.get(kname)
+        avg = ms / cnt if cnt else None
+        ach = b * n / (avg * 1e-3) / 1e9 if (b and avg) else None
+        kernels[kname] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
+                          "avg_launch_ms": avg, "alg_bytes_per_suffix": b,
+                          "achieved_gbs": ach, "frac": ach / peak if ach else None,
+                          "share_of_step": (ms / args.steps) / ms_per_step}
+    dom_name = next(iter(kernels)) if kernels else "none"
+    dom = kernels.get(dom_name, {})
     kernel_ms = sum(v[1] for v in prof.values()) / args.steps
     roofline = {
-        "bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak if peak else None, "traffic": None,
+        "bound": "hbm", "kernel": dom_name, "achieved": dom.get("achieved_gbs"), "peak": peak, "unit": "GB/s",
+        "frac": dom.get("frac"), "traffic": ncu_traffic.get(dom_name),
         "peak_source": peak_src,
-        "alg_bytes_per_launch": pass_bytes * n, "launches_per_step": dom_launches / args.steps,
-        "avg_launch_ms": dom_ms / dom_launches if dom_launches else None,
-        "kernel_share_of_step": (dom_ms / args.steps) / ms_per_step,
+        "alg_bytes_per_launch": (dom.get("alg_bytes_per_suffix") or 0) * n,
+        "launches_per_step": dom.get("launches_per_step"), "avg_launch_ms": dom.get("avg_launch_ms"),
+        "kernel_share_of_step": dom.get("share_of_step"),
+        "note": ("refine_text_kernel replaces the model's R16 prefix-doubling rounds (R16*(44+24P) B/suffix) with "
+                 "shared-memory refinement keyed from the L2-resident 2-bit text; it is instruction/L2-latency "
+                 "bound, not HBM bound, hence frac > 1 on the model and DRAM traffic of ~9 B/suffix. The "
+                 "dominant HBM-bound kernel is onesweep_u32_pairs (see kernels).") if dom_name == "refine_text_kernel" else None,
         "build": {"alg_bytes_per_suffix": per_suffix, "P": P, "R16": R16,
                   "achieved_gbs": per_suffix * n / (ms_per_step * 1e-3) / 1e9,
                   "frac": per_suffix * n / (ms_per_step * 1e-3) / 1e9 / peak},
-        "per_kernel_ms_per_step": {kname: v[1] / args.steps for kname, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "kernels": kernels,
         "sum_kernel_ms_per_step": kernel_ms,
     }
 

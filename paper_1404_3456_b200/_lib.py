@@ -95,6 +95,11 @@ SIGNATURES = {
     "reseq_cuda_chunked_radix_sort": (C.c_int, [_vp, _vp, _vp, C.c_size_t, C.c_uint, _vp, _vp]),
     "reseq_cuda_build_sa": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp, C.POINTER(SaStats)]),
     "reseq_cuda_build_sa_device": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp, C.POINTER(SaStats)]),
+    "reseq_cuda_sa_shard_create": (C.c_int, [_vp, _vp, C.c_size_t, C.POINTER(_vp), C.POINTER(C.c_int)]),
+    "reseq_cuda_sa_shard_destroy": (None, [_vp]),
+    "reseq_cuda_sa_shard_keys": (C.c_int, [_vp, C.c_uint64, C.c_size_t, _vp, _vp]),
+    "reseq_cuda_sa_shard_finish": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _u64p]),
+    "reseq_cuda_inverse_device": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
     "reseq_cuda_checksum_u32_device": (C.c_int, [_vp, _vp, C.c_size_t, _u64p]),
     "reseq_cuda_index_create": (C.c_int, [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(_vp)]),
     "reseq_cuda_index_destroy": (None, [_vp]),
@@ -107,6 +112,7 @@ SIGNATURES = {
     "reseq_cuda_index_prefix_related_batch": (C.c_int, [_vp, _vp, _vp, C.c_size_t, C.POINTER(PrefixRelations)]),
     "reseq_cuda_prefix_relations_free": (None, [C.POINTER(PrefixRelations)]),
     "reseq_cuda_index_overlaps": (C.c_int, [_vp, C.c_uint32, C.POINTER(Overlaps)]),
+    "reseq_cuda_index_overlaps_range": (C.c_int, [_vp, C.c_uint32, C.c_size_t, C.c_size_t, C.POINTER(Overlaps)]),
     "reseq_cuda_overlaps_free": (None, [C.POINTER(Overlaps)]),
     "reseq_greedy_superstring": (C.c_int, [_vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(Overlaps), C.c_uint32,
                                            _vp, C.POINTER(C.c_size_t), _vp, C.POINTER(C.c_size_t)]),

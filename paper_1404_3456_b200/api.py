@@ -393,9 +393,14 @@ class FragmentIndex:
         """prefix_related(residual{frag, off}) (fragment_index.hpp:78-80)."""
         return self.prefix_related_batch([frag], [off])[0]
 
-    def overlaps(self, min_overlap: int = 1) -> OverlapList:
+    def overlaps(self, min_overlap: int = 1, frag_begin: int = 0, frag_end: Optional[int] = None) -> OverlapList:
+        """Sparse overlap graph; [frag_begin, frag_end) restricts the querying fragments (the
+        unit of sharding across GPUs)."""
         ov = _lib.Overlaps()
-        _lib.check(self._lib.reseq_cuda_index_overlaps(self._h, int(min_overlap), C.byref(ov)))
+        if frag_end is None:
+            frag_end = self.set.starts.size
+        _lib.check(self._lib.reseq_cuda_index_overlaps_range(self._h, int(min_overlap), int(frag_begin),
+                                                             int(frag_end), C.byref(ov)))
         try:
             m, k = int(ov.count), self.set.starts.size
             take = lambda p, cnt, dt: (np.ctypeslib.as_array(p, shape=(cnt,)).astype(dt, copy=True)

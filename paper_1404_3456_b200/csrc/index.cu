@@ -304,15 +304,15 @@ locate_patterns_kernel(IndexView iv, const u8* __restrict__ pats, const u64* __r
 // (overlap.hpp:16-23).  Stores, per query, the start-list interval; per fragment, the
 // absorb_contained verdict (overlap.hpp:51-67) from the o = 0 query.
 __global__ void __launch_bounds__(256)
-overlap_count_kernel(IndexView iv, u32 min_ov, const u64* __restrict__ qoff, u32* __restrict__ q_first,
-                     u32* __restrict__ q_count, u8* __restrict__ contained) {
+overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __restrict__ qoff,
+                     u32* __restrict__ q_first, u32* __restrict__ q_count, u8* __restrict__ contained) {
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     const unsigned lane = lane_id();
-    for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < iv.k; i += warps) {
+    for (u64 i = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < f1; i += warps) {
         const u32 len = iv.lens[i];
         const u64 start = iv.starts[i];
-        const u64 qbase = qoff[i];
-        const u32 nq = static_cast<u32>(qoff[i + 1] - qbase);  // offsets 0 .. len - min_ov
+        const u64 qbase = qoff[i - f0];
+        const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);  // offsets 0 .. len - min_ov
         // a fragment shorter than min_ov still runs its o = 0 query for the containment flag
         const u32 steps = nq ? nq : 1u;
         for (u32 o = lane; o < steps; o += 32) {
@@ -347,15 +347,15 @@ overlap_count_kernel(IndexView iv, u32 min_ov, const u64* __restrict__ qoff, u32
 // (i, o ascending) order so that after a STABLE sort on (i, j) the first record of every
 // pair carries its maximum w.
 __global__ void __launch_bounds__(256)
-overlap_fill_kernel(IndexView iv, const u64* __restrict__ qoff, const u32* __restrict__ q_first,
+overlap_fill_kernel(IndexView iv, u64 f0, u64 f1, const u64* __restrict__ qoff, const u32* __restrict__ q_first,
                     const u32* __restrict__ q_count, const u32* __restrict__ q_out, u64* __restrict__ keys,
                     u32* __restrict__ w) {
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     const unsigned lane = lane_id();
-    for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < iv.k; i += warps) {
+    for (u64 i = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < f1; i += warps) {
         const u32 len = iv.lens[i];
-        const u64 qbase = qoff[i];
-        const u32 nq = static_cast<u32>(qoff[i + 1] - qbase);
+        const u64 qbase = qoff[i - f0];
+        const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);
         for (u32 o = lane; o < nq; o += 32) {
             const u32 cnt = q_count[qbase + o];
             if (!cnt) continue;
@@ -810,9 +810,16 @@ int reseq_cuda_index_prefix_related_batch(reseq_cuda_index* ix, const uint32_t* 
 }
 
 int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_overlaps* out) {
+    return reseq_cuda_index_overlaps_range(ix, min_overlap, 0, ix ? ix->k : 0, out);
+}
+
+int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag_begin,
+                                    size_t frag_end, reseq_overlaps* out) {
     if (!ix || !out) return fail(RESEQ_INVALID_ARGUMENT, "null argument");
     std::memset(out, 0, sizeof(*out));
+    if (frag_begin > frag_end || frag_end > ix->k) return fail(RESEQ_INVALID_ARGUMENT, "fragment range out of bounds");
     if (min_overlap < 1) min_overlap = 1;
+    const size_t f0 = frag_begin, f1 = frag_end, kr = frag_end - frag_begin;
     reseq_cuda_ctx* ctx = ix->ctx;
     RSQ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -823,9 +830,10 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
     std::vector<u32> lens(k);
     RSQ_CUDA(cudaMemcpyAsync(lens.data(), ix->d_lens, sizeof(u32) * k, cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaStreamSynchronize(s));
-    std::vector<u64> qoff(k + 1, 0);
-    for (size_t i = 0; i < k; ++i) qoff[i + 1] = qoff[i] + (lens[i] >= min_overlap ? lens[i] - min_overlap + 1 : 0);
-    const u64 Q = qoff[k];
+    std::vector<u64> qoff(kr + 1, 0);
+    for (size_t i = 0; i < kr; ++i)
+        qoff[i + 1] = qoff[i] + (lens[f0 + i] >= min_overlap ? lens[f0 + i] - min_overlap + 1 : 0);
+    const u64 Q = qoff[kr];
     out->queries = Q;
     out->contained = static_cast<uint8_t*>(std::calloc(k, 1));
     if (!out->contained) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
@@ -835,11 +843,11 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
     RSQ_CUDA(cudaEventCreate(&ev0));
     RSQ_CUDA(cudaEventCreate(&ev1));
 
-    size_t need = pad(sizeof(u64) * (k + 1)) + 3 * pad(sizeof(u32) * (Q + 1)) + pad(k) +
+    size_t need = pad(sizeof(u64) * (kr + 1)) + 3 * pad(sizeof(u32) * (Q + 1)) + pad(k) +
                   scan_workspace_bytes(Q + 1) + 8192;
     RSQ_TRY(ctx->reserve(need));
     ctx->begin();
-    u64* d_qoff = ctx->alloc<u64>(k + 1);
+    u64* d_qoff = ctx->alloc<u64>(kr + 1);
     u32* q_first = ctx->alloc<u32>(Q + 1);
     u32* q_count = ctx->alloc<u32>(Q + 1);
     u32* q_out = ctx->alloc<u32>(Q + 1);
@@ -847,17 +855,17 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
     u64* d_total = ctx->alloc<u64>(1);
     if (!d_qoff || !q_first || !q_count || !q_out || !d_contained || !d_total)
         return fail(RESEQ_OUT_OF_MEMORY, "overlap workspace");
-    RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (k + 1), cudaMemcpyHostToDevice, s));
+    RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (kr + 1), cudaMemcpyHostToDevice, s));
     RSQ_CUDA(cudaMemsetAsync(d_contained, 0, k, s));
     RSQ_CUDA(cudaMemsetAsync(q_count + Q, 0, sizeof(u32), s));
     const IndexView iv = view_of(ix);
 
     RSQ_CUDA(cudaEventRecord(ev0, s));
     u64 raw = 0;
-    if (Q > 0) {
-        const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+    if (kr > 0) {
+        const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
         RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
-        overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, d_qoff, q_first, q_count, d_contained);
+        overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
         RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
         RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
@@ -878,17 +886,17 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
             // grow: the arena is re-allocated, so redo pass 1 state in the new block
             RSQ_TRY(ctx->reserve(used_before + more));
             ctx->begin();
-            d_qoff = ctx->alloc<u64>(k + 1);
+            d_qoff = ctx->alloc<u64>(kr + 1);
             q_first = ctx->alloc<u32>(Q + 1);
             q_count = ctx->alloc<u32>(Q + 1);
             q_out = ctx->alloc<u32>(Q + 1);
             d_contained = ctx->alloc<u8>(k);
             d_total = ctx->alloc<u64>(1);
-            RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (k + 1), cudaMemcpyHostToDevice, s));
+            RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (kr + 1), cudaMemcpyHostToDevice, s));
             RSQ_CUDA(cudaMemsetAsync(q_count + Q, 0, sizeof(u32), s));
-            const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+            const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
             RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
-            overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, d_qoff, q_first, q_count, d_contained);
+            overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
             RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
             RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
@@ -906,9 +914,9 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
         if (!keys_a || !keys_b || !w_a || !w_b || !flag || !dst || !oi || !oj || !ow || !d_total2)
             return fail(RESEQ_OUT_OF_MEMORY, "overlap record workspace");
         {
-            const unsigned grid = grid_1d(ctx, k * 32, 256, 32);
+            const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
             RSQ_LAUNCH_BEGIN(ctx, "overlap_fill_kernel");
-            overlap_fill_kernel<<<grid, 256, 0, s>>>(iv, d_qoff, q_first, q_count, q_out, keys_a, w_a);
+            overlap_fill_kernel<<<grid, 256, 0, s>>>(iv, f0, f1, d_qoff, q_first, q_count, q_out, keys_a, w_a);
             RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
         }
@@ -940,9 +948,9 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total2, sizeof(u64), cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaStreamSynchronize(s));
         uniq = *reinterpret_cast<volatile u64*>(ctx->pinned);
-        out->i = static_cast<uint32_t*>(std::malloc(sizeof(u32) * uniq));
-        out->j = static_cast<uint32_t*>(std::malloc(sizeof(u32) * uniq));
-        out->w = static_cast<uint32_t*>(std::malloc(sizeof(u32) * uniq));
+        out->i = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
+        out->j = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
+        out->w = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
         if (!out->i || !out->j || !out->w) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
         RSQ_CUDA(cudaMemcpyAsync(out->i, oi, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaMemcpyAsync(out->j, oj, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));

@@ -116,18 +116,21 @@ constexpr int kDnaFieldBits = 5;
 constexpr int kByteK = 3;       // bytes per initial key: 24 bits + 3-bit terminator field
 constexpr int kByteFieldBits = 3;
 
+// Keys of the `count` suffixes starting at text position pos0 (the whole text: pos0 = 0,
+// count = n; a multi-GPU rank keys only its slice).  keys[i] / vals[i] belong to pos0 + i.
 __global__ void __launch_bounds__(256)
-initkey_dna_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n,
+initkey_dna_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n, u64 pos0, u64 count,
                    u32* __restrict__ keys, u32* __restrict__ vals, PassTable pt,
                    u32* __restrict__ g_hist) {
     extern __shared__ u32 s_hist[];
     for (int i = threadIdx.x; i < pt.count * kRadix; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    const u64 rounds = (n + stride - 1) / stride;
-    u64 pos = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (u64 r = 0; r < rounds; ++r, pos += stride) {
-        const bool in = pos < n;
+    const u64 rounds = (count + stride - 1) / stride;
+    u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (u64 r = 0; r < rounds; ++r, idx += stride) {
+        const bool in = idx < count;
+        const u64 pos = pos0 + idx;
         u32 key = 0;
         if (in) {
             const u32 bases = static_cast<u32>(base_window(packed, pos) >> (64 - 2 * kDnaK));
@@ -141,8 +144,8 @@ initkey_dna_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
             else { len = kDnaK; field = 2 * kDnaK; }              // k full bases
             const u32 kept = bases & ~((1u << (2 * (kDnaK - len))) - 1u);
             key = (kept << kDnaFieldBits) | field;
-            keys[pos] = key;
-            vals[pos] = static_cast<u32>(pos);
+            keys[idx] = key;
+            vals[idx] = static_cast<u32>(pos);
         }
         for (int p = 0; p < pt.count; ++p)
             hist_add(s_hist + p * kRadix, key_digit(key, pt.shift[p], pt.mask(p)), in);
@@ -384,9 +387,11 @@ headbits_kernel(const u32* __restrict__ keys, u64 n, u32 uniq_mask, u32 uniq_ful
 // contiguous) -- late rounds, where few suffixes are tied, then cost in proportion to what
 // is left instead of dragging 32-wide warps through one or two live lanes.
 __global__ void __launch_bounds__(kRefBlock)
-refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n,
-                   u32* __restrict__ sa, const u32* __restrict__ bits_old, u32* __restrict__ bits_new,
+refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n_text,
+                   u32* __restrict__ sa, u64 n, const u32* __restrict__ bits_old, u32* __restrict__ bits_new,
                    u32 depth, int max_rounds, bool use_shortcut, u32* __restrict__ counters) {
+    // n_text: length of the text the positions refer to; n: number of suffixes in sa (equal for
+    // a whole-text build, a bucket of it for a multi-GPU rank)
     extern __shared__ __align__(16) unsigned char ref_smem[];
     u64* s_key = reinterpret_cast<u64*>(ref_smem);               // [cap] keys of the round ...
     u32* s_pos2 = reinterpret_cast<u32*>(ref_smem);              // ... then the permuted positions
@@ -530,7 +535,7 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
             const u64 q = static_cast<u64>(s_pos[a]) + depth;
             if (shortcut) {
                 u32 dist = kNoDist;
-                for (u32 c0 = 0; c0 <= kDistCap && q + c0 < n; c0 += 64) {
+                for (u32 c0 = 0; c0 <= kDistCap && q + c0 < n_text; c0 += 64) {
                     const u64 w = sent_window(sent, q + c0);
                     if (w) {
                         dist = c0 + static_cast<u32>(__clzll(w));
@@ -540,7 +545,7 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
                 if (dist > kDistCap) dist = kNoDist;
                 s_key[a] = (static_cast<u64>(dist) << kTextSlotBits) | static_cast<u32>(a);
             } else {
-                s_key[a] = text_key(packed, sent, n, q, static_cast<u32>(a));
+                s_key[a] = text_key(packed, sent, n_text, q, static_cast<u32>(a));
             }
         }
         __syncthreads();
@@ -827,7 +832,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         const size_t smem = sizeof(u32) * pt0.count * kRadix;
         RSQ_LAUNCH_BEGIN(ctx, dna ? "initkey_dna_kernel" : "initkey_bytes_kernel");
         if (dna)
-            initkey_dna_kernel<<<grid, 256, smem, s>>>(packed, sent, n, k32_a, d_sa, pt0, ws.hist);
+            initkey_dna_kernel<<<grid, 256, smem, s>>>(packed, sent, n, 0, n, k32_a, d_sa, pt0, ws.hist);
         else
             initkey_bytes_kernel<<<grid, 256, smem, s>>>(d_text, n, k32_a, d_sa, pt0, ws.hist);
         RSQ_LAUNCH_END(ctx);
@@ -887,7 +892,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
             RSQ_CUDA(cudaMemcpyAsync(bits_b, bits_a, sizeof(u32) * words, cudaMemcpyDeviceToDevice, s));
             RSQ_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * sizeof(u32), s));
             RSQ_LAUNCH_BEGIN(ctx, "refine_text_kernel");
-            refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sa_cur, bits_a, bits_b,
+            refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sa_cur, n, bits_a, bits_b,
                                                                    static_cast<u32>(h), ctx->opt_text_rounds,
                                                                    use_shortcut, counters + 4);
             RSQ_LAUNCH_END(ctx);
@@ -1007,4 +1012,160 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     return RESEQ_OK;
 }
 
+
+// ---- multi-GPU building blocks -----------------------------------------------
+// One rank of a sample-sort partitioned build: the text is replicated (packed: n/4 bytes), the
+// rank keys a slice of positions, and after the all-to-all finishes the bucket of suffixes whose
+// keys fall in its splitter range -- same kernels as the single-GPU path, no exchange needed
+// afterwards because refinement keys come from the replicated text.
+
+}  // namespace rsq
+
+struct reseq_cuda_sa_shard {
+    reseq_cuda_ctx* ctx = nullptr;
+    const rsq::u8* d_text = nullptr;
+    size_t n = 0;
+    rsq::u64* packed = nullptr;
+    rsq::u64* sent = nullptr;
+    rsq::u32* flags = nullptr;
+    bool dna = false;
+    bool use_shortcut = false;
+};
+
+extern "C" {
+
+int reseq_cuda_sa_shard_create(reseq_cuda_ctx* ctx, const uint8_t* d_text, size_t n, reseq_cuda_sa_shard** out,
+                               int* is_dna) {
+    using namespace rsq;
+    if (!ctx || !out || !d_text || n == 0) return fail(RESEQ_INVALID_ARGUMENT, "null or empty argument");
+    if (n > RESEQ_CUDA_MAX_TEXT) return fail(RESEQ_TEXT_TOO_LARGE, "text exceeds 2^32-2");
+    *out = nullptr;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    auto* sh = new reseq_cuda_sa_shard();
+    sh->ctx = ctx;
+    sh->d_text = d_text;
+    sh->n = n;
+    if (cudaMalloc(&sh->packed, sizeof(u64) * (n / 32 + 8)) != cudaSuccess ||
+        cudaMalloc(&sh->sent, sizeof(u64) * (n / 64 + 8)) != cudaSuccess ||
+        cudaMalloc(&sh->flags, 256) != cudaSuccess) {
+        cudaGetLastError();
+        reseq_cuda_sa_shard_destroy(sh);
+        return fail(RESEQ_OUT_OF_MEMORY, "cudaMalloc failed for the packed text");
+    }
+    u64 n_sep = 0;
+    int st = pack_dna_device(ctx, d_text, n, sh->packed, sh->sent, sh->flags, &sh->dna, &n_sep);
+    if (st != RESEQ_OK) {
+        reseq_cuda_sa_shard_destroy(sh);
+        return st;
+    }
+    sh->use_shortcut = ctx->opt_shortcut != 0 && n_sep * 1024 >= n;
+    if (is_dna) *is_dna = sh->dna ? 1 : 0;
+    *out = sh;
+    return RESEQ_OK;
+}
+
+void reseq_cuda_sa_shard_destroy(reseq_cuda_sa_shard* sh) {
+    if (!sh) return;
+    if (sh->ctx) {
+        cudaSetDevice(sh->ctx->device);
+        cudaStreamSynchronize(sh->ctx->stream);
+    }
+    cudaFree(sh->packed);
+    cudaFree(sh->sent);
+    cudaFree(sh->flags);
+    delete sh;
+}
+
+int reseq_cuda_sa_shard_keys(reseq_cuda_sa_shard* sh, uint64_t pos_begin, size_t count, uint32_t* d_keys,
+                             uint32_t* d_pos) {
+    using namespace rsq;
+    if (!sh || !sh->dna) return fail(RESEQ_INVALID_ARGUMENT, "the sharded build needs a DNA text");
+    if (count == 0) return RESEQ_OK;
+    if (pos_begin + count > sh->n) return fail(RESEQ_INVALID_ARGUMENT, "position slice out of range");
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    RSQ_TRY(ctx->reserve(reseq_cuda_ctx::padded(sizeof(u32) * kMaxPasses * kRadix) + 4096));
+    ctx->begin();
+    u32* hist = ctx->alloc<u32>(kMaxPasses * kRadix);  // the slice's histogram is not used: buckets re-count
+    const PassTable pt0 = make_passes(0, 2 * kDnaK + kDnaFieldBits);
+    RSQ_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * pt0.count * kRadix, ctx->stream));
+    RSQ_LAUNCH_BEGIN(ctx, "initkey_dna_kernel");
+    initkey_dna_kernel<<<grid_for(ctx, count, 256, 8, 8), 256, sizeof(u32) * pt0.count * kRadix, ctx->stream>>>(
+        sh->packed, sh->sent, sh->n, pos_begin, count, d_keys, d_pos, pt0, hist);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
+}
+
+int reseq_cuda_sa_shard_finish(reseq_cuda_sa_shard* sh, uint32_t* d_keys, uint32_t* d_pos, size_t m,
+                               uint32_t* d_sa_out, uint64_t* unfinished) {
+    using namespace rsq;
+    if (!sh || !sh->dna || !unfinished) return fail(RESEQ_INVALID_ARGUMENT, "bad shard argument");
+    *unfinished = 0;
+    if (m == 0) return RESEQ_OK;
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    auto pad = reseq_cuda_ctx::padded;
+    RSQ_TRY(ctx->reserve(2 * pad(sizeof(u32) * m) + 2 * pad(sizeof(u32) * (m / 32 + 8)) + sort_workspace_bytes(m) + 8192));
+    ctx->begin();
+    u32* keys_b = ctx->alloc<u32>(m);
+    u32* pos_b = ctx->alloc<u32>(m);
+    u32* bits_a = ctx->alloc<u32>(m / 32 + 8);
+    u32* bits_b = ctx->alloc<u32>(m / 32 + 8);
+    u32* counters = ctx->alloc<u32>(64);
+    SortWorkspace ws;
+    if (!keys_b || !pos_b || !bits_a || !bits_b || !counters) return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
+    RSQ_TRY(sort_workspace_carve(ctx, m, &ws));
+    // stable sort of the bucket on the 31-bit key: equal keys stay in ascending position order
+    // because the exchange delivers the slices in rank (= position) order
+    const PassTable pt0 = make_passes(0, 2 * kDnaK + kDnaFieldBits);
+    bool in_b = false;
+    RSQ_TRY(onesweep_sort<u32>(ctx, d_keys, keys_b, d_pos, pos_b, m, pt0, ws, false, 0, &in_b));
+    u32* sa_cur = in_b ? pos_b : d_pos;
+    const size_t words = (m + 31) / 32 + 4;
+    RSQ_CUDA(cudaMemsetAsync(bits_a, 0, sizeof(u32) * words, s));
+    RSQ_CUDA(cudaMemsetAsync(counters, 0, 256, s));
+    RSQ_LAUNCH_BEGIN(ctx, "headbits_kernel");
+    headbits_kernel<<<grid_for(ctx, m, 256, 4, 16), 256, 0, s>>>(in_b ? keys_b : d_keys, m, (1u << kDnaFieldBits) - 1u,
+                                                                 2u * kDnaK, bits_a, counters);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(bits_b, bits_a, sizeof(u32) * words, cudaMemcpyDeviceToDevice, s));
+    RSQ_CUDA(cudaMemsetAsync(counters, 0, 256, s));
+    static bool configured = false;
+    if (!configured) {
+        RSQ_CUDA(cudaFuncSetAttribute(refine_text_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kRefSmem)));
+        configured = true;
+    }
+    const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
+    RSQ_LAUNCH_BEGIN(ctx, "refine_text_kernel");
+    refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(sh->packed, sh->sent, sh->n, sa_cur, m, bits_a, bits_b,
+                                                          kDnaK, 1 << 20, sh->use_shortcut, counters);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(d_sa_out, sa_cur, sizeof(u32) * m, cudaMemcpyDeviceToDevice, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    // still tied (only possible through an oversize group: the round limit is out of reach)
+    *unfinished = reinterpret_cast<volatile u32*>(ctx->pinned)[0] + (reinterpret_cast<volatile u32*>(ctx->pinned)[1] ? 1u : 0u);
+    return RESEQ_OK;
+}
+
+int reseq_cuda_inverse_device(reseq_cuda_ctx* ctx, const uint32_t* d_sa, size_t n, uint32_t* d_rank) {
+    using namespace rsq;
+    if (!ctx) return fail(RESEQ_INVALID_ARGUMENT, "null context");
+    if (n == 0) return RESEQ_OK;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
+    inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, ctx->stream>>>(d_sa, n, d_rank);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
+}
+
+}  // extern "C"
+
+namespace rsq {
 }  // namespace rsq

@@ -1,0 +1,113 @@
+// C++ drop-in test: the reference's own KATs (proj/tests/test_suffix_array.cpp:10-14,38-44;
+// test_parallel.cpp:52-66,86-97,125-132,165-170; test_fragment_index.cpp:33-53,129-138;
+// SPEC.md:300) through include/reseq_b200/reseq_cuda.hpp.  With -DRESEQ_B200_WITH_REFERENCE the
+// device results are also compared with the reference's own functions on the same inputs.
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <string>
+
+#include "reseq_b200/reseq_cuda.hpp"
+
+#ifdef RESEQ_B200_WITH_REFERENCE
+#include "reseq/fragment_index.hpp"
+#include "reseq/sequence.hpp"
+#endif
+
+using namespace reseq::cuda;
+using u32v = std::vector<std::uint32_t>;
+
+static int failures = 0;
+#define REQUIRE(cond)                                                         \
+    do {                                                                      \
+        if (!(cond)) {                                                        \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);       \
+            ++failures;                                                       \
+        }                                                                     \
+    } while (0)
+template <typename E, typename F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int main() {
+    device_executor dev(0);
+    REQUIRE(build_parallel("banana", dev).sa == (u32v{5, 3, 1, 0, 4, 2}));
+    REQUIRE(build_parallel("aaa", dev).sa == (u32v{2, 1, 0}));
+    REQUIRE(build_parallel("", dev).sa.empty());
+    REQUIRE(build_parallel(std::string("GA\0TT\0", 6), dev).sa == (u32v{2, 5, 1, 0, 4, 3}));
+    {
+        auto sp = build_parallel("mississippi", dev);
+        for (std::uint32_t i = 0; i < sp.sa.size(); ++i) REQUIRE(sp.rank[sp.sa[i]] == i);
+    }
+    REQUIRE(exclusive_scan(u32v{3, 1, 7, 0}, dev) == (u32v{0, 3, 4, 11}));
+    REQUIRE(exclusive_scan(u32v{}, dev).empty());
+    REQUIRE(throws<scan_overflow_error>([&] { exclusive_scan(u32v{0xFFFFFFFFu, 1u}, dev); }));
+    REQUIRE(exclusive_scan(u32v{0xFFFFFFFEu, 1u}, dev) == (u32v{0, 0xFFFFFFFEu}));
+    REQUIRE(split_by_bit(key_array{{5, 2, 7, 4}, {}}, 0, dev).keys == (u32v{2, 4, 5, 7}));
+    {
+        auto s = split_by_bit(key_array{{1, 1, 0, 0}, {10, 11, 12, 13}}, 0, dev);
+        REQUIRE(s.keys == (u32v{0, 0, 1, 1}));
+        REQUIRE(s.payload == (u32v{12, 13, 10, 11}));
+    }
+    REQUIRE(radix_sort(key_array{{170, 45, 75, 90, 2, 24, 802, 66}, {}}, dev).keys ==
+            (u32v{2, 24, 45, 66, 75, 90, 170, 802}));
+    REQUIRE(radix_sort(key_array{}, dev).keys.empty());
+    REQUIRE((radix_sort(key_array{{7}, {0}}, dev) == key_array{{7}, {0}}));
+    REQUIRE(throws<std::invalid_argument>([&] { chunked_radix_sort(key_array{{1, 2}, {}}, dev, 0); }));
+    REQUIRE(throws<std::invalid_argument>([&] { chunked_radix_sort(key_array{{1, 2}, {}}, dev, 9); }));
+    {
+        std::mt19937_64 rng(31);
+        key_array a;
+        for (int i = 0; i < 5000; ++i) {
+            a.keys.push_back(static_cast<std::uint32_t>(rng()));
+            a.payload.push_back(i);
+        }
+        REQUIRE(radix_sort(a, dev) == chunked_radix_sort(a, dev, 4));
+#ifdef RESEQ_B200_WITH_REFERENCE
+        REQUIRE(radix_sort(a, dev) == reseq::radix_sort(a));
+        REQUIRE(split_by_bit(a, 7, dev) == reseq::split_by_bit(a, 7));
+        REQUIRE(exclusive_scan(std::span<const std::uint32_t>(a.payload), dev) == reseq::exclusive_scan(a.payload));
+#endif
+    }
+    {
+        // the worked instance of test_fragment_index.cpp:33-45
+        const std::string concat("GATT\0ACA\0GGT\0GA\0TTAC\0AGGT\0", 26);
+        const u32v starts{0, 5, 9, 13, 16, 21};
+        fragment_index ix(concat, starts, dev);
+        auto [lo, hi] = ix.locate_prefix_range("GA");
+        REQUIRE(hi - lo == 2);
+        auto sa = ix.sa();
+        u32v pos{sa.sa[lo], sa.sa[lo + 1]};
+        REQUIRE((pos == u32v{0, 13} || pos == u32v{13, 0}));
+        auto [l2, h2] = ix.locate_prefix_range("QQ");
+        REQUIRE(l2 == h2);
+    }
+    {
+        // the paper's five fragments: SPEC.md:300
+        const std::string concat("abthatb\0hatbpaab\0tbabhhatbpaa\0paabtabh\0bhaabtpb\0", 48);
+        const u32v starts{0, 8, 17, 30, 39};
+        fragment_index ix(concat, starts, dev);
+        auto g = ix.greedy_superstring_with_order(1);
+        REQUIRE(g.superstring == "abthatbabhhatbpaabtabhaabtpb");
+        REQUIRE(g.order == (u32v{0, 2, 1, 3, 4}));
+#ifdef RESEQ_B200_WITH_REFERENCE
+        auto set = reseq::make_fragment_set({"abthatb", "hatbpaab", "tbabhhatbpaa", "paabtabh", "bhaabtpb"},
+                                            reseq::alphabet::generic_byte);
+        reseq::fragment_index ref_ix(set, reseq::fragment_index::builder::scan_radix);
+        REQUIRE(ix.sa().sa == ref_ix.sa().sa);
+        REQUIRE(ix.start_rank_list() == ref_ix.start_rank_list());
+        auto rg = reseq::greedy_superstring_with_order(set);
+        REQUIRE(g.superstring == rg.superstring && g.order == rg.order);
+#endif
+    }
+    std::printf(failures ? "%d FAILED\n" : "shim ok\n", failures);
+    return failures ? 1 : 0;
+}

@@ -170,3 +170,22 @@ def test_reconstruction_at_config1_scale_properties(rq, ex):
     assert sorted(order.tolist()) == kept.tolist()
     for i in range(0, len(starts), 97):
         assert fs.bytes(i) in sup
+
+
+def test_cpp_shim_drop_in(tmp_path):
+    """include/reseq_b200/reseq_cuda.hpp: the reference's KATs through the C++ value-semantics
+    shim, standalone and -- where the reference headers exist -- against the reference itself."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    lib = root / "paper_1404_3456_b200" / "libreseq_cuda.so"
+    variants = [[]]
+    if Path("/root/reference/proj/include").is_dir():
+        variants.append(["-DRESEQ_B200_WITH_REFERENCE", "-I/root/reference/proj/include", "-pthread"])
+    for extra in variants:
+        exe = tmp_path / f"shim{len(extra)}"
+        subprocess.run(["g++", "-std=c++20", "-O1", *extra, "-I", str(root / "include"),
+                        str(root / "tests" / "cpp" / "test_shim.cpp"), str(lib), f"-Wl,-rpath,{lib.parent}",
+                        "-o", str(exe)], check=True)
+        r = subprocess.run([str(exe)], capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr

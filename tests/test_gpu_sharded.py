@@ -1,0 +1,110 @@
+"""The multi-GPU path (paper_1404_3456_b200/sharded.py) run as G virtual ranks -- threads of one
+process sharing the one B200, each with its own context, exchanging through LocalComm.  Checks the
+sample-sort partitioned build and the read-sharded overlap search bit-for-bit against the
+single-GPU results for several G."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(G, fn):
+    from paper_1404_3456_b200.sharded import LocalComm
+    comms = LocalComm.make(G)
+    out, err = [None] * G, [None] * G
+
+    def work(r):
+        try:
+            out[r] = fn(comms[r])
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+            try:
+                comms[r].s.barrier.abort()
+            except Exception:
+                pass
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(G)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    for e in err:
+        if e is not None and not isinstance(e, threading.BrokenBarrierError):
+            raise e
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+def sharded_build(rq, text, G):
+    from paper_1404_3456_b200.sharded import GpuBackend, build_sa_sharded
+    d_text = torch.from_numpy(np.array(text, dtype=np.uint8, copy=True)).cuda()
+
+    def fn(comm):
+        ex = rq.Executor(0)
+        stats = {}
+        sa, rank = build_sa_sharded(d_text, comm, GpuBackend(ex), stats)
+        torch.cuda.synchronize()
+        res = sa.cpu().numpy().view(np.uint32), rank.cpu().numpy().view(np.uint32), stats
+        ex.close()
+        return res
+
+    return run_ranks(G, fn)
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_sharded_build_equals_single_gpu(rq, ex, oracle, G):
+    text, _ = rq.synth_read_text(60_000, 100, 6_000)
+    want = rq.build_parallel(text, ex)
+    assert oracle.verify_sa(text, want.sa) == 0
+    for sa, rank, stats in sharded_build(rq, text, G):
+        assert stats["path"] == "sharded"
+        assert np.array_equal(sa, want.sa) and np.array_equal(rank, want.rank)
+    # the buckets partition the suffixes: every rank sent and received something
+    sizes = [s["bucket"] for _, _, s in sharded_build(rq, text, G)]
+    assert sum(sizes) == text.size and min(sizes) > 0
+
+
+def test_sharded_build_ragged_and_tiny(rq, ex):
+    rng = np.random.default_rng(3)
+    t = rng.choice([65, 67, 71, 84, 0], 50_001, p=[.24, .24, .24, .24, .04]).astype(np.uint8)
+    t[-1] = 0
+    want = rq.build_parallel(t, ex)
+    for sa, rank, stats in sharded_build(rq, t, 3):
+        assert np.array_equal(sa, want.sa) and np.array_equal(rank, want.rank)
+    tiny = np.frombuffer(b"GA\0TT\0", np.uint8)
+    for sa, rank, stats in sharded_build(rq, tiny, 2):
+        assert sa.tolist() == [2, 5, 1, 0, 4, 3] and stats["path"] == "replicated"
+
+
+def test_sharded_build_fallbacks(rq, ex):
+    generic = np.frombuffer(b"abthatb\0hatbpaab\0tbabhhatbpaa\0paabtabh\0bhaabtpb\0" * 20, np.uint8)
+    want = rq.build_parallel(generic, ex)
+    for sa, rank, stats in sharded_build(rq, generic, 2):
+        assert stats["path"] == "replicated" and np.array_equal(sa, want.sa)
+    big_groups = np.frombuffer((b"ACGTACGTAC" * 12 + b"\0") * 3000, np.uint8)   # groups of 3000 > refine window
+    want = rq.build_parallel(big_groups, ex)
+    for sa, rank, stats in sharded_build(rq, big_groups, 2):
+        assert stats["path"] == "replicated-fallback"
+        assert np.array_equal(sa, want.sa) and np.array_equal(rank, want.rank)
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_sharded_overlaps_equal_single_gpu(rq, ex, G):
+    from paper_1404_3456_b200.sharded import gather_overlaps, overlaps_sharded
+    text, starts = rq.synth_read_text(30_000, 80, 4_000)
+    fset = rq.fragment_set_from_text(text, starts)
+    ix = rq.FragmentIndex(fset, ex)
+    want = ix.overlaps(16)
+    def fn(comm):   # one context per rank: a context serves one host thread at a time
+        e = rq.Executor(0)
+        part = overlaps_sharded(fset, comm, e, 16)
+        e.close()
+        return part
+
+    parts = run_ranks(G, fn)
+    got = gather_overlaps(parts)
+    assert np.array_equal(got.i, want.i) and np.array_equal(got.j, want.j) and np.array_equal(got.w, want.w)
+    assert np.array_equal(got.contained, want.contained) and got.queries == want.queries

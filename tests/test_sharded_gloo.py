@@ -1,0 +1,139 @@
+"""Host logic of the multi-GPU path under REAL collectives: two processes, gloo backend, CPU
+tensors.  The per-rank kernels are replaced by a numpy stand-in (NumpyBackend below, checker-grade
+code that leans on the oracle), so what is exercised is sharded.py itself: position slicing,
+splitter selection from the all-reduced histogram, the all-to-all of (key, position) records, the
+ordering guarantee the bucket sort relies on, the all-gather of buckets and the fallbacks."""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def initial_keys(text: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """numpy restatement of the 31-bit initial key of csrc/sa.cu (13 bases zero padded at a
+    terminator << 5 | 2*len + kind)."""
+    n = text.size
+    code = np.zeros(256, np.int64)
+    code[[65, 67, 71, 84]] = [0, 1, 2, 3]
+    keys = np.zeros(hi - lo, np.int64)
+    for i, pos in enumerate(range(lo, hi)):
+        bases, ln, field = 0, 0, 26
+        for t in range(13):
+            if pos + t >= n:
+                field = 2 * ln
+                break
+            c = text[pos + t]
+            if c == 0:
+                field = 2 * ln + 1
+                break
+            bases |= int(code[c]) << (2 * (12 - t))
+            ln += 1
+        keys[i] = (bases << 5) | field
+    return keys
+
+
+class NumpyBackend:
+    def __init__(self, oracle_rank):
+        self.oracle_rank = oracle_rank   # inverse SA of the whole text from the oracle
+
+    def open(self, d_text):
+        self.text = d_text.numpy()
+        return bool(np.isin(self.text, [0, 65, 67, 71, 84]).all())
+
+    def close(self):
+        pass
+
+    def keys(self, lo, count):
+        return (torch.from_numpy(initial_keys(self.text, lo, lo + count).astype(np.int32)),
+                torch.arange(lo, lo + count, dtype=torch.int32))
+
+    def prefix_histogram(self, keys):
+        return torch.bincount((keys >> 15).to(torch.int64), minlength=1 << 16)
+
+    def partition(self, keys, pos, bounds):
+        dest = torch.bucketize((keys >> 15).to(torch.int64), bounds, right=True)
+        order = torch.argsort(dest, stable=True)
+        counts = torch.bincount(dest, minlength=bounds.numel() + 1)
+        return keys[order].contiguous(), pos[order].contiguous(), [int(c) for c in counts.tolist()]
+
+    def finish(self, keys, pos):
+        p = pos.numpy().astype(np.int64)
+        # the exchange must deliver equal keys in ascending position order (stability contract)
+        k = keys.numpy().astype(np.int64)
+        order = np.argsort(k, kind="stable")
+        same = k[order][1:] == k[order][:-1]
+        assert np.all(p[order][1:][same] > p[order][:-1][same]), "records of equal key arrived out of position order"
+        by_suffix = p[np.argsort(self.oracle_rank[p], kind="stable")]
+        return torch.from_numpy(by_suffix.astype(np.int32)), 0
+
+    def inverse(self, sa):
+        s = sa.numpy().astype(np.int64)
+        r = np.empty_like(s)
+        r[s] = np.arange(s.size)
+        return torch.from_numpy(r.astype(np.int32))
+
+    def full_build(self, d_text):
+        sa = np.argsort(self.oracle_rank, kind="stable")
+        return torch.from_numpy(sa.astype(np.int32)), torch.from_numpy(self.oracle_rank.astype(np.int32))
+
+
+def worker(rank, world, port, text_bytes, oracle_rank, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, str(ROOT))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1404_3456_b200.sharded import TorchComm, build_sa_sharded
+    comm = TorchComm()
+    d_text = torch.from_numpy(np.frombuffer(text_bytes, np.uint8).copy())
+    stats = {}
+    sa, rk = build_sa_sharded(d_text, comm, NumpyBackend(oracle_rank), stats)
+    np.save(Path(out_dir) / f"sa{rank}.npy", sa.numpy())
+    np.save(Path(out_dir) / f"rank{rank}.npy", rk.numpy())
+    (Path(out_dir) / f"stats{rank}.txt").write_text(f"{stats['path']} {stats.get('bucket', 0)} {stats.get('sent', 0)}")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sample_sort_exchange_under_gloo(oracle, tmp_path, world):
+    rng = np.random.default_rng(11)
+    genome = rng.choice([65, 67, 71, 84], 900).astype(np.uint8)
+    reads = [bytes(genome[s:s + 40]) + b"\0" for s in rng.integers(0, 860, 120)]
+    text = np.frombuffer(b"".join(reads), np.uint8)
+    want_sa, want_rank = oracle.build_sa(text)
+    port = 29500 + int(rng.integers(0, 2000))
+    mp.spawn(worker, args=(world, port, text.tobytes(), want_rank.astype(np.int64), str(tmp_path)), nprocs=world,
+             join=True)
+    buckets = []
+    for r in range(world):
+        sa = np.load(tmp_path / f"sa{r}.npy").view(np.uint32)
+        rk = np.load(tmp_path / f"rank{r}.npy").view(np.uint32)
+        assert np.array_equal(sa, want_sa) and np.array_equal(rk, want_rank)
+        path, bucket, sent = (tmp_path / f"stats{r}.txt").read_text().split()
+        assert path == "sharded" and int(sent) > 0
+        buckets.append(int(bucket))
+    assert sum(buckets) == text.size and min(buckets) > text.size // 4   # balanced by the splitters
+
+
+def test_bounds_are_balanced_and_monotone():
+    sys.path.insert(0, str(ROOT))
+    from paper_1404_3456_b200.sharded import choose_bounds
+    rng = np.random.default_rng(5)
+    hist = torch.from_numpy(rng.integers(0, 50, 1 << 16))
+    for G in (2, 3, 4, 8):
+        b = choose_bounds(hist, G)
+        assert b.numel() == G - 1 and bool(torch.all(b[1:] >= b[:-1]))
+        edges = [0] + [int(x) for x in b] + [1 << 16]
+        loads = [int(hist[edges[g]:edges[g + 1]].sum()) for g in range(G)]
+        assert max(loads) - min(loads) <= 2 * 50 + int(hist.sum()) // (50 * G)
+    skew = torch.zeros(1 << 16, dtype=torch.int64)
+    skew[7] = 1000                       # everything in one prefix: one rank takes it all, no crash
+    b = choose_bounds(skew, 4)
+    assert bool(torch.all(b[1:] >= b[:-1]))
