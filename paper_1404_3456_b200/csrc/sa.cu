@@ -542,7 +542,7 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
                         break;
                     }
                 }
-                if (dist > kDistCap) dist = kNoDist;
+                if (dist > kDistCap || q + dist >= n_text) dist = kNoDist;
                 s_key[a] = (static_cast<u64>(dist) << kTextSlotBits) | static_cast<u32>(a);
             } else {
                 s_key[a] = text_key(packed, sent, n_text, q, static_cast<u32>(a));
@@ -574,16 +574,19 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
             const int dst = s_dst[u];
             const bool opens = (s_bits[dst >> 5] >> (dst & 31)) & 1u;  // slot dst starts the group
             if (shortcut) {
-                // verify: the predecessor in the new order must be a prefix of this suffix
+                // verify: this suffix must agree with the group's LONGEST member (last in the new
+                // order) on all of its own `dist` symbols.  Then every member is a prefix of every
+                // longer one, which is exactly what ordering by distance assumes.  The lanes of a
+                // warp mostly work on one group, so the reference's words are one broadcast load.
                 const u32 dist = static_cast<u32>(s_key[a] >> kTextSlotBits);
                 bool ok = dist != kNoDist;
-                if (ok && !opens) {
-                    const int pa = s_src[dst - 1];
-                    const u32 pd = static_cast<u32>(s_key[pa] >> kTextSlotBits);  // <= dist
-                    const u64 qa = static_cast<u64>(s_pos[a]) + depth, qp = static_cast<u64>(s_pos[pa]) + depth;
-                    for (u32 c0 = 0; c0 < pd && ok; c0 += 32) {
-                        const u32 len = pd - c0 < 32u ? pd - c0 : 32u;
-                        ok = ((base_window(packed, qa + c0) ^ base_window(packed, qp + c0)) >> (64 - 2 * len)) == 0;
+                const int ra = s_src[group_end(a) - 1];
+                if (static_cast<u32>(s_key[ra] >> kTextSlotBits) == kNoDist) ok = false;  // no usable reference
+                if (ok && ra != a) {
+                    const u64 qa = static_cast<u64>(s_pos[a]) + depth, qr = static_cast<u64>(s_pos[ra]) + depth;
+                    for (u32 c0 = 0; c0 < dist && ok; c0 += 32) {
+                        const u32 len = dist - c0 < 32u ? dist - c0 : 32u;
+                        ok = ((base_window(packed, qa + c0) ^ base_window(packed, qr + c0)) >> (64 - 2 * len)) == 0;
                     }
                 }
                 if (!ok) {
