@@ -302,8 +302,8 @@ def main():
     model = {
         "pack_dna_kernel": 1.375, "initkey_dna_kernel": 8.375, "initkey_bytes_kernel": 9.0,
         "onesweep_u32_pairs": 16.0, "onesweep_u32_keys": 8.0, "onesweep_u64_pairs": 24.0,
-        "headbits_kernel": 4.03, "refine_text_kernel": float(R16 * (44 + 24 * P)),
-        "onesweep_u32_partition": 14.0, "window_scatter_kernel": 12.0, "scatter_pairs_kernel": 12.0,
+        "init_elems_kernel": 8.375, "onesweep_u64_keys": 16.0, "onesweep_u64_pack_iota": 12.0,
+        "refine_elems_kernel": 13.4, "window_scatter_kernel": 12.0, "scatter_records_kernel": 12.0,
         "inverse_kernel": 8.0, "pair_key_kernel": 20.0, "rerank_kernel": 16.0, "hist_kernel": 4.0,
     }
     ncu_traffic = {"refine_text_kernel": 1.259e9}  # dram read+write per launch, profiles/r1_ncu_refine.txt

@@ -150,9 +150,10 @@ int reseq_cuda_build_sa_device(reseq_cuda_ctx* ctx, const uint8_t* d_text, size_
 
 /* ---- multi-GPU building blocks (one process per GPU; see paper_1404_3456_b200/sharded.py) ----
  * A sample-sort partitioned build of the same suffix array: the text is replicated on every
- * rank, each rank keys a slice of positions (shard_keys), the (key, position) records are
- * exchanged by splitter range (NCCL all-to-all, done by the caller), and each rank finishes its
- * bucket (shard_finish).  The concatenation of the buckets in splitter order is the array
+ * rank, each rank makes the 64-bit records of a slice of positions (shard_records:
+ * key24 << 40 | terminator byte << 32 | position, key24 = the first 12 bases), the records are
+ * exchanged by splitter range on the key's top 16 bits (NCCL all-to-all, done by the caller), and
+ * each rank finishes its bucket (shard_finish).  The concatenation of the buckets in splitter order is the array
  * reseq_cuda_build_sa returns.  Only the 2-bit DNA path shards (a text with other bytes is
  * built replicated).  shard_finish reports `unfinished` > 0 when a group exceeded the refine
  * kernel's window; the caller then falls back to the replicated single-device build. */
@@ -160,13 +161,13 @@ typedef struct reseq_cuda_sa_shard reseq_cuda_sa_shard;
 int reseq_cuda_sa_shard_create(reseq_cuda_ctx* ctx, const uint8_t* d_text, size_t n,
                                reseq_cuda_sa_shard** out, int* is_dna /* nullable */);
 void reseq_cuda_sa_shard_destroy(reseq_cuda_sa_shard* shard);
-/* d_keys[i], d_pos[i] = initial 31-bit key and position of suffix pos_begin + i, i < count. */
-int reseq_cuda_sa_shard_keys(reseq_cuda_sa_shard* shard, uint64_t pos_begin, size_t count,
-                             uint32_t* d_keys, uint32_t* d_pos);
-/* Sorts (stable, by key; both input arrays are clobbered) and refines a bucket of m records
+/* d_records[i] = record of suffix pos_begin + i, i < count. */
+int reseq_cuda_sa_shard_records(reseq_cuda_sa_shard* shard, uint64_t pos_begin, size_t count,
+                                uint64_t* d_records);
+/* Sorts (stable, by key24; the input array is clobbered) and refines a bucket of m records
  * that arrive in ascending position order within equal keys; d_sa_out receives the m suffix
  * positions in suffix order. */
-int reseq_cuda_sa_shard_finish(reseq_cuda_sa_shard* shard, uint32_t* d_keys, uint32_t* d_pos, size_t m,
+int reseq_cuda_sa_shard_finish(reseq_cuda_sa_shard* shard, uint64_t* d_records, size_t m,
                                uint32_t* d_sa_out, uint64_t* unfinished);
 /* d_rank[d_sa[i]] = i (suffix_array.hpp:118-122). */
 int reseq_cuda_inverse_device(reseq_cuda_ctx* ctx, const uint32_t* d_sa, size_t n, uint32_t* d_rank);

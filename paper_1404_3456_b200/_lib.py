@@ -97,8 +97,8 @@ SIGNATURES = {
     "reseq_cuda_build_sa_device": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp, C.POINTER(SaStats)]),
     "reseq_cuda_sa_shard_create": (C.c_int, [_vp, _vp, C.c_size_t, C.POINTER(_vp), C.POINTER(C.c_int)]),
     "reseq_cuda_sa_shard_destroy": (None, [_vp]),
-    "reseq_cuda_sa_shard_keys": (C.c_int, [_vp, C.c_uint64, C.c_size_t, _vp, _vp]),
-    "reseq_cuda_sa_shard_finish": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _u64p]),
+    "reseq_cuda_sa_shard_records": (C.c_int, [_vp, C.c_uint64, C.c_size_t, _vp]),
+    "reseq_cuda_sa_shard_finish": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _u64p]),
     "reseq_cuda_inverse_device": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
     "reseq_cuda_checksum_u32_device": (C.c_int, [_vp, _vp, C.c_size_t, _u64p]),
     "reseq_cuda_index_create": (C.c_int, [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(_vp)]),

@@ -25,7 +25,7 @@ digit_base_kernel(const u32* __restrict__ g_hist, u32* __restrict__ g_base) {
 template <> struct SortTuning<u32, false> { static constexpr int kBlock = 256, kItems = 16; };
 template <> struct SortTuning<u32, true>  { static constexpr int kBlock = 384, kItems = 12; };
 template <> struct SortTuning<u64, true>  { static constexpr int kBlock = 256, kItems = 16; };
-template <> struct SortTuning<u64, false> { static constexpr int kBlock = 256, kItems = 16; };
+template <> struct SortTuning<u64, false> { static constexpr int kBlock = 384, kItems = 12; };
 
 // The smallest tile among the tunings bounds the look-back array.
 static constexpr size_t kMinTile = 256 * 8;
@@ -49,45 +49,70 @@ int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws) {
     return RESEQ_OK;
 }
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS>
-static int launch_pass_cfg(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u32* vin, u32* vout,
-                           size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket) {
+template <typename KeyT, bool HAS_VAL, int LOAD>
+static const char* pass_name() {
+    if (LOAD == kLoadPackIota) return "onesweep_u64_pack_iota";
+    return sizeof(KeyT) == 8 ? (HAS_VAL ? "onesweep_u64_pairs" : "onesweep_u64_keys")
+                             : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys");
+}
+
+// Only the look-back words of the tiles a pass really has need clearing.
+template <int TILE>
+static size_t lookback_bytes_for(size_t n) {
+    return sizeof(u64) * ((n + TILE - 1) / TILE) * kRadix;
+}
+
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, int LOAD, bool HI>
+static int launch_pass_kernel(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
+                              size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket) {
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
-    auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS>;
+    auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, LOAD, HI>;
     static bool configured = false;
     if (!configured) {
         RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Cfg::kSmem)));
         configured = true;
     }
+    RSQ_CUDA(cudaMemsetAsync(lookback, 0, lookback_bytes_for<Cfg::kTile>(n), ctx->stream));
     const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
-    RSQ_LAUNCH_BEGIN(ctx, sizeof(KeyT) == 8 ? (HAS_VAL ? "onesweep_u64_pairs" : "onesweep_u64_keys")
-                                           : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys"));
+    RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL, LOAD>()));
     kern<<<static_cast<unsigned>(tiles), BLOCK, Cfg::kSmem, ctx->stream>>>(
-        kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
 }
 
-template <typename KeyT, bool HAS_VAL>
-static int launch_pass(reseq_cuda_ctx* ctx, const KeyT* kin, KeyT* kout, const u32* vin, u32* vout,
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, int LOAD>
+static int launch_pass_cfg(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
+                           size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket) {
+    if constexpr (sizeof(KeyT) == 8) {
+        if (shift >= 32)
+            return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, LOAD, true>(ctx, kin, kout, vin, vout, n, shift, mask,
+                                                                               base, lookback, ticket);
+    }
+    return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, LOAD, false>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+                                                                        lookback, ticket);
+}
+
+template <typename KeyT, bool HAS_VAL, int LOAD = kLoadPlain>
+static int launch_pass(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
                        size_t n, int shift, u32 mask, const u32* base, u64* lookback,
                        u32* ticket) {
     // "sort_cfg" picks a tile shape (tuning knob; every shape gives the same result)
     switch (ctx->opt_sort_cfg) {
-        case 1: return launch_pass_cfg<KeyT, HAS_VAL, 512, 8>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 2: return launch_pass_cfg<KeyT, HAS_VAL, 512, 12>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 3: return launch_pass_cfg<KeyT, HAS_VAL, 256, 12>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 4: return launch_pass_cfg<KeyT, HAS_VAL, 256, 8>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 5: return launch_pass_cfg<KeyT, HAS_VAL, 384, 12>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 6: return launch_pass_cfg<KeyT, HAS_VAL, 1024, 4>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 7: return launch_pass_cfg<KeyT, HAS_VAL, 512, 16>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 1: return launch_pass_cfg<KeyT, HAS_VAL, 512, 8, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 2: return launch_pass_cfg<KeyT, HAS_VAL, 512, 12, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 3: return launch_pass_cfg<KeyT, HAS_VAL, 256, 12, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 4: return launch_pass_cfg<KeyT, HAS_VAL, 256, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 5: return launch_pass_cfg<KeyT, HAS_VAL, 384, 12, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 6: return launch_pass_cfg<KeyT, HAS_VAL, 384, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 7: return launch_pass_cfg<KeyT, HAS_VAL, 512, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
         default: break;
     }
     using T = SortTuning<KeyT, HAS_VAL>;
-    return launch_pass_cfg<KeyT, HAS_VAL, T::kBlock, T::kItems>(ctx, kin, kout, vin, vout, n, shift, mask, base,
-                                                               lookback, ticket);
+    return launch_pass_cfg<KeyT, HAS_VAL, T::kBlock, T::kItems, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+                                                                     lookback, ticket);
 }
 
 template <typename KeyT>
@@ -121,7 +146,6 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
     bool flipped = false;
     for (int p = 0; p < pt.count; ++p) {
         if (skip_mask & (1u << p)) continue;
-        RSQ_CUDA(cudaMemsetAsync(ws.lookback, 0, ws.lookback_bytes, ctx->stream));
         if (has_val)
             RSQ_TRY((launch_pass<KeyT, true>(ctx, kin, kout, vin, vout, n, pt.shift[p], pt.mask(p),
                                              ws.base + p * kRadix, ws.lookback, ws.tickets + p)));
@@ -137,41 +161,28 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
     return RESEQ_OK;
 }
 
-template <bool IOTA>
-static int partition_impl(reseq_cuda_ctx* ctx, const u32* keys, const u32* vals, u32* keys_out, u32* vals_out,
-                          size_t n, int shift, int bits, const SortWorkspace& ws) {
+template <int LOAD>
+static int partition_impl(reseq_cuda_ctx* ctx, const void* in, u64* out, size_t n, int shift, int bits,
+                          const SortWorkspace& ws) {
     if (n == 0) return RESEQ_OK;
-    using T = SortTuning<u32, true>;
-    using Cfg = OnesweepCfg<u32, true, T::kBlock, T::kItems>;
-    auto kern = onesweep_kernel<u32, true, T::kBlock, T::kItems, IOTA>;
-    static bool configured = false;
-    if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem)));
-        configured = true;
-    }
     RSQ_CUDA(cudaMemsetAsync(ws.tickets, 0, sizeof(u32) * kMaxPasses, ctx->stream));
-    RSQ_CUDA(cudaMemsetAsync(ws.lookback, 0, ws.lookback_bytes, ctx->stream));
     RSQ_LAUNCH_BEGIN(ctx, "digit_base_kernel");
     digit_base_kernel<<<1, kRadix, 0, ctx->stream>>>(ws.hist, ws.base);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
-    const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
-    RSQ_LAUNCH_BEGIN(ctx, "onesweep_u32_partition");
-    kern<<<static_cast<unsigned>(tiles), T::kBlock, Cfg::kSmem, ctx->stream>>>(
-        keys, keys_out, vals, vals_out, n, shift, (1u << bits) - 1u, ws.base, ws.lookback, ws.tickets);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_CUDA(cudaGetLastError());
-    return RESEQ_OK;
+    // the partition digit lives in the upper word of the record
+    return launch_pass<u64, false, LOAD>(ctx, in, out, nullptr, nullptr, n, 32 + shift, (1u << bits) - 1u, ws.base,
+                                         ws.lookback, ws.tickets);
 }
 
-int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out, u32* idx_out, size_t n,
-                            int shift, int bits, const SortWorkspace& ws) {
-    return partition_impl<true>(ctx, keys, nullptr, keys_out, idx_out, n, shift, bits, ws);
+int onesweep_partition_pack_iota(reseq_cuda_ctx* ctx, const u32* v, u64* out, size_t n, int shift, int bits,
+                                 const SortWorkspace& ws) {
+    return partition_impl<kLoadPackIota>(ctx, v, out, n, shift, bits, ws);
 }
 
-int onesweep_partition_pairs(reseq_cuda_ctx* ctx, const u32* keys, const u32* vals, u32* keys_out, u32* vals_out,
-                             size_t n, int shift, int bits, const SortWorkspace& ws) {
-    return partition_impl<false>(ctx, keys, vals, keys_out, vals_out, n, shift, bits, ws);
+int onesweep_partition_packed(reseq_cuda_ctx* ctx, const u64* in, u64* out, size_t n, int shift, int bits,
+                              const SortWorkspace& ws) {
+    return partition_impl<kLoadPlain>(ctx, in, out, n, shift, bits, ws);
 }
 
 template int onesweep_sort<u32>(reseq_cuda_ctx*, u32*, u32*, u32*, u32*, size_t, const PassTable&,

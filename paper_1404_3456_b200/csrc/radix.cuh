@@ -94,20 +94,46 @@ hist_kernel(const KeyT* __restrict__ keys, u64 n, PassTable pt, u32* __restrict_
 
 // ---- one digit pass -----------------------------------------------------------------
 
-// Lanes of the warp holding the same digit.  Built from one ballot per digit bit: on
-// sm_100a eight VOTE + LOP3 pairs sustain a far higher rate than one MATCH.ANY, whose issue
-// rate (not latency) capped the ranking loop at ~1.5 TB/s of key traffic (ncu: the BREV
-// consuming the match result held 38 % of the stall samples, profiles/r1_onesweep_match.txt).
-__device__ __forceinline__ unsigned warp_match_digit(u32 d, u32 mask) {
+// Lanes of the warp holding the same 8-bit digit, from one ballot per digit bit.  On sm_100a a
+// pass is bound by issue slots and shared-memory wavefronts, not by HBM (ncu, profiles/
+// r1c_ncu_full_onesweep_kernel.txt: ALU pipe 49 %, LSU wavefronts 54 %, DRAM 22 %), so the
+// match is written to cost 4 instructions per bit (LOP3 -> predicate, VOTE, predicated NOT, AND)
+// instead of the 7.6 per bit the C++ form compiled to; MATCH.ANY is slower still (its issue rate
+// capped the ranking loop at 1.5 TB/s of key traffic).  Digit bits above a narrow pass's width
+// are zero in every lane, so their ballots leave `peers` unchanged: all passes run 8 ballots.
+__device__ __forceinline__ unsigned warp_match_digit(u32 d) {
     unsigned peers = 0xffffffffu;
 #pragma unroll
     for (int b = 0; b < kRadixBits; ++b) {
-        if ((mask >> b) & 1u) {  // warp-uniform: the last pass of a key may be narrower
-            const unsigned vote = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            peers &= ((d >> b) & 1u) ? vote : ~vote;
-        }
+        unsigned m;
+        asm volatile(
+            "{\n\t"
+            ".reg .pred p;\n\t"
+            ".reg .b32 t;\n\t"
+            "and.b32 t, %1, %2;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+            "@!p not.b32 %0, %0;\n\t"
+            "}"
+            : "=r"(m)
+            : "r"(d), "r"(1u << b));
+        peers &= m;
     }
     return peers;
+}
+
+// How a pass reads its input.
+enum : int {
+    kLoadPlain = 0,     // keys_in[i] (and vals_in[i])
+    kLoadPackIota = 1,  // u64 keys only: keys_in is a u32 array v; element i is (v[i] << 32) | i
+};
+
+// Digit of a key.  HI (u64 keys, shift >= 32): the digit lies in the upper word, one 32-bit
+// shift instead of a 64-bit funnel sequence -- the digit is extracted four times per item.
+template <bool HI, typename KeyT>
+__device__ __forceinline__ u32 pass_digit(KeyT k, int shift, u32 mask) {
+    if constexpr (HI) return (static_cast<u32>(static_cast<u64>(k) >> 32) >> shift) & mask;  // shift is already -32
+    else return static_cast<u32>(k >> shift) & mask;
 }
 
 template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS>
@@ -115,17 +141,17 @@ struct OnesweepCfg {
     static constexpr int kWarps = BLOCK / 32;
     static constexpr int kTile = BLOCK * ITEMS;
     static constexpr size_t kSmem = sizeof(KeyT) * kTile + (HAS_VAL ? sizeof(u32) * kTile : 0) +
-                                    sizeof(u32) * (kWarps * kRadix + 2 * kRadix + 32 + 4);
+                                    sizeof(u32) * (kWarps * kRadix + kRadix + 32 + 4);
 };
 
-// IOTA_VAL: the payload of element i is i itself (no payload array is read).
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, bool IOTA_VAL = false>
-__global__ void __launch_bounds__(BLOCK)
-onesweep_kernel(const KeyT* __restrict__ keys_in, KeyT* __restrict__ keys_out,
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, int LOAD = kLoadPlain, bool HI = false>
+__global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? 4 : (BLOCK <= 384 ? 3 : (BLOCK <= 512 ? 2 : 1))))
+onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,
                 u32 mask, const u32* __restrict__ digit_base, u64* __restrict__ lookback,
                 u32* __restrict__ ticket) {
     static_assert(BLOCK >= kRadix && BLOCK % 32 == 0, "one thread per digit is assumed");
+    static_assert(LOAD == kLoadPlain || (sizeof(KeyT) == 8 && !HAS_VAL), "pack-iota feeds u64 keys only");
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
     constexpr int WARPS = Cfg::kWarps;
     constexpr int TILE = Cfg::kTile;
@@ -133,9 +159,8 @@ onesweep_kernel(const KeyT* __restrict__ keys_in, KeyT* __restrict__ keys_out,
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KeyT* s_keys = reinterpret_cast<KeyT*>(smem_raw);
     u32* s_vals = reinterpret_cast<u32*>(s_keys + TILE);
-    u32* s_whist = s_vals + (HAS_VAL ? TILE : 0);  // [WARPS][256] counts -> warp offsets
-    u32* s_binstart = s_whist + WARPS * kRadix;    // [256] first tile slot of each digit
-    u32* s_gofs = s_binstart + kRadix;             // [256] global index of slot 0 of digit
+    u32* s_whist = s_vals + (HAS_VAL ? TILE : 0);  // [WARPS][256] counts -> tile slot of the warp's run
+    u32* s_gofs = s_whist + WARPS * kRadix;        // [256] global index of tile slot 0 of the digit
     u32* s_scan = s_gofs + kRadix;                 // [32] warp totals for the digit scan
     u32* s_tile = s_scan + 32;
 
@@ -144,76 +169,84 @@ onesweep_kernel(const KeyT* __restrict__ keys_in, KeyT* __restrict__ keys_out,
     const unsigned lane = lane_id();
 
     if (tid == 0) *s_tile = atomicAdd(ticket, 1u);
-    for (int i = tid; i < WARPS * kRadix; i += BLOCK) s_whist[i] = 0;
+    {
+        uint4* z = reinterpret_cast<uint4*>(s_whist);
+        for (int i = tid; i < WARPS * kRadix / 4; i += BLOCK) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
     __syncthreads();
     const u32 tile = *s_tile;
     const u64 tile_base = static_cast<u64>(tile) * TILE;
     const u32 valid = static_cast<u32>(n - tile_base < static_cast<u64>(TILE) ? n - tile_base : TILE);
+    const bool full = valid == TILE;
 
     // -- load: warp-striped, so that (warp, step, lane) order == memory order ---------
     KeyT key[ITEMS];
     u32 val[ITEMS];
     const u32 wbase = warp * (ITEMS * 32) + lane;
-    if (valid == TILE) {
+    auto load_key = [&](u64 i) -> KeyT {
+        if constexpr (LOAD == kLoadPackIota)
+            return static_cast<KeyT>((static_cast<u64>(static_cast<const u32*>(keys_in_raw)[i]) << 32) | (i & 0xffffffffu));
+        else
+            return static_cast<const KeyT*>(keys_in_raw)[i];
+    };
+    if (full) {
 #pragma unroll
-        for (int j = 0; j < ITEMS; ++j) key[j] = keys_in[tile_base + wbase + j * 32];
+        for (int j = 0; j < ITEMS; ++j) key[j] = load_key(tile_base + wbase + j * 32);
         if (HAS_VAL) {
 #pragma unroll
-            for (int j = 0; j < ITEMS; ++j)
-                val[j] = IOTA_VAL ? static_cast<u32>(tile_base + wbase + j * 32) : vals_in[tile_base + wbase + j * 32];
+            for (int j = 0; j < ITEMS; ++j) val[j] = vals_in[tile_base + wbase + j * 32];
         }
     } else {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
             const u32 li = wbase + j * 32;
-            key[j] = li < valid ? keys_in[tile_base + li] : ~KeyT(0);  // pads rank last
-            if (HAS_VAL) val[j] = li < valid ? (IOTA_VAL ? static_cast<u32>(tile_base + li) : vals_in[tile_base + li]) : 0u;
+            key[j] = li < valid ? load_key(tile_base + li) : ~KeyT(0);  // pads rank last
+            if (HAS_VAL) val[j] = li < valid ? vals_in[tile_base + li] : 0u;
         }
     }
 
-    // -- rank inside the warp: match.any groups equal digits; the lowest lane of each group
-    //    bumps the warp's private counter once for the whole group.  The bump is a shared
+    // -- rank inside the warp: equal digits are grouped by the ballots; the lowest lane of each
+    //    group bumps the warp's private counter once for the whole group.  The bump is a shared
     //    atomicAdd whose old value is consumed only after a batch of them has been issued:
     //    successive steps of one warp are then independent instructions in flight instead of
-    //    a load -> add -> store chain that exposes the shared-memory latency 16 times. --------
+    //    a load -> add -> store chain that exposes the shared-memory latency ITEMS times. ------
     u32* wh = s_whist + warp * kRadix;
-    unsigned short rnk[ITEMS];
+    static_assert(ITEMS % 2 == 0, "ranks are kept two to a register");
+    u32 rnk2[ITEMS / 2];  // two 16-bit ranks per register: the live key/payload registers leave little room
     const unsigned lt = lanemask_lt();
-    constexpr int kBatch = ITEMS % 8 == 0 ? 8 : (ITEMS % 4 == 0 ? 4 : 1);
+    constexpr int kBatch = ITEMS % 8 == 0 ? 8 : (ITEMS % 4 == 0 ? 4 : (ITEMS % 3 == 0 ? 3 : 1));
 #pragma unroll
     for (int j0 = 0; j0 < ITEMS; j0 += kBatch) {
         unsigned peers[kBatch];
         u32 base[kBatch];
 #pragma unroll
-        for (int b = 0; b < kBatch; ++b)
-            peers[b] = warp_match_digit(key_digit(key[j0 + b], shift, mask), mask);
+        for (int b = 0; b < kBatch; ++b) peers[b] = warp_match_digit(pass_digit<HI>(key[j0 + b], shift, mask));
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             base[b] = 0;
             if ((peers[b] & lt) == 0)  // lowest lane of its group
-                base[b] = atomicAdd(wh + key_digit(key[j0 + b], shift, mask), __popc(peers[b]));
+                base[b] = atomicAdd(wh + pass_digit<HI>(key[j0 + b], shift, mask), __popc(peers[b]));
         }
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             const u32 first = __shfl_sync(0xffffffffu, base[b], __ffs(peers[b]) - 1);
-            rnk[j0 + b] = static_cast<unsigned short>(first + __popc(peers[b] & lt));
+            const u32 r = first + __popc(peers[b] & lt);
+            if (((j0 + b) & 1) == 0) rnk2[(j0 + b) >> 1] = r;
+            else rnk2[(j0 + b) >> 1] |= r << 16;
         }
     }
     __syncthreads();
 
-    // -- per digit: offsets of each warp inside the digit's run, tile total -----------
+    // -- per digit: tile total, published at once as this tile's aggregate --------------
     u32 total = 0;
     if (tid < kRadix) {
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) {
-            const u32 c = s_whist[w * kRadix + tid];
-            s_whist[w * kRadix + tid] = total;
-            total += c;
-        }
+        for (int w = 0; w < WARPS; ++w) total += s_whist[w * kRadix + tid];
         if (tile > 0) st_relaxed_u64(lookback + static_cast<u64>(tile) * kRadix + tid, kDescAggregate | total);
     }
 
-    // -- exclusive scan of the 256 totals -> first slot of every digit in the tile ----
+    // -- exclusive scan of the 256 totals -> first tile slot of every digit; each warp's counter
+    //    becomes the tile slot where its run of the digit starts ---------------------------------
     u32 inc = total;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -222,13 +255,33 @@ onesweep_kernel(const KeyT* __restrict__ keys_in, KeyT* __restrict__ keys_out,
     }
     if (lane == 31) s_scan[warp] = inc;
     __syncthreads();
+    u32 bin_start = 0;
     if (tid < kRadix) {
         u32 add = 0;
-        for (int w = 0; w < warp; ++w) add += s_scan[w];
-        const u32 bin_start = add + inc - total;
-        s_binstart[tid] = bin_start;
+#pragma unroll
+        for (int w = 0; w < kRadix / 32; ++w) add += w < warp ? s_scan[w] : 0u;
+        bin_start = add + inc - total;
+        u32 run = bin_start;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+            const u32 c = s_whist[w * kRadix + tid];
+            s_whist[w * kRadix + tid] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
 
-        // -- decoupled look-back over earlier tiles for this digit ---------------------
+    // -- exchange through shared memory: the tile becomes digit-sorted ----------------
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const u32 pos = wh[pass_digit<HI>(key[j], shift, mask)] + ((j & 1) ? rnk2[j >> 1] >> 16 : rnk2[j >> 1] & 0xffffu);
+        s_keys[pos] = key[j];
+        if (HAS_VAL) s_vals[pos] = val[j];
+    }
+
+    // -- decoupled look-back over earlier tiles, one thread per digit.  It runs after the exchange
+    //    so that the predecessors have had the time of this tile's exchange to publish. ----------
+    if (tid < kRadix) {
         u32 excl = 0;
         if (tile > 0) {
             long long t = static_cast<long long>(tile) - 1;
@@ -245,25 +298,26 @@ onesweep_kernel(const KeyT* __restrict__ keys_in, KeyT* __restrict__ keys_out,
     }
     __syncthreads();
 
-    // -- exchange through shared memory: the tile becomes digit-sorted ----------------
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const u32 d = key_digit(key[j], shift, mask);
-        const u32 pos = s_binstart[d] + wh[d] + rnk[j];
-        s_keys[pos] = key[j];
-        if (HAS_VAL) s_vals[pos] = val[j];
-    }
-    __syncthreads();
-
     // -- coalesced scatter: consecutive slots of one digit go to consecutive addresses -
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const u32 i = tid + j * BLOCK;
-        if (i < valid) {
+        for (int j = 0; j < ITEMS; ++j) {
+            const u32 i = tid + j * BLOCK;
             const KeyT k = s_keys[i];
-            const u32 dst = s_gofs[key_digit(k, shift, mask)] + i;
+            const u32 dst = s_gofs[pass_digit<HI>(k, shift, mask)] + i;
             keys_out[dst] = k;
             if (HAS_VAL) vals_out[dst] = s_vals[i];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const u32 i = tid + j * BLOCK;
+            if (i < valid) {
+                const KeyT k = s_keys[i];
+                const u32 dst = s_gofs[pass_digit<HI>(k, shift, mask)] + i;
+                keys_out[dst] = k;
+                if (HAS_VAL) vals_out[dst] = s_vals[i];
+            }
         }
     }
 }
@@ -294,12 +348,13 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
                   size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
                   u32 skip_mask, bool* in_b);
 
-// One stable partition pass of (keys[i], i) on key bits [shift, shift + bits): keys_out /
-// idx_out receive the pairs grouped by digit.  ws.hist[0..255] must hold the digit counts.
-int onesweep_partition_iota(reseq_cuda_ctx* ctx, const u32* keys, u32* keys_out, u32* idx_out, size_t n,
-                            int shift, int bits, const SortWorkspace& ws);
-// The same for explicit (key, payload) pairs.
-int onesweep_partition_pairs(reseq_cuda_ctx* ctx, const u32* keys, const u32* vals, u32* keys_out, u32* vals_out,
-                             size_t n, int shift, int bits, const SortWorkspace& ws);
+// One stable partition pass producing (value, index) records: element i of the input is the
+// u64 (v[i] << 32) | i, partitioned on bits [shift, shift + bits) of v.  ws.hist[0..255] must
+// hold the digit counts.
+int onesweep_partition_pack_iota(reseq_cuda_ctx* ctx, const u32* v, u64* out, size_t n, int shift, int bits,
+                                 const SortWorkspace& ws);
+// The same for records already packed as (v << 32) | payload.
+int onesweep_partition_packed(reseq_cuda_ctx* ctx, const u64* in, u64* out, size_t n, int shift, int bits,
+                              const SortWorkspace& ws);
 
 }  // namespace rsq

@@ -32,6 +32,7 @@
 #include "sa.cuh"
 #include "scan.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace rsq {
@@ -198,7 +199,7 @@ constexpr int kRankBlock = 256;
 constexpr int kRankItems = 8;
 constexpr int kRankTile = kRankBlock * kRankItems;
 
-template <typename KeyT, bool FLAGS_ONLY>
+template <typename KeyT>
 __global__ void __launch_bounds__(kRankBlock)
 rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, u32 uniq_mask,
               u32 uniq_full, u32* __restrict__ rank, u32* __restrict__ head_of,
@@ -231,10 +232,8 @@ rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, 
 #pragma unroll
     for (int j = 0; j < kRankItems; ++j) {
         const u64 idx = base + j;
-        // FLAGS_ONLY: the "keys" are 0/1 head flags expanded from a head bitmap
-        const bool head = idx < n && (FLAGS_ONLY ? (idx == 0 || k[j] != KeyT(0))
-                                                 : (idx == 0 || k[j] != prev ||
-                                                    (static_cast<u32>(k[j]) & uniq_mask) != uniq_full));
+        const bool head = idx < n && (idx == 0 || k[j] != prev ||
+                                      (static_cast<u32>(k[j]) & uniq_mask) != uniq_full);
         prev = k[j];
         heads += head;
         if (head) run = static_cast<u32>(idx) + 1u;
@@ -304,38 +303,117 @@ rerank_kernel(const KeyT* __restrict__ keys, const u32* __restrict__ sa, u64 n, 
     }
 }
 
-// ---- group refinement from L2-resident text windows ----------------------------------
+// ---- DNA fast path: sort records, refine groups from L2-resident text --------------------
 //
-// After the initial sort the suffixes are grouped by their first `depth` symbols; groups
-// are contiguous in sa and delimited by a head bitmap (bit idx set <=> sa[idx] starts a
-// group).  On B200 the 2-bit packed text (n/4 bytes: 35 MB at 4.6 Mbp x 30) fits the 126 MB
-// L2 while the 4n-byte rank array does not, so the next 29 symbols of every still-tied
-// suffix are fetched straight from the packed text (an L2 hit) instead of through
-// rank[pos + h] (a DRAM sector per suffix, plus a DRAM read-modify-write per suffix to
-// scatter the new ranks).  Each CTA owns the groups that START inside its 2048-suffix tile,
-// stages them in shared memory, ranks every tied suffix inside its group by enumeration
-// (groups of a shotgun read set hold ~coverage suffixes), writes the refined order back in
-// place and ORs the new group heads into the next bitmap.  No global sort, no rank array.
+// One 64-bit record per suffix:   key24 << 40 | p8 << 32 | pos
+//   key24  three 8-bit sort digits.  Upper two: bases 0..7 (2 bits each, zero padded from the
+//          terminator on).  Low digit: 0x80 | bases 8..10 | upper bit of base 11 for a suffix
+//          with more than 8 symbols, and 2*t + kind (< 0x80) for a suffix that terminates after
+//          t <= 8 symbols (kind 0 = end of text, 1 = sentinel).  Zero padding alone would tie
+//          "b$" with "bA$", "bAA$" ... and with every suffix starting b AAAA...: the k empty
+//          suffixes of a k-read set would form ONE group.  With the escape bit those short
+//          suffixes sort before everything that shares their padded bases, by length, then (the
+//          sort is stable) by position -- which is their final order: they are finished by the
+//          sort alone.  What remains tied shares 11 symbols.
+//   p8     where the suffix terminates, measured once while the positions are still in text
+//          order (a streaming read of the sentinel bitmap):
+//            2*t + kind   terminator after t < 11 symbols
+//            t + 11       sentinel after 11 <= t <= 242 symbols
+//            254          sentinel farther away / not determined: the refine kernel scans for it
+//            255          the text ends first (no sentinel at all behind the suffix)
+//   pos    text position.
+// Three onesweep passes on key24 (the records move as single 64-bit elements: half the load /
+// store / exchange instructions of separate key and payload arrays) leave the suffixes grouped
+// by key with positions ascending inside a group.
+//
+// After the sort a group holds suffixes that agree on their first 11 symbols (with zero
+// padding: a suffix terminating after 9 or 10 symbols joins the group of its padded bases).  On B200 the
+// 2-bit packed text (n/4 bytes: 35 MB at 4.6 Mbp x 30) fits the 126 MB L2 while the 4n-byte rank
+// array of a doubling round does not, so the order inside a group is settled from the text
+// itself.  Each CTA owns the groups that START inside its 2048-suffix tile, stages them in
+// shared memory, finishes them there and writes the suffix array tile once.  No global sort, no
+// rank array, no scatter.
 //
 // A group that does not fit the CTA's shared-memory window (more than kRefExt suffixes past
-// the tile) is left untouched and reported; the host then switches to the general
-// prefix-doubling rounds below, which have no size limit.
+// the tile) is reported; the host then rebuilds with the general prefix-doubling engine below,
+// which has no size limit.
+
+constexpr int kElemK = 11;                  // symbols every member of a group is known to share
+constexpr int kElemEsc = 8;                 // suffixes terminating after <= 8 symbols are finished by the sort
+constexpr u32 kElemEscBit = 0x80;
+constexpr int kElemKeyShift = 40;
+constexpr u32 kPShortEnd = 2 * kElemK;      // payloads below this: terminator inside the shared symbols
+constexpr u32 kPMaxNear = 253;              // largest payload that encodes a distance (242 + 11)
+constexpr u32 kPFar = 254;
+constexpr u32 kPEot = 255;
 
 constexpr int kRefBlock = 256;
 constexpr int kRefTile = 2048;
-constexpr int kRefExt = 1024;
+constexpr int kRefExt = 768;
 constexpr int kRefCap = kRefTile + kRefExt;
 constexpr int kRefWords = kRefCap / 32 + 2;
 constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 3 * sizeof(unsigned short) * kRefCap +
-                            sizeof(u32) * (4 * kRefWords + 16);
-constexpr int kTextK = 23;          // bases per refinement round
+                            kRefCap + sizeof(u32) * (4 * kRefWords + 16);
+constexpr int kTextK = 23;          // bases per text step
 constexpr int kTextFieldBits = 6;   // terminator field: 2*len + kind, 2*kTextK = "no terminator"
-constexpr u32 kDistCap = 4095;      // farthest sentinel the distance shortcut looks for
-constexpr int kTextSlotBits = 12;   // window slot of the suffix: makes every key of a round unique
+constexpr u32 kDistCap = 4095;      // farthest sentinel the bitmap scan looks for
+constexpr u32 kOrdNone = 0x1FFF;    // "no usable distance": sorts last, its group cannot use the shortcut
+constexpr int kTextSlotBits = 12;   // window slot of the suffix: makes every key of a step unique
 static_assert(kRefCap <= (1 << kTextSlotBits), "window slots must fit the key's slot field");
 static_assert(2 * kTextK + kTextFieldBits + kTextSlotBits == 64, "refinement key layout");
+static_assert(kDistCap + kElemK < kOrdNone, "order values must stay below the none marker");
 
-// Key of one round for the suffix in window slot `slot`: the next 23 symbols from `pos`
+// Records of the `count` suffixes starting at text position pos0 (the whole text: pos0 = 0,
+// count = n; a multi-GPU rank keys only its slice), plus the digit histograms of the three sort
+// passes.
+__global__ void __launch_bounds__(256)
+init_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n, u64 pos0, u64 count,
+                  u64* __restrict__ elems, u32* __restrict__ g_hist) {
+    __shared__ u32 s_hist[3 * kRadix];
+    for (int i = threadIdx.x; i < 3 * kRadix; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < count; idx += stride) {
+        const u64 pos = pos0 + idx;
+        const u32 bases = static_cast<u32>(base_window(packed, pos) >> 40);   // 12 bases
+        // distance to the first sentinel at or after pos, looking 256 positions ahead
+        u32 t = 256;
+#pragma unroll 1
+        for (u32 c0 = 0; c0 < 256; c0 += 64) {
+            const u64 w = sent_window(sent, pos + c0);
+            if (w) {
+                t = c0 + static_cast<u32>(__clzll(w));
+                break;
+            }
+        }
+        const u64 rem = n - pos;  // >= 1
+        u32 tt, kind;              // symbols before the terminator (256 = not within reach), its kind
+        if (t < 256 && t < rem) { tt = t; kind = 1; }
+        else if (rem <= 256) { tt = static_cast<u32>(rem); kind = 0; }
+        else { tt = 256; kind = 1; }
+        const u32 kept = tt >= 12 ? bases : bases & ~((1u << (24 - 2 * tt)) - 1u);   // zero padded
+        u32 key, p;
+        if (tt <= kElemEsc) {
+            key = ((kept >> 8) << 8) | (2 * tt + kind);
+            p = 2 * tt + kind;
+        } else {
+            const u32 b23 = kept >> 1;   // bases 0..10 and the upper bit of base 11
+            key = ((b23 >> 7) << 8) | kElemEscBit | (b23 & 0x7fu);
+            if (tt < kElemK) p = 2 * tt + kind;
+            else if (tt == 256) p = kPFar;
+            else if (kind == 0) p = kPEot;
+            else p = tt + kElemK <= kPMaxNear ? tt + kElemK : kPFar;
+        }
+        elems[idx] = (static_cast<u64>(key) << kElemKeyShift) | (static_cast<u64>(p) << 32) | (pos & 0xffffffffu);
+        atomicAdd(&s_hist[key & 0xffu], 1u);
+        atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
+        atomicAdd(&s_hist[2 * kRadix + (key >> 16)], 1u);
+    }
+    __syncthreads();
+    hist_flush(s_hist, g_hist, 3);
+}
+
+// Key of one text step for the suffix in window slot `slot`: the next 23 symbols from `pos`
 // (zero padded at a terminator) | terminator field | slot.  Keys of equal content keep
 // their slot order, so the order of the full 64-bit keys IS the stable refined order.
 __device__ __forceinline__ u64 text_key(const u64* __restrict__ packed, const u64* __restrict__ sent,
@@ -354,73 +432,94 @@ __device__ __forceinline__ u64 text_key(const u64* __restrict__ packed, const u6
     return (((kept << kTextFieldBits) | field) << kTextSlotBits) | slot;
 }
 
-// Head bitmap from the sorted initial keys: a suffix starts a group iff its key differs
-// from its left neighbour's or carries a terminator (unique by construction).
-__global__ void __launch_bounds__(256)
-headbits_kernel(const u32* __restrict__ keys, u64 n, u32 uniq_mask, u32 uniq_full,
-                u32* __restrict__ bits, u32* __restrict__ counters) {
-    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    const u64 rounds = (n + stride - 1) / stride;
-    u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
-    u32 nonheads = 0;
-    for (u64 r = 0; r < rounds; ++r, idx += stride) {
-        const bool in = idx < n;
-        bool head = false;
-        if (in) {
-            const u32 k = keys[idx];
-            head = idx == 0 || k != keys[idx - 1] || (k & uniq_mask) != uniq_full;
-        }
-        const unsigned b = __ballot_sync(0xffffffffu, head);
-        const unsigned act = __ballot_sync(0xffffffffu, in);
-        if (lane_id() == 0 && act) {
-            bits[idx >> 5] = b;
-            nonheads += __popc(act & ~b);
-        }
-    }
-    if (nonheads) atomicAdd(counters, nonheads);
+// 128-bit load of two consecutive packed words (the pair index is even: 16-byte aligned).
+__device__ __forceinline__ void ld_words2(const u64* __restrict__ p, u64& w0, u64& w1) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    w0 = (static_cast<u64>(v.y) << 32) | v.x;
+    w1 = (static_cast<u64>(v.w) << 32) | v.z;
 }
 
-// One CTA refines every group that starts in its tile to completion: the key of a tied
-// suffix depends only on (position, depth), never on another group, so all rounds run
-// back to back in shared memory and the tile goes back to HBM once.  Every round first
-// compacts the still-tied suffixes into a dense list (order preserving, so a group stays
-// contiguous) -- late rounds, where few suffixes are tied, then cost in proportion to what
-// is left instead of dragging 32-wide warps through one or two live lanes.
+// One CTA finishes every group that starts in its tile: the key of a tied suffix depends only
+// on (position, depth), never on another group, so all steps run back to back in shared memory.
+//
+// Steps alternate, starting with a DISTANCE step.
+//   DISTANCE  In a read set the members of a group are reads over one locus: each is a prefix
+//             of the longer ones, so their order is (distance to the terminator, position).
+//             The members are ranked by that key, then every member is compared base by base,
+//             over its own remaining length, with the group's longest member (each member
+//             fetches its text as 128-bit words: the kernel is bound by L1 wavefronts, one per
+//             lane per gather, so fewer and wider gathers is what counts).  If all agree the
+//             group is final in ONE step.  If not (chance 12-mer repeats, mixed loci) the
+//             permutation is kept -- it is harmless: members that can still tie have equal
+//             distance and keep their position order -- and only the members that terminate
+//             inside the already-compared prefix become final.
+//   TEXT      what the distance step could not settle is split by the next 23 symbols
+//             (zero padded at a terminator | terminator field), fetched from the packed text.
+// Every step first compacts the still-tied suffixes into a dense list (order preserving, so a
+// group stays contiguous): late steps cost in proportion to what is left.
 __global__ void __launch_bounds__(kRefBlock)
-refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n_text,
-                   u32* __restrict__ sa, u64 n, const u32* __restrict__ bits_old, u32* __restrict__ bits_new,
-                   u32 depth, int max_rounds, bool use_shortcut, u32* __restrict__ counters) {
-    // n_text: length of the text the positions refer to; n: number of suffixes in sa (equal for
-    // a whole-text build, a bucket of it for a multi-GPU rank)
+refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n_text,
+                    const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
+                    int max_rounds, bool use_shortcut, u32* __restrict__ counters) {
+    // n_text: length of the text the positions refer to; m: number of records (equal for a
+    // whole-text build, a bucket of it for a multi-GPU rank)
     extern __shared__ __align__(16) unsigned char ref_smem[];
-    u64* s_key = reinterpret_cast<u64*>(ref_smem);               // [cap] keys of the round ...
+    u64* s_key = reinterpret_cast<u64*>(ref_smem);               // [cap] records, then keys of the step ...
     u32* s_pos2 = reinterpret_cast<u32*>(ref_smem);              // ... then the permuted positions
+    u8* s_p2 = reinterpret_cast<u8*>(s_pos2 + kRefCap);          // ... and their payloads
     u32* s_pos = reinterpret_cast<u32*>(s_key + kRefCap);        // [cap] suffix positions, sa order
     unsigned short* s_list = reinterpret_cast<unsigned short*>(s_pos + kRefCap);  // [cap] tied slots
     unsigned short* s_dst = s_list + kRefCap;                    // [cap] new slot of list entry u
     unsigned short* s_src = s_dst + kRefCap;                     // [cap] old slot of new slot d
-    u32* s_bits = reinterpret_cast<u32*>(s_src + kRefCap);       // [words] head bits of the window
-    u32* s_new = s_bits + kRefWords;                             // [words] heads created this round
-    u32* s_fail = s_new + kRefWords;                             // [words] groups the shortcut gave up on
+    u8* s_p = reinterpret_cast<u8*>(s_src + kRefCap);            // [cap] payload p8 of the suffix
+    u32* s_bits = reinterpret_cast<u32*>(s_p + kRefCap);         // [words] head bits of the window
+    u32* s_new = s_bits + kRefWords;                             // [words] heads created this step
+    u32* s_fail = s_new + kRefWords;                             // [words] groups the distance step gave up on
     u32* s_cnt = s_fail + kRefWords;                             // [words + 1] tied-count scan
     __shared__ int s_first, s_end, s_last;
 
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     const u64 t0 = static_cast<u64>(blockIdx.x) * kRefTile;
-    const u64 w0 = t0 >> 5;
-    const int lim = static_cast<int>(n - t0 < static_cast<u64>(kRefTile) ? n - t0 : kRefTile);
-    const u64 total_words = (n + 31) >> 5;
+    const int lim = static_cast<int>(m - t0 < static_cast<u64>(kRefTile) ? m - t0 : kRefTile);
+    const int avail = static_cast<int>(m - t0 < static_cast<u64>(kRefCap) ? m - t0 : kRefCap);  // records behind t0
 
     if (tid == 0) { s_first = 0x7fffffff; s_end = 0x7fffffff; s_last = -1; }
-    for (int j = tid; j < kRefWords; j += kRefBlock) {
-        s_bits[j] = w0 + j < total_words ? bits_old[w0 + j] : 0u;
-        s_new[j] = 0;
+    for (int j = tid; j < kRefWords; j += kRefBlock) { s_bits[j] = 0; s_new[j] = 0; }
+
+    // -- load the tile's records plus the first stretch behind it; group heads from adjacent keys.
+    //    The window grows only while the tile's last group has not ended (rare). ------------------
+    int loaded = 0;
+    const u32 prev_key = t0 > 0 ? static_cast<u32>(elems[t0 - 1] >> kElemKeyShift) : 0xffffffffu;
+    for (int want = lim + kRefBlock < avail ? lim + kRefBlock : avail;;) {
+        for (int j = loaded + tid; j < want; j += kRefBlock) s_key[j] = elems[t0 + j];
+        __syncthreads();
+        for (int j0 = loaded - (loaded & 31); j0 < want; j0 += kRefBlock) {   // word aligned
+            const int j = j0 + tid;
+            bool head = false;
+            if (j >= loaded && j < want) {
+                const u32 k = static_cast<u32>(s_key[j] >> kElemKeyShift);
+                const u32 kp = j > 0 ? static_cast<u32>(s_key[j - 1] >> kElemKeyShift) : prev_key;
+                head = k != kp || !(k & kElemEscBit) || (t0 == 0 && j == 0);   // no escape bit: finished by the sort
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, head);
+            if (lane == 0 && b) atomicOr(&s_bits[j >> 5], b);
+        }
+        loaded = want;
+        __syncthreads();
+        // position m acts as a head so that the last group has an end
+        if (tid == 0 && loaded == static_cast<int>(m - t0) && loaded < kRefWords * 32)
+            s_bits[loaded >> 5] |= 1u << (loaded & 31);
+        __syncthreads();
+        bool ended = false;  // is there a head at or behind slot lim?
+        for (int j = (lim >> 5) + tid; j < kRefWords; j += kRefBlock) {
+            u32 w = s_bits[j];
+            if (j == (lim >> 5)) w &= 0xffffffffu << (lim & 31);
+            ended |= w != 0;
+        }
+        if (__syncthreads_or(ended) || loaded >= avail) break;
+        want = loaded + kRefBlock < avail ? loaded + kRefBlock : avail;
     }
-    __syncthreads();
-    // position n acts as a head so that the last group has an end
-    if (tid == 0 && n - t0 < static_cast<u64>(kRefWords) * 32) s_bits[(n - t0) >> 5] |= 1u << ((n - t0) & 31);
-    __syncthreads();
 
     // first / last head inside the tile, first head at or after its end
     for (int j = tid; j < kRefWords; j += kRefBlock) {
@@ -439,11 +538,18 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
     const int first = s_first;
     if (first == 0x7fffffff) return;  // no group starts in this tile
     int end = s_end;
-    if (end > kRefCap) {              // the tile's last group overruns the window
+    if (end == 0x7fffffff) {          // the tile's last group overruns the window
         if (tid == 0) atomicOr(counters + 1, 1u);
-        end = s_last;                 // leave that group alone
+        end = s_last;                 // that group is nobody's: the host rebuilds
     }
-    if (end - first <= 1) return;
+
+    // unpack the records this CTA owns
+    for (int a = first + tid; a < end; a += kRefBlock) {
+        const u64 e = s_key[a];
+        s_pos[a] = static_cast<u32>(e);
+        s_p[a] = static_cast<u8>(e >> 32);
+    }
+    __syncthreads();
 
     // Tied slots of window word j, restricted to [first, end): slot a is tied unless it is a
     // head whose successor is a head too.
@@ -460,7 +566,6 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
 
     constexpr u32 kFieldMask = (1u << kTextFieldBits) - 1u;
     constexpr u32 kFull = 2 * kTextK;
-    constexpr u32 kNoDist = kDistCap + 1;  // "no sentinel within reach": the shortcut does not apply
 
     // group start of window slot a: the last head at or before it
     auto group_start = [&](int a) {
@@ -476,14 +581,13 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
         return w * 32 + __ffs(word) - 1;
     };
 
-    bool loaded = false;
+    u32 depth = kElemK;
     int rounds = 0;
-    // Steps alternate: a SHORTCUT step (below) on everything tied, then a TEXT step (the next
-    // 23 symbols) on what the shortcut could not settle.
     for (int step = 0;; ++step) {
-        const bool shortcut = use_shortcut && (step & 1) == 0;
-        if (!shortcut && rounds >= max_rounds) break;
-        if (!use_shortcut && (step & 1) == 0) continue;
+        const bool dstep = (step & 1) == 0;           // distance step
+        const bool verify = dstep && use_shortcut;    // without it the step only settles what terminates before `depth`
+        if (dstep && step > 0 && !use_shortcut) continue;
+        if (!dstep && rounds >= max_rounds) break;
 
         // -- compact the tied slots, in order ------------------------------------------------
         u32 tw = 0, c = 0;
@@ -516,36 +620,30 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
                 s_list[at++] = static_cast<unsigned short>(tid * 32 + b);
             }
         }
-        if (!loaded) {
-            for (int a = first + tid; a < end; a += kRefBlock) s_pos[a] = sa[t0 + a];
-            loaded = true;
-        }
         __syncthreads();
         const int cnt = static_cast<int>(total);
 
-        // -- keys.  TEXT: the next 23 symbols (an L2 hit).  SHORTCUT: the distance from the
-        //    current depth to the suffix's sentinel.  In a read set the members of a group are
-        //    reads over one locus: each is a prefix of the longer ones, so their order is
-        //    (distance, position) -- provided that really holds, which the verify pass below
-        //    checks base by base on neighbours in the new order (prefix-of is transitive along
-        //    the sorted chain).  A verified group is completely ordered in ONE step instead of
-        //    ceil(length / 23). ----------------------------------------------------------------
+        // -- keys ----------------------------------------------------------------------------------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
-            const u64 q = static_cast<u64>(s_pos[a]) + depth;
-            if (shortcut) {
-                u32 dist = kNoDist;
-                for (u32 c0 = 0; c0 <= kDistCap && q + c0 < n_text; c0 += 64) {
-                    const u64 w = sent_window(sent, q + c0);
-                    if (w) {
-                        dist = c0 + static_cast<u32>(__clzll(w));
-                        break;
+            if (dstep) {
+                u32 ord = s_p[a];
+                if (ord == kPEot) ord = kOrdNone;
+                else if (ord == kPFar) {     // scan the sentinel bitmap (long reads; rare)
+                    const u64 q = static_cast<u64>(s_pos[a]) + kElemK;   // no sentinel before that (p8 would say)
+                    u32 dist = kDistCap + 1;
+                    for (u32 c0 = 0; c0 <= kDistCap && q + c0 < n_text; c0 += 64) {
+                        const u64 w = sent_window(sent, q + c0);
+                        if (w) {
+                            dist = c0 + static_cast<u32>(__clzll(w));
+                            break;
+                        }
                     }
+                    ord = (dist + kElemK > kDistCap || q + dist >= n_text) ? kOrdNone : dist + 2 * kElemK;
                 }
-                if (dist > kDistCap || q + dist >= n_text) dist = kNoDist;
-                s_key[a] = (static_cast<u64>(dist) << kTextSlotBits) | static_cast<u32>(a);
+                s_key[a] = (static_cast<u64>(ord) << kTextSlotBits) | static_cast<u32>(a);
             } else {
-                s_key[a] = text_key(packed, sent, n_text, q, static_cast<u32>(a));
+                s_key[a] = text_key(packed, sent, n_text, static_cast<u64>(s_pos[a]) + depth, static_cast<u32>(a));
             }
         }
         __syncthreads();
@@ -568,34 +666,44 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
         }
         __syncthreads();
 
-        // -- new heads -------------------------------------------------------------------------
+        // -- distance step: compare with the group's longest member; text step: new heads ---------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
             const int dst = s_dst[u];
-            const bool opens = (s_bits[dst >> 5] >> (dst & 31)) & 1u;  // slot dst starts the group
-            if (shortcut) {
-                // verify: this suffix must agree with the group's LONGEST member (last in the new
-                // order) on all of its own `dist` symbols.  Then every member is a prefix of every
-                // longer one, which is exactly what ordering by distance assumes.  The lanes of a
-                // warp mostly work on one group, so the reference's words are one broadcast load.
-                const u32 dist = static_cast<u32>(s_key[a] >> kTextSlotBits);
-                bool ok = dist != kNoDist;
-                const int ra = s_src[group_end(a) - 1];
-                if (static_cast<u32>(s_key[ra] >> kTextSlotBits) == kNoDist) ok = false;  // no usable reference
-                if (ok && ra != a) {
-                    const u64 qa = static_cast<u64>(s_pos[a]) + depth, qr = static_cast<u64>(s_pos[ra]) + depth;
-                    for (u32 c0 = 0; c0 < dist && ok; c0 += 32) {
-                        const u32 len = dist - c0 < 32u ? dist - c0 : 32u;
-                        ok = ((base_window(packed, qa + c0) ^ base_window(packed, qr + c0)) >> (64 - 2 * len)) == 0;
+            if (dstep) {
+                if (!verify) continue;
+                const u32 ord = static_cast<u32>(s_key[a] >> kTextSlotBits);
+                const int ge = group_end(a);
+                const int ra = s_src[ge - 1];     // last in the new order: the longest member
+                bool ok = ord != kOrdNone && static_cast<u32>(s_key[ra] >> kTextSlotBits) != kOrdNone;
+                // symbols of this suffix still to be confirmed: [depth, tdist); tdist = ord - kElemK
+                if (ok && ra != a && ord > depth + kElemK) {
+                    const u64 qa = static_cast<u64>(s_pos[a]) + depth;
+                    const u64 qr = static_cast<u64>(s_pos[ra]) + depth;
+                    const u64 qe = qa + (ord - kElemK - depth);       // end of the stretch (exclusive)
+                    const u64 w_first = qa >> 5, w_last = (qe - 1) >> 5;
+                    for (u64 w = w_first & ~1ull; w <= w_last && ok; w += 2) {
+                        u64 own[2];
+                        ld_words2(packed + w, own[0], own[1]);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const u64 wb = (w + h) << 5;                 // first base of this word
+                            if (w + h < w_first || w + h > w_last) continue;
+                            const u64 lo = wb > qa ? wb : qa;
+                            const u64 hi = wb + 32 < qe ? wb + 32 : qe;
+                            const unsigned sh = static_cast<unsigned>(lo - wb) * 2;
+                            const unsigned nb = static_cast<unsigned>(hi - lo) * 2;   // 2..64 bits
+                            const u64 mine = own[h] << sh;
+                            const u64 theirs = base_window(packed, qr + (lo - qa));
+                            ok = ok && ((mine ^ theirs) >> (64 - nb)) == 0;
+                        }
                     }
                 }
-                if (!ok) {
-                    const int gs = group_start(a);
-                    atomicOr(&s_fail[gs >> 5], 1u << (gs & 31));
-                }
+                if (!ok) atomicOr(&s_fail[(ge - 1) >> 5], 1u << ((ge - 1) & 31));
             } else {
                 // a suffix starts a group iff its content differs from its predecessor's in the
                 // new order, or it carries a terminator (unique by construction)
+                const bool opens = (s_bits[dst >> 5] >> (dst & 31)) & 1u;  // slot dst starts the group
                 const u64 ki = s_key[a] >> kTextSlotBits;
                 bool head = (static_cast<u32>(ki) & kFieldMask) != kFull;
                 if (!head && !opens) head = (s_key[s_src[dst - 1]] >> kTextSlotBits) != ki;
@@ -604,52 +712,61 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
         }
         __syncthreads();
 
-        // -- permute (the key buffer is dead: it receives the new order) -----------------------
-        for (int u = tid; u < cnt; u += kRefBlock) {
-            const int a = s_list[u];
-            int dst = s_dst[u];
-            if (shortcut) {
-                const int gs = group_start(a);
-                if ((s_fail[gs >> 5] >> (gs & 31)) & 1u) {
-                    s_dst[u] = 0xffff;  // group left as it was
-                    continue;
+        // -- permute (the key buffer is dead after its last reads here: it receives the new order) --
+        bool head_me[(kRefCap + kRefBlock - 1) / kRefBlock];
+#pragma unroll
+        for (int i = 0; i < (kRefCap + kRefBlock - 1) / kRefBlock; ++i) {
+            const int u = tid + i * kRefBlock;
+            head_me[i] = false;
+            if (u < cnt && dstep) {
+                const int a = s_list[u];
+                const int dst = s_dst[u];
+                const int ge = group_end(a);
+                const bool failed = !verify || ((s_fail[(ge - 1) >> 5] >> ((ge - 1) & 31)) & 1u);
+                if (!failed) head_me[i] = true;   // verified: every member is final
+                else {
+                    // final: what terminates before `depth`; the first of the others opens their group
+                    const u32 ord = static_cast<u32>(s_key[a] >> kTextSlotBits);
+                    const bool opens = (s_bits[dst >> 5] >> (dst & 31)) & 1u;
+                    head_me[i] = ord < kPShortEnd ||
+                                 (!opens && static_cast<u32>(s_key[s_src[dst - 1]] >> kTextSlotBits) < kPShortEnd);
                 }
-                atomicOr(&s_new[dst >> 5], 1u << (dst & 31));  // verified: every member is final
             }
-            s_pos2[dst] = s_pos[a];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < (kRefCap + kRefBlock - 1) / kRefBlock; ++i) {
+            const int u = tid + i * kRefBlock;
+            if (u < cnt) {
+                const int a = s_list[u];
+                const int dst = s_dst[u];
+                s_pos2[dst] = s_pos[a];
+                s_p2[dst] = s_p[a];
+                if (head_me[i]) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
+            }
         }
         __syncthreads();
         for (int u = tid; u < cnt; u += kRefBlock) {
-            if (s_dst[u] == 0xffff) continue;
             const int a = s_list[u];
             s_pos[a] = s_pos2[a];
+            s_p[a] = s_p2[a];
         }
         if (tid < kRefWords) {
             s_bits[tid] |= s_new[tid];
             s_new[tid] = 0;
         }
         __syncthreads();
-        if (!shortcut) {
+        if (!dstep) {
             ++rounds;
             depth += kTextK;
         }
     }
-    if (!loaded) return;  // nothing was tied in this tile
 
-    // write the tile back once; publish the new heads; count what is still tied
+    // write the tile's suffixes once; count what is still tied
     u32 nonheads = 0;
     for (int a = first + tid; a < end; a += kRefBlock) {
-        sa[t0 + a] = s_pos[a];
+        sa_out[t0 + a] = s_pos[a];
         nonheads += !((s_bits[a >> 5] >> (a & 31)) & 1u);
-    }
-    const int n_local = n - t0 < static_cast<u64>(kRefWords) * 32 ? static_cast<int>(n - t0) : kRefWords * 32;
-    for (int j = tid; j < kRefWords; j += kRefBlock) {
-        const int base = j * 32;
-        if (base >= n_local || base >= end) break;
-        u32 w = s_bits[j];
-        if (base + 32 > n_local) w &= (1u << (n_local - base)) - 1u;  // drop the artificial end bit
-        if (base + 32 > end) w &= (1u << (end - base)) - 1u;
-        if (w) atomicOr(bits_new + w0 + j, w);
     }
     for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
     if (lane == 0 && nonheads) atomicAdd(counters, nonheads);
@@ -658,9 +775,9 @@ refine_text_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent,
 
 // rank = inverse permutation of sa.  A direct scatter rank[sa[i]] = i is n random 4-byte
 // writes, each a DRAM read-modify-write of a whole sector (measured 5.9 ms at n = 139 M).
-// Instead the (sa[i], i) pairs are first partitioned by the top 8 bits of sa[i] -- one
-// streaming onesweep pass -- so that consecutive pairs target one n/256-entry window of
-// rank; the scatter then hits in L2 and DRAM only sees whole lines written once.
+// Instead the (sa[i] << 32 | i) records are first partitioned by the top bits of sa[i] -- two
+// streaming onesweep passes -- so that consecutive records target one small window of rank,
+// which is then scattered in shared memory and written as whole lines.
 __global__ void perm_digit_hist_kernel(u64 n, int shift, int bits, u32* __restrict__ hist) {
     // sa is a permutation of [0, n): the number of values v with digit (v >> shift) & mask == d
     // is known in closed form -- count of such v below n
@@ -673,26 +790,29 @@ __global__ void perm_digit_hist_kernel(u64 n, int shift, int bits, u32* __restri
     hist[d] = static_cast<u32>(full * span + part);
 }
 
-__global__ void scatter_pairs_kernel(const u32* __restrict__ pos, const u32* __restrict__ idx, u64 n,
-                                     u32* __restrict__ rank) {
+__global__ void scatter_records_kernel(const u64* __restrict__ rec, u64 n, u32* __restrict__ rank) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        rank[pos[i]] = idx[i];
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const u64 r = rec[i];
+        rank[r >> 32] = static_cast<u32>(r);
+    }
 }
 
 // After the partition passes every aligned window of 2^win_bits rank entries has all of its
-// (pos, idx) pairs in the same index range of the pair arrays (sa is a permutation, so the
-// buckets are exactly window-sized).  One CTA per window: scatter in shared memory, store the
+// (pos << 32 | idx) records in the same index range of the record array (sa is a permutation, so
+// the buckets are exactly window-sized).  One CTA per window: scatter in shared memory, store the
 // window with full-width coalesced writes -- 139 M single-sector L2 write transactions become
 // 4.3 M full lines.
 __global__ void __launch_bounds__(512)
-window_scatter_kernel(const u32* __restrict__ pos, const u32* __restrict__ idx, u64 n, int win_bits,
-                      u32* __restrict__ rank) {
+window_scatter_kernel(const u64* __restrict__ rec, u64 n, int win_bits, u32* __restrict__ rank) {
     extern __shared__ u32 s_win[];
     const u64 base = static_cast<u64>(blockIdx.x) << win_bits;
     const u32 size = static_cast<u32>(n - base < (1ull << win_bits) ? n - base : (1ull << win_bits));
     const u32 mask = (1u << win_bits) - 1u;
-    for (u32 t = threadIdx.x; t < size; t += blockDim.x) s_win[pos[base + t] & mask] = idx[base + t];
+    for (u32 t = threadIdx.x; t < size; t += blockDim.x) {
+        const u64 r = rec[base + t];
+        s_win[static_cast<u32>(r >> 32) & mask] = static_cast<u32>(r);
+    }
     __syncthreads();
     for (u32 t = threadIdx.x; t < size; t += blockDim.x) rank[base + t] = s_win[t];
 }
@@ -701,12 +821,6 @@ __global__ void inverse_kernel(const u32* __restrict__ sa, u64 n, u32* __restric
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
         rank[sa[i]] = static_cast<u32>(i);
-}
-
-__global__ void expand_bits_kernel(const u32* __restrict__ bits, u64 n, u32* __restrict__ flags) {
-    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        flags[i] = (bits[i >> 5] >> (i & 31)) & 1u;
 }
 
 // ---- doubling round: build the pair keys --------------------------------------------
@@ -775,15 +889,108 @@ size_t sa_workspace_bytes(size_t n) {
     size_t total = 0;
     total += pad(sizeof(u64) * (n / 32 + 8));        // packed bases
     total += pad(sizeof(u64) * (n / 64 + 8));        // sentinel bitmap
-    total += 2 * pad(sizeof(u64) * n);               // key buffers a / b
+    total += 2 * pad(sizeof(u64) * n);               // record / key buffers a and b
     total += 2 * pad(sizeof(u32) * n);               // payload buffer b, head_of
     total += pad(sizeof(u32) * n);                   // rank when the caller wants none
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
-    total += 2 * pad(sizeof(u32) * (n / 32 + 8));    // head bitmaps
     total += sort_workspace_bytes(n);
     return total + 4096;
 }
+
+namespace {
+
+// rank = inverse permutation of the finished sa (scratch: two u64 record buffers of n entries).
+int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64* rec_a, u64* rec_b,
+                   const SortWorkspace& ws) {
+    cudaStream_t s = ctx->stream;
+    if (n < (size_t{1} << 22)) {  // the whole rank array is L2-resident: scatter directly
+        RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
+        inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa, n, rank);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_CUDA(cudaGetLastError());
+        return RESEQ_OK;
+    }
+    // two stable passes (low bits of the top 13, then the top 8): windows of ~n / 8192 rank entries
+    const int nb = static_cast<int>(bit_width_u64(n - 1));
+    const int shift = nb - 8;
+    int lo_bits = shift - 13;  // aim at windows of 8192 entries (32 KB of shared memory)
+    if (lo_bits < 0) lo_bits = 0;
+    if (lo_bits > 8) lo_bits = 8;
+    if (ctx->opt_inverse_lo_bits >= 0 && ctx->opt_inverse_lo_bits <= 8) lo_bits = ctx->opt_inverse_lo_bits;
+    const int win_bits = shift - lo_bits;
+    const u64* rec = rec_a;
+    if (lo_bits > 0) {
+        RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
+        perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift - lo_bits, lo_bits, ws.hist);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_TRY(onesweep_partition_pack_iota(ctx, sa, rec_b, n, shift - lo_bits, lo_bits, ws));
+        RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
+        perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_TRY(onesweep_partition_packed(ctx, rec_b, rec_a, n, shift, 8, ws));
+    } else {
+        RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
+        perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_TRY(onesweep_partition_pack_iota(ctx, sa, rec_a, n, shift, 8, ws));
+    }
+    if (win_bits <= 14) {
+        static bool configured = false;
+        if (!configured) {
+            RSQ_CUDA(cudaFuncSetAttribute(window_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          64 * 1024));
+            configured = true;
+        }
+        const unsigned windows = static_cast<unsigned>((n + (size_t{1} << win_bits) - 1) >> win_bits);
+        RSQ_LAUNCH_BEGIN(ctx, "window_scatter_kernel");
+        window_scatter_kernel<<<windows, 512, sizeof(u32) << win_bits, s>>>(rec, n, win_bits, rank);
+        RSQ_LAUNCH_END(ctx);
+    } else {
+        RSQ_LAUNCH_BEGIN(ctx, "scatter_records_kernel");
+        scatter_records_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(rec, n, rank);
+        RSQ_LAUNCH_END(ctx);
+    }
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
+}
+
+// The DNA fast path on `count` records: sort on key24, finish every group from the text.
+// Returns through *unfinished the number of suffixes still tied (+1 if a group was too large
+// for the shared-memory window): 0 means sa_out is final.
+int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n_text, u64* elems_a,
+                    u64* elems_b, size_t m, bool hist_ready, u32* sa_out, int max_rounds, bool use_shortcut,
+                    u32* counters, const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
+    cudaStream_t s = ctx->stream;
+    const PassTable pt = make_passes(kElemKeyShift, 64);
+    bool in_b = false;
+    RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, m, pt, ws, hist_ready, 0, &in_b));
+    st->sort_passes += pt.count;
+    static bool configured = false;
+    if (!configured) {
+        RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kRefSmem)));
+        configured = true;
+    }
+    RSQ_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(u32), s));
+    const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
+    RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
+    refine_elems_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m, sa_out,
+                                                           max_rounds, use_shortcut, counters);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    const volatile u32* c = reinterpret_cast<volatile u32*>(ctx->pinned);
+    *unfinished = static_cast<u64>(c[0]) + (c[1] ? 1u : 0u);
+    if (std::getenv("RESEQ_DEBUG"))
+        std::fprintf(stderr, "[reseq] refine: records=%zu tied_left=%u oversize=%u text_steps=%u\n", m, c[0], c[1], c[2]);
+    st->rounds += c[2];
+    st->refined_tile += m;
+    return RESEQ_OK;
+}
+
+}  // namespace
 
 int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, u32* d_rank,
                     reseq_sa_stats* stats) {
@@ -806,11 +1013,9 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     u32* rank = d_rank ? d_rank : ctx->alloc<u32>(n);
     const size_t rank_tiles = (n + kRankTile - 1) / kRankTile;
     u64* desc = ctx->alloc<u64>(rank_tiles + 4);
-    u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads, [4..5] refine
-    u32* bits_0 = ctx->alloc<u32>(n / 32 + 8);
-    u32* bits_1 = ctx->alloc<u32>(n / 32 + 8);
+    u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads, [4..7] refine
     SortWorkspace ws;
-    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !bits_0 || !bits_1)
+    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters)
         return fail(RESEQ_OUT_OF_MEMORY, "suffix-array workspace does not fit the reserved arena");
     RSQ_TRY(sort_workspace_carve(ctx, n, &ws));
 
@@ -819,12 +1024,32 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     bool dna = false;
     u64 n_separators = 0;
     RSQ_TRY(pack_dna_device(ctx, d_text, n, packed, sent, counters + 16, &dna, &n_separators));
-    // The sentinel-distance shortcut pays off on read sets (a sentinel every <= 1024 symbols on
-    // average); on sentinel-free texts every probe would scan to its cap for nothing.
+    // The distance shortcut pays off on read sets (a sentinel every <= 1024 symbols on average);
+    // on sentinel-free texts no group could use it.
     const bool use_shortcut = ctx->opt_shortcut != 0 && n_separators * 1024 >= n;
     st.alphabet = dna ? 0 : 1;
 
-    // -- initial keys + their digit histograms, 32-bit LSD sort --------------------------
+    // -- DNA fast path: 12-base records, 3 digit passes, groups finished from the L2-resident text --
+    if (dna && ctx->opt_text_rounds > 0) {
+        RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * 3 * kRadix, s));
+        RSQ_LAUNCH_BEGIN(ctx, "init_elems_kernel");
+        init_elems_kernel<<<grid_for(ctx, n, 256, 8, 8), 256, 0, s>>>(packed, sent, n, 0, n, keys_a, ws.hist);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_CUDA(cudaGetLastError());
+        u64 unfinished = 0;
+        RSQ_TRY(sort_and_refine(ctx, packed, sent, n, keys_a, keys_b, n, true, d_sa, ctx->opt_text_rounds, use_shortcut,
+                                counters + 4, ws, &st, &unfinished));
+        st.init_symbols = kElemK;
+        if (unfinished == 0) {
+            RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, ws));
+            st.kernel_launches = ctx->launches - launches0;
+            if (stats) *stats = st;
+            return RESEQ_OK;
+        }
+        // a group outgrew the window or the step limit: rebuild with the general engine
+    }
+
+    // -- general engine: k-mer initial ranks, then prefix doubling (any alphabet, any group size) --
     u32* k32_a = reinterpret_cast<u32*>(keys_a);
     u32* k32_b = reinterpret_cast<u32*>(keys_b);
     const int key_bits = dna ? 2 * kDnaK + kDnaFieldBits : 8 * kByteK + kByteFieldBits;
@@ -848,12 +1073,12 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     u32* sa_cur = in_b ? vals_b : d_sa;
     u32* sa_alt = in_b ? d_sa : vals_b;
 
-    auto rerank = [&](auto* keys, auto flags_only, u32 uniq_mask, u32 uniq_full) -> int {
+    auto rerank = [&](auto* keys, u32 uniq_mask, u32 uniq_full) -> int {
         RSQ_CUDA(cudaMemsetAsync(desc, 0, sizeof(u64) * (rank_tiles + 4), s));
         RSQ_CUDA(cudaMemsetAsync(counters + 1, 0, 2 * sizeof(u32), s));
         using K = std::remove_pointer_t<decltype(keys)>;
         RSQ_LAUNCH_BEGIN(ctx, "rerank_kernel");
-        rerank_kernel<K, decltype(flags_only)::value><<<static_cast<unsigned>(rank_tiles), kRankBlock, 0, s>>>(
+        rerank_kernel<K><<<static_cast<unsigned>(rank_tiles), kRankBlock, 0, s>>>(
             keys, sa_cur, n, uniq_mask, uniq_full, rank, head_of, desc, counters + 1, counters + 2);
         RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
@@ -864,132 +1089,12 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
 
     const u32 field_mask = (1u << (dna ? kDnaFieldBits : kByteFieldBits)) - 1u;
     const u32 field_full = 2u * (dna ? kDnaK : kByteK);
-    u64 heads = 0;
-    u64 h = st.init_symbols;
-    bool ranked = false;  // rank / head_of valid for the current order
+    RSQ_TRY(rerank(in_b ? k32_b : k32_a, field_mask, field_full));
+    u64 heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
 
-    // -- DNA fast path: refine groups from L2-resident text windows -------------------------
-    if (dna && ctx->opt_text_rounds > 0) {
-        const size_t words = (n + 31) / 32 + 4;
-        u32* bits_a = bits_0;
-        u32* bits_b = bits_1;
-        static bool configured = false;
-        if (!configured) {
-            RSQ_CUDA(cudaFuncSetAttribute(refine_text_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kRefSmem)));
-            configured = true;
-        }
-        RSQ_CUDA(cudaMemsetAsync(bits_a, 0, sizeof(u32) * words, s));
-        RSQ_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * sizeof(u32), s));
-        RSQ_LAUNCH_BEGIN(ctx, "headbits_kernel");
-        headbits_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(in_b ? k32_b : k32_a, n, field_mask,
-                                                                     field_full, bits_a, counters + 4);
-        RSQ_LAUNCH_END(ctx);
-        RSQ_CUDA(cudaGetLastError());
-        RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 4, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
-        RSQ_CUDA(cudaStreamSynchronize(s));
-        u32 tied = reinterpret_cast<volatile u32*>(ctx->pinned)[0];
-        bool oversize = false;
-        if (tied > 0) {
-            const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
-            RSQ_CUDA(cudaMemcpyAsync(bits_b, bits_a, sizeof(u32) * words, cudaMemcpyDeviceToDevice, s));
-            RSQ_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * sizeof(u32), s));
-            RSQ_LAUNCH_BEGIN(ctx, "refine_text_kernel");
-            refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sa_cur, n, bits_a, bits_b,
-                                                                   static_cast<u32>(h), ctx->opt_text_rounds,
-                                                                   use_shortcut, counters + 4);
-            RSQ_LAUNCH_END(ctx);
-            RSQ_CUDA(cudaGetLastError());
-            RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 4, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
-            RSQ_CUDA(cudaStreamSynchronize(s));
-            st.refined_tile += tied;
-            tied = reinterpret_cast<volatile u32*>(ctx->pinned)[0];
-            oversize = reinterpret_cast<volatile u32*>(ctx->pinned)[1] != 0;
-            st.rounds += reinterpret_cast<volatile u32*>(ctx->pinned)[2];
-            u32* t = bits_a; bits_a = bits_b; bits_b = t;
-            // Groups still tied after the kernel share at least h + 29 * max_rounds symbols --
-            // unless one was skipped as oversize: that one is still tied at depth h, and prefix
-            // doubling must resume from the smallest depth any group is known to share.
-            if (!oversize) h += static_cast<u64>(kTextK) * ctx->opt_text_rounds;
-        }
-        if (tied == 0 && !oversize) {
-            // every group is a singleton: sa is final and rank is its inverse
-            const int nb = static_cast<int>(bit_width_u64(n - 1));
-            if (n >= (size_t{1} << 22)) {
-                // two stable passes (low 5 bits of the top 13, then the top 8): windows of
-                // n / 8192 rank entries
-                const int shift = nb - 8;
-                int lo_bits = shift - 13;  // aim at windows of 8192 entries (32 KB of shared memory)
-                if (lo_bits < 0) lo_bits = 0;
-                if (lo_bits > 8) lo_bits = 8;
-                if (ctx->opt_inverse_lo_bits >= 0) lo_bits = ctx->opt_inverse_lo_bits;
-                const int win_bits = shift - lo_bits;
-                u32* part_pos = reinterpret_cast<u32*>(keys_a);
-                u32* part_idx = part_pos + n;
-                const u32* src_pos = sa_cur;
-                if (lo_bits > 0) {
-                    u32* p0 = reinterpret_cast<u32*>(keys_b);
-                    u32* i0 = p0 + n;
-                    RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
-                    perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift - lo_bits, lo_bits, ws.hist);
-                    RSQ_LAUNCH_END(ctx);
-                    RSQ_TRY(onesweep_partition_iota(ctx, sa_cur, p0, i0, n, shift - lo_bits, lo_bits, ws));
-                    RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
-                    perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
-                    RSQ_LAUNCH_END(ctx);
-                    RSQ_TRY(onesweep_partition_pairs(ctx, p0, i0, part_pos, part_idx, n, shift, 8, ws));
-                } else {
-                    RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
-                    perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
-                    RSQ_LAUNCH_END(ctx);
-                    RSQ_TRY(onesweep_partition_iota(ctx, src_pos, part_pos, part_idx, n, shift, 8, ws));
-                }
-                if (win_bits <= 14) {
-                    static bool configured = false;
-                    if (!configured) {
-                        RSQ_CUDA(cudaFuncSetAttribute(window_scatter_kernel,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-                        configured = true;
-                    }
-                    const unsigned windows = static_cast<unsigned>((n + (size_t{1} << win_bits) - 1) >> win_bits);
-                    RSQ_LAUNCH_BEGIN(ctx, "window_scatter_kernel");
-                    window_scatter_kernel<<<windows, 512, sizeof(u32) << win_bits, s>>>(part_pos, part_idx, n,
-                                                                                        win_bits, rank);
-                    RSQ_LAUNCH_END(ctx);
-                } else {
-                    RSQ_LAUNCH_BEGIN(ctx, "scatter_pairs_kernel");
-                    scatter_pairs_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(part_pos, part_idx, n, rank);
-                    RSQ_LAUNCH_END(ctx);
-                }
-            } else {  // the whole rank array is L2-resident: scatter directly
-                RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
-                inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa_cur, n, rank);
-                RSQ_LAUNCH_END(ctx);
-            }
-            RSQ_CUDA(cudaGetLastError());
-            heads = n;
-            ranked = true;
-        } else {
-            // hand over to prefix doubling: group-head ranks from the bitmap
-            u32* flags = reinterpret_cast<u32*>(keys_b);  // the initial keys are no longer needed
-            RSQ_LAUNCH_BEGIN(ctx, "expand_bits_kernel");
-            expand_bits_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(bits_a, n, flags);
-            RSQ_LAUNCH_END(ctx);
-            RSQ_CUDA(cudaGetLastError());
-            RSQ_TRY(rerank(flags, std::true_type{}, 0u, 0u));
-            heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
-            ranked = true;
-        }
-    }
-    if (!ranked) {
-        RSQ_TRY(rerank(in_b ? k32_b : k32_a, std::false_type{}, field_mask, field_full));
-        heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
-    }
-
-    // -- prefix doubling (general engine: any alphabet, any group size, any LCP) --------------
     const int b = static_cast<int>(bit_width_u64(n));
     const PassTable pt = make_passes(0, 2 * b);
-    for (; heads < n && h < n; h <<= 1) {
+    for (u64 h = st.init_symbols; heads < n && h < n; h <<= 1) {
         RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * pt.count * kRadix, s));
         {
             const unsigned grid = grid_for(ctx, n, 256, 8, 8);
@@ -1002,7 +1107,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         RSQ_TRY(onesweep_sort<u64>(ctx, keys_a, keys_b, sa_cur, sa_alt, n, pt, ws, true, 0, &in_b));
         st.sort_passes += pt.count;
         if (in_b) { u32* t = sa_cur; sa_cur = sa_alt; sa_alt = t; }
-        RSQ_TRY(rerank(in_b ? keys_b : keys_a, std::false_type{}, 0u, 0u));
+        RSQ_TRY(rerank(in_b ? keys_b : keys_a, 0u, 0u));
         heads = *reinterpret_cast<volatile u32*>(ctx->pinned);
         ++st.rounds;
         st.refined_global += n;
@@ -1079,8 +1184,7 @@ void reseq_cuda_sa_shard_destroy(reseq_cuda_sa_shard* sh) {
     delete sh;
 }
 
-int reseq_cuda_sa_shard_keys(reseq_cuda_sa_shard* sh, uint64_t pos_begin, size_t count, uint32_t* d_keys,
-                             uint32_t* d_pos) {
+int reseq_cuda_sa_shard_records(reseq_cuda_sa_shard* sh, uint64_t pos_begin, size_t count, uint64_t* d_records) {
     using namespace rsq;
     if (!sh || !sh->dna) return fail(RESEQ_INVALID_ARGUMENT, "the sharded build needs a DNA text");
     if (count == 0) return RESEQ_OK;
@@ -1090,69 +1194,36 @@ int reseq_cuda_sa_shard_keys(reseq_cuda_sa_shard* sh, uint64_t pos_begin, size_t
     RSQ_TRY(ctx->reserve(reseq_cuda_ctx::padded(sizeof(u32) * kMaxPasses * kRadix) + 4096));
     ctx->begin();
     u32* hist = ctx->alloc<u32>(kMaxPasses * kRadix);  // the slice's histogram is not used: buckets re-count
-    const PassTable pt0 = make_passes(0, 2 * kDnaK + kDnaFieldBits);
-    RSQ_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * pt0.count * kRadix, ctx->stream));
-    RSQ_LAUNCH_BEGIN(ctx, "initkey_dna_kernel");
-    initkey_dna_kernel<<<grid_for(ctx, count, 256, 8, 8), 256, sizeof(u32) * pt0.count * kRadix, ctx->stream>>>(
-        sh->packed, sh->sent, sh->n, pos_begin, count, d_keys, d_pos, pt0, hist);
+    RSQ_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * 3 * kRadix, ctx->stream));
+    RSQ_LAUNCH_BEGIN(ctx, "init_elems_kernel");
+    init_elems_kernel<<<grid_for(ctx, count, 256, 8, 8), 256, 0, ctx->stream>>>(sh->packed, sh->sent, sh->n, pos_begin,
+                                                                                  count, d_records, hist);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
 }
 
-int reseq_cuda_sa_shard_finish(reseq_cuda_sa_shard* sh, uint32_t* d_keys, uint32_t* d_pos, size_t m,
-                               uint32_t* d_sa_out, uint64_t* unfinished) {
+int reseq_cuda_sa_shard_finish(reseq_cuda_sa_shard* sh, uint64_t* d_records, size_t m, uint32_t* d_sa_out,
+                               uint64_t* unfinished) {
     using namespace rsq;
     if (!sh || !sh->dna || !unfinished) return fail(RESEQ_INVALID_ARGUMENT, "bad shard argument");
     *unfinished = 0;
     if (m == 0) return RESEQ_OK;
     reseq_cuda_ctx* ctx = sh->ctx;
     RSQ_CUDA(cudaSetDevice(ctx->device));
-    cudaStream_t s = ctx->stream;
     auto pad = reseq_cuda_ctx::padded;
-    RSQ_TRY(ctx->reserve(2 * pad(sizeof(u32) * m) + 2 * pad(sizeof(u32) * (m / 32 + 8)) + sort_workspace_bytes(m) + 8192));
+    RSQ_TRY(ctx->reserve(pad(sizeof(u64) * m) + sort_workspace_bytes(m) + 8192));
     ctx->begin();
-    u32* keys_b = ctx->alloc<u32>(m);
-    u32* pos_b = ctx->alloc<u32>(m);
-    u32* bits_a = ctx->alloc<u32>(m / 32 + 8);
-    u32* bits_b = ctx->alloc<u32>(m / 32 + 8);
+    u64* rec_b = ctx->alloc<u64>(m);
     u32* counters = ctx->alloc<u32>(64);
     SortWorkspace ws;
-    if (!keys_b || !pos_b || !bits_a || !bits_b || !counters) return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
+    if (!rec_b || !counters) return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
     RSQ_TRY(sort_workspace_carve(ctx, m, &ws));
-    // stable sort of the bucket on the 31-bit key: equal keys stay in ascending position order
+    // stable sort of the bucket on the 24-bit key: equal keys stay in ascending position order
     // because the exchange delivers the slices in rank (= position) order
-    const PassTable pt0 = make_passes(0, 2 * kDnaK + kDnaFieldBits);
-    bool in_b = false;
-    RSQ_TRY(onesweep_sort<u32>(ctx, d_keys, keys_b, d_pos, pos_b, m, pt0, ws, false, 0, &in_b));
-    u32* sa_cur = in_b ? pos_b : d_pos;
-    const size_t words = (m + 31) / 32 + 4;
-    RSQ_CUDA(cudaMemsetAsync(bits_a, 0, sizeof(u32) * words, s));
-    RSQ_CUDA(cudaMemsetAsync(counters, 0, 256, s));
-    RSQ_LAUNCH_BEGIN(ctx, "headbits_kernel");
-    headbits_kernel<<<grid_for(ctx, m, 256, 4, 16), 256, 0, s>>>(in_b ? keys_b : d_keys, m, (1u << kDnaFieldBits) - 1u,
-                                                                 2u * kDnaK, bits_a, counters);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_CUDA(cudaGetLastError());
-    RSQ_CUDA(cudaMemcpyAsync(bits_b, bits_a, sizeof(u32) * words, cudaMemcpyDeviceToDevice, s));
-    RSQ_CUDA(cudaMemsetAsync(counters, 0, 256, s));
-    static bool configured = false;
-    if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(refine_text_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kRefSmem)));
-        configured = true;
-    }
-    const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
-    RSQ_LAUNCH_BEGIN(ctx, "refine_text_kernel");
-    refine_text_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(sh->packed, sh->sent, sh->n, sa_cur, m, bits_a, bits_b,
-                                                          kDnaK, 1 << 20, sh->use_shortcut, counters);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_CUDA(cudaGetLastError());
-    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
-    RSQ_CUDA(cudaMemcpyAsync(d_sa_out, sa_cur, sizeof(u32) * m, cudaMemcpyDeviceToDevice, s));
-    RSQ_CUDA(cudaStreamSynchronize(s));
-    // still tied (only possible through an oversize group: the round limit is out of reach)
-    *unfinished = reinterpret_cast<volatile u32*>(ctx->pinned)[0] + (reinterpret_cast<volatile u32*>(ctx->pinned)[1] ? 1u : 0u);
+    reseq_sa_stats st{};
+    RSQ_TRY(sort_and_refine(ctx, sh->packed, sh->sent, sh->n, d_records, rec_b, m, false, d_sa_out, 1 << 20,
+                            sh->use_shortcut, counters, ws, &st, unfinished));
     return RESEQ_OK;
 }
 

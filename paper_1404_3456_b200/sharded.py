@@ -1,9 +1,10 @@
 """Multi-GPU form of the hot path: one process per GPU.
 
-  SA build       sample sort on the 31-bit initial key.  The text is replicated (2-bit packed it
-                 is n/4 bytes); every rank keys its 1/G slice of positions; G-1 splitters are read
-                 off an all-reduced histogram of the key's top 16 bits; one ALL-TO-ALL moves every
-                 (key, position) record to the rank owning its splitter range; each rank finishes
+  SA build       sample sort on the 24-bit initial key (12 bases).  The text is replicated (2-bit
+                 packed it is n/4 bytes); every rank makes the 64-bit records (key24 << 40 |
+                 terminator byte << 32 | position) of its 1/G slice of positions; G-1 splitters are
+                 read off an all-reduced histogram of the key's top 16 bits; one ALL-TO-ALL moves
+                 every record to the rank owning its splitter range; each rank finishes
                  its bucket with the single-GPU kernels (refinement keys come from the replicated
                  text, so no further exchange is needed); the buckets, concatenated in splitter
                  order, ARE the suffix array (all-gather); rank = local inverse.
@@ -29,8 +30,13 @@ import torch
 from . import _lib
 from .api import Executor, FragmentIndex, FragmentSet, OverlapList
 
-PREFIX_BITS = 16   # splitters are chosen on the top 16 bits (8 bases) of the 31-bit initial key
-KEY_BITS = 31
+PREFIX_BITS = 16   # splitters are chosen on the top 16 bits (8 bases) of the record's 24-bit key
+PREFIX_SHIFT = 64 - PREFIX_BITS
+
+
+def record_prefix(records: torch.Tensor) -> torch.Tensor:
+    """Top 16 key bits of int64-typed records (bit pattern of the u64 record)."""
+    return (records >> PREFIX_SHIFT) & ((1 << PREFIX_BITS) - 1)
 
 
 # ---- collectives --------------------------------------------------------------------------------
@@ -156,36 +162,35 @@ class GpuBackend:
             self.lib.reseq_cuda_sa_shard_destroy(self.shard)
             self.shard = None
 
-    def keys(self, pos_begin: int, count: int):
-        k = torch.empty(count, dtype=torch.int32, device=self.device)
-        p = torch.empty(count, dtype=torch.int32, device=self.device)
-        _lib.check(self.lib.reseq_cuda_sa_shard_keys(self.shard, pos_begin, count, _p(k), _p(p)))
+    def records(self, pos_begin: int, count: int) -> torch.Tensor:
+        r = torch.empty(count, dtype=torch.int64, device=self.device)
+        _lib.check(self.lib.reseq_cuda_sa_shard_records(self.shard, pos_begin, count, _p(r)))
         self.ex.synchronize()
-        return k, p
+        return r
 
-    def prefix_histogram(self, keys: torch.Tensor) -> torch.Tensor:
-        return torch.bincount((keys >> (KEY_BITS - PREFIX_BITS)).to(torch.int64), minlength=1 << PREFIX_BITS)
+    def prefix_histogram(self, records: torch.Tensor) -> torch.Tensor:
+        return torch.bincount(record_prefix(records), minlength=1 << PREFIX_BITS)
 
-    def partition(self, keys, pos, bounds: torch.Tensor):
+    def partition(self, records, bounds: torch.Tensor):
         """Groups the records by destination rank, keeping their order inside each group.  The
         grouping itself is one stable pass of this library's radix sort on the rank id."""
-        dest = torch.bucketize((keys >> (KEY_BITS - PREFIX_BITS)).to(torch.int64), bounds.to(keys.device), right=True)
+        dest = torch.bucketize(record_prefix(records), bounds.to(records.device), right=True)
         counts = torch.bincount(dest, minlength=bounds.numel() + 1)
         dest32 = dest.to(torch.int32)
-        idx = torch.arange(keys.numel(), dtype=torch.int32, device=keys.device)
+        idx = torch.arange(records.numel(), dtype=torch.int32, device=records.device)
         d_out, i_out = torch.empty_like(dest32), torch.empty_like(idx)
-        if keys.numel():
-            _lib.check(self.lib.reseq_cuda_radix_sort_device(self.ex.handle, _p(dest32), _p(idx), keys.numel(),
+        if records.numel():
+            _lib.check(self.lib.reseq_cuda_radix_sort_device(self.ex.handle, _p(dest32), _p(idx), records.numel(),
                                                              _p(d_out), _p(i_out)))
             self.ex.synchronize()
         order = i_out.to(torch.int64)
-        return keys[order].contiguous(), pos[order].contiguous(), [int(c) for c in counts.tolist()]
+        return records[order].contiguous(), [int(c) for c in counts.tolist()]
 
-    def finish(self, keys, pos):
-        m = keys.numel()
+    def finish(self, records):
+        m = records.numel()
         sa = torch.empty(m, dtype=torch.int32, device=self.device)
         unfinished = C.c_uint64(0)
-        _lib.check(self.lib.reseq_cuda_sa_shard_finish(self.shard, _p(keys), _p(pos), m, _p(sa), C.byref(unfinished)))
+        _lib.check(self.lib.reseq_cuda_sa_shard_finish(self.shard, _p(records), m, _p(sa), C.byref(unfinished)))
         return sa, int(unfinished.value)
 
     def inverse(self, sa):
@@ -228,15 +233,14 @@ def build_sa_sharded(d_text: torch.Tensor, comm, backend, stats: Optional[dict] 
             stats["path"] = "replicated"
             return backend.full_build(d_text)
         lo, hi = (n * r) // G, (n * (r + 1)) // G
-        keys, pos = backend.keys(lo, hi - lo)
-        hist = comm.all_reduce_sum(backend.prefix_histogram(keys))
+        records = backend.records(lo, hi - lo)
+        hist = comm.all_reduce_sum(backend.prefix_histogram(records))
         bounds = choose_bounds(hist, G)
-        keys, pos, counts = backend.partition(keys, pos, bounds)
-        rk, _ = comm.all_to_all_v(keys, counts)
-        rp, rc = comm.all_to_all_v(pos, counts)
-        stats["bucket"] = int(rk.numel())
+        records, counts = backend.partition(records, bounds)
+        mine, _ = comm.all_to_all_v(records, counts)
+        stats["bucket"] = int(mine.numel())
         stats["sent"] = int(sum(counts) - counts[r])
-        bucket, unfinished = backend.finish(rk, rp)
+        bucket, unfinished = backend.finish(mine)
         flag = comm.all_reduce_sum(torch.tensor([unfinished], dtype=torch.int64, device=d_text.device))
         if int(flag.item()) != 0:
             # a group outgrew the refine window somewhere: every rank builds the whole array

@@ -23,8 +23,8 @@ def doubling_executor(rq):
 
 
 def no_shortcut_executor(rq):
-    """A third context: shared-memory refinement by 23-symbol text rounds only (the
-    sentinel-distance shortcut switched off)."""
+    """A third context: shared-memory refinement by 23-symbol text steps only (the distance
+    shortcut switched off)."""
     if "ns" not in _doubling:
         e = rq.Executor(0)
         e.set_option("sa_shortcut", 0)
@@ -140,7 +140,7 @@ def test_generic_byte_texts(rq, ex, oracle):
 def test_read_sets_against_the_oracle(rq, ex, oracle, G, L, k):
     text, _ = rq.synth_read_text(G, L, k)
     got = check(rq, ex, oracle, text)
-    assert got.stats.alphabet == 0 and got.stats.init_symbols == 13
+    assert got.stats.alphabet == 0 and got.stats.init_symbols == 11
     assert got.stats.rounds <= 6 and got.stats.refined_global == 0
 
 

@@ -1,7 +1,7 @@
 """Host logic of the multi-GPU path under REAL collectives: two processes, gloo backend, CPU
 tensors.  The per-rank kernels are replaced by a numpy stand-in (NumpyBackend below, checker-grade
 code that leans on the oracle), so what is exercised is sharded.py itself: position slicing,
-splitter selection from the all-reduced histogram, the all-to-all of (key, position) records, the
+splitter selection from the all-reduced histogram, the all-to-all of the 64-bit suffix records, the
 ordering guarantee the bucket sort relies on, the all-gather of buckets and the fallbacks."""
 import os
 import sys
@@ -16,27 +16,43 @@ import torch.multiprocessing as mp
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def initial_keys(text: np.ndarray, lo: int, hi: int) -> np.ndarray:
-    """numpy restatement of the 31-bit initial key of csrc/sa.cu (13 bases zero padded at a
-    terminator << 5 | 2*len + kind)."""
+def records_of(text: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """numpy restatement of the 64-bit suffix record of csrc/sa.cu: key24 << 40 | p8 << 32 | pos.
+    key24: bases 0..7 in the upper 16 bits; low digit = 0x80 | bases 8..10 | upper bit of base 11
+    for suffixes of more than 8 symbols, 2*t + kind for those terminating after t <= 8 symbols."""
     n = text.size
     code = np.zeros(256, np.int64)
     code[[65, 67, 71, 84]] = [0, 1, 2, 3]
-    keys = np.zeros(hi - lo, np.int64)
+    out = np.zeros(hi - lo, np.int64)
     for i, pos in enumerate(range(lo, hi)):
-        bases, ln, field = 0, 0, 26
-        for t in range(13):
-            if pos + t >= n:
-                field = 2 * ln
-                break
-            c = text[pos + t]
-            if c == 0:
-                field = 2 * ln + 1
-                break
-            bases |= int(code[c]) << (2 * (12 - t))
-            ln += 1
-        keys[i] = (bases << 5) | field
-    return keys
+        t = 0
+        while pos + t < n and text[pos + t] != 0 and t < 256:
+            t += 1
+        if pos + t < n and t < 256:
+            tt, kind = t, 1                      # a sentinel comes first
+        elif n - pos <= 256:
+            tt, kind = n - pos, 0                # the text ends first
+        else:
+            tt, kind = 256, 1
+        bases = 0
+        for b in range(min(tt, 12)):
+            bases |= int(code[text[pos + b]]) << (2 * (11 - b))
+        if tt <= 8:
+            key, p = ((bases >> 8) << 8) | (2 * tt + kind), 2 * tt + kind
+        else:
+            b23 = bases >> 1
+            key = ((b23 >> 7) << 8) | 0x80 | (b23 & 0x7F)
+            if tt < 11:
+                p = 2 * tt + kind
+            elif tt == 256:
+                p = 254
+            elif kind == 0:
+                p = 255
+            else:
+                p = tt + 11 if tt + 11 <= 253 else 254
+        v = (key << 40) | (p << 32) | pos
+        out[i] = v - (1 << 64) if v >= (1 << 63) else v
+    return out
 
 
 class NumpyBackend:
@@ -50,23 +66,23 @@ class NumpyBackend:
     def close(self):
         pass
 
-    def keys(self, lo, count):
-        return (torch.from_numpy(initial_keys(self.text, lo, lo + count).astype(np.int32)),
-                torch.arange(lo, lo + count, dtype=torch.int32))
+    def records(self, lo, count):
+        return torch.from_numpy(records_of(self.text, lo, lo + count))
 
-    def prefix_histogram(self, keys):
-        return torch.bincount((keys >> 15).to(torch.int64), minlength=1 << 16)
+    def prefix_histogram(self, records):
+        return torch.bincount((records >> 48) & 0xFFFF, minlength=1 << 16)
 
-    def partition(self, keys, pos, bounds):
-        dest = torch.bucketize((keys >> 15).to(torch.int64), bounds, right=True)
+    def partition(self, records, bounds):
+        dest = torch.bucketize((records >> 48) & 0xFFFF, bounds, right=True)
         order = torch.argsort(dest, stable=True)
         counts = torch.bincount(dest, minlength=bounds.numel() + 1)
-        return keys[order].contiguous(), pos[order].contiguous(), [int(c) for c in counts.tolist()]
+        return records[order].contiguous(), [int(c) for c in counts.tolist()]
 
-    def finish(self, keys, pos):
-        p = pos.numpy().astype(np.int64)
+    def finish(self, records):
+        r = records.numpy()
+        p = r & 0xFFFFFFFF
         # the exchange must deliver equal keys in ascending position order (stability contract)
-        k = keys.numpy().astype(np.int64)
+        k = (r >> 40) & 0xFFFFFF
         order = np.argsort(k, kind="stable")
         same = k[order][1:] == k[order][:-1]
         assert np.all(p[order][1:][same] > p[order][:-1][same]), "records of equal key arrived out of position order"
