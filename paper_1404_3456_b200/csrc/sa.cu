@@ -349,19 +349,21 @@ constexpr u32 kPEot = 255;
 
 constexpr int kRefBlock = 256;
 constexpr int kRefTile = 2048;
-constexpr int kRefExt = 768;
+constexpr int kRefExt = 640;
 constexpr int kRefCap = kRefTile + kRefExt;
 constexpr int kRefWords = kRefCap / 32 + 2;
-constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 3 * sizeof(unsigned short) * kRefCap +
-                            kRefCap + sizeof(u32) * (4 * kRefWords + 16);
-constexpr int kTextK = 23;          // bases per text step
-constexpr int kTextFieldBits = 6;   // terminator field: 2*len + kind, 2*kTextK = "no terminator"
+constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 4 * sizeof(unsigned short) * kRefCap +
+                            sizeof(u32) * (4 * kRefWords + 16);
+constexpr int kStepK = 16;          // bases compared per refinement step
 constexpr u32 kDistCap = 4095;      // farthest sentinel the bitmap scan looks for
-constexpr u32 kOrdNone = 0x1FFF;    // "no usable distance": sorts last, its group cannot use the shortcut
-constexpr int kTextSlotBits = 12;   // window slot of the suffix: makes every key of a step unique
-static_assert(kRefCap <= (1 << kTextSlotBits), "window slots must fit the key's slot field");
-static_assert(2 * kTextK + kTextFieldBits + kTextSlotBits == 64, "refinement key layout");
-static_assert(kDistCap + kElemK < kOrdNone, "order values must stay below the none marker");
+constexpr u32 kTdNone = 0xFFFF;     // "terminator not known": the suffix can only be split by its bases
+constexpr u32 kTdMax = 16000;       // largest distance to the terminator kept (2 * t + kind must fit 16 bits)
+constexpr u32 kOrdNone = 0x7FFF;
+constexpr int kOrdBits = 15;
+constexpr int kSlotBits = 12;       // window slot of the suffix: makes every key of a step unique
+static_assert(kRefCap <= (1 << kSlotBits), "window slots must fit the key's slot field");
+static_assert(2 * kStepK + kOrdBits + kSlotBits <= 64, "step key layout");
+static_assert(2 * kTdMax + 1 + 2 * kElemK < kOrdNone && 2 * (kDistCap + kElemK) + 1 <= 2 * kTdMax + 1, "terminator distances must fit the order field");
 
 // Records of the `count` suffixes starting at text position pos0 (the whole text: pos0 = 0,
 // count = n; a multi-GPU rank keys only its slice), plus the digit histograms of the three sort
@@ -413,25 +415,6 @@ init_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, 
     hist_flush(s_hist, g_hist, 3);
 }
 
-// Key of one text step for the suffix in window slot `slot`: the next 23 symbols from `pos`
-// (zero padded at a terminator) | terminator field | slot.  Keys of equal content keep
-// their slot order, so the order of the full 64-bit keys IS the stable refined order.
-__device__ __forceinline__ u64 text_key(const u64* __restrict__ packed, const u64* __restrict__ sent,
-                                        u64 n, u64 pos, u32 slot) {
-    if (pos >= n) return slot;  // the text ends exactly here: end-of-text after 0 symbols
-    const u64 bases = base_window(packed, pos) >> (64 - 2 * kTextK);
-    const u32 sw = static_cast<u32>(sent_window(sent, pos) >> (64 - kTextK));
-    const u32 t = sw ? static_cast<u32>(__clz(sw)) - (32 - kTextK) : kTextK;
-    const u64 rem = n - pos;
-    const u32 lim = rem < kTextK ? static_cast<u32>(rem) : kTextK;
-    u32 len, field;
-    if (t < lim) { len = t; field = 2 * t + 1; }
-    else if (lim < kTextK) { len = lim; field = 2 * lim; }
-    else { len = kTextK; field = 2 * kTextK; }
-    const u64 kept = len == kTextK ? bases : bases & ~((1ull << (2 * (kTextK - len))) - 1ull);
-    return (((kept << kTextFieldBits) | field) << kTextSlotBits) | slot;
-}
-
 // 128-bit load of two consecutive packed words (the pair index is even: 16-byte aligned).
 __device__ __forceinline__ void ld_words2(const u64* __restrict__ p, u64& w0, u64& w1) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
@@ -439,22 +422,38 @@ __device__ __forceinline__ void ld_words2(const u64* __restrict__ p, u64& w0, u6
     w1 = (static_cast<u64>(v.w) << 32) | v.z;
 }
 
+// The 16 bases starting at position q, top aligned in 32 bits.  One 128-bit gather of the aligned
+// word pair serves 3 windows in 4; the kernel is bound by issue slots and L1 wavefronts (one per
+// lane per gather), so fewer, wider gathers is what counts.
+__device__ __forceinline__ u32 bases16(const u64* __restrict__ packed, u64 q) {
+    const u64 w = q >> 5;
+    const unsigned s = static_cast<unsigned>(q & 31) * 2;
+    u64 w0, w1;
+    ld_words2(packed + (w & ~1ull), w0, w1);
+    u64 hi = (w & 1) ? w1 : w0;
+    u64 win = hi << s;
+    if (s > 32) {  // the window runs into the next word
+        const u64 lo = (w & 1) ? packed[w + 1] : w1;
+        win |= lo >> (64 - s);
+    }
+    return static_cast<u32>(win >> 32);
+}
+
 // One CTA finishes every group that starts in its tile: the key of a tied suffix depends only
 // on (position, depth), never on another group, so all steps run back to back in shared memory.
 //
-// Steps alternate, starting with a DISTANCE step.
-//   DISTANCE  In a read set the members of a group are reads over one locus: each is a prefix
-//             of the longer ones, so their order is (distance to the terminator, position).
-//             The members are ranked by that key, then every member is compared base by base,
-//             over its own remaining length, with the group's longest member (each member
-//             fetches its text as 128-bit words: the kernel is bound by L1 wavefronts, one per
-//             lane per gather, so fewer and wider gathers is what counts).  If all agree the
-//             group is final in ONE step.  If not (chance 12-mer repeats, mixed loci) the
-//             permutation is kept -- it is harmless: members that can still tie have equal
-//             distance and keep their position order -- and only the members that terminate
-//             inside the already-compared prefix become final.
-//   TEXT      what the distance step could not settle is split by the next 23 symbols
-//             (zero padded at a terminator | terminator field), fetched from the packed text.
+// A step at depth d (all members of a group share their first d symbols) orders each group by
+//     ( next 16 bases, zero padded from the terminator on | 2 * (t - d) + kind | slot )
+// where t is the suffix's distance to its terminator, known from the record.  Suffixes that
+// differ in the 16 bases are split for good.  Those that agree form a subgroup ordered by
+// terminator distance, which is their final order IF every member is a prefix of the longest
+// one -- in a read set a subgroup is the reads over one locus, so that is the rule, not the
+// exception.  Every member is therefore compared base by base, over its remaining length, with
+// the subgroup's longest member (128-bit gathers from the L2-resident packed text).  If all
+// agree the subgroup is final: ONE step instead of ceil(read length / 16).  If not (repeats),
+// the members that terminate inside the 16 bases are final, the others stay tied at depth
+// d + 16 and take another step.  Slots keep position order among equal keys, which is what
+// the total order asks for where two suffixes are identical up to their sentinels.
 // Every step first compacts the still-tied suffixes into a dense list (order preserving, so a
 // group stays contiguous): late steps cost in proportion to what is left.
 __global__ void __launch_bounds__(kRefBlock)
@@ -466,15 +465,15 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     extern __shared__ __align__(16) unsigned char ref_smem[];
     u64* s_key = reinterpret_cast<u64*>(ref_smem);               // [cap] records, then keys of the step ...
     u32* s_pos2 = reinterpret_cast<u32*>(ref_smem);              // ... then the permuted positions
-    u8* s_p2 = reinterpret_cast<u8*>(s_pos2 + kRefCap);          // ... and their payloads
+    unsigned short* s_td2 = reinterpret_cast<unsigned short*>(s_pos2 + kRefCap);  // ... and terminators
     u32* s_pos = reinterpret_cast<u32*>(s_key + kRefCap);        // [cap] suffix positions, sa order
     unsigned short* s_list = reinterpret_cast<unsigned short*>(s_pos + kRefCap);  // [cap] tied slots
     unsigned short* s_dst = s_list + kRefCap;                    // [cap] new slot of list entry u
     unsigned short* s_src = s_dst + kRefCap;                     // [cap] old slot of new slot d
-    u8* s_p = reinterpret_cast<u8*>(s_src + kRefCap);            // [cap] payload p8 of the suffix
-    u32* s_bits = reinterpret_cast<u32*>(s_p + kRefCap);         // [words] head bits of the window
+    unsigned short* s_td = s_src + kRefCap;                      // [cap] 2 * t + kind of the suffix, or kTdNone
+    u32* s_bits = reinterpret_cast<u32*>(s_td + kRefCap);        // [words] head bits of the window
     u32* s_new = s_bits + kRefWords;                             // [words] heads created this step
-    u32* s_fail = s_new + kRefWords;                             // [words] groups the distance step gave up on
+    u32* s_fail = s_new + kRefWords;                             // [words] subgroups that failed the prefix check
     u32* s_cnt = s_fail + kRefWords;                             // [words + 1] tied-count scan
     __shared__ int s_first, s_end, s_last;
 
@@ -543,11 +542,35 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
         end = s_last;                 // that group is nobody's: the host rebuilds
     }
 
-    // unpack the records this CTA owns
+    // -- unpack the records this CTA owns: position, and 2 * t + kind from the terminator byte ----
     for (int a = first + tid; a < end; a += kRefBlock) {
         const u64 e = s_key[a];
-        s_pos[a] = static_cast<u32>(e);
-        s_p[a] = static_cast<u8>(e >> 32);
+        const u32 pos = static_cast<u32>(e);
+        const u32 p = static_cast<u32>(e >> 32) & 0xffu;
+        u32 td;
+        if (p < kPShortEnd) td = p;
+        else if (p <= kPMaxNear) td = 2 * (p - kElemK) + 1;
+        else if (p == kPEot) {
+            const u64 t = n_text - pos;
+            td = t <= kTdMax ? 2 * static_cast<u32>(t) : kTdNone;
+        } else if (!use_shortcut) {
+            td = kTdNone;              // sparse sentinels: the key phase looks for one window by window
+        } else {                       // scan the sentinel bitmap (long reads; rare)
+            const u64 q = static_cast<u64>(pos) + kElemK;   // no sentinel before that (the byte would say)
+            u32 dist = kDistCap + 1, c0 = 0;
+            for (; c0 <= kDistCap && q + c0 < n_text; c0 += 64) {
+                const u64 w = sent_window(sent, q + c0);
+                if (w) {
+                    dist = c0 + static_cast<u32>(__clzll(w));
+                    break;
+                }
+            }
+            if (dist <= kDistCap && q + dist < n_text) td = 2 * (dist + kElemK) + 1;
+            else if (q + c0 >= n_text && n_text - pos <= kTdMax) td = 2 * static_cast<u32>(n_text - pos);  // none up to the end
+            else td = kTdNone;
+        }
+        s_pos[a] = pos;
+        s_td[a] = static_cast<unsigned short>(td);
     }
     __syncthreads();
 
@@ -563,10 +586,6 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
         if (base + 32 > end) t &= (1u << (end - base)) - 1u;
         return t;
     };
-
-    constexpr u32 kFieldMask = (1u << kTextFieldBits) - 1u;
-    constexpr u32 kFull = 2 * kTextK;
-
     // group start of window slot a: the last head at or before it
     auto group_start = [&](int a) {
         int w = a >> 5;
@@ -580,15 +599,11 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
         while (!word) word = s_bits[++w];
         return w * 32 + __ffs(word) - 1;
     };
+    auto is_head = [&](int a) { return (s_bits[a >> 5] >> (a & 31)) & 1u; };
 
     u32 depth = kElemK;
     int rounds = 0;
-    for (int step = 0;; ++step) {
-        const bool dstep = (step & 1) == 0;           // distance step
-        const bool verify = dstep && use_shortcut;    // without it the step only settles what terminates before `depth`
-        if (dstep && step > 0 && !use_shortcut) continue;
-        if (!dstep && rounds >= max_rounds) break;
-
+    for (; rounds < max_rounds; ++rounds) {
         // -- compact the tied slots, in order ------------------------------------------------
         u32 tw = 0, c = 0;
         if (tid < kRefWords) {
@@ -623,28 +638,30 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
         __syncthreads();
         const int cnt = static_cast<int>(total);
 
-        // -- keys ----------------------------------------------------------------------------------
+        // -- keys: 16 bases from the L2-resident text | terminator distance | slot --------------------
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
-            if (dstep) {
-                u32 ord = s_p[a];
-                if (ord == kPEot) ord = kOrdNone;
-                else if (ord == kPFar) {     // scan the sentinel bitmap (long reads; rare)
-                    const u64 q = static_cast<u64>(s_pos[a]) + kElemK;   // no sentinel before that (p8 would say)
-                    u32 dist = kDistCap + 1;
-                    for (u32 c0 = 0; c0 <= kDistCap && q + c0 < n_text; c0 += 64) {
-                        const u64 w = sent_window(sent, q + c0);
-                        if (w) {
-                            dist = c0 + static_cast<u32>(__clzll(w));
-                            break;
-                        }
-                    }
-                    ord = (dist + kElemK > kDistCap || q + dist >= n_text) ? kOrdNone : dist + 2 * kElemK;
-                }
-                s_key[a] = (static_cast<u64>(ord) << kTextSlotBits) | static_cast<u32>(a);
-            } else {
-                s_key[a] = text_key(packed, sent, n_text, static_cast<u64>(s_pos[a]) + depth, static_cast<u32>(a));
+            const u64 q = static_cast<u64>(s_pos[a]) + depth;
+            u32 td = s_td[a];
+            if (td == kTdNone) {   // is there a terminator inside this window?
+                const u32 sw = q < n_text ? static_cast<u32>(sent_window(sent, q) >> (64 - kStepK)) : 0u;
+                const u32 t = sw ? static_cast<u32>(__clz(sw)) - (32 - kStepK) : kStepK;
+                const u64 rem = q < n_text ? n_text - q : 0;
+                if (t < rem && t < kStepK) td = 2 * (depth + t) + 1;
+                else if (rem < kStepK) td = 2 * (depth + static_cast<u32>(rem));
+                if (td != kTdNone) s_td[a] = static_cast<unsigned short>(td);
             }
+            u32 left = kStepK;                  // real symbols in the window
+            u32 ord = kOrdNone;
+            if (td != kTdNone) {
+                const u32 t = td >> 1;          // >= depth, except for the 9- and 10-symbol suffixes of the first step
+                const u32 rest = t > depth ? t - depth : 0u;
+                if (rest < left) left = rest;
+                ord = td + 2 * kElemK - 2 * depth;   // 2 * (t - depth) + kind, biased so that it stays >= 0
+            }
+            u32 b = left ? bases16(packed, q) : 0u;
+            if (left < kStepK) b = left ? b & ~((1u << (2 * (kStepK - left))) - 1u) : 0u;
+            s_key[a] = (((static_cast<u64>(b) << kOrdBits) | ord) << kSlotBits) | static_cast<u32>(a);
         }
         __syncthreads();
 
@@ -655,9 +672,11 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
             const u64 ki = s_key[a];
             u32 r0 = 0, r1 = 0;
             int j = gs;
+            if (j & 1) { r0 += s_key[j] < ki; ++j; }
             for (; j + 1 < ge; j += 2) {   // every member of the group runs the same trip count
-                r0 += s_key[j] < ki;
-                r1 += s_key[j + 1] < ki;
+                const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key + j);
+                r0 += k2.x < ki;
+                r1 += k2.y < ki;
             }
             if (j < ge) r0 += s_key[j] < ki;
             const int dst = gs + static_cast<int>(r0 + r1);
@@ -666,74 +685,20 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
         }
         __syncthreads();
 
-        // -- distance step: compare with the group's longest member; text step: new heads ---------
-        for (int u = tid; u < cnt; u += kRefBlock) {
-            const int a = s_list[u];
-            const int dst = s_dst[u];
-            if (dstep) {
-                if (!verify) continue;
-                const u32 ord = static_cast<u32>(s_key[a] >> kTextSlotBits);
-                const int ge = group_end(a);
-                const int ra = s_src[ge - 1];     // last in the new order: the longest member
-                bool ok = ord != kOrdNone && static_cast<u32>(s_key[ra] >> kTextSlotBits) != kOrdNone;
-                // symbols of this suffix still to be confirmed: [depth, tdist); tdist = ord - kElemK
-                if (ok && ra != a && ord > depth + kElemK) {
-                    const u64 qa = static_cast<u64>(s_pos[a]) + depth;
-                    const u64 qr = static_cast<u64>(s_pos[ra]) + depth;
-                    const u64 qe = qa + (ord - kElemK - depth);       // end of the stretch (exclusive)
-                    const u64 w_first = qa >> 5, w_last = (qe - 1) >> 5;
-                    for (u64 w = w_first & ~1ull; w <= w_last && ok; w += 2) {
-                        u64 own[2];
-                        ld_words2(packed + w, own[0], own[1]);
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const u64 wb = (w + h) << 5;                 // first base of this word
-                            if (w + h < w_first || w + h > w_last) continue;
-                            const u64 lo = wb > qa ? wb : qa;
-                            const u64 hi = wb + 32 < qe ? wb + 32 : qe;
-                            const unsigned sh = static_cast<unsigned>(lo - wb) * 2;
-                            const unsigned nb = static_cast<unsigned>(hi - lo) * 2;   // 2..64 bits
-                            const u64 mine = own[h] << sh;
-                            const u64 theirs = base_window(packed, qr + (lo - qa));
-                            ok = ok && ((mine ^ theirs) >> (64 - nb)) == 0;
-                        }
-                    }
-                }
-                if (!ok) atomicOr(&s_fail[(ge - 1) >> 5], 1u << ((ge - 1) & 31));
-            } else {
-                // a suffix starts a group iff its content differs from its predecessor's in the
-                // new order, or it carries a terminator (unique by construction)
-                const bool opens = (s_bits[dst >> 5] >> (dst & 31)) & 1u;  // slot dst starts the group
-                const u64 ki = s_key[a] >> kTextSlotBits;
-                bool head = (static_cast<u32>(ki) & kFieldMask) != kFull;
-                if (!head && !opens) head = (s_key[s_src[dst - 1]] >> kTextSlotBits) != ki;
-                if (head) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
-            }
-        }
-        __syncthreads();
-
-        // -- permute (the key buffer is dead after its last reads here: it receives the new order) --
-        bool head_me[(kRefCap + kRefBlock - 1) / kRefBlock];
+        // -- subgroup heads: the 16 bases differ from the predecessor's in the new order -------------
+        bool sub_head[(kRefCap + kRefBlock - 1) / kRefBlock];
 #pragma unroll
         for (int i = 0; i < (kRefCap + kRefBlock - 1) / kRefBlock; ++i) {
             const int u = tid + i * kRefBlock;
-            head_me[i] = false;
-            if (u < cnt && dstep) {
-                const int a = s_list[u];
+            sub_head[i] = false;
+            if (u < cnt) {
                 const int dst = s_dst[u];
-                const int ge = group_end(a);
-                const bool failed = !verify || ((s_fail[(ge - 1) >> 5] >> ((ge - 1) & 31)) & 1u);
-                if (!failed) head_me[i] = true;   // verified: every member is final
-                else {
-                    // final: what terminates before `depth`; the first of the others opens their group
-                    const u32 ord = static_cast<u32>(s_key[a] >> kTextSlotBits);
-                    const bool opens = (s_bits[dst >> 5] >> (dst & 31)) & 1u;
-                    head_me[i] = ord < kPShortEnd ||
-                                 (!opens && static_cast<u32>(s_key[s_src[dst - 1]] >> kTextSlotBits) < kPShortEnd);
-                }
+                if (!is_head(dst))
+                    sub_head[i] = (s_key[s_src[dst - 1]] >> (kOrdBits + kSlotBits)) != (s_key[s_list[u]] >> (kOrdBits + kSlotBits));
             }
         }
         __syncthreads();
+        // -- permute (the key buffer is dead: it receives the new order) ---------------------------
 #pragma unroll
         for (int i = 0; i < (kRefCap + kRefBlock - 1) / kRefBlock; ++i) {
             const int u = tid + i * kRefBlock;
@@ -741,32 +706,88 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
                 const int a = s_list[u];
                 const int dst = s_dst[u];
                 s_pos2[dst] = s_pos[a];
-                s_p2[dst] = s_p[a];
-                if (head_me[i]) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
+                s_td2[dst] = s_td[a];
+                if (sub_head[i]) atomicOr(&s_new[dst >> 5], 1u << (dst & 31));
             }
         }
         __syncthreads();
         for (int u = tid; u < cnt; u += kRefBlock) {
             const int a = s_list[u];
             s_pos[a] = s_pos2[a];
-            s_p[a] = s_p2[a];
+            s_td[a] = s_td2[a];
         }
         if (tid < kRefWords) {
             s_bits[tid] |= s_new[tid];
             s_new[tid] = 0;
         }
         __syncthreads();
-        if (!dstep) {
-            ++rounds;
-            depth += kTextK;
+
+        // -- prefix check: the member now in slot a against the last (= longest) of its subgroup ----
+        const u32 depth2 = depth + kStepK;
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            const int ge = group_end(a);
+            s_dst[u] = static_cast<unsigned short>(ge);
+            if (!use_shortcut) continue;
+            if (is_head(a) && ge == a + 1) continue;     // alone in its subgroup
+            const int ra = ge - 1;
+            const u32 td = s_td[a], tr = s_td[ra];
+            bool ok = td != kTdNone && tr != kTdNone;
+            // symbols of this suffix still to be confirmed: [depth2, t)
+            if (ok && ra != a && (td >> 1) > depth2) {
+                const u64 qa = static_cast<u64>(s_pos[a]) + depth2;
+                const u64 qr = static_cast<u64>(s_pos[ra]) + depth2;
+                const u64 qe = static_cast<u64>(s_pos[a]) + (td >> 1);   // end of the stretch (exclusive)
+                const u64 w_first = qa >> 5, w_last = (qe - 1) >> 5;
+                for (u64 w = w_first & ~1ull; w <= w_last && ok; w += 2) {
+                    u64 own[2];
+                    ld_words2(packed + w, own[0], own[1]);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const u64 wb = (w + h) << 5;                 // first base of this word
+                        if (w + h < w_first || w + h > w_last) continue;
+                        const u64 lo = wb > qa ? wb : qa;
+                        const u64 hi = wb + 32 < qe ? wb + 32 : qe;
+                        const unsigned sh = static_cast<unsigned>(lo - wb) * 2;
+                        const unsigned nb = static_cast<unsigned>(hi - lo) * 2;   // 2..64 bits
+                        const u64 mine = own[h] << sh;
+                        const u64 theirs = base_window(packed, qr + (lo - qa));
+                        ok = ok && ((mine ^ theirs) >> (64 - nb)) == 0;
+                    }
+                }
+            }
+            if (!ok) atomicOr(&s_fail[ra >> 5], 1u << (ra & 31));
         }
+        __syncthreads();
+
+        // -- new heads: a confirmed subgroup is final; in the others, what terminates inside the
+        //    16 bases is final and the first of the rest opens what stays tied ----------------------
+        for (int u = tid; u < cnt; u += kRefBlock) {
+            const int a = s_list[u];
+            if (is_head(a)) continue;
+            const int ra = s_dst[u] - 1;
+            bool head;
+            if (use_shortcut && !((s_fail[ra >> 5] >> (ra & 31)) & 1u)) head = true;
+            else {
+                const u32 tp = s_td[a - 1];     // the predecessor is in the same subgroup
+                head = tp != kTdNone && (tp >> 1) < depth2;   // (this suffix itself terminates later, or also inside)
+            }
+            if (head) atomicOr(&s_new[a >> 5], 1u << (a & 31));
+        }
+        __syncthreads();
+        if (tid < kRefWords) {
+            s_bits[tid] |= s_new[tid];
+            s_new[tid] = 0;
+        }
+        __syncthreads();
+        depth = depth2;
     }
 
     // write the tile's suffixes once; count what is still tied
     u32 nonheads = 0;
     for (int a = first + tid; a < end; a += kRefBlock) {
         sa_out[t0 + a] = s_pos[a];
-        nonheads += !((s_bits[a >> 5] >> (a & 31)) & 1u);
+        nonheads += !is_head(a);
     }
     for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
     if (lane == 0 && nonheads) atomicAdd(counters, nonheads);
