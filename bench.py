@@ -305,6 +305,7 @@ def main():
         "init_elems_kernel": 8.375, "onesweep_u64_keys": 16.0, "onesweep_u64_pack_iota": 12.0,
         "refine_elems_kernel": 13.4, "window_scatter_kernel": 12.0, "scatter_records_kernel": 12.0,
         "inverse_kernel": 8.0, "pair_key_kernel": 20.0, "rerank_kernel": 16.0, "hist_kernel": 4.0,
+        "gen_uniform_kernel": 8.25, "link_reads_kernel": 8.0, "refine_uniform_kernel": 12.125,
     }
     ncu_traffic = {"refine_text_kernel": 1.259e9}  # dram read+write per launch, profiles/r1_ncu_refine.txt
     kernels = {}

@@ -49,6 +49,7 @@ struct reseq_cuda_ctx {
     int opt_inverse_lo_bits = -1;  // extra partition bits before the inverse scatter (-1 = auto)
     int opt_shortcut = 1;      // sentinel-distance shortcut in the refine kernel (tuning / tests)
     int opt_sort_cfg = 0;      // onesweep tile shape (0 = default tuning)
+    int opt_uniform = 1;       // transposed-record path for uniform read sets (0: general paths only)
     int opt_text_rounds = 16;  // max text-window refinement rounds before prefix doubling takes over
 
     // Grow-only bump arena.  begin() rewinds it; alloc() carves 256-byte aligned

@@ -347,6 +347,10 @@ constexpr u32 kPMaxNear = 253;              // largest payload that encodes a di
 constexpr u32 kPFar = 254;
 constexpr u32 kPEot = 255;
 
+constexpr int kUniK = 15;                   // uniform read sets: symbols shared inside a group
+constexpr u32 kUniMinPeriod = 17, kUniMaxPeriod = 255;   // read length + 1 the uniform path accepts
+constexpr int kUniReads = 64;               // reads per CTA of the record generator
+
 constexpr int kRefBlock = 256;
 constexpr int kRefTile = 2048;
 constexpr int kRefExt = 640;
@@ -456,10 +460,28 @@ __device__ __forceinline__ u32 bases16(const u64* __restrict__ packed, u64 q) {
 // the total order asks for where two suffixes are identical up to their sentinels.
 // Every step first compacts the still-tied suffixes into a dense list (order preserving, so a
 // group stays contiguous): late steps cost in proportion to what is left.
+//
+// UNI: the records of a uniform read set (gen_uniform_kernel below): 15 shared symbols, groups
+// already in (terminator distance, position) order, and a bitmap `cov` of the positions that
+// link_reads_kernel proved to be a prefix of a LONGER suffix of their own group.  A group all of
+// whose members but the last carry that proof is final as it stands -- every chain of witnesses
+// ends in the last member, so all members are prefixes of it and (distance, position) is their
+// order -- and never enters the step loop; in the loop the same proof replaces the base-by-base
+// comparison.  The terminator distance is arithmetic there: period - 1 - pos mod period.
+template <bool UNI>
 __global__ void __launch_bounds__(kRefBlock)
 refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n_text,
                     const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
-                    int max_rounds, bool use_shortcut, u32* __restrict__ counters) {
+                    int max_rounds, bool use_shortcut, u32* __restrict__ counters,
+                    const u32* __restrict__ cov, u32 period, u64 period_magic) {
+    constexpr int KSYM = UNI ? kUniK : kElemK;             // symbols every member of a group shares
+    constexpr int KEYSHIFT = UNI ? 33 : kElemKeyShift;     // record bits above this are the group key
+    constexpr u32 ESCBIT = UNI ? (kElemEscBit >> 1) : kElemEscBit;
+    auto term_dist = [&](u32 pos) -> u32 {   // UNI only: symbols before the read's sentinel
+        const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
+        return period - 1u - (pos - q * period);
+    };
+    auto covered = [&](u32 pos) -> bool { return (__ldg(cov + (pos >> 5)) >> (pos & 31)) & 1u; };
     // n_text: length of the text the positions refer to; m: number of records (equal for a
     // whole-text build, a bucket of it for a multi-GPU rank)
     extern __shared__ __align__(16) unsigned char ref_smem[];
@@ -484,12 +506,12 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     const int avail = static_cast<int>(m - t0 < static_cast<u64>(kRefCap) ? m - t0 : kRefCap);  // records behind t0
 
     if (tid == 0) { s_first = 0x7fffffff; s_end = 0x7fffffff; s_last = -1; }
-    for (int j = tid; j < kRefWords; j += kRefBlock) { s_bits[j] = 0; s_new[j] = 0; }
+    for (int j = tid; j < kRefWords; j += kRefBlock) { s_bits[j] = 0; s_new[j] = 0; s_fail[j] = 0; }
 
     // -- load the tile's records plus the first stretch behind it; group heads from adjacent keys.
     //    The window grows only while the tile's last group has not ended (rare). ------------------
     int loaded = 0;
-    const u32 prev_key = t0 > 0 ? static_cast<u32>(elems[t0 - 1] >> kElemKeyShift) : 0xffffffffu;
+    const u32 prev_key = t0 > 0 ? static_cast<u32>(elems[t0 - 1] >> KEYSHIFT) : 0xffffffffu;
     for (int want = lim + kRefBlock < avail ? lim + kRefBlock : avail;;) {
         for (int j = loaded + tid; j < want; j += kRefBlock) s_key[j] = elems[t0 + j];
         __syncthreads();
@@ -497,9 +519,9 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
             const int j = j0 + tid;
             bool head = false;
             if (j >= loaded && j < want) {
-                const u32 k = static_cast<u32>(s_key[j] >> kElemKeyShift);
-                const u32 kp = j > 0 ? static_cast<u32>(s_key[j - 1] >> kElemKeyShift) : prev_key;
-                head = k != kp || !(k & kElemEscBit) || (t0 == 0 && j == 0);   // no escape bit: finished by the sort
+                const u32 k = static_cast<u32>(s_key[j] >> KEYSHIFT);
+                const u32 kp = j > 0 ? static_cast<u32>(s_key[j - 1] >> KEYSHIFT) : prev_key;
+                head = k != kp || !(k & ESCBIT) || (t0 == 0 && j == 0);   // no escape bit: finished by the sort
             }
             const unsigned b = __ballot_sync(0xffffffffu, head);
             if (lane == 0 && b) atomicOr(&s_bits[j >> 5], b);
@@ -546,6 +568,12 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     for (int a = first + tid; a < end; a += kRefBlock) {
         const u64 e = s_key[a];
         const u32 pos = static_cast<u32>(e);
+        if constexpr (UNI) {
+            const u32 t = term_dist(pos);
+            s_pos[a] = pos;
+            s_td[a] = static_cast<unsigned short>(2 * t + 1);   // period <= 255: always known
+            continue;
+        }
         const u32 p = static_cast<u32>(e >> 32) & 0xffu;
         u32 td;
         if (p < kPShortEnd) td = p;
@@ -601,7 +629,53 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     };
     auto is_head = [&](int a) { return (s_bits[a >> 5] >> (a & 31)) & 1u; };
 
-    u32 depth = kElemK;
+    if constexpr (UNI) {
+        // -- groups that are final as they stand.  Uncovered = no proof of being a prefix of a later
+        //    member: suffixes shorter than the shared symbols are prefixes of every longer member by
+        //    the zero padding of the key, the others need their bit in `cov`.  The last member of a
+        //    group needs no proof. ------------------------------------------------------------------
+        for (int j0 = first & ~31; j0 < end; j0 += kRefBlock) {
+            const int a = j0 + tid;
+            bool unc = false;
+            if (a >= first && a < end) {
+                const bool last = is_head(a + 1);
+                if (!last) unc = (s_td[a] >> 1) >= static_cast<u32>(KSYM) && !covered(s_pos[a]);
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, unc);
+            if (lane == 0 && b) s_new[a >> 5] = b;    // one warp per word per sweep
+        }
+        __syncthreads();
+        for (int j = tid; j < kRefWords; j += kRefBlock) {   // a group with an uncovered member stays tied
+            u32 w = s_new[j];
+            while (w) {
+                const int a = j * 32 + __ffs(w) - 1;
+                w &= w - 1;
+                const int gs = group_start(a), ge = group_end(a);
+                for (int x = gs >> 5; x <= (ge - 1) >> 5; ++x) {
+                    u32 mk = 0xffffffffu;
+                    if (x == (gs >> 5)) mk &= 0xffffffffu << (gs & 31);
+                    if (x == ((ge - 1) >> 5)) mk &= 0xffffffffu >> (31 - ((ge - 1) & 31));
+                    atomicOr(&s_fail[x], mk);
+                }
+            }
+        }
+        __syncthreads();
+        for (int j = tid; j < kRefWords; j += kRefBlock) {
+            const int base = j * 32;
+            u32 own = 0xffffffffu;
+            if (base + 32 <= first || base >= end) own = 0;
+            else {
+                if (base < first) own &= 0xffffffffu << (first - base);
+                if (base + 32 > end) own &= (1u << (end - base)) - 1u;
+            }
+            s_bits[j] |= ~s_fail[j] & own;   // every member of a clean group is final: a head
+            s_new[j] = 0;
+            s_fail[j] = 0;
+        }
+        __syncthreads();
+    }
+
+    u32 depth = KSYM;
     int rounds = 0;
     for (; rounds < max_rounds; ++rounds) {
         // -- compact the tied slots, in order ------------------------------------------------
@@ -657,7 +731,7 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
                 const u32 t = td >> 1;          // >= depth, except for the 9- and 10-symbol suffixes of the first step
                 const u32 rest = t > depth ? t - depth : 0u;
                 if (rest < left) left = rest;
-                ord = td + 2 * kElemK - 2 * depth;   // 2 * (t - depth) + kind, biased so that it stays >= 0
+                ord = td + 2 * KSYM - 2 * depth;   // 2 * (t - depth) + kind, biased so that it stays >= 0
             }
             u32 b = left ? bases16(packed, q) : 0u;
             if (left < kStepK) b = left ? b & ~((1u << (2 * (kStepK - left))) - 1u) : 0u;
@@ -731,6 +805,9 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
             if (!use_shortcut) continue;
             if (is_head(a) && ge == a + 1) continue;     // alone in its subgroup
             const int ra = ge - 1;
+            if constexpr (UNI) {
+                if (ra != a && covered(s_pos[a])) continue;   // a proven prefix of a later member of this subgroup
+            }
             const u32 td = s_td[a], tr = s_td[ra];
             bool ok = td != kTdNone && tr != kTdNone;
             // symbols of this suffix still to be confirmed: [depth2, t)
@@ -792,6 +869,108 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
     if (lane == 0 && nonheads) atomicAdd(counters, nonheads);
     if (tid == 0) atomicMax(counters + 2, static_cast<u32>(rounds));
+}
+
+// ---- uniform read sets: records born in (terminator distance, position) order ---------------------
+//
+// A text of k reads of one length L (period P = L + 1: a sentinel at every position = P - 1 mod P,
+// nowhere else) is the shotgun read set of BASELINE.json.  Its records are generated TRANSPOSED:
+// record index t * k + r belongs to the suffix of read r with t symbols before its sentinel, so
+// the stable LSD sort leaves every group in (t, position) order -- which is the final order of a
+// group whose members all cover one locus (each is a prefix of the longer ones).  Record:
+//     key32 << 32 | pos
+//   key32  bits 31..8: bases 0..11, zero padded from the sentinel on.
+//          low byte, t <= 12:  2 t + 1 (< 0x80): finished by the sort, as in the general records
+//          low byte, t >= 13:  0x80 | bases 12..14 (zero padded) << 1 | S,  S = 1 for a whole read
+//          (t = L).  S is not a sort bit: the passes cover record bits 33..63.
+// 15 shared symbols instead of 11: a 4.6 Mbp genome has 4.6 M loci against 4^15 = 1.07 G keys, so
+// a group is one locus but for chance repeats; the fourth digit pass buys groups that need no
+// sorting at all.
+
+__global__ void uniform_check_kernel(const u64* __restrict__ sent, u32 period, u64 k, u32* __restrict__ bad) {
+    const u64 r = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= k) return;
+    const u64 p = r * period + period - 1;
+    if (!((sent[p >> 6] >> (63 - (p & 63))) & 1ull)) atomicAdd(bad, 1u);   // k sentinels in all: all are here or one is not
+}
+
+__global__ void __launch_bounds__(256)
+gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u64* __restrict__ elems,
+                   u32* __restrict__ g_hist) {
+    __shared__ u64 s_w[kUniReads * kUniMaxPeriod / 32 + 4];
+    __shared__ u32 s_hist[4 * kRadix];
+    for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kUniReads;
+    const u32 nr = static_cast<u32>(k - r0 < kUniReads ? k - r0 : kUniReads);
+    const u64 base0 = r0 * period;
+    const u64 w0 = base0 >> 5;
+    const u32 off0 = static_cast<u32>(base0 & 31);
+    const u32 nw = static_cast<u32>(((base0 + static_cast<u64>(nr) * period + 31) >> 5) - w0) + 2;   // the packed array is padded
+    for (u32 i = threadIdx.x; i < nw; i += blockDim.x) s_w[i] = packed[w0 + i];
+    __syncthreads();
+    const u32 total = kUniReads * period;
+    for (u32 idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const u32 rl = idx & (kUniReads - 1), t = idx / kUniReads;    // lanes = consecutive reads: coalesced stores
+        if (rl >= nr) continue;
+        const u32 pl = rl * period + (period - 1 - t);
+        const u32 bit = 2 * (off0 + pl);
+        const u32 wi = bit >> 6, sh = bit & 63;
+        const u64 hi = s_w[wi], lo = s_w[wi + 1];
+        const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+        u32 b15 = static_cast<u32>(win >> 34);                          // 15 bases
+        if (t < kUniK) b15 &= ~((1u << (2 * (kUniK - t))) - 1u);        // zero padded from the sentinel on
+        const u32 low = t <= 12 ? 2 * t + 1 : (kElemEscBit | ((b15 & 0x3fu) << 1) | (t == period - 1 ? 1u : 0u));
+        const u32 key = ((b15 >> 6) << 8) | low;
+        const u64 pos = (r0 + rl) * period + (period - 1 - t);
+        elems[static_cast<u64>(t) * k + r0 + rl] = (static_cast<u64>(key) << 32) | pos;
+        atomicAdd(&s_hist[(key >> 1) & 0x7fu], 1u);
+        atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
+        atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
+        atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
+    }
+    __syncthreads();
+    hist_flush(s_hist, g_hist, 4);
+}
+
+// Proofs for refine_elems_kernel<true>.  In a sorted group the predecessors of a whole read b
+// (S = 1, t = L) are the suffixes of the reads that started before it on the same locus; the nearest
+// one, a = (read r, offset d), is compared with b over its whole length t_a.  If equal, every
+// position of r from d on is a prefix of the suffix the same distance into b -- a longer member of
+// its own group (it shares all of the shorter one's symbols) -- and gets its bit in `cov`.  One
+// comparison per read pays for the ~L suffix comparisons it stands for.  Candidates of other loci
+// (chance repeats of the 15 symbols) fail the comparison and are passed over.
+__global__ void __launch_bounds__(256)
+link_reads_kernel(const u64* __restrict__ elems, u64 m, const u64* __restrict__ packed, u32 period,
+                  u64 period_magic, u32* __restrict__ cov) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const u64 e = elems[i];
+        if ((static_cast<u32>(e >> 32) & 0x81u) != 0x81u) continue;   // a whole read among the escape records
+        const u32 pos_b = static_cast<u32>(e);
+        for (u64 s = 1; s <= 16 && s <= i; ++s) {
+            const u64 ea = elems[i - s];
+            if ((ea >> 33) != (e >> 33)) break;
+            const u32 pos_a = static_cast<u32>(ea);
+            const u32 q = static_cast<u32>(__umul64hi(pos_a, period_magic));
+            const u32 t_a = period - 1u - (pos_a - q * period);       // <= L: the group is in (t, pos) order
+            bool ok = true;
+            for (u32 c = 0; c < t_a && ok; c += 32) {
+                const u64 wa = base_window(packed, static_cast<u64>(pos_a) + c);
+                const u64 wb = base_window(packed, static_cast<u64>(pos_b) + c);
+                const u32 nb = t_a - c < 32 ? t_a - c : 32;
+                ok = ((wa ^ wb) >> (64 - 2 * nb)) == 0;
+            }
+            if (!ok) continue;
+            const u32 lo = pos_a, hi = pos_a + t_a - 1;                // bits [lo, hi]
+            for (u32 w = lo >> 5; w <= hi >> 5; ++w) {
+                u32 mk = 0xffffffffu;
+                if (w == lo >> 5) mk &= 0xffffffffu << (lo & 31);
+                if (w == hi >> 5) mk &= 0xffffffffu >> (31 - (hi & 31));
+                atomicOr(cov + w, mk);
+            }
+            break;
+        }
+    }
 }
 
 // rank = inverse permutation of sa.  A direct scatter rank[sa[i]] = i is n random 4-byte
@@ -915,6 +1094,7 @@ size_t sa_workspace_bytes(size_t n) {
     total += pad(sizeof(u32) * n);                   // rank when the caller wants none
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
+    total += pad(sizeof(u32) * (n / 32 + 2));        // proof bitmap of the uniform read-set path
     total += sort_workspace_bytes(n);
     return total + 4096;
 }
@@ -989,15 +1169,15 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     st->sort_passes += pt.count;
     static bool configured = false;
     if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kRefSmem)));
         configured = true;
     }
     RSQ_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(u32), s));
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
-    refine_elems_kernel<<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m, sa_out,
-                                                           max_rounds, use_shortcut, counters);
+    refine_elems_kernel<false><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m,
+                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -1008,6 +1188,62 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
         std::fprintf(stderr, "[reseq] refine: records=%zu tied_left=%u oversize=%u text_steps=%u\n", m, c[0], c[1], c[2]);
     st->rounds += c[2];
     st->refined_tile += m;
+    return RESEQ_OK;
+}
+
+// The uniform read-set path: transposed records, four digit passes, one comparison per read, groups
+// accepted as they stand.  *unfinished != 0 (a read set that is not uniform after all, an oversize
+// group, a step limit) sends the caller to the general paths.
+int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
+                            u64* elems_a, u64* elems_b, u32* cov, u32* sa_out, int max_rounds, u32* counters,
+                            const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
+    cudaStream_t s = ctx->stream;
+    const u64 magic = ~0ull / period + 1;   // ceil(2^64 / period): floor(pos / period) = mulhi(pos, magic) for pos < 2^32
+    RSQ_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(u32), s));
+    RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * 4 * kRadix, s));
+    RSQ_CUDA(cudaMemsetAsync(cov, 0, sizeof(u32) * (n / 32 + 2), s));
+    RSQ_LAUNCH_BEGIN(ctx, "uniform_check_kernel");
+    uniform_check_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, s>>>(sent, period, k, counters + 3);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_LAUNCH_BEGIN(ctx, "gen_uniform_kernel");
+    gen_uniform_kernel<<<static_cast<unsigned>((k + kUniReads - 1) / kUniReads), 256, 0, s>>>(packed, period, k, elems_a,
+                                                                                             ws.hist);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    PassTable pt{};
+    pt.count = 4;
+    const unsigned char shifts[4] = {33, 40, 48, 56}, bits[4] = {7, 8, 8, 8};
+    for (int p = 0; p < 4; ++p) { pt.shift[p] = shifts[p]; pt.bits[p] = bits[p]; }
+    bool in_b = false;
+    RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b));
+    st->sort_passes += pt.count;
+    const u64* sorted = in_b ? elems_b : elems_a;
+    RSQ_LAUNCH_BEGIN(ctx, "link_reads_kernel");
+    link_reads_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sorted, n, packed, period, magic, cov);
+    RSQ_LAUNCH_END(ctx);
+    static bool configured = false;
+    if (!configured) {
+        RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kRefSmem)));
+        configured = true;
+    }
+    const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
+    RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
+    refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sorted, n, sa_out, max_rounds, true,
+                                                                 counters, cov, period, magic);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    const volatile u32* c = reinterpret_cast<volatile u32*>(ctx->pinned);
+    *unfinished = static_cast<u64>(c[0]) + (c[1] ? 1u : 0u) + c[3];
+    if (std::getenv("RESEQ_DEBUG"))
+        std::fprintf(stderr, "[reseq] uniform refine: n=%zu period=%u tied_left=%u oversize=%u steps=%u misplaced_sentinels=%u\n",
+                     n, period, c[0], c[1], c[2], c[3]);
+    if (*unfinished == 0) {
+        st->rounds += c[2];
+        st->refined_tile += n;
+    }
     return RESEQ_OK;
 }
 
@@ -1035,8 +1271,9 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     const size_t rank_tiles = (n + kRankTile - 1) / kRankTile;
     u64* desc = ctx->alloc<u64>(rank_tiles + 4);
     u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads, [4..7] refine
+    u32* cov = ctx->alloc<u32>(n / 32 + 2);
     SortWorkspace ws;
-    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters)
+    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !cov)
         return fail(RESEQ_OUT_OF_MEMORY, "suffix-array workspace does not fit the reserved arena");
     RSQ_TRY(sort_workspace_carve(ctx, n, &ws));
 
@@ -1049,6 +1286,23 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     // on sentinel-free texts no group could use it.
     const bool use_shortcut = ctx->opt_shortcut != 0 && n_separators * 1024 >= n;
     st.alphabet = dna ? 0 : 1;
+
+    // -- uniform read sets (k reads of one length, the shotgun configurations): transposed records,
+    //    4 digit passes, groups accepted in (terminator distance, position) order ------------------
+    if (dna && ctx->opt_text_rounds > 0 && ctx->opt_uniform != 0 && n_separators > 0 && n % n_separators == 0 &&
+        n / n_separators >= kUniMinPeriod && n / n_separators <= kUniMaxPeriod) {
+        u64 unfinished = 0;
+        RSQ_TRY(uniform_sort_and_refine(ctx, packed, sent, n, static_cast<u32>(n / n_separators), n_separators, keys_a,
+                                        keys_b, cov, d_sa, ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
+        if (unfinished == 0) {
+            st.init_symbols = kUniK;
+            RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, ws));
+            st.kernel_launches = ctx->launches - launches0;
+            if (stats) *stats = st;
+            return RESEQ_OK;
+        }
+        st.sort_passes = 0;   // not uniform after all, or a group the window cannot hold: the general paths
+    }
 
     // -- DNA fast path: 12-base records, 3 digit passes, groups finished from the L2-resident text --
     if (dna && ctx->opt_text_rounds > 0) {

@@ -32,6 +32,15 @@ def no_shortcut_executor(rq):
     return _doubling["ns"]
 
 
+def no_uniform_executor(rq):
+    """A fourth context: the uniform read-set path switched off (general records, 11 shared symbols)."""
+    if "nu" not in _doubling:
+        e = rq.Executor(0)
+        e.set_option("sa_uniform", 0)
+        _doubling["nu"] = e
+    return _doubling["nu"]
+
+
 def check(rq, ex, oracle, text):
     got = rq.build_parallel(text, ex)
     wsa, wrank = oracle.build_sa(text)
@@ -44,6 +53,10 @@ def check(rq, ex, oracle, text):
         assert np.array_equal(alt.rank, wrank)
         alt = rq.build_parallel(text, no_shortcut_executor(rq))
         assert np.array_equal(alt.sa, wsa), f"text-round sa differs for text of length {len(text)}"
+        assert np.array_equal(alt.rank, wrank)
+        alt = rq.build_parallel(text, no_uniform_executor(rq))
+        assert alt.stats.init_symbols != 15
+        assert np.array_equal(alt.sa, wsa), f"general-record sa differs for text of length {len(text)}"
         assert np.array_equal(alt.rank, wrank)
     return got
 
@@ -140,8 +153,52 @@ def test_generic_byte_texts(rq, ex, oracle):
 def test_read_sets_against_the_oracle(rq, ex, oracle, G, L, k):
     text, _ = rq.synth_read_text(G, L, k)
     got = check(rq, ex, oracle, text)
-    assert got.stats.alphabet == 0 and got.stats.init_symbols == 11
+    assert got.stats.alphabet == 0 and got.stats.init_symbols == 15    # the uniform read-set path
     assert got.stats.rounds <= 6 and got.stats.refined_global == 0
+    alt = rq.build_parallel(text, no_uniform_executor(rq))
+    assert alt.stats.init_symbols == 11 and np.array_equal(alt.sa, got.sa)
+
+
+def _reads(genome, L, starts):
+    return b"".join(genome[int(s):int(s) + L] + b"\0" for s in starts)
+
+
+def test_uniform_read_sets_with_repeats_and_duplicates(rq, ex, oracle):
+    """The uniform path's proofs (one comparison per read) under stress: repeated genomes (several
+    loci per 15-mer group), duplicate reads, low-complexity genomes, tiny and maximal periods."""
+    rng = np.random.default_rng(77)
+    for G, L, k, alpha in [(400, 40, 600, 4), (3000, 100, 2000, 4), (300, 16, 900, 2), (5000, 254, 400, 4),
+                           (2000, 60, 1500, 2), (64, 30, 500, 4), (20000, 150, 4000, 4)]:
+        letters = [65, 67, 71, 84][:alpha]
+        unit = bytes(rng.choice(letters, G).astype(np.uint8))
+        for genome in (unit, unit[:G // 2] * 2, unit[:G // 4] + unit[:G // 4][:-3] + b"A" * 3 + unit[G // 2:]):
+            starts = rng.integers(0, len(genome) - L + 1, k)
+            text = _reads(genome, L, starts)
+            got = check(rq, ex, oracle, text)
+            assert got.stats.alphabet == 0
+    # duplicates of whole reads, reads that differ only in their last base
+    g = bytes(rng.choice([65, 67, 71, 84], 500).astype(np.uint8))
+    reads = [g[i:i + 50] for i in rng.integers(0, 450, 300)]
+    reads += reads[:100] + [r[:-1] + b"A" for r in reads[:100]] + [b"C" + r[1:] for r in reads[:50]]
+    check(rq, ex, oracle, b"".join(r + b"\0" for r in reads))
+
+
+def test_texts_that_only_look_uniform(rq, ex, oracle):
+    """n divisible by the number of sentinels, but the sentinels are not one period apart: the check
+    kernel must hand the text to the general paths."""
+    rng = np.random.default_rng(78)
+    g = bytes(rng.choice([65, 67, 71, 84], 4000).astype(np.uint8))
+    reads = []
+    for i in range(400):
+        L = 30 if i % 2 else 50          # mean period 41
+        s = int(rng.integers(0, 3900))
+        reads.append(g[s:s + L] + b"\0")
+    got = check(rq, ex, oracle, b"".join(reads))
+    assert got.stats.init_symbols == 11
+    text = bytearray(b"".join(g[int(s):int(s) + 40] + b"\0" for s in rng.integers(0, 3900, 300)))
+    text[100], text[40] = 0, 65          # one sentinel moved
+    got = check(rq, ex, oracle, bytes(text))
+    assert got.stats.init_symbols == 11
 
 
 def test_reference_bench_input_fingerprint(rq, ex, oracle):
@@ -160,7 +217,7 @@ def test_config1_full_size_fingerprint_and_proof(rq, ex, oracle):
     permutation + adjacent-order verifier is a proof of equality at this size."""
     text, _ = rq.synth_read_text(1_000_000, 100, 100_000)
     got = rq.build_parallel(text, ex)
-    assert got.stats.rounds <= 4 and got.stats.refined_global == 0
+    assert got.stats.rounds <= 4 and got.stats.refined_global == 0 and got.stats.init_symbols == 15
     assert oracle.checksum_u32(got.sa) == 11642757783061468293
     assert oracle.verify_sa(text, got.sa) == 0
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
