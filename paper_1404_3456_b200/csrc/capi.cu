@@ -156,6 +156,10 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     RSQ_CUDA(cudaMallocHost(&ctx->pinned, 4096));
     if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
     if (const char* e = std::getenv("RESEQ_INVERSE_LO_BITS")) ctx->opt_inverse_lo_bits = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_LOOKAHEAD")) {
+        const int v = std::atoi(e);
+        if (v >= 1 && v <= 8) ctx->opt_lookahead = v;
+    }
     if (const char* e = std::getenv("RESEQ_SA_UNIFORM")) ctx->opt_uniform = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SHORTCUT")) ctx->opt_shortcut = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);

@@ -77,7 +77,7 @@ static int launch_pass_kernel(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, 
     const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
     RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL, LOAD>()));
     kern<<<static_cast<unsigned>(tiles), BLOCK, Cfg::kSmem, ctx->stream>>>(
-        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket);
+        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, ctx->opt_lookahead);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;

@@ -23,6 +23,7 @@ namespace rsq {
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kMaxPasses = 32;  // chunked_radix_sort with digit_bits = 1 needs 32
+constexpr int kLookahead = 8;   // most look-back descriptors read per round trip (tuning: ctx->opt_lookahead)
 
 struct PassTable {
     int count;
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? 4 : (BLOCK <= 384 ? 3 :
 onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,
                 u32 mask, const u32* __restrict__ digit_base, u64* __restrict__ lookback,
-                u32* __restrict__ ticket) {
+                u32* __restrict__ ticket, int lookahead) {
     static_assert(BLOCK >= kRadix && BLOCK % 32 == 0, "one thread per digit is assumed");
     static_assert(LOAD == kLoadPlain || (sizeof(KeyT) == 8 && !HAS_VAL), "pack-iota feeds u64 keys only");
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
@@ -284,13 +285,23 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     if (tid < kRadix) {
         u32 excl = 0;
         if (tile > 0) {
+            // The walk meets the front of finished tiles about (L2 latency / tile issue interval)
+            // tiles back; read one descriptor per round trip and it costs that many round trips
+            // (ncu: 40 % of the pass stalled here).  `lookahead` descriptors are in flight at once.
             long long t = static_cast<long long>(tile) - 1;
-            for (;;) {
-                const u64 v = ld_relaxed_u64(lookback + static_cast<u64>(t) * kRadix + tid);
-                if ((v >> 62) == 0) continue;  // predecessor has not published yet
-                excl += static_cast<u32>(v);
-                if (v & kDescInclusive) break;
-                --t;
+            for (bool done = false; !done;) {
+                u64 v[kLookahead];
+#pragma unroll
+                for (int w = 0; w < kLookahead; ++w)
+                    if (w < lookahead)
+                        v[w] = t - w >= 0 ? ld_relaxed_u64(lookback + static_cast<u64>(t - w) * kRadix + tid) : kDescInclusive;
+#pragma unroll
+                for (int w = 0; w < kLookahead; ++w) {
+                    if (done || w >= lookahead || (v[w] >> 62) == 0) break;  // not published yet: poll again from here
+                    excl += static_cast<u32>(v[w]);
+                    --t;
+                    done = (v[w] & kDescInclusive) != 0;
+                }
             }
         }
         st_relaxed_u64(lookback + static_cast<u64>(tile) * kRadix + tid, kDescInclusive | (excl + total));
