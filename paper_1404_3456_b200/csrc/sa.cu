@@ -473,7 +473,8 @@ __global__ void __launch_bounds__(kRefBlock)
 refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n_text,
                     const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
                     int max_rounds, bool use_shortcut, u32* __restrict__ counters,
-                    const u32* __restrict__ cov, u32 period, u64 period_magic) {
+                    const u32* __restrict__ cov, u32 period, u64 period_magic,
+                    const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits) {
     constexpr int KSYM = UNI ? kUniK : kElemK;             // symbols every member of a group shares
     constexpr int KEYSHIFT = UNI ? 33 : kElemKeyShift;     // record bits above this are the group key
     constexpr u32 ESCBIT = UNI ? (kElemEscBit >> 1) : kElemEscBit;
@@ -508,6 +509,27 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     if (tid == 0) { s_first = 0x7fffffff; s_end = 0x7fffffff; s_last = -1; }
     for (int j = tid; j < kRefWords; j += kRefBlock) { s_bits[j] = 0; s_new[j] = 0; s_fail[j] = 0; }
 
+    if constexpr (UNI) {
+        // -- group heads and uncovered members of the window were found by accept_uniform_kernel ----
+        for (int j = tid; j < kRefWords; j += kRefBlock) {
+            u32 h = 0, u = 0;
+            if (j * 32 < avail) {
+                h = g_headbits[(t0 >> 5) + j];
+                u = g_uncbits[(t0 >> 5) + j];
+                if (j * 32 + 32 > avail) {
+                    const u32 mk = (1u << (avail - j * 32)) - 1u;
+                    h &= mk;
+                    u &= mk;
+                }
+            }
+            s_bits[j] = h;
+            s_new[j] = u;
+        }
+        __syncthreads();
+        if (tid == 0 && avail == static_cast<int>(m - t0) && avail < kRefWords * 32)
+            s_bits[avail >> 5] |= 1u << (avail & 31);   // position m acts as a head
+        __syncthreads();
+    } else {
     // -- load the tile's records plus the first stretch behind it; group heads from adjacent keys.
     //    The window grows only while the tile's last group has not ended (rare). ------------------
     int loaded = 0;
@@ -541,6 +563,7 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
         if (__syncthreads_or(ended) || loaded >= avail) break;
         want = loaded + kRefBlock < avail ? loaded + kRefBlock : avail;
     }
+    }
 
     // first / last head inside the tile, first head at or after its end
     for (int j = tid; j < kRefWords; j += kRefBlock) {
@@ -562,6 +585,26 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     if (end == 0x7fffffff) {          // the tile's last group overruns the window
         if (tid == 0) atomicOr(counters + 1, 1u);
         end = s_last;                 // that group is nobody's: the host rebuilds
+    }
+
+    if constexpr (UNI) {
+        // -- nothing uncovered in the groups this CTA owns: accept_uniform_kernel's output stands ----
+        bool any = false;
+        for (int j = tid; j < kRefWords; j += kRefBlock) {
+            const int base = j * 32;
+            u32 own = 0xffffffffu;
+            if (base + 32 <= first || base >= end) own = 0;
+            else {
+                if (base < first) own &= 0xffffffffu << (first - base);
+                if (base + 32 > end) own &= (1u << (end - base)) - 1u;
+            }
+            const u32 u = s_new[j] & own;
+            s_new[j] = u;
+            any |= u != 0;
+        }
+        if (!__syncthreads_or(any)) return;
+        for (int a = first + tid; a < end; a += kRefBlock) s_key[a] = elems[t0 + a];
+        __syncthreads();
     }
 
     // -- unpack the records this CTA owns: position, and 2 * t + kind from the terminator byte ----
@@ -634,17 +677,7 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
         //    member: suffixes shorter than the shared symbols are prefixes of every longer member by
         //    the zero padding of the key, the others need their bit in `cov`.  The last member of a
         //    group needs no proof. ------------------------------------------------------------------
-        for (int j0 = first & ~31; j0 < end; j0 += kRefBlock) {
-            const int a = j0 + tid;
-            bool unc = false;
-            if (a >= first && a < end) {
-                const bool last = is_head(a + 1);
-                if (!last) unc = (s_td[a] >> 1) >= static_cast<u32>(KSYM) && !covered(s_pos[a]);
-            }
-            const unsigned b = __ballot_sync(0xffffffffu, unc);
-            if (lane == 0 && b) s_new[a >> 5] = b;    // one warp per word per sweep
-        }
-        __syncthreads();
+        // (s_new holds the uncovered, not-last members of the owned groups)
         for (int j = tid; j < kRefWords; j += kRefBlock) {   // a group with an uncovered member stays tied
             u32 w = s_new[j];
             while (w) {
@@ -939,36 +972,129 @@ gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u64* __res
 // its own group (it shares all of the shorter one's symbols) -- and gets its bit in `cov`.  One
 // comparison per read pays for the ~L suffix comparisons it stands for.  Candidates of other loci
 // (chance repeats of the 15 symbols) fail the comparison and are passed over.
+constexpr int kLinkChunk = 32768;   // records scanned per CTA before the whole reads found are processed
+constexpr int kLinkQueue = 4096;
+
+__device__ __forceinline__ void link_one_read(const u64* __restrict__ elems, u64 i, const u64* __restrict__ packed,
+                                              u32 period, u64 period_magic, u32* __restrict__ cov) {
+    const u64 e = elems[i];
+    const u32 pos_b = static_cast<u32>(e);
+    for (u64 s = 1; s <= 16 && s <= i; ++s) {
+        const u64 ea = elems[i - s];
+        if ((ea >> 33) != (e >> 33)) break;
+        const u32 pos_a = static_cast<u32>(ea);
+        const u32 q = static_cast<u32>(__umul64hi(pos_a, period_magic));
+        const u32 t_a = period - 1u - (pos_a - q * period);       // <= L: the group is in (t, pos) order
+        bool ok = true;
+        for (u32 c = 0; c < t_a && ok; c += 32) {
+            const u64 wa = base_window(packed, static_cast<u64>(pos_a) + c);
+            const u64 wb = base_window(packed, static_cast<u64>(pos_b) + c);
+            const u32 nb = t_a - c < 32 ? t_a - c : 32;
+            ok = ((wa ^ wb) >> (64 - 2 * nb)) == 0;
+        }
+        if (!ok) continue;
+        const u32 lo = pos_a, hi = pos_a + t_a - 1;                // bits [lo, hi]
+        for (u32 w = lo >> 5; w <= hi >> 5; ++w) {
+            u32 mk = 0xffffffffu;
+            if (w == lo >> 5) mk &= 0xffffffffu << (lo & 31);
+            if (w == hi >> 5) mk &= 0xffffffffu >> (31 - (hi & 31));
+            atomicOr(cov + w, mk);
+        }
+        return;
+    }
+}
+
+// Whole reads are 1 record in period: a thread that stops to compare one stalls its warp for a
+// chain of dependent L2 loads.  Each CTA therefore streams a chunk of records, queues the whole
+// reads it meets in shared memory and then compares them with every lane busy.
 __global__ void __launch_bounds__(256)
 link_reads_kernel(const u64* __restrict__ elems, u64 m, const u64* __restrict__ packed, u32 period,
                   u64 period_magic, u32* __restrict__ cov) {
-    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
-        const u64 e = elems[i];
-        if ((static_cast<u32>(e >> 32) & 0x81u) != 0x81u) continue;   // a whole read among the escape records
-        const u32 pos_b = static_cast<u32>(e);
-        for (u64 s = 1; s <= 16 && s <= i; ++s) {
-            const u64 ea = elems[i - s];
-            if ((ea >> 33) != (e >> 33)) break;
-            const u32 pos_a = static_cast<u32>(ea);
-            const u32 q = static_cast<u32>(__umul64hi(pos_a, period_magic));
-            const u32 t_a = period - 1u - (pos_a - q * period);       // <= L: the group is in (t, pos) order
-            bool ok = true;
-            for (u32 c = 0; c < t_a && ok; c += 32) {
-                const u64 wa = base_window(packed, static_cast<u64>(pos_a) + c);
-                const u64 wb = base_window(packed, static_cast<u64>(pos_b) + c);
-                const u32 nb = t_a - c < 32 ? t_a - c : 32;
-                ok = ((wa ^ wb) >> (64 - 2 * nb)) == 0;
+    __shared__ u32 s_q[kLinkQueue];
+    __shared__ u32 s_n;
+    for (u64 base = static_cast<u64>(blockIdx.x) * kLinkChunk; base < m; base += static_cast<u64>(gridDim.x) * kLinkChunk) {
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const u32 cnt = static_cast<u32>(m - base < kLinkChunk ? m - base : kLinkChunk);
+        for (u32 j0 = threadIdx.x * 2; j0 < cnt; j0 += 2 * 256 * 4) {
+            ulonglong2 v[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const u32 j = j0 + c * 512;
+                v[c] = make_ulonglong2(0, 0);
+                if (j + 1 < cnt) v[c] = *reinterpret_cast<const ulonglong2*>(elems + base + j);   // base, j even: 16-byte aligned
+                else if (j < cnt) v[c].x = elems[base + j];
             }
-            if (!ok) continue;
-            const u32 lo = pos_a, hi = pos_a + t_a - 1;                // bits [lo, hi]
-            for (u32 w = lo >> 5; w <= hi >> 5; ++w) {
-                u32 mk = 0xffffffffu;
-                if (w == lo >> 5) mk &= 0xffffffffu << (lo & 31);
-                if (w == hi >> 5) mk &= 0xffffffffu >> (31 - (hi & 31));
-                atomicOr(cov + w, mk);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const u32 j = j0 + c * 512;
+                const u64 e2[2] = {v[c].x, v[c].y};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if ((static_cast<u32>(e2[h] >> 32) & 0x81u) != 0x81u) continue;   // a whole read among the escape records
+                    const u32 slot = atomicAdd(&s_n, 1u);
+                    if (slot < kLinkQueue) s_q[slot] = j + h;
+                    else link_one_read(elems, base + j + h, packed, period, period_magic, cov);   // queue full (clustered duplicates)
+                }
             }
-            break;
+        }
+        __syncthreads();
+        const u32 nq = s_n < kLinkQueue ? s_n : kLinkQueue;
+        for (u32 q = threadIdx.x; q < nq; q += 256) link_one_read(elems, base + s_q[q], packed, period, period_magic, cov);
+        __syncthreads();
+    }
+}
+
+// The sorted records become the suffix array as they stand (sa_out[i] = position of record i)
+// wherever refine_elems_kernel<true> finds nothing to do; this kernel also leaves it the two
+// bitmaps it decides that from: group heads (key change, or a suffix finished by the sort) and
+// members that are neither the last of their group nor proven a prefix of a later member.
+__global__ void __launch_bounds__(256)
+accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u32* __restrict__ cov, u32 period,
+                      u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
+                      u32* __restrict__ uncbits) {
+    constexpr int kPer = 4;   // records per thread in flight
+    constexpr u32 ESC = kElemEscBit >> 1;
+    const unsigned lane = lane_id();
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    for (u64 i0 = ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * (32 * kPer); i0 < m;
+         i0 += warps * 32 * kPer) {
+        u64 e[kPer];
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) {
+            const u64 i = i0 + c * 32 + lane;
+            e[c] = i < m ? elems[i] : 0;
+        }
+        // the record before the first and after the last one of this warp's stretch
+        u64 e_before = 0, e_after = 0;
+        if (lane == 0 && i0 > 0) e_before = elems[i0 - 1];
+        if (lane == 31 && i0 + 32 * kPer < m) e_after = elems[i0 + 32 * kPer];
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) {
+            const u64 i = i0 + c * 32 + lane;
+            u64 ep = __shfl_up_sync(0xffffffffu, e[c], 1);
+            u64 en = __shfl_down_sync(0xffffffffu, e[c], 1);
+            const u64 prev_last = __shfl_sync(0xffffffffu, c > 0 ? e[c > 0 ? c - 1 : 0] : e_before, c > 0 ? 31 : 0);
+            const u64 next_first = __shfl_sync(0xffffffffu, c + 1 < kPer ? e[c + 1 < kPer ? c + 1 : c] : e_after, c + 1 < kPer ? 0 : 31);
+            if (lane == 0) ep = prev_last;
+            if (lane == 31) en = next_first;
+            const bool in = i < m;
+            const u32 key = static_cast<u32>(e[c] >> 33), kp = static_cast<u32>(ep >> 33), kn = static_cast<u32>(en >> 33);
+            const bool head = in && (i == 0 || key != kp || !(key & ESC));
+            const bool last = i + 1 >= m || kn != key || !(kn & ESC);
+            const u32 pos = static_cast<u32>(e[c]);
+            bool unc = false;
+            if (in && !last) {
+                const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
+                const u32 t = period - 1u - (pos - q * period);
+                unc = t >= static_cast<u32>(kUniK) && !((__ldg(cov + (pos >> 5)) >> (pos & 31)) & 1u);
+            }
+            if (in) sa_out[i] = pos;
+            const unsigned hb = __ballot_sync(0xffffffffu, head), ub = __ballot_sync(0xffffffffu, unc);
+            if (lane == 0 && i < m) {
+                headbits[i >> 5] = hb;
+                uncbits[i >> 5] = ub;
+            }
         }
     }
 }
@@ -1094,7 +1220,7 @@ size_t sa_workspace_bytes(size_t n) {
     total += pad(sizeof(u32) * n);                   // rank when the caller wants none
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
-    total += pad(sizeof(u32) * (n / 32 + 2));        // proof bitmap of the uniform read-set path
+    total += 3 * pad(sizeof(u32) * (n / 32 + 2));    // proof / head / uncovered bitmaps of the uniform read-set path
     total += sort_workspace_bytes(n);
     return total + 4096;
 }
@@ -1177,7 +1303,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
     refine_elems_kernel<false><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m,
-                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0);
+                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -1195,7 +1321,8 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
 // accepted as they stand.  *unfinished != 0 (a read set that is not uniform after all, an oversize
 // group, a step limit) sends the caller to the general paths.
 int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
-                            u64* elems_a, u64* elems_b, u32* cov, u32* sa_out, int max_rounds, u32* counters,
+                            u64* elems_a, u64* elems_b, u32* cov, u32* headbits, u32* uncbits, u32* sa_out,
+                            int max_rounds, u32* counters,
                             const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
     cudaStream_t s = ctx->stream;
     const u64 magic = ~0ull / period + 1;   // ceil(2^64 / period): floor(pos / period) = mulhi(pos, magic) for pos < 2^32
@@ -1219,7 +1346,11 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     st->sort_passes += pt.count;
     const u64* sorted = in_b ? elems_b : elems_a;
     RSQ_LAUNCH_BEGIN(ctx, "link_reads_kernel");
-    link_reads_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sorted, n, packed, period, magic, cov);
+    link_reads_kernel<<<grid_for(ctx, n, kLinkChunk, 1, 8), 256, 0, s>>>(sorted, n, packed, period, magic, cov);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
+    accept_uniform_kernel<<<grid_for(ctx, n, 256, 4, 8), 256, 0, s>>>(sorted, n, cov, period, magic, sa_out, headbits,
+                                                                       uncbits);
     RSQ_LAUNCH_END(ctx);
     static bool configured = false;
     if (!configured) {
@@ -1230,7 +1361,7 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
     refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sorted, n, sa_out, max_rounds, true,
-                                                                 counters, cov, period, magic);
+                                                                 counters, cov, period, magic, headbits, uncbits);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -1272,8 +1403,10 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     u64* desc = ctx->alloc<u64>(rank_tiles + 4);
     u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads, [4..7] refine
     u32* cov = ctx->alloc<u32>(n / 32 + 2);
+    u32* headbits = ctx->alloc<u32>(n / 32 + 2);
+    u32* uncbits = ctx->alloc<u32>(n / 32 + 2);
     SortWorkspace ws;
-    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !cov)
+    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !cov || !headbits || !uncbits)
         return fail(RESEQ_OUT_OF_MEMORY, "suffix-array workspace does not fit the reserved arena");
     RSQ_TRY(sort_workspace_carve(ctx, n, &ws));
 
@@ -1293,7 +1426,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         n / n_separators >= kUniMinPeriod && n / n_separators <= kUniMaxPeriod) {
         u64 unfinished = 0;
         RSQ_TRY(uniform_sort_and_refine(ctx, packed, sent, n, static_cast<u32>(n / n_separators), n_separators, keys_a,
-                                        keys_b, cov, d_sa, ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
+                                        keys_b, cov, headbits, uncbits, d_sa, ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
         if (unfinished == 0) {
             st.init_symbols = kUniK;
             RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, ws));
