@@ -474,7 +474,8 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
                     const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
                     int max_rounds, bool use_shortcut, u32* __restrict__ counters,
                     const u32* __restrict__ cov, u32 period, u64 period_magic,
-                    const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits) {
+                    const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits,
+                    u32* __restrict__ patch_list) {
     constexpr int KSYM = UNI ? kUniK : kElemK;             // symbols every member of a group shares
     constexpr int KEYSHIFT = UNI ? 33 : kElemKeyShift;     // record bits above this are the group key
     constexpr u32 ESCBIT = UNI ? (kElemEscBit >> 1) : kElemEscBit;
@@ -902,6 +903,11 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
     if (lane == 0 && nonheads) atomicAdd(counters, nonheads);
     if (tid == 0) atomicMax(counters + 2, static_cast<u32>(rounds));
+    if (UNI && tid == 0 && patch_list) {   // the inverse has already read these records: rank is patched later
+        const u32 e = atomicAdd(counters + 4, 1u);
+        patch_list[2 * e] = static_cast<u32>(t0) + first;
+        patch_list[2 * e + 1] = static_cast<u32>(t0) + end;
+    }
 }
 
 // ---- uniform read sets: records born in (terminator distance, position) order ---------------------
@@ -1143,6 +1149,138 @@ window_scatter_kernel(const u64* __restrict__ rec, u64 n, int win_bits, u32* __r
     for (u32 t = threadIdx.x; t < size; t += blockDim.x) rank[base + t] = s_win[t];
 }
 
+// ---- inverse permutation, lean partition passes ---------------------------------------------------
+// The partition that feeds window_scatter_kernel need not be stable, and because sa is a
+// permutation every bucket (positions sharing their top bits) has a size and a base known in
+// closed form.  So a pass needs neither the ballot ranking nor the look-back chain of the sort: a
+// record takes its slot in the tile's bin from ONE shared-memory atomicAdd, a bin claims its
+// stretch of the bucket with one global atomicAdd, and the tile leaves through shared memory as
+// one contiguous run per bin.  Measured on B200 the sort pass is bound by issue slots and
+// shared-memory wavefronts (the SM-to-HBM ratio is half an A100's), which is what this sheds.
+//
+// kIpAccept: the pass reads the SORTED RECORDS of the uniform path instead of sa and does
+// accept_uniform_kernel's work on the way (sa_out, head and uncovered bitmaps): one read of the
+// records serves both.  kIpSa: element i is (sa[i] << 32) | i.  kIpRec: records of a previous pass.
+enum : int { kIpAccept = 0, kIpSa = 1, kIpRec = 2 };
+constexpr int kIpBlock = 512;
+constexpr int kIpItems = 8;
+constexpr int kIpTile = kIpBlock * kIpItems;
+constexpr int kIpMaxBins = 1024;
+
+template <int MODE>
+__global__ void __launch_bounds__(kIpBlock, 3)
+inv_partition_kernel(const void* __restrict__ in_raw, u64 n, int shift, int prev_shift, int nbins,
+                     u32* __restrict__ claim, u64* __restrict__ out,
+                     const u32* __restrict__ cov, u32 period, u64 period_magic, u32* __restrict__ sa_out,
+                     u32* __restrict__ headbits, u32* __restrict__ uncbits) {
+    __shared__ __align__(16) u64 s_rec[kIpTile];
+    __shared__ u32 s_cnt[kIpMaxBins];
+    __shared__ u32 s_ofs[kIpMaxBins];
+    __shared__ u32 s_gdst[kIpMaxBins];
+    __shared__ u32 s_warp[kIpBlock / 32];
+    const int tid = threadIdx.x;
+    const unsigned lane = lane_id();
+    const u64 tile_base = static_cast<u64>(blockIdx.x) * kIpTile;
+    const u32 valid = static_cast<u32>(n - tile_base < static_cast<u64>(kIpTile) ? n - tile_base : kIpTile);
+    // first bucket this tile can hold records of: a later pass reads the previous pass's buckets,
+    // which lie at [d << prev_shift, (d + 1) << prev_shift) -- at most two of them per tile
+    const u32 bin0 = MODE == kIpRec ? static_cast<u32>(tile_base >> prev_shift) << (prev_shift - shift) : 0u;
+    for (int b = tid; b < nbins; b += kIpBlock) s_cnt[b] = 0;
+    __syncthreads();
+
+    u64 rec[kIpItems];
+    u32 slot[kIpItems];
+#pragma unroll
+    for (int j = 0; j < kIpItems; ++j) {
+        const u64 i = tile_base + static_cast<u64>(j) * kIpBlock + tid;
+        const bool in = i < n;
+        if constexpr (MODE == kIpAccept) {
+            constexpr u32 ESC = kElemEscBit >> 1;
+            const u64* elems = static_cast<const u64*>(in_raw);
+            const u64 e = in ? elems[i] : 0;
+            u64 ep = __shfl_up_sync(0xffffffffu, e, 1);
+            u64 en = __shfl_down_sync(0xffffffffu, e, 1);
+            if (lane == 0) ep = (in && i > 0) ? elems[i - 1] : 0;
+            if (lane == 31) en = i + 1 < n ? elems[i + 1] : 0;
+            const u32 key = static_cast<u32>(e >> 33), kp = static_cast<u32>(ep >> 33), kn = static_cast<u32>(en >> 33);
+            const bool head = in && (i == 0 || key != kp || !(key & ESC));
+            const bool last = i + 1 >= n || kn != key || !(kn & ESC);
+            const u32 pos = static_cast<u32>(e);
+            bool unc = false;
+            if (in && !last) {
+                const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
+                const u32 t = period - 1u - (pos - q * period);
+                unc = t >= static_cast<u32>(kUniK) && !((__ldg(cov + (pos >> 5)) >> (pos & 31)) & 1u);
+            }
+            if (in) sa_out[i] = pos;
+            const unsigned hb = __ballot_sync(0xffffffffu, head), ub = __ballot_sync(0xffffffffu, unc);
+            if (lane == 0 && in) {
+                headbits[i >> 5] = hb;
+                uncbits[i >> 5] = ub;
+            }
+            rec[j] = (static_cast<u64>(pos) << 32) | (i & 0xffffffffu);
+        } else if constexpr (MODE == kIpSa) {
+            rec[j] = in ? (static_cast<u64>(static_cast<const u32*>(in_raw)[i]) << 32) | (i & 0xffffffffu) : 0;
+        } else {
+            rec[j] = in ? static_cast<const u64*>(in_raw)[i] : 0;
+        }
+        slot[j] = 0;
+        if (in) slot[j] = atomicAdd(&s_cnt[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0], 1u);
+    }
+    __syncthreads();
+
+    // exclusive scan of the bin counts (two bins per thread); every non-empty bin claims its stretch
+    const int b0 = 2 * tid, b1 = 2 * tid + 1;
+    const u32 c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
+    u32 inc = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (static_cast<int>(lane) >= o) inc += t;
+    }
+    if (lane == 31) s_warp[tid >> 5] = inc;
+    __syncthreads();
+    u32 before = 0;
+#pragma unroll
+    for (int w = 0; w < kIpBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
+    const u32 excl = before + inc - (c0 + c1);
+    if (b0 < nbins) {
+        s_ofs[b0] = excl;
+        if (c0) s_gdst[b0] = ((bin0 + b0) << shift) + atomicAdd(claim + bin0 + b0, c0) - excl;
+    }
+    if (b1 < nbins) {
+        s_ofs[b1] = excl + c0;
+        if (c1) s_gdst[b1] = ((bin0 + b1) << shift) + atomicAdd(claim + bin0 + b1, c1) - (excl + c0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kIpItems; ++j) {
+        const u32 li = static_cast<u32>(j) * kIpBlock + tid;
+        if (li < valid) s_rec[s_ofs[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0] + slot[j]] = rec[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kIpItems; ++j) {
+        const u32 p = static_cast<u32>(j) * kIpBlock + tid;
+        if (p < valid) {
+            const u64 r = s_rec[p];
+            out[s_gdst[(static_cast<u32>(r >> 32) >> shift) - bin0] + p] = r;
+        }
+    }
+}
+
+// rank[sa[i]] = i over the index ranges refine_elems_kernel<true> re-sorted after the partition had
+// already read the records (list of [begin, end) pairs, *count entries).
+__global__ void __launch_bounds__(256)
+patch_rank_kernel(const u32* __restrict__ sa, u32* __restrict__ rank, const u32* __restrict__ list,
+                  const u32* __restrict__ count) {
+    const u32 entries = *count;
+    for (u32 e = blockIdx.x; e < entries; e += gridDim.x) {
+        const u32 lo = list[2 * e], hi = list[2 * e + 1];
+        for (u32 i = lo + threadIdx.x; i < hi; i += blockDim.x) rank[sa[i]] = i;
+    }
+}
+
 __global__ void inverse_kernel(const u32* __restrict__ sa, u64 n, u32* __restrict__ rank) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -1210,6 +1348,9 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
     return RESEQ_OK;
 }
 
+// claim counters of both partition passes + the list of re-sorted index ranges
+static size_t inverse_scratch_words(size_t n) { return 1024 + (n >> 13) + 64 + 2 * (n / 2048 + 2); }
+
 size_t sa_workspace_bytes(size_t n) {
     auto pad = reseq_cuda_ctx::padded;
     size_t total = 0;
@@ -1221,11 +1362,56 @@ size_t sa_workspace_bytes(size_t n) {
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
     total += 3 * pad(sizeof(u32) * (n / 32 + 2));    // proof / head / uncovered bitmaps of the uniform read-set path
+    total += pad(sizeof(u32) * inverse_scratch_words(n));
     total += sort_workspace_bytes(n);
     return total + 4096;
 }
 
 namespace {
+
+// How the position bits are split between the partition passes and the shared-memory window.
+struct InversePlan {
+    bool partitioned;   // false: small text, direct scatter
+    int win_bits;       // rank entries per window_scatter_kernel CTA = 1 << win_bits
+    int lo_bits;        // bits of the second pass (0: one pass is enough)
+    int shift1;         // first pass: bucket = position >> shift1
+    int bins1;          // buckets of the first pass
+    u32 buckets2;       // buckets after the second pass (= windows)
+    unsigned tiles;
+};
+
+InversePlan make_inverse_plan(size_t n) {
+    InversePlan p{};
+    p.partitioned = n >= (size_t{1} << 22);
+    if (!p.partitioned) return p;
+    const int nb = static_cast<int>(bit_width_u64(n - 1));   // >= 23
+    p.win_bits = 13;
+    int rest = nb - p.win_bits;                               // bits the passes must consume
+    int top = rest < 8 ? rest : 8;
+    int lo = rest - top;
+    if (lo > 9) { p.win_bits = 14; --lo; }                    // n >= 2^31
+    if (lo > 9) { top += lo - 9; lo = 9; }                    // n > 2^31: wider first pass (<= 10 bits)
+    p.lo_bits = lo;
+    p.shift1 = p.win_bits + lo;
+    p.bins1 = static_cast<int>(((n - 1) >> p.shift1) + 1);
+    p.buckets2 = static_cast<u32>(((n - 1) >> p.win_bits) + 1);
+    p.tiles = static_cast<unsigned>((n + kIpTile - 1) / kIpTile);
+    return p;
+}
+
+int window_scatter_device(reseq_cuda_ctx* ctx, const u64* rec, size_t n, int win_bits, u32* rank) {
+    static bool configured = false;
+    if (!configured) {
+        RSQ_CUDA(cudaFuncSetAttribute(window_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        configured = true;
+    }
+    const unsigned windows = static_cast<unsigned>((n + (size_t{1} << win_bits) - 1) >> win_bits);
+    RSQ_LAUNCH_BEGIN(ctx, "window_scatter_kernel");
+    window_scatter_kernel<<<windows, 512, sizeof(u32) << win_bits, ctx->stream>>>(rec, n, win_bits, rank);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
+}
 
 // rank = inverse permutation of the finished sa (scratch: two u64 record buffers of n entries).
 int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64* rec_a, u64* rec_b,
@@ -1303,7 +1489,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
     refine_elems_kernel<false><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m,
-                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr);
+                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr, nullptr);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -1322,7 +1508,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
 // group, a step limit) sends the caller to the general paths.
 int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
                             u64* elems_a, u64* elems_b, u32* cov, u32* headbits, u32* uncbits, u32* sa_out,
-                            int max_rounds, u32* counters,
+                            u32* rank, u32* inv_scratch, bool* rank_done, int max_rounds, u32* counters,
                             const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
     cudaStream_t s = ctx->stream;
     const u64 magic = ~0ull / period + 1;   // ceil(2^64 / period): floor(pos / period) = mulhi(pos, magic) for pos < 2^32
@@ -1345,13 +1531,31 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b));
     st->sort_passes += pt.count;
     const u64* sorted = in_b ? elems_b : elems_a;
+    u64* other = in_b ? elems_a : elems_b;
     RSQ_LAUNCH_BEGIN(ctx, "link_reads_kernel");
     link_reads_kernel<<<grid_for(ctx, n, kLinkChunk, 1, 8), 256, 0, s>>>(sorted, n, packed, period, magic, cov);
     RSQ_LAUNCH_END(ctx);
-    RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
-    accept_uniform_kernel<<<grid_for(ctx, n, 256, 4, 8), 256, 0, s>>>(sorted, n, cov, period, magic, sa_out, headbits,
-                                                                       uncbits);
-    RSQ_LAUNCH_END(ctx);
+
+    // The inverse permutation starts here when the text is large enough for the partitioned
+    // scatter: its first pass reads the sorted records once for both jobs (sa + bitmaps, and the
+    // (position, index) records bucketed by the top bits of the position).
+    const InversePlan plan = make_inverse_plan(n);
+    const bool fused = plan.partitioned && ctx->opt_fused_inverse != 0;
+    u32* claim1 = inv_scratch;
+    u32* claim2 = inv_scratch + kIpMaxBins;
+    u32* patch_list = claim2 + plan.buckets2 + 32;
+    if (fused) {
+        RSQ_CUDA(cudaMemsetAsync(inv_scratch, 0, sizeof(u32) * (kIpMaxBins + plan.buckets2 + 32), s));
+        RSQ_LAUNCH_BEGIN(ctx, "inv_partition_accept");
+        inv_partition_kernel<kIpAccept><<<plan.tiles, kIpBlock, 0, s>>>(sorted, n, plan.shift1, 0, plan.bins1, claim1, other,
+                                                                       cov, period, magic, sa_out, headbits, uncbits);
+        RSQ_LAUNCH_END(ctx);
+    } else {
+        RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
+        accept_uniform_kernel<<<grid_for(ctx, n, 256, 4, 8), 256, 0, s>>>(sorted, n, cov, period, magic, sa_out, headbits,
+                                                                           uncbits);
+        RSQ_LAUNCH_END(ctx);
+    }
     static bool configured = false;
     if (!configured) {
         RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1361,20 +1565,41 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
     refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sorted, n, sa_out, max_rounds, true,
-                                                                 counters, cov, period, magic, headbits, uncbits);
+                                                                 counters, cov, period, magic, headbits, uncbits,
+                                                                 fused ? patch_list : nullptr);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
-    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 5 * sizeof(u32), cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaStreamSynchronize(s));
     const volatile u32* c = reinterpret_cast<volatile u32*>(ctx->pinned);
     *unfinished = static_cast<u64>(c[0]) + (c[1] ? 1u : 0u) + c[3];
     if (std::getenv("RESEQ_DEBUG"))
-        std::fprintf(stderr, "[reseq] uniform refine: n=%zu period=%u tied_left=%u oversize=%u steps=%u misplaced_sentinels=%u\n",
-                     n, period, c[0], c[1], c[2], c[3]);
-    if (*unfinished == 0) {
-        st->rounds += c[2];
-        st->refined_tile += n;
+        std::fprintf(stderr, "[reseq] uniform refine: n=%zu period=%u tied_left=%u oversize=%u steps=%u misplaced_sentinels=%u resorted_tiles=%u\n",
+                     n, period, c[0], c[1], c[2], c[3], c[4]);
+    if (*unfinished != 0) return RESEQ_OK;
+    st->rounds += c[2];
+    st->refined_tile += n;
+    if (!fused) return RESEQ_OK;
+
+    // -- rest of the inverse: second partition pass, window scatter, patch of the re-sorted ranges --
+    const u32 resorted = c[4];
+    const u64* rec = other;
+    if (plan.lo_bits > 0) {
+        RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec");
+        inv_partition_kernel<kIpRec><<<plan.tiles, kIpBlock, 0, s>>>(other, n, plan.win_bits, plan.shift1, 2 << plan.lo_bits,
+                                                                    claim2, const_cast<u64*>(sorted), nullptr, 0, 0, nullptr,
+                                                                    nullptr, nullptr);
+        RSQ_LAUNCH_END(ctx);
+        rec = sorted;
     }
+    RSQ_TRY(window_scatter_device(ctx, rec, n, plan.win_bits, rank));
+    if (resorted) {
+        RSQ_LAUNCH_BEGIN(ctx, "patch_rank_kernel");
+        patch_rank_kernel<<<resorted < 1024u ? resorted : 1024u, 256, 0, s>>>(sa_out, rank, patch_list, counters + 4);
+        RSQ_LAUNCH_END(ctx);
+    }
+    RSQ_CUDA(cudaGetLastError());
+    *rank_done = true;
     return RESEQ_OK;
 }
 
@@ -1405,8 +1630,9 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     u32* cov = ctx->alloc<u32>(n / 32 + 2);
     u32* headbits = ctx->alloc<u32>(n / 32 + 2);
     u32* uncbits = ctx->alloc<u32>(n / 32 + 2);
+    u32* inv_scratch = ctx->alloc<u32>(inverse_scratch_words(n));
     SortWorkspace ws;
-    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !cov || !headbits || !uncbits)
+    if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !cov || !headbits || !uncbits || !inv_scratch)
         return fail(RESEQ_OUT_OF_MEMORY, "suffix-array workspace does not fit the reserved arena");
     RSQ_TRY(sort_workspace_carve(ctx, n, &ws));
 
@@ -1425,11 +1651,13 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     if (dna && ctx->opt_text_rounds > 0 && ctx->opt_uniform != 0 && n_separators > 0 && n % n_separators == 0 &&
         n / n_separators >= kUniMinPeriod && n / n_separators <= kUniMaxPeriod) {
         u64 unfinished = 0;
+        bool rank_done = false;
         RSQ_TRY(uniform_sort_and_refine(ctx, packed, sent, n, static_cast<u32>(n / n_separators), n_separators, keys_a,
-                                        keys_b, cov, headbits, uncbits, d_sa, ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
+                                        keys_b, cov, headbits, uncbits, d_sa, rank, inv_scratch, &rank_done,
+                                        ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
         if (unfinished == 0) {
             st.init_symbols = kUniK;
-            RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, ws));
+            if (!rank_done) RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, ws));
             st.kernel_launches = ctx->launches - launches0;
             if (stats) *stats = st;
             return RESEQ_OK;

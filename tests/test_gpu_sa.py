@@ -183,6 +183,27 @@ def test_uniform_read_sets_with_repeats_and_duplicates(rq, ex, oracle):
     check(rq, ex, oracle, b"".join(r + b"\0" for r in reads))
 
 
+def test_uniform_path_patches_rank_of_resorted_groups(rq, ex, oracle):
+    """n >= 2^22: the inverse's first partition pass runs before the refine kernel re-sorts the groups
+    that mix loci (a genome with long repeats has plenty); their ranks are patched afterwards."""
+    rng = np.random.default_rng(79)
+    unit = bytes(rng.choice([65, 67, 71, 84], 60_000).astype(np.uint8))
+    genome = unit + unit[:30_000] + bytes(rng.choice([65, 67, 71, 84], 20_000).astype(np.uint8)) + unit[10_000:40_000]
+    starts = rng.integers(0, len(genome) - 100 + 1, 45_000)
+    text = np.frombuffer(_reads(genome, 100, starts), dtype=np.uint8)
+    assert text.size >= 1 << 22
+    got = rq.build_parallel(text, ex)
+    assert got.stats.init_symbols == 15 and got.stats.rounds >= 1     # some groups took refinement steps
+    assert oracle.verify_sa(text, got.sa) == 0
+    assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
+    alt = rq.build_parallel(text, no_uniform_executor(rq))
+    assert np.array_equal(alt.sa, got.sa) and np.array_equal(alt.rank, got.rank)
+    e = rq.Executor(0)
+    e.set_option("sa_fused_inverse", 0)
+    alt = rq.build_parallel(text, e)
+    assert alt.stats.init_symbols == 15 and np.array_equal(alt.sa, got.sa) and np.array_equal(alt.rank, got.rank)
+
+
 def test_texts_that_only_look_uniform(rq, ex, oracle):
     """n divisible by the number of sentinels, but the sentinels are not one period apart: the check
     kernel must hand the text to the general paths."""
