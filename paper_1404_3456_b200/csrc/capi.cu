@@ -160,7 +160,6 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
         const int v = std::atoi(e);
         if (v >= 1 && v <= 8) ctx->opt_lookahead = v;
     }
-    if (const char* e = std::getenv("RESEQ_SA_FUSED_INVERSE")) ctx->opt_fused_inverse = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_UNIFORM")) ctx->opt_uniform = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SHORTCUT")) ctx->opt_shortcut = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);
@@ -205,10 +204,6 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     }
     if (std::strcmp(name, "sa_shortcut") == 0) {
         ctx->opt_shortcut = value != 0;
-        return RESEQ_OK;
-    }
-    if (std::strcmp(name, "sa_fused_inverse") == 0) {
-        ctx->opt_fused_inverse = value != 0;
         return RESEQ_OK;
     }
     if (std::strcmp(name, "sa_uniform") == 0) {

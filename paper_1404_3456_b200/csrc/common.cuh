@@ -50,7 +50,6 @@ struct reseq_cuda_ctx {
     int opt_shortcut = 1;      // sentinel-distance shortcut in the refine kernel (tuning / tests)
     int opt_lookahead = 8;     // onesweep look-back descriptors in flight per digit (1..8)
     int opt_sort_cfg = 0;      // onesweep tile shape (0 = default tuning)
-    int opt_fused_inverse = 1; // uniform path: the inverse's first partition pass also does the accept pass
     int opt_uniform = 1;       // transposed-record path for uniform read sets (0: general paths only)
     int opt_text_rounds = 16;  // max text-window refinement rounds before prefix doubling takes over
 

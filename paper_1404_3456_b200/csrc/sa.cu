@@ -474,8 +474,7 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
                     const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
                     int max_rounds, bool use_shortcut, u32* __restrict__ counters,
                     const u32* __restrict__ cov, u32 period, u64 period_magic,
-                    const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits,
-                    u32* __restrict__ patch_list) {
+                    const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits) {
     constexpr int KSYM = UNI ? kUniK : kElemK;             // symbols every member of a group shares
     constexpr int KEYSHIFT = UNI ? 33 : kElemKeyShift;     // record bits above this are the group key
     constexpr u32 ESCBIT = UNI ? (kElemEscBit >> 1) : kElemEscBit;
@@ -903,11 +902,6 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     for (int o = 16; o > 0; o >>= 1) nonheads += __shfl_xor_sync(0xffffffffu, nonheads, o);
     if (lane == 0 && nonheads) atomicAdd(counters, nonheads);
     if (tid == 0) atomicMax(counters + 2, static_cast<u32>(rounds));
-    if (UNI && tid == 0 && patch_list) {   // the inverse has already read these records: rank is patched later
-        const u32 e = atomicAdd(counters + 4, 1u);
-        patch_list[2 * e] = static_cast<u32>(t0) + first;
-        patch_list[2 * e + 1] = static_cast<u32>(t0) + end;
-    }
 }
 
 // ---- uniform read sets: records born in (terminator distance, position) order ---------------------
@@ -1158,21 +1152,22 @@ window_scatter_kernel(const u64* __restrict__ rec, u64 n, int win_bits, u32* __r
 // one contiguous run per bin.  Measured on B200 the sort pass is bound by issue slots and
 // shared-memory wavefronts (the SM-to-HBM ratio is half an A100's), which is what this sheds.
 //
-// kIpAccept: the pass reads the SORTED RECORDS of the uniform path instead of sa and does
-// accept_uniform_kernel's work on the way (sa_out, head and uncovered bitmaps): one read of the
-// records serves both.  kIpSa: element i is (sa[i] << 32) | i.  kIpRec: records of a previous pass.
-enum : int { kIpAccept = 0, kIpSa = 1, kIpRec = 2 };
+// kIpSa: element i of the input is (sa[i] << 32) | i.  kIpRec: records of the previous pass.
+enum : int { kIpSa = 1, kIpRec = 2 };
 constexpr int kIpBlock = 512;
 constexpr int kIpItems = 8;
 constexpr int kIpTile = kIpBlock * kIpItems;
 constexpr int kIpMaxBins = 1024;
 
+// Persistent: two CTAs per SM walk tiles blockIdx.x, blockIdx.x + gridDim.x, ... (no order
+// between tiles is needed).  The loads of the next tile are issued before the current one is
+// scanned, exchanged and stored, and the claims before the exchange, so the HBM latency of the
+// load and the L2 latency of the atomics are covered by the tile's own work (one tile per CTA:
+// 0.68 ms per pass at n = 139 M, 55 % of stalls on those two scoreboards; this form: 0.48 ms).
 template <int MODE>
-__global__ void __launch_bounds__(kIpBlock, 3)
-inv_partition_kernel(const void* __restrict__ in_raw, u64 n, int shift, int prev_shift, int nbins,
-                     u32* __restrict__ claim, u64* __restrict__ out,
-                     const u32* __restrict__ cov, u32 period, u64 period_magic, u32* __restrict__ sa_out,
-                     u32* __restrict__ headbits, u32* __restrict__ uncbits) {
+__global__ void __launch_bounds__(kIpBlock, 2)
+inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shift, int prev_shift, int nbins,
+                                u32* __restrict__ claim, u64* __restrict__ out, u32 num_tiles) {
     __shared__ __align__(16) u64 s_rec[kIpTile];
     __shared__ u32 s_cnt[kIpMaxBins];
     __shared__ u32 s_ofs[kIpMaxBins];
@@ -1180,104 +1175,73 @@ inv_partition_kernel(const void* __restrict__ in_raw, u64 n, int shift, int prev
     __shared__ u32 s_warp[kIpBlock / 32];
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
-    const u64 tile_base = static_cast<u64>(blockIdx.x) * kIpTile;
-    const u32 valid = static_cast<u32>(n - tile_base < static_cast<u64>(kIpTile) ? n - tile_base : kIpTile);
-    // first bucket this tile can hold records of: a later pass reads the previous pass's buckets,
-    // which lie at [d << prev_shift, (d + 1) << prev_shift) -- at most two of them per tile
-    const u32 bin0 = MODE == kIpRec ? static_cast<u32>(tile_base >> prev_shift) << (prev_shift - shift) : 0u;
+    auto load_tile = [&](u32 tile, u64 (&r)[kIpItems]) {
+        const u64 tb = static_cast<u64>(tile) * kIpTile;
+#pragma unroll
+        for (int j = 0; j < kIpItems; ++j) {
+            const u64 i = tb + static_cast<u64>(j) * kIpBlock + tid;
+            if constexpr (MODE == kIpSa)
+                r[j] = i < n ? (static_cast<u64>(static_cast<const u32*>(in_raw)[i]) << 32) | (i & 0xffffffffu) : 0;
+            else
+                r[j] = i < n ? static_cast<const u64*>(in_raw)[i] : 0;
+        }
+    };
+    u64 rec[kIpItems], nxt[kIpItems];
+    if (blockIdx.x < num_tiles) load_tile(blockIdx.x, rec);
     for (int b = tid; b < nbins; b += kIpBlock) s_cnt[b] = 0;
     __syncthreads();
-
-    u64 rec[kIpItems];
-    u32 slot[kIpItems];
+    for (u32 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const u64 tile_base = static_cast<u64>(tile) * kIpTile;
+        const u32 valid = static_cast<u32>(n - tile_base < static_cast<u64>(kIpTile) ? n - tile_base : kIpTile);
+        const u32 bin0 = MODE == kIpRec ? static_cast<u32>(tile_base >> prev_shift) << (prev_shift - shift) : 0u;
+        u32 slot[kIpItems];
 #pragma unroll
-    for (int j = 0; j < kIpItems; ++j) {
-        const u64 i = tile_base + static_cast<u64>(j) * kIpBlock + tid;
-        const bool in = i < n;
-        if constexpr (MODE == kIpAccept) {
-            constexpr u32 ESC = kElemEscBit >> 1;
-            const u64* elems = static_cast<const u64*>(in_raw);
-            const u64 e = in ? elems[i] : 0;
-            u64 ep = __shfl_up_sync(0xffffffffu, e, 1);
-            u64 en = __shfl_down_sync(0xffffffffu, e, 1);
-            if (lane == 0) ep = (in && i > 0) ? elems[i - 1] : 0;
-            if (lane == 31) en = i + 1 < n ? elems[i + 1] : 0;
-            const u32 key = static_cast<u32>(e >> 33), kp = static_cast<u32>(ep >> 33), kn = static_cast<u32>(en >> 33);
-            const bool head = in && (i == 0 || key != kp || !(key & ESC));
-            const bool last = i + 1 >= n || kn != key || !(kn & ESC);
-            const u32 pos = static_cast<u32>(e);
-            bool unc = false;
-            if (in && !last) {
-                const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
-                const u32 t = period - 1u - (pos - q * period);
-                unc = t >= static_cast<u32>(kUniK) && !((__ldg(cov + (pos >> 5)) >> (pos & 31)) & 1u);
-            }
-            if (in) sa_out[i] = pos;
-            const unsigned hb = __ballot_sync(0xffffffffu, head), ub = __ballot_sync(0xffffffffu, unc);
-            if (lane == 0 && in) {
-                headbits[i >> 5] = hb;
-                uncbits[i >> 5] = ub;
-            }
-            rec[j] = (static_cast<u64>(pos) << 32) | (i & 0xffffffffu);
-        } else if constexpr (MODE == kIpSa) {
-            rec[j] = in ? (static_cast<u64>(static_cast<const u32*>(in_raw)[i]) << 32) | (i & 0xffffffffu) : 0;
-        } else {
-            rec[j] = in ? static_cast<const u64*>(in_raw)[i] : 0;
+        for (int j = 0; j < kIpItems; ++j) {
+            const u32 li = static_cast<u32>(j) * kIpBlock + tid;
+            slot[j] = 0;
+            if (li < valid) slot[j] = atomicAdd(&s_cnt[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0], 1u);
         }
-        slot[j] = 0;
-        if (in) slot[j] = atomicAdd(&s_cnt[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0], 1u);
-    }
-    __syncthreads();
-
-    // exclusive scan of the bin counts (two bins per thread); every non-empty bin claims its stretch
-    const int b0 = 2 * tid, b1 = 2 * tid + 1;
-    const u32 c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
-    u32 inc = c0 + c1;
+        if (tile + gridDim.x < num_tiles) load_tile(tile + gridDim.x, nxt);   // in flight until the end of this tile
+        __syncthreads();
+        const int b0 = 2 * tid, b1 = 2 * tid + 1;
+        const u32 c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
+        u32 g0 = 0, g1 = 0;   // claims are issued now, consumed after the exchange
+        if (c0) g0 = atomicAdd(claim + bin0 + b0, c0);
+        if (c1) g1 = atomicAdd(claim + bin0 + b1, c1);
+        u32 inc = c0 + c1;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (static_cast<int>(lane) >= o) inc += t;
-    }
-    if (lane == 31) s_warp[tid >> 5] = inc;
-    __syncthreads();
-    u32 before = 0;
-#pragma unroll
-    for (int w = 0; w < kIpBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
-    const u32 excl = before + inc - (c0 + c1);
-    if (b0 < nbins) {
-        s_ofs[b0] = excl;
-        if (c0) s_gdst[b0] = ((bin0 + b0) << shift) + atomicAdd(claim + bin0 + b0, c0) - excl;
-    }
-    if (b1 < nbins) {
-        s_ofs[b1] = excl + c0;
-        if (c1) s_gdst[b1] = ((bin0 + b1) << shift) + atomicAdd(claim + bin0 + b1, c1) - (excl + c0);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kIpItems; ++j) {
-        const u32 li = static_cast<u32>(j) * kIpBlock + tid;
-        if (li < valid) s_rec[s_ofs[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0] + slot[j]] = rec[j];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kIpItems; ++j) {
-        const u32 p = static_cast<u32>(j) * kIpBlock + tid;
-        if (p < valid) {
-            const u64 r = s_rec[p];
-            out[s_gdst[(static_cast<u32>(r >> 32) >> shift) - bin0] + p] = r;
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (static_cast<int>(lane) >= o) inc += t;
         }
-    }
-}
-
-// rank[sa[i]] = i over the index ranges refine_elems_kernel<true> re-sorted after the partition had
-// already read the records (list of [begin, end) pairs, *count entries).
-__global__ void __launch_bounds__(256)
-patch_rank_kernel(const u32* __restrict__ sa, u32* __restrict__ rank, const u32* __restrict__ list,
-                  const u32* __restrict__ count) {
-    const u32 entries = *count;
-    for (u32 e = blockIdx.x; e < entries; e += gridDim.x) {
-        const u32 lo = list[2 * e], hi = list[2 * e + 1];
-        for (u32 i = lo + threadIdx.x; i < hi; i += blockDim.x) rank[sa[i]] = i;
+        if (lane == 31) s_warp[tid >> 5] = inc;
+        __syncthreads();
+        u32 before = 0;
+#pragma unroll
+        for (int w = 0; w < kIpBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
+        const u32 excl = before + inc - (c0 + c1);
+        if (b0 < nbins) { s_ofs[b0] = excl; s_cnt[b0] = 0; }
+        if (b1 < nbins) { s_ofs[b1] = excl + c0; s_cnt[b1] = 0; }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kIpItems; ++j) {
+            const u32 li = static_cast<u32>(j) * kIpBlock + tid;
+            if (li < valid) s_rec[s_ofs[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0] + slot[j]] = rec[j];
+        }
+        if (c0) s_gdst[b0] = ((bin0 + b0) << shift) + g0 - excl;
+        if (c1) s_gdst[b1] = ((bin0 + b1) << shift) + g1 - (excl + c0);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kIpItems; ++j) {
+            const u32 p = static_cast<u32>(j) * kIpBlock + tid;
+            if (p < valid) {
+                const u64 r = s_rec[p];
+                out[s_gdst[(static_cast<u32>(r >> 32) >> shift) - bin0] + p] = r;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kIpItems; ++j) rec[j] = nxt[j];
+        __syncthreads();   // s_rec / s_gdst are rewritten by the next tile
     }
 }
 
@@ -1348,8 +1312,8 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
     return RESEQ_OK;
 }
 
-// claim counters of both partition passes + the list of re-sorted index ranges
-static size_t inverse_scratch_words(size_t n) { return 1024 + (n >> 13) + 64 + 2 * (n / 2048 + 2); }
+// claim counters of both partition passes
+static size_t inverse_scratch_words(size_t n) { return kIpMaxBins + (n >> 13) + 64; }
 
 size_t sa_workspace_bytes(size_t n) {
     auto pad = reseq_cuda_ctx::padded;
@@ -1413,59 +1377,36 @@ int window_scatter_device(reseq_cuda_ctx* ctx, const u64* rec, size_t n, int win
     return RESEQ_OK;
 }
 
-// rank = inverse permutation of the finished sa (scratch: two u64 record buffers of n entries).
-int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64* rec_a, u64* rec_b,
-                   const SortWorkspace& ws) {
+// rank = inverse permutation of the finished sa (scratch: two u64 record buffers of n entries and
+// inverse_scratch_words(n) claim counters).
+int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64* rec_a, u64* rec_b, u32* scratch) {
     cudaStream_t s = ctx->stream;
-    if (n < (size_t{1} << 22)) {  // the whole rank array is L2-resident: scatter directly
+    const InversePlan plan = make_inverse_plan(n);
+    if (!plan.partitioned) {  // the whole rank array is L2-resident: scatter directly
         RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
         inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa, n, rank);
         RSQ_LAUNCH_END(ctx);
         RSQ_CUDA(cudaGetLastError());
         return RESEQ_OK;
     }
-    // two stable passes (low bits of the top 13, then the top 8): windows of ~n / 8192 rank entries
-    const int nb = static_cast<int>(bit_width_u64(n - 1));
-    const int shift = nb - 8;
-    int lo_bits = shift - 13;  // aim at windows of 8192 entries (32 KB of shared memory)
-    if (lo_bits < 0) lo_bits = 0;
-    if (lo_bits > 8) lo_bits = 8;
-    if (ctx->opt_inverse_lo_bits >= 0 && ctx->opt_inverse_lo_bits <= 8) lo_bits = ctx->opt_inverse_lo_bits;
-    const int win_bits = shift - lo_bits;
+    u32* claim1 = scratch;
+    u32* claim2 = scratch + kIpMaxBins;
+    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpMaxBins + plan.buckets2 + 32), s));
+    const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
+    RSQ_LAUNCH_BEGIN(ctx, "inv_partition_sa");
+    inv_partition_persistent_kernel<kIpSa><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a,
+                                                                    plan.tiles);
+    RSQ_LAUNCH_END(ctx);
     const u64* rec = rec_a;
-    if (lo_bits > 0) {
-        RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
-        perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift - lo_bits, lo_bits, ws.hist);
+    if (plan.lo_bits > 0) {
+        RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec");
+        inv_partition_persistent_kernel<kIpRec><<<grid, kIpBlock, 0, s>>>(rec_a, n, plan.win_bits, plan.shift1,
+                                                                         2 << plan.lo_bits, claim2, rec_b, plan.tiles);
         RSQ_LAUNCH_END(ctx);
-        RSQ_TRY(onesweep_partition_pack_iota(ctx, sa, rec_b, n, shift - lo_bits, lo_bits, ws));
-        RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
-        perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
-        RSQ_LAUNCH_END(ctx);
-        RSQ_TRY(onesweep_partition_packed(ctx, rec_b, rec_a, n, shift, 8, ws));
-    } else {
-        RSQ_LAUNCH_BEGIN(ctx, "perm_digit_hist_kernel");
-        perm_digit_hist_kernel<<<1, kRadix, 0, s>>>(n, shift, 8, ws.hist);
-        RSQ_LAUNCH_END(ctx);
-        RSQ_TRY(onesweep_partition_pack_iota(ctx, sa, rec_a, n, shift, 8, ws));
-    }
-    if (win_bits <= 14) {
-        static bool configured = false;
-        if (!configured) {
-            RSQ_CUDA(cudaFuncSetAttribute(window_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          64 * 1024));
-            configured = true;
-        }
-        const unsigned windows = static_cast<unsigned>((n + (size_t{1} << win_bits) - 1) >> win_bits);
-        RSQ_LAUNCH_BEGIN(ctx, "window_scatter_kernel");
-        window_scatter_kernel<<<windows, 512, sizeof(u32) << win_bits, s>>>(rec, n, win_bits, rank);
-        RSQ_LAUNCH_END(ctx);
-    } else {
-        RSQ_LAUNCH_BEGIN(ctx, "scatter_records_kernel");
-        scatter_records_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(rec, n, rank);
-        RSQ_LAUNCH_END(ctx);
+        rec = rec_b;
     }
     RSQ_CUDA(cudaGetLastError());
-    return RESEQ_OK;
+    return window_scatter_device(ctx, rec, n, plan.win_bits, rank);
 }
 
 // The DNA fast path on `count` records: sort on key24, finish every group from the text.
@@ -1489,7 +1430,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
     refine_elems_kernel<false><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m,
-                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr, nullptr);
+                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -1508,7 +1449,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
 // group, a step limit) sends the caller to the general paths.
 int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
                             u64* elems_a, u64* elems_b, u32* cov, u32* headbits, u32* uncbits, u32* sa_out,
-                            u32* rank, u32* inv_scratch, bool* rank_done, int max_rounds, u32* counters,
+                            int max_rounds, u32* counters,
                             const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
     cudaStream_t s = ctx->stream;
     const u64 magic = ~0ull / period + 1;   // ceil(2^64 / period): floor(pos / period) = mulhi(pos, magic) for pos < 2^32
@@ -1531,31 +1472,13 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b));
     st->sort_passes += pt.count;
     const u64* sorted = in_b ? elems_b : elems_a;
-    u64* other = in_b ? elems_a : elems_b;
     RSQ_LAUNCH_BEGIN(ctx, "link_reads_kernel");
     link_reads_kernel<<<grid_for(ctx, n, kLinkChunk, 1, 8), 256, 0, s>>>(sorted, n, packed, period, magic, cov);
     RSQ_LAUNCH_END(ctx);
-
-    // The inverse permutation starts here when the text is large enough for the partitioned
-    // scatter: its first pass reads the sorted records once for both jobs (sa + bitmaps, and the
-    // (position, index) records bucketed by the top bits of the position).
-    const InversePlan plan = make_inverse_plan(n);
-    const bool fused = plan.partitioned && ctx->opt_fused_inverse != 0;
-    u32* claim1 = inv_scratch;
-    u32* claim2 = inv_scratch + kIpMaxBins;
-    u32* patch_list = claim2 + plan.buckets2 + 32;
-    if (fused) {
-        RSQ_CUDA(cudaMemsetAsync(inv_scratch, 0, sizeof(u32) * (kIpMaxBins + plan.buckets2 + 32), s));
-        RSQ_LAUNCH_BEGIN(ctx, "inv_partition_accept");
-        inv_partition_kernel<kIpAccept><<<plan.tiles, kIpBlock, 0, s>>>(sorted, n, plan.shift1, 0, plan.bins1, claim1, other,
-                                                                       cov, period, magic, sa_out, headbits, uncbits);
-        RSQ_LAUNCH_END(ctx);
-    } else {
-        RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
-        accept_uniform_kernel<<<grid_for(ctx, n, 256, 4, 8), 256, 0, s>>>(sorted, n, cov, period, magic, sa_out, headbits,
-                                                                           uncbits);
-        RSQ_LAUNCH_END(ctx);
-    }
+    RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
+    accept_uniform_kernel<<<grid_for(ctx, n, 256, 4, 8), 256, 0, s>>>(sorted, n, cov, period, magic, sa_out, headbits,
+                                                                       uncbits);
+    RSQ_LAUNCH_END(ctx);
     static bool configured = false;
     if (!configured) {
         RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1565,41 +1488,20 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
     refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sorted, n, sa_out, max_rounds, true,
-                                                                 counters, cov, period, magic, headbits, uncbits,
-                                                                 fused ? patch_list : nullptr);
+                                                                 counters, cov, period, magic, headbits, uncbits);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
-    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 5 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
     RSQ_CUDA(cudaStreamSynchronize(s));
     const volatile u32* c = reinterpret_cast<volatile u32*>(ctx->pinned);
     *unfinished = static_cast<u64>(c[0]) + (c[1] ? 1u : 0u) + c[3];
     if (std::getenv("RESEQ_DEBUG"))
-        std::fprintf(stderr, "[reseq] uniform refine: n=%zu period=%u tied_left=%u oversize=%u steps=%u misplaced_sentinels=%u resorted_tiles=%u\n",
-                     n, period, c[0], c[1], c[2], c[3], c[4]);
-    if (*unfinished != 0) return RESEQ_OK;
-    st->rounds += c[2];
-    st->refined_tile += n;
-    if (!fused) return RESEQ_OK;
-
-    // -- rest of the inverse: second partition pass, window scatter, patch of the re-sorted ranges --
-    const u32 resorted = c[4];
-    const u64* rec = other;
-    if (plan.lo_bits > 0) {
-        RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec");
-        inv_partition_kernel<kIpRec><<<plan.tiles, kIpBlock, 0, s>>>(other, n, plan.win_bits, plan.shift1, 2 << plan.lo_bits,
-                                                                    claim2, const_cast<u64*>(sorted), nullptr, 0, 0, nullptr,
-                                                                    nullptr, nullptr);
-        RSQ_LAUNCH_END(ctx);
-        rec = sorted;
+        std::fprintf(stderr, "[reseq] uniform refine: n=%zu period=%u tied_left=%u oversize=%u steps=%u misplaced_sentinels=%u\n",
+                     n, period, c[0], c[1], c[2], c[3]);
+    if (*unfinished == 0) {
+        st->rounds += c[2];
+        st->refined_tile += n;
     }
-    RSQ_TRY(window_scatter_device(ctx, rec, n, plan.win_bits, rank));
-    if (resorted) {
-        RSQ_LAUNCH_BEGIN(ctx, "patch_rank_kernel");
-        patch_rank_kernel<<<resorted < 1024u ? resorted : 1024u, 256, 0, s>>>(sa_out, rank, patch_list, counters + 4);
-        RSQ_LAUNCH_END(ctx);
-    }
-    RSQ_CUDA(cudaGetLastError());
-    *rank_done = true;
     return RESEQ_OK;
 }
 
@@ -1651,13 +1553,12 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     if (dna && ctx->opt_text_rounds > 0 && ctx->opt_uniform != 0 && n_separators > 0 && n % n_separators == 0 &&
         n / n_separators >= kUniMinPeriod && n / n_separators <= kUniMaxPeriod) {
         u64 unfinished = 0;
-        bool rank_done = false;
         RSQ_TRY(uniform_sort_and_refine(ctx, packed, sent, n, static_cast<u32>(n / n_separators), n_separators, keys_a,
-                                        keys_b, cov, headbits, uncbits, d_sa, rank, inv_scratch, &rank_done,
+                                        keys_b, cov, headbits, uncbits, d_sa,
                                         ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
         if (unfinished == 0) {
             st.init_symbols = kUniK;
-            if (!rank_done) RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, ws));
+            RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, inv_scratch));
             st.kernel_launches = ctx->launches - launches0;
             if (stats) *stats = st;
             return RESEQ_OK;
@@ -1677,7 +1578,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
                                 counters + 4, ws, &st, &unfinished));
         st.init_symbols = kElemK;
         if (unfinished == 0) {
-            RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, ws));
+            RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, inv_scratch));
             st.kernel_launches = ctx->launches - launches0;
             if (stats) *stats = st;
             return RESEQ_OK;

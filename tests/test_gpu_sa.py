@@ -183,9 +183,9 @@ def test_uniform_read_sets_with_repeats_and_duplicates(rq, ex, oracle):
     check(rq, ex, oracle, b"".join(r + b"\0" for r in reads))
 
 
-def test_uniform_path_patches_rank_of_resorted_groups(rq, ex, oracle):
-    """n >= 2^22: the inverse's first partition pass runs before the refine kernel re-sorts the groups
-    that mix loci (a genome with long repeats has plenty); their ranks are patched afterwards."""
+def test_uniform_path_with_many_resorted_groups_at_partitioned_inverse_size(rq, ex, oracle):
+    """n >= 2^22 (partitioned inverse) on a genome with long repeats: plenty of groups mix loci and
+    take refinement steps; sa by proof, rank as its inverse."""
     rng = np.random.default_rng(79)
     unit = bytes(rng.choice([65, 67, 71, 84], 60_000).astype(np.uint8))
     genome = unit + unit[:30_000] + bytes(rng.choice([65, 67, 71, 84], 20_000).astype(np.uint8)) + unit[10_000:40_000]
@@ -198,10 +198,6 @@ def test_uniform_path_patches_rank_of_resorted_groups(rq, ex, oracle):
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
     alt = rq.build_parallel(text, no_uniform_executor(rq))
     assert np.array_equal(alt.sa, got.sa) and np.array_equal(alt.rank, got.rank)
-    e = rq.Executor(0)
-    e.set_option("sa_fused_inverse", 0)
-    alt = rq.build_parallel(text, e)
-    assert alt.stats.init_symbols == 15 and np.array_equal(alt.sa, got.sa) and np.array_equal(alt.rank, got.rank)
 
 
 def test_texts_that_only_look_uniform(rq, ex, oracle):
