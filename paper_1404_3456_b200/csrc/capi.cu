@@ -152,6 +152,8 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     RSQ_CUDA(cudaGetDeviceProperties(&prop, device));
     ctx->sm_count = prop.multiProcessorCount > 0 ? prop.multiProcessorCount : kSmCount;
     RSQ_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    RSQ_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    RSQ_CUDA(cudaEventCreateWithFlags(&ctx->copy_event, cudaEventDisableTiming));
     ctx->stream = ctx->own_stream;
     RSQ_CUDA(cudaMallocHost(&ctx->pinned, 4096));
     if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
@@ -179,6 +181,8 @@ void reseq_cuda_ctx_destroy(reseq_cuda_ctx* ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->copy_event) cudaEventDestroy(ctx->copy_event);
     delete ctx;
 }
 
@@ -407,11 +411,19 @@ int reseq_cuda_build_sa(reseq_cuda_ctx* ctx, const uint8_t* text, size_t n, uint
     u32* d_sa = ctx->alloc<u32>(n);
     u32* d_rank = ctx->alloc<u32>(n);
     RSQ_CUDA(cudaMemcpyAsync(d_text, text, n, cudaMemcpyHostToDevice, ctx->stream));
-    RSQ_TRY(build_sa_device(ctx, d_text, n, d_sa, d_rank, stats));
-    RSQ_CUDA(cudaMemcpyAsync(sa, d_sa, sizeof(u32) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sa_host_dst = sa;   // copied out by sa_ready() as soon as it is final, under the inverse's kernels
+    const int st = build_sa_device(ctx, d_text, n, d_sa, d_rank, stats);
+    const bool sa_pending = ctx->sa_host_dst != nullptr;
+    ctx->sa_host_dst = nullptr;
+    if (st != RESEQ_OK) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        return st;
+    }
+    if (sa_pending) RSQ_CUDA(cudaMemcpyAsync(sa, d_sa, sizeof(u32) * n, cudaMemcpyDeviceToHost, ctx->stream));
     if (rank)
         RSQ_CUDA(cudaMemcpyAsync(rank, d_rank, sizeof(u32) * n, cudaMemcpyDeviceToHost, ctx->stream));
     RSQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    RSQ_CUDA(cudaStreamSynchronize(ctx->copy_stream));
     return RESEQ_OK;
 }
 

@@ -60,6 +60,20 @@ struct reseq_cuda_ctx {
     size_t arena_cap = 0;
     size_t arena_used = 0;
 
+    // Host-buffer builds: the suffix array is final before its inverse is computed, so its D2H copy
+    // is started on a second stream the moment it is (sa_ready), under the inverse's kernels.
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_event = nullptr;
+    uint32_t* sa_host_dst = nullptr;   // set by reseq_cuda_build_sa for the duration of one build
+    int sa_ready(const uint32_t* d_sa, size_t n) {
+        if (!sa_host_dst) return RESEQ_OK;
+        if (cudaEventRecord(copy_event, stream) != cudaSuccess || cudaStreamWaitEvent(copy_stream, copy_event, 0) != cudaSuccess ||
+            cudaMemcpyAsync(sa_host_dst, d_sa, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, copy_stream) != cudaSuccess)
+            return ::rsq::fail(RESEQ_CUDA_ERROR, "early copy-out of the suffix array failed");
+        sa_host_dst = nullptr;
+        return RESEQ_OK;
+    }
+
     // pinned staging word for small D2H reads (round-termination flags etc.)
     uint64_t* pinned = nullptr;
 

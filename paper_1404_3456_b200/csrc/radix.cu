@@ -51,7 +51,6 @@ int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws) {
 
 template <typename KeyT, bool HAS_VAL, int LOAD>
 static const char* pass_name() {
-    if (LOAD == kLoadPackIota) return "onesweep_u64_pack_iota";
     return sizeof(KeyT) == 8 ? (HAS_VAL ? "onesweep_u64_pairs" : "onesweep_u64_keys")
                              : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys");
 }
@@ -159,30 +158,6 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
     }
     *in_b = flipped;
     return RESEQ_OK;
-}
-
-template <int LOAD>
-static int partition_impl(reseq_cuda_ctx* ctx, const void* in, u64* out, size_t n, int shift, int bits,
-                          const SortWorkspace& ws) {
-    if (n == 0) return RESEQ_OK;
-    RSQ_CUDA(cudaMemsetAsync(ws.tickets, 0, sizeof(u32) * kMaxPasses, ctx->stream));
-    RSQ_LAUNCH_BEGIN(ctx, "digit_base_kernel");
-    digit_base_kernel<<<1, kRadix, 0, ctx->stream>>>(ws.hist, ws.base);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_CUDA(cudaGetLastError());
-    // the partition digit lives in the upper word of the record
-    return launch_pass<u64, false, LOAD>(ctx, in, out, nullptr, nullptr, n, 32 + shift, (1u << bits) - 1u, ws.base,
-                                         ws.lookback, ws.tickets);
-}
-
-int onesweep_partition_pack_iota(reseq_cuda_ctx* ctx, const u32* v, u64* out, size_t n, int shift, int bits,
-                                 const SortWorkspace& ws) {
-    return partition_impl<kLoadPackIota>(ctx, v, out, n, shift, bits, ws);
-}
-
-int onesweep_partition_packed(reseq_cuda_ctx* ctx, const u64* in, u64* out, size_t n, int shift, int bits,
-                              const SortWorkspace& ws) {
-    return partition_impl<kLoadPlain>(ctx, in, out, n, shift, bits, ws);
 }
 
 template int onesweep_sort<u32>(reseq_cuda_ctx*, u32*, u32*, u32*, u32*, size_t, const PassTable&,

@@ -359,13 +359,4 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
                   size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
                   u32 skip_mask, bool* in_b);
 
-// One stable partition pass producing (value, index) records: element i of the input is the
-// u64 (v[i] << 32) | i, partitioned on bits [shift, shift + bits) of v.  ws.hist[0..255] must
-// hold the digit counts.
-int onesweep_partition_pack_iota(reseq_cuda_ctx* ctx, const u32* v, u64* out, size_t n, int shift, int bits,
-                                 const SortWorkspace& ws);
-// The same for records already packed as (v << 32) | payload.
-int onesweep_partition_packed(reseq_cuda_ctx* ctx, const u64* in, u64* out, size_t n, int shift, int bits,
-                              const SortWorkspace& ws);
-
 }  // namespace rsq

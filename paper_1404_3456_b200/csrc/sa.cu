@@ -474,7 +474,8 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
                     const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
                     int max_rounds, bool use_shortcut, u32* __restrict__ counters,
                     const u32* __restrict__ cov, u32 period, u64 period_magic,
-                    const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits) {
+                    const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits,
+                    const u8* __restrict__ g_tileflags) {
     constexpr int KSYM = UNI ? kUniK : kElemK;             // symbols every member of a group shares
     constexpr int KEYSHIFT = UNI ? 33 : kElemKeyShift;     // record bits above this are the group key
     constexpr u32 ESCBIT = UNI ? (kElemEscBit >> 1) : kElemEscBit;
@@ -500,6 +501,9 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     u32* s_cnt = s_fail + kRefWords;                             // [words + 1] tied-count scan
     __shared__ int s_first, s_end, s_last;
 
+    if constexpr (UNI) {
+        if (!g_tileflags[blockIdx.x]) return;   // no uncovered member in this tile or the next: nothing to re-sort
+    }
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     const u64 t0 = static_cast<u64>(blockIdx.x) * kRefTile;
@@ -580,7 +584,11 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     }
     __syncthreads();
     const int first = s_first;
-    if (first == 0x7fffffff) return;  // no group starts in this tile
+    if (first == 0x7fffffff) {        // no group starts in this tile
+        // UNI: the tile was flagged, so a group with uncovered members runs through all of it
+        if (UNI && tid == 0) atomicOr(counters + 1, 1u);
+        return;
+    }
     int end = s_end;
     if (end == 0x7fffffff) {          // the tile's last group overruns the window
         if (tid == 0) atomicOr(counters + 1, 1u);
@@ -1052,7 +1060,7 @@ link_reads_kernel(const u64* __restrict__ elems, u64 m, const u64* __restrict__ 
 __global__ void __launch_bounds__(256)
 accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u32* __restrict__ cov, u32 period,
                       u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
-                      u32* __restrict__ uncbits) {
+                      u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
     constexpr int kPer = 4;   // records per thread in flight
     constexpr u32 ESC = kElemEscBit >> 1;
     const unsigned lane = lane_id();
@@ -1094,6 +1102,11 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u32* __restric
             if (lane == 0 && i < m) {
                 headbits[i >> 5] = hb;
                 uncbits[i >> 5] = ub;
+                if (ub) {   // the group of an uncovered member starts in this refine tile or the one before
+                    const u64 tile = i / kRefTile;
+                    tileflags[tile] = 1;
+                    if (tile) tileflags[tile - 1] = 1;
+                }
             }
         }
     }
@@ -1104,26 +1117,6 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u32* __restric
 // Instead the (sa[i] << 32 | i) records are first partitioned by the top bits of sa[i] -- two
 // streaming onesweep passes -- so that consecutive records target one small window of rank,
 // which is then scattered in shared memory and written as whole lines.
-__global__ void perm_digit_hist_kernel(u64 n, int shift, int bits, u32* __restrict__ hist) {
-    // sa is a permutation of [0, n): the number of values v with digit (v >> shift) & mask == d
-    // is known in closed form -- count of such v below n
-    const u64 d = threadIdx.x;
-    const u64 period = 1ull << (shift + bits), span = 1ull << shift;
-    if (d >= (1ull << bits)) { hist[d] = 0; return; }
-    const u64 full = n / period, rem = n % period;
-    const u64 lo = d * span;
-    const u64 part = rem > lo ? (rem - lo < span ? rem - lo : span) : 0;
-    hist[d] = static_cast<u32>(full * span + part);
-}
-
-__global__ void scatter_records_kernel(const u64* __restrict__ rec, u64 n, u32* __restrict__ rank) {
-    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const u64 r = rec[i];
-        rank[r >> 32] = static_cast<u32>(r);
-    }
-}
-
 // After the partition passes every aligned window of 2^win_bits rank entries has all of its
 // (pos << 32 | idx) records in the same index range of the record array (sa is a permutation, so
 // the buckets are exactly window-sized).  One CTA per window: scatter in shared memory, store the
@@ -1325,7 +1318,7 @@ size_t sa_workspace_bytes(size_t n) {
     total += pad(sizeof(u32) * n);                   // rank when the caller wants none
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
-    total += 3 * pad(sizeof(u32) * (n / 32 + 2));    // proof / head / uncovered bitmaps of the uniform read-set path
+    total += 3 * pad(sizeof(u32) * (n / 32 + 2 + n / kRefTile / 4 + 2));   // proof / head / uncovered bitmaps, tile flags
     total += pad(sizeof(u32) * inverse_scratch_words(n));
     total += sort_workspace_bytes(n);
     return total + 4096;
@@ -1430,7 +1423,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
     refine_elems_kernel<false><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m,
-                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr);
+                                                                  sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr, nullptr);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -1476,8 +1469,10 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     link_reads_kernel<<<grid_for(ctx, n, kLinkChunk, 1, 8), 256, 0, s>>>(sorted, n, packed, period, magic, cov);
     RSQ_LAUNCH_END(ctx);
     RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
+    u8* tileflags = reinterpret_cast<u8*>(uncbits + n / 32 + 2);   // carved behind the bitmap by the caller
+    RSQ_CUDA(cudaMemsetAsync(tileflags, 0, n / kRefTile + 2, s));
     accept_uniform_kernel<<<grid_for(ctx, n, 256, 4, 8), 256, 0, s>>>(sorted, n, cov, period, magic, sa_out, headbits,
-                                                                       uncbits);
+                                                                       uncbits, tileflags);
     RSQ_LAUNCH_END(ctx);
     static bool configured = false;
     if (!configured) {
@@ -1488,7 +1483,8 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
     refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sorted, n, sa_out, max_rounds, true,
-                                                                 counters, cov, period, magic, headbits, uncbits);
+                                                                 counters, cov, period, magic, headbits, uncbits,
+                                                                 tileflags);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -1531,7 +1527,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads, [4..7] refine
     u32* cov = ctx->alloc<u32>(n / 32 + 2);
     u32* headbits = ctx->alloc<u32>(n / 32 + 2);
-    u32* uncbits = ctx->alloc<u32>(n / 32 + 2);
+    u32* uncbits = ctx->alloc<u32>(n / 32 + 2 + (n / kRefTile + 2 + 3) / 4);   // + one flag byte per refine tile
     u32* inv_scratch = ctx->alloc<u32>(inverse_scratch_words(n));
     SortWorkspace ws;
     if (!packed || !sent || !keys_a || !keys_b || !vals_b || !head_of || !rank || !desc || !counters || !cov || !headbits || !uncbits || !inv_scratch)
@@ -1558,6 +1554,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
                                         ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
         if (unfinished == 0) {
             st.init_symbols = kUniK;
+            RSQ_TRY(ctx->sa_ready(d_sa, n));
             RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, inv_scratch));
             st.kernel_launches = ctx->launches - launches0;
             if (stats) *stats = st;
@@ -1578,6 +1575,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
                                 counters + 4, ws, &st, &unfinished));
         st.init_symbols = kElemK;
         if (unfinished == 0) {
+            RSQ_TRY(ctx->sa_ready(d_sa, n));
             RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, inv_scratch));
             st.kernel_launches = ctx->launches - launches0;
             if (stats) *stats = st;
