@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU-box visit: parity suite, bench line, ncu launch list, ncu full captures of the top kernels.
+# One GPU-box visit: parity suite, bench line, reference arm, ncu launch list, ncu full captures of the top kernels.
 # usage: scripts/gpu_round.sh <tag> [kernel-regex ...]
 set -u
 tag=${1:-x}; shift || true
