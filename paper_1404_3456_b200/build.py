@@ -81,6 +81,24 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+TOOL = PKG / "reseq_b200"
+
+
+def build_tools() -> Path:
+    """tools/reseq_b200.cpp -> paper_1404_3456_b200/reseq_b200 (build-sa / bench with the reference's
+    file formats), linked against the in-tree library."""
+    src = ROOT / "tools" / "reseq_b200.cpp"
+    deps = [src, ROOT / "include" / "reseq_cuda.h", ROOT / "include" / "reseq_b200" / "reseq_cuda.hpp"]
+    if TOOL.exists() and all(TOOL.stat().st_mtime >= d.stat().st_mtime for d in deps + [LIB]):
+        return TOOL
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"), str(src), str(LIB),
+           "-Wl,-rpath,$ORIGIN", "-o", str(TOOL)]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"tool build failed:\n{r.stdout}")
+    return TOOL
+
+
 def build_oracle() -> None:
     """Compiles oracle/liboracle.so and, when /root/reference is present, oracle/_ref."""
     r = subprocess.run(["make", "-C", str(ROOT / "oracle"), "all"], stdout=subprocess.PIPE,
@@ -91,5 +109,6 @@ def build_oracle() -> None:
 
 if __name__ == "__main__":
     build_library(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build_tools()
     build_oracle()
     print(LIB)

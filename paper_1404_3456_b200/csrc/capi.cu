@@ -215,7 +215,7 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
         return RESEQ_OK;
     }
     if (std::strcmp(name, "sort_cfg") == 0) {
-        if (value < 0 || value > 7) return fail(RESEQ_INVALID_ARGUMENT, "sort_cfg must be in 0..7");
+        if (value < 0 || value > 9) return fail(RESEQ_INVALID_ARGUMENT, "sort_cfg must be in 0..9");
         ctx->opt_sort_cfg = static_cast<int>(value);
         return RESEQ_OK;
     }

@@ -107,6 +107,8 @@ static int launch_pass(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u
         case 5: return launch_pass_cfg<KeyT, HAS_VAL, 384, 12, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
         case 6: return launch_pass_cfg<KeyT, HAS_VAL, 384, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
         case 7: return launch_pass_cfg<KeyT, HAS_VAL, 512, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 8: return launch_pass_cfg<KeyT, HAS_VAL, 384, 8, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
+        case 9: return launch_pass_cfg<KeyT, HAS_VAL, 256, 8, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
         default: break;
     }
     using T = SortTuning<KeyT, HAS_VAL>;

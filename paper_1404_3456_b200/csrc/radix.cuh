@@ -146,7 +146,7 @@ struct OnesweepCfg {
 };
 
 template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, int LOAD = kLoadPlain, bool HI = false>
-__global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? 4 : (BLOCK <= 384 ? 3 : (BLOCK <= 512 ? 2 : 1))))
+__global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? (ITEMS <= 8 ? 6 : 4) : (BLOCK <= 384 ? (ITEMS <= 8 ? 4 : 3) : (BLOCK <= 512 ? (ITEMS <= 8 ? 3 : 2) : 1))))
 onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,
                 u32 mask, const u32* __restrict__ digit_base, u64* __restrict__ lookback,
