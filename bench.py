@@ -42,12 +42,14 @@ WORKLOADS = {
     "c2": (4_600_000, 150, 920_000),
     "c3": (10_000_000, 150, 666_666),
     "c4": (100_000_000, 150, 6_666_666),
+    "c5": (300_000_000, 150, 20_000_000),
 }
 DESCRIPTION = {
     "c1": "config[0]: 1 Mbp genome, 100-bp reads, 10x (n=10.1M suffixes)",
     "c2": "config[1]: 4.6 Mbp genome, 150-bp reads, 30x (n=138.92M suffixes)",
     "c3": "config[2]: 100 Mbp concatenated read text (n=100.67M suffixes)",
     "c4": "config[3]: 1 Gbp read set (n=1.0067G suffixes)",
+    "c5": "config[4]: 3 Gbp human-scale read set (n=3.02G suffixes; beyond the reference's 2^31-1 cap)",
 }
 METRIC = "sa_build_msuffixes_per_s"
 UNIT = "Msuffixes/s"

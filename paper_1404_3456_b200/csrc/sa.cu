@@ -347,7 +347,7 @@ constexpr u32 kPMaxNear = 253;              // largest payload that encodes a di
 constexpr u32 kPFar = 254;
 constexpr u32 kPEot = 255;
 
-constexpr int kUniK = 15;                   // uniform read sets: symbols shared inside a group
+constexpr int kUniK = 16;                   // uniform read sets: symbols shared inside a group
 constexpr u32 kUniMinPeriod = 17, kUniMaxPeriod = 255;   // read length + 1 the uniform path accepts
 constexpr int kUniReads = 64;               // reads per CTA of the record generator
 
@@ -462,7 +462,8 @@ __device__ __forceinline__ u32 bases16(const u64* __restrict__ packed, u64 q) {
 // group stays contiguous): late steps cost in proportion to what is left.
 //
 // UNI: the records of a uniform read set (gen_uniform_kernel below): 15 shared symbols, groups
-// already in (terminator distance, position) order, and a bitmap `cov` of the positions that
+// already in (terminator distance, position) order, and a table `cov` (one byte per read: its
+// suffixes with at most that many symbols before the sentinel) of the positions that
 // link_reads_kernel proved to be a prefix of a LONGER suffix of their own group.  A group all of
 // whose members but the last carry that proof is final as it stands -- every chain of witnesses
 // ends in the last member, so all members are prefixes of it and (distance, position) is their
@@ -473,17 +474,20 @@ __global__ void __launch_bounds__(kRefBlock)
 refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n_text,
                     const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
                     int max_rounds, bool use_shortcut, u32* __restrict__ counters,
-                    const u32* __restrict__ cov, u32 period, u64 period_magic,
+                    const u8* __restrict__ cov, u32 period, u64 period_magic,
                     const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits,
                     const u8* __restrict__ g_tileflags) {
     constexpr int KSYM = UNI ? kUniK : kElemK;             // symbols every member of a group shares
-    constexpr int KEYSHIFT = UNI ? 33 : kElemKeyShift;     // record bits above this are the group key
-    constexpr u32 ESCBIT = UNI ? (kElemEscBit >> 1) : kElemEscBit;
+    constexpr int KEYSHIFT = kElemKeyShift;                // general records: bits above this are the group key
+    constexpr u32 ESCBIT = kElemEscBit;                    // (the uniform path reads its group heads from a bitmap)
     auto term_dist = [&](u32 pos) -> u32 {   // UNI only: symbols before the read's sentinel
         const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
         return period - 1u - (pos - q * period);
     };
-    auto covered = [&](u32 pos) -> bool { return (__ldg(cov + (pos >> 5)) >> (pos & 31)) & 1u; };
+    auto covered = [&](u32 pos) -> bool {    // UNI only: proven a prefix of a later member of its group
+        const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
+        return period - 1u - (pos - q * period) <= __ldg(cov + q);
+    };
     // n_text: length of the text the positions refer to; m: number of records (equal for a
     // whole-text build, a bucket of it for a multi-GPU rank)
     extern __shared__ __align__(16) unsigned char ref_smem[];
@@ -917,16 +921,16 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
 // A text of k reads of one length L (period P = L + 1: a sentinel at every position = P - 1 mod P,
 // nowhere else) is the shotgun read set of BASELINE.json.  Its records are generated TRANSPOSED:
 // record index t * k + r belongs to the suffix of read r with t symbols before its sentinel, so
-// the stable LSD sort leaves every group in (t, position) order -- which is the final order of a
-// group whose members all cover one locus (each is a prefix of the longer ones).  Record:
-//     key32 << 32 | pos
-//   key32  bits 31..8: bases 0..11, zero padded from the sentinel on.
-//          low byte, t <= 12:  2 t + 1 (< 0x80): finished by the sort, as in the general records
-//          low byte, t >= 13:  0x80 | bases 12..14 (zero padded) << 1 | S,  S = 1 for a whole read
-//          (t = L).  S is not a sort bit: the passes cover record bits 33..63.
-// 15 shared symbols instead of 11: a 4.6 Mbp genome has 4.6 M loci against 4^15 = 1.07 G keys, so
-// a group is one locus but for chance repeats; the fourth digit pass buys groups that need no
-// sorting at all.
+// the stable LSD sort leaves every run of equal keys in (t, position) order -- which is the final
+// order of a run whose members all cover one locus (each is a prefix of the longer ones).  Record:
+//     key32 << 32 | pos,   key32 = the first 16 bases, zero padded from the sentinel on.
+// No length code is needed: a suffix with t < 16 symbols ties only with suffixes that continue its
+// t symbols with A's, it is a prefix of every one of them, and with the (t, position) start order
+// the stable sort puts it first -- suffixes that short are final after the sort and are group
+// heads by themselves; a group is what remains: >= 16 shared symbols.  Whole reads (t = L) are
+// recognised arithmetically (position mod period = 0).  A 4.6 Mbp genome has 4.6 M loci against
+// 4^16 = 4.3 G keys, so a group is one locus but for chance repeats; the fourth digit pass buys
+// groups that need no sorting at all.
 
 __global__ void uniform_check_kernel(const u64* __restrict__ sent, u32 period, u64 k, u32* __restrict__ bad) {
     const u64 r = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -958,13 +962,11 @@ gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u64* __res
         const u32 wi = bit >> 6, sh = bit & 63;
         const u64 hi = s_w[wi], lo = s_w[wi + 1];
         const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
-        u32 b15 = static_cast<u32>(win >> 34);                          // 15 bases
-        if (t < kUniK) b15 &= ~((1u << (2 * (kUniK - t))) - 1u);        // zero padded from the sentinel on
-        const u32 low = t <= 12 ? 2 * t + 1 : (kElemEscBit | ((b15 & 0x3fu) << 1) | (t == period - 1 ? 1u : 0u));
-        const u32 key = ((b15 >> 6) << 8) | low;
+        u32 key = static_cast<u32>(win >> 32);                          // 16 bases
+        if (t < kUniK) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;   // zero padded from the sentinel on
         const u64 pos = (r0 + rl) * period + (period - 1 - t);
         elems[static_cast<u64>(t) * k + r0 + rl] = (static_cast<u64>(key) << 32) | pos;
-        atomicAdd(&s_hist[(key >> 1) & 0x7fu], 1u);
+        atomicAdd(&s_hist[key & 0xffu], 1u);
         atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
         atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
         atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
@@ -984,15 +986,16 @@ constexpr int kLinkChunk = 16384;   // records scanned per CTA before the whole 
 constexpr int kLinkQueue = 4096;
 
 __device__ __forceinline__ void link_one_read(const u64* __restrict__ elems, u64 i, const u64* __restrict__ packed,
-                                              u32 period, u64 period_magic, u32* __restrict__ cov) {
+                                              u32 period, u64 period_magic, u8* __restrict__ cov) {
     const u64 e = elems[i];
     const u32 pos_b = static_cast<u32>(e);
     for (u64 s = 1; s <= 16 && s <= i; ++s) {
         const u64 ea = elems[i - s];
-        if ((ea >> 33) != (e >> 33)) break;
+        if ((ea >> 32) != (e >> 32)) break;
         const u32 pos_a = static_cast<u32>(ea);
         const u32 q = static_cast<u32>(__umul64hi(pos_a, period_magic));
-        const u32 t_a = period - 1u - (pos_a - q * period);       // <= L: the group is in (t, pos) order
+        const u32 t_a = period - 1u - (pos_a - q * period);       // <= L: the run is in (t, pos) order
+        if (t_a < static_cast<u32>(kUniK)) break;                 // only shorter suffixes before this one: not of the group
         bool ok = true;
         for (u32 c = 0; c < t_a && ok; c += 32) {
             const u64 wa = base_window(packed, static_cast<u64>(pos_a) + c);
@@ -1001,13 +1004,7 @@ __device__ __forceinline__ void link_one_read(const u64* __restrict__ elems, u64
             ok = ((wa ^ wb) >> (64 - 2 * nb)) == 0;
         }
         if (!ok) continue;
-        const u32 lo = pos_a, hi = pos_a + t_a - 1;                // bits [lo, hi]
-        for (u32 w = lo >> 5; w <= hi >> 5; ++w) {
-            u32 mk = 0xffffffffu;
-            if (w == lo >> 5) mk &= 0xffffffffu << (lo & 31);
-            if (w == hi >> 5) mk &= 0xffffffffu >> (31 - (hi & 31));
-            atomicOr(cov + w, mk);
-        }
+        cov[q] = static_cast<u8>(t_a);   // read q: every suffix with <= t_a symbols left is proven (a racing second proof is as good)
         return;
     }
 }
@@ -1017,7 +1014,7 @@ __device__ __forceinline__ void link_one_read(const u64* __restrict__ elems, u64
 // reads it meets in shared memory and then compares them with every lane busy.
 __global__ void __launch_bounds__(256)
 link_reads_kernel(const u64* __restrict__ elems, u64 m, const u64* __restrict__ packed, u32 period,
-                  u64 period_magic, u32* __restrict__ cov) {
+                  u64 period_magic, u8* __restrict__ cov) {
     __shared__ u32 s_q[kLinkQueue];
     __shared__ u32 s_n;
     for (u64 base = static_cast<u64>(blockIdx.x) * kLinkChunk; base < m; base += static_cast<u64>(gridDim.x) * kLinkChunk) {
@@ -1039,7 +1036,8 @@ link_reads_kernel(const u64* __restrict__ elems, u64 m, const u64* __restrict__ 
                 const u64 e2[2] = {v[c].x, v[c].y};
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    if ((static_cast<u32>(e2[h] >> 32) & 0x81u) != 0x81u) continue;   // a whole read among the escape records
+                    const u32 p = static_cast<u32>(e2[h]);
+                    if (j + h >= cnt || p != static_cast<u32>(__umul64hi(p, period_magic)) * period) continue;   // whole reads only
                     const u32 slot = atomicAdd(&s_n, 1u);
                     if (slot < kLinkQueue) s_q[slot] = j + h;
                     else link_one_read(elems, base + j + h, packed, period, period_magic, cov);   // queue full (clustered duplicates)
@@ -1058,11 +1056,10 @@ link_reads_kernel(const u64* __restrict__ elems, u64 m, const u64* __restrict__ 
 // bitmaps it decides that from: group heads (key change, or a suffix finished by the sort) and
 // members that are neither the last of their group nor proven a prefix of a later member.
 __global__ void __launch_bounds__(256)
-accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u32* __restrict__ cov, u32 period,
+accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict__ cov, u32 period,
                       u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
                       u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
     constexpr int kPer = 4;   // records per thread in flight
-    constexpr u32 ESC = kElemEscBit >> 1;
     const unsigned lane = lane_id();
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     for (u64 i0 = ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * (32 * kPer); i0 < m;
@@ -1087,16 +1084,20 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u32* __restric
             if (lane == 0) ep = prev_last;
             if (lane == 31) en = next_first;
             const bool in = i < m;
-            const u32 key = static_cast<u32>(e[c] >> 33), kp = static_cast<u32>(ep >> 33), kn = static_cast<u32>(en >> 33);
-            const bool head = in && (i == 0 || key != kp || !(key & ESC));
-            const bool last = i + 1 >= m || kn != key || !(kn & ESC);
+            const u32 key = static_cast<u32>(e[c] >> 32), kp = static_cast<u32>(ep >> 32), kn = static_cast<u32>(en >> 32);
+            auto term = [&](u32 p, u32* q) {
+                *q = static_cast<u32>(__umul64hi(p, period_magic));
+                return period - 1u - (p - *q * period);
+            };
             const u32 pos = static_cast<u32>(e[c]);
-            bool unc = false;
-            if (in && !last) {
-                const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
-                const u32 t = period - 1u - (pos - q * period);
-                unc = t >= static_cast<u32>(kUniK) && !((__ldg(cov + (pos >> 5)) >> (pos & 31)) & 1u);
-            }
+            u32 q, qn, qp;
+            const u32 t = term(pos, &q), tp = term(static_cast<u32>(ep), &qp), tn = term(static_cast<u32>(en), &qn);
+            constexpr u32 K = kUniK;
+            // a suffix shorter than the key is final after the sort; a group starts where the key
+            // changes or right behind such a suffix
+            const bool head = in && (i == 0 || key != kp || t < K || tp < K);
+            const bool last = i + 1 >= m || kn != key || tn < K;   // (t < K: the next record is a head then, too)
+            const bool unc = in && !last && t >= K && t > __ldg(cov + q);
             if (in) sa_out[i] = pos;
             const unsigned hb = __ballot_sync(0xffffffffu, head), ub = __ballot_sync(0xffffffffu, unc);
             if (lane == 0 && i < m) {
@@ -1345,7 +1346,8 @@ size_t sa_workspace_bytes(size_t n) {
     total += pad(sizeof(u32) * n);                   // rank when the caller wants none
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
-    total += 3 * pad(sizeof(u32) * (n / 32 + 2 + n / kRefTile / 4 + 2));   // proof / head / uncovered bitmaps, tile flags
+    total += pad(n / kUniMinPeriod + 2);             // uniform read-set path: proof table, one byte per read
+    total += 2 * pad(sizeof(u32) * (n / 32 + 2 + n / kRefTile / 4 + 2));   // head / uncovered bitmaps, tile flags
     total += pad(sizeof(u32) * inverse_scratch_words(n));
     total += sort_workspace_bytes(n);
     return total + 4096;
@@ -1468,14 +1470,14 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
 // accepted as they stand.  *unfinished != 0 (a read set that is not uniform after all, an oversize
 // group, a step limit) sends the caller to the general paths.
 int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
-                            u64* elems_a, u64* elems_b, u32* cov, u32* headbits, u32* uncbits, u32* sa_out,
+                            u64* elems_a, u64* elems_b, u8* cov, u32* headbits, u32* uncbits, u32* sa_out,
                             int max_rounds, u32* counters,
                             const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
     cudaStream_t s = ctx->stream;
     const u64 magic = ~0ull / period + 1;   // ceil(2^64 / period): floor(pos / period) = mulhi(pos, magic) for pos < 2^32
     RSQ_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(u32), s));
     RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * 4 * kRadix, s));
-    RSQ_CUDA(cudaMemsetAsync(cov, 0, sizeof(u32) * (n / 32 + 2), s));
+    RSQ_CUDA(cudaMemsetAsync(cov, 0, k, s));
     RSQ_LAUNCH_BEGIN(ctx, "uniform_check_kernel");
     uniform_check_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, s>>>(sent, period, k, counters + 3);
     RSQ_LAUNCH_END(ctx);
@@ -1484,10 +1486,7 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
                                                                                              ws.hist);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
-    PassTable pt{};
-    pt.count = 4;
-    const unsigned char shifts[4] = {33, 40, 48, 56}, bits[4] = {7, 8, 8, 8};
-    for (int p = 0; p < 4; ++p) { pt.shift[p] = shifts[p]; pt.bits[p] = bits[p]; }
+    const PassTable pt = make_passes(32, 64);
     bool in_b = false;
     RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b));
     st->sort_passes += pt.count;
@@ -1552,7 +1551,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     const size_t rank_tiles = (n + kRankTile - 1) / kRankTile;
     u64* desc = ctx->alloc<u64>(rank_tiles + 4);
     u32* counters = ctx->alloc<u32>(256);  // [0] bad byte flag, [1] rerank ticket, [2] heads, [4..7] refine
-    u32* cov = ctx->alloc<u32>(n / 32 + 2);
+    u8* cov = ctx->alloc<u8>(n / kUniMinPeriod + 2);   // one byte per read of a uniform read set
     u32* headbits = ctx->alloc<u32>(n / 32 + 2);
     u32* uncbits = ctx->alloc<u32>(n / 32 + 2 + (n / kRefTile + 2 + 3) / 4);   // + one flag byte per refine tile
     u32* inv_scratch = ctx->alloc<u32>(inverse_scratch_words(n));

@@ -55,7 +55,7 @@ def check(rq, ex, oracle, text):
         assert np.array_equal(alt.sa, wsa), f"text-round sa differs for text of length {len(text)}"
         assert np.array_equal(alt.rank, wrank)
         alt = rq.build_parallel(text, no_uniform_executor(rq))
-        assert alt.stats.init_symbols != 15
+        assert alt.stats.init_symbols != 16
         assert np.array_equal(alt.sa, wsa), f"general-record sa differs for text of length {len(text)}"
         assert np.array_equal(alt.rank, wrank)
     return got
@@ -153,7 +153,7 @@ def test_generic_byte_texts(rq, ex, oracle):
 def test_read_sets_against_the_oracle(rq, ex, oracle, G, L, k):
     text, _ = rq.synth_read_text(G, L, k)
     got = check(rq, ex, oracle, text)
-    assert got.stats.alphabet == 0 and got.stats.init_symbols == 15    # the uniform read-set path
+    assert got.stats.alphabet == 0 and got.stats.init_symbols == 16    # the uniform read-set path
     assert got.stats.rounds <= 6 and got.stats.refined_global == 0
     alt = rq.build_parallel(text, no_uniform_executor(rq))
     assert alt.stats.init_symbols == 11 and np.array_equal(alt.sa, got.sa)
@@ -193,7 +193,7 @@ def test_uniform_path_with_many_resorted_groups_at_partitioned_inverse_size(rq, 
     text = np.frombuffer(_reads(genome, 100, starts), dtype=np.uint8)
     assert text.size >= 1 << 22
     got = rq.build_parallel(text, ex)
-    assert got.stats.init_symbols == 15 and got.stats.rounds >= 1     # some groups took refinement steps
+    assert got.stats.init_symbols == 16 and got.stats.rounds >= 1     # some groups took refinement steps
     assert oracle.verify_sa(text, got.sa) == 0
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
     alt = rq.build_parallel(text, no_uniform_executor(rq))
@@ -234,7 +234,7 @@ def test_config1_full_size_fingerprint_and_proof(rq, ex, oracle):
     permutation + adjacent-order verifier is a proof of equality at this size."""
     text, _ = rq.synth_read_text(1_000_000, 100, 100_000)
     got = rq.build_parallel(text, ex)
-    assert got.stats.rounds <= 4 and got.stats.refined_global == 0 and got.stats.init_symbols == 15
+    assert got.stats.rounds <= 4 and got.stats.refined_global == 0 and got.stats.init_symbols == 16
     assert oracle.checksum_u32(got.sa) == 11642757783061468293
     assert oracle.verify_sa(text, got.sa) == 0
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
@@ -287,7 +287,7 @@ def test_oversize_groups_hand_over_to_prefix_doubling(rq, ex, oracle):
     text = (b"ACGTACGTAC" * 12 + b"\0") * 3000          # 3000 identical reads: groups of 3000
     got = check(rq, ex, oracle, text)
     # the uniform path proves every duplicate a prefix of the next one: no group needs sorting, whatever its size
-    assert got.stats.init_symbols == 15 and got.stats.refined_global == 0
+    assert got.stats.init_symbols == 16 and got.stats.refined_global == 0
     alt = rq.build_parallel(text, no_uniform_executor(rq))
     assert alt.stats.refined_global > 0 and np.array_equal(alt.sa, got.sa)
     rng = np.random.default_rng(8)
