@@ -357,7 +357,7 @@ constexpr int kRefExt = 640;
 constexpr int kRefCap = kRefTile + kRefExt;
 constexpr int kRefWords = kRefCap / 32 + 2;
 constexpr size_t kRefSmem = sizeof(u64) * kRefCap + sizeof(u32) * kRefCap + 4 * sizeof(unsigned short) * kRefCap +
-                            sizeof(u32) * (4 * kRefWords + 16);
+                            sizeof(u32) * (5 * kRefWords + 16);
 constexpr int kStepK = 16;          // bases compared per refinement step
 constexpr u32 kDistCap = 4095;      // farthest sentinel the bitmap scan looks for
 constexpr u32 kTdNone = 0xFFFF;     // "terminator not known": the suffix can only be split by its bases
@@ -503,6 +503,7 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     u32* s_new = s_bits + kRefWords;                             // [words] heads created this step
     u32* s_fail = s_new + kRefWords;                             // [words] subgroups that failed the prefix check
     u32* s_cnt = s_fail + kRefWords;                             // [words + 1] tied-count scan
+    u32* s_mine = s_cnt + kRefWords + 16;                        // [words] UNI: members of the groups this CTA re-sorts
     __shared__ int s_first, s_end, s_last;
 
     if constexpr (UNI) {
@@ -615,20 +616,12 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
             any |= u != 0;
         }
         if (!__syncthreads_or(any)) return;
-        for (int a = first + tid; a < end; a += kRefBlock) s_key[a] = elems[t0 + a];
-        __syncthreads();
     }
 
     // -- unpack the records this CTA owns: position, and 2 * t + kind from the terminator byte ----
-    for (int a = first + tid; a < end; a += kRefBlock) {
+    for (int a = first + tid; a < end && !UNI; a += kRefBlock) {
         const u64 e = s_key[a];
         const u32 pos = static_cast<u32>(e);
-        if constexpr (UNI) {
-            const u32 t = term_dist(pos);
-            s_pos[a] = pos;
-            s_td[a] = static_cast<unsigned short>(2 * t + 1);   // period <= 255: always known
-            continue;
-        }
         const u32 p = static_cast<u32>(e >> 32) & 0xffu;
         u32 td;
         if (p < kPShortEnd) td = p;
@@ -714,8 +707,16 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
                 if (base + 32 > end) own &= (1u << (end - base)) - 1u;
             }
             s_bits[j] |= ~s_fail[j] & own;   // every member of a clean group is final: a head
+            s_mine[j] = s_fail[j] & own;     // the others are all this CTA reads, sorts and writes back
             s_new[j] = 0;
             s_fail[j] = 0;
+        }
+        __syncthreads();
+        for (int a = first + tid; a < end; a += kRefBlock) {
+            if (!((s_mine[a >> 5] >> (a & 31)) & 1u)) continue;
+            const u32 pos = sa_out[t0 + a];   // accept_uniform_kernel left the sorted records' positions there
+            s_pos[a] = pos;
+            s_td[a] = static_cast<unsigned short>(2 * term_dist(pos) + 1);   // period <= 255: always known
         }
         __syncthreads();
     }
@@ -908,6 +909,7 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
     // write the tile's suffixes once; count what is still tied
     u32 nonheads = 0;
     for (int a = first + tid; a < end; a += kRefBlock) {
+        if (UNI && !((s_mine[a >> 5] >> (a & 31)) & 1u)) continue;
         sa_out[t0 + a] = s_pos[a];
         nonheads += !is_head(a);
     }
