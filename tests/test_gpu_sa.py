@@ -249,6 +249,49 @@ def test_config2_full_size_proof(rq, ex, oracle):
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
 
 
+def test_config5_three_billion_suffixes_beyond_the_reference_cap(rq, oracle):
+    """BASELINE config 5 (300 Mbp genome, 150 bp, 10x; n = 3.02 G > 2^31 - 1, the reference's cap,
+    suffix_array.hpp:64) on one B200 through the device-resident entry point: every index above 2^31
+    exercises the 64-bit address arithmetic of each kernel.  Proof of equality on the host
+    (permutation + adjacent suffix_less over all n), inverse checked on the device."""
+    import torch
+    free, _total = torch.cuda.mem_get_info()
+    if free < 120 * 2**30:
+        pytest.skip("needs ~105 GB of device memory")
+    try:
+        import psutil
+        if psutil.virtual_memory().available < 48 * 2**30:
+            pytest.skip("needs ~25 GB of host memory")
+    except ImportError:
+        pass
+    text, _ = rq.synth_read_text(300_000_000, 150, 20_000_000)
+    n = int(text.size)
+    assert n == 3_020_000_000
+    e = rq.Executor(0)
+    try:
+        d_text = torch.from_numpy(text).cuda()
+        d_sa = torch.empty(n, dtype=torch.int32, device="cuda")
+        d_rank = torch.empty(n, dtype=torch.int32, device="cuda")
+        st = rq.SaStats()
+        lib = rq._lib.load()
+        rq._lib.check(lib.reseq_cuda_build_sa_device(e.handle, C.c_void_p(d_text.data_ptr()), n,
+                                                     C.c_void_p(d_sa.data_ptr()), C.c_void_p(d_rank.data_ptr()), C.byref(st)))
+        e.synchronize()
+        assert st.init_symbols == 16 and st.refined_global == 0
+        chunk = 1 << 27
+        for b in range(0, n, chunk):
+            hi = min(n, b + chunk)
+            sa_c = d_sa[b:hi].to(torch.int64) & 0xFFFFFFFF
+            assert torch.equal(d_rank[sa_c].to(torch.int64) & 0xFFFFFFFF, torch.arange(b, hi, device="cuda", dtype=torch.int64))
+            del sa_c
+        sa = d_sa.cpu().numpy().view(np.uint32)
+        del d_sa, d_rank, d_text
+    finally:
+        e.close()
+        torch.cuda.empty_cache()
+    assert oracle.verify_sa(text, sa, threads=32) == 0
+
+
 def test_text_too_large_is_rejected_before_any_work(rq, ex):
     lib = rq._lib.load()
     dummy = np.zeros(16, np.uint8)
