@@ -4,8 +4,8 @@
 //     memory (hist_add, fused into whichever kernel produces the keys) and turned into
 //     per-pass exclusive digit bases by digit_base_kernel;
 //   - each pass is ONE kernel: tiles are claimed through an atomic ticket, keys are
-//     ranked inside the warp with match.any (warp-aggregated: one shared-memory
-//     read-modify-write per distinct digit per warp step, no atomics), tile totals are
+//     ranked inside the warp by ballots (warp-aggregated: one shared-memory atomicAdd
+//     per distinct digit per warp step), tile totals are
 //     chained across tiles by decoupled look-back (one 64-bit descriptor per digit), the
 //     tile is re-ordered through shared memory so every digit's run leaves as one
 //     contiguous, coalesced global store;

@@ -1,11 +1,18 @@
-// Suffix-array construction on sm_100a: 2-bit packing, k-mer initial ranking, prefix
-// doubling over (rank[i], rank[i+h]) pairs.
+// Suffix-array construction on sm_100a.
 //
-// Replaces build_parallel, suffix_array.hpp:61-124.  Same mathematical result -- the
-// unique permutation sorted by suffix_less (suffix_array.hpp:28-41) and its inverse --
-// reached with far fewer, far fatter phases:
+// Replaces build_parallel, suffix_array.hpp:61-124.  Same mathematical result -- the unique
+// permutation sorted by suffix_less (suffix_array.hpp:28-41) and its inverse -- by one of three
+// routes, chosen from what pack_dna_kernel finds in the text (build_sa_device at the bottom):
 //
-//   reference                                   here
+//   (i)   uniform read sets (k reads of one length): transposed 16-base records, 4 onesweep passes,
+//         one verified overlap per READ proves the order of its suffixes, groups accepted as they
+//         stand (gen_uniform / link_reads / accept_uniform / refine_elems<true>);
+//   (ii)  other DNA texts: 11.5-base records + terminator byte, 3 passes, groups finished in shared
+//         memory from the L2-resident 2-bit text (init_elems / refine_elems<false>);
+//   (iii) anything else -- generic alphabets, groups too large for (i)/(ii): prefix doubling over
+//         (rank[i], rank[i+h]) pairs, the reference's own scheme with fatter phases:
+//
+//   reference                                   route (iii)
 //   ---------------------------------------     ------------------------------------------
 //   1-byte initial ranks (:68-87)               13-base (DNA, 2-bit packed) or 3-byte
 //                                               (generic) sentinel-aware initial ranks:
@@ -21,6 +28,9 @@
 //                                               decoupled look-back, scatter fused
 //   inverse permutation phase (:118-122)        free: with all groups singletons the
 //                                               group-head rank array IS the inverse
+//
+// The inverse permutation of (i) and (ii) is two lean partition passes + a shared-memory window
+// scatter (inv_partition_persistent_kernel, window_scatter_kernel).
 //
 // Sentinel semantics (suffix_array.hpp:16-20): every byte 0 is its own symbol, ordered
 // by text position, below every other byte; end of text is below everything.  A suffix

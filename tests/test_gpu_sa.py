@@ -181,6 +181,11 @@ def test_uniform_read_sets_with_repeats_and_duplicates(rq, ex, oracle):
     reads = [g[i:i + 50] for i in rng.integers(0, 450, 300)]
     reads += reads[:100] + [r[:-1] + b"A" for r in reads[:100]] + [b"C" + r[1:] for r in reads[:50]]
     check(rq, ex, oracle, b"".join(r + b"\0" for r in reads))
+    # more whole reads inside one chunk than the link kernel's queue holds (they are compared inline then)
+    check(rq, ex, oracle, (b"ACGTACGTACGTACGT" + b"\0") * 6000)
+    check(rq, ex, oracle, (b"A" * 20 + b"\0") * 5000)                 # one group: every suffix of >= 16 A's
+    mixed = [b"A" * 20, b"A" * 19 + b"C", b"C" + b"A" * 19, b"ACGTA" * 4] * 1500
+    check(rq, ex, oracle, b"".join(r + b"\0" for r in mixed))        # oversize groups mixing loci: handed on
 
 
 def test_uniform_path_with_many_resorted_groups_at_partitioned_inverse_size(rq, ex, oracle):
