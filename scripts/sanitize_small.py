@@ -1,0 +1,52 @@
+"""Small end-to-end workload for compute-sanitizer (memcheck / racecheck / synccheck): every kernel
+family once, on inputs small enough for the tool's slowdown.  Asserts parity like the tests do."""
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+import paper_1404_3456_b200 as rq
+from tests.oracle_lib import Oracle
+
+ora = Oracle()
+ex = rq.Executor(0)
+rng = np.random.default_rng(1)
+
+def check(text, e=ex):
+    got = rq.build_parallel(text, e)
+    wsa, wrank = ora.build_sa(text)
+    assert np.array_equal(got.sa, wsa) and np.array_equal(got.rank, wrank)
+    return got
+
+# uniform read sets: clean, with repeats (refine), at partitioned-inverse size
+text, starts = rq.synth_read_text(40_000, 100, 4_000)
+assert check(text).stats.init_symbols == 16
+unit = bytes(rng.choice([65, 67, 71, 84], 3000).astype(np.uint8))
+genome = unit + unit[:1500] + unit
+reads = b"".join(genome[int(s):int(s) + 60] + b"\0" for s in rng.integers(0, len(genome) - 60, 3000))
+check(np.frombuffer(reads, np.uint8))
+big, _ = rq.synth_read_text(400_000, 100, 42_000)          # n = 4.24 M >= 2^22: partition passes + window scatter
+got = rq.build_parallel(big, ex)
+assert np.array_equal(got.rank[got.sa], np.arange(big.size, dtype=np.uint32)) and ora.verify_sa(big, got.sa) == 0
+# general DNA records, text steps, prefix doubling, generic bytes
+ragged = rng.choice([65, 67, 71, 84, 0], 60_000, p=[.24, .24, .24, .24, .04]).astype(np.uint8)
+check(ragged)
+e2 = rq.Executor(0); e2.set_option("sa_text_rounds", 0); check(ragged, e2); check(text, e2)
+e3 = rq.Executor(0); e3.set_option("sa_uniform", 0); check(text, e3)
+check(np.frombuffer(b"abthatb\0hatbpaab\0tbabhhatbpaa\0paabtabh\0bhaabtpb\0" * 50, np.uint8))
+check(np.frombuffer(b"A" * 5000, np.uint8))
+# primitives
+keys = rng.integers(0, 2**32, 50_000, dtype=np.uint64).astype(np.uint32)
+pay = np.arange(keys.size, dtype=np.uint32)
+k2, p2 = rq.radix_sort(keys, pay, ex)
+order = np.argsort(keys, kind="stable")
+assert np.array_equal(k2, keys[order]) and np.array_equal(p2, pay[order])
+assert np.array_equal(rq.exclusive_scan(np.ones(70_000, np.uint32), ex), np.arange(70_000, dtype=np.uint32))
+# index, queries, overlaps, merge
+fs = rq.fragment_set_from_text(text, starts)
+ix = rq.FragmentIndex(fs, ex)
+ov = ix.overlaps(20)
+lens = fs.lengths()
+wi, wj, ww = ora.overlap_list(fs.concat, fs.starts, lens, 20)
+assert np.array_equal(ov.i, wi) and np.array_equal(ov.j, wj) and np.array_equal(ov.w, ww)
+sup, order = rq.greedy_superstring_from_overlaps(fs, ov)
+assert len(sup) > 0
+print("sanitize_small: all parity checks passed")
