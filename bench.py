@@ -307,13 +307,12 @@ def main():
         "init_elems_kernel": 8.375, "onesweep_u64_keys": 16.0,
         "refine_elems_kernel": 13.4, "window_scatter_kernel": 12.0, "inv_partition_sa": 12.0, "inv_partition_rec": 16.0,
         "inverse_kernel": 8.0, "pair_key_kernel": 20.0, "rerank_kernel": 16.0, "hist_kernel": 4.0,
-        "gen_uniform_kernel": 8.25, "link_reads_kernel": 8.0, "accept_uniform_kernel": 12.25,
-        "refine_uniform_kernel": 12.125,
+        "gen_uniform_kernel": 8.25, "accept_uniform_kernel": 12.25,   # link / refine touch a few % of the suffixes: no figure
     }
     # dram__bytes_read.sum + dram__bytes_write.sum per launch at config 2, ncu --set full captures under
     # profiles/ (r1f): what the kernel really moved, next to the algorithmic figure above
     ncu_traffic = {"onesweep_u64_keys": 2.253e9, "accept_uniform_kernel": 1.707e9, "inv_partition_rec": 2.177e9,
-                   "window_scatter_kernel": 1.636e9, "gen_uniform_kernel": 1.086e9, "link_reads_kernel": 1.427e9}
+                   "window_scatter_kernel": 1.636e9, "gen_uniform_kernel": 1.086e9}
     if workload != "c2":
         ncu_traffic = {}
     kernels = {}

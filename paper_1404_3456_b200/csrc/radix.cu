@@ -49,7 +49,7 @@ int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws) {
     return RESEQ_OK;
 }
 
-template <typename KeyT, bool HAS_VAL, int LOAD>
+template <typename KeyT, bool HAS_VAL>
 static const char* pass_name() {
     return sizeof(KeyT) == 8 ? (HAS_VAL ? "onesweep_u64_pairs" : "onesweep_u64_keys")
                              : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys");
@@ -61,65 +61,69 @@ static size_t lookback_bytes_for(size_t n) {
     return sizeof(u64) * ((n + TILE - 1) / TILE) * kRadix;
 }
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, int LOAD, bool HI>
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT, bool HI>
 static int launch_pass_kernel(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
-                              size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket) {
+                              size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket,
+                              const EMIT& emit) {
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
-    auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, LOAD, HI>;
+    auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, HI>;
+    const size_t smem = Cfg::kSmem + (EMIT::kActive ? sizeof(u32) * (kEmitCap + 2) : 0);
     static bool configured = false;
     if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(Cfg::kSmem)));
+        RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         configured = true;
     }
     RSQ_CUDA(cudaMemsetAsync(lookback, 0, lookback_bytes_for<Cfg::kTile>(n), ctx->stream));
     const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
-    RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL, LOAD>()));
-    kern<<<static_cast<unsigned>(tiles), BLOCK, Cfg::kSmem, ctx->stream>>>(
-        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, ctx->opt_lookahead);
+    RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL>()));
+    kern<<<static_cast<unsigned>(tiles), BLOCK, smem, ctx->stream>>>(
+        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, ctx->opt_lookahead, emit);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
 }
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, int LOAD>
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT>
 static int launch_pass_cfg(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
-                           size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket) {
+                           size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket,
+                           const EMIT& emit) {
     if constexpr (sizeof(KeyT) == 8) {
         if (shift >= 32)
-            return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, LOAD, true>(ctx, kin, kout, vin, vout, n, shift, mask,
-                                                                               base, lookback, ticket);
+            return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, true>(ctx, kin, kout, vin, vout, n, shift, mask,
+                                                                               base, lookback, ticket, emit);
     }
-    return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, LOAD, false>(ctx, kin, kout, vin, vout, n, shift, mask, base,
-                                                                        lookback, ticket);
+    return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, false>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+                                                                        lookback, ticket, emit);
 }
 
-template <typename KeyT, bool HAS_VAL, int LOAD = kLoadPlain>
+template <typename KeyT, bool HAS_VAL, class EMIT = EmitNone>
 static int launch_pass(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
                        size_t n, int shift, u32 mask, const u32* base, u64* lookback,
-                       u32* ticket) {
+                       u32* ticket, const EMIT& emit = EMIT{}) {
     // "sort_cfg" picks a tile shape (tuning knob; every shape gives the same result)
-    switch (ctx->opt_sort_cfg) {
-        case 1: return launch_pass_cfg<KeyT, HAS_VAL, 512, 8, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 2: return launch_pass_cfg<KeyT, HAS_VAL, 512, 12, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 3: return launch_pass_cfg<KeyT, HAS_VAL, 256, 12, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 4: return launch_pass_cfg<KeyT, HAS_VAL, 256, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 5: return launch_pass_cfg<KeyT, HAS_VAL, 384, 12, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 6: return launch_pass_cfg<KeyT, HAS_VAL, 384, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 7: return launch_pass_cfg<KeyT, HAS_VAL, 512, 16, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 8: return launch_pass_cfg<KeyT, HAS_VAL, 384, 8, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        case 9: return launch_pass_cfg<KeyT, HAS_VAL, 256, 8, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket);
-        default: break;
+    if constexpr (!EMIT::kActive) {
+        switch (ctx->opt_sort_cfg) {
+            case 1: return launch_pass_cfg<KeyT, HAS_VAL, 512, 8, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 2: return launch_pass_cfg<KeyT, HAS_VAL, 512, 12, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 3: return launch_pass_cfg<KeyT, HAS_VAL, 256, 12, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 4: return launch_pass_cfg<KeyT, HAS_VAL, 256, 16, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 5: return launch_pass_cfg<KeyT, HAS_VAL, 384, 12, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 6: return launch_pass_cfg<KeyT, HAS_VAL, 384, 16, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 7: return launch_pass_cfg<KeyT, HAS_VAL, 512, 16, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 8: return launch_pass_cfg<KeyT, HAS_VAL, 384, 8, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            case 9: return launch_pass_cfg<KeyT, HAS_VAL, 256, 8, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base, lookback, ticket, emit);
+            default: break;
+        }
     }
     using T = SortTuning<KeyT, HAS_VAL>;
-    return launch_pass_cfg<KeyT, HAS_VAL, T::kBlock, T::kItems, LOAD>(ctx, kin, kout, vin, vout, n, shift, mask, base,
-                                                                     lookback, ticket);
+    return launch_pass_cfg<KeyT, HAS_VAL, T::kBlock, T::kItems, EMIT>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+                                                                     lookback, ticket, emit);
 }
 
 template <typename KeyT>
 int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, u32* vals_b,
                   size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
-                  u32 skip_mask, bool* in_b) {
+                  u32 skip_mask, bool* in_b, const EmitMultiples* emit_last) {
     *in_b = false;
     if (n == 0 || pt.count == 0) return RESEQ_OK;
     const bool has_val = vals_a != nullptr;
@@ -145,8 +149,21 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
     u32* vin = vals_a;
     u32* vout = vals_b;
     bool flipped = false;
+    int last_pass = -1;
+    for (int p = 0; p < pt.count; ++p)
+        if (!(skip_mask & (1u << p))) last_pass = p;
     for (int p = 0; p < pt.count; ++p) {
         if (skip_mask & (1u << p)) continue;
+        if constexpr (sizeof(KeyT) == 8) {
+            if (emit_last && !has_val && p == last_pass) {
+                RSQ_TRY((launch_pass<KeyT, false, EmitMultiples>(ctx, kin, kout, nullptr, nullptr, n, pt.shift[p], pt.mask(p),
+                                                                 ws.base + p * kRadix, ws.lookback, ws.tickets + p,
+                                                                 *emit_last)));
+                KeyT* tk = kin; kin = kout; kout = tk;
+                flipped = !flipped;
+                continue;
+            }
+        }
         if (has_val)
             RSQ_TRY((launch_pass<KeyT, true>(ctx, kin, kout, vin, vout, n, pt.shift[p], pt.mask(p),
                                              ws.base + p * kRadix, ws.lookback, ws.tickets + p)));
@@ -163,8 +180,8 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
 }
 
 template int onesweep_sort<u32>(reseq_cuda_ctx*, u32*, u32*, u32*, u32*, size_t, const PassTable&,
-                                const SortWorkspace&, bool, u32, bool*);
+                                const SortWorkspace&, bool, u32, bool*, const EmitMultiples*);
 template int onesweep_sort<u64>(reseq_cuda_ctx*, u64*, u64*, u32*, u32*, size_t, const PassTable&,
-                                const SortWorkspace&, bool, u32, bool*);
+                                const SortWorkspace&, bool, u32, bool*, const EmitMultiples*);
 
 }  // namespace rsq

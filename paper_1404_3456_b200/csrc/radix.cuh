@@ -123,11 +123,25 @@ __device__ __forceinline__ unsigned warp_match_digit(u32 d) {
     return peers;
 }
 
-// How a pass reads its input.
-enum : int {
-    kLoadPlain = 0,     // keys_in[i] (and vals_in[i])
-    kLoadPackIota = 1,  // u64 keys only: keys_in is a u32 array v; element i is (v[i] << 32) | i
+// What a pass reports besides sorting.  EmitMultiples: the OUTPUT index of every record whose low
+// 32 bits are a multiple of `period` is appended to `list` (in no particular order) -- how the
+// suffix-array builder learns where the whole reads of a read set landed without another sweep
+// over the sorted records.  Hits are gathered per tile in shared memory: one global atomic per tile.
+struct EmitNone {
+    static constexpr bool kActive = false;
 };
+struct EmitMultiples {
+    static constexpr bool kActive = true;
+    u32 period;
+    u64 magic;    // ceil(2^64 / period)
+    u32* list;
+    u32* count;
+    __device__ __forceinline__ bool hit(u64 k) const {
+        const u32 p = static_cast<u32>(k);
+        return p == static_cast<u32>(__umul64hi(p, magic)) * period;
+    }
+};
+constexpr int kEmitCap = 510;   // hits staged per tile; the overflow goes out one atomic each
 
 // Digit of a key.  HI (u64 keys, shift >= 32): the digit lies in the upper word, one 32-bit
 // shift instead of a 64-bit funnel sequence -- the digit is extracted four times per item.
@@ -145,14 +159,14 @@ struct OnesweepCfg {
                                     sizeof(u32) * (kWarps * kRadix + kRadix + 32 + 4);
 };
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, int LOAD = kLoadPlain, bool HI = false>
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT = EmitNone, bool HI = false>
 __global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? (ITEMS <= 8 ? 6 : 4) : (BLOCK <= 384 ? (ITEMS <= 8 ? 4 : 3) : (BLOCK <= 512 ? (ITEMS <= 8 ? 3 : 2) : 1))))
 onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,
                 u32 mask, const u32* __restrict__ digit_base, u64* __restrict__ lookback,
-                u32* __restrict__ ticket, int lookahead) {
+                u32* __restrict__ ticket, int lookahead, EMIT emit) {
     static_assert(BLOCK >= kRadix && BLOCK % 32 == 0, "one thread per digit is assumed");
-    static_assert(LOAD == kLoadPlain || (sizeof(KeyT) == 8 && !HAS_VAL), "pack-iota feeds u64 keys only");
+    static_assert(!EMIT::kActive || sizeof(KeyT) == 8, "emit hooks look at 64-bit records");
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
     constexpr int WARPS = Cfg::kWarps;
     constexpr int TILE = Cfg::kTile;
@@ -164,12 +178,16 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     u32* s_gofs = s_whist + WARPS * kRadix;        // [256] global index of tile slot 0 of the digit
     u32* s_scan = s_gofs + kRadix;                 // [32] warp totals for the digit scan
     u32* s_tile = s_scan + 32;
+    u32* s_emit = s_tile + 4;                      // EMIT: [0] hits of this tile, [1] their base in the list, [2..] indices
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const unsigned lane = lane_id();
 
-    if (tid == 0) *s_tile = atomicAdd(ticket, 1u);
+    if (tid == 0) {
+        *s_tile = atomicAdd(ticket, 1u);
+        if (EMIT::kActive) s_emit[0] = 0;
+    }
     {
         uint4* z = reinterpret_cast<uint4*>(s_whist);
         for (int i = tid; i < WARPS * kRadix / 4; i += BLOCK) z[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -184,12 +202,7 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     KeyT key[ITEMS];
     u32 val[ITEMS];
     const u32 wbase = warp * (ITEMS * 32) + lane;
-    auto load_key = [&](u64 i) -> KeyT {
-        if constexpr (LOAD == kLoadPackIota)
-            return static_cast<KeyT>((static_cast<u64>(static_cast<const u32*>(keys_in_raw)[i]) << 32) | (i & 0xffffffffu));
-        else
-            return static_cast<const KeyT*>(keys_in_raw)[i];
-    };
+    auto load_key = [&](u64 i) -> KeyT { return static_cast<const KeyT*>(keys_in_raw)[i]; };
     if (full) {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) key[j] = load_key(tile_base + wbase + j * 32);
@@ -310,6 +323,15 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     __syncthreads();
 
     // -- coalesced scatter: consecutive slots of one digit go to consecutive addresses -
+    auto report = [&](KeyT k, u32 dst) {
+        if constexpr (EMIT::kActive) {
+            if (emit.hit(static_cast<u64>(k))) {
+                const u32 slot = atomicAdd(&s_emit[0], 1u);
+                if (slot < static_cast<u32>(kEmitCap)) s_emit[2 + slot] = dst;
+                else emit.list[atomicAdd(emit.count, 1u)] = dst;   // a tile dense with hits
+            }
+        }
+    };
     if (full) {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
@@ -318,6 +340,7 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
             const u32 dst = s_gofs[pass_digit<HI>(k, shift, mask)] + i;
             keys_out[dst] = k;
             if (HAS_VAL) vals_out[dst] = s_vals[i];
+            report(k, dst);
         }
     } else {
 #pragma unroll
@@ -328,8 +351,16 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
                 const u32 dst = s_gofs[pass_digit<HI>(k, shift, mask)] + i;
                 keys_out[dst] = k;
                 if (HAS_VAL) vals_out[dst] = s_vals[i];
+                report(k, dst);
             }
         }
+    }
+    if constexpr (EMIT::kActive) {
+        __syncthreads();
+        const u32 staged = s_emit[0] < static_cast<u32>(kEmitCap) ? s_emit[0] : static_cast<u32>(kEmitCap);
+        if (tid == 0 && staged) s_emit[1] = atomicAdd(emit.count, staged);
+        __syncthreads();
+        for (u32 x = tid; x < staged; x += BLOCK) emit.list[s_emit[1] + x] = s_emit[2 + x];
     }
 }
 
@@ -354,9 +385,10 @@ int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws);
 // passes (fused into its key-producing kernel); otherwise a histogram kernel runs first.
 // `skip_mask` bit p set => pass p is skipped (its digit is constant).  On return
 // *in_b says which buffer holds the result.
+// `emit_last` (u64 keys without payload only): hook run by the LAST pass, see EmitMultiples.
 template <typename KeyT>
 int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, u32* vals_b,
                   size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
-                  u32 skip_mask, bool* in_b);
+                  u32 skip_mask, bool* in_b, const EmitMultiples* emit_last = nullptr);
 
 }  // namespace rsq

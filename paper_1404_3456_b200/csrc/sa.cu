@@ -994,9 +994,6 @@ gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u64* __res
 // its own group (it shares all of the shorter one's symbols) -- and gets its bit in `cov`.  One
 // comparison per read pays for the ~L suffix comparisons it stands for.  Candidates of other loci
 // (chance repeats of the 15 symbols) fail the comparison and are passed over.
-constexpr int kLinkChunk = 16384;   // records scanned per CTA before the whole reads found are processed
-constexpr int kLinkQueue = 4096;
-
 __device__ __forceinline__ void link_one_read(const u64* __restrict__ elems, u64 i, const u64* __restrict__ packed,
                                               u32 period, u64 period_magic, u8* __restrict__ cov) {
     const u64 e = elems[i];
@@ -1021,46 +1018,15 @@ __device__ __forceinline__ void link_one_read(const u64* __restrict__ elems, u64
     }
 }
 
-// Whole reads are 1 record in period: a thread that stops to compare one stalls its warp for a
-// chain of dependent L2 loads.  Each CTA therefore streams a chunk of records, queues the whole
-// reads it meets in shared memory and then compares them with every lane busy.
+// One thread per whole read: `list` holds the indices at which the last sort pass left them
+// (EmitMultiples, radix.cuh), so nothing is swept to find them.
 __global__ void __launch_bounds__(256)
-link_reads_kernel(const u64* __restrict__ elems, u64 m, const u64* __restrict__ packed, u32 period,
-                  u64 period_magic, u8* __restrict__ cov) {
-    __shared__ u32 s_q[kLinkQueue];
-    __shared__ u32 s_n;
-    for (u64 base = static_cast<u64>(blockIdx.x) * kLinkChunk; base < m; base += static_cast<u64>(gridDim.x) * kLinkChunk) {
-        if (threadIdx.x == 0) s_n = 0;
-        __syncthreads();
-        const u32 cnt = static_cast<u32>(m - base < kLinkChunk ? m - base : kLinkChunk);
-        for (u32 j0 = threadIdx.x * 2; j0 < cnt; j0 += 2 * 256 * 4) {
-            ulonglong2 v[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const u32 j = j0 + c * 512;
-                v[c] = make_ulonglong2(0, 0);
-                if (j + 1 < cnt) v[c] = *reinterpret_cast<const ulonglong2*>(elems + base + j);   // base, j even: 16-byte aligned
-                else if (j < cnt) v[c].x = elems[base + j];
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const u32 j = j0 + c * 512;
-                const u64 e2[2] = {v[c].x, v[c].y};
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const u32 p = static_cast<u32>(e2[h]);
-                    if (j + h >= cnt || p != static_cast<u32>(__umul64hi(p, period_magic)) * period) continue;   // whole reads only
-                    const u32 slot = atomicAdd(&s_n, 1u);
-                    if (slot < kLinkQueue) s_q[slot] = j + h;
-                    else link_one_read(elems, base + j + h, packed, period, period_magic, cov);   // queue full (clustered duplicates)
-                }
-            }
-        }
-        __syncthreads();
-        const u32 nq = s_n < kLinkQueue ? s_n : kLinkQueue;
-        for (u32 q = threadIdx.x; q < nq; q += 256) link_one_read(elems, base + s_q[q], packed, period, period_magic, cov);
-        __syncthreads();
-    }
+link_reads_kernel(const u64* __restrict__ elems, const u32* __restrict__ list, const u32* __restrict__ count,
+                  const u64* __restrict__ packed, u32 period, u64 period_magic, u8* __restrict__ cov) {
+    const u64 k = *count;   // = the number of reads when the text really is uniform
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 x = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; x < k; x += stride)
+        link_one_read(elems, list[x], packed, period, period_magic, cov);
 }
 
 // The sorted records become the suffix array as they stand (sa_out[i] = position of record i)
@@ -1482,7 +1448,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
 // accepted as they stand.  *unfinished != 0 (a read set that is not uniform after all, an oversize
 // group, a step limit) sends the caller to the general paths.
 int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
-                            u64* elems_a, u64* elems_b, u8* cov, u32* headbits, u32* uncbits, u32* sa_out,
+                            u64* elems_a, u64* elems_b, u8* cov, u32* headbits, u32* uncbits, u32* whole, u32* sa_out,
                             int max_rounds, u32* counters,
                             const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
     cudaStream_t s = ctx->stream;
@@ -1500,11 +1466,13 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     RSQ_CUDA(cudaGetLastError());
     const PassTable pt = make_passes(32, 64);
     bool in_b = false;
-    RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b));
+    // the last pass also reports where the k whole reads (position = 0 mod period) ended up
+    const EmitMultiples emit{period, magic, whole, counters + 4};
+    RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b, &emit));
     st->sort_passes += pt.count;
     const u64* sorted = in_b ? elems_b : elems_a;
     RSQ_LAUNCH_BEGIN(ctx, "link_reads_kernel");
-    link_reads_kernel<<<grid_for(ctx, n, kLinkChunk, 1, 16), 256, 0, s>>>(sorted, n, packed, period, magic, cov);
+    link_reads_kernel<<<grid_for(ctx, k, 256, 1, 16), 256, 0, s>>>(sorted, whole, counters + 4, packed, period, magic, cov);
     RSQ_LAUNCH_END(ctx);
     RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
     u8* tileflags = reinterpret_cast<u8*>(uncbits + n / 32 + 2);   // carved behind the bitmap by the caller
@@ -1588,7 +1556,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
         n / n_separators >= kUniMinPeriod && n / n_separators <= kUniMaxPeriod) {
         u64 unfinished = 0;
         RSQ_TRY(uniform_sort_and_refine(ctx, packed, sent, n, static_cast<u32>(n / n_separators), n_separators, keys_a,
-                                        keys_b, cov, headbits, uncbits, d_sa,
+                                        keys_b, cov, headbits, uncbits, vals_b /* n words: the whole reads' indices */, d_sa,
                                         ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished));
         if (unfinished == 0) {
             st.init_symbols = kUniK;
