@@ -37,6 +37,8 @@ struct reseq_cuda_index {
     size_t n = 0, k = 0;
     bool dna = false;
     int dir_bases = 0;
+    int sdir_bases = 0;     // the start-suffix directory is shallower: k entries spread thin, and it stays in L2
+    u32 min_len = 0;
     u8* d_text = nullptr;
     u64* d_packed = nullptr;
     u64* d_sent = nullptr;
@@ -230,6 +232,8 @@ struct IndexView {
     const u32* dir;   // dir[x] = lower bound of D-base pattern x; nullptr when absent
     const u32* sdir;
     int D;
+    int sD;        // bases indexing sdir (<= D)
+    u32 min_len;   // shortest fragment
     u32 k;
 };
 
@@ -242,8 +246,9 @@ __device__ __forceinline__ void locate_residual(const IndexView& iv, u64 ppos, u
             const u32 x = static_cast<u32>(base_window(iv.tv.packed, ppos) >> (64 - 2 * iv.D));
             l0 = iv.dir[x];
             r0 = iv.dir[x + 1];
-            f0 = iv.sdir[x];
-            f1 = iv.sdir[x + 1];
+            const u32 xs = x >> (2 * (iv.D - iv.sD));
+            f0 = iv.sdir[xs];
+            f1 = iv.sdir[xs + 1];
         }
         bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_packed(iv.tv, spos, ppos, m); }, lo, hi);
     } else {
@@ -264,10 +269,33 @@ __device__ __forceinline__ void locate_residual(const IndexView& iv, u64 ppos, u
 // Same (s_first, s_last) as locate_residual; ~3 DRAM gathers per query instead of ~12.
 __device__ __forceinline__ void locate_residual_starts(const IndexView& iv, u64 ppos, u32 m, u32* s_first,
                                                        u32* s_last) {
+    // the bracket of the start suffixes does not depend on the rank: both chains of loads (rank from
+    // HBM; text word -> L2-resident directory) are issued before either result is needed
+    u32 f0 = 0, f1 = iv.k;
     const u32 r = iv.rank[ppos];
-    auto is_match = [&](u32 idx) { return cmp_packed(iv.tv, iv.sa[idx], ppos, m) >= 0; };   // idx <= r: never greater
+    if (iv.sdir && m >= static_cast<u32>(iv.sD)) {
+        const u32 x = static_cast<u32>(base_window(iv.tv.packed, ppos) >> (64 - 2 * iv.sD));
+        f0 = iv.sdir[x];
+        f1 = iv.sdir[x + 1];
+    }
+    // idx <= r: the suffix there is never greater than the pattern; it is smaller -- no match -- exactly
+    // when it differs from it or ends first.  It usually ends first (the neighbour below a read suffix
+    // is the same locus seen from a read that ends earlier), which the sentinel bitmap alone tells:
+    // one to three loads instead of a chunk-by-chunk comparison of ~t symbols.
+    auto is_match = [&](u32 idx) {
+        const u64 spos = iv.sa[idx];
+        for (u32 c = 0; c < m; c += 64) {
+            if (spos + c >= iv.tv.n) return false;
+            u64 w = sent_window(iv.tv.sent, spos + c);
+            if (m - c < 64) w &= ~0ull << (64 - (m - c));
+            if (w) return false;                 // a sentinel inside the first m symbols
+        }
+        return cmp_packed(iv.tv, spos, ppos, m) >= 0;
+    };
     u32 ok = r, bad = 0xFFFFFFFFu;          // ok: lowest index known to match; bad: highest known not to (none yet)
-    for (u32 step = 1; ok > 0; step <<= 1) {
+    // The copies below r matter only if one of them is a whole fragment (equal to the pattern): none
+    // is when the pattern is shorter than every fragment -- every o > 0 query of a uniform read set.
+    for (u32 step = 1; ok > 0 && m >= iv.min_len; step <<= 1) {
         const u32 probe = ok > step ? ok - step : 0u;
         if (is_match(probe)) ok = probe;
         else { bad = probe; break; }
@@ -281,15 +309,21 @@ __device__ __forceinline__ void locate_residual_starts(const IndexView& iv, u64 
         }
     }
     const u32 lo = ok;
-    u32 f0 = 0, f1 = iv.k;
-    if (iv.sdir && m >= static_cast<u32>(iv.D)) {
-        const u32 x = static_cast<u32>(base_window(iv.tv.packed, ppos) >> (64 - 2 * iv.D));
-        f0 = iv.sdir[x];
-        f1 = iv.sdir[x + 1];
-    }
     const u32 sf = lower_bound_u32(iv.start_rank, f0, f1, lo);
+    // does fragment j begin with the pattern?  Both are runs of >= m bases when lens[j] >= m, so this
+    // is a plain comparison of packed words (no sentinel bookkeeping): the warp's lanes diverge here,
+    // and every instruction in this loop is paid by all of them.
+    auto begins_with_pattern = [&](u32 j) {
+        if (iv.lens[j] < m) return false;
+        const u64 a = iv.starts[j];
+        for (u32 c = 0; c < m; c += 32) {
+            const u32 nb = m - c < 32u ? m - c : 32u;
+            if ((base_window(iv.tv.packed, a + c) ^ base_window(iv.tv.packed, ppos + c)) >> (64 - 2 * nb)) return false;
+        }
+        return true;
+    };
     u32 sl = sf;
-    while (sl < f1 && cmp_packed(iv.tv, iv.starts[iv.start_frag[sl]], ppos, m) == 0) ++sl;
+    while (sl < f1 && begins_with_pattern(iv.start_frag[sl])) ++sl;
     *s_first = sf;
     *s_last = sl;
 }
@@ -503,6 +537,8 @@ IndexView view_of(const reseq_cuda_index* ix) {
     iv.dir = ix->dna && ix->d_dir ? ix->d_dir + 1 : nullptr;
     iv.sdir = ix->dna && ix->d_sdir ? ix->d_sdir + 1 : nullptr;
     iv.D = ix->dir_bases;
+    iv.sD = ix->sdir_bases;
+    iv.min_len = ix->min_len;
     iv.k = static_cast<u32>(ix->k);
     return iv;
 }
@@ -633,6 +669,7 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
                 if (seen[v]) lens.push_back(static_cast<u32>(v));
         }
         ix->n_lengths = static_cast<u32>(lens.size());
+        ix->min_len = lens.empty() ? 0u : lens.front();
         IX_TRY(dev_alloc(ix, &ix->d_lengths, lens.size()));
         IX_CUDA(cudaMemcpy(ix->d_lengths, lens.data(), sizeof(u32) * lens.size(), cudaMemcpyHostToDevice));
     }
@@ -641,17 +678,21 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
         bool is_dna = true;
         IX_TRY(pack_dna_device(ctx, ix->d_text, n, ix->d_packed, ix->d_sent, counters + 8, &is_dna, nullptr));
         ix->dir_bases = D;
+        ix->sdir_bases = D < 11 ? D : 11;   // 4^11 entries = 16 MB: L2-resident, and k start suffixes still land ~1 per bucket
+        const size_t sdir_entries = (size_t{1} << (2 * ix->sdir_bases)) + 2;
         IX_TRY(dev_alloc(ix, &ix->d_dir, dir_entries));
-        IX_TRY(dev_alloc(ix, &ix->d_sdir, dir_entries));
+        IX_TRY(dev_alloc(ix, &ix->d_sdir, sdir_entries));
         for (int which = 0; which < 2; ++which) {
-            IX_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * dir_entries, s));
+            const size_t entries = which == 0 ? dir_entries : sdir_entries;
+            IX_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * entries, s));
             const size_t count = which == 0 ? n : k;
             RSQ_LAUNCH_BEGIN(ctx, "dir_hist_kernel");
             dir_hist_kernel<<<grid_1d(ctx, count, 256), 256, 0, s>>>(
-                ix->d_packed, ix->d_sent, n, which == 0 ? nullptr : ix->d_starts, count, D, hist);
+                ix->d_packed, ix->d_sent, n, which == 0 ? nullptr : ix->d_starts, count,
+                which == 0 ? D : ix->sdir_bases, hist);
             RSQ_LAUNCH_END(ctx);
             IX_CUDA(cudaGetLastError());
-            IX_TRY(scan_table(ctx, hist, which == 0 ? ix->d_dir : ix->d_sdir, dir_entries));
+            IX_TRY(scan_table(ctx, hist, which == 0 ? ix->d_dir : ix->d_sdir, entries));
         }
     }
     IX_CUDA(cudaStreamSynchronize(s));
