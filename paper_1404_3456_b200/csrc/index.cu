@@ -377,6 +377,10 @@ locate_patterns_kernel(IndexView iv, const u8* __restrict__ pats, const u64* __r
 // whose prefix equals that pattern, i.e. overlap_weight(f_i, f_j) >= |f_i| - o
 // (overlap.hpp:16-23).  Stores, per query, the start-list interval; per fragment, the
 // absorb_contained verdict (overlap.hpp:51-67) from the o = 0 query.
+// CONTAINED: also derive the containment verdict from the o = 0 query (needs the whole interval: a
+// full search by one lane while 31 wait) -- used only where the rank-anchored search does not apply;
+// otherwise contained_kernel does that with one thread per fragment.
+template <bool CONTAINED>
 __global__ void __launch_bounds__(256)
 overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __restrict__ qoff,
                      u32* __restrict__ q_first, u32* __restrict__ q_count, u8* __restrict__ contained) {
@@ -388,19 +392,18 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
         const u64 qbase = qoff[i - f0];
         const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);  // offsets 0 .. len - min_ov
         // a fragment shorter than min_ov still runs its o = 0 query for the containment flag
-        const u32 steps = nq ? nq : 1u;
+        const u32 steps = CONTAINED ? (nq ? nq : 1u) : nq;
+        const u32 self = iv.start_inv[i];
         for (u32 o = lane; o < steps; o += 32) {
             const u32 m = len - o;
             u32 lo = 0, hi = 0, sf, sl;
-            // o = 0 needs the size of the whole interval for the containment verdict
-            if (o == 0 || !iv.tv.packed || !iv.sdir) locate_residual(iv, start + o, m, &lo, &hi, &sf, &sl);
+            if constexpr (CONTAINED) locate_residual(iv, start + o, m, &lo, &hi, &sf, &sl);
             else locate_residual_starts(iv, start + o, m, &sf, &sl);
             // f_i's own start suffix lies in the interval at o = 0, and at o > 0 whenever f_i
             // overlaps itself; the diagonal is zero by convention (overlap.hpp:26,41)
-            const u32 self = iv.start_inv[i];
             const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
             const u32 cnt = sl - sf - self_in;
-            if (o == 0) {
+            if (CONTAINED && o == 0) {
                 u32 exact = 0, min_id = 0xFFFFFFFFu;
                 for (u32 t = sf; t < sl; ++t) {
                     const u32 id = iv.start_frag[t];
@@ -416,6 +419,29 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
                 q_count[qbase + o] = cnt;
             }
         }
+    }
+}
+
+// absorb_contained (overlap.hpp:51-67) for fragments [f0, f1): fragment i is dropped iff it occurs
+// inside a longer fragment or equals one with a lower id -- i.e. iff the SA interval of the whole
+// fragment holds more suffixes than the fragments equal to it, or one of those has a lower id.
+// One thread per fragment (the interval needs both binary searches).
+__global__ void __launch_bounds__(256)
+contained_kernel(IndexView iv, u64 f0, u64 f1, u8* __restrict__ contained) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = f0 + static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < f1; i += stride) {
+        const u32 m = iv.lens[i];
+        u32 lo, hi, sf, sl;
+        locate_residual(iv, iv.starts[i], m, &lo, &hi, &sf, &sl);
+        u32 exact = 0, min_id = 0xFFFFFFFFu;
+        for (u32 t = sf; t < sl; ++t) {
+            const u32 id = iv.start_frag[t];
+            if (iv.lens[id] == m) {
+                ++exact;
+                min_id = min(min_id, id);
+            }
+        }
+        contained[i] = (hi - lo > exact) || (min_id < static_cast<u32>(i));
     }
 }
 
@@ -555,6 +581,28 @@ int scan_table(reseq_cuda_ctx* ctx, const u32* hist, u32* out, size_t count) {
     u64* d_total = ctx->alloc<u64>(1);
     if (!d_total) return fail(RESEQ_OUT_OF_MEMORY, "directory scan workspace");
     return exclusive_scan_device(ctx, hist, out, count, d_total);
+}
+
+// The two kernels behind the overlap counts: with a packed text and a directory every query is
+// anchored at its own rank and the containment flags come from contained_kernel; otherwise (generic
+// alphabets) the full interval search does both.
+int launch_overlap_count(reseq_cuda_ctx* ctx, const IndexView& iv, u32 min_overlap, u64 f0, u64 f1, const u64* d_qoff,
+                         u32* q_first, u32* q_count, u8* d_contained, unsigned grid) {
+    cudaStream_t s = ctx->stream;
+    if (iv.tv.packed && iv.sdir) {
+        RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
+        overlap_count_kernel<false><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_LAUNCH_BEGIN(ctx, "contained_kernel");
+        contained_kernel<<<grid_1d(ctx, f1 - f0, 256), 256, 0, s>>>(iv, f0, f1, d_contained);
+        RSQ_LAUNCH_END(ctx);
+    } else {
+        RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
+        overlap_count_kernel<true><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
+        RSQ_LAUNCH_END(ctx);
+    }
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
 }
 
 }  // namespace
@@ -953,10 +1001,7 @@ int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, 
     u64 raw = 0;
     if (kr > 0) {
         const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
-        RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
-        overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
-        RSQ_LAUNCH_END(ctx);
-        RSQ_CUDA(cudaGetLastError());
+        RSQ_TRY(launch_overlap_count(ctx, iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained, grid));
         RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total, sizeof(u64), cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaStreamSynchronize(s));
@@ -984,10 +1029,7 @@ int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, 
             RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (kr + 1), cudaMemcpyHostToDevice, s));
             RSQ_CUDA(cudaMemsetAsync(q_count + Q, 0, sizeof(u32), s));
             const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
-            RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
-            overlap_count_kernel<<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
-            RSQ_LAUNCH_END(ctx);
-            RSQ_CUDA(cudaGetLastError());
+            RSQ_TRY(launch_overlap_count(ctx, iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained, grid));
             RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
         }
         u64* keys_a = ctx->alloc<u64>(raw);
