@@ -48,7 +48,8 @@ enum reseq_status {
     RESEQ_SCAN_OVERFLOW = 3,    /* reseq::scan_overflow_error */
     RESEQ_CUDA_ERROR = 4,       /* reseq::error carrying the CUDA message */
     RESEQ_OUT_OF_MEMORY = 5,
-    RESEQ_NO_DEVICE = 6
+    RESEQ_NO_DEVICE = 6,
+    RESEQ_BUFFER_TOO_SMALL = 7  /* caller-provided output arrays too short; the needed size is reported */
 };
 
 /* Largest text the device path accepts.  The reference caps at 2^31-1
@@ -247,6 +248,14 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
 int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag_begin,
                                     size_t frag_end, reseq_overlaps* out);
 void reseq_cuda_overlaps_free(reseq_overlaps* o);
+/* The same into arrays the caller owns (i, j, w: `capacity` entries each; contained: k bytes) --
+ * page-locked arrays receive the result at PCIe speed with no intermediate copy.  `out` is filled as
+ * above with its pointers set to the caller's arrays (do not pass it to reseq_cuda_overlaps_free).
+ * If more than `capacity` triples exist nothing is copied, out->count holds the number needed and
+ * the call returns RESEQ_BUFFER_TOO_SMALL. */
+int reseq_cuda_index_overlaps_into(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag_begin, size_t frag_end,
+                                   uint32_t* i, uint32_t* j, uint32_t* w, size_t capacity, uint8_t* contained,
+                                   reseq_overlaps* out);
 
 /* ---- L3 host merge (stays on the host by design) -------------------------------- */
 

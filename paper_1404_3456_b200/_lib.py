@@ -12,7 +12,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libreseq_cuda.so"
 
-OK, INVALID_ARGUMENT, TEXT_TOO_LARGE, SCAN_OVERFLOW, CUDA_ERROR, OUT_OF_MEMORY, NO_DEVICE = range(7)
+OK, INVALID_ARGUMENT, TEXT_TOO_LARGE, SCAN_OVERFLOW, CUDA_ERROR, OUT_OF_MEMORY, NO_DEVICE, BUFFER_TOO_SMALL = range(8)
 MAX_TEXT = 0xFFFFFFFE
 
 
@@ -114,6 +114,8 @@ SIGNATURES = {
     "reseq_cuda_index_overlaps": (C.c_int, [_vp, C.c_uint32, C.POINTER(Overlaps)]),
     "reseq_cuda_index_overlaps_range": (C.c_int, [_vp, C.c_uint32, C.c_size_t, C.c_size_t, C.POINTER(Overlaps)]),
     "reseq_cuda_overlaps_free": (None, [C.POINTER(Overlaps)]),
+    "reseq_cuda_index_overlaps_into": (C.c_int, [_vp, C.c_uint32, C.c_size_t, C.c_size_t, _vp, _vp, _vp, C.c_size_t, _vp,
+                                                 C.POINTER(Overlaps)]),
     "reseq_greedy_superstring": (C.c_int, [_vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(Overlaps), C.c_uint32,
                                            _vp, C.POINTER(C.c_size_t), _vp, C.POINTER(C.c_size_t)]),
     "reseq_synth_random_dna": (None, [C.c_size_t, C.c_uint64, _vp]),

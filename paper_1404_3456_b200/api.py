@@ -32,6 +32,18 @@ from ._lib import (NoDeviceError, ReseqError, SaStats, ScanOverflowError,  # noq
                    TextTooLargeError)
 
 
+def _host_array(count: int, dtype) -> np.ndarray:
+    """A numpy array over page-locked memory when a CUDA device is there (PCIe-speed D2H), plain otherwise."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            t = torch.empty(int(count) * np.dtype(dtype).itemsize, dtype=torch.uint8).pin_memory()
+            return t.numpy().view(dtype)
+    except Exception:
+        pass
+    return np.empty(int(count), dtype)
+
+
 def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -393,23 +405,39 @@ class FragmentIndex:
         """prefix_related(residual{frag, off}) (fragment_index.hpp:78-80)."""
         return self.prefix_related_batch([frag], [off])[0]
 
-    def overlaps(self, min_overlap: int = 1, frag_begin: int = 0, frag_end: Optional[int] = None) -> OverlapList:
+    def overlaps(self, min_overlap: int = 1, frag_begin: int = 0, frag_end: Optional[int] = None,
+                 reuse_buffers: bool = False) -> OverlapList:
         """Sparse overlap graph; [frag_begin, frag_end) restricts the querying fragments (the
-        unit of sharding across GPUs)."""
-        ov = _lib.Overlaps()
+        unit of sharding across GPUs).  The device writes the triples straight into the arrays of
+        the returned OverlapList (reseq_cuda_index_overlaps_into).  With `reuse_buffers` those
+        arrays are page-locked buffers kept by this index (PCIe-speed transfer, no allocation per
+        call) and stay valid only until the next such call."""
+        k = self.set.starts.size
         if frag_end is None:
-            frag_end = self.set.starts.size
-        _lib.check(self._lib.reseq_cuda_index_overlaps_range(self._h, int(min_overlap), int(frag_begin),
-                                                             int(frag_end), C.byref(ov)))
-        try:
-            m, k = int(ov.count), self.set.starts.size
-            take = lambda p, cnt, dt: (np.ctypeslib.as_array(p, shape=(cnt,)).astype(dt, copy=True)
-                                       if cnt else np.zeros(0, dt))
-            return OverlapList(take(ov.i, m, np.uint32), take(ov.j, m, np.uint32), take(ov.w, m, np.uint32),
-                               take(ov.contained, k, np.uint8), int(ov.queries), float(ov.device_ms),
-                               max(1, int(min_overlap)))
-        finally:
-            self._lib.reseq_cuda_overlaps_free(C.byref(ov))
+            frag_end = k
+        cap = getattr(self, "_ov_cap", 0) or max(1024, 32 * (int(frag_end) - int(frag_begin)))
+        while True:
+            if reuse_buffers:
+                bufs = getattr(self, "_ov_bufs", None)
+                if bufs is None or bufs[0].size < cap or bufs[3].size < k:
+                    bufs = tuple(_host_array(cap, np.uint32) for _ in range(3)) + (_host_array(max(1, k), np.uint8),)
+                    self._ov_bufs = bufs
+                i, j, w, contained = bufs
+            else:
+                i, j, w = (np.empty(cap, np.uint32) for _ in range(3))
+                contained = np.empty(max(1, k), np.uint8)
+            ov = _lib.Overlaps()
+            st = self._lib.reseq_cuda_index_overlaps_into(self._h, int(min_overlap), int(frag_begin), int(frag_end),
+                                                          _ptr(i), _ptr(j), _ptr(w), i.size, _ptr(contained), C.byref(ov))
+            if st == _lib.BUFFER_TOO_SMALL:
+                cap = int(ov.count) + int(ov.count) // 8 + 1024
+                continue
+            _lib.check(st)
+            break
+        m = int(ov.count)
+        self._ov_cap = m + m // 8 + 1024          # the next call on this index starts with room to spare
+        return OverlapList(i[:m], j[:m], w[:m], contained[:k], int(ov.queries), float(ov.device_ms),
+                           max(1, int(min_overlap)))
 
 
 # ---- L3 host merge ---------------------------------------------------------------------------

@@ -950,8 +950,18 @@ int reseq_cuda_index_overlaps(reseq_cuda_index* ix, uint32_t min_overlap, reseq_
     return reseq_cuda_index_overlaps_range(ix, min_overlap, 0, ix ? ix->k : 0, out);
 }
 
-int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag_begin,
-                                    size_t frag_end, reseq_overlaps* out) {
+}  // extern "C"
+
+namespace {
+struct OverlapDest {   // caller-owned output arrays of reseq_cuda_index_overlaps_into
+    u32 *i, *j, *w;
+    size_t capacity;
+    u8* contained;
+};
+}  // namespace
+
+static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag_begin, size_t frag_end,
+                         reseq_overlaps* out, const OverlapDest* dest) {
     if (!ix || !out) return fail(RESEQ_INVALID_ARGUMENT, "null argument");
     std::memset(out, 0, sizeof(*out));
     if (frag_begin > frag_end || frag_end > ix->k) return fail(RESEQ_INVALID_ARGUMENT, "fragment range out of bounds");
@@ -972,7 +982,12 @@ int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, 
         qoff[i + 1] = qoff[i] + (lens[f0 + i] >= min_overlap ? lens[f0 + i] - min_overlap + 1 : 0);
     const u64 Q = qoff[kr];
     out->queries = Q;
-    out->contained = static_cast<uint8_t*>(std::calloc(k, 1));
+    if (dest) {
+        out->contained = dest->contained;
+        std::memset(out->contained, 0, k);
+    } else {
+        out->contained = static_cast<uint8_t*>(std::calloc(k, 1));
+    }
     if (!out->contained) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
     if (Q > 0xFFFFFFF0ull) return fail(RESEQ_INVALID_ARGUMENT, "more than 2^32 overlap queries in one call");
 
@@ -1079,9 +1094,22 @@ int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, 
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total2, sizeof(u64), cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaStreamSynchronize(s));
         uniq = *reinterpret_cast<volatile u64*>(ctx->pinned);
-        out->i = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
-        out->j = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
-        out->w = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
+        if (dest) {
+            if (uniq > dest->capacity) {
+                cudaEventDestroy(ev0);
+                cudaEventDestroy(ev1);
+                out->count = uniq;
+                return fail(RESEQ_BUFFER_TOO_SMALL, "overlap arrays hold " + std::to_string(dest->capacity) +
+                                                        " triples, " + std::to_string(uniq) + " found");
+            }
+            out->i = dest->i;
+            out->j = dest->j;
+            out->w = dest->w;
+        } else {
+            out->i = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
+            out->j = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
+            out->w = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
+        }
         if (!out->i || !out->j || !out->w) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
         RSQ_CUDA(cudaMemcpyAsync(out->i, oi, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaMemcpyAsync(out->j, oj, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
@@ -1097,6 +1125,21 @@ int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, 
     out->device_ms = ms;
     out->count = uniq;
     return RESEQ_OK;
+}
+
+extern "C" {
+
+int reseq_cuda_index_overlaps_range(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag_begin,
+                                    size_t frag_end, reseq_overlaps* out) {
+    return overlaps_impl(ix, min_overlap, frag_begin, frag_end, out, nullptr);
+}
+
+int reseq_cuda_index_overlaps_into(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag_begin, size_t frag_end,
+                                   uint32_t* i, uint32_t* j, uint32_t* w, size_t capacity, uint8_t* contained,
+                                   reseq_overlaps* out) {
+    if (!contained || (capacity && (!i || !j || !w))) return fail(RESEQ_INVALID_ARGUMENT, "null output array");
+    const OverlapDest dest{i, j, w, capacity, contained};
+    return overlaps_impl(ix, min_overlap, frag_begin, frag_end, out, &dest);
 }
 
 void reseq_cuda_overlaps_free(reseq_overlaps* o) {
