@@ -531,6 +531,113 @@ prefix_related_kernel(IndexView iv, const u32* __restrict__ lengths, u32 n_lengt
     }
 }
 
+// Overlap pass 2, fast form: the records of one fragment (~26 at 30x coverage) are produced, sorted by
+// j and deduplicated by ONE warp in shared memory and leave already in their final (i, j) order --
+// fragments are processed in id order, so no global sort (six 12-byte radix passes over all the
+// records), no flag/scan/compact for uniqueness.  A fragment with more than kOvCap raw records
+// raises `overflow`; the caller then takes the general route below for the whole call.
+constexpr int kOvCap = 256;
+
+__device__ __forceinline__ void warp_bitonic_sort(u64* a, int n, unsigned lane) {   // n: power of two
+    for (int k2 = 2; k2 <= n; k2 <<= 1) {
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            for (int t = lane; t < (n >> 1); t += 32) {
+                const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));   // bit j clear
+                const int l = i | j;
+                const bool up = (i & k2) == 0;
+                const u64 x = a[i], y = a[l];
+                if ((x > y) == up) {
+                    a[i] = y;
+                    a[l] = x;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+overlap_fill_sorted_kernel(IndexView iv, u64 f0, u64 f1, const u64* __restrict__ qoff,
+                           const u32* __restrict__ q_first, const u32* __restrict__ q_count,
+                           const u32* __restrict__ q_out, u32* __restrict__ ti, u32* __restrict__ tj,
+                           u32* __restrict__ tw, u32* __restrict__ ucount, u32* __restrict__ overflow) {
+    __shared__ u64 s_all[8 * kOvCap];
+    u64* a = s_all + (threadIdx.x >> 5) * kOvCap;
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (u64 i = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < f1; i += warps) {
+        const u32 len = iv.lens[i];
+        const u64 qbase = qoff[i - f0];
+        const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);
+        const u32 base = q_out[qbase];
+        const u32 raw = q_out[qbase + nq] - base;   // q_out has an entry behind the last query
+        if (raw > static_cast<u32>(kOvCap)) {
+            if (lane == 0) {
+                atomicOr(overflow, 1u);
+                ucount[i - f0] = 0;
+            }
+            continue;
+        }
+        if (raw == 0) {
+            if (lane == 0) ucount[i - f0] = 0;
+            continue;
+        }
+        int n2 = 2;
+        while (n2 < static_cast<int>(raw)) n2 <<= 1;
+        for (int t = raw + lane; t < n2; t += 32) a[t] = ~0ull;
+        for (u32 o = lane; o < nq; o += 32) {
+            const u32 cnt = q_count[qbase + o];
+            if (!cnt) continue;
+            u32 out = q_out[qbase + o] - base;
+            const u32 sf = q_first[qbase + o] & 0x7FFFFFFFu;
+            const u32 span = cnt + (q_first[qbase + o] >> 31);
+            for (u32 t = 0; t < span; ++t) {
+                const u32 j = iv.start_frag[sf + t];
+                if (j == static_cast<u32>(i)) continue;
+                a[out++] = (static_cast<u64>(j) << 32) | (~(len - o));   // ties on j: the larger weight first
+            }
+        }
+        __syncwarp();
+        warp_bitonic_sort(a, n2, lane);
+        u32 run = 0;
+        for (u32 t0 = 0; t0 < raw; t0 += 32) {
+            const u32 t = t0 + lane;
+            const bool valid = t < raw;
+            const u64 key = valid ? a[t] : 0;
+            const bool head = valid && (t == 0 || static_cast<u32>(key >> 32) != static_cast<u32>(a[t - 1] >> 32));
+            const unsigned mask = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                const u32 d = base + run + __popc(mask & lanemask_lt());
+                ti[d] = static_cast<u32>(i);
+                tj[d] = static_cast<u32>(key >> 32);
+                tw[d] = ~static_cast<u32>(key);
+            }
+            run += __popc(mask);
+        }
+        if (lane == 0) ucount[i - f0] = run;
+        __syncwarp();
+    }
+}
+
+// Closes the gaps dropped duplicates left: fragment f's `ucount[f]` records move from their raw
+// offset to the scanned unique offset.
+__global__ void __launch_bounds__(256)
+overlap_close_gaps_kernel(u64 kr, const u64* __restrict__ qoff, const u32* __restrict__ q_out,
+                          const u32* __restrict__ ucount, const u32* __restrict__ uoff,
+                          const u32* __restrict__ ti, const u32* __restrict__ tj, const u32* __restrict__ tw,
+                          u32* __restrict__ oi, u32* __restrict__ oj, u32* __restrict__ ow) {
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (u64 f = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; f < kr; f += warps) {
+        const u32 src = q_out[qoff[f]], dst = uoff[f], c = ucount[f];
+        for (u32 t = lane; t < c; t += 32) {
+            oi[dst + t] = ti[src + t];
+            oj[dst + t] = tj[src + t];
+            ow[dst + t] = tw[src + t];
+        }
+    }
+}
+
 __global__ void unique_flag_kernel(const u64* __restrict__ keys, u64 m, u32* __restrict__ flag) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 t = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; t < m; t += stride)
@@ -1030,7 +1137,8 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
         // The query arrays stay where they are; the record buffers follow them in the arena.
         const size_t used_before = ctx->arena_used;
         const size_t more = 2 * pad(sizeof(u64) * raw) + 4 * pad(sizeof(u32) * raw) + 3 * pad(sizeof(u32) * raw) +
-                            sort_workspace_bytes(raw) + scan_workspace_bytes(raw) + 8192;
+                            2 * pad(sizeof(u32) * (kr + 1)) + sort_workspace_bytes(raw) +
+                            scan_workspace_bytes(raw) + scan_workspace_bytes(kr + 1) + 8192;
         if (ctx->arena_cap < used_before + more) {
             // grow: the arena is re-allocated, so redo pass 1 state in the new block
             RSQ_TRY(ctx->reserve(used_before + more));
@@ -1057,8 +1165,44 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
         u32* oj = ctx->alloc<u32>(raw);
         u32* ow = ctx->alloc<u32>(raw);
         u64* d_total2 = ctx->alloc<u64>(1);
-        if (!keys_a || !keys_b || !w_a || !w_b || !flag || !dst || !oi || !oj || !ow || !d_total2)
+        u32* ucount = ctx->alloc<u32>(kr + 1);
+        u32* uoff = ctx->alloc<u32>(kr + 1);
+        if (!keys_a || !keys_b || !w_a || !w_b || !flag || !dst || !oi || !oj || !ow || !d_total2 || !ucount || !uoff)
             return fail(RESEQ_OUT_OF_MEMORY, "overlap record workspace");
+        // -- fast form: every fragment's records sorted and deduplicated by one warp in shared memory --
+        bool done = false;
+        u32 *fin_i = oi, *fin_j = oj, *fin_w = ow;
+        {
+            u32* overflow = reinterpret_cast<u32*>(d_total2) + 1;   // upper half of the total word: free until the scan
+            RSQ_CUDA(cudaMemsetAsync(d_total2, 0, sizeof(u64), s));
+            const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
+            RSQ_LAUNCH_BEGIN(ctx, "overlap_fill_sorted_kernel");
+            overlap_fill_sorted_kernel<<<grid, 256, 0, s>>>(iv, f0, f1, d_qoff, q_first, q_count, q_out, w_a, w_b, flag,
+                                                            ucount, overflow);
+            RSQ_LAUNCH_END(ctx);
+            RSQ_CUDA(cudaGetLastError());
+            RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, overflow, sizeof(u32), cudaMemcpyDeviceToHost, s));
+            RSQ_CUDA(cudaMemsetAsync(ucount + kr, 0, sizeof(u32), s));
+            RSQ_TRY(exclusive_scan_device(ctx, ucount, uoff, kr + 1, d_total2));
+            RSQ_CUDA(cudaMemcpyAsync(ctx->pinned + 1, d_total2, sizeof(u64), cudaMemcpyDeviceToHost, s));
+            RSQ_CUDA(cudaStreamSynchronize(s));
+            if (*reinterpret_cast<volatile u32*>(ctx->pinned) == 0) {
+                done = true;
+                uniq = *reinterpret_cast<volatile u64*>(ctx->pinned + 1);
+                if (uniq == raw) {   // nothing was dropped: the raw offsets are the final ones
+                    fin_i = w_a;
+                    fin_j = w_b;
+                    fin_w = flag;
+                } else {
+                    RSQ_LAUNCH_BEGIN(ctx, "overlap_close_gaps_kernel");
+                    overlap_close_gaps_kernel<<<grid, 256, 0, s>>>(kr, d_qoff, q_out, ucount, uoff, w_a, w_b, flag, oi, oj, ow);
+                    RSQ_LAUNCH_END(ctx);
+                    RSQ_CUDA(cudaGetLastError());
+                }
+                RSQ_CUDA(cudaEventRecord(ev1, s));
+            }
+        }
+        if (!done) {   // a fragment with more raw records than a warp's window: global sort + unique
         {
             const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
             RSQ_LAUNCH_BEGIN(ctx, "overlap_fill_kernel");
@@ -1094,6 +1238,7 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total2, sizeof(u64), cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaStreamSynchronize(s));
         uniq = *reinterpret_cast<volatile u64*>(ctx->pinned);
+        }
         if (dest) {
             if (uniq > dest->capacity) {
                 cudaEventDestroy(ev0);
@@ -1111,9 +1256,9 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
             out->w = static_cast<uint32_t*>(std::malloc(sizeof(u32) * (uniq + 1)));
         }
         if (!out->i || !out->j || !out->w) return fail(RESEQ_OUT_OF_MEMORY, "host allocation failed");
-        RSQ_CUDA(cudaMemcpyAsync(out->i, oi, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
-        RSQ_CUDA(cudaMemcpyAsync(out->j, oj, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
-        RSQ_CUDA(cudaMemcpyAsync(out->w, ow, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaMemcpyAsync(out->i, fin_i, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaMemcpyAsync(out->j, fin_j, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
+        RSQ_CUDA(cudaMemcpyAsync(out->w, fin_w, sizeof(u32) * uniq, cudaMemcpyDeviceToHost, s));
     } else {
         RSQ_CUDA(cudaEventRecord(ev1, s));
     }

@@ -1772,12 +1772,17 @@ int reseq_cuda_inverse_device(reseq_cuda_ctx* ctx, const uint32_t* d_sa, size_t 
     using namespace rsq;
     if (!ctx) return fail(RESEQ_INVALID_ARGUMENT, "null context");
     if (n == 0) return RESEQ_OK;
+    if (!d_sa || !d_rank) return fail(RESEQ_INVALID_ARGUMENT, "null device buffer");
     RSQ_CUDA(cudaSetDevice(ctx->device));
-    RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
-    inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, ctx->stream>>>(d_sa, n, d_rank);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_CUDA(cudaGetLastError());
-    return RESEQ_OK;
+    // the partitioned inverse of the single-GPU build (two lean passes + window scatter)
+    auto pad = reseq_cuda_ctx::padded;
+    RSQ_TRY(ctx->reserve(2 * pad(sizeof(u64) * n) + pad(sizeof(u32) * inverse_scratch_words(n)) + 4096));
+    ctx->begin();
+    u64* rec_a = ctx->alloc<u64>(n);
+    u64* rec_b = ctx->alloc<u64>(n);
+    u32* scratch = ctx->alloc<u32>(inverse_scratch_words(n));
+    if (!rec_a || !rec_b || !scratch) return fail(RESEQ_OUT_OF_MEMORY, "inverse workspace");
+    return inverse_device(ctx, d_sa, n, d_rank, rec_a, rec_b, scratch);
 }
 
 }  // extern "C"

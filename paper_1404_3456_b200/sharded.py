@@ -297,14 +297,17 @@ def bench_main(args, workload: str, rank: int, world: int, local_rank: int) -> N
     for _ in range(max(1, args.warmup)):
         sa, rk = build_sa_sharded(d_text, comm, GpuBackend(ex, dev), stats)
     launches0 = ex.launch_count
+    # device time between barriers (CUDA events on the launching stream), maximum over the ranks
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     dist.barrier()
-    t0 = time.perf_counter()
+    ev0.record()
     for _ in range(args.steps):
         sa, rk = build_sa_sharded(d_text, comm, GpuBackend(ex, dev), stats)
+    ev1.record()
     torch.cuda.synchronize()
     dist.barrier()
-    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dt = torch.tensor([ev0.elapsed_time(ev1) * 1e-3], dtype=torch.float64, device=dev)
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     ms = float(dt.item()) / args.steps * 1e3
     idx = torch.arange(n, device=dev, dtype=torch.int64)

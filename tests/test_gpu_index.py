@@ -134,6 +134,12 @@ def test_overlap_lists_on_read_sets(rq, ex, oracle):
     _check_overlaps(rq, ex, oracle, shotgun(rng, 8_000, 3_000, 30, 150), "dna", 16)
     _check_overlaps(rq, ex, oracle, shotgun(rng, 3_000, 2_000, 60, 60), "dna", 5)     # duplicates, deep coverage
     _check_overlaps(rq, ex, oracle, [b"ACGT" * 10] * 5 + [b"CGTA" * 10, b"A" * 30, b"A" * 31], "dna", 3)
+    # more raw records per fragment than one warp sorts in shared memory (periodic duplicates: every
+    # offset matches every copy): the global sort + unique route
+    _check_overlaps(rq, ex, oracle, [b"ACGT" * 10] * 120 + [b"CGTA" * 10] * 40, "dna", 4)
+    rng2 = np.random.default_rng(56)
+    g = bytes(rng2.choice([65, 67, 71, 84], 300).astype(np.uint8))
+    _check_overlaps(rq, ex, oracle, [g[s:s + 50] for s in rng2.integers(0, 250, 2000)], "dna", 10)   # 400x coverage
 
 
 def test_greedy_reconstruction_matches_the_oracle(rq, ex, oracle):
