@@ -267,17 +267,24 @@ __device__ __forceinline__ void locate_residual(const IndexView& iv, u64 ppos, u
 // from lower_bound(lo) on for as long as the fragment they name begins with X -- so the upper
 // bound is never computed; the work is one comparison per overlap found plus one.
 // Same (s_first, s_last) as locate_residual; ~3 DRAM gathers per query instead of ~12.
-__device__ __forceinline__ void locate_residual_starts(const IndexView& iv, u64 ppos, u32 m, u32* s_first,
-                                                       u32* s_last) {
-    // the bracket of the start suffixes does not depend on the rank: both chains of loads (rank from
-    // HBM; text word -> L2-resident directory) are issued before either result is needed
-    u32 f0 = 0, f1 = iv.k;
-    const u32 r = iv.rank[ppos];
+// Part 1: the query's own rank and the bracket of start suffixes that share its first sD bases.
+// An empty bracket (4 queries in 5 on a read set) means no overlap: nothing else is loaded.
+__device__ __forceinline__ void residual_bracket(const IndexView& iv, u64 ppos, u32 m, u32* r, u32* f0, u32* f1) {
+    // the bracket does not depend on the rank: both chains of loads (rank from HBM; text word ->
+    // L2-resident directory) are issued before either result is needed
+    *f0 = 0;
+    *f1 = iv.k;
+    *r = iv.rank[ppos];
     if (iv.sdir && m >= static_cast<u32>(iv.sD)) {
         const u32 x = static_cast<u32>(base_window(iv.tv.packed, ppos) >> (64 - 2 * iv.sD));
-        f0 = iv.sdir[x];
-        f1 = iv.sdir[x + 1];
+        *f0 = iv.sdir[x];
+        *f1 = iv.sdir[x + 1];
     }
+}
+
+// Part 2: [s_first, s_last) inside the bracket.
+__device__ __forceinline__ void residual_starts_in_bracket(const IndexView& iv, u64 ppos, u32 m, u32 r, u32 f0, u32 f1,
+                                                           u32* s_first, u32* s_last) {
     // idx <= r: the suffix there is never greater than the pattern; it is smaller -- no match -- exactly
     // when it differs from it or ends first.  It usually ends first (the neighbour below a read suffix
     // is the same locus seen from a read that ends earlier), which the sentinel bitmap alone tells:
@@ -326,6 +333,13 @@ __device__ __forceinline__ void locate_residual_starts(const IndexView& iv, u64 
     while (sl < f1 && begins_with_pattern(iv.start_frag[sl])) ++sl;
     *s_first = sf;
     *s_last = sl;
+}
+
+__device__ __forceinline__ void locate_residual_starts(const IndexView& iv, u64 ppos, u32 m, u32* s_first,
+                                                       u32* s_last) {
+    u32 r, f0, f1;
+    residual_bracket(iv, ppos, m, &r, &f0, &f1);
+    residual_starts_in_bracket(iv, ppos, m, r, f0, f1, s_first, s_last);
 }
 
 __global__ void __launch_bounds__(256)
@@ -386,24 +400,93 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
                      u32* __restrict__ q_first, u32* __restrict__ q_count, u8* __restrict__ contained) {
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     const unsigned lane = lane_id();
+    if constexpr (!CONTAINED) {
+        // Rank-anchored form.  Four queries in five end at an empty bracket after two loads; the fifth
+        // walks start_rank and compares fragments -- a chain of ~10 dependent L2 round trips that, run
+        // in place, every lane of the warp would wait for in every iteration.  Queries with a
+        // non-empty bracket are therefore queued per warp and worked off 32 at a time, all lanes busy.
+        __shared__ u32 s_qr[8][64], s_qf0[8][64], s_qf1o[8][64];   // rank, bracket start, (bracket size << 8 | offset)
+        u32* qr = s_qr[threadIdx.x >> 5];
+        u32* qf0 = s_qf0[threadIdx.x >> 5];
+        u32* qf1o = s_qf1o[threadIdx.x >> 5];
+        for (u64 i = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < f1; i += warps) {
+            const u32 len = iv.lens[i];
+            const u64 start = iv.starts[i];
+            const u64 qbase = qoff[i - f0];
+            const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);
+            const u32 self = iv.start_inv[i];
+            u32 queued = 0;
+            auto work_off = [&](u32 count) {   // the first `count` (<= 32) queue entries
+                if (lane < count) {
+                    const u32 o = qf1o[lane] & 0xffu, b0 = qf0[lane], b1 = b0 + (qf1o[lane] >> 8);
+                    u32 sf, sl;
+                    residual_starts_in_bracket(iv, start + o, len - o, qr[lane], b0, b1, &sf, &sl);
+                    const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
+                    q_first[qbase + o] = sf | (self_in << 31);
+                    q_count[qbase + o] = sl - sf - self_in;
+                }
+                __syncwarp();
+                const bool moves = lane + count < queued;   // the rest (< 32 entries) moves to the front
+                u32 a = 0, b = 0, c = 0;
+                if (moves) { a = qr[lane + count]; b = qf0[lane + count]; c = qf1o[lane + count]; }
+                __syncwarp();
+                if (moves) { qr[lane] = a; qf0[lane] = b; qf1o[lane] = c; }
+                __syncwarp();
+                queued -= count;
+            };
+            for (u32 o0 = 0; o0 < nq; o0 += 32) {
+                const u32 o = o0 + lane;
+                bool has = false;
+                u32 r = 0, b0 = 0, b1 = 0;
+                if (o < nq) {
+                    residual_bracket(iv, start + o, len - o, &r, &b0, &b1);
+                    has = b0 < b1;
+                    if (!has) {   // the diagonal cannot be inside an empty bracket either
+                        q_first[qbase + o] = b0;
+                        q_count[qbase + o] = 0;
+                    }
+                }
+                // offsets above 255 or brackets above 2^24 entries do not fit the packed queue word: in place
+                if (has && (o > 255u || b1 - b0 >= (1u << 24))) {
+                    u32 sf, sl;
+                    residual_starts_in_bracket(iv, start + o, len - o, r, b0, b1, &sf, &sl);
+                    const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
+                    q_first[qbase + o] = sf | (self_in << 31);
+                    q_count[qbase + o] = sl - sf - self_in;
+                    has = false;
+                }
+                const unsigned mask = __ballot_sync(0xffffffffu, has);
+                if (has) {
+                    const u32 slot = queued + __popc(mask & lanemask_lt());
+                    qr[slot] = r;
+                    qf0[slot] = b0;
+                    qf1o[slot] = ((b1 - b0) << 8) | o;
+                }
+                queued += __popc(mask);
+                __syncwarp();
+                if (queued >= 32) work_off(32);
+            }
+            if (queued) work_off(queued);
+        }
+        return;
+    }
     for (u64 i = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < f1; i += warps) {
         const u32 len = iv.lens[i];
         const u64 start = iv.starts[i];
         const u64 qbase = qoff[i - f0];
         const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);  // offsets 0 .. len - min_ov
         // a fragment shorter than min_ov still runs its o = 0 query for the containment flag
-        const u32 steps = CONTAINED ? (nq ? nq : 1u) : nq;
+        const u32 steps = nq ? nq : 1u;
         const u32 self = iv.start_inv[i];
         for (u32 o = lane; o < steps; o += 32) {
             const u32 m = len - o;
             u32 lo = 0, hi = 0, sf, sl;
-            if constexpr (CONTAINED) locate_residual(iv, start + o, m, &lo, &hi, &sf, &sl);
-            else locate_residual_starts(iv, start + o, m, &sf, &sl);
+            locate_residual(iv, start + o, m, &lo, &hi, &sf, &sl);
             // f_i's own start suffix lies in the interval at o = 0, and at o > 0 whenever f_i
             // overlaps itself; the diagonal is zero by convention (overlap.hpp:26,41)
             const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
             const u32 cnt = sl - sf - self_in;
-            if (CONTAINED && o == 0) {
+            if (o == 0) {
                 u32 exact = 0, min_id = 0xFFFFFFFFu;
                 for (u32 t = sf; t < sl; ++t) {
                     const u32 id = iv.start_frag[t];
