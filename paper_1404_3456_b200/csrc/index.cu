@@ -397,9 +397,16 @@ locate_patterns_kernel(IndexView iv, const u8* __restrict__ pats, const u64* __r
 template <bool CONTAINED>
 __global__ void __launch_bounds__(256)
 overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __restrict__ qoff,
-                     u32* __restrict__ q_first, u32* __restrict__ q_count, u8* __restrict__ contained) {
+                     u32* __restrict__ q_first, u32* __restrict__ q_count, u8* __restrict__ contained,
+                     u32* __restrict__ rawcount) {
+    // rawcount[i - f0] = records fragment i will produce: the record offsets are then one scan over
+    // the fragments (plus a warp scan inside each) instead of one over all the queries
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     const unsigned lane = lane_id();
+    auto publish = [&](u64 i, u32 mine) {
+        for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
+        if (lane == 0) rawcount[i - f0] = mine;
+    };
     if constexpr (!CONTAINED) {
         // Rank-anchored form.  Four queries in five end at an empty bracket after two loads; the fifth
         // walks start_rank and compares fragments -- a chain of ~10 dependent L2 round trips that, run
@@ -415,7 +422,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
             const u64 qbase = qoff[i - f0];
             const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);
             const u32 self = iv.start_inv[i];
-            u32 queued = 0;
+            u32 queued = 0, mine = 0;
             auto work_off = [&](u32 count) {   // the first `count` (<= 32) queue entries
                 if (lane < count) {
                     const u32 o = qf1o[lane] & 0xffu, b0 = qf0[lane], b1 = b0 + (qf1o[lane] >> 8);
@@ -424,6 +431,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
                     const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
                     q_first[qbase + o] = sf | (self_in << 31);
                     q_count[qbase + o] = sl - sf - self_in;
+                    mine += sl - sf - self_in;
                 }
                 __syncwarp();
                 const bool moves = lane + count < queued;   // the rest (< 32 entries) moves to the front
@@ -453,6 +461,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
                     const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
                     q_first[qbase + o] = sf | (self_in << 31);
                     q_count[qbase + o] = sl - sf - self_in;
+                    mine += sl - sf - self_in;
                     has = false;
                 }
                 const unsigned mask = __ballot_sync(0xffffffffu, has);
@@ -467,6 +476,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
                 if (queued >= 32) work_off(32);
             }
             if (queued) work_off(queued);
+            publish(i, mine);
         }
         return;
     }
@@ -478,6 +488,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
         // a fragment shorter than min_ov still runs its o = 0 query for the containment flag
         const u32 steps = nq ? nq : 1u;
         const u32 self = iv.start_inv[i];
+        u32 mine = 0;
         for (u32 o = lane; o < steps; o += 32) {
             const u32 m = len - o;
             u32 lo = 0, hi = 0, sf, sl;
@@ -500,8 +511,10 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
             if (o < nq) {
                 q_first[qbase + o] = sf | (self_in << 31);  // k < 2^31: a fragment takes >= 2 bytes
                 q_count[qbase + o] = cnt;
+                mine += cnt;
             }
         }
+        publish(i, mine);
     }
 }
 
@@ -642,7 +655,7 @@ __device__ __forceinline__ void warp_bitonic_sort(u64* a, int n, unsigned lane) 
 __global__ void __launch_bounds__(256)
 overlap_fill_sorted_kernel(IndexView iv, u64 f0, u64 f1, const u64* __restrict__ qoff,
                            const u32* __restrict__ q_first, const u32* __restrict__ q_count,
-                           const u32* __restrict__ q_out, u32* __restrict__ ti, u32* __restrict__ tj,
+                           const u32* __restrict__ rbase, u32* __restrict__ ti, u32* __restrict__ tj,
                            u32* __restrict__ tw, u32* __restrict__ ucount, u32* __restrict__ overflow) {
     __shared__ u64 s_all[8 * kOvCap];
     u64* a = s_all + (threadIdx.x >> 5) * kOvCap;
@@ -652,8 +665,8 @@ overlap_fill_sorted_kernel(IndexView iv, u64 f0, u64 f1, const u64* __restrict__
         const u32 len = iv.lens[i];
         const u64 qbase = qoff[i - f0];
         const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);
-        const u32 base = q_out[qbase];
-        const u32 raw = q_out[qbase + nq] - base;   // q_out has an entry behind the last query
+        const u32 base = rbase[i - f0];
+        const u32 raw = rbase[i - f0 + 1] - base;   // rbase has an entry behind the last fragment
         if (raw > static_cast<u32>(kOvCap)) {
             if (lane == 0) {
                 atomicOr(overflow, 1u);
@@ -668,17 +681,27 @@ overlap_fill_sorted_kernel(IndexView iv, u64 f0, u64 f1, const u64* __restrict__
         int n2 = 2;
         while (n2 < static_cast<int>(raw)) n2 <<= 1;
         for (int t = raw + lane; t < n2; t += 32) a[t] = ~0ull;
-        for (u32 o = lane; o < nq; o += 32) {
-            const u32 cnt = q_count[qbase + o];
-            if (!cnt) continue;
-            u32 out = q_out[qbase + o] - base;
-            const u32 sf = q_first[qbase + o] & 0x7FFFFFFFu;
-            const u32 span = cnt + (q_first[qbase + o] >> 31);
-            for (u32 t = 0; t < span; ++t) {
-                const u32 j = iv.start_frag[sf + t];
-                if (j == static_cast<u32>(i)) continue;
-                a[out++] = (static_cast<u64>(j) << 32) | (~(len - o));   // ties on j: the larger weight first
+        u32 before = 0;   // records of the offsets below this sweep
+        for (u32 o0 = 0; o0 < nq; o0 += 32) {
+            const u32 o = o0 + lane;
+            const u32 cnt = o < nq ? q_count[qbase + o] : 0u;
+            u32 inc = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const u32 t = __shfl_up_sync(0xffffffffu, inc, d);
+                if (static_cast<int>(lane) >= d) inc += t;
             }
+            if (cnt) {
+                u32 out = before + inc - cnt;
+                const u32 sf = q_first[qbase + o] & 0x7FFFFFFFu;
+                const u32 span = cnt + (q_first[qbase + o] >> 31);
+                for (u32 t = 0; t < span; ++t) {
+                    const u32 j = iv.start_frag[sf + t];
+                    if (j == static_cast<u32>(i)) continue;
+                    a[out++] = (static_cast<u64>(j) << 32) | (~(len - o));   // ties on j: the larger weight first
+                }
+            }
+            before += __shfl_sync(0xffffffffu, inc, 31);
         }
         __syncwarp();
         warp_bitonic_sort(a, n2, lane);
@@ -705,14 +728,14 @@ overlap_fill_sorted_kernel(IndexView iv, u64 f0, u64 f1, const u64* __restrict__
 // Closes the gaps dropped duplicates left: fragment f's `ucount[f]` records move from their raw
 // offset to the scanned unique offset.
 __global__ void __launch_bounds__(256)
-overlap_close_gaps_kernel(u64 kr, const u64* __restrict__ qoff, const u32* __restrict__ q_out,
+overlap_close_gaps_kernel(u64 kr, const u32* __restrict__ rbase,
                           const u32* __restrict__ ucount, const u32* __restrict__ uoff,
                           const u32* __restrict__ ti, const u32* __restrict__ tj, const u32* __restrict__ tw,
                           u32* __restrict__ oi, u32* __restrict__ oj, u32* __restrict__ ow) {
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     const unsigned lane = lane_id();
     for (u64 f = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; f < kr; f += warps) {
-        const u32 src = q_out[qoff[f]], dst = uoff[f], c = ucount[f];
+        const u32 src = rbase[f], dst = uoff[f], c = ucount[f];
         for (u32 t = lane; t < c; t += 32) {
             oi[dst + t] = ti[src + t];
             oj[dst + t] = tj[src + t];
@@ -777,18 +800,20 @@ int scan_table(reseq_cuda_ctx* ctx, const u32* hist, u32* out, size_t count) {
 // anchored at its own rank and the containment flags come from contained_kernel; otherwise (generic
 // alphabets) the full interval search does both.
 int launch_overlap_count(reseq_cuda_ctx* ctx, const IndexView& iv, u32 min_overlap, u64 f0, u64 f1, const u64* d_qoff,
-                         u32* q_first, u32* q_count, u8* d_contained, unsigned grid) {
+                         u32* q_first, u32* q_count, u8* d_contained, u32* rawcount, unsigned grid) {
     cudaStream_t s = ctx->stream;
     if (iv.tv.packed && iv.sdir) {
         RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
-        overlap_count_kernel<false><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
+        overlap_count_kernel<false><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained,
+                                                         rawcount);
         RSQ_LAUNCH_END(ctx);
         RSQ_LAUNCH_BEGIN(ctx, "contained_kernel");
         contained_kernel<<<grid_1d(ctx, f1 - f0, 256), 256, 0, s>>>(iv, f0, f1, d_contained);
         RSQ_LAUNCH_END(ctx);
     } else {
         RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
-        overlap_count_kernel<true><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained);
+        overlap_count_kernel<true><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained,
+                                                        rawcount);
         RSQ_LAUNCH_END(ctx);
     }
     RSQ_CUDA(cudaGetLastError());
@@ -1186,7 +1211,7 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
     RSQ_CUDA(cudaEventCreate(&ev1));
 
     size_t need = pad(sizeof(u64) * (kr + 1)) + 3 * pad(sizeof(u32) * (Q + 1)) + pad(k) +
-                  scan_workspace_bytes(Q + 1) + 8192;
+                  2 * pad(sizeof(u32) * (kr + 1)) + scan_workspace_bytes(Q + 1) + scan_workspace_bytes(kr + 1) + 8192;
     RSQ_TRY(ctx->reserve(need));
     ctx->begin();
     u64* d_qoff = ctx->alloc<u64>(kr + 1);
@@ -1195,7 +1220,9 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
     u32* q_out = ctx->alloc<u32>(Q + 1);
     u8* d_contained = ctx->alloc<u8>(k);
     u64* d_total = ctx->alloc<u64>(1);
-    if (!d_qoff || !q_first || !q_count || !q_out || !d_contained || !d_total)
+    u32* rawcount = ctx->alloc<u32>(kr + 1);
+    u32* rbase = ctx->alloc<u32>(kr + 1);
+    if (!d_qoff || !q_first || !q_count || !q_out || !d_contained || !d_total || !rawcount || !rbase)
         return fail(RESEQ_OUT_OF_MEMORY, "overlap workspace");
     RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (kr + 1), cudaMemcpyHostToDevice, s));
     RSQ_CUDA(cudaMemsetAsync(d_contained, 0, k, s));
@@ -1206,8 +1233,9 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
     u64 raw = 0;
     if (kr > 0) {
         const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
-        RSQ_TRY(launch_overlap_count(ctx, iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained, grid));
-        RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
+        RSQ_CUDA(cudaMemsetAsync(rawcount + kr, 0, sizeof(u32), s));
+        RSQ_TRY(launch_overlap_count(ctx, iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained, rawcount, grid));
+        RSQ_TRY(exclusive_scan_device(ctx, rawcount, rbase, kr + 1, d_total));
         RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total, sizeof(u64), cudaMemcpyDeviceToHost, s));
         RSQ_CUDA(cudaStreamSynchronize(s));
         raw = *reinterpret_cast<volatile u64*>(ctx->pinned);
@@ -1221,7 +1249,7 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
         const size_t used_before = ctx->arena_used;
         const size_t more = 2 * pad(sizeof(u64) * raw) + 4 * pad(sizeof(u32) * raw) + 3 * pad(sizeof(u32) * raw) +
                             2 * pad(sizeof(u32) * (kr + 1)) + sort_workspace_bytes(raw) +
-                            scan_workspace_bytes(raw) + scan_workspace_bytes(kr + 1) + 8192;
+                            scan_workspace_bytes(raw) + scan_workspace_bytes(kr + 1) + scan_workspace_bytes(Q + 1) + 8192;
         if (ctx->arena_cap < used_before + more) {
             // grow: the arena is re-allocated, so redo pass 1 state in the new block
             RSQ_TRY(ctx->reserve(used_before + more));
@@ -1232,11 +1260,15 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
             q_out = ctx->alloc<u32>(Q + 1);
             d_contained = ctx->alloc<u8>(k);
             d_total = ctx->alloc<u64>(1);
+            rawcount = ctx->alloc<u32>(kr + 1);
+            rbase = ctx->alloc<u32>(kr + 1);
             RSQ_CUDA(cudaMemcpyAsync(d_qoff, qoff.data(), sizeof(u64) * (kr + 1), cudaMemcpyHostToDevice, s));
             RSQ_CUDA(cudaMemsetAsync(q_count + Q, 0, sizeof(u32), s));
+            RSQ_CUDA(cudaMemsetAsync(rawcount + kr, 0, sizeof(u32), s));
             const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
-            RSQ_TRY(launch_overlap_count(ctx, iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained, grid));
-            RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));
+            RSQ_TRY(launch_overlap_count(ctx, iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained, rawcount,
+                                         grid));
+            RSQ_TRY(exclusive_scan_device(ctx, rawcount, rbase, kr + 1, d_total));
         }
         u64* keys_a = ctx->alloc<u64>(raw);
         u64* keys_b = ctx->alloc<u64>(raw);
@@ -1260,7 +1292,7 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
             RSQ_CUDA(cudaMemsetAsync(d_total2, 0, sizeof(u64), s));
             const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
             RSQ_LAUNCH_BEGIN(ctx, "overlap_fill_sorted_kernel");
-            overlap_fill_sorted_kernel<<<grid, 256, 0, s>>>(iv, f0, f1, d_qoff, q_first, q_count, q_out, w_a, w_b, flag,
+            overlap_fill_sorted_kernel<<<grid, 256, 0, s>>>(iv, f0, f1, d_qoff, q_first, q_count, rbase, w_a, w_b, flag,
                                                             ucount, overflow);
             RSQ_LAUNCH_END(ctx);
             RSQ_CUDA(cudaGetLastError());
@@ -1278,7 +1310,7 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
                     fin_w = flag;
                 } else {
                     RSQ_LAUNCH_BEGIN(ctx, "overlap_close_gaps_kernel");
-                    overlap_close_gaps_kernel<<<grid, 256, 0, s>>>(kr, d_qoff, q_out, ucount, uoff, w_a, w_b, flag, oi, oj, ow);
+                    overlap_close_gaps_kernel<<<grid, 256, 0, s>>>(kr, rbase, ucount, uoff, w_a, w_b, flag, oi, oj, ow);
                     RSQ_LAUNCH_END(ctx);
                     RSQ_CUDA(cudaGetLastError());
                 }
@@ -1287,6 +1319,7 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
         }
         if (!done) {   // a fragment with more raw records than a warp's window: global sort + unique
         {
+            RSQ_TRY(exclusive_scan_device(ctx, q_count, q_out, Q + 1, d_total));   // per-query record offsets
             const unsigned grid = grid_1d(ctx, kr * 32, 256, 32);
             RSQ_LAUNCH_BEGIN(ctx, "overlap_fill_kernel");
             overlap_fill_kernel<<<grid, 256, 0, s>>>(iv, f0, f1, d_qoff, q_first, q_count, q_out, keys_a, w_a);
