@@ -74,10 +74,14 @@ int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx);
 uint64_t reseq_cuda_ctx_launch_count(const reseq_cuda_ctx* ctx);
 /* Bytes currently held by the context's workspace arena. */
 size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
-/* Tuning / test knobs.  "sa_text_rounds": maximum number of shared-memory group-refinement
- * rounds (keys fetched from the packed text) the DNA suffix-array path runs before handing
- * over to prefix doubling; 0 forces pure prefix doubling.  Unknown names are
- * RESEQ_INVALID_ARGUMENT.  Results never depend on these options. */
+/* Tuning / test knobs; results never depend on them.  Unknown names are RESEQ_INVALID_ARGUMENT.
+ *   "sa_uniform"      0 switches off the path for uniform read sets (k reads of one length:
+ *                     transposed 16-base records, one verified overlap per read); default 1
+ *   "sa_text_rounds"  maximum number of shared-memory group-refinement rounds (keys fetched from
+ *                     the packed text) the DNA paths run before handing over to prefix doubling;
+ *                     0 forces pure prefix doubling; default 16
+ *   "sa_shortcut"     0 switches off the sentinel-distance shortcut of the general DNA path
+ *   "sort_cfg"        onesweep tile shape, 0 (default tuning) .. 9 */
 int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long value);
 /* Per-kernel device timing, measured with CUDA events recorded on the launching stream
  * around every launch while enabled.  reseq_cuda_ctx_profile(ctx, 1) clears and starts,
