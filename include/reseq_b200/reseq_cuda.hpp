@@ -120,6 +120,25 @@ inline key_array split_by_bit(const key_array& arr, unsigned bit, const device_e
     return out;
 }
 
+/// detail::split_destinations, radix_sort.hpp:35-52 (Alg. 1).
+struct split_plan {
+    std::vector<std::uint32_t> destinations;
+    std::uint32_t total_false = 0;
+};
+inline split_plan split_destinations(std::span<const std::uint32_t> keys, unsigned bit, const device_executor& dev) {
+    split_plan plan;
+    plan.destinations.resize(keys.size());
+    detail::check(reseq_cuda_split_destinations(dev.handle(), keys.data(), keys.size(), bit, plan.destinations.data(),
+                                                &plan.total_false));
+    return plan;
+}
+/// detail::phase_is_sorted, radix_sort.hpp:54-66.
+inline bool phase_is_sorted(std::span<const std::uint32_t> keys, const device_executor& dev) {
+    int sorted = 1;
+    detail::check(reseq_cuda_is_sorted(dev.handle(), keys.data(), keys.size(), &sorted));
+    return sorted != 0;
+}
+
 inline key_array radix_sort(const key_array& arr, const device_executor& dev) {
     key_array out;
     out.keys.resize(arr.keys.size());

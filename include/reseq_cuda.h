@@ -113,6 +113,16 @@ int reseq_cuda_exclusive_scan_device(reseq_cuda_ctx* ctx, const uint32_t* d_valu
 int reseq_cuda_split_by_bit(reseq_cuda_ctx* ctx, const uint32_t* keys, const uint32_t* payload,
                             size_t n, unsigned bit, uint32_t* keys_out, uint32_t* payload_out);
 
+/* Replaces detail::split_destinations, radix_sort.hpp:35-52 (the paper's Alg. 1 dataflow,
+ * PAPER.md:310-348): b = bit value, e = 1 - b, f = exclusive scan of e, tof = e[n-1] + f[n-1],
+ * destinations[i] = b[i] ? i - f[i] + tof : f[i]; *total_false = tof (0 for n = 0).
+ * bit > 31 is RESEQ_INVALID_ARGUMENT. */
+int reseq_cuda_split_destinations(reseq_cuda_ctx* ctx, const uint32_t* keys, size_t n, unsigned bit,
+                                  uint32_t* destinations, uint32_t* total_false);
+/* Replaces detail::phase_is_sorted, radix_sort.hpp:54-66 (radix_sort's early exit, :151):
+ * *sorted = 1 iff keys[i-1] <= keys[i] for all i. */
+int reseq_cuda_is_sorted(reseq_cuda_ctx* ctx, const uint32_t* keys, size_t n, int* sorted);
+
 /* Replaces radix_sort, radix_sort.hpp:143-161: stable ascending sort on keys, payload
  * carried.  Implemented as an 8-bit-digit LSD "onesweep" radix sort; passes whose
  * digit is constant over the whole array are skipped (the analogue of the

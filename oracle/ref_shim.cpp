@@ -130,6 +130,23 @@ int ref_split_by_bit(const uint32_t* k, const uint32_t* p, size_t n, unsigned bi
     });
 }
 
+int ref_split_destinations(const uint32_t* k, size_t n, unsigned bit, unsigned workers, size_t chunk,
+                           uint32_t* d, uint32_t* total_false) {
+    return guarded([&] {
+        reseq::executor ex(reseq::executor_config{workers, chunk});
+        auto plan = reseq::detail::split_destinations(std::span<const uint32_t>(k, n), bit, ex);
+        if (n) std::memcpy(d, plan.destinations.data(), n * 4);
+        *total_false = plan.total_false;
+    });
+}
+
+int ref_is_sorted(const uint32_t* k, size_t n, unsigned workers, size_t chunk, int* sorted) {
+    return guarded([&] {
+        reseq::executor ex(reseq::executor_config{workers, chunk});
+        *sorted = reseq::detail::phase_is_sorted(std::span<const uint32_t>(k, n), ex) ? 1 : 0;
+    });
+}
+
 int ref_radix_sort(const uint32_t* k, const uint32_t* p, size_t n, unsigned workers,
                    size_t chunk, uint32_t* ko, uint32_t* po) {
     return guarded([&] {

@@ -90,6 +90,8 @@ SIGNATURES = {
     "reseq_cuda_exclusive_scan": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
     "reseq_cuda_exclusive_scan_device": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _u64p]),
     "reseq_cuda_split_by_bit": (C.c_int, [_vp, _vp, _vp, C.c_size_t, C.c_uint, _vp, _vp]),
+    "reseq_cuda_split_destinations": (C.c_int, [_vp, _vp, C.c_size_t, C.c_uint, _vp, _u32p]),
+    "reseq_cuda_is_sorted": (C.c_int, [_vp, _vp, C.c_size_t, C.POINTER(C.c_int)]),
     "reseq_cuda_radix_sort": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "reseq_cuda_radix_sort_device": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "reseq_cuda_chunked_radix_sort": (C.c_int, [_vp, _vp, _vp, C.c_size_t, C.c_uint, _vp, _vp]),

@@ -162,6 +162,25 @@ def split_by_bit(keys, payload=None, bit: int = 0, exec: Optional[Executor] = No
     return ko, (po if po is not None else np.empty(0, np.uint32))
 
 
+def split_destinations(keys, bit: int = 0, exec: Optional[Executor] = None):
+    """detail::split_destinations, radix_sort.hpp:35-52 (Alg. 1): (destinations, total_false)."""
+    ex = exec or default_executor()
+    k = _u32(keys, "keys")
+    d = np.empty_like(k)
+    tof = C.c_uint32(0)
+    _lib.check(ex._lib.reseq_cuda_split_destinations(ex.handle, _ptr(k), k.size, int(bit), _ptr(d), C.byref(tof)))
+    return d, int(tof.value)
+
+
+def is_sorted(keys, exec: Optional[Executor] = None) -> bool:
+    """detail::phase_is_sorted, radix_sort.hpp:54-66."""
+    ex = exec or default_executor()
+    k = _u32(keys, "keys")
+    flag = C.c_int(1)
+    _lib.check(ex._lib.reseq_cuda_is_sorted(ex.handle, _ptr(k), k.size, C.byref(flag)))
+    return bool(flag.value)
+
+
 def radix_sort(keys, payload=None, exec: Optional[Executor] = None):
     """radix_sort.hpp:143-161: stable ascending sort on keys, payload carried."""
     ex = exec or default_executor()

@@ -308,6 +308,102 @@ int reseq_cuda_exclusive_scan(reseq_cuda_ctx* ctx, const uint32_t* values, size_
 
 // ---- split / sorts ----------------------------------------------------------------
 
+}  // extern "C"
+
+namespace {
+
+// Alg. 1 (radix_sort.hpp:35-52) as three phases: e = 1 - bit, f = exclusive scan
+// of e (single-pass decoupled look-back scan instead of the listing's Hillis-Steele loop), then
+// d = bit ? i - f + tof : f.
+__global__ void split_flags_kernel(const u32* __restrict__ keys, size_t n, unsigned bit, u32* __restrict__ e) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        e[i] = ((keys[i] >> bit) & 1u) ^ 1u;
+}
+
+__global__ void split_dest_kernel(const u32* __restrict__ keys, const u32* __restrict__ f, size_t n, unsigned bit,
+                                  const u64* __restrict__ tof, u32* __restrict__ d) {
+    const u32 total_false = static_cast<u32>(*tof);
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        d[i] = ((keys[i] >> bit) & 1u) ? static_cast<u32>(i) - f[i] + total_false : f[i];
+}
+
+__global__ void is_sorted_kernel(const u32* __restrict__ keys, size_t n, u32* __restrict__ unsorted) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    bool bad = false;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x + 1; i < n; i += stride)
+        bad |= keys[i - 1] > keys[i];
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(unsorted, 1u);
+}
+
+unsigned stream_grid(const reseq_cuda_ctx* ctx, size_t n) {
+    const size_t want = (n + 1023) / 1024, cap = static_cast<size_t>(ctx->sm_count) * 16;
+    return static_cast<unsigned>(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+}  // namespace
+
+extern "C" {
+
+int reseq_cuda_split_destinations(reseq_cuda_ctx* ctx, const uint32_t* keys, size_t n, unsigned bit,
+                                  uint32_t* destinations, uint32_t* total_false) {
+    if (bit > 31) return fail(RESEQ_INVALID_ARGUMENT, "bit must be in 0..31");
+    RSQ_TRY(check_ctx(ctx));
+    if (total_false) *total_false = 0;
+    if (n == 0) return RESEQ_OK;
+    if (!keys || !destinations) return fail(RESEQ_INVALID_ARGUMENT, "null buffer");
+    if (n > RESEQ_CUDA_MAX_TEXT) return fail(RESEQ_INVALID_ARGUMENT, "more than 2^32-2 keys");
+    const size_t arr = reseq_cuda_ctx::padded(sizeof(u32) * n);
+    RSQ_TRY(ctx->reserve(4 * arr + scan_workspace_bytes(n) + 4096));
+    ctx->begin();
+    u32* d_keys = ctx->alloc<u32>(n);
+    u32* d_e = ctx->alloc<u32>(n);
+    u32* d_f = ctx->alloc<u32>(n);
+    u32* d_d = ctx->alloc<u32>(n);
+    u64* d_tof = ctx->alloc<u64>(1);
+    if (!d_keys || !d_e || !d_f || !d_d || !d_tof) return fail(RESEQ_OUT_OF_MEMORY, "split workspace");
+    cudaStream_t s = ctx->stream;
+    RSQ_CUDA(cudaMemcpyAsync(d_keys, keys, sizeof(u32) * n, cudaMemcpyHostToDevice, s));
+    RSQ_LAUNCH_BEGIN(ctx, "split_flags_kernel");
+    split_flags_kernel<<<stream_grid(ctx, n), 256, 0, s>>>(d_keys, n, bit, d_e);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_TRY(exclusive_scan_device(ctx, d_e, d_f, n, d_tof));   // the total of e is tof = e[n-1] + f[n-1]
+    RSQ_LAUNCH_BEGIN(ctx, "split_dest_kernel");
+    split_dest_kernel<<<stream_grid(ctx, n), 256, 0, s>>>(d_keys, d_f, n, bit, d_tof, d_d);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(destinations, d_d, sizeof(u32) * n, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_tof, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    if (total_false) *total_false = static_cast<uint32_t>(*reinterpret_cast<volatile u64*>(ctx->pinned));
+    return RESEQ_OK;
+}
+
+int reseq_cuda_is_sorted(reseq_cuda_ctx* ctx, const uint32_t* keys, size_t n, int* sorted) {
+    RSQ_TRY(check_ctx(ctx));
+    if (!sorted) return fail(RESEQ_INVALID_ARGUMENT, "null out pointer");
+    *sorted = 1;
+    if (n < 2) return RESEQ_OK;
+    if (!keys) return fail(RESEQ_INVALID_ARGUMENT, "null buffer");
+    RSQ_TRY(ctx->reserve(reseq_cuda_ctx::padded(sizeof(u32) * n) + 4096));
+    ctx->begin();
+    u32* d_keys = ctx->alloc<u32>(n);
+    u32* d_flag = ctx->alloc<u32>(1);
+    if (!d_keys || !d_flag) return fail(RESEQ_OUT_OF_MEMORY, "is_sorted workspace");
+    cudaStream_t s = ctx->stream;
+    RSQ_CUDA(cudaMemcpyAsync(d_keys, keys, sizeof(u32) * n, cudaMemcpyHostToDevice, s));
+    RSQ_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(u32), s));
+    RSQ_LAUNCH_BEGIN(ctx, "is_sorted_kernel");
+    is_sorted_kernel<<<stream_grid(ctx, n), 256, 0, s>>>(d_keys, n, d_flag);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_flag, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    *sorted = *reinterpret_cast<volatile u32*>(ctx->pinned) == 0 ? 1 : 0;
+    return RESEQ_OK;
+}
+
 int reseq_cuda_split_by_bit(reseq_cuda_ctx* ctx, const uint32_t* keys, const uint32_t* payload,
                             size_t n, unsigned bit, uint32_t* keys_out, uint32_t* payload_out) {
     if (bit > 31) return fail(RESEQ_INVALID_ARGUMENT, "bit must be in 0..31");

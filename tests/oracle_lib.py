@@ -84,6 +84,17 @@ class Oracle:
         self.lib.orc_split_by_bit(vp(k), vp(p), C.c_size_t(k.size), C.c_uint(bit), vp(ko), vp(po))
         return ko, po
 
+    def split_destinations(self, k, bit):
+        k = u32(k)
+        d = np.empty_like(k)
+        tof = C.c_uint32(0)
+        self.lib.orc_split_destinations(vp(k), C.c_size_t(k.size), C.c_uint(bit), vp(d), C.byref(tof))
+        return d, int(tof.value)
+
+    def is_sorted(self, k) -> bool:
+        k = u32(k)
+        return bool(self.lib.orc_is_sorted(vp(k), C.c_size_t(k.size)))
+
     def stable_sort(self, k, p):
         k = u32(k)
         p = None if p is None else u32(p)
@@ -220,6 +231,21 @@ class Reference:
 
     def split_by_bit(self, k, p, bit, workers=1, chunk=1 << 15):
         return self._sort(self.lib.ref_split_by_bit, k, p, C.c_uint(bit), C.c_uint(workers), C.c_size_t(chunk))
+
+    def split_destinations(self, k, bit, workers=1, chunk=1 << 15):
+        k = u32(k)
+        d = np.empty_like(k)
+        tof = C.c_uint32(0)
+        st = self.lib.ref_split_destinations(vp(k), C.c_size_t(k.size), C.c_uint(bit), C.c_uint(workers),
+                                             C.c_size_t(chunk), vp(d), C.byref(tof))
+        assert st == 0
+        return d, int(tof.value)
+
+    def is_sorted(self, k, workers=1, chunk=1 << 15) -> bool:
+        k = u32(k)
+        flag = C.c_int(0)
+        assert self.lib.ref_is_sorted(vp(k), C.c_size_t(k.size), C.c_uint(workers), C.c_size_t(chunk), C.byref(flag)) == 0
+        return bool(flag.value)
 
     def radix_sort(self, k, p, workers=1, chunk=1 << 15):
         return self._sort(self.lib.ref_radix_sort, k, p, C.c_uint(workers), C.c_size_t(chunk))

@@ -160,3 +160,28 @@ def test_chunked_digit_width_is_validated(rq, ex):
         rq.chunked_radix_sort([1, 2], None, ex, 0)
     with pytest.raises(ValueError):
         rq.chunked_radix_sort([1, 2], None, ex, 9)
+
+
+def test_split_destinations_and_is_sorted(rq, ex, oracle):
+    """radix_sort.hpp:35-66 (Alg. 1's dataflow and the early-exit test) through the C ABI."""
+    rng = np.random.default_rng(30)
+    for n in [1, 2, 31, 32, 33, 2047, 2048, 2049, 100_003, 1_000_000]:
+        keys = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+        for bit in (0, 7, 31, int(rng.integers(0, 32))):
+            d, tof = rq.split_destinations(keys, bit, ex)
+            wd, wtof = oracle.split_destinations(keys, bit)
+            assert tof == wtof and np.array_equal(d, wd), (n, bit)
+            ko, _ = rq.split_by_bit(keys, None, bit, ex)
+            out = np.empty_like(keys)
+            out[d] = keys
+            assert np.array_equal(out, ko)
+        assert rq.is_sorted(keys, ex) == oracle.is_sorted(keys)
+        s = np.sort(keys)
+        assert rq.is_sorted(s, ex)
+        if n > 2:
+            s[n // 2], s[n // 2 - 1] = s[n // 2 - 1], s[n // 2] + np.uint32(1) if s[n // 2] < 2**32 - 1 else s[n // 2]
+            assert rq.is_sorted(s, ex) == oracle.is_sorted(s)
+    d, tof = rq.split_destinations(np.zeros(0, np.uint32), 0, ex)
+    assert d.size == 0 and tof == 0 and rq.is_sorted(np.zeros(0, np.uint32), ex)
+    with pytest.raises(ValueError):
+        rq.split_destinations(np.zeros(4, np.uint32), 32, ex)

@@ -189,3 +189,30 @@ def test_against_the_reference_itself(oracle, ref):
     assert ref.exclusive_scan([0xFFFFFFFF, 1])[0] == 3
     assert ref.checksum_u32(k) == oracle.checksum_u32(k)
     assert ref.fnv1a64(b"reseq") == oracle.fnv1a64(b"reseq")
+
+
+def test_split_plan_restatement_against_the_reference(oracle, ref):
+    """test_parallel.cpp:109-123 (seed 29 property) on the restatement, and equality with the
+    reference's own detail::split_destinations / phase_is_sorted where it could be built."""
+    rng = np.random.default_rng(29)
+    for it in range(60):
+        n = int(rng.integers(1, 801))
+        keys = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+        if it % 5 == 0:
+            keys &= np.uint32(0xFF)
+        bit = int(rng.integers(0, 32))
+        d, tof = oracle.split_destinations(keys, bit)
+        assert tof == int((((keys >> np.uint32(bit)) & 1) ^ 1).sum())
+        assert np.array_equal(np.sort(d), np.arange(n, dtype=np.uint32))
+        ko, _ = oracle.split_by_bit(keys, None, bit)
+        out = np.empty_like(keys)
+        out[d] = keys
+        assert np.array_equal(out, ko)                      # the plan IS the split (radix_sort.hpp:126-139)
+        assert oracle.is_sorted(keys) == bool(np.all(keys[:-1] <= keys[1:]))
+        assert oracle.is_sorted(np.sort(keys))
+        if ref is not None:
+            rd, rtof = ref.split_destinations(keys, bit, workers=1 + it % 4, chunk=64)
+            assert rtof == tof and np.array_equal(rd, d)
+            assert ref.is_sorted(keys, workers=2, chunk=100) == oracle.is_sorted(keys)
+    d, tof = oracle.split_destinations(np.zeros(0, np.uint32), 3)
+    assert d.size == 0 and tof == 0
