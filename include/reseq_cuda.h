@@ -210,6 +210,9 @@ size_t reseq_cuda_index_fragments(const reseq_cuda_index* ix);
  * any pointer may be NULL. */
 int reseq_cuda_index_get(const reseq_cuda_index* ix, uint32_t* sa, uint32_t* rank,
                          uint32_t* start_rank_list);
+/* start_fragments[t] = frag_at_start_[sa[start_rank_list[t]]] (fragment_index.hpp:44,98): the id of
+ * the fragment whose start suffix has the t-th smallest rank; k entries. */
+int reseq_cuda_index_start_fragments(const reseq_cuda_index* ix, uint32_t* start_fragments);
 /* Device pointers to the same arrays (valid until destroy). */
 int reseq_cuda_index_device_ptrs(const reseq_cuda_index* ix, const uint32_t** d_sa,
                                  const uint32_t** d_rank, const uint32_t** d_start_rank_list);

@@ -108,6 +108,7 @@ SIGNATURES = {
     "reseq_cuda_index_text_len": (C.c_size_t, [_vp]),
     "reseq_cuda_index_fragments": (C.c_size_t, [_vp]),
     "reseq_cuda_index_get": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "reseq_cuda_index_start_fragments": (C.c_int, [_vp, _vp]),
     "reseq_cuda_index_device_ptrs": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
     "reseq_cuda_index_locate_batch": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "reseq_cuda_index_locate_residuals": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
@@ -135,7 +136,7 @@ def load() -> C.CDLL:
         return _lib
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1404_3456_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` "
             "(there is no CPU fallback for the reseq B200 backend)")
     lib = C.CDLL(str(LIB_PATH))
     for name, (res, args) in SIGNATURES.items():

@@ -424,6 +424,52 @@ class FragmentIndex:
         """prefix_related(residual{frag, off}) (fragment_index.hpp:78-80)."""
         return self.prefix_related_batch([frag], [off])[0]
 
+    def prefix_related_patterns(self, patterns: Iterable):
+        """fragment_index::prefix_related(std::string_view) (fragment_index.hpp:82-109) for arbitrary
+        byte patterns (non-empty, no separator byte).  The interval searches -- one per distinct
+        fragment length below |pattern| plus one for the whole pattern -- run on the device as one
+        batch (at each length the reference's narrowed interval equals locate_prefix_range of that
+        prefix, :75-80); the classification over start_rank_list is the reference's, on the host.
+        Like the reference (:91), a pattern whose interval empties at an intermediate length returns
+        at once: its prefixes_of then stay in (length, rank) order instead of ascending ids."""
+        pats = [bytes(p) if not isinstance(p, str) else p.encode("latin-1") for p in patterns]
+        if any(len(p) == 0 for p in pats):
+            raise ValueError("patterns must be non-empty (fragment_index.hpp:63-64)")
+        lens = self.set.lengths()
+        lengths = np.unique(lens)
+        queries, spans = [], []
+        for p in pats:
+            cuts = [int(c) for c in lengths if c < len(p)]
+            spans.append((len(queries), cuts))
+            queries.extend(p[:c] for c in cuts)
+            queries.append(p)
+        lo, hi = self.locate_batch(queries) if queries else (np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+        if not hasattr(self, "_start_rank"):
+            self._start_rank = self._get(2)
+            sf = np.empty(self.set.starts.size, np.uint32)
+            _lib.check(self._lib.reseq_cuda_index_start_fragments(self._h, _ptr(sf)))
+            self._start_frag = sf
+        out = []
+        for p, (q0, cuts) in zip(pats, spans):
+            prefixes, early = [], False
+            for t, c in enumerate(cuts):
+                l, h = int(lo[q0 + t]), int(hi[q0 + t])
+                if l == h:
+                    early = True
+                    break
+                a, b = np.searchsorted(self._start_rank, [l, h], side="left")
+                ids = self._start_frag[a:b]
+                prefixes.extend(ids[lens[ids] == c].tolist())      # ranks ascending (collect_starts_of_length, :150-158)
+            if early:
+                out.append((np.array(prefixes, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.uint32)))
+                continue
+            l, h = int(lo[q0 + len(cuts)]), int(hi[q0 + len(cuts)])
+            a, b = np.searchsorted(self._start_rank, [l, h], side="left")
+            ids = self._start_frag[a:b]
+            out.append((np.sort(np.array(prefixes, np.uint32)), np.sort(ids[lens[ids] > len(p)]).astype(np.uint32),
+                        np.sort(ids[lens[ids] == len(p)]).astype(np.uint32)))
+        return out
+
     def overlaps(self, min_overlap: int = 1, frag_begin: int = 0, frag_end: Optional[int] = None,
                  reuse_buffers: bool = False) -> OverlapList:
         """Sparse overlap graph; [frag_begin, frag_end) restricts the querying fragments (the

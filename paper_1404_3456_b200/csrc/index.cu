@@ -990,6 +990,15 @@ int reseq_cuda_index_get(const reseq_cuda_index* ix, uint32_t* sa, uint32_t* ran
     return RESEQ_OK;
 }
 
+int reseq_cuda_index_start_fragments(const reseq_cuda_index* ix, uint32_t* start_fragments) {
+    if (!ix || !start_fragments) return fail(RESEQ_INVALID_ARGUMENT, "null argument");
+    RSQ_CUDA(cudaSetDevice(ix->ctx->device));
+    cudaStream_t s = ix->ctx->stream;
+    RSQ_CUDA(cudaMemcpyAsync(start_fragments, ix->d_start_frag, sizeof(u32) * ix->k, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    return RESEQ_OK;
+}
+
 int reseq_cuda_index_device_ptrs(const reseq_cuda_index* ix, const uint32_t** d_sa, const uint32_t** d_rank,
                                  const uint32_t** d_start_rank_list) {
     if (!ix) return fail(RESEQ_INVALID_ARGUMENT, "null index");

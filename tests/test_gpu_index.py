@@ -195,3 +195,45 @@ def test_cpp_shim_drop_in(tmp_path):
                         "-o", str(exe)], check=True)
         r = subprocess.run([str(exe)], capture_output=True, text=True)
         assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_prefix_related_for_arbitrary_patterns(rq, ex, oracle, ref):
+    """fragment_index::prefix_related(std::string_view), fragment_index.hpp:82-109: the golden
+    vectors generated from the real reference, random patterns against the reference itself (when
+    its shim is there) and the by-definition oracle -- including the early return that leaves
+    prefixes_of unsorted (:91)."""
+    import json
+    from pathlib import Path
+    golden = json.loads((Path(__file__).parent / "golden" / "golden.json").read_text())
+    checked = 0
+    for inst in golden["index"]:
+        frags = [bytes(f) for f in inst["fragments"]]
+        fs = rq.make_fragment_set(frags, inst["alphabet"])
+        ix = rq.FragmentIndex(fs, ex)
+        got = ix.prefix_related_patterns([bytes(q["pattern"]) for q in inst["queries"]])
+        for q, (a, e, x) in zip(inst["queries"], got):
+            assert a.tolist() == q["prefixes"] and e.tolist() == q["extensions"] and x.tolist() == q["exact"], q
+            checked += 1
+        ix.close()
+    assert checked > 50
+    rng = np.random.default_rng(57)
+    for it in range(12):
+        frags = random_frags(rng, int(rng.integers(3, 40)), 1, 9, (65, 67, 71, 84), [.5, .3, .1, .1])
+        fs = rq.make_fragment_set(frags, "dna")
+        ix = rq.FragmentIndex(fs, ex)
+        lens = fs.lengths()
+        pats = [bytes(rng.choice([65, 67, 71, 84], int(rng.integers(1, 12)), p=[.5, .3, .1, .1]).astype(np.uint8))
+                for _ in range(60)] + [f + b"A" for f in frags[:5]] + [f[:-1] + b"T" + b"G" for f in frags[:5] if len(f) > 1]
+        got = ix.prefix_related_patterns(pats)
+        rix = ref.index(frags, "dna") if ref is not None else None
+        for p, (a, e, x) in zip(pats, got):
+            oa, oe, ox = oracle.prefix_related(fs.concat, fs.starts, lens, p)
+            if rix is not None:
+                ra, re_, rx = rix.prefix_related(p)
+                assert a.tolist() == ra.tolist() and e.tolist() == re_.tolist() and x.tolist() == rx.tolist(), (frags, p)
+            full = sorted(a.tolist()) == oa.tolist() and e.tolist() == oe.tolist() and x.tolist() == ox.tolist()
+            early = e.size == 0 and x.size == 0 and set(a.tolist()) <= set(oa.tolist())
+            assert full or early, (frags, p)
+        if rix is not None:
+            rix.close()
+        ix.close()
