@@ -2,7 +2,7 @@
 shotgun read sets + suffix-array-driven overlap search), behind the reference's interface.
 
 Importing the package loads the in-tree CUDA library; it fails loudly when the library has
-not been built (`python -m paper_1404_3456_b200.build`).  There is no CPU fallback.
+not been built (`python __graft_entry__.py`).  There is no CPU fallback.
 """
 from . import _lib
 
