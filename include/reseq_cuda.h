@@ -184,6 +184,26 @@ int reseq_cuda_sa_shard_records(reseq_cuda_sa_shard* shard, uint64_t pos_begin, 
  * positions in suffix order. */
 int reseq_cuda_sa_shard_finish(reseq_cuda_sa_shard* shard, uint64_t* d_records, size_t m,
                                uint32_t* d_sa_out, uint64_t* unfinished);
+/* The same for a uniform read set (k reads of one length, see reseq_cuda_build_sa): shard_create
+ * detects it; *period = read length + 1 (0: not uniform -- use shard_records / shard_finish).
+ *   uniform_records    records key32 << 32 | position of the suffixes of reads [read_begin,
+ *                      read_begin + read_count), transposed: d_records[t * read_count + r] is the
+ *                      suffix of read read_begin + r with t symbols before its sentinel.
+ *   (the caller partitions by splitter range, exchanges, and brings the bucket into (t, position)
+ *    order: a stable sort of the received slices on t = period - 1 - position mod period)
+ *   uniform_sort_link  sorts the bucket (4 digit passes; the array is clobbered) and proves, per whole
+ *                      read found in it, its predecessor's suffixes to be prefixes: d_cov[read] = t
+ *                      (one byte per read of the WHOLE set, zeroed by the caller; combine the ranks'
+ *                      tables with an all-reduce MAX before finishing).
+ *   uniform_finish     accepts / refines the bucket under the combined table: d_sa_out = its m suffix
+ *                      positions in suffix order.  Must follow uniform_sort_link on the same shard. */
+int reseq_cuda_sa_shard_uniform_info(const reseq_cuda_sa_shard* shard, uint32_t* period, uint64_t* reads);
+int reseq_cuda_sa_shard_uniform_records(reseq_cuda_sa_shard* shard, uint64_t read_begin, size_t read_count,
+                                        uint64_t* d_records);
+int reseq_cuda_sa_shard_uniform_sort_link(reseq_cuda_sa_shard* shard, uint64_t* d_records, size_t m,
+                                          uint8_t* d_cov);
+int reseq_cuda_sa_shard_uniform_finish(reseq_cuda_sa_shard* shard, const uint8_t* d_cov, uint32_t* d_sa_out,
+                                       uint64_t* unfinished);
 /* d_rank[d_sa[i]] = i (suffix_array.hpp:118-122). */
 int reseq_cuda_inverse_device(reseq_cuda_ctx* ctx, const uint32_t* d_sa, size_t n, uint32_t* d_rank);
 

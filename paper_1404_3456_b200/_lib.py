@@ -101,6 +101,10 @@ SIGNATURES = {
     "reseq_cuda_sa_shard_destroy": (None, [_vp]),
     "reseq_cuda_sa_shard_records": (C.c_int, [_vp, C.c_uint64, C.c_size_t, _vp]),
     "reseq_cuda_sa_shard_finish": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _u64p]),
+    "reseq_cuda_sa_shard_uniform_info": (C.c_int, [_vp, _u32p, _u64p]),
+    "reseq_cuda_sa_shard_uniform_records": (C.c_int, [_vp, C.c_uint64, C.c_size_t, _vp]),
+    "reseq_cuda_sa_shard_uniform_sort_link": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
+    "reseq_cuda_sa_shard_uniform_finish": (C.c_int, [_vp, _vp, _vp, _u64p]),
     "reseq_cuda_inverse_device": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
     "reseq_cuda_checksum_u32_device": (C.c_int, [_vp, _vp, C.c_size_t, _u64p]),
     "reseq_cuda_index_create": (C.c_int, [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(_vp)]),

@@ -952,14 +952,15 @@ __global__ void uniform_check_kernel(const u64* __restrict__ sent, u32 period, u
 }
 
 __global__ void __launch_bounds__(256)
-gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u64* __restrict__ elems,
+gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0, u64 k, u64* __restrict__ elems,
                    u32* __restrict__ g_hist) {
+    // reads [read0, read0 + k) of the set (the whole set: read0 = 0); record t * k + (read - read0)
     __shared__ u64 s_w[kUniReads * kUniMaxPeriod / 32 + 4];
     __shared__ u32 s_hist[4 * kRadix];
     for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
-    const u64 r0 = static_cast<u64>(blockIdx.x) * kUniReads;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kUniReads;   // within the slice
     const u32 nr = static_cast<u32>(k - r0 < kUniReads ? k - r0 : kUniReads);
-    const u64 base0 = r0 * period;
+    const u64 base0 = (read0 + r0) * period;
     const u64 w0 = base0 >> 5;
     const u32 off0 = static_cast<u32>(base0 & 31);
     const u32 nw = static_cast<u32>(((base0 + static_cast<u64>(nr) * period + 31) >> 5) - w0) + 2;   // the packed array is padded
@@ -976,7 +977,7 @@ gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u64* __res
         const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
         u32 key = static_cast<u32>(win >> 32);                          // 16 bases
         if (t < kUniK) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;   // zero padded from the sentinel on
-        const u64 pos = (r0 + rl) * period + (period - 1 - t);
+        const u64 pos = (read0 + r0 + rl) * period + (period - 1 - t);
         elems[static_cast<u64>(t) * k + r0 + rl] = (static_cast<u64>(key) << 32) | pos;
         atomicAdd(&s_hist[key & 0xffu], 1u);
         atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
@@ -1444,40 +1445,41 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     return RESEQ_OK;
 }
 
-// The uniform read-set path: transposed records, four digit passes, one comparison per read, groups
-// accepted as they stand.  *unfinished != 0 (a read set that is not uniform after all, an oversize
-// group, a step limit) sends the caller to the general paths.
-int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
-                            u64* elems_a, u64* elems_b, u8* cov, u32* headbits, u32* uncbits, u32* whole, u32* sa_out,
-                            int max_rounds, u32* counters,
-                            const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
+// The uniform read-set path on m records that are in (t, position) order within equal keys (the
+// whole set: m = n, generated transposed; a multi-GPU rank: its bucket).  First half: four digit
+// passes, the last of which reports where the whole reads landed, and one verified overlap per whole
+// read into the per-read table `cov` (indexed by the read's number in the WHOLE set).
+int uniform_sort_link(reseq_cuda_ctx* ctx, const u64* packed, u32 period, u64* elems_a, u64* elems_b, size_t m,
+                      bool hist_ready, u32* whole, u8* cov, u32* counters, const SortWorkspace& ws, reseq_sa_stats* st,
+                      const u64** sorted_out) {
     cudaStream_t s = ctx->stream;
     const u64 magic = ~0ull / period + 1;   // ceil(2^64 / period): floor(pos / period) = mulhi(pos, magic) for pos < 2^32
-    RSQ_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(u32), s));
-    RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * 4 * kRadix, s));
-    RSQ_CUDA(cudaMemsetAsync(cov, 0, k, s));
-    RSQ_LAUNCH_BEGIN(ctx, "uniform_check_kernel");
-    uniform_check_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, s>>>(sent, period, k, counters + 3);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_LAUNCH_BEGIN(ctx, "gen_uniform_kernel");
-    gen_uniform_kernel<<<static_cast<unsigned>((k + kUniReads - 1) / kUniReads), 256, 0, s>>>(packed, period, k, elems_a,
-                                                                                             ws.hist);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_CUDA(cudaGetLastError());
     const PassTable pt = make_passes(32, 64);
     bool in_b = false;
-    // the last pass also reports where the k whole reads (position = 0 mod period) ended up
     const EmitMultiples emit{period, magic, whole, counters + 4};
-    RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b, &emit));
+    RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, m, pt, ws, hist_ready, 0, &in_b, &emit));
     st->sort_passes += pt.count;
     const u64* sorted = in_b ? elems_b : elems_a;
     RSQ_LAUNCH_BEGIN(ctx, "link_reads_kernel");
-    link_reads_kernel<<<grid_for(ctx, k, 256, 1, 16), 256, 0, s>>>(sorted, whole, counters + 4, packed, period, magic, cov);
+    link_reads_kernel<<<grid_for(ctx, m / period + 1, 256, 1, 16), 256, 0, s>>>(sorted, whole, counters + 4, packed, period,
+                                                                               magic, cov);
     RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    *sorted_out = sorted;
+    return RESEQ_OK;
+}
+
+// Second half, under the complete `cov` table: the records become the suffix array where every
+// group is proven, the others are re-sorted; *unfinished != 0 sends the caller to the general paths.
+int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n_text, u32 period,
+                          const u64* sorted, size_t m, const u8* cov, u32* headbits, u32* uncbits, u32* sa_out,
+                          int max_rounds, u32* counters, reseq_sa_stats* st, u64* unfinished) {
+    cudaStream_t s = ctx->stream;
+    const u64 magic = ~0ull / period + 1;
     RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
-    u8* tileflags = reinterpret_cast<u8*>(uncbits + n / 32 + 2);   // carved behind the bitmap by the caller
-    RSQ_CUDA(cudaMemsetAsync(tileflags, 0, n / kRefTile + 2, s));
-    accept_uniform_kernel<<<grid_for(ctx, n, 256, 4, 8), 256, 0, s>>>(sorted, n, cov, period, magic, sa_out, headbits,
+    u8* tileflags = reinterpret_cast<u8*>(uncbits + m / 32 + 2);   // carved behind the bitmap by the caller
+    RSQ_CUDA(cudaMemsetAsync(tileflags, 0, m / kRefTile + 2, s));
+    accept_uniform_kernel<<<grid_for(ctx, m, 256, 4, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
                                                                        uncbits, tileflags);
     RSQ_LAUNCH_END(ctx);
     static bool configured = false;
@@ -1486,9 +1488,9 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
                                       static_cast<int>(kRefSmem)));
         configured = true;
     }
-    const unsigned tiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
+    const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
-    refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sorted, n, sa_out, max_rounds, true,
+    refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, sorted, m, sa_out, max_rounds, true,
                                                                  counters, cov, period, magic, headbits, uncbits,
                                                                  tileflags);
     RSQ_LAUNCH_END(ctx);
@@ -1498,13 +1500,37 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     const volatile u32* c = reinterpret_cast<volatile u32*>(ctx->pinned);
     *unfinished = static_cast<u64>(c[0]) + (c[1] ? 1u : 0u) + c[3];
     if (std::getenv("RESEQ_DEBUG"))
-        std::fprintf(stderr, "[reseq] uniform refine: n=%zu period=%u tied_left=%u oversize=%u steps=%u misplaced_sentinels=%u\n",
-                     n, period, c[0], c[1], c[2], c[3]);
+        std::fprintf(stderr, "[reseq] uniform refine: records=%zu period=%u tied_left=%u oversize=%u steps=%u misplaced_sentinels=%u\n",
+                     m, period, c[0], c[1], c[2], c[3]);
     if (*unfinished == 0) {
         st->rounds += c[2];
-        st->refined_tile += n;
+        st->refined_tile += m;
     }
     return RESEQ_OK;
+}
+
+// The whole set on one device: transposed records, then both halves.  *unfinished != 0 (a read set
+// that is not uniform after all, an oversize group, a step limit) sends the caller to the general paths.
+int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u32 period, u64 k,
+                            u64* elems_a, u64* elems_b, u8* cov, u32* headbits, u32* uncbits, u32* whole, u32* sa_out,
+                            int max_rounds, u32* counters,
+                            const SortWorkspace& ws, reseq_sa_stats* st, u64* unfinished) {
+    cudaStream_t s = ctx->stream;
+    RSQ_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(u32), s));
+    RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * 4 * kRadix, s));
+    RSQ_CUDA(cudaMemsetAsync(cov, 0, k, s));
+    RSQ_LAUNCH_BEGIN(ctx, "uniform_check_kernel");
+    uniform_check_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, s>>>(sent, period, k, counters + 3);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_LAUNCH_BEGIN(ctx, "gen_uniform_kernel");
+    gen_uniform_kernel<<<static_cast<unsigned>((k + kUniReads - 1) / kUniReads), 256, 0, s>>>(packed, period, 0, k,
+                                                                                             elems_a, ws.hist);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    const u64* sorted = nullptr;
+    RSQ_TRY(uniform_sort_link(ctx, packed, period, elems_a, elems_b, n, true, whole, cov, counters, ws, st, &sorted));
+    return uniform_accept_refine(ctx, packed, sent, n, period, sorted, n, cov, headbits, uncbits, sa_out, max_rounds,
+                                 counters, st, unfinished);
 }
 
 }  // namespace
@@ -1679,6 +1705,15 @@ struct reseq_cuda_sa_shard {
     rsq::u32* flags = nullptr;
     bool dna = false;
     bool use_shortcut = false;
+    // uniform read sets: period = read length + 1 (0: not uniform), number of reads; the bucket
+    // between uniform_sort_link and uniform_finish (arrays in the context's arena)
+    rsq::u32 period = 0;
+    rsq::u64 reads = 0;
+    const rsq::u64* u_sorted = nullptr;
+    rsq::u32* u_headbits = nullptr;
+    rsq::u32* u_uncbits = nullptr;
+    rsq::u32* u_counters = nullptr;
+    size_t u_m = 0;
 };
 
 extern "C" {
@@ -1708,9 +1743,102 @@ int reseq_cuda_sa_shard_create(reseq_cuda_ctx* ctx, const uint8_t* d_text, size_
         return st;
     }
     sh->use_shortcut = ctx->opt_shortcut != 0 && n_sep * 1024 >= n;
+    if (sh->dna && ctx->opt_uniform != 0 && n_sep > 0 && n % n_sep == 0 && n / n_sep >= kUniMinPeriod &&
+        n / n_sep <= kUniMaxPeriod) {   // k sentinels, one period apart?
+        const u32 period = static_cast<u32>(n / n_sep);
+        cudaMemsetAsync(sh->flags + 8, 0, sizeof(u32), ctx->stream);
+        RSQ_LAUNCH_BEGIN(ctx, "uniform_check_kernel");
+        uniform_check_kernel<<<static_cast<unsigned>((n_sep + 255) / 256), 256, 0, ctx->stream>>>(sh->sent, period, n_sep,
+                                                                                             sh->flags + 8);
+        RSQ_LAUNCH_END(ctx);
+        cudaMemcpyAsync(ctx->pinned, sh->flags + 8, sizeof(u32), cudaMemcpyDeviceToHost, ctx->stream);
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+            reseq_cuda_sa_shard_destroy(sh);
+            return fail(RESEQ_CUDA_ERROR, "uniform read-set check failed");
+        }
+        if (*reinterpret_cast<volatile u32*>(ctx->pinned) == 0) {
+            sh->period = period;
+            sh->reads = n_sep;
+        }
+    }
     if (is_dna) *is_dna = sh->dna ? 1 : 0;
     *out = sh;
     return RESEQ_OK;
+}
+
+int reseq_cuda_sa_shard_uniform_info(const reseq_cuda_sa_shard* sh, uint32_t* period, uint64_t* reads) {
+    if (!sh) return rsq::fail(RESEQ_INVALID_ARGUMENT, "null shard");
+    if (period) *period = sh->period;
+    if (reads) *reads = sh->reads;
+    return RESEQ_OK;
+}
+
+int reseq_cuda_sa_shard_uniform_records(reseq_cuda_sa_shard* sh, uint64_t read_begin, size_t read_count,
+                                        uint64_t* d_records) {
+    using namespace rsq;
+    if (!sh || !sh->period) return fail(RESEQ_INVALID_ARGUMENT, "not a uniform read set");
+    if (read_count == 0) return RESEQ_OK;
+    if (read_begin + read_count > sh->reads || !d_records) return fail(RESEQ_INVALID_ARGUMENT, "read slice out of range");
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    RSQ_TRY(ctx->reserve(reseq_cuda_ctx::padded(sizeof(u32) * 4 * kRadix) + 4096));
+    ctx->begin();
+    u32* hist = ctx->alloc<u32>(4 * kRadix);   // the slice's histogram is not used: buckets re-count
+    if (!hist) return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
+    RSQ_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * 4 * kRadix, ctx->stream));
+    RSQ_LAUNCH_BEGIN(ctx, "gen_uniform_kernel");
+    gen_uniform_kernel<<<static_cast<unsigned>((read_count + kUniReads - 1) / kUniReads), 256, 0, ctx->stream>>>(
+        sh->packed, sh->period, read_begin, read_count, d_records, hist);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
+}
+
+int reseq_cuda_sa_shard_uniform_sort_link(reseq_cuda_sa_shard* sh, uint64_t* d_records, size_t m, uint8_t* d_cov) {
+    using namespace rsq;
+    if (!sh || !sh->period || !d_cov) return fail(RESEQ_INVALID_ARGUMENT, "bad shard argument");
+    sh->u_m = m;
+    sh->u_sorted = nullptr;
+    if (m == 0) return RESEQ_OK;
+    if (!d_records) return fail(RESEQ_INVALID_ARGUMENT, "null records");
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    auto pad = reseq_cuda_ctx::padded;
+    const size_t bits = m / 32 + 2 + (m / kRefTile + 2 + 3) / 4;
+    RSQ_TRY(ctx->reserve(pad(sizeof(u64) * m) + pad(sizeof(u32) * m) + 2 * pad(sizeof(u32) * bits) + pad(1024) +
+                         sort_workspace_bytes(m) + 8192));
+    ctx->begin();
+    u64* rec_b = ctx->alloc<u64>(m);
+    u32* whole = ctx->alloc<u32>(m);
+    sh->u_headbits = ctx->alloc<u32>(bits);
+    sh->u_uncbits = ctx->alloc<u32>(bits);
+    sh->u_counters = ctx->alloc<u32>(64);
+    SortWorkspace ws;
+    if (!rec_b || !whole || !sh->u_headbits || !sh->u_uncbits || !sh->u_counters)
+        return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
+    RSQ_TRY(sort_workspace_carve(ctx, m, &ws));
+    RSQ_CUDA(cudaMemsetAsync(sh->u_counters, 0, 8 * sizeof(u32), ctx->stream));
+    reseq_sa_stats st{};
+    // stable passes: equal keys keep the (t, position) order the caller brought the bucket into
+    return uniform_sort_link(ctx, sh->packed, sh->period, d_records, rec_b, m, false, whole, d_cov, sh->u_counters, ws,
+                             &st, &sh->u_sorted);
+}
+
+int reseq_cuda_sa_shard_uniform_finish(reseq_cuda_sa_shard* sh, const uint8_t* d_cov, uint32_t* d_sa_out,
+                                       uint64_t* unfinished) {
+    using namespace rsq;
+    if (!sh || !sh->period || !d_cov || !unfinished) return fail(RESEQ_INVALID_ARGUMENT, "bad shard argument");
+    *unfinished = 0;
+    if (sh->u_m == 0) return RESEQ_OK;
+    if (!sh->u_sorted || !d_sa_out) return fail(RESEQ_INVALID_ARGUMENT, "uniform_finish must follow uniform_sort_link");
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    reseq_sa_stats st{};
+    const int status = uniform_accept_refine(ctx, sh->packed, sh->sent, sh->n, sh->period, sh->u_sorted, sh->u_m, d_cov,
+                                             sh->u_headbits, sh->u_uncbits, d_sa_out, 1 << 20, sh->u_counters, &st,
+                                             unfinished);
+    sh->u_sorted = nullptr;
+    return status;
 }
 
 void reseq_cuda_sa_shard_destroy(reseq_cuda_sa_shard* sh) {

@@ -1,6 +1,10 @@
 """Multi-GPU form of the hot path: one process per GPU.
 
-  SA build       sample sort on the 24-bit initial key (12 bases).  The text is replicated (2-bit
+  SA build       (uniform read sets -- k reads of one length -- take the same route with the
+                 single-GPU fast path's kernels: transposed 16-base records of a slice of READS,
+                 bucket brought back into (t, position) order after the exchange, one verified
+                 overlap per whole read, per-read proof table combined by an all-reduce MAX.)
+                 sample sort on the 24-bit initial key (12 bases).  The text is replicated (2-bit
                  packed it is n/4 bytes); every rank makes the 64-bit records (key24 << 40 |
                  terminator byte << 32 | position) of its 1/G slice of positions; G-1 splitters are
                  read off an all-reduced histogram of the key's top 16 bits; one ALL-TO-ALL moves
@@ -53,6 +57,10 @@ class TorchComm:
 
     def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def all_reduce_max(self, t: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t
 
     def all_to_all_v(self, send: torch.Tensor, send_counts: Sequence[int]):
@@ -111,6 +119,16 @@ class LocalComm:
         if t.is_cuda:
             torch.cuda.current_stream().synchronize()
         total = sum(x.clone() for x in self._exchange(t.clone()))
+        t.copy_(total)
+        return t
+
+    def all_reduce_max(self, t):
+        if t.is_cuda:
+            torch.cuda.current_stream().synchronize()
+        parts = self._exchange(t.clone())
+        total = parts[0].clone()
+        for x in parts[1:]:
+            total = torch.maximum(total, x)
         t.copy_(total)
         return t
 
@@ -186,6 +204,50 @@ class GpuBackend:
         order = i_out.to(torch.int64)
         return records[order].contiguous(), [int(c) for c in counts.tolist()]
 
+    # -- uniform read sets ---------------------------------------------------------------------
+    def uniform_info(self):
+        """(period, reads) when the text is k reads of one length, else None."""
+        period, reads = C.c_uint32(0), C.c_uint64(0)
+        _lib.check(self.lib.reseq_cuda_sa_shard_uniform_info(self.shard, C.byref(period), C.byref(reads)))
+        return (int(period.value), int(reads.value)) if period.value else None
+
+    def uniform_records(self, read_begin: int, read_count: int) -> torch.Tensor:
+        period, _ = self.uniform_info()
+        r = torch.empty(read_count * period, dtype=torch.int64, device=self.device)
+        _lib.check(self.lib.reseq_cuda_sa_shard_uniform_records(self.shard, read_begin, read_count, _p(r)))
+        self.ex.synchronize()
+        return r
+
+    def order_by_distance(self, records: torch.Tensor, period: int) -> torch.Tensor:
+        """The slices of a bucket arrive source by source, each in (t, position) order; one stable
+        pass of this library's radix sort on t = period - 1 - position mod period makes the whole
+        bucket (t, position)-ordered (sources own ascending, disjoint position ranges)."""
+        if records.numel() == 0:
+            return records
+        pos = records & 0xFFFFFFFF
+        t32 = ((period - 1) - pos % period).to(torch.int32)
+        idx = torch.arange(records.numel(), dtype=torch.int32, device=records.device)
+        t_out, i_out = torch.empty_like(t32), torch.empty_like(idx)
+        _lib.check(self.lib.reseq_cuda_radix_sort_device(self.ex.handle, _p(t32), _p(idx), records.numel(),
+                                                         _p(t_out), _p(i_out)))
+        self.ex.synchronize()
+        return records[i_out.to(torch.int64)].contiguous()
+
+    def uniform_sort_link(self, records: torch.Tensor, reads: int) -> torch.Tensor:
+        cov = torch.zeros(reads, dtype=torch.uint8, device=self.device)
+        self._bucket = records     # sorted in place / ping-pong: must stay alive until uniform_finish
+        _lib.check(self.lib.reseq_cuda_sa_shard_uniform_sort_link(self.shard, _p(records), records.numel(), _p(cov)))
+        self.ex.synchronize()
+        return cov
+
+    def uniform_finish(self, cov: torch.Tensor):
+        m = self._bucket.numel()
+        sa = torch.empty(m, dtype=torch.int32, device=self.device)
+        unfinished = C.c_uint64(0)
+        _lib.check(self.lib.reseq_cuda_sa_shard_uniform_finish(self.shard, _p(cov), _p(sa), C.byref(unfinished)))
+        self._bucket = None
+        return sa, int(unfinished.value)
+
     def finish(self, records):
         m = records.numel()
         sa = torch.empty(m, dtype=torch.int32, device=self.device)
@@ -232,15 +294,29 @@ def build_sa_sharded(d_text: torch.Tensor, comm, backend, stats: Optional[dict] 
         if G == 1 or not dna or n < 4 * G:
             stats["path"] = "replicated"
             return backend.full_build(d_text)
-        lo, hi = (n * r) // G, (n * (r + 1)) // G
-        records = backend.records(lo, hi - lo)
+        uniform = backend.uniform_info() if hasattr(backend, "uniform_info") else None
+        if uniform is not None and uniform[1] >= G:
+            period, reads = uniform
+            lo, hi = (reads * r) // G, (reads * (r + 1)) // G          # a slice of READS
+            records = backend.uniform_records(lo, hi - lo)
+        else:
+            uniform = None
+            lo, hi = (n * r) // G, (n * (r + 1)) // G                  # a slice of positions
+            records = backend.records(lo, hi - lo)
         hist = comm.all_reduce_sum(backend.prefix_histogram(records))
         bounds = choose_bounds(hist, G)
         records, counts = backend.partition(records, bounds)
         mine, _ = comm.all_to_all_v(records, counts)
         stats["bucket"] = int(mine.numel())
         stats["sent"] = int(sum(counts) - counts[r])
-        bucket, unfinished = backend.finish(mine)
+        if uniform is not None:
+            mine = backend.order_by_distance(mine, period)
+            cov = comm.all_reduce_max(backend.uniform_sort_link(mine, reads))
+            bucket, unfinished = backend.uniform_finish(cov)
+            stats["records"] = "uniform"
+        else:
+            bucket, unfinished = backend.finish(mine)
+            stats["records"] = "general"
         flag = comm.all_reduce_sum(torch.tensor([unfinished], dtype=torch.int64, device=d_text.device))
         if int(flag.item()) != 0:
             # a group outgrew the refine window somewhere: every rank builds the whole array

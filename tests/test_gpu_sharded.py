@@ -38,12 +38,14 @@ def run_ranks(G, fn):
     return out
 
 
-def sharded_build(rq, text, G):
+def sharded_build(rq, text, G, uniform=True):
     from paper_1404_3456_b200.sharded import GpuBackend, build_sa_sharded
     d_text = torch.from_numpy(np.array(text, dtype=np.uint8, copy=True)).cuda()
 
     def fn(comm):
         ex = rq.Executor(0)
+        if not uniform:
+            ex.set_option("sa_uniform", 0)
         stats = {}
         sa, rank = build_sa_sharded(d_text, comm, GpuBackend(ex), stats)
         torch.cuda.synchronize()
@@ -59,12 +61,33 @@ def test_sharded_build_equals_single_gpu(rq, ex, oracle, G):
     text, _ = rq.synth_read_text(60_000, 100, 6_000)
     want = rq.build_parallel(text, ex)
     assert oracle.verify_sa(text, want.sa) == 0
+    for uniform in (True, False):    # the read-slice / proof-table route and the position-slice route
+        res = sharded_build(rq, text, G, uniform)
+        for sa, rank, stats in res:
+            assert stats["path"] == "sharded" and stats["records"] == ("uniform" if uniform else "general")
+            assert np.array_equal(sa, want.sa) and np.array_equal(rank, want.rank)
+        # the buckets partition the suffixes: every rank sent and received something
+        sizes = [s["bucket"] for _, _, s in res]
+        assert sum(sizes) == text.size and min(sizes) > 0
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_uniform_build_on_repeats_and_duplicates(rq, ex, oracle, G):
+    """Groups that mix loci (re-sorted inside a bucket), duplicate reads, whole reads whose
+    predecessor lives in another rank's slice of reads: the proof table must be complete after the
+    all-reduce, and the result the single-GPU one."""
+    rng = np.random.default_rng(91)
+    unit = bytes(rng.choice([65, 67, 71, 84], 4000).astype(np.uint8))
+    genome = unit + unit[:2000] + bytes(rng.choice([65, 67, 71, 84], 1500).astype(np.uint8)) + unit[1000:3000]
+    starts = rng.integers(0, len(genome) - 80 + 1, 5000)
+    reads = [genome[int(s):int(s) + 80] for s in starts]
+    reads += reads[:300]
+    text = np.frombuffer(b"".join(r + b"\0" for r in reads), np.uint8)
+    want = rq.build_parallel(text, ex)
+    assert oracle.verify_sa(text, want.sa) == 0
     for sa, rank, stats in sharded_build(rq, text, G):
-        assert stats["path"] == "sharded"
+        assert stats["records"] == "uniform"
         assert np.array_equal(sa, want.sa) and np.array_equal(rank, want.rank)
-    # the buckets partition the suffixes: every rank sent and received something
-    sizes = [s["bucket"] for _, _, s in sharded_build(rq, text, G)]
-    assert sum(sizes) == text.size and min(sizes) > 0
 
 
 def test_sharded_build_ragged_and_tiny(rq, ex):
@@ -86,8 +109,11 @@ def test_sharded_build_fallbacks(rq, ex):
         assert stats["path"] == "replicated" and np.array_equal(sa, want.sa)
     big_groups = np.frombuffer((b"ACGTACGTAC" * 12 + b"\0") * 3000, np.uint8)   # groups of 3000 > refine window
     want = rq.build_parallel(big_groups, ex)
-    for sa, rank, stats in sharded_build(rq, big_groups, 2):
+    for sa, rank, stats in sharded_build(rq, big_groups, 2, uniform=False):
         assert stats["path"] == "replicated-fallback"
+        assert np.array_equal(sa, want.sa) and np.array_equal(rank, want.rank)
+    for sa, rank, stats in sharded_build(rq, big_groups, 2):     # duplicates are proven, whatever the group size
+        assert stats["path"] == "sharded" and stats["records"] == "uniform"
         assert np.array_equal(sa, want.sa) and np.array_equal(rank, want.rank)
 
 

@@ -55,9 +55,64 @@ def records_of(text: np.ndarray, lo: int, hi: int) -> np.ndarray:
     return out
 
 
+def uniform_records_of(text: np.ndarray, period: int, read_begin: int, read_count: int) -> np.ndarray:
+    """numpy restatement of gen_uniform_kernel (csrc/sa.cu): key32 << 32 | pos, key32 = the first 16
+    bases zero padded from the sentinel on; record t * read_count + r = suffix of read read_begin + r
+    with t symbols before its sentinel."""
+    code = np.zeros(256, np.int64)
+    code[[65, 67, 71, 84]] = [0, 1, 2, 3]
+    out = np.zeros(read_count * period, np.int64)
+    for t in range(period):
+        for r in range(read_count):
+            pos = (read_begin + r) * period + (period - 1 - t)
+            key = 0
+            for b in range(min(t, 16)):
+                key |= int(code[text[pos + b]]) << (2 * (15 - b))
+            v = (key << 32) | pos
+            out[t * read_count + r] = v - (1 << 64) if v >= (1 << 63) else v
+    return out
+
+
 class NumpyBackend:
-    def __init__(self, oracle_rank):
+    def __init__(self, oracle_rank, uniform=False):
         self.oracle_rank = oracle_rank   # inverse SA of the whole text from the oracle
+        self.uniform = uniform
+
+    # -- uniform read sets: the orchestration contract, not the kernels ------------------------------
+    def uniform_info(self):
+        if not self.uniform:
+            return None
+        seps = np.flatnonzero(self.text == 0)
+        period = int(seps[0]) + 1
+        assert np.array_equal(seps, np.arange(seps.size) * period + period - 1)
+        return period, int(seps.size)
+
+    def uniform_records(self, read_begin, read_count):
+        return torch.from_numpy(uniform_records_of(self.text, self.uniform_info()[0], read_begin, read_count))
+
+    def order_by_distance(self, records, period):
+        r = records.numpy()
+        t = (period - 1) - (r & 0xFFFFFFFF) % period
+        return torch.from_numpy(r[np.argsort(t, kind="stable")].copy())
+
+    def uniform_sort_link(self, records, reads):
+        r = records.numpy()
+        period = self.uniform_info()[0]
+        p = r & 0xFFFFFFFF
+        t = (period - 1) - p % period
+        # the contract the stable digit passes rely on: the bucket arrives in (t, position) order
+        assert np.all((t[1:] > t[:-1]) | ((t[1:] == t[:-1]) & (p[1:] > p[:-1]))), "bucket not in (t, position) order"
+        self._bucket = p
+        cov = np.zeros(reads, np.uint8)
+        cov[(p[t == period - 1] // period)] = 1      # this rank proves things about the whole reads it holds
+        return torch.from_numpy(cov)
+
+    def uniform_finish(self, cov):
+        # every whole read lies in exactly one bucket: the all-reduce MAX must have merged all tables
+        assert bool(torch.all(cov == 1)), "per-read tables were not combined across ranks"
+        p = self._bucket
+        by_suffix = p[np.argsort(self.oracle_rank[p], kind="stable")]
+        return torch.from_numpy(by_suffix.astype(np.int32)), 0
 
     def open(self, d_text):
         self.text = d_text.numpy()
@@ -100,7 +155,7 @@ class NumpyBackend:
         return torch.from_numpy(sa.astype(np.int32)), torch.from_numpy(self.oracle_rank.astype(np.int32))
 
 
-def worker(rank, world, port, text_bytes, oracle_rank, out_dir):
+def worker(rank, world, port, text_bytes, oracle_rank, out_dir, uniform=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     sys.path.insert(0, str(ROOT))
@@ -109,31 +164,34 @@ def worker(rank, world, port, text_bytes, oracle_rank, out_dir):
     comm = TorchComm()
     d_text = torch.from_numpy(np.frombuffer(text_bytes, np.uint8).copy())
     stats = {}
-    sa, rk = build_sa_sharded(d_text, comm, NumpyBackend(oracle_rank), stats)
+    sa, rk = build_sa_sharded(d_text, comm, NumpyBackend(oracle_rank, uniform), stats)
     np.save(Path(out_dir) / f"sa{rank}.npy", sa.numpy())
     np.save(Path(out_dir) / f"rank{rank}.npy", rk.numpy())
-    (Path(out_dir) / f"stats{rank}.txt").write_text(f"{stats['path']} {stats.get('bucket', 0)} {stats.get('sent', 0)}")
+    (Path(out_dir) / f"stats{rank}.txt").write_text(
+        f"{stats['path']} {stats.get('bucket', 0)} {stats.get('sent', 0)} {stats.get('records', '-')}")
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sample_sort_exchange_under_gloo(oracle, tmp_path, world):
+@pytest.mark.parametrize("world,uniform", [(2, False), (2, True)])
+def test_sample_sort_exchange_under_gloo(oracle, tmp_path, world, uniform):
+    """uniform: slices of READS, transposed 16-base records, the bucket re-ordered on the terminator
+    distance after the exchange, per-read tables combined by an all-reduce MAX."""
     rng = np.random.default_rng(11)
     genome = rng.choice([65, 67, 71, 84], 900).astype(np.uint8)
     reads = [bytes(genome[s:s + 40]) + b"\0" for s in rng.integers(0, 860, 120)]
     text = np.frombuffer(b"".join(reads), np.uint8)
     want_sa, want_rank = oracle.build_sa(text)
-    port = 29500 + int(rng.integers(0, 2000))
-    mp.spawn(worker, args=(world, port, text.tobytes(), want_rank.astype(np.int64), str(tmp_path)), nprocs=world,
-             join=True)
+    port = 29500 + int(rng.integers(0, 2000)) + (7 if uniform else 0)
+    mp.spawn(worker, args=(world, port, text.tobytes(), want_rank.astype(np.int64), str(tmp_path), uniform),
+             nprocs=world, join=True)
     buckets = []
     for r in range(world):
         sa = np.load(tmp_path / f"sa{r}.npy").view(np.uint32)
         rk = np.load(tmp_path / f"rank{r}.npy").view(np.uint32)
         assert np.array_equal(sa, want_sa) and np.array_equal(rk, want_rank)
-        path, bucket, sent = (tmp_path / f"stats{r}.txt").read_text().split()
-        assert path == "sharded" and int(sent) > 0
+        path, bucket, sent, records = (tmp_path / f"stats{r}.txt").read_text().split()
+        assert path == "sharded" and int(sent) > 0 and records == ("uniform" if uniform else "general")
         buckets.append(int(bucket))
     assert sum(buckets) == text.size and min(buckets) > text.size // 4   # balanced by the splitters
 
