@@ -33,6 +33,11 @@ int reseq_cuda_ctx::reserve(size_t bytes) {
     cudaError_t e = cudaMalloc(&arena, want);
     if (e != cudaSuccess) {
         cudaGetLastError();
+        {   // blocks cached by the index allocator's pool are of no use to cudaMalloc: hand them back
+            cudaMemPool_t pool = nullptr;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess && pool) cudaMemPoolTrimTo(pool, 0);
+            cudaGetLastError();
+        }
         e = cudaMalloc(&arena, bytes);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -156,6 +161,14 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     RSQ_CUDA(cudaEventCreateWithFlags(&ctx->copy_event, cudaEventDisableTiming));
     ctx->stream = ctx->own_stream;
     RSQ_CUDA(cudaMallocHost(&ctx->pinned, 4096));
+    {   // index arrays come from the default memory pool: keep freed blocks cached for the next index
+        cudaMemPool_t pool = nullptr;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess && pool) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
     if (const char* e = std::getenv("RESEQ_INVERSE_LO_BITS")) ctx->opt_inverse_lo_bits = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_LOOKAHEAD")) {

@@ -63,7 +63,10 @@ template <typename T>
 int dev_alloc(reseq_cuda_index* ix, T** p, size_t count) {
     *p = nullptr;
     void* raw = nullptr;
-    cudaError_t e = cudaMalloc(&raw, std::max<size_t>(count, 1) * sizeof(T));
+    // stream-ordered allocation from the device's default pool (its release threshold is raised at
+    // context creation): an index built after another one was destroyed reuses the cached blocks
+    // instead of paying cudaMalloc / cudaFree of gigabytes (40-200 ms of wall time per index before)
+    cudaError_t e = cudaMallocAsync(&raw, std::max<size_t>(count, 1) * sizeof(T), ix->ctx->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(RESEQ_OUT_OF_MEMORY, "cudaMalloc failed while building the index");
@@ -971,7 +974,8 @@ void reseq_cuda_index_destroy(reseq_cuda_index* ix) {
         cudaSetDevice(ix->ctx->device);
         cudaStreamSynchronize(ix->ctx->stream);
     }
-    for (void* p : ix->owned) cudaFree(p);
+    for (void* p : ix->owned) cudaFreeAsync(p, ix->ctx ? ix->ctx->stream : nullptr);
+    if (ix->ctx) cudaStreamSynchronize(ix->ctx->stream);
     delete ix;
 }
 
