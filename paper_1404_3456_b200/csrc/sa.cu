@@ -71,19 +71,30 @@ pack_dna_kernel(const u8* __restrict__ text, u64 n, u64* __restrict__ packed,
         const u64 base = w << 6;
         u64 p0 = 0, p1 = 0, s = 0;
         if (VEC && base + 64 <= n) {
+            // four bytes at a time (the kernel was bound by its ~20 instructions per byte, not by HBM):
+            //   code  = ((c >> 1) ^ (c >> 2)) & 3 in every byte lane; one multiply gathers the four 2-bit
+            //           codes into a byte, first base highest (no partial products collide below bit 24,
+            //           the others overflow);
+            //   zero  = the classic has-zero-byte mask; valid = zero or equal to one of A, C, G, T.
+            auto zero_mask = [](u32 v) { return ~(((v & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v | 0x7f7f7f7fu); };   // 0x80 per zero byte
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint4 v = ld_stream_v4(text + base + 16 * q);
                 const u32 word[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const u32 c = (word[t >> 2] >> (8 * (t & 3))) & 0xFFu;
-                    bad |= !is_dna_or_zero(c);
-                    const int p = 16 * q + t;
-                    const u64 code = dna_code(c) & (c ? 3u : 0u);
-                    if (p < 32) p0 |= code << (62 - 2 * p);
-                    else p1 |= code << (62 - 2 * (p - 32));
-                    s |= static_cast<u64>(c == 0u) << (63 - p);
+                for (int t = 0; t < 4; ++t) {
+                    const u32 w4 = word[t];
+                    const u32 zm = zero_mask(w4);
+                    const u32 ok = zm | zero_mask(w4 ^ 0x41414141u) | zero_mask(w4 ^ 0x43434343u) |
+                                   zero_mask(w4 ^ 0x47474747u) | zero_mask(w4 ^ 0x54545454u);
+                    bad |= ok != 0x80808080u;
+                    const u32 codes = ((w4 >> 1) ^ (w4 >> 2)) & 0x03030303u;                // zero bytes give 0
+                    const u64 byte = (codes * 0x40100401u) >> 24;                           // c0 c1 c2 c3, 2 bits each
+                    const u64 zbits = ((zm >> 7) * 0x08040201u) >> 24 & 0xfu;               // z0 z1 z2 z3 -> bits 3..0
+                    const int p = 16 * q + 4 * t;                                           // first position of the group
+                    if (p < 32) p0 |= byte << (56 - 2 * p);
+                    else p1 |= byte << (56 - 2 * (p - 32));
+                    s |= zbits << (60 - p);
                 }
             }
         } else {
