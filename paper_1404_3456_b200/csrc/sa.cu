@@ -990,13 +990,32 @@ gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0, u64 k,
         if (t < kUniK) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;   // zero padded from the sentinel on
         const u64 pos = (read0 + r0 + rl) * period + (period - 1 - t);
         elems[static_cast<u64>(t) * k + r0 + rl] = (static_cast<u64>(key) << 32) | pos;
-        atomicAdd(&s_hist[key & 0xffu], 1u);
-        atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
-        atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
-        atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
+        // One histogram serves all four passes: digit j of a suffix (bases 4j..4j+3 of its window,
+        // zero padded) is the TOP digit of the suffix 4j positions further into the same read, and 0
+        // if there is none.  So H_j = A - B_j + [0] * 4jk, A = top-digit histogram of all suffixes,
+        // B_j = that of the suffixes at the first 4j offsets of a read (8 % of them); see
+        // uniform_hist_kernel.  Rows here: [3] = A, [2] = B_1, [1] = B_2, [0] = B_3.
+        const u32 top = key >> 24, o = period - 1 - t;
+        atomicAdd(&s_hist[3 * kRadix + top], 1u);
+        if (o < 12) {
+            atomicAdd(&s_hist[top], 1u);
+            if (o < 8) atomicAdd(&s_hist[kRadix + top], 1u);
+            if (o < 4) atomicAdd(&s_hist[2 * kRadix + top], 1u);
+        }
     }
     __syncthreads();
     hist_flush(s_hist, g_hist, 4);
+}
+
+// Turns gen_uniform_kernel's rows (A, B_1, B_2, B_3) into the digit histograms of the four passes
+// for k reads: pass p (p = 3: top digit) counts H = A - B_(3-p) + [digit 0] * 4 (3 - p) k.
+__global__ void uniform_hist_kernel(u32* __restrict__ hist, u64 k) {
+    const u32 v = threadIdx.x;
+    const u32 a = hist[3 * kRadix + v];
+    for (int p = 0; p < 3; ++p) {
+        const u32 pad = v == 0 ? static_cast<u32>(4ull * (3 - p) * k) : 0u;
+        hist[p * kRadix + v] = a - hist[p * kRadix + v] + pad;
+    }
 }
 
 // Proofs for refine_elems_kernel<true>.  In a sorted group the predecessors of a whole read b
@@ -1536,6 +1555,9 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     RSQ_LAUNCH_BEGIN(ctx, "gen_uniform_kernel");
     gen_uniform_kernel<<<static_cast<unsigned>((k + kUniReads - 1) / kUniReads), 256, 0, s>>>(packed, period, 0, k,
                                                                                              elems_a, ws.hist);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_LAUNCH_BEGIN(ctx, "uniform_hist_kernel");
+    uniform_hist_kernel<<<1, kRadix, 0, s>>>(ws.hist, k);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     const u64* sorted = nullptr;
