@@ -1068,7 +1068,7 @@ __global__ void __launch_bounds__(256)
 accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict__ cov, u32 period,
                       u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
                       u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
-    constexpr int kPer = 4;   // records per thread in flight
+    constexpr int kPer = 8;   // records per thread in flight
     const unsigned lane = lane_id();
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     for (u64 i0 = ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * (32 * kPer); i0 < m;
