@@ -338,13 +338,6 @@ __device__ __forceinline__ void residual_starts_in_bracket(const IndexView& iv, 
     *s_last = sl;
 }
 
-__device__ __forceinline__ void locate_residual_starts(const IndexView& iv, u64 ppos, u32 m, u32* s_first,
-                                                       u32* s_last) {
-    u32 r, f0, f1;
-    residual_bracket(iv, ppos, m, &r, &f0, &f1);
-    residual_starts_in_bracket(iv, ppos, m, r, f0, f1, s_first, s_last);
-}
-
 __global__ void __launch_bounds__(256)
 locate_residuals_kernel(IndexView iv, const u32* __restrict__ frag, const u32* __restrict__ off, u64 q,
                         u32* __restrict__ lo, u32* __restrict__ hi) {
@@ -481,8 +474,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
             if (queued) work_off(queued);
             publish(i, mine);
         }
-        return;
-    }
+    } else {
     for (u64 i = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < f1; i += warps) {
         const u32 len = iv.lens[i];
         const u64 start = iv.starts[i];
@@ -518,6 +510,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
             }
         }
         publish(i, mine);
+    }
     }
 }
 
