@@ -375,14 +375,15 @@ def bench_main(args, workload: str, rank: int, world: int, local_rank: int) -> N
     launches0 = ex.launch_count
     # device time between barriers (CUDA events on the launching stream), maximum over the ranks
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    dist.barrier()
-    ev0.record()
-    for _ in range(args.steps):
-        sa, rk = build_sa_sharded(d_text, comm, GpuBackend(ex, dev), stats)
-    ev1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
+    with B.ClockSampler(local_rank) as clocks:   # nvidia-smi clocks / throttle reasons during the timed region
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            sa, rk = build_sa_sharded(d_text, comm, GpuBackend(ex, dev), stats)
+        ev1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
     dt = torch.tensor([ev0.elapsed_time(ev1) * 1e-3], dtype=torch.float64, device=dev)
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     ms = float(dt.item()) / args.steps * 1e3
@@ -396,9 +397,11 @@ def bench_main(args, workload: str, rank: int, world: int, local_rank: int) -> N
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": B.DESCRIPTION[workload], "suffixes": n, "path": stats.get("path"),
+                       "records": stats.get("records"),
                        "bucket_rank0": stats.get("bucket"), "records_sent_rank0": stats.get("sent"),
                        "l2_policy": "inputs larger than L2"},
             "gpu_launches": int(ex.launch_count - launches0),
+            "clocks": clocks.summary(),
             "roofline": {"bound": "hbm", "kernel": "whole build", "achieved": per_suffix * n / (ms * 1e-3) / 1e9 / world,
                          "peak": peak, "unit": "GB/s", "frac": per_suffix * n / (ms * 1e-3) / 1e9 / world / peak,
                          "traffic": None, "peak_source": peak_src},
