@@ -410,3 +410,5 @@ def bench_main(args, workload: str, rank: int, world: int, local_rank: int) -> N
                     "note": "multi-GPU line: device-resident replicated text; see the N=1 line for the host-buffer path"},
             "checks": {"rank_is_inverse_of_sa": ok},
         }))
+    dist.barrier()
+    dist.destroy_process_group()
