@@ -1762,9 +1762,10 @@ int reseq_cuda_sa_shard_create(reseq_cuda_ctx* ctx, const uint8_t* d_text, size_
     sh->ctx = ctx;
     sh->d_text = d_text;
     sh->n = n;
-    if (cudaMalloc(&sh->packed, sizeof(u64) * (n / 32 + 8)) != cudaSuccess ||
-        cudaMalloc(&sh->sent, sizeof(u64) * (n / 64 + 8)) != cudaSuccess ||
-        cudaMalloc(&sh->flags, 256) != cudaSuccess) {
+    // stream-ordered pool allocations (cached across shards: a build per step pays no cudaMalloc)
+    if (cudaMallocAsync(&sh->packed, sizeof(u64) * (n / 32 + 8), ctx->stream) != cudaSuccess ||
+        cudaMallocAsync(&sh->sent, sizeof(u64) * (n / 64 + 8), ctx->stream) != cudaSuccess ||
+        cudaMallocAsync(&sh->flags, 256, ctx->stream) != cudaSuccess) {
         cudaGetLastError();
         reseq_cuda_sa_shard_destroy(sh);
         return fail(RESEQ_OUT_OF_MEMORY, "cudaMalloc failed for the packed text");
@@ -1880,9 +1881,11 @@ void reseq_cuda_sa_shard_destroy(reseq_cuda_sa_shard* sh) {
         cudaSetDevice(sh->ctx->device);
         cudaStreamSynchronize(sh->ctx->stream);
     }
-    cudaFree(sh->packed);
-    cudaFree(sh->sent);
-    cudaFree(sh->flags);
+    cudaStream_t st = sh->ctx ? sh->ctx->stream : nullptr;
+    if (sh->packed) cudaFreeAsync(sh->packed, st);
+    if (sh->sent) cudaFreeAsync(sh->sent, st);
+    if (sh->flags) cudaFreeAsync(sh->flags, st);
+    if (sh->ctx) cudaStreamSynchronize(st);
     delete sh;
 }
 
