@@ -71,7 +71,27 @@ int main() {
             a.payload.push_back(i);
         }
         REQUIRE(radix_sort(a, dev) == chunked_radix_sort(a, dev, 4));
+        {   // split plan (radix_sort.hpp:35-52; test_parallel.cpp:109-123): tof counts the zero bits,
+            // the destinations are a permutation and realise split_by_bit
+            const auto plan = split_destinations(a.keys, 5, dev);
+            std::uint32_t zeros = 0;
+            for (auto k : a.keys) zeros += ((k >> 5) & 1u) ^ 1u;
+            REQUIRE(plan.total_false == zeros);
+            key_array moved{u32v(a.keys.size()), u32v(a.keys.size())};
+            for (std::size_t i = 0; i < a.keys.size(); ++i) {
+                moved.keys[plan.destinations[i]] = a.keys[i];
+                moved.payload[plan.destinations[i]] = a.payload[i];
+            }
+            REQUIRE(moved == split_by_bit(a, 5, dev));
+            REQUIRE(!phase_is_sorted(a.keys, dev));
+            REQUIRE(phase_is_sorted(radix_sort(a, dev).keys, dev));
+        }
 #ifdef RESEQ_B200_WITH_REFERENCE
+        {
+            const auto plan = split_destinations(a.keys, 5, dev);
+            const auto ref_plan = reseq::detail::split_destinations(a.keys, 5, reseq::executor{});
+            REQUIRE(plan.destinations == ref_plan.destinations && plan.total_false == ref_plan.total_false);
+        }
         REQUIRE(radix_sort(a, dev) == reseq::radix_sort(a));
         REQUIRE(split_by_bit(a, 7, dev) == reseq::split_by_bit(a, 7));
         REQUIRE(exclusive_scan(std::span<const std::uint32_t>(a.payload), dev) == reseq::exclusive_scan(a.payload));
