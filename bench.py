@@ -402,7 +402,19 @@ def main():
         rate = probe.size / cpu_build(cpu_lib, kind, probe, workers)
         sample = cpu_sample(text, L, int(min(1 << 20, max(1 << 17, rate * 15.0))))
         dt = cpu_build(cpu_lib, kind, sample, workers)
-        cpu = {"value": sample.size / dt / 1e6, "unit": UNIT, "cores": workers, "kind": kind,
+        also = None
+        if kind == "reference":   # the reference's other two ways to the same array, one thread each
+            vp = lambda a: a.ctypes.data_as(C.c_void_p)
+            tmp = np.empty(sample.size, np.uint32)
+            t0 = time.perf_counter()
+            cpu_lib.ref_build_naive(vp(sample), C.c_size_t(sample.size), vp(tmp), None)
+            t_naive = time.perf_counter() - t0
+            small = cpu_sample(text, L, 1 << 17)
+            t_one = cpu_build(cpu_lib, kind, small, 1)
+            also = {"build_naive_1_thread_msuffixes_per_s": sample.size / t_naive / 1e6,
+                    "build_parallel_1_worker_msuffixes_per_s": small.size / t_one / 1e6,
+                    "build_parallel_1_worker_sample_suffixes": int(small.size)}
+        cpu = {"value": sample.size / dt / 1e6, "unit": UNIT, "cores": workers, "kind": kind, "also": also,
                "sample": f"first {sample.size // (L + 1)} reads ({sample.size} suffixes) of the same text, 1 build, "
                          f"{dt:.1f} s; reference build_parallel with executor{{workers={workers}}}" if kind == "reference"
                else f"first {sample.size} suffixes, oracle port, 1 thread, {dt:.1f} s"}
