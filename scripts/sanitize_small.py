@@ -40,6 +40,9 @@ k2, p2 = rq.radix_sort(keys, pay, ex)
 order = np.argsort(keys, kind="stable")
 assert np.array_equal(k2, keys[order]) and np.array_equal(p2, pay[order])
 assert np.array_equal(rq.exclusive_scan(np.ones(70_000, np.uint32), ex), np.arange(70_000, dtype=np.uint32))
+d, tof = rq.split_destinations(keys, 3, ex)
+wd, wtof = ora.split_destinations(keys, 3)
+assert tof == wtof and np.array_equal(d, wd) and not rq.is_sorted(keys, ex) and rq.is_sorted(k2, ex)
 # index, queries, overlaps, merge
 fs = rq.fragment_set_from_text(text, starts)
 ix = rq.FragmentIndex(fs, ex)
@@ -49,4 +52,34 @@ wi, wj, ww = ora.overlap_list(fs.concat, fs.starts, lens, 20)
 assert np.array_equal(ov.i, wi) and np.array_equal(ov.j, wj) and np.array_equal(ov.w, ww)
 sup, order = rq.greedy_superstring_from_overlaps(fs, ov)
 assert len(sup) > 0
+ov2 = ix.overlaps(20, reuse_buffers=True)
+assert np.array_equal(ov2.i, wi) and np.array_equal(ov2.w, ww)
+dup = rq.make_fragment_set([b"ACGT" * 10] * 120 + [b"CGTA" * 10] * 40, "dna")     # overflow route of the overlap fill
+ixd = rq.FragmentIndex(dup, ex)
+ovd = ixd.overlaps(4)
+di, dj, dw = ora.overlap_list(dup.concat, dup.starts, dup.lengths(), 4)
+assert np.array_equal(ovd.i, di) and np.array_equal(ovd.j, dj) and np.array_equal(ovd.w, dw)
+rel = ix.prefix_related_patterns([fs.bytes(0)[:30], fs.bytes(1), b"ACGTACGTAC"])
+assert len(rel) == 3
+import os
+if os.environ.get("SANITIZE_NO_SHARDED"):
+    print("sanitize_small: all parity checks passed (sharded part skipped)")
+    raise SystemExit(0)
+# the sharded build of a uniform read set as three virtual ranks
+import threading, torch
+from paper_1404_3456_b200.sharded import GpuBackend, LocalComm, build_sa_sharded
+d_text = torch.from_numpy(np.array(text, copy=True)).cuda()
+comms, outs = LocalComm.make(3), [None] * 3
+def work(r):
+    e = rq.Executor(0)
+    st = {}
+    sa, rk = build_sa_sharded(d_text, comms[r], GpuBackend(e), st)
+    torch.cuda.synchronize()
+    outs[r] = (sa.cpu().numpy().view(np.uint32), st)
+    e.close()
+th = [threading.Thread(target=work, args=(r,)) for r in range(3)]
+[t.start() for t in th]; [t.join() for t in th]
+want = rq.build_parallel(text, ex).sa
+for sa, st in outs:
+    assert st["records"] == "uniform" and np.array_equal(sa, want)
 print("sanitize_small: all parity checks passed")
