@@ -178,6 +178,35 @@ def test_reconstruction_at_config1_scale_properties(rq, ex):
         assert fs.bytes(i) in sup
 
 
+def test_overlaps_at_config2_scale_properties(rq, ex):
+    """BASELINE config 2 (920 000 reads of 150 bp, 30x): 120.5 M queries.  Size-independent
+    properties of the overlap list: sorted unique (i, j), every sampled triple is a true
+    suffix/prefix match and maximal (overlap_weight, overlap.hpp:16-23), the diagonal is absent,
+    a second run is identical, and the sharded ranges concatenate to the same list."""
+    text, starts = rq.synth_read_text(4_600_000, 150, 920_000)
+    fs = rq.fragment_set_from_text(text, starts)
+    ix = rq.FragmentIndex(fs, ex)
+    ov = ix.overlaps(20)
+    assert ov.queries == 920_000 * (150 - 20 + 1)
+    key = (ov.i.astype(np.uint64) << np.uint64(32)) | ov.j.astype(np.uint64)
+    assert np.all(key[1:] > key[:-1]) and not np.any(ov.i == ov.j)
+    assert ov.w.min() >= 20 and ov.w.max() <= 150
+    rng = np.random.default_rng(61)
+    reads = text.reshape(-1, 151)[:, :150]
+    for t in rng.integers(0, ov.i.size, 3000):
+        a, b, w = reads[ov.i[t]], reads[ov.j[t]], int(ov.w[t])
+        assert np.array_equal(a[150 - w:], b[:w])
+        for longer in range(w + 1, 151):                      # no longer overlap exists
+            assert not np.array_equal(a[150 - longer:], b[:longer])
+    again = ix.overlaps(20, reuse_buffers=True)
+    assert np.array_equal(again.i, ov.i) and np.array_equal(again.j, ov.j) and np.array_equal(again.w, ov.w)
+    assert np.array_equal(again.contained, ov.contained)
+    parts = [ix.overlaps(20, lo, hi) for lo, hi in ((0, 300_000), (300_000, 300_001), (300_001, 920_000))]
+    assert np.array_equal(np.concatenate([p.i for p in parts]), ov.i)
+    assert np.array_equal(np.concatenate([p.w for p in parts]), ov.w)
+    ix.close()
+
+
 def test_cpp_shim_drop_in(tmp_path):
     """include/reseq_b200/reseq_cuda.hpp: the reference's KATs through the C++ value-semantics
     shim, standalone and -- where the reference headers exist -- against the reference itself."""
