@@ -207,6 +207,27 @@ def test_overlaps_at_config2_scale_properties(rq, ex):
     ix.close()
 
 
+def test_reconstruction_at_config2_scale(rq, ex):
+    """BASELINE config 2 end to end: device index + overlaps, host greedy merge
+    (overlap.hpp:80-113 at scale).  With 30x error-free coverage of a random genome every merge is
+    a true overlap, so the reconstructed sequence is the genome between the first and the last
+    read: an exact substring of it, every kept read a substring of the result."""
+    G = 4_600_000
+    text, starts = rq.synth_read_text(G, 150, 920_000)
+    fs = rq.fragment_set_from_text(text, starts)
+    ix = rq.FragmentIndex(fs, ex)
+    ov = ix.overlaps(20)
+    sup, order = rq.greedy_superstring_from_overlaps(fs, ov)
+    genome = rq.synth_random_dna(G, 1).tobytes()
+    assert G - 200 < len(sup) <= G and sup in genome
+    kept = np.flatnonzero(ov.contained == 0)
+    assert sorted(order.tolist()) == kept.tolist()
+    rng = np.random.default_rng(62)
+    for i in rng.integers(0, 920_000, 500):
+        assert fs.bytes(int(i)) in sup
+    ix.close()
+
+
 def test_cpp_shim_drop_in(tmp_path):
     """include/reseq_b200/reseq_cuda.hpp: the reference's KATs through the C++ value-semantics
     shim, standalone and -- where the reference headers exist -- against the reference itself."""
