@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the hot path: suffix-array build (Msuffixes/s) + overlap queries/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c1|c2|c3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c1..c5] [--sweep]
 
 One "step" = one complete SA build (2-bit pack, k-mer initial sort, prefix-doubling rounds)
 over the synthetic read text of the named BASELINE.json configuration.  Prints ONE JSON line.
@@ -15,7 +15,12 @@ over the synthetic read text of the named BASELINE.json configuration.  Prints O
              timed live with CUDA events around every launch inside the timed region
   cpu_baseline : the reference's own build_parallel (oracle/_ref) on a bounded prefix of the
              same text, on this box's host cores
-  overlap  : the batched SA binary-search job (queries/s), measured once after the timed steps
+  routes   : the same text through the two general engines (general DNA records: what a ragged read
+             set takes; prefix doubling: the north star's algorithm), forced by context options
+  overlap  : the batched SA search job (queries/s) measured after the timed steps, with its own
+             roofline (per-kernel CUDA-event times, ncu DRAM bytes from profiles/), e2e and the
+             reference's locate_prefix_range loop on this box's host cores as cpu_baseline
+  sweep    : (--sweep, or --workload c3) SA build throughput over n = 2^20 .. full by truncating k
 
 `--impl reference` times the reference CPU implementation only (no GPU work).
 """
@@ -148,6 +153,18 @@ def _load_cpu_lib():
     return C.CDLL(str(port)), "port"
 
 
+def cpu_read_text(G: int, L: int, k: int) -> np.ndarray:
+    """The first k reads of the SURVEY 8(d) text, generated by the CPU libraries (reads are drawn one
+    after another from one RNG stream, so a prefix of the reads is a prefix of the text)."""
+    lib, kind = _load_cpu_lib()
+    out = np.empty(k * (L + 1), np.uint8)
+    fn = lib.ref_make_read_text if kind == "reference" else lib.orc_make_read_text
+    st = fn(C.c_size_t(G), C.c_size_t(L), C.c_size_t(k), C.c_uint64(1), C.c_uint64(2), out.ctypes.data_as(C.c_void_p))
+    if st != 0:
+        raise RuntimeError("CPU text generator failed")
+    return out
+
+
 def cpu_build(lib, kind: str, text: np.ndarray, workers: int) -> float:
     """One reference build_parallel (or oracle build) of `text`; returns seconds."""
     n = text.size
@@ -177,9 +194,9 @@ def run_reference(args, text, read_len, workload):
     # calibrate the sample so that (steps + warmup) builds end within ~150 s
     probe = cpu_sample(text, read_len, 1 << 17)
     t_probe = cpu_build(lib, kind, probe, workers)
-    rate = probe.size / t_probe  # suffixes / s, roughly flat in n for this code
-    budget = 150.0 / max(1, steps + warmup)
-    target = int(min(1 << 20, max(1 << 16, rate * budget)))
+    # build_parallel is ~n log^2 n: time(n) ~ t_probe * (n / n_probe)^1.35 measured here; solve for the budget
+    budget = 120.0 / max(1, steps + warmup)
+    target = int(min(1 << 22, max(1 << 16, probe.size * (budget / t_probe) ** (1 / 1.35))))
     sample = cpu_sample(text, read_len, target)
     for _ in range(warmup):
         cpu_build(lib, kind, sample, workers)
@@ -200,6 +217,56 @@ def run_reference(args, text, read_len, workload):
     print(json.dumps(line))
 
 
+def ncu_overlap_traffic(workload: str) -> dict:
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the overlap kernels, from the ncu
+    --set full captures committed under profiles/ (r2_ncu_overlap_traffic.json: {workload: {kernel: bytes}})."""
+    p = ROOT / "profiles" / "r2_ncu_overlap_traffic.json"
+    if p.exists():
+        try:
+            return {k: float(v) for k, v in json.loads(p.read_text()).get(workload, {}).items()}
+        except Exception:
+            pass
+    return {}
+
+
+def cpu_query_baseline(G: int, L: int, k: int, min_overlap: int = 20) -> dict:
+    """The overlap job's query stream through the reference's own fragment_index::locate_prefix_range
+    (fragment_index.hpp:65-70) on this box's host cores: 1 thread and all threads over one shared index
+    of a labelled prefix of the reads, a bounded number of queries each."""
+    lib, kind = _load_cpu_lib()
+    if kind != "reference":
+        return {"unavailable": "oracle/_ref not present: the reference's fragment_index cannot be timed"}
+    kk = min(k, (1 << 21) // (L + 1))
+    text = cpu_read_text(G, L, kk)
+    starts = (np.arange(kk, dtype=np.uint32) * np.uint32(L + 1))
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    lib.ref_index_create_from_text.restype = C.c_void_p
+    lib.ref_index_query_bench.restype = C.c_double
+    t0 = time.perf_counter()
+    h = lib.ref_index_create_from_text(vp(text), C.c_size_t(text.size), vp(starts), C.c_size_t(kk), 0, 0, 1, C.c_size_t(1 << 15))
+    t_build = time.perf_counter() - t0
+    if not h:
+        return {"unavailable": "reference index construction failed"}
+    cores = os.cpu_count() or 1
+    out = {"kind": "reference", "unit": "Mqueries/s", "what": "fragment_index::locate_prefix_range (fragment_index.hpp:65-70)",
+           "sample": f"index (builder::direct, {t_build:.1f} s) over the first {kk} reads ({text.size} suffixes) of the same text; "
+                     f"query stream = every read suffix of length >= {min_overlap}"}
+    for label, threads, budget in (("1_thread", 1, 400_000), ("all_threads", cores, 400_000 * min(cores, 16))):
+        done, acc = C.c_uint64(0), C.c_uint64(0)
+        sec = lib.ref_index_query_bench(C.c_void_p(h), C.c_uint32(min_overlap), C.c_uint(threads), C.c_uint64(budget), 0,
+                                        C.byref(done), C.byref(acc))
+        out[label] = {"value": done.value / sec / 1e6, "threads": threads, "queries": int(done.value), "seconds": sec}
+    done, acc = C.c_uint64(0), C.c_uint64(0)
+    sec = lib.ref_index_query_bench(C.c_void_p(h), C.c_uint32(min_overlap), C.c_uint(cores), C.c_uint64(100_000 * min(cores, 16)), 1,
+                                    C.byref(done), C.byref(acc))
+    out["prefix_related_all_threads"] = {"value": done.value / sec / 1e6, "threads": cores, "queries": int(done.value),
+                                         "seconds": sec, "what": "fragment_index::prefix_related (fragment_index.hpp:72-109)"}
+    out["value"] = out["all_threads"]["value"]
+    out["cores"] = cores
+    lib.ref_index_destroy(C.c_void_p(h))
+    return out
+
+
 # ---- main arm ----------------------------------------------------------------------------------
 
 def main():
@@ -210,7 +277,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--no-overlap", action="store_true", help="skip the overlap-query measurement")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines")
+    ap.add_argument("--no-routes", action="store_true", help="skip the general-route measurements")
+    ap.add_argument("--sweep", action="store_true",
+                    help="SA build throughput over n = 2^20, 2^22, ... full (BASELINE config 3's sweep; implied by --workload c3)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU code path (sharded.bench_main) even with one rank: a plumbing check")
     args = ap.parse_args()
@@ -225,13 +295,11 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        import paper_1404_3456_b200._lib as lib_mod  # synthetic generator only (host code)
-        lib = lib_mod.load()
-        # the reference arm needs only a prefix of the text: generate 2^20 bytes' worth of reads
-        kk = min(k, (1 << 20) // (L + 1) + 1)
-        text = np.empty(kk * (L + 1), np.uint8)
-        lib.reseq_synth_read_text(G, L, kk, 1, 2, text.ctypes.data_as(C.c_void_p), None)
-        run_reference(args, text, L, workload)
+        # the arm maps oracle/ only (never the product library): the text generator is the reference's
+        # own make_fragment_set over its own RNG draws (oracle/ref_shim.cpp ref_make_read_text), or the
+        # oracle port's restatement of it.  A prefix of the reads is all the arm needs (2^22 bytes' worth).
+        kk = min(k, (1 << 22) // (L + 1) + 1)
+        run_reference(args, cpu_read_text(G, L, kk), L, workload)
         return
 
     import torch
@@ -257,7 +325,10 @@ def main():
     text, starts = rq.synth_read_text(G, L, k, 1, 2, pinned=True)
     n = int(text.size)
     ex = rq.Executor(local_rank)
-    stream = torch.cuda.current_stream()
+    # everything below runs on ONE explicit stream: the library launches on it, torch allocates and
+    # copies on it, and the timing events are recorded on it (CUDA events see only their own stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ex.set_stream(stream.cuda_stream)
     lib = rq._lib.load()
     d_text = torch.from_numpy(text).cuda()
@@ -370,27 +441,101 @@ def main():
     e2e = {"value": n / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": n, "d2h_bytes_per_step": 8 * n,
            "ms_per_step": e2e_s * 1e3, "steps": e2e_steps, "matches_device_run": same}
 
+    peak_frac = lambda b, ms: b / (ms * 1e-3) / 1e9 / peak
+
+    def timed_builds(executor, dn_text, dn, steps, warm=1):
+        """ms per device-resident build of the first dn bytes of the text on `executor`."""
+        s2 = rq.SaStats()
+        run = lambda: rq._lib.check(lib.reseq_cuda_build_sa_device(executor.handle, C.c_void_p(dn_text.data_ptr()), dn,
+                                                                    C.c_void_p(d_sa.data_ptr()), C.c_void_p(d_rank.data_ptr()),
+                                                                    C.byref(s2)))
+        for _ in range(warm):
+            run()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(steps):
+            run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps, s2
+
+    # ---- the general routes on the same text (what ragged reads / other alphabets take) -----------
+    routes = None
+    if not args.no_routes and n <= 400_000_000:
+        routes = {}
+        for name, opt in (("general_dna", ("sa_uniform", 0)), ("doubling", ("sa_text_rounds", 0))):
+            e2 = rq.Executor(local_rank)
+            e2.set_stream(stream.cuda_stream)
+            e2.set_option(*opt)
+            ms_r, st_r = timed_builds(e2, d_text, n, 3)
+            e2.close()
+            routes[name] = {"option": f"{opt[0]}={opt[1]}", "ms_per_build": ms_r, "msuffixes_per_s": n / (ms_r * 1e-3) / 1e6,
+                            "vs_default_route": ms_r / ms_per_step, "rounds": int(st_r.rounds),
+                            "sort_passes": int(st_r.sort_passes), "init_symbols": int(st_r.init_symbols),
+                            "frac_of_8d_model": peak_frac(per_suffix * n, ms_r)}
+
+    # ---- BASELINE config 3: throughput sweep over n by truncating k ---------------------------------
+    sweep = None
+    if args.sweep or workload == "c3":
+        sweep = []
+        sizes = [e for e in range(20, 40, 2) if (1 << e) < n]
+        for kk in [max(1, (1 << e) // (L + 1)) for e in sizes] + [k]:
+            dn = kk * (L + 1)
+            ms_s, _ = timed_builds(ex, d_text, dn, 10 if dn < (1 << 26) else 5, warm=2)
+            b_s, _, _ = bytes_alg_per_suffix(dn, L)
+            sweep.append({"reads": kk, "suffixes": dn, "ms_per_build": ms_s, "msuffixes_per_s": dn / (ms_s * 1e-3) / 1e6,
+                          "frac_of_8d_model": peak_frac(b_s * dn, ms_s)})
+
     # ---- overlap queries -------------------------------------------------------------------------
     overlap = None
     if not args.no_overlap:
         del h_rank
         fset = rq.fragment_set_from_text(text, starts)
+        rq.FragmentIndex(fset, ex).close()    # warm-up: arena growth, pool allocations
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         ix = rq.FragmentIndex(fset, ex)
         torch.cuda.synchronize()
         t_index = time.perf_counter() - t0
         ix.overlaps(20, reuse_buffers=True)  # warm-up (arena growth, page-locked result arrays)
+        ex.profile(True)
         t0 = time.perf_counter()
         ov = ix.overlaps(20, reuse_buffers=True)
         t_ov = time.perf_counter() - t0
+        ov_prof = ex.profile_read()
+        ex.profile(False)
+        q_alg = 2 * int(np.ceil(np.log2(n))) * 64 + 64
+        traffic = ncu_overlap_traffic(workload)
+        ov_kernels = {}
+        for kname, (cnt, ms) in sorted(ov_prof.items(), key=lambda kv: -kv[1][1]):
+            tr = traffic.get(kname)
+            ov_kernels[kname] = {"ms": ms, "launches": cnt, "share": ms / ov.device_ms if ov.device_ms else None,
+                                 "dram_bytes_ncu": tr, "dram_gbs": tr / (ms * 1e-3) / 1e9 if tr and ms else None,
+                                 "dram_frac_of_peak": tr / (ms * 1e-3) / 1e9 / peak if tr and ms else None}
+        dom_ov = next(iter(ov_kernels)) if ov_kernels else None
+        dom_rec = ov_kernels.get(dom_ov, {})
         overlap = {"metric": "overlap_queries_per_s", "min_overlap": 20, "queries": ov.queries,
                    "value": ov.queries / (ov.device_ms * 1e-3) / 1e6, "unit": "Mqueries/s",
-                   "device_ms": ov.device_ms, "e2e_ms": t_ov * 1e3,
-                   "e2e_value": ov.queries / t_ov / 1e6, "overlaps_found": int(ov.i.size),
+                   "device_ms": ov.device_ms,
+                   "e2e": {"value": ov.queries / t_ov / 1e6, "unit": "Mqueries/s", "ms": t_ov * 1e3,
+                           "h2d_bytes": 8 * (k + 1), "d2h_bytes": int(12 * ov.i.size + k),
+                           "note": "index resident; query offsets in, (i, j, w) triples + containment flags out to page-locked host arrays"},
+                   "overlaps_found": int(ov.i.size),
                    "contained_reads": int(ov.contained.sum()), "index_build_ms": t_index * 1e3,
-                   "alg_bytes_per_query": 2 * int(np.ceil(np.log2(n))) * 64 + 64}
-        overlap["alg_frac_of_peak"] = overlap["alg_bytes_per_query"] * ov.queries / (ov.device_ms * 1e-3) / 1e9 / peak
+                   "roofline": {"bound": "hbm", "kernel": dom_ov, "peak": peak, "unit": "GB/s",
+                                "traffic": dom_rec.get("dram_bytes_ncu"), "achieved": dom_rec.get("dram_gbs"),
+                                "frac": dom_rec.get("dram_frac_of_peak"),
+                                "alg_bytes_per_query_cold_model": q_alg,
+                                "cold_model_frac": q_alg * ov.queries / (ov.device_ms * 1e-3) / 1e9 / peak,
+                                "note": ("achieved = ncu dram bytes of the dominant kernel / its CUDA-event time in this run. "
+                                         "SURVEY 8(d)'s cold binary-search model (2 ceil(log2 n) x 64 + 64 B/query) assumes ~2 log n "
+                                         "DRAM probes; the directory + rank anchor need ~1 DRAM gather per query, so the cold-model "
+                                         "fraction is above 1 and is reported only for continuity"),
+                                "kernels": ov_kernels}}
         ix.close()
+        if not args.no_cpu:
+            overlap["cpu_baseline"] = cpu_query_baseline(G, L, k)
 
     # ---- CPU baseline -------------------------------------------------------------------------------
     cpu = None
@@ -424,12 +569,13 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
         "config": {"workload": DESCRIPTION[workload], "genome_bp": G, "read_len": L, "reads": k, "suffixes": n,
-                   "l2_policy": "inputs larger than L2 (text 139 MB, key/rank arrays >= 556 MB each vs 126 MB L2)"
-                   if n > 64_000_000 else "working set exceeds L2 only partly; no flush",
+                   "l2_policy": (f"inputs larger than L2 (text {n / 1e6:.0f} MB, record arrays {8 * n / 1e6:.0f} MB each, "
+                                 f"sa / rank {4 * n / 1e6:.0f} MB each vs 126 MB L2)")
+                   if 4 * n > 256_000_000 else "working set exceeds L2 only partly; no flush",
                    "rounds": int(st.rounds), "init_symbols": int(st.init_symbols),
                    "sort_passes": int(st.sort_passes), "alphabet": "dna-2bit" if st.alphabet == 0 else "bytes"},
         "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
-        "roofline": roofline, "cpu_baseline": cpu, "overlap": overlap,
+        "roofline": roofline, "cpu_baseline": cpu, "overlap": overlap, "routes": routes, "sweep": sweep,
         "checks": {"rank_is_inverse_of_sa": perm_ok, "host_run_equals_device_run": same},
     }
     print(json.dumps(line))

@@ -67,7 +67,13 @@ typedef struct reseq_cuda_index reseq_cuda_index; /* device-resident fragment in
 int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out);
 void reseq_cuda_ctx_destroy(reseq_cuda_ctx* ctx);
 /* Launch on an externally owned cudaStream_t (e.g. torch's current stream) so callers
- * can bracket work with their own events.  NULL restores the context's own stream. */
+ * can bracket work with their own events and order it against their own kernels and NCCL.
+ * NULL restores the context's own (non-blocking) stream.  The legacy default stream -- whose
+ * cudaStream_t value is also 0, which is what torch.cuda.current_stream().cuda_stream returns
+ * unless a side stream is current -- is selected with RESEQ_CUDA_STREAM_LEGACY (the value of
+ * cudaStreamLegacy); RESEQ_CUDA_STREAM_PER_THREAD likewise (cudaStreamPerThread). */
+#define RESEQ_CUDA_STREAM_LEGACY ((void*)0x1)
+#define RESEQ_CUDA_STREAM_PER_THREAD ((void*)0x2)
 int reseq_cuda_ctx_set_stream(reseq_cuda_ctx* ctx, void* cuda_stream);
 int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx);
 /* Number of kernels this context has launched since creation (bench `gpu_launches`). */

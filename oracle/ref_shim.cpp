@@ -8,9 +8,12 @@
 //
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
 // arm may load the resulting library.
+#include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <thread>
 #include <random>
 #include <string>
 #include <string_view>
@@ -260,6 +263,79 @@ void ref_index_prefix_related(void* hv, const uint8_t* pat, size_t m, uint32_t* 
     std::memcpy(prefixes, rel.prefixes_of.data(), rel.prefixes_of.size() * 4);
     std::memcpy(extensions, rel.extensions_of.data(), rel.extensions_of.size() * 4);
     std::memcpy(exact, rel.exact_matches.data(), rel.exact_matches.size() * 4);
+}
+
+// CPU query baseline: the overlap job's query stream -- for every fragment i and every
+// offset o in [0, |f_i| - min_overlap], the pattern f_i[o..] -- through the reference's own
+// locate_prefix_range (fragment_index.hpp:65-70; mode 0) or prefix_related (:72-109; mode 1), over a
+// shared immutable index from `threads` host threads (fragments dealt in blocks of 64).
+// Stops taking new blocks once `max_queries` have been issued.  Returns seconds; *done = queries run;
+// *acc = sum of interval widths / relation counts (keeps the calls observable).
+double ref_index_query_bench(void* hv, uint32_t min_overlap, unsigned threads, uint64_t max_queries, int mode,
+                             uint64_t* done, uint64_t* acc) {
+    auto* h = static_cast<ref_index*>(hv);
+    const uint32_t k = h->set.size();
+    std::atomic<uint32_t> next{0};
+    std::atomic<uint64_t> issued{0}, total{0};
+    if (threads == 0) threads = 1;
+    auto work = [&] {
+        uint64_t local = 0, mine = 0;
+        for (;;) {
+            if (issued.load(std::memory_order_relaxed) >= max_queries) break;
+            const uint32_t b = next.fetch_add(64);
+            if (b >= k) break;
+            uint64_t q = 0;
+            for (uint32_t i = b; i < k && i < b + 64; ++i) {
+                const std::string_view f = h->set.bytes(i);
+                if (f.size() < min_overlap) continue;
+                for (size_t o = 0; o + min_overlap <= f.size(); ++o) {
+                    const std::string_view pat = f.substr(o);
+                    if (mode == 0) {
+                        const auto r = h->ix->locate_prefix_range(pat);
+                        local += r.second - r.first;
+                    } else {
+                        const auto rel = h->ix->prefix_related(pat);
+                        local += rel.prefixes_of.size() + rel.extensions_of.size() + rel.exact_matches.size();
+                    }
+                    ++q;
+                }
+            }
+            mine += q;
+            issued.fetch_add(q, std::memory_order_relaxed);
+        }
+        total.fetch_add(local);
+        (void)mine;
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < threads; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    if (done) *done = issued.load();
+    if (acc) *acc = total.load();
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// The same index over an already concatenated fragment text (concat = f0 \0 f1 \0 ...; `starts` as in
+// fragment_set): saves the caller the blob/offset detour for large read sets.
+void* ref_index_create_from_text(const uint8_t* concat, size_t n, const uint32_t* starts, size_t k, int alphabet,
+                                 int builder, unsigned workers, size_t chunk) {
+    try {
+        std::vector<std::string> frags(k);
+        for (size_t i = 0; i < k; ++i) {
+            const size_t b = starts[i], e = (i + 1 < k ? starts[i + 1] : n) - 1;
+            frags[i].assign(reinterpret_cast<const char*>(concat) + b, e - b);
+        }
+        auto h = std::make_unique<ref_index>();
+        h->set = reseq::make_fragment_set(frags, alphabet == 0 ? reseq::alphabet::dna : reseq::alphabet::generic_byte);
+        reseq::executor ex(reseq::executor_config{workers, chunk});
+        h->ix = std::make_unique<reseq::fragment_index>(
+            h->set, builder ? reseq::fragment_index::builder::scan_radix : reseq::fragment_index::builder::direct, ex);
+        return h.release();
+    } catch (...) {
+        return nullptr;
+    }
 }
 
 // ---- overlap.hpp -----------------------------------------------------------

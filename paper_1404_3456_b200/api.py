@@ -83,7 +83,17 @@ class Executor:
         return self._h
 
     def set_stream(self, cuda_stream: Optional[int]) -> None:
-        _lib.check(self._lib.reseq_cuda_ctx_set_stream(self._h, C.c_void_p(cuda_stream or 0)))
+        """Launch on the given cudaStream_t.  `None` restores the context's own stream.  The integer
+        0 -- what `torch.cuda.current_stream().cuda_stream` returns for torch's default stream -- means
+        the legacy default stream (RESEQ_CUDA_STREAM_LEGACY), so that library kernels are ordered
+        with torch's and NCCL's work on that stream."""
+        if cuda_stream is None:
+            handle = 0
+        elif int(cuda_stream) == 0:
+            handle = 1   # RESEQ_CUDA_STREAM_LEGACY == cudaStreamLegacy
+        else:
+            handle = int(cuda_stream)
+        _lib.check(self._lib.reseq_cuda_ctx_set_stream(self._h, C.c_void_p(handle)))
 
     def synchronize(self) -> None:
         _lib.check(self._lib.reseq_cuda_ctx_synchronize(self._h))

@@ -424,6 +424,7 @@ int reseq_cuda_split_by_bit(reseq_cuda_ctx* ctx, const uint32_t* keys, const uin
     if ((payload == nullptr) != (payload_out == nullptr))
         return fail(RESEQ_INVALID_ARGUMENT, "payload and payload_out must both be given or both be null");
     if (n == 0) return RESEQ_OK;
+    if (!keys || !keys_out) return fail(RESEQ_INVALID_ARGUMENT, "null key buffer");
     if (n == 1) {  // the sort path returns early below two keys; a split of one key is a copy
         keys_out[0] = keys[0];
         if (payload) payload_out[0] = payload[0];
@@ -464,6 +465,8 @@ int reseq_cuda_radix_sort_device(reseq_cuda_ctx* ctx, const uint32_t* d_keys, co
     if ((d_payload == nullptr) != (d_payload_out == nullptr))
         return fail(RESEQ_INVALID_ARGUMENT, "payload and payload_out must both be given or both be null");
     if (n == 0) return RESEQ_OK;
+    if (!d_keys || !d_keys_out) return fail(RESEQ_INVALID_ARGUMENT, "null device key buffer");
+    if (n > RESEQ_CUDA_MAX_TEXT) return fail(RESEQ_INVALID_ARGUMENT, "more than 2^32-2 keys");
     const bool has_val = d_payload != nullptr;
     const size_t arr = reseq_cuda_ctx::padded(sizeof(u32) * n);
     RSQ_TRY(ctx->reserve(arr * (has_val ? 2 : 1) + sort_workspace_bytes(n) + 4096));

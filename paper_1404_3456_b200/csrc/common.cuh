@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -35,6 +36,21 @@ int fail(int code, const std::string& msg);
     do {                               \
         int _s = (expr);               \
         if (_s != RESEQ_OK) return _s; \
+    } while (0)
+
+// Opt a kernel in to more than 48 KB of dynamic shared memory.  The attribute is per DEVICE, a
+// context may sit on any ordinal and contexts may be driven from several host threads: one bit
+// per device and call site, set after the attribute is.
+#define RSQ_OPT_IN_SMEM(ctx, kern, bytes)                                                               \
+    do {                                                                                                \
+        static std::atomic<uint64_t> _done[4];                                                          \
+        const unsigned _dev = static_cast<unsigned>((ctx)->device) & 255u;                              \
+        const uint64_t _bit = 1ull << (_dev & 63u);                                                     \
+        if (!(_done[_dev >> 6].load(std::memory_order_acquire) & _bit)) {                               \
+            RSQ_CUDA(cudaFuncSetAttribute((kern), cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                          static_cast<int>(bytes)));                                    \
+            _done[_dev >> 6].fetch_or(_bit, std::memory_order_release);                                 \
+        }                                                                                               \
     } while (0)
 
 }  // namespace rsq

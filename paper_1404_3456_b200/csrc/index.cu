@@ -832,6 +832,18 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
         return fail(RESEQ_INVALID_ARGUMENT, "an index needs at least one fragment");
     if (concat[n - 1] != 0)
         return fail(RESEQ_INVALID_ARGUMENT, "concat must end with the separator byte (sequence.hpp:60-62)");
+    // The reference can only build a fragment_set through make_fragment_set (sequence.hpp:103-124),
+    // which guarantees this layout; the C ABI takes raw arrays, so it is checked here, O(k) on the host:
+    // starts[0] == 0, strictly ascending, inside the text, every fragment non-empty and preceded by a
+    // separator.  (Separators INSIDE a fragment are not looked for: that is O(n).)
+    if (starts[0] != 0) return fail(RESEQ_INVALID_ARGUMENT, "starts[0] must be 0 (sequence.hpp:119)");
+    for (size_t i = 1; i < k; ++i) {
+        const uint64_t a = starts[i - 1], b = starts[i];
+        if (b >= n || b < a + 2 || concat[b - 1] != 0)
+            return fail(RESEQ_INVALID_ARGUMENT, "starts[" + std::to_string(i) + "] does not follow a separator-terminated, non-empty fragment (sequence.hpp:60-62,110)");
+    }
+    if (static_cast<uint64_t>(starts[k - 1]) + 2 > n)
+        return fail(RESEQ_INVALID_ARGUMENT, "the last fragment is empty (sequence.hpp:110)");
 
     auto* ix = new reseq_cuda_index();
     ix->ctx = ctx;

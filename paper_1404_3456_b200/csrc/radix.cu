@@ -68,11 +68,7 @@ static int launch_pass_kernel(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, 
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
     auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, HI>;
     const size_t smem = Cfg::kSmem + (EMIT::kActive ? sizeof(u32) * (kEmitCap + 2) : 0);
-    static bool configured = false;
-    if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = true;
-    }
+    RSQ_OPT_IN_SMEM(ctx, kern, smem);
     RSQ_CUDA(cudaMemsetAsync(lookback, 0, lookback_bytes_for<Cfg::kTile>(n), ctx->stream));
     const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
     RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL>()));

@@ -1395,11 +1395,7 @@ InversePlan make_inverse_plan(size_t n) {
 }
 
 int window_scatter_device(reseq_cuda_ctx* ctx, const u64* rec, size_t n, int win_bits, u32* rank) {
-    static bool configured = false;
-    if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(window_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        configured = true;
-    }
+    RSQ_OPT_IN_SMEM(ctx, window_scatter_kernel, 64 * 1024);
     const unsigned windows = static_cast<unsigned>((n + (size_t{1} << win_bits) - 1) >> win_bits);
     RSQ_LAUNCH_BEGIN(ctx, "window_scatter_kernel");
     window_scatter_kernel<<<windows, 512, sizeof(u32) << win_bits, ctx->stream>>>(rec, n, win_bits, rank);
@@ -1451,12 +1447,7 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     bool in_b = false;
     RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, m, pt, ws, hist_ready, 0, &in_b));
     st->sort_passes += pt.count;
-    static bool configured = false;
-    if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kRefSmem)));
-        configured = true;
-    }
+    RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<false>, kRefSmem);
     RSQ_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(u32), s));
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
@@ -1512,12 +1503,7 @@ int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sen
     accept_uniform_kernel<<<grid_for(ctx, m, 256, 4, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
                                                                        uncbits, tileflags);
     RSQ_LAUNCH_END(ctx);
-    static bool configured = false;
-    if (!configured) {
-        RSQ_CUDA(cudaFuncSetAttribute(refine_elems_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kRefSmem)));
-        configured = true;
-    }
+    RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<true>, kRefSmem);
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
     refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, sorted, m, sa_out, max_rounds, true,

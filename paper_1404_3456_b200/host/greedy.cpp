@@ -5,7 +5,7 @@
 // (O(k^3 L^2); the reference cannot run it beyond k ~ 10^3).  The north star keeps this step
 // on the host; what changes is the data structure.
 //
-// Equivalence argument (kept under differential test in tests/test_greedy.py):
+// Equivalence argument (kept under differential test in tests/test_greedy_host.py):
 //  * after absorb_contained (overlap.hpp:51-67) the fragment set is substring-free, and for
 //    substring-free sets the overlap of two merged chains equals the overlap of the last
 //    fragment of the left chain with the first fragment of the right chain (Blum, Jiang, Li,
@@ -99,6 +99,15 @@ extern "C" int reseq_greedy_superstring(const uint8_t* concat, size_t n, const u
     if (!concat || !starts || !ov || !ov->contained || !superstring || !order)
         return RESEQ_INVALID_ARGUMENT;
     if (min_overlap < 1) min_overlap = 1;
+    // raw arrays from the C ABI: the fragment_set layout (sequence.hpp:60-62) and the ids of the
+    // overlap list are checked before anything is indexed with them
+    if (n < 2 || starts[0] != 0 || static_cast<uint64_t>(starts[k - 1]) + 2 > n) return RESEQ_INVALID_ARGUMENT;
+    for (size_t i = 1; i < k; ++i)
+        if (static_cast<uint64_t>(starts[i]) < static_cast<uint64_t>(starts[i - 1]) + 2 || starts[i] >= n)
+            return RESEQ_INVALID_ARGUMENT;
+    if (ov->count && (!ov->i || !ov->j || !ov->w)) return RESEQ_INVALID_ARGUMENT;
+    for (uint64_t t = 0; t < ov->count; ++t)
+        if (ov->i[t] >= k || ov->j[t] >= k) return RESEQ_INVALID_ARGUMENT;
 
     std::vector<uint32_t> lens(k);
     for (size_t i = 0; i < k; ++i)

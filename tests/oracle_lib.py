@@ -54,6 +54,7 @@ class Oracle:
         L.orc_checksum_u32.restype = C.c_uint64
         L.orc_checksum_u32_from.restype = C.c_uint64
         L.orc_overlap_list.restype = C.c_uint64
+        L.orc_overlap_list_fast.restype = C.c_uint64
         L.orc_absorb_contained.restype = C.c_size_t
         L.orc_overlap_weight.restype = C.c_uint32
 
@@ -158,6 +159,25 @@ class Oracle:
             if m <= cap:
                 return oi[:m].copy(), oj[:m].copy(), ow[:m].copy()
             cap = m
+
+    def overlap_list_fast(self, text, starts, lens, min_ov=1, threads=8, cap=None):
+        """orc_overlap_list_fast: the same list by per-length hash tables over `threads` host threads
+        (BASELINE configs 1 and 2 at full size)."""
+        t, s, l = u8(text), u32(starts), u32(lens)
+        cap = int(cap or max(1 << 16, 40 * s.size))
+        while True:
+            oi, oj, ow = (np.empty(cap, np.uint32) for _ in range(3))
+            m = int(self.lib.orc_overlap_list_fast(vp(t), vp(s), vp(l), C.c_size_t(s.size), C.c_uint32(min_ov),
+                                                   C.c_uint(threads), vp(oi), vp(oj), vp(ow), C.c_uint64(cap)))
+            if m <= cap:
+                return oi[:m].copy(), oj[:m].copy(), ow[:m].copy()
+            cap = m
+
+    def make_read_text(self, G, L, k, genome_seed=1, read_seed=2):
+        out = np.empty(k * (L + 1), np.uint8)
+        assert self.lib.orc_make_read_text(C.c_size_t(G), C.c_size_t(L), C.c_size_t(k), C.c_uint64(genome_seed),
+                                           C.c_uint64(read_seed), vp(out)) == 0
+        return out
 
     def absorb_contained(self, text, starts, lens):
         t, s, l = u8(text), u32(starts), u32(lens)

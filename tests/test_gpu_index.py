@@ -207,6 +207,44 @@ def test_overlaps_at_config2_scale_properties(rq, ex):
     ix.close()
 
 
+def _uniform_contained(text, L):
+    """absorb_contained (overlap.hpp:51-67) restated for reads of ONE length, without a suffix array:
+    no read lies inside a longer one, so read i is dropped iff an equal read has a lower id."""
+    reads = np.ascontiguousarray(text.reshape(-1, L + 1)[:, :L])
+    rows = reads.view(np.dtype((np.void, L))).ravel()
+    _, first, inv = np.unique(rows, return_index=True, return_inverse=True)
+    return (first[inv.ravel()] != np.arange(rows.size)).astype(np.uint8)
+
+
+def _exact_overlaps(rq, ex, oracle, G, L, k, tau, threads):
+    text, starts = rq.synth_read_text(G, L, k)
+    fs = rq.fragment_set_from_text(text, starts)
+    ix = rq.FragmentIndex(fs, ex)
+    ov = ix.overlaps(tau)
+    ix.close()
+    wi, wj, ww = oracle.overlap_list_fast(text, starts, fs.lengths(), tau, threads=threads, cap=40 * k)
+    assert ov.i.size == wi.size, f"{ov.i.size} overlaps found, {wi.size} exist"
+    assert np.array_equal(ov.i, wi) and np.array_equal(ov.j, wj) and np.array_equal(ov.w, ww)
+    assert np.array_equal(ov.contained, _uniform_contained(text, L))
+    return ov
+
+
+def test_overlap_list_is_exact_at_config1_full_size(rq, ex, oracle):
+    """BASELINE config 1 at full size (100 000 reads of 100 bp, tau = 20): the device list equals, triple
+    for triple, the SA-free oracle (every (i, j) with overlap_weight >= 20 and its weight: completeness
+    AND maximality, overlap.hpp:16-45), and the containment flags equal absorb_contained (:51-67)."""
+    ov = _exact_overlaps(rq, ex, oracle, 1_000_000, 100, 100_000, 20, 16)
+    assert ov.queries == 100_000 * 81
+
+
+def test_overlap_list_is_exact_at_config2_full_size(rq, ex, oracle):
+    """BASELINE config 2 at full size (920 000 reads of 150 bp, 30x, tau = 20; 120.5 M queries): set
+    equality with the SA-free oracle -- no overlap missing, none spurious, every weight maximal -- and
+    the containment flags."""
+    ov = _exact_overlaps(rq, ex, oracle, 4_600_000, 150, 920_000, 20, 32)
+    assert ov.queries == 920_000 * 131 and ov.i.size > 20_000_000
+
+
 def test_reconstruction_at_config2_scale(rq, ex):
     """BASELINE config 2 end to end: device index + overlaps, host greedy merge
     (overlap.hpp:80-113 at scale).  With 30x error-free coverage of a random genome every merge is

@@ -254,6 +254,77 @@ def test_config2_full_size_proof(rq, ex, oracle):
     assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
 
 
+def test_config3_full_size_proof(rq, ex, oracle):
+    """BASELINE config 3 (one text of ~100 Mbp of reads: 10 Mbp genome, 150 bp, 10x; n = 100 666 566):
+    proof of equality with the reference order at full size."""
+    text, _ = rq.synth_read_text(10_000_000, 150, 666_666)
+    assert text.size == 100_666_566
+    got = rq.build_parallel(text, ex)
+    assert got.stats.init_symbols == 16 and got.stats.refined_global == 0
+    assert oracle.verify_sa(text, got.sa, threads=32) == 0
+    assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
+
+
+@pytest.mark.parametrize("option,value,name", [("sa_uniform", 0, "general DNA records (route ii)"),
+                                               ("sa_text_rounds", 0, "prefix doubling (route iii)")])
+def test_general_routes_at_config2_full_size(rq, oracle, option, value, name):
+    """The two general engines forced on BASELINE config 2's full text (n = 138 920 000): the route a
+    ragged read set takes (sa_uniform = 0) and the north star's prefix doubling (sa_text_rounds = 0),
+    each proved equal to the reference order."""
+    e = rq.Executor(0)
+    try:
+        e.set_option(option, value)
+        text, _ = rq.synth_read_text(4_600_000, 150, 920_000)
+        got = rq.build_parallel(text, e)
+        if option == "sa_uniform":
+            assert got.stats.init_symbols != 16 and got.stats.refined_global == 0, name
+        else:
+            assert got.stats.refined_tile == 0 and got.stats.refined_global > 0, name
+        assert oracle.verify_sa(text, got.sa, threads=32) == 0, name
+        assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32)), name
+    finally:
+        e.close()
+
+
+def _device_build_and_prove(rq, oracle, G, L, k, need_gib):
+    import torch
+    free, _total = torch.cuda.mem_get_info()
+    if free < need_gib * 2**30:
+        pytest.skip(f"needs ~{need_gib} GB of device memory")
+    text, _ = rq.synth_read_text(G, L, k)
+    n = int(text.size)
+    e = rq.Executor(0)
+    try:
+        d_text = torch.from_numpy(text).cuda()
+        d_sa = torch.empty(n, dtype=torch.int32, device="cuda")
+        d_rank = torch.empty(n, dtype=torch.int32, device="cuda")
+        st = rq.SaStats()
+        lib = rq._lib.load()
+        rq._lib.check(lib.reseq_cuda_build_sa_device(e.handle, C.c_void_p(d_text.data_ptr()), n,
+                                                     C.c_void_p(d_sa.data_ptr()), C.c_void_p(d_rank.data_ptr()), C.byref(st)))
+        e.synchronize()
+        assert st.init_symbols == 16 and st.refined_global == 0
+        chunk = 1 << 27
+        for b in range(0, n, chunk):
+            hi = min(n, b + chunk)
+            sa_c = d_sa[b:hi].to(torch.int64) & 0xFFFFFFFF
+            assert torch.equal(d_rank[sa_c].to(torch.int64) & 0xFFFFFFFF, torch.arange(b, hi, device="cuda", dtype=torch.int64))
+            del sa_c
+        sa = d_sa.cpu().numpy().view(np.uint32)
+        del d_sa, d_rank, d_text
+    finally:
+        e.close()
+        torch.cuda.empty_cache()
+    assert oracle.verify_sa(text, sa, threads=32) == 0
+    return n
+
+
+def test_config4_one_billion_suffixes(rq, oracle):
+    """BASELINE config 4 (100 Mbp genome, 150 bp, 10x; n = 1 006 666 566) on one B200 through the
+    device-resident entry point: proof of equality on the host, inverse checked on the device."""
+    assert _device_build_and_prove(rq, oracle, 100_000_000, 150, 6_666_666, 45) == 1_006_666_566
+
+
 def test_config5_three_billion_suffixes_beyond_the_reference_cap(rq, oracle):
     """BASELINE config 5 (300 Mbp genome, 150 bp, 10x; n = 3.02 G > 2^31 - 1, the reference's cap,
     suffix_array.hpp:64) on one B200 through the device-resident entry point: every index above 2^31

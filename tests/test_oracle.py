@@ -134,6 +134,44 @@ def test_golden_overlaps_and_greedy(oracle):
         assert list(sup) == c["superstring"] and order.tolist() == c["order"]
 
 
+def test_fast_overlap_oracle_equals_the_definitional_one(oracle, ref):
+    """orc_overlap_list_fast (the checker of the config-size GPU tests) against orc_overlap_list, the
+    dense graph restatement and -- where it was compiled -- the reference's build_overlap_graph
+    (overlap.hpp:26-45): golden instances, random read sets with repeats, duplicates, containments,
+    mixed lengths and periodic reads (several match lengths per pair), every threshold, 1..5 threads."""
+    for c in GOLDEN["overlap"]:
+        frags = [b(f) for f in c["fragments"]]
+        concat, starts, lens = concat_of(frags)
+        oi, oj, ow = oracle.overlap_list_fast(concat, starts, lens, 1, threads=3)
+        sparse = np.zeros((len(frags), len(frags)), np.uint32)
+        sparse[oi, oj] = ow
+        assert sparse.tolist() == c["weight"]
+    rng = np.random.default_rng(77)
+    for it in range(60):
+        alpha = [[65, 67, 71, 84], [65, 67], [65]][it % 3]
+        G = int(rng.integers(30, 400))
+        genome = rng.choice(alpha, G).astype(np.uint8)
+        frags = []
+        for _ in range(int(rng.integers(2, 60))):
+            ln = min(G, int(rng.integers(1, 40)))
+            s0 = int(rng.integers(0, G - ln + 1))
+            frags.append(bytes(genome[s0:s0 + ln]))
+        frags += frags[:2]                                  # duplicates
+        concat, starts, lens = concat_of(frags)
+        dense = oracle.overlap_graph(concat, starts, lens)
+        if ref is not None and it % 4 == 0:
+            assert np.array_equal(ref.overlap_graph(frags), dense)
+        for tau in (1, 2, 5, 20):
+            a = oracle.overlap_list(concat, starts, lens, tau)
+            f = oracle.overlap_list_fast(concat, starts, lens, tau, threads=1 + it % 5)
+            assert all(np.array_equal(x, y) for x, y in zip(a, f)), (frags, tau)
+            want = np.argwhere(dense >= tau)
+            assert np.array_equal(np.stack([f[0], f[1]], 1).astype(np.int64), want) and np.array_equal(f[2], dense[dense >= tau])
+    # the text generator used by bench.py's reference arm
+    if ref is not None:
+        assert np.array_equal(oracle.make_read_text(5000, 60, 300), ref.make_read_text(5000, 60, 300))
+
+
 # ---- the real reference, where it could be compiled -------------------------------------------
 
 def test_against_the_reference_itself(oracle, ref):
