@@ -87,7 +87,13 @@ size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
  *                     the packed text) the DNA paths run before handing over to prefix doubling;
  *                     0 forces pure prefix doubling; default 16
  *   "sa_shortcut"     0 switches off the sentinel-distance shortcut of the general DNA path
- *   "sort_cfg"        onesweep tile shape, 0 (default tuning) .. 9 */
+ *   "sort_cfg"        onesweep tile shape, 0 (default tuning) .. 9
+ *   "sa_speculate"    0: never start a build on the previous build's route (default 1: a context that
+ *                     has just built a uniform read set of n bytes queues the next n-byte build on the
+ *                     same route without a host round trip; the route's premises are re-checked on the
+ *                     device and a text of another kind is rebuilt the ordinary way)
+ *   "inverse_mode"    how rank = sa^-1 is computed above 2^22 suffixes: 0 two partition passes + a
+ *                     shared-memory window scatter, 1 one partition pass + an L2-window scatter */
 int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long value);
 /* Per-kernel device timing, measured with CUDA events recorded on the launching stream
  * around every launch while enabled.  reseq_cuda_ctx_profile(ctx, 1) clears and starts,
@@ -260,7 +266,7 @@ int reseq_cuda_index_locate_residuals(reseq_cuda_index* ix, const uint32_t* frag
  * patterns given as residuals (the assembler's use, assembler.hpp:74-78,117).  Results are
  * CSR: list i of each kind occupies [*_off[i], *_off[i+1]) of the malloc'ed id arrays
  * (each list ascending by id, fragment_index.hpp:105-107).  Free with
- * reseq_cuda_free_host(). */
+ * reseq_cuda_prefix_relations_free(). */
 typedef struct reseq_prefix_relations {
     size_t q;
     uint64_t *prefixes_off, *extensions_off, *exact_off; /* q+1 each */

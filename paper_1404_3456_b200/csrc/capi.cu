@@ -171,11 +171,14 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     }
     if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
     if (const char* e = std::getenv("RESEQ_INVERSE_LO_BITS")) ctx->opt_inverse_lo_bits = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_INVERSE_MODE")) ctx->opt_inverse_mode = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_LOOKBACK_PACK")) ctx->opt_lookback_pack = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_LOOKAHEAD")) {
         const int v = std::atoi(e);
         if (v >= 1 && v <= 8) ctx->opt_lookahead = v;
     }
     if (const char* e = std::getenv("RESEQ_SA_UNIFORM")) ctx->opt_uniform = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_SA_SPECULATE")) ctx->opt_speculate = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SHORTCUT")) ctx->opt_shortcut = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);
     *out = ctx;
@@ -225,6 +228,15 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     }
     if (std::strcmp(name, "sa_uniform") == 0) {
         ctx->opt_uniform = value != 0;
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "sa_speculate") == 0) {
+        ctx->opt_speculate = value != 0;
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "inverse_mode") == 0) {
+        if (value < 0 || value > 1) return fail(RESEQ_INVALID_ARGUMENT, "inverse_mode must be 0 or 1");
+        ctx->opt_inverse_mode = static_cast<int>(value);
         return RESEQ_OK;
     }
     if (std::strcmp(name, "sort_cfg") == 0) {
@@ -524,9 +536,11 @@ int reseq_cuda_build_sa(reseq_cuda_ctx* ctx, const uint8_t* text, size_t n, uint
     u32* d_rank = ctx->alloc<u32>(n);
     RSQ_CUDA(cudaMemcpyAsync(d_text, text, n, cudaMemcpyHostToDevice, ctx->stream));
     ctx->sa_host_dst = sa;   // copied out by sa_ready() as soon as it is final, under the inverse's kernels
+    ctx->sa_host_saved = sa;
     const int st = build_sa_device(ctx, d_text, n, d_sa, d_rank, stats);
     const bool sa_pending = ctx->sa_host_dst != nullptr;
     ctx->sa_host_dst = nullptr;
+    ctx->sa_host_saved = nullptr;
     if (st != RESEQ_OK) {
         cudaStreamSynchronize(ctx->copy_stream);
         return st;

@@ -63,11 +63,16 @@ struct reseq_cuda_ctx {
     int sm_count = rsq::kSmCount;
     uint64_t launches = 0;
     int opt_inverse_lo_bits = -1;  // extra partition bits before the inverse scatter (-1 = auto)
+    int opt_inverse_mode = 0;      // 0: two partition passes + shared-memory window; 1: one pass + L2-window scatter
     int opt_shortcut = 1;      // sentinel-distance shortcut in the refine kernel (tuning / tests)
     int opt_lookahead = 8;     // onesweep look-back descriptors in flight per digit (1..8)
     int opt_sort_cfg = 0;      // onesweep tile shape (0 = default tuning)
+    int opt_lookback_pack = 1; // two digits per look-back descriptor word when n < 2^30 (0: always one)
     int opt_uniform = 1;       // transposed-record path for uniform read sets (0: general paths only)
     int opt_text_rounds = 16;  // max text-window refinement rounds before prefix doubling takes over
+    int opt_speculate = 1;     // start on the previous build's route when the text length matches (verified on device)
+    size_t hint_n = 0;         // text length and period of the last build that finished on the uniform read-set route
+    uint32_t hint_period = 0;
 
     // Grow-only bump arena.  begin() rewinds it; alloc() carves 256-byte aligned
     // blocks.  If the arena is too small the whole block is re-allocated *before* any
@@ -81,6 +86,7 @@ struct reseq_cuda_ctx {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_event = nullptr;
     uint32_t* sa_host_dst = nullptr;   // set by reseq_cuda_build_sa for the duration of one build
+    uint32_t* sa_host_saved = nullptr; // the same pointer, kept so that a failed speculative route can copy again
     int sa_ready(const uint32_t* d_sa, size_t n) {
         if (!sa_host_dst) return RESEQ_OK;
         if (cudaEventRecord(copy_event, stream) != cudaSuccess || cudaStreamWaitEvent(copy_stream, copy_event, 0) != cudaSuccess ||
@@ -156,10 +162,27 @@ __device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
                  "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
+// 128-bit load served by L2 (never a stale L1 line): data published by another CTA behind a flag.
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
 __device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
     u64 v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ u32 ld_relaxed_u32(const u32* p) {
+    u32 v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(u32* p, u32 v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -27,14 +27,17 @@ template <> struct SortTuning<u32, true>  { static constexpr int kBlock = 384, k
 template <> struct SortTuning<u64, true>  { static constexpr int kBlock = 256, kItems = 16; };
 template <> struct SortTuning<u64, false> { static constexpr int kBlock = 384, kItems = 12; };
 
-// The smallest tile among the tunings bounds the look-back array.
+// The smallest tile among the tunings bounds the look-back arrays.
 static constexpr size_t kMinTile = 256 * 8;
+
+static size_t lookback_bytes(size_t tiles) {   // one 64-bit descriptor per (tile, digit) at most (DPW 1)
+    return reseq_cuda_ctx::padded(sizeof(u64) * tiles * kRadix);
+}
 
 size_t sort_workspace_bytes(size_t n) {
     const size_t tiles = (n + kMinTile - 1) / kMinTile + 1;
     return reseq_cuda_ctx::padded(sizeof(u32) * kMaxPasses * kRadix) * 2 +
-           reseq_cuda_ctx::padded(sizeof(u32) * kMaxPasses) +
-           reseq_cuda_ctx::padded(sizeof(u64) * tiles * kRadix);
+           reseq_cuda_ctx::padded(sizeof(u32) * kMaxPasses) + lookback_bytes(tiles);
 }
 
 int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws) {
@@ -42,8 +45,8 @@ int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws) {
     ws->hist = ctx->alloc<u32>(kMaxPasses * kRadix);
     ws->base = ctx->alloc<u32>(kMaxPasses * kRadix);
     ws->tickets = ctx->alloc<u32>(kMaxPasses);
-    ws->lookback = ctx->alloc<u64>(tiles * kRadix);
-    ws->lookback_bytes = sizeof(u64) * tiles * kRadix;
+    ws->lookback_bytes = lookback_bytes(tiles);
+    ws->lookback = ctx->alloc<u64>(ws->lookback_bytes / sizeof(u64));
     if (!ws->hist || !ws->base || !ws->tickets || !ws->lookback)
         return fail(RESEQ_OUT_OF_MEMORY, "sort workspace does not fit the reserved arena");
     return RESEQ_OK;
@@ -55,28 +58,35 @@ static const char* pass_name() {
                              : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys");
 }
 
-// Only the look-back words of the tiles a pass really has need clearing.
-template <int TILE>
-static size_t lookback_bytes_for(size_t n) {
-    return sizeof(u64) * ((n + TILE - 1) / TILE) * kRadix;
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT, bool HI, int DPW>
+static int launch_pass_dpw(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
+                           size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket,
+                           const EMIT& emit) {
+    using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
+    auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, HI, DPW>;
+    const size_t smem = Cfg::kSmem + (EMIT::kActive ? sizeof(u32) * (kEmitCap + 2) : 0);
+    RSQ_OPT_IN_SMEM(ctx, kern, smem);
+    const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
+    // only the descriptor words of the tiles this pass really has need clearing
+    RSQ_CUDA(cudaMemsetAsync(lookback, 0, sizeof(u64) * tiles * (kRadix / DPW), ctx->stream));
+    RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL>()));
+    kern<<<static_cast<unsigned>(tiles), BLOCK, smem, ctx->stream>>>(
+        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, emit);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
 }
 
 template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT, bool HI>
 static int launch_pass_kernel(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
                               size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket,
                               const EMIT& emit) {
-    using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
-    auto kern = onesweep_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, HI>;
-    const size_t smem = Cfg::kSmem + (EMIT::kActive ? sizeof(u32) * (kEmitCap + 2) : 0);
-    RSQ_OPT_IN_SMEM(ctx, kern, smem);
-    RSQ_CUDA(cudaMemsetAsync(lookback, 0, lookback_bytes_for<Cfg::kTile>(n), ctx->stream));
-    const size_t tiles = (n + Cfg::kTile - 1) / Cfg::kTile;
-    RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL>()));
-    kern<<<static_cast<unsigned>(tiles), BLOCK, smem, ctx->stream>>>(
-        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, ctx->opt_lookahead, emit);
-    RSQ_LAUNCH_END(ctx);
-    RSQ_CUDA(cudaGetLastError());
-    return RESEQ_OK;
+    // two digits per descriptor word while every count fits 30 bits (all configurations below 2^30 suffixes)
+    if (n < kPackedLimit && ctx->opt_lookback_pack != 0)
+        return launch_pass_dpw<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, HI, 2>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+                                                                          lookback, ticket, emit);
+    return launch_pass_dpw<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, HI, 1>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+                                                                      lookback, ticket, emit);
 }
 
 template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT>

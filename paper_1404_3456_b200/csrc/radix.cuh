@@ -6,8 +6,9 @@
 //   - each pass is ONE kernel: tiles are claimed through an atomic ticket, keys are
 //     ranked inside the warp by ballots (warp-aggregated: one shared-memory atomicAdd
 //     per distinct digit per warp step), tile totals are
-//     chained across tiles by decoupled look-back (one 64-bit descriptor per digit), the
-//     tile is re-ordered through shared memory so every digit's run leaves as one
+//     chained across tiles by decoupled look-back over PACKED descriptors (four 16-bit digit
+//     aggregates per 64-bit word, walked by 64 threads; inclusive prefixes behind one flag per
+//     tile), the tile is re-ordered through shared memory so every digit's run leaves as one
 //     contiguous, coalesced global store;
 //   - HBM traffic per pass = read keys(+payload) once, write keys(+payload) once.
 //
@@ -23,7 +24,23 @@ namespace rsq {
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kMaxPasses = 32;  // chunked_radix_sort with digit_bits = 1 needs 32
-constexpr int kLookahead = 8;   // most look-back descriptors read per round trip (tuning: ctx->opt_lookahead)
+constexpr int kLookahead = 8;   // look-back descriptors read per round trip by each walker thread
+
+// Look-back descriptors.  One 64-bit word is published by ONE relaxed store, so status and value are
+// seen together and no fence is needed.  DPW = digits per word:
+//   DPW 1: [status:2 | value:62]                      one digit, any n          (256 walker threads)
+//   DPW 2: two lanes of [status:2 | value:30]         two digits, n < 2^30      (128 walker threads)
+// status 0 = not published, 1 = the tile's own count (aggregate), 2 = inclusive prefix.
+// Why pack: with ~450 tiles in flight a walk meets the front of finished tiles ~27 tiles back (L2 round
+// trip / tile issue interval); at one digit per word the walk was 28 % of the pass's instructions and
+// more L2 sectors (51 M) than the key loads (35 M) (ncu source page of profiles/r1k_ncu_full_onesweep_kernel).
+// Measured and dropped: four 16-bit aggregates per word with the inclusive prefixes behind a per-tile
+// flag (two fences on the chain): the longer publish latency pushed the front further back and the
+// pass went from 0.76 to 1.11 ms (profiles/r2b_negative_results.md).
+constexpr u32 kLaneAggregate = 1u << 30;
+constexpr u32 kLaneInclusive = 2u << 30;
+constexpr u32 kLaneValueMask = (1u << 30) - 1u;
+constexpr u64 kPackedLimit = 1ull << 30;   // DPW 2 needs every digit count below this
 
 struct PassTable {
     int count;
@@ -156,15 +173,15 @@ struct OnesweepCfg {
     static constexpr int kWarps = BLOCK / 32;
     static constexpr int kTile = BLOCK * ITEMS;
     static constexpr size_t kSmem = sizeof(KeyT) * kTile + (HAS_VAL ? sizeof(u32) * kTile : 0) +
-                                    sizeof(u32) * (kWarps * kRadix + kRadix + 32 + 4);
+                                    sizeof(u32) * (kWarps * kRadix + 3 * kRadix + 32 + 4);   // + s_gofs, s_total, s_bin
 };
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT = EmitNone, bool HI = false>
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT = EmitNone, bool HI = false, int DPW = 1>
 __global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? (ITEMS <= 8 ? 6 : 4) : (BLOCK <= 384 ? (ITEMS <= 8 ? 4 : 3) : (BLOCK <= 512 ? (ITEMS <= 8 ? 3 : 2) : 1))))
 onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,
                 u32 mask, const u32* __restrict__ digit_base, u64* __restrict__ lookback,
-                u32* __restrict__ ticket, int lookahead, EMIT emit) {
+                u32* __restrict__ ticket, EMIT emit) {
     static_assert(BLOCK >= kRadix && BLOCK % 32 == 0, "one thread per digit is assumed");
     static_assert(!EMIT::kActive || sizeof(KeyT) == 8, "emit hooks look at 64-bit records");
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
@@ -176,7 +193,9 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     u32* s_vals = reinterpret_cast<u32*>(s_keys + TILE);
     u32* s_whist = s_vals + (HAS_VAL ? TILE : 0);  // [WARPS][256] counts -> tile slot of the warp's run
     u32* s_gofs = s_whist + WARPS * kRadix;        // [256] global index of tile slot 0 of the digit
-    u32* s_scan = s_gofs + kRadix;                 // [32] warp totals for the digit scan
+    u32* s_total = s_gofs + kRadix;                // [256] tile count of the digit
+    u32* s_bin = s_total + kRadix;                 // [256] first tile slot of the digit
+    u32* s_scan = s_bin + kRadix;                  // [32] warp totals for the digit scan
     u32* s_tile = s_scan + 32;
     u32* s_emit = s_tile + 4;                      // EMIT: [0] hits of this tile, [1] their base in the list, [2..] indices
 
@@ -251,12 +270,22 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     }
     __syncthreads();
 
-    // -- per digit: tile total, published at once as this tile's aggregate --------------
+    // -- per digit: tile total, published at once as this tile's aggregate (DPW 2: the even lane of
+    //    a digit pair stores the word for both) ---------------------------------------------------
+    constexpr int WALKERS = kRadix / DPW;
     u32 total = 0;
     if (tid < kRadix) {
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) total += s_whist[w * kRadix + tid];
-        if (tile > 0) st_relaxed_u64(lookback + static_cast<u64>(tile) * kRadix + tid, kDescAggregate | total);
+        s_total[tid] = total;
+        if constexpr (DPW == 1) {
+            if (tile > 0) st_relaxed_u64(lookback + static_cast<u64>(tile) * WALKERS + tid, kDescAggregate | total);
+        } else {
+            const u32 odd = __shfl_down_sync(0xffffffffu, total, 1);
+            if (tile > 0 && !(tid & 1))
+                st_relaxed_u64(lookback + static_cast<u64>(tile) * WALKERS + (tid >> 1),
+                               (static_cast<u64>(kLaneAggregate | odd) << 32) | (kLaneAggregate | total));
+        }
     }
 
     // -- exclusive scan of the 256 totals -> first tile slot of every digit; each warp's counter
@@ -269,12 +298,12 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     }
     if (lane == 31) s_scan[warp] = inc;
     __syncthreads();
-    u32 bin_start = 0;
     if (tid < kRadix) {
         u32 add = 0;
 #pragma unroll
         for (int w = 0; w < kRadix / 32; ++w) add += w < warp ? s_scan[w] : 0u;
-        bin_start = add + inc - total;
+        const u32 bin_start = add + inc - total;
+        s_bin[tid] = bin_start;
         u32 run = bin_start;
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) {
@@ -293,32 +322,51 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
         if (HAS_VAL) s_vals[pos] = val[j];
     }
 
-    // -- decoupled look-back over earlier tiles, one thread per digit.  It runs after the exchange
-    //    so that the predecessors have had the time of this tile's exchange to publish. ----------
-    if (tid < kRadix) {
-        u32 excl = 0;
+    // -- decoupled look-back over earlier tiles, one thread per descriptor word.  It runs after the
+    //    exchange so that the predecessors have had the time of this tile's exchange to publish.  The
+    //    walk meets the front of finished tiles about (L2 latency / tile issue interval) tiles back;
+    //    kLookahead descriptors are in flight at once. -------------------------------------------------
+    if (tid < WALKERS) {
+        u32 ex[DPW];
+#pragma unroll
+        for (int g = 0; g < DPW; ++g) ex[g] = 0;
         if (tile > 0) {
-            // The walk meets the front of finished tiles about (L2 latency / tile issue interval)
-            // tiles back; read one descriptor per round trip and it costs that many round trips
-            // (ncu: 40 % of the pass stalled here).  `lookahead` descriptors are in flight at once.
             long long t = static_cast<long long>(tile) - 1;
             for (bool done = false; !done;) {
                 u64 v[kLookahead];
 #pragma unroll
                 for (int w = 0; w < kLookahead; ++w)
-                    if (w < lookahead)
-                        v[w] = t - w >= 0 ? ld_relaxed_u64(lookback + static_cast<u64>(t - w) * kRadix + tid) : kDescInclusive;
+                    v[w] = t - w >= 0 ? ld_relaxed_u64(lookback + static_cast<u64>(t - w) * WALKERS + tid)
+                                      : (DPW == 1 ? kDescInclusive : (static_cast<u64>(kLaneInclusive) << 32) | kLaneInclusive);
 #pragma unroll
                 for (int w = 0; w < kLookahead; ++w) {
-                    if (done || w >= lookahead || (v[w] >> 62) == 0) break;  // not published yet: poll again from here
-                    excl += static_cast<u32>(v[w]);
+                    if (done) break;
+                    if constexpr (DPW == 1) {
+                        if ((v[w] >> 62) == 0) break;   // not published yet: poll again from here
+                        ex[0] += static_cast<u32>(v[w]);
+                        done = (v[w] & kDescInclusive) != 0;
+                    } else {
+                        const u32 l0 = static_cast<u32>(v[w]), l1 = static_cast<u32>(v[w] >> 32);
+                        if ((l0 >> 30) == 0) break;     // (both lanes are published by one store)
+                        ex[0] += l0 & kLaneValueMask;
+                        ex[1] += l1 & kLaneValueMask;
+                        done = (l0 & kLaneInclusive) != 0;
+                    }
                     --t;
-                    done = (v[w] & kDescInclusive) != 0;
                 }
             }
         }
-        st_relaxed_u64(lookback + static_cast<u64>(tile) * kRadix + tid, kDescInclusive | (excl + total));
-        s_gofs[tid] = digit_base[tid] + excl - bin_start;
+        if constexpr (DPW == 1) {
+            st_relaxed_u64(lookback + static_cast<u64>(tile) * WALKERS + tid, kDescInclusive | (ex[0] + s_total[tid]));
+            s_gofs[tid] = digit_base[tid] + ex[0] - s_bin[tid];
+        } else {
+            const uint2 t2 = *reinterpret_cast<const uint2*>(s_total + 2 * tid);
+            st_relaxed_u64(lookback + static_cast<u64>(tile) * WALKERS + tid,
+                           (static_cast<u64>(kLaneInclusive | (ex[1] + t2.y)) << 32) | (kLaneInclusive | (ex[0] + t2.x)));
+            const uint2 b2 = *reinterpret_cast<const uint2*>(digit_base + 2 * tid);
+            const uint2 s2 = *reinterpret_cast<const uint2*>(s_bin + 2 * tid);
+            *reinterpret_cast<uint2*>(s_gofs + 2 * tid) = make_uint2(b2.x + ex[0] - s2.x, b2.y + ex[1] - s2.y);
+        }
     }
     __syncthreads();
 

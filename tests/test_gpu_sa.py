@@ -223,6 +223,41 @@ def test_texts_that_only_look_uniform(rq, ex, oracle):
     assert got.stats.init_symbols == 11
 
 
+def test_speculative_route_is_verified_on_the_device(rq, oracle):
+    """A context starts the next build of a text of the same length on the previous build's route
+    without a host round trip (sa.cu build_sa_device); the route's premises are re-checked on the
+    device every time.  Same length, different kind of text -- ragged reads, a byte outside the
+    alphabet, other genome, shifted sentinels -- must still give the reference order, and the
+    route must come back for the next uniform text."""
+    e = rq.Executor(0)
+    try:
+        rng = np.random.default_rng(71)
+        L, k = 60, 3000
+        def uniform(seed):
+            g = np.random.default_rng(seed).choice([65, 67, 71, 84], 20_000).astype(np.uint8)
+            st = np.random.default_rng(seed + 1).integers(0, 20_000 - L, k)
+            return b"".join(bytes(g[x:x + L]) + b"\0" for x in st)
+        a = uniform(1)
+        n = len(a)
+        texts = [a, a, uniform(5)]
+        ragged = bytearray(uniform(9))
+        ragged[L] = 65; ragged[L - 7] = 0                     # one sentinel moved: k separators, not one per period
+        texts.append(bytes(ragged))
+        other = bytearray(uniform(11)); other[1234] = ord("N")  # not a DNA text
+        texts.append(bytes(other))
+        fewer = bytearray(uniform(13)); fewer[L] = 71         # k - 1 separators
+        texts.append(bytes(fewer))
+        texts += [uniform(17), bytes(rng.choice([65, 67], n).astype(np.uint8)), uniform(19)]
+        for t in texts:
+            assert len(t) == n
+            got = rq.build_parallel(t, e)
+            wsa, wrank = oracle.build_sa(t)
+            assert np.array_equal(got.sa, wsa) and np.array_equal(got.rank, wrank)
+        assert got.stats.init_symbols == 16
+    finally:
+        e.close()
+
+
 def test_reference_bench_input_fingerprint(rq, ex, oracle):
     """make_random_dna(1<<20, 1): checksum_u32(sa) == 7546189330682201289 (BASELINE.md section 2,
     the reference's own build_parallel and build_naive)."""
