@@ -217,6 +217,101 @@ def run_reference(args, text, read_len, workload):
     print(json.dumps(line))
 
 
+# B/suffix one launch of each kernel accounts for in the SURVEY 8(d) model.  The refine kernel
+# stands for ALL doubling rounds of the model (R16 * (44 + 24 P)): it reaches the same order by
+# fetching keys from the L2-resident packed text, so its figure can exceed the HBM peak -- its
+# real DRAM traffic is in `traffic` (ncu).  The partition passes + window scatter stand for the
+# model's inverse-permutation phase (8 B/suffix) and are listed with their own minimal traffic.
+KERNEL_MODEL_BYTES = {
+    "pack_dna_kernel": 1.375, "initkey_dna_kernel": 8.375, "initkey_bytes_kernel": 9.0,
+    "onesweep_u32_pairs": 16.0, "onesweep_u32_keys": 8.0, "onesweep_u64_pairs": 24.0,
+    "init_elems_kernel": 8.375, "onesweep_u64_keys": 16.0,
+    "refine_elems_kernel": 13.4, "window_scatter_kernel": 12.0, "inv_partition_sa": 12.0, "inv_partition_rec": 16.0,
+    "inv_partition_rec0": 16.0, "inv_partition_sa_val": 16.0,
+    "inverse_kernel": 8.0, "pair_key_kernel": 20.0, "rerank_kernel": 16.0, "hist_kernel": 4.0,
+    "gen_uniform_kernel": 8.25, "accept_uniform_kernel": 12.25,   # link / refine touch a few % of the suffixes: no figure
+    "owner_partition_kernel": 12.0, "owner_count_kernel": 4.0,
+}
+
+
+def ncu_sa_traffic(workload: str) -> dict:
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the SA kernels from the ncu --set full
+    captures under profiles/ (r2_ncu_sa_traffic.json: {workload: {kernel: bytes}})."""
+    p = ROOT / "profiles" / "r2_ncu_sa_traffic.json"
+    if p.exists():
+        try:
+            return {k: float(v) for k, v in json.loads(p.read_text()).get(workload, {}).items()}
+        except Exception:
+            pass
+    return {}
+
+
+def roofline_block(prof: dict, n: int, L: int, steps: int, ms_per_step: float, workload: str, n_kernel: int = None) -> dict:
+    """`prof` = {kernel: (launches, total ms)} over `steps` steps; n_kernel = suffixes one launch
+    processes when that is not n (a multi-GPU rank's bucket)."""
+    peak, peak_src = measured_peak()
+    per_suffix, P, R16 = bytes_alg_per_suffix(n, L)
+    nk = n_kernel or n
+    ncu_traffic = ncu_sa_traffic(workload)
+    kernels = {}
+    for kname, (cnt, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        b = KERNEL_MODEL_BYTES.get(kname)
+        avg = ms / cnt if cnt else None
+        ach = b * nk / (avg * 1e-3) / 1e9 if (b and avg) else None
+        kernels[kname] = {"ms_per_step": ms / steps, "launches_per_step": cnt / steps,
+                          "avg_launch_ms": avg, "alg_bytes_per_suffix": b,
+                          "achieved_gbs": ach, "frac": ach / peak if ach else None,
+                          "share_of_step": (ms / steps) / ms_per_step}
+    dom_name = next(iter(kernels)) if kernels else "none"
+    dom = kernels.get(dom_name, {})
+    kernel_ms = sum(v[1] for v in prof.values()) / steps
+    return {
+        "bound": "hbm", "kernel": dom_name, "achieved": dom.get("achieved_gbs"), "peak": peak, "unit": "GB/s",
+        "frac": dom.get("frac"), "traffic": ncu_traffic.get(dom_name),
+        "peak_source": peak_src,
+        "alg_bytes_per_launch": (dom.get("alg_bytes_per_suffix") or 0) * nk,
+        "launches_per_step": dom.get("launches_per_step"), "avg_launch_ms": dom.get("avg_launch_ms"),
+        "kernel_share_of_step": dom.get("share_of_step"),
+        "note": ("one 8-bit digit pass over 64-bit suffix records (read once, written once); the build runs 4 of them. "
+                 "build.frac compares the whole build with SURVEY 8(d)'s prefix-doubling byte model: the "
+                 "uniform read-set path replaces the model's doubling rounds by one verified overlap per read, so the "
+                 "build moves ~130 B/suffix and that fraction exceeds 1"),
+        "build": {"alg_bytes_per_suffix": per_suffix, "P": P, "R16": R16,
+                  "achieved_gbs": per_suffix * n / (ms_per_step * 1e-3) / 1e9,
+                  "frac": per_suffix * n / (ms_per_step * 1e-3) / 1e9 / peak},
+        "kernels": kernels,
+        "sum_kernel_ms_per_step": kernel_ms,
+    }
+
+
+def cpu_sa_baseline(text: np.ndarray, L: int) -> dict:
+    """The reference's build_parallel (all host threads) on a bounded prefix of `text`, plus its other
+    two routes to the same array on one thread."""
+    cpu_lib, kind = _load_cpu_lib()
+    cores = os.cpu_count() or 1
+    workers = cores if kind == "reference" else 1
+    probe = cpu_sample(text, L, 1 << 17)
+    t_probe = cpu_build(cpu_lib, kind, probe, workers)
+    sample = cpu_sample(text, L, int(min(1 << 22, max(1 << 17, probe.size * (15.0 / t_probe) ** (1 / 1.35)))))
+    dt = cpu_build(cpu_lib, kind, sample, workers)
+    also = None
+    if kind == "reference":   # SURVEY 8(d): the reference's other two ways to the same array, one thread each
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        tmp = np.empty(sample.size, np.uint32)
+        t0 = time.perf_counter()
+        cpu_lib.ref_build_naive(vp(sample), C.c_size_t(sample.size), vp(tmp), None)
+        t_naive = time.perf_counter() - t0
+        small = cpu_sample(text, L, 1 << 17)
+        t_one = cpu_build(cpu_lib, kind, small, 1)
+        also = {"build_naive_1_thread_msuffixes_per_s": sample.size / t_naive / 1e6,
+                "build_parallel_1_worker_msuffixes_per_s": small.size / t_one / 1e6,
+                "build_parallel_1_worker_sample_suffixes": int(small.size)}
+    return {"value": sample.size / dt / 1e6, "unit": UNIT, "cores": workers, "kind": kind, "also": also,
+            "sample": f"first {sample.size // (L + 1)} reads ({sample.size} suffixes) of the same text, 1 build, "
+                      f"{dt:.1f} s; reference build_parallel with executor{{workers={workers}}}" if kind == "reference"
+            else f"first {sample.size} suffixes, oracle port, 1 thread, {dt:.1f} s"}
+
+
 def ncu_overlap_traffic(workload: str) -> dict:
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the overlap kernels, from the ncu
     --set full captures committed under profiles/ (r2_ncu_overlap_traffic.json: {workload: {kernel: bytes}})."""
@@ -315,6 +410,8 @@ def main():
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # (the default workload stays config 2 for every N so that the driver's per-N values are comparable;
+        #  --workload c4 / c5 are the configurations the sharded build is meant for)
 
     if world > 1 or args.force_sharded:
         from paper_1404_3456_b200 import sharded
@@ -372,54 +469,7 @@ def main():
     # ---- roofline: per-kernel algorithmic bytes over live CUDA-event durations ----
     peak, peak_src = measured_peak()
     per_suffix, P, R16 = bytes_alg_per_suffix(n, L)
-    # B/suffix one launch of each kernel accounts for in the SURVEY 8(d) model.  The refine kernel
-    # stands for ALL doubling rounds of the model (R16 * (44 + 24 P)): it reaches the same order by
-    # fetching keys from the L2-resident packed text, so its figure can exceed the HBM peak -- its
-    # real DRAM traffic is in `traffic` (ncu).  The partition passes + window scatter stand for the
-    # model's inverse-permutation phase (8 B/suffix) and are listed with their own minimal traffic.
-    model = {
-        "pack_dna_kernel": 1.375, "initkey_dna_kernel": 8.375, "initkey_bytes_kernel": 9.0,
-        "onesweep_u32_pairs": 16.0, "onesweep_u32_keys": 8.0, "onesweep_u64_pairs": 24.0,
-        "init_elems_kernel": 8.375, "onesweep_u64_keys": 16.0,
-        "refine_elems_kernel": 13.4, "window_scatter_kernel": 12.0, "inv_partition_sa": 12.0, "inv_partition_rec": 16.0,
-        "inverse_kernel": 8.0, "pair_key_kernel": 20.0, "rerank_kernel": 16.0, "hist_kernel": 4.0,
-        "gen_uniform_kernel": 8.25, "accept_uniform_kernel": 12.25,   # link / refine touch a few % of the suffixes: no figure
-    }
-    # dram__bytes_read.sum + dram__bytes_write.sum per launch at config 2, ncu --set full captures under
-    # profiles/ (r1f): what the kernel really moved, next to the algorithmic figure above
-    ncu_traffic = {"onesweep_u64_keys": 2.253e9, "accept_uniform_kernel": 1.707e9, "inv_partition_rec": 2.177e9,
-                   "window_scatter_kernel": 1.636e9, "gen_uniform_kernel": 1.086e9}
-    if workload != "c2":
-        ncu_traffic = {}
-    kernels = {}
-    for kname, (cnt, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
-        b = model.get(kname)
-        avg = ms / cnt if cnt else None
-        ach = b * n / (avg * 1e-3) / 1e9 if (b and avg) else None
-        kernels[kname] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
-                          "avg_launch_ms": avg, "alg_bytes_per_suffix": b,
-                          "achieved_gbs": ach, "frac": ach / peak if ach else None,
-                          "share_of_step": (ms / args.steps) / ms_per_step}
-    dom_name = next(iter(kernels)) if kernels else "none"
-    dom = kernels.get(dom_name, {})
-    kernel_ms = sum(v[1] for v in prof.values()) / args.steps
-    roofline = {
-        "bound": "hbm", "kernel": dom_name, "achieved": dom.get("achieved_gbs"), "peak": peak, "unit": "GB/s",
-        "frac": dom.get("frac"), "traffic": ncu_traffic.get(dom_name),
-        "peak_source": peak_src,
-        "alg_bytes_per_launch": (dom.get("alg_bytes_per_suffix") or 0) * n,
-        "launches_per_step": dom.get("launches_per_step"), "avg_launch_ms": dom.get("avg_launch_ms"),
-        "kernel_share_of_step": dom.get("share_of_step"),
-        "note": ("one 8-bit digit pass over 64-bit suffix records (read once, written once); the build runs 4 of them. "
-                 "build.frac compares the whole build with SURVEY 8(d)'s prefix-doubling byte model (936 B/suffix): the "
-                 "uniform read-set path replaces the model's doubling rounds by one verified overlap per read, so the "
-                 "build moves ~140 B/suffix and that fraction exceeds 1"),
-        "build": {"alg_bytes_per_suffix": per_suffix, "P": P, "R16": R16,
-                  "achieved_gbs": per_suffix * n / (ms_per_step * 1e-3) / 1e9,
-                  "frac": per_suffix * n / (ms_per_step * 1e-3) / 1e9 / peak},
-        "kernels": kernels,
-        "sum_kernel_ms_per_step": kernel_ms,
-    }
+    roofline = roofline_block(prof, n, L, args.steps, ms_per_step, workload)
 
     # ---- e2e: host buffers through the C ABI -----------------------------------------------------
     h_sa = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -538,31 +588,7 @@ def main():
             overlap["cpu_baseline"] = cpu_query_baseline(G, L, k)
 
     # ---- CPU baseline -------------------------------------------------------------------------------
-    cpu = None
-    if not args.no_cpu:
-        cpu_lib, kind = _load_cpu_lib()
-        cores = os.cpu_count() or 1
-        workers = cores if kind == "reference" else 1
-        probe = cpu_sample(text, L, 1 << 17)
-        rate = probe.size / cpu_build(cpu_lib, kind, probe, workers)
-        sample = cpu_sample(text, L, int(min(1 << 20, max(1 << 17, rate * 15.0))))
-        dt = cpu_build(cpu_lib, kind, sample, workers)
-        also = None
-        if kind == "reference":   # the reference's other two ways to the same array, one thread each
-            vp = lambda a: a.ctypes.data_as(C.c_void_p)
-            tmp = np.empty(sample.size, np.uint32)
-            t0 = time.perf_counter()
-            cpu_lib.ref_build_naive(vp(sample), C.c_size_t(sample.size), vp(tmp), None)
-            t_naive = time.perf_counter() - t0
-            small = cpu_sample(text, L, 1 << 17)
-            t_one = cpu_build(cpu_lib, kind, small, 1)
-            also = {"build_naive_1_thread_msuffixes_per_s": sample.size / t_naive / 1e6,
-                    "build_parallel_1_worker_msuffixes_per_s": small.size / t_one / 1e6,
-                    "build_parallel_1_worker_sample_suffixes": int(small.size)}
-        cpu = {"value": sample.size / dt / 1e6, "unit": UNIT, "cores": workers, "kind": kind, "also": also,
-               "sample": f"first {sample.size // (L + 1)} reads ({sample.size} suffixes) of the same text, 1 build, "
-                         f"{dt:.1f} s; reference build_parallel with executor{{workers={workers}}}" if kind == "reference"
-               else f"first {sample.size} suffixes, oracle port, 1 thread, {dt:.1f} s"}
+    cpu = None if args.no_cpu else cpu_sa_baseline(text, L)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,

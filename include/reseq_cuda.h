@@ -216,6 +216,32 @@ int reseq_cuda_sa_shard_uniform_sort_link(reseq_cuda_sa_shard* shard, uint64_t* 
                                           uint8_t* d_cov);
 int reseq_cuda_sa_shard_uniform_finish(reseq_cuda_sa_shard* shard, const uint8_t* d_cov, uint32_t* d_sa_out,
                                        uint64_t* unfinished);
+/* Bucket-local record generation (no record travels: the text is replicated).
+ *   prefix_hist     d_hist[4096] (device, u32) = histogram of the 12-bit key prefix (6 bases, zero padded
+ *                   from the terminator on) over the suffixes of `unit_count` units from `unit_begin`:
+ *                   reads for a uniform read set, positions otherwise.  The ranks' histograms are summed
+ *                   (all-reduce) and the G - 1 splitters read off the cumulative counts.
+ *   bucket_size     *m = number of suffixes of the WHOLE text whose prefix lies in [prefix_lo, prefix_hi)
+ *                   (a count sweep over all suffix keys + one scan, kept on the shard)
+ *   bucket_records  writes those m records (same layouts as uniform_records / shard_records) in the
+ *                   order the stable digit passes start from: (terminator distance, position) for a
+ *                   uniform read set, position otherwise.  Must follow bucket_size on the same shard. */
+int reseq_cuda_sa_shard_prefix_hist(reseq_cuda_sa_shard* shard, uint64_t unit_begin, size_t unit_count,
+                                    uint32_t* d_hist);
+int reseq_cuda_sa_shard_bucket_size(reseq_cuda_sa_shard* shard, uint32_t prefix_lo, uint32_t prefix_hi, uint64_t* m);
+int reseq_cuda_sa_shard_bucket_records(reseq_cuda_sa_shard* shard, uint64_t* d_records);
+/* rank sharded by POSITION (suffix_array.hpp:118-122 without replicating the inverse): rank g owns the
+ * positions [floor(n g / G), floor(n (g+1) / G)).
+ *   rank_shard_partition  for a bucket of the suffix array (positions d_sa_bucket[0..m), global indices
+ *                         global_offset + i): d_records_out (m entries) = records
+ *                         (position - owner's base) << 32 | global index, grouped by owner;
+ *                         counts_out[g] (host, `world` entries) = records for owner g.  These go through
+ *                         ONE all-to-all.
+ *   rank_shard_finish     on the owner: `len` received records (a permutation of its slice; clobbered)
+ *                         -> d_rank_slice[p - base] = global index. */
+int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bucket, size_t m, uint64_t global_offset,
+                                    uint64_t n, int world, uint64_t* d_records_out, uint64_t* counts_out);
+int reseq_cuda_rank_shard_finish(reseq_cuda_ctx* ctx, uint64_t* d_records, size_t len, uint32_t* d_rank_slice);
 /* d_rank[d_sa[i]] = i (suffix_array.hpp:118-122). */
 int reseq_cuda_inverse_device(reseq_cuda_ctx* ctx, const uint32_t* d_sa, size_t n, uint32_t* d_rank);
 

@@ -106,6 +106,11 @@ SIGNATURES = {
     "reseq_cuda_sa_shard_uniform_sort_link": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
     "reseq_cuda_sa_shard_uniform_finish": (C.c_int, [_vp, _vp, _vp, _u64p]),
     "reseq_cuda_inverse_device": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
+    "reseq_cuda_sa_shard_prefix_hist": (C.c_int, [_vp, C.c_uint64, C.c_size_t, _vp]),
+    "reseq_cuda_sa_shard_bucket_size": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _u64p]),
+    "reseq_cuda_sa_shard_bucket_records": (C.c_int, [_vp, _vp]),
+    "reseq_cuda_rank_shard_partition": (C.c_int, [_vp, _vp, C.c_size_t, C.c_uint64, C.c_uint64, C.c_int, _vp, _u64p]),
+    "reseq_cuda_rank_shard_finish": (C.c_int, [_vp, _vp, C.c_size_t, _vp]),
     "reseq_cuda_checksum_u32_device": (C.c_int, [_vp, _vp, C.c_size_t, _u64p]),
     "reseq_cuda_index_create": (C.c_int, [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(_vp)]),
     "reseq_cuda_index_destroy": (None, [_vp]),

@@ -393,6 +393,40 @@ static_assert(2 * kTdMax + 1 + 2 * kElemK < kOrdNone && 2 * (kDistCap + kElemK) 
 // Records of the `count` suffixes starting at text position pos0 (the whole text: pos0 = 0,
 // count = n; a multi-GPU rank keys only its slice), plus the digit histograms of the three sort
 // passes.
+// The record of the suffix at `pos` (layout above).
+__device__ __forceinline__ u64 elem_of(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n, u64 pos) {
+    const u32 bases = static_cast<u32>(base_window(packed, pos) >> 40);   // 12 bases
+    // distance to the first sentinel at or after pos, looking 256 positions ahead
+    u32 t = 256;
+#pragma unroll 1
+    for (u32 c0 = 0; c0 < 256; c0 += 64) {
+        const u64 w = sent_window(sent, pos + c0);
+        if (w) {
+            t = c0 + static_cast<u32>(__clzll(w));
+            break;
+        }
+    }
+    const u64 rem = n - pos;  // >= 1
+    u32 tt, kind;              // symbols before the terminator (256 = not within reach), its kind
+    if (t < 256 && t < rem) { tt = t; kind = 1; }
+    else if (rem <= 256) { tt = static_cast<u32>(rem); kind = 0; }
+    else { tt = 256; kind = 1; }
+    const u32 kept = tt >= 12 ? bases : bases & ~((1u << (24 - 2 * tt)) - 1u);   // zero padded
+    u32 key, p;
+    if (tt <= kElemEsc) {
+        key = ((kept >> 8) << 8) | (2 * tt + kind);
+        p = 2 * tt + kind;
+    } else {
+        const u32 b23 = kept >> 1;   // bases 0..10 and the upper bit of base 11
+        key = ((b23 >> 7) << 8) | kElemEscBit | (b23 & 0x7fu);
+        if (tt < kElemK) p = 2 * tt + kind;
+        else if (tt == 256) p = kPFar;
+        else if (kind == 0) p = kPEot;
+        else p = tt + kElemK <= kPMaxNear ? tt + kElemK : kPFar;
+    }
+    return (static_cast<u64>(key) << kElemKeyShift) | (static_cast<u64>(p) << 32) | (pos & 0xffffffffu);
+}
+
 __global__ void __launch_bounds__(256)
 init_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n, u64 pos0, u64 count,
                   u64* __restrict__ elems, u32* __restrict__ g_hist) {
@@ -401,37 +435,9 @@ init_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, 
     __syncthreads();
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < count; idx += stride) {
-        const u64 pos = pos0 + idx;
-        const u32 bases = static_cast<u32>(base_window(packed, pos) >> 40);   // 12 bases
-        // distance to the first sentinel at or after pos, looking 256 positions ahead
-        u32 t = 256;
-#pragma unroll 1
-        for (u32 c0 = 0; c0 < 256; c0 += 64) {
-            const u64 w = sent_window(sent, pos + c0);
-            if (w) {
-                t = c0 + static_cast<u32>(__clzll(w));
-                break;
-            }
-        }
-        const u64 rem = n - pos;  // >= 1
-        u32 tt, kind;              // symbols before the terminator (256 = not within reach), its kind
-        if (t < 256 && t < rem) { tt = t; kind = 1; }
-        else if (rem <= 256) { tt = static_cast<u32>(rem); kind = 0; }
-        else { tt = 256; kind = 1; }
-        const u32 kept = tt >= 12 ? bases : bases & ~((1u << (24 - 2 * tt)) - 1u);   // zero padded
-        u32 key, p;
-        if (tt <= kElemEsc) {
-            key = ((kept >> 8) << 8) | (2 * tt + kind);
-            p = 2 * tt + kind;
-        } else {
-            const u32 b23 = kept >> 1;   // bases 0..10 and the upper bit of base 11
-            key = ((b23 >> 7) << 8) | kElemEscBit | (b23 & 0x7fu);
-            if (tt < kElemK) p = 2 * tt + kind;
-            else if (tt == 256) p = kPFar;
-            else if (kind == 0) p = kPEot;
-            else p = tt + kElemK <= kPMaxNear ? tt + kElemK : kPFar;
-        }
-        elems[idx] = (static_cast<u64>(key) << kElemKeyShift) | (static_cast<u64>(p) << 32) | (pos & 0xffffffffu);
+        const u64 e = elem_of(packed, sent, n, pos0 + idx);
+        const u32 key = static_cast<u32>(e >> kElemKeyShift);
+        elems[idx] = e;
         atomicAdd(&s_hist[key & 0xffu], 1u);
         atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
         atomicAdd(&s_hist[2 * kRadix + (key >> 16)], 1u);
@@ -1229,7 +1235,7 @@ window_scatter_kernel(const u64* __restrict__ rec, u64 n, int win_bits, u32* __r
 // shared-memory wavefronts (the SM-to-HBM ratio is half an A100's), which is what this sheds.
 //
 // kIpSa: element i of the input is (sa[i] << 32) | i.  kIpRec: records of the previous pass.
-enum : int { kIpSa = 1, kIpRec = 2 };
+enum : int { kIpSa = 1, kIpRec = 2, kIpRec0 = 3 };   // kIpRec0: records in no particular order (first pass of a slice)
 constexpr int kIpBlock = 512;
 constexpr int kIpItems = 8;
 constexpr int kIpTile = kIpBlock * kIpItems;
@@ -1269,7 +1275,7 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
     for (u32 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const u64 tile_base = static_cast<u64>(tile) * kIpTile;
         const u32 valid = static_cast<u32>(n - tile_base < static_cast<u64>(kIpTile) ? n - tile_base : kIpTile);
-        const u32 bin0 = MODE == kIpRec ? static_cast<u32>(tile_base >> prev_shift) << (prev_shift - shift) : 0u;
+        const u32 bin0 = MODE == kIpRec ? static_cast<u32>(tile_base >> prev_shift) << (prev_shift - shift) : 0u;   // kIpSa, kIpRec0: 0
         u32 slot[kIpItems];
 #pragma unroll
         for (int j = 0; j < kIpItems; ++j) {
@@ -1385,6 +1391,331 @@ pair_key_kernel(const u32* __restrict__ sa, const u32* __restrict__ head_of,
     __syncthreads();
     hist_flush(s_hist, g_hist, pt.count);
 }
+
+// ---- multi-GPU building blocks: a rank makes the records of ITS bucket straight from the
+//      replicated packed text -----------------------------------------------------------------
+// Sample sort needs every suffix record on the rank whose splitter range holds its key.  The text is
+// replicated (n/4 bytes packed), so no record has to travel: each rank walks all suffix keys and KEEPS
+// those whose 12-bit key prefix (6 bases, zero padded from the terminator on -- the top of both record
+// kinds' keys) lies in [plo, phi).  What it keeps must come out in the order the stable digit passes
+// start from: (terminator distance, position) for uniform read sets, position for general records.
+// That is a stream compaction in that order: a count sweep, one scan of the counts, a write sweep.
+constexpr int kShPrefixBits = 12;
+constexpr int kShReads = 256;      // uniform: reads per CTA; thread = read
+constexpr int kShTile = 2048;      // general: positions per CTA; thread = 8 consecutive positions
+
+// Calls f(t, key32) for every suffix of the read whose first base is bit `bit0` of the staged words,
+// t = period - 1 down to 0 (offset 0 up to the sentinel).  key32 = its first 16 bases, zero padded
+// from the sentinel on.  Trip counts are uniform across a warp (f may vote).
+template <class F>
+__device__ __forceinline__ void for_each_suffix_of_read(const u64* __restrict__ s_w, u32 bit0, u32 period, F f) {
+    for (u32 o = 0; o < period; ++o) {
+        const u32 t = period - 1 - o;
+        const u32 bit = bit0 + 2 * o;
+        const u32 wi = bit >> 6, sh = bit & 63;
+        const u64 hi = s_w[wi], lo = s_w[wi + 1];
+        const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+        u32 key = static_cast<u32>(win >> 32);
+        if (t < static_cast<u32>(kUniK)) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;
+        f(t, key);
+    }
+}
+
+// Stages the packed words of reads [r0, r0 + nr) of a uniform read set; returns the bit offset of
+// read r0's first base inside the staged words.
+__device__ __forceinline__ u32 stage_reads(const u64* __restrict__ packed, u64* __restrict__ s_w, u64 r0, u32 nr, u32 period) {
+    const u64 base0 = r0 * period;
+    const u64 w0 = base0 >> 5;
+    const u32 nw = static_cast<u32>(((base0 + static_cast<u64>(nr) * period + 31) >> 5) - w0) + 2;   // the packed array is padded
+    for (u32 i = threadIdx.x; i < nw; i += blockDim.x) s_w[i] = packed[w0 + i];
+    return 2 * static_cast<u32>(base0 & 31);
+}
+
+// Histogram of the 12-bit key prefix over the suffixes of reads [read0, read0 + count).
+__global__ void __launch_bounds__(kShReads)
+shard_hist_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0, u64 count, u32* __restrict__ g_hist) {
+    __shared__ u64 s_w[kShReads * kUniMaxPeriod / 32 + 4];
+    __shared__ u32 s_hist[1 << kShPrefixBits];
+    for (int i = threadIdx.x; i < (1 << kShPrefixBits); i += blockDim.x) s_hist[i] = 0;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
+    const u32 nr = static_cast<u32>(count - r0 < kShReads ? count - r0 : kShReads);
+    const u32 bit0 = stage_reads(packed, s_w, read0 + r0, nr, period);
+    __syncthreads();
+    const bool in = threadIdx.x < nr;
+    for_each_suffix_of_read(s_w, bit0 + (in ? 2 * threadIdx.x * period : 0u), period, [&](u32, u32 key) {
+        if (in) atomicAdd(&s_hist[key >> (32 - kShPrefixBits)], 1u);
+    });
+    __syncthreads();
+    for (int i = threadIdx.x; i < (1 << kShPrefixBits); i += blockDim.x)
+        if (s_hist[i]) atomicAdd(g_hist + i, s_hist[i]);
+}
+
+// counts[t * tiles + tile] = suffixes with t symbols before their sentinel, of the reads of `tile`,
+// whose key prefix lies in [plo, phi): the flattened array scans into slot bases in (t, read) order.
+__global__ void __launch_bounds__(kShReads)
+shard_count_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 plo, u32 phi, u32 tiles,
+                           u32* __restrict__ counts) {
+    __shared__ u64 s_w[kShReads * kUniMaxPeriod / 32 + 4];
+    __shared__ u32 s_cnt[kUniMaxPeriod + 1];
+    for (int i = threadIdx.x; i <= static_cast<int>(kUniMaxPeriod); i += blockDim.x) s_cnt[i] = 0;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
+    const u32 nr = static_cast<u32>(k - r0 < kShReads ? k - r0 : kShReads);
+    const u32 bit0 = stage_reads(packed, s_w, r0, nr, period);
+    __syncthreads();
+    const bool in = threadIdx.x < nr;
+    for_each_suffix_of_read(s_w, bit0 + (in ? 2 * threadIdx.x * period : 0u), period, [&](u32 t, u32 key) {
+        const u32 pre = key >> (32 - kShPrefixBits);
+        const unsigned b = __ballot_sync(0xffffffffu, in && pre >= plo && pre < phi);
+        if (b && lane_id() == 0) atomicAdd(&s_cnt[t], __popc(b));
+    });
+    __syncthreads();
+    for (u32 t = threadIdx.x; t < period; t += blockDim.x) counts[static_cast<u64>(t) * tiles + blockIdx.x] = s_cnt[t];
+}
+
+// Writes the kept records key32 << 32 | position at offsets[t * tiles + tile] + (rank of the read
+// among the tile's kept reads at this t): the bucket comes out in (t, position) order.
+__global__ void __launch_bounds__(kShReads)
+shard_write_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 plo, u32 phi, u32 tiles,
+                           const u32* __restrict__ offsets, u64* __restrict__ out, u32* __restrict__ g_hist) {
+    __shared__ u64 s_w[kShReads * kUniMaxPeriod / 32 + 4];
+    __shared__ unsigned short s_wcnt[kShReads / 32][kUniMaxPeriod + 1];   // kept per (warp, t), then exclusive over warps
+    __shared__ u32 s_hist[4 * kRadix];                                    // digit histograms of the bucket's four sort passes
+    for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
+    const u32 nr = static_cast<u32>(k - r0 < kShReads ? k - r0 : kShReads);
+    const u32 bit0 = stage_reads(packed, s_w, r0, nr, period);
+    __syncthreads();
+    const bool in = threadIdx.x < nr;
+    const int warp = threadIdx.x >> 5;
+    const u32 my_bit0 = bit0 + (in ? 2 * threadIdx.x * period : 0u);   // (idle threads walk read 0: staged words only)
+    for_each_suffix_of_read(s_w, my_bit0, period, [&](u32 t, u32 key) {
+        const u32 pre = key >> (32 - kShPrefixBits);
+        const unsigned b = __ballot_sync(0xffffffffu, in && pre >= plo && pre < phi);
+        if (lane_id() == 0) s_wcnt[warp][t] = static_cast<unsigned short>(__popc(b));
+    });
+    __syncthreads();
+    for (u32 t = threadIdx.x; t < period; t += blockDim.x) {
+        u32 run = 0;
+        for (int w = 0; w < kShReads / 32; ++w) {
+            const u32 c = s_wcnt[w][t];
+            s_wcnt[w][t] = static_cast<unsigned short>(run);
+            run += c;
+        }
+    }
+    __syncthreads();
+    const u64 pos0 = (r0 + threadIdx.x) * period;
+    for_each_suffix_of_read(s_w, my_bit0, period, [&](u32 t, u32 key) {
+        const u32 pre = key >> (32 - kShPrefixBits);
+        const bool keep = in && pre >= plo && pre < phi;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const u64 slot = static_cast<u64>(offsets[static_cast<u64>(t) * tiles + blockIdx.x]) + s_wcnt[warp][t] +
+                             __popc(b & lanemask_lt());
+            out[slot] = (static_cast<u64>(key) << 32) | (pos0 + (period - 1 - t));
+            atomicAdd(&s_hist[key & 0xffu], 1u);
+            atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
+            atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
+            atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
+        }
+    });
+    __syncthreads();
+    hist_flush(s_hist, g_hist, 4);
+}
+
+// The general records (elem_of): prefix = the first 6 bases of the 24-bit key.
+__device__ __forceinline__ u32 elem_prefix(u64 e) { return static_cast<u32>(e >> (kElemKeyShift + 24 - kShPrefixBits)); }
+
+__global__ void __launch_bounds__(256)
+shard_hist_general_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n, u64 pos0, u64 count,
+                          u32* __restrict__ g_hist) {
+    __shared__ u32 s_hist[1 << kShPrefixBits];
+    for (int i = threadIdx.x; i < (1 << kShPrefixBits); i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < count; idx += stride)
+        atomicAdd(&s_hist[elem_prefix(elem_of(packed, sent, n, pos0 + idx))], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < (1 << kShPrefixBits); i += blockDim.x)
+        if (s_hist[i]) atomicAdd(g_hist + i, s_hist[i]);
+}
+
+// WRITE = false: counts[tile] = kept positions of the tile; true: the kept records at offsets[tile] on,
+// in position order.
+template <bool WRITE>
+__global__ void __launch_bounds__(256)
+shard_general_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n, u32 plo, u32 phi,
+                     u32* __restrict__ counts, const u32* __restrict__ offsets, u64* __restrict__ out,
+                     u32* __restrict__ g_hist) {
+    __shared__ u32 s_warp[8];
+    __shared__ u32 s_hist[WRITE ? 3 * kRadix : 1];
+    if constexpr (WRITE) {
+        for (int i = threadIdx.x; i < 3 * kRadix; i += blockDim.x) s_hist[i] = 0;
+    }
+    constexpr int kPer = kShTile / 256;
+    const u64 p0 = static_cast<u64>(blockIdx.x) * kShTile + static_cast<u64>(threadIdx.x) * kPer;
+    u64 e[kPer];
+    u32 mine = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        e[j] = 0;
+        bool keep = false;
+        if (p0 + j < n) {
+            e[j] = elem_of(packed, sent, n, p0 + j);
+            const u32 pre = elem_prefix(e[j]);
+            keep = pre >= plo && pre < phi;
+        }
+        if (!keep) e[j] = ~0ull;   // (no record is all ones: its position would be 2^32 - 1 > the largest text)
+        mine += keep;
+    }
+    u32 inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (static_cast<int>(lane_id()) >= o) inc += t;
+    }
+    if (lane_id() == 31) s_warp[threadIdx.x >> 5] = inc;
+    __syncthreads();
+    u32 before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        before += w < static_cast<int>(threadIdx.x >> 5) ? s_warp[w] : 0u;
+        total += s_warp[w];
+    }
+    if constexpr (!WRITE) {
+        if (threadIdx.x == 0) counts[blockIdx.x] = total;
+    } else {
+        u64 slot = static_cast<u64>(offsets[blockIdx.x]) + before + inc - mine;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j)
+            if (e[j] != ~0ull) {
+                out[slot++] = e[j];
+                const u32 key = static_cast<u32>(e[j] >> kElemKeyShift);
+                atomicAdd(&s_hist[key & 0xffu], 1u);
+                atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
+                atomicAdd(&s_hist[2 * kRadix + (key >> 16)], 1u);
+            }
+        __syncthreads();
+        hist_flush(s_hist, g_hist, 3);
+    }
+}
+
+// ---- rank sharded by position: the second exchange ---------------------------------------------------
+// A rank holds a bucket of the suffix array: positions sa[i], global indices offset + i.  Position p
+// belongs to the rank g with base(g) <= p < base(g + 1), base(g) = floor(n g / G).  Its record
+// (p - base(g)) << 32 | (offset + i) goes to g; there the records are a permutation of the slice and
+// inverse_from_records turns them into the slice of `rank`.
+__device__ __forceinline__ u32 owner_of(u64 p, u64 n, u32 G, u64* base) {
+    u32 g = static_cast<u32>((p * G) / n);
+    if (g >= G) g = G - 1;
+    while (g + 1 < G && (n * (g + 1)) / G <= p) ++g;
+    while (g > 0 && (n * g) / G > p) --g;
+    *base = (n * g) / G;
+    return g;
+}
+
+// Bins = owner x 64 sub-ranges of the owner's slice: the sub-bins only spread the shared-memory
+// atomics (and leave every owner's group roughly position-ordered); the exchange sends whole owners.
+constexpr int kOwnSub = 64;
+constexpr int kOwnBlock = 512, kOwnItems = 8, kOwnTile = kOwnBlock * kOwnItems;
+__device__ __forceinline__ u32 owner_bin(u64 p, u64 n, u32 G, u64* rel) {
+    u64 base;
+    const u32 g = owner_of(p, n, G, &base);
+    const u64 len = (n * (g + 1)) / G - base;
+    *rel = p - base;
+    u32 sub = static_cast<u32>((*rel * kOwnSub) / len);
+    return g * kOwnSub + (sub < kOwnSub ? sub : kOwnSub - 1);
+}
+
+__global__ void __launch_bounds__(256)
+owner_count_kernel(const u32* __restrict__ sa, u64 m, u64 n, u32 G, u32* __restrict__ counts) {
+    __shared__ u32 s_cnt[16 * kOwnSub];
+    const u32 bins = G * kOwnSub;
+    for (u32 b = threadIdx.x; b < bins; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+        u64 rel;
+        atomicAdd(&s_cnt[owner_bin(sa[i], n, G, &rel)], 1u);
+    }
+    __syncthreads();
+    for (u32 b = threadIdx.x; b < bins; b += blockDim.x)
+        if (s_cnt[b]) atomicAdd(counts + b, s_cnt[b]);
+}
+
+// One lean partition pass (see inv_partition_persistent_kernel): a record takes its slot in the tile's bin
+// from one shared-memory atomicAdd, a bin claims its stretch with one global atomicAdd on a counter that
+// starts at the bin's base, the tile leaves through shared memory as one contiguous run per bin.
+__global__ void __launch_bounds__(kOwnBlock, 2)
+owner_partition_kernel(const u32* __restrict__ sa, u64 m, u64 n, u32 G, u64 offset, u32* __restrict__ claim,
+                       u64* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char own_smem[];
+    u64* s_rec = reinterpret_cast<u64*>(own_smem);                                  // [tile] records, bin-sorted
+    u32* s_cnt = reinterpret_cast<u32*>(s_rec + kOwnTile);                          // [1024]
+    u32* s_ofs = s_cnt + 16 * kOwnSub;                                              // [1024]
+    u32* s_gdst = s_ofs + 16 * kOwnSub;                                             // [1024]
+    u32* s_warp = s_gdst + 16 * kOwnSub;                                            // [16]
+    unsigned short* s_binof = reinterpret_cast<unsigned short*>(s_warp + kOwnBlock / 32);   // [tile] bin of the record in that slot
+    const int tid = threadIdx.x;
+    const unsigned lane = lane_id();
+    const int bins = static_cast<int>(G) * kOwnSub;
+    for (int b = tid; b < bins; b += kOwnBlock) s_cnt[b] = 0;
+    __syncthreads();
+    const u64 tb = static_cast<u64>(blockIdx.x) * kOwnTile;
+    const u32 valid = static_cast<u32>(m - tb < static_cast<u64>(kOwnTile) ? m - tb : kOwnTile);
+    u64 rec[kOwnItems];
+    u32 slot[kOwnItems], bin[kOwnItems];
+#pragma unroll
+    for (int j = 0; j < kOwnItems; ++j) {
+        const u32 li = static_cast<u32>(j) * kOwnBlock + tid;
+        slot[j] = 0;
+        bin[j] = 0;
+        rec[j] = 0;
+        if (li < valid) {
+            u64 rel;
+            bin[j] = owner_bin(sa[tb + li], n, G, &rel);
+            rec[j] = (rel << 32) | ((offset + tb + li) & 0xffffffffu);
+            slot[j] = atomicAdd(&s_cnt[bin[j]], 1u);
+        }
+    }
+    __syncthreads();
+    // two bins per thread (bins <= 1024 = 2 * block): counts, claims, exclusive scan
+    const int b0 = 2 * tid, b1 = 2 * tid + 1;
+    const u32 c0 = b0 < bins ? s_cnt[b0] : 0u, c1 = b1 < bins ? s_cnt[b1] : 0u;
+    u32 g0 = 0, g1 = 0;
+    if (c0) g0 = atomicAdd(claim + b0, c0);
+    if (c1) g1 = atomicAdd(claim + b1, c1);
+    u32 inc = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (static_cast<int>(lane) >= o) inc += t;
+    }
+    if (lane == 31) s_warp[tid >> 5] = inc;
+    __syncthreads();
+    u32 before = 0;
+#pragma unroll
+    for (int w = 0; w < kOwnBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
+    const u32 excl = before + inc - (c0 + c1);
+    if (b0 < bins) { s_ofs[b0] = excl; s_gdst[b0] = g0 - excl; }
+    if (b1 < bins) { s_ofs[b1] = excl + c0; s_gdst[b1] = g1 - (excl + c0); }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kOwnItems; ++j) {
+        const u32 li = static_cast<u32>(j) * kOwnBlock + tid;
+        if (li < valid) {
+            const u32 at = s_ofs[bin[j]] + slot[j];
+            s_rec[at] = rec[j];
+            s_binof[at] = static_cast<unsigned short>(bin[j]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kOwnItems; ++j) {
+        const u32 pidx = static_cast<u32>(j) * kOwnBlock + tid;
+        if (pidx < valid) out[static_cast<u64>(s_gdst[s_binof[pidx]]) + pidx] = s_rec[pidx];
+    }
+}
+constexpr size_t kOwnSmem = sizeof(u64) * kOwnTile + sizeof(u32) * (3 * 16 * kOwnSub + kOwnBlock / 32) + sizeof(unsigned short) * kOwnTile;
 
 unsigned grid_for(const reseq_cuda_ctx* ctx, size_t n, int block, int per_thread, int waves) {
     size_t want = (n + static_cast<size_t>(block) * per_thread - 1) /
@@ -1527,6 +1858,46 @@ int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64*
     }
     RSQ_CUDA(cudaGetLastError());
     return window_scatter_device(ctx, rec, n, plan.win_bits, rank);
+}
+
+__global__ void inverse_records_kernel(const u64* __restrict__ rec, u64 m, u32* __restrict__ rank) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride)
+        rank[rec[i] >> 32] = static_cast<u32>(rec[i]);
+}
+
+// rank[p] = v for `len` records (p << 32 | v) in no particular order whose p's are a permutation of
+// [0, len) -- one position slice of a multi-GPU build after the exchange.  Same machinery as
+// inverse_device: the records are partitioned by the top bits of p (rec_a is clobbered, rec_b is
+// scratch of the same size), then scattered window by window.
+int inverse_from_records(reseq_cuda_ctx* ctx, u64* rec_a, size_t len, u32* rank, u64* rec_b, u32* scratch) {
+    cudaStream_t s = ctx->stream;
+    const InversePlan plan = make_inverse_plan(len, 0);
+    if (!plan.partitioned) {
+        RSQ_LAUNCH_BEGIN(ctx, "inverse_records_kernel");
+        inverse_records_kernel<<<grid_for(ctx, len, 256, 4, 16), 256, 0, s>>>(rec_a, len, rank);
+        RSQ_LAUNCH_END(ctx);
+        RSQ_CUDA(cudaGetLastError());
+        return RESEQ_OK;
+    }
+    u32* claim1 = scratch;
+    u32* claim2 = scratch + kIpMaxBins;
+    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpMaxBins + plan.buckets2 + 32), s));
+    const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
+    RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec0");
+    inv_partition_persistent_kernel<kIpRec0><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b,
+                                                                      plan.tiles);
+    RSQ_LAUNCH_END(ctx);
+    const u64* rec = rec_b;
+    if (plan.lo_bits > 0) {
+        RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec");
+        inv_partition_persistent_kernel<kIpRec><<<grid, kIpBlock, 0, s>>>(rec_b, len, plan.win_bits, plan.shift1,
+                                                                         2 << plan.lo_bits, claim2, rec_a, plan.tiles);
+        RSQ_LAUNCH_END(ctx);
+        rec = rec_a;
+    }
+    RSQ_CUDA(cudaGetLastError());
+    return window_scatter_device(ctx, rec, len, plan.win_bits, rank);
 }
 
 // The DNA fast path on `count` records: sort on key24, finish every group from the text.
@@ -1876,6 +2247,14 @@ struct reseq_cuda_sa_shard {
     rsq::u32* u_uncbits = nullptr;
     rsq::u32* u_counters = nullptr;
     size_t u_m = 0;
+    // bucket between reseq_cuda_sa_shard_bucket_size and _bucket_records (arrays in the context's arena)
+    rsq::u32 b_plo = 0, b_phi = 0, b_tiles = 0;
+    rsq::u32* b_offsets = nullptr;
+    size_t b_m = 0;
+    bool b_ready = false;
+    rsq::u32* b_hist = nullptr;     // [4][256] digit histograms of the bucket written last (own allocation)
+    bool b_hist_valid = false;
+    const void* b_records = nullptr;   // ... which is this array
 };
 
 extern "C" {
@@ -1894,7 +2273,8 @@ int reseq_cuda_sa_shard_create(reseq_cuda_ctx* ctx, const uint8_t* d_text, size_
     // stream-ordered pool allocations (cached across shards: a build per step pays no cudaMalloc)
     if (cudaMallocAsync(&sh->packed, sizeof(u64) * (n / 32 + 8), ctx->stream) != cudaSuccess ||
         cudaMallocAsync(&sh->sent, sizeof(u64) * (n / 64 + 8), ctx->stream) != cudaSuccess ||
-        cudaMallocAsync(&sh->flags, 256, ctx->stream) != cudaSuccess) {
+        cudaMallocAsync(&sh->flags, 256, ctx->stream) != cudaSuccess ||
+        cudaMallocAsync(&sh->b_hist, sizeof(u32) * 4 * kRadix, ctx->stream) != cudaSuccess) {
         cudaGetLastError();
         reseq_cuda_sa_shard_destroy(sh);
         return fail(RESEQ_OUT_OF_MEMORY, "cudaMalloc failed for the packed text");
@@ -1982,8 +2362,11 @@ int reseq_cuda_sa_shard_uniform_sort_link(reseq_cuda_sa_shard* sh, uint64_t* d_r
     RSQ_TRY(sort_workspace_carve(ctx, m, &ws));
     RSQ_CUDA(cudaMemsetAsync(sh->u_counters, 0, 8 * sizeof(u32), ctx->stream));
     reseq_sa_stats st{};
-    // stable passes: equal keys keep the (t, position) order the caller brought the bucket into
-    return uniform_sort_link(ctx, sh->packed, sh->period, d_records, rec_b, m, false, whole, d_cov, sh->u_counters, ws,
+    const bool hist_ready = sh->b_hist_valid && sh->b_records == d_records && sh->b_m == m;   // written by bucket_records
+    sh->b_hist_valid = false;
+    if (hist_ready) RSQ_CUDA(cudaMemcpyAsync(ws.hist, sh->b_hist, sizeof(u32) * 4 * kRadix, cudaMemcpyDeviceToDevice, ctx->stream));
+    // stable passes: equal keys keep the (t, position) order the bucket was born in
+    return uniform_sort_link(ctx, sh->packed, sh->period, d_records, rec_b, m, hist_ready, whole, d_cov, sh->u_counters, ws,
                              &st, &sh->u_sorted);
 }
 
@@ -2014,6 +2397,7 @@ void reseq_cuda_sa_shard_destroy(reseq_cuda_sa_shard* sh) {
     if (sh->packed) cudaFreeAsync(sh->packed, st);
     if (sh->sent) cudaFreeAsync(sh->sent, st);
     if (sh->flags) cudaFreeAsync(sh->flags, st);
+    if (sh->b_hist) cudaFreeAsync(sh->b_hist, st);
     if (sh->ctx) cudaStreamSynchronize(st);
     delete sh;
 }
@@ -2056,9 +2440,160 @@ int reseq_cuda_sa_shard_finish(reseq_cuda_sa_shard* sh, uint64_t* d_records, siz
     // stable sort of the bucket on the 24-bit key: equal keys stay in ascending position order
     // because the exchange delivers the slices in rank (= position) order
     reseq_sa_stats st{};
-    RSQ_TRY(sort_and_refine(ctx, sh->packed, sh->sent, sh->n, d_records, rec_b, m, false, d_sa_out, 1 << 20,
+    const bool hist_ready = sh->b_hist_valid && sh->b_records == d_records && sh->b_m == m;   // written by bucket_records
+    sh->b_hist_valid = false;
+    if (hist_ready) RSQ_CUDA(cudaMemcpyAsync(ws.hist, sh->b_hist, sizeof(u32) * 3 * kRadix, cudaMemcpyDeviceToDevice, ctx->stream));
+    RSQ_TRY(sort_and_refine(ctx, sh->packed, sh->sent, sh->n, d_records, rec_b, m, hist_ready, d_sa_out, 1 << 20,
                             sh->use_shortcut, counters, ws, &st, unfinished));
     return RESEQ_OK;
+}
+
+int reseq_cuda_sa_shard_prefix_hist(reseq_cuda_sa_shard* sh, uint64_t unit_begin, size_t unit_count, uint32_t* d_hist) {
+    using namespace rsq;
+    if (!sh || !sh->dna || !d_hist) return fail(RESEQ_INVALID_ARGUMENT, "the sharded build needs a DNA text");
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    RSQ_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(u32) << kShPrefixBits, ctx->stream));
+    if (unit_count == 0) return RESEQ_OK;
+    if (sh->period) {
+        if (unit_begin + unit_count > sh->reads) return fail(RESEQ_INVALID_ARGUMENT, "read slice out of range");
+        RSQ_LAUNCH_BEGIN(ctx, "shard_hist_uniform_kernel");
+        shard_hist_uniform_kernel<<<static_cast<unsigned>((unit_count + kShReads - 1) / kShReads), kShReads, 0, ctx->stream>>>(
+            sh->packed, sh->period, unit_begin, unit_count, d_hist);
+        RSQ_LAUNCH_END(ctx);
+    } else {
+        if (unit_begin + unit_count > sh->n) return fail(RESEQ_INVALID_ARGUMENT, "position slice out of range");
+        RSQ_LAUNCH_BEGIN(ctx, "shard_hist_general_kernel");
+        shard_hist_general_kernel<<<grid_for(ctx, unit_count, 256, 8, 8), 256, 0, ctx->stream>>>(sh->packed, sh->sent, sh->n,
+                                                                                               unit_begin, unit_count, d_hist);
+        RSQ_LAUNCH_END(ctx);
+    }
+    RSQ_CUDA(cudaGetLastError());
+    return RESEQ_OK;
+}
+
+int reseq_cuda_sa_shard_bucket_size(reseq_cuda_sa_shard* sh, uint32_t prefix_lo, uint32_t prefix_hi, uint64_t* m) {
+    using namespace rsq;
+    if (!sh || !sh->dna || !m) return fail(RESEQ_INVALID_ARGUMENT, "the sharded build needs a DNA text");
+    if (prefix_lo > prefix_hi || prefix_hi > (1u << kShPrefixBits)) return fail(RESEQ_INVALID_ARGUMENT, "prefix range out of order");
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    sh->b_ready = false;
+    const u64 units = sh->period ? sh->reads : sh->n;
+    const u32 tiles = static_cast<u32>(sh->period ? (units + kShReads - 1) / kShReads : (units + kShTile - 1) / kShTile);
+    const size_t cells = sh->period ? static_cast<size_t>(tiles) * sh->period : tiles;
+    auto pad = reseq_cuda_ctx::padded;
+    RSQ_TRY(ctx->reserve(2 * pad(sizeof(u32) * (cells + 1)) + scan_workspace_bytes(cells + 1) + 8192));
+    ctx->begin();
+    u32* counts = ctx->alloc<u32>(cells + 1);
+    u32* offsets = ctx->alloc<u32>(cells + 1);
+    u64* d_total = ctx->alloc<u64>(1);
+    if (!counts || !offsets || !d_total) return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
+    RSQ_CUDA(cudaMemsetAsync(counts + cells, 0, sizeof(u32), s));
+    if (sh->period) {
+        RSQ_LAUNCH_BEGIN(ctx, "shard_count_uniform_kernel");
+        shard_count_uniform_kernel<<<tiles, kShReads, 0, s>>>(sh->packed, sh->period, sh->reads, prefix_lo, prefix_hi, tiles, counts);
+        RSQ_LAUNCH_END(ctx);
+    } else {
+        RSQ_LAUNCH_BEGIN(ctx, "shard_count_general_kernel");
+        shard_general_kernel<false><<<tiles, 256, 0, s>>>(sh->packed, sh->sent, sh->n, prefix_lo, prefix_hi, counts, nullptr, nullptr, nullptr);
+        RSQ_LAUNCH_END(ctx);
+    }
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_TRY(exclusive_scan_device(ctx, counts, offsets, cells + 1, d_total));
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, d_total, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    sh->b_m = *reinterpret_cast<volatile u64*>(ctx->pinned);
+    sh->b_plo = prefix_lo;
+    sh->b_phi = prefix_hi;
+    sh->b_tiles = tiles;
+    sh->b_offsets = offsets;
+    sh->b_ready = true;
+    *m = sh->b_m;
+    return RESEQ_OK;
+}
+
+int reseq_cuda_sa_shard_bucket_records(reseq_cuda_sa_shard* sh, uint64_t* d_records) {
+    using namespace rsq;
+    if (!sh || !sh->b_ready) return fail(RESEQ_INVALID_ARGUMENT, "bucket_records must follow bucket_size on the same shard");
+    sh->b_ready = false;
+    if (sh->b_m == 0) return RESEQ_OK;
+    if (!d_records) return fail(RESEQ_INVALID_ARGUMENT, "null records");
+    reseq_cuda_ctx* ctx = sh->ctx;
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    RSQ_CUDA(cudaMemsetAsync(sh->b_hist, 0, sizeof(u32) * 4 * kRadix, ctx->stream));
+    if (sh->period) {
+        RSQ_LAUNCH_BEGIN(ctx, "shard_write_uniform_kernel");
+        shard_write_uniform_kernel<<<sh->b_tiles, kShReads, 0, ctx->stream>>>(sh->packed, sh->period, sh->reads, sh->b_plo, sh->b_phi,
+                                                                             sh->b_tiles, sh->b_offsets, d_records, sh->b_hist);
+        RSQ_LAUNCH_END(ctx);
+    } else {
+        RSQ_LAUNCH_BEGIN(ctx, "shard_write_general_kernel");
+        shard_general_kernel<true><<<sh->b_tiles, 256, 0, ctx->stream>>>(sh->packed, sh->sent, sh->n, sh->b_plo, sh->b_phi, nullptr,
+                                                                        sh->b_offsets, d_records, sh->b_hist);
+        RSQ_LAUNCH_END(ctx);
+    }
+    RSQ_CUDA(cudaGetLastError());
+    sh->b_hist_valid = true;    // the sort of exactly this array may skip its histogram sweep
+    sh->b_records = d_records;
+    return RESEQ_OK;
+}
+
+int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bucket, size_t m, uint64_t global_offset,
+                                    uint64_t n, int world, uint64_t* d_records_out, uint64_t* counts_out) {
+    using namespace rsq;
+    if (!ctx || !counts_out || world < 1 || world > 16 || n == 0) return fail(RESEQ_INVALID_ARGUMENT, "bad argument (1 <= world <= 16)");
+    for (int g = 0; g < world; ++g) counts_out[g] = 0;
+    if (m == 0) return RESEQ_OK;
+    if (!d_sa_bucket || !d_records_out) return fail(RESEQ_INVALID_ARGUMENT, "null device buffer");
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    RSQ_TRY(ctx->reserve(16384));
+    ctx->begin();
+    const int bins = world * kOwnSub;
+    u32* counts = ctx->alloc<u32>(2 * 16 * kOwnSub);
+    if (!counts) return fail(RESEQ_OUT_OF_MEMORY, "rank shard workspace");
+    u32* claim = counts + 16 * kOwnSub;
+    RSQ_CUDA(cudaMemsetAsync(counts, 0, sizeof(u32) * bins, s));
+    RSQ_LAUNCH_BEGIN(ctx, "owner_count_kernel");
+    owner_count_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(d_sa_bucket, m, n, static_cast<u32>(world), counts);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    u32* h = reinterpret_cast<u32*>(ctx->pinned);   // 4096 pinned bytes: 16 * 64 counters
+    RSQ_CUDA(cudaMemcpyAsync(h, counts, sizeof(u32) * bins, cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    u64 run = 0;
+    for (int b = 0; b < bins; ++b) {   // counts -> exclusive bases, in place
+        const u32 c = h[b];
+        counts_out[b / kOwnSub] += c;
+        h[b] = static_cast<u32>(run);
+        run += c;
+    }
+    RSQ_CUDA(cudaMemcpyAsync(claim, h, sizeof(u32) * bins, cudaMemcpyHostToDevice, s));
+    RSQ_LAUNCH_BEGIN(ctx, "owner_partition_kernel");
+    RSQ_OPT_IN_SMEM(ctx, owner_partition_kernel, kOwnSmem);
+    owner_partition_kernel<<<static_cast<unsigned>((m + kOwnTile - 1) / kOwnTile), kOwnBlock, kOwnSmem, s>>>(
+        d_sa_bucket, m, n, static_cast<u32>(world), global_offset, claim, d_records_out);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaStreamSynchronize(s));   // the pinned staging words are reused by the next call
+    return RESEQ_OK;
+}
+
+int reseq_cuda_rank_shard_finish(reseq_cuda_ctx* ctx, uint64_t* d_records, size_t len, uint32_t* d_rank_slice) {
+    using namespace rsq;
+    if (!ctx) return fail(RESEQ_INVALID_ARGUMENT, "null context");
+    if (len == 0) return RESEQ_OK;
+    if (!d_records || !d_rank_slice) return fail(RESEQ_INVALID_ARGUMENT, "null device buffer");
+    RSQ_CUDA(cudaSetDevice(ctx->device));
+    auto pad = reseq_cuda_ctx::padded;
+    RSQ_TRY(ctx->reserve(pad(sizeof(u64) * len) + pad(sizeof(u32) * inverse_scratch_words(len)) + 4096));
+    ctx->begin();
+    u64* rec_b = ctx->alloc<u64>(len);
+    u32* scratch = ctx->alloc<u32>(inverse_scratch_words(len));
+    if (!rec_b || !scratch) return fail(RESEQ_OUT_OF_MEMORY, "inverse workspace");
+    return inverse_from_records(ctx, d_records, len, d_rank_slice, rec_b, scratch);
 }
 
 int reseq_cuda_inverse_device(reseq_cuda_ctx* ctx, const uint32_t* d_sa, size_t n, uint32_t* d_rank) {

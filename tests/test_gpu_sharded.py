@@ -71,6 +71,44 @@ def test_sharded_build_equals_single_gpu(rq, ex, oracle, G):
         assert sum(sizes) == text.size and min(sizes) > 0
 
 
+@pytest.mark.parametrize("G,uniform", [(4, True), (3, False), (8, True)])
+def test_sharded_parts_on_side_streams_at_config1_size(rq, ex, oracle, G, uniform):
+    """The build LEFT SHARDED (sa by splitter bucket, rank by position slice) at BASELINE config 1's full
+    size, every virtual rank on its own torch.cuda.Stream: the library's kernels, torch's allocations
+    and copies and the exchange are ordered by that stream alone (no device-wide synchronisation in
+    between), so a missing dependency shows up as a wrong array here."""
+    from paper_1404_3456_b200.sharded import GpuBackend, build_sa_sharded_parts
+    text, _ = rq.synth_read_text(1_000_000, 100, 100_000)
+    n = text.size
+    want = rq.build_parallel(text, ex)
+    assert oracle.checksum_u32(want.sa) == 11642757783061468293
+    d_text = torch.from_numpy(text).cuda()
+    torch.cuda.synchronize()
+
+    def fn(comm):
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            e = rq.Executor(0)
+            if not uniform:
+                e.set_option("sa_uniform", 0)
+            stats = {}
+            parts = build_sa_sharded_parts(d_text, comm, GpuBackend(e), stats)
+            res = (parts.sa_bucket.cpu().numpy().view(np.uint32), parts.sa_offset, parts.rank_slice.cpu().numpy().view(np.uint32),
+                   parts.rank_base, stats)
+            side.synchronize()
+            e.close()
+        return res
+
+    res = run_ranks(G, fn)
+    assert all(st["path"] == "sharded" for *_, st in res)
+    assert [off for _, off, _, _, _ in res] == list(np.cumsum([0] + [b.size for b, *_ in res[:-1]]))
+    assert [base for _, _, _, base, _ in res] == [(n * g) // G for g in range(G)]
+    assert np.array_equal(np.concatenate([b for b, *_ in res]), want.sa)
+    assert np.array_equal(np.concatenate([r for _, _, r, _, _ in res]), want.rank)
+    sizes = [b.size for b, *_ in res]
+    assert max(sizes) < 1.25 * n / G            # the splitters balance the buckets
+
+
 @pytest.mark.parametrize("G", [2, 3])
 def test_sharded_uniform_build_on_repeats_and_duplicates(rq, ex, oracle, G):
     """Groups that mix loci (re-sorted inside a bucket), duplicate reads, whole reads whose

@@ -1,8 +1,9 @@
 """Host logic of the multi-GPU path under REAL collectives: two processes, gloo backend, CPU
 tensors.  The per-rank kernels are replaced by a numpy stand-in (NumpyBackend below, checker-grade
-code that leans on the oracle), so what is exercised is sharded.py itself: position slicing,
-splitter selection from the all-reduced histogram, the all-to-all of the 64-bit suffix records, the
-ordering guarantee the bucket sort relies on, the all-gather of buckets and the fallbacks."""
+code that leans on the oracle), so what is exercised is sharded.py itself: read / position slicing,
+splitter selection from the all-reduced prefix histogram, bucket-local record generation and the
+ordering guarantee the bucket sort relies on, the combined proof table, the all-to-all of the
+(position, index) records that shards rank by position, the gather into place and the fallbacks."""
 import os
 import sys
 from pathlib import Path
@@ -78,7 +79,13 @@ class NumpyBackend:
         self.oracle_rank = oracle_rank   # inverse SA of the whole text from the oracle
         self.uniform = uniform
 
-    # -- uniform read sets: the orchestration contract, not the kernels ------------------------------
+    def open(self, d_text):
+        self.text = d_text.numpy()
+        return bool(np.isin(self.text, [0, 65, 67, 71, 84]).all())
+
+    def close(self):
+        pass
+
     def uniform_info(self):
         if not self.uniform:
             return None
@@ -87,20 +94,37 @@ class NumpyBackend:
         assert np.array_equal(seps, np.arange(seps.size) * period + period - 1)
         return period, int(seps.size)
 
-    def uniform_records(self, read_begin, read_count):
-        return torch.from_numpy(uniform_records_of(self.text, self.uniform_info()[0], read_begin, read_count))
+    def _all_records(self):
+        if not hasattr(self, "_recs"):
+            if self.uniform:
+                period, reads = self.uniform_info()
+                self._recs = uniform_records_of(self.text, period, 0, reads)            # (t, read) order
+                self._prefix = (self._recs >> 52) & 0xFFF
+            else:
+                self._recs = records_of(self.text, 0, self.text.size)                   # position order
+                self._prefix = (self._recs >> 52) & 0xFFF
+        return self._recs, self._prefix
 
-    def order_by_distance(self, records, period):
-        r = records.numpy()
-        t = (period - 1) - (r & 0xFFFFFFFF) % period
-        return torch.from_numpy(r[np.argsort(t, kind="stable")].copy())
+    def prefix_hist(self, unit_begin, unit_count):
+        recs, prefix = self._all_records()
+        pos = recs & 0xFFFFFFFF
+        if self.uniform:
+            period = self.uniform_info()[0]
+            mine = (pos // period >= unit_begin) & (pos // period < unit_begin + unit_count)
+        else:
+            mine = (pos >= unit_begin) & (pos < unit_begin + unit_count)
+        return torch.from_numpy(np.bincount(prefix[mine], minlength=1 << 12).astype(np.int64))
+
+    def bucket(self, plo, phi):
+        recs, prefix = self._all_records()
+        return torch.from_numpy(recs[(prefix >= plo) & (prefix < phi)].copy())
 
     def uniform_sort_link(self, records, reads):
         r = records.numpy()
         period = self.uniform_info()[0]
         p = r & 0xFFFFFFFF
         t = (period - 1) - p % period
-        # the contract the stable digit passes rely on: the bucket arrives in (t, position) order
+        # the contract the stable digit passes rely on: the bucket is born in (t, position) order
         assert np.all((t[1:] > t[:-1]) | ((t[1:] == t[:-1]) & (p[1:] > p[:-1]))), "bucket not in (t, position) order"
         self._bucket = p
         cov = np.zeros(reads, np.uint8)
@@ -114,41 +138,30 @@ class NumpyBackend:
         by_suffix = p[np.argsort(self.oracle_rank[p], kind="stable")]
         return torch.from_numpy(by_suffix.astype(np.int32)), 0
 
-    def open(self, d_text):
-        self.text = d_text.numpy()
-        return bool(np.isin(self.text, [0, 65, 67, 71, 84]).all())
-
-    def close(self):
-        pass
-
-    def records(self, lo, count):
-        return torch.from_numpy(records_of(self.text, lo, lo + count))
-
-    def prefix_histogram(self, records):
-        return torch.bincount((records >> 48) & 0xFFFF, minlength=1 << 16)
-
-    def partition(self, records, bounds):
-        dest = torch.bucketize((records >> 48) & 0xFFFF, bounds, right=True)
-        order = torch.argsort(dest, stable=True)
-        counts = torch.bincount(dest, minlength=bounds.numel() + 1)
-        return records[order].contiguous(), [int(c) for c in counts.tolist()]
-
     def finish(self, records):
         r = records.numpy()
         p = r & 0xFFFFFFFF
-        # the exchange must deliver equal keys in ascending position order (stability contract)
-        k = (r >> 40) & 0xFFFFFF
-        order = np.argsort(k, kind="stable")
-        same = k[order][1:] == k[order][:-1]
-        assert np.all(p[order][1:][same] > p[order][:-1][same]), "records of equal key arrived out of position order"
+        assert np.all(p[1:] > p[:-1]), "general records must be born in position order"
         by_suffix = p[np.argsort(self.oracle_rank[p], kind="stable")]
         return torch.from_numpy(by_suffix.astype(np.int32)), 0
 
-    def inverse(self, sa):
-        s = sa.numpy().astype(np.int64)
-        r = np.empty_like(s)
-        r[s] = np.arange(s.size)
-        return torch.from_numpy(r.astype(np.int32))
+    def rank_records(self, bucket, offset, n, world):
+        p = bucket.numpy().astype(np.int64) & 0xFFFFFFFF
+        base = np.array([(n * g) // world for g in range(world + 1)], np.int64)
+        owner = np.searchsorted(base, p, side="right") - 1
+        order = np.argsort(owner, kind="stable")[::-1].copy()          # any order inside an owner's group is allowed
+        order = order[np.argsort(owner[order], kind="stable")]
+        recs = ((p - base[owner]) << 32) | (offset + np.arange(p.size, dtype=np.int64))
+        return torch.from_numpy(recs[order].copy()), [int(c) for c in np.bincount(owner, minlength=world)]
+
+    def rank_finish(self, records, slice_len):
+        r = records.numpy()
+        assert r.size == slice_len, "a position slice must receive exactly its own records"
+        p, v = r >> 32, r & 0xFFFFFFFF
+        assert np.array_equal(np.sort(p), np.arange(slice_len)), "records are not a permutation of the slice"
+        out = np.empty(slice_len, np.int64)
+        out[p] = v
+        return torch.from_numpy(out.astype(np.int32))
 
     def full_build(self, d_text):
         sa = np.argsort(self.oracle_rank, kind="stable")
@@ -164,7 +177,12 @@ def worker(rank, world, port, text_bytes, oracle_rank, out_dir, uniform=False):
     comm = TorchComm()
     d_text = torch.from_numpy(np.frombuffer(text_bytes, np.uint8).copy())
     stats = {}
-    sa, rk = build_sa_sharded(d_text, comm, NumpyBackend(oracle_rank, uniform), stats)
+    from paper_1404_3456_b200.sharded import build_sa_sharded_parts
+    parts = build_sa_sharded_parts(d_text, comm, NumpyBackend(oracle_rank, uniform), stats)
+    np.save(Path(out_dir) / f"bucket{rank}.npy", parts.sa_bucket.numpy())      # what stays sharded ...
+    np.save(Path(out_dir) / f"slice{rank}.npy", parts.rank_slice.numpy())
+    assert parts.sa_offset == sum(parts.bucket_sizes[:rank]) and parts.rank_base == (d_text.numel() * rank) // world
+    sa, rk = parts.replicate(comm)                                             # ... and the gather into place
     np.save(Path(out_dir) / f"sa{rank}.npy", sa.numpy())
     np.save(Path(out_dir) / f"rank{rank}.npy", rk.numpy())
     (Path(out_dir) / f"stats{rank}.txt").write_text(
@@ -194,20 +212,23 @@ def test_sample_sort_exchange_under_gloo(oracle, tmp_path, world, uniform):
         assert path == "sharded" and int(sent) > 0 and records == ("uniform" if uniform else "general")
         buckets.append(int(bucket))
     assert sum(buckets) == text.size and min(buckets) > text.size // 4   # balanced by the splitters
+    # the sharded form: buckets concatenate to sa, position slices to rank
+    assert np.array_equal(np.concatenate([np.load(tmp_path / f"bucket{r}.npy").view(np.uint32) for r in range(world)]), want_sa)
+    assert np.array_equal(np.concatenate([np.load(tmp_path / f"slice{r}.npy").view(np.uint32) for r in range(world)]), want_rank)
 
 
 def test_bounds_are_balanced_and_monotone():
     sys.path.insert(0, str(ROOT))
     from paper_1404_3456_b200.sharded import choose_bounds
     rng = np.random.default_rng(5)
-    hist = torch.from_numpy(rng.integers(0, 50, 1 << 16))
+    hist = torch.from_numpy(rng.integers(0, 50, 1 << 12))
     for G in (2, 3, 4, 8):
         b = choose_bounds(hist, G)
-        assert b.numel() == G - 1 and bool(torch.all(b[1:] >= b[:-1]))
-        edges = [0] + [int(x) for x in b] + [1 << 16]
+        assert len(b) == G - 1 and all(y >= x for x, y in zip(b, b[1:]))
+        edges = [0] + [int(x) for x in b] + [1 << 12]
         loads = [int(hist[edges[g]:edges[g + 1]].sum()) for g in range(G)]
         assert max(loads) - min(loads) <= 2 * 50 + int(hist.sum()) // (50 * G)
-    skew = torch.zeros(1 << 16, dtype=torch.int64)
+    skew = torch.zeros(1 << 12, dtype=torch.int64)
     skew[7] = 1000                       # everything in one prefix: one rank takes it all, no crash
     b = choose_bounds(skew, 4)
-    assert bool(torch.all(b[1:] >= b[:-1]))
+    assert all(y >= x for x, y in zip(b, b[1:]))
