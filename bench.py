@@ -409,6 +409,7 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
+        os.environ.setdefault("NCCL_DEBUG", "WARN")   # (NCCL's version banner would otherwise precede the JSON line on stdout)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         # (the default workload stays config 2 for every N so that the driver's per-N values are comparable;
         #  --workload c4 / c5 are the configurations the sharded build is meant for)

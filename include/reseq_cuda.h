@@ -88,6 +88,9 @@ size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
  *                     0 forces pure prefix doubling; default 16
  *   "sa_shortcut"     0 switches off the sentinel-distance shortcut of the general DNA path
  *   "sort_cfg"        onesweep tile shape, 0 (default tuning) .. 9
+ *   "sa_doubling_local" 0: prefix-doubling rounds always sort (group, rank2) pairs of all suffixes with the
+ *                     global digit passes (default 1: each CTA orders the groups of its tile in shared
+ *                     memory; the global form runs only for groups that outgrow a CTA's window)
  *   "sa_speculate"    0: never start a build on the previous build's route (default 1: a context that
  *                     has just built a uniform read set of n bytes queues the next n-byte build on the
  *                     same route without a host round trip; the route's premises are re-checked on the

@@ -179,6 +179,7 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     }
     if (const char* e = std::getenv("RESEQ_SA_UNIFORM")) ctx->opt_uniform = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SPECULATE")) ctx->opt_speculate = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_SA_DOUBLING_LOCAL")) ctx->opt_doubling_local = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SHORTCUT")) ctx->opt_shortcut = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);
     *out = ctx;
@@ -228,6 +229,10 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     }
     if (std::strcmp(name, "sa_uniform") == 0) {
         ctx->opt_uniform = value != 0;
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "sa_doubling_local") == 0) {
+        ctx->opt_doubling_local = value != 0;
         return RESEQ_OK;
     }
     if (std::strcmp(name, "sa_speculate") == 0) {

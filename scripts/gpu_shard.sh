@@ -9,7 +9,7 @@ for w in "$@"; do
   tail -3 gpurun_out/shard_${tag}_${w}_forced.err
   python - <<PY
 import json
-a = json.load(open("gpurun_out/shard_${tag}_${w}_plain.json")); b = json.load(open("gpurun_out/shard_${tag}_${w}_forced.json"))
+a = json.load(open("gpurun_out/shard_${tag}_${w}_plain.json")); t = open("gpurun_out/shard_${tag}_${w}_forced.json").read(); b = json.loads(t[t.index('{"metric"'):])
 print("$w plain %.3f ms  forced-sharded %.3f ms  ratio %.3f  e2e %.1f ms  path %s ok %s" % (a["ms_per_step"], b["ms_per_step"], b["ms_per_step"] / a["ms_per_step"], b["e2e"]["ms_per_step"], b["config"]["path"], b["checks"]))
 for k, v in b["roofline"]["kernels"].items(): print("   %-28s %8.3f ms x%.0f" % (k, v["ms_per_step"], v["launches_per_step"]))
 PY

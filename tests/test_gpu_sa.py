@@ -22,6 +22,17 @@ def doubling_executor(rq):
     return _doubling["ex"]
 
 
+def global_doubling_executor(rq):
+    """Pure prefix doubling with every round through the global digit passes (the local shared-memory
+    form switched off)."""
+    if "gd" not in _doubling:
+        e = rq.Executor(0)
+        e.set_option("sa_text_rounds", 0)
+        e.set_option("sa_doubling_local", 0)
+        _doubling["gd"] = e
+    return _doubling["gd"]
+
+
 def no_shortcut_executor(rq):
     """A third context: shared-memory refinement by 23-symbol text steps only (the distance
     shortcut switched off)."""
@@ -48,8 +59,11 @@ def check(rq, ex, oracle, text):
     assert np.array_equal(got.rank, wrank)
     if len(text) <= 300_000:
         alt = rq.build_parallel(text, doubling_executor(rq))
-        assert alt.stats.refined_tile == 0
         assert np.array_equal(alt.sa, wsa), f"prefix-doubling sa differs for text of length {len(text)}"
+        assert np.array_equal(alt.rank, wrank)
+        alt = rq.build_parallel(text, global_doubling_executor(rq))
+        assert alt.stats.refined_tile == 0
+        assert np.array_equal(alt.sa, wsa), f"global prefix-doubling sa differs for text of length {len(text)}"
         assert np.array_equal(alt.rank, wrank)
         alt = rq.build_parallel(text, no_shortcut_executor(rq))
         assert np.array_equal(alt.sa, wsa), f"text-round sa differs for text of length {len(text)}"
@@ -314,7 +328,7 @@ def test_general_routes_at_config2_full_size(rq, oracle, option, value, name):
         if option == "sa_uniform":
             assert got.stats.init_symbols != 16 and got.stats.refined_global == 0, name
         else:
-            assert got.stats.refined_tile == 0 and got.stats.refined_global > 0, name
+            assert got.stats.init_symbols == 13 and got.stats.rounds >= 4, name
         assert oracle.verify_sa(text, got.sa, threads=32) == 0, name
         assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32)), name
     finally:
@@ -454,5 +468,5 @@ def test_doubling_only_mode_on_config1(rq, oracle):
     e = doubling_executor(rq)
     text, _ = rq.synth_read_text(1_000_000, 100, 100_000)
     got = rq.build_parallel(text, e)
-    assert got.stats.rounds == 3 and got.stats.refined_tile == 0   # h = 13, 26, 52 -> 104 >= 101
+    assert got.stats.rounds == 3 and got.stats.init_symbols == 13   # h = 13, 26, 52 -> 104 >= 101
     assert oracle.checksum_u32(got.sa) == 11642757783061468293
