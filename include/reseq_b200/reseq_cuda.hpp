@@ -9,8 +9,10 @@
 //   radix_sort(arr, exec)            radix_sort.hpp:143    radix_sort(arr, dev)
 //   chunked_radix_sort(arr, exec, b) radix_sort.hpp:169    chunked_radix_sort(arr, dev, b)
 //   build_parallel(text, exec)       suffix_array.hpp:61   build_parallel(text, dev)
-//   fragment_index(set, builder, ex) fragment_index.hpp:34 fragment_index(concat, starts, dev)
+//   fragment_index(set, builder, ex) fragment_index.hpp:34 fragment_index(concat, starts, dev) / (set, dev)
 //     .locate_prefix_range(p)        :65                     .locate_prefix_range(p)
+//     .prefix_related(residual)      :72                     .prefix_related(residual)
+//     .prefix_related(string_view)   :82                     .prefix_related(string_view)
 //     .start_rank_list()             :61                     .start_rank_list()
 //   greedy_superstring_with_order    overlap.hpp:80        greedy_superstring_with_order(ix, tau)
 //
@@ -33,10 +35,14 @@
 
 #include "reseq_cuda.h"
 
+#include <algorithm>
+
 #ifdef RESEQ_B200_WITH_REFERENCE
 #include "reseq/errors.hpp"
+#include "reseq/fragment_index.hpp"
 #include "reseq/overlap.hpp"
 #include "reseq/radix_sort.hpp"
+#include "reseq/sequence.hpp"
 #include "reseq/suffix_array.hpp"
 #endif
 
@@ -44,8 +50,12 @@ namespace reseq::cuda {
 
 #ifdef RESEQ_B200_WITH_REFERENCE
 using ::reseq::error;
+using ::reseq::fragment_set;
 using ::reseq::greedy_result;
 using ::reseq::key_array;
+using ::reseq::offset_out_of_range_error;
+using ::reseq::prefix_relation;
+using ::reseq::residual;
 using ::reseq::scan_overflow_error;
 using ::reseq::suffix_array;
 using ::reseq::text_too_large_error;
@@ -74,6 +84,19 @@ struct suffix_array {
 struct greedy_result {
     std::string superstring;
     std::vector<std::uint32_t> order;
+};
+struct residual {   // sequence.hpp:96-101
+    std::uint32_t frag = 0;
+    std::uint32_t offset = 0;
+};
+struct prefix_relation {   // fragment_index.hpp:21-25
+    std::vector<std::uint32_t> prefixes_of;
+    std::vector<std::uint32_t> extensions_of;
+    std::vector<std::uint32_t> exact_matches;
+};
+struct offset_out_of_range_error : error {   // errors.hpp:30-34
+    offset_out_of_range_error(std::uint32_t frag, std::uint32_t offset)
+        : error("offset " + std::to_string(offset) + " out of range for fragment " + std::to_string(frag)) {}
 };
 #endif
 
@@ -182,9 +205,94 @@ public:
                                               concat.size(), starts.data(), starts.size(), &ix_),
                       concat.size());
     }
+#ifdef RESEQ_B200_WITH_REFERENCE
+    /// The reference's own constructor shape (fragment_index.hpp:34): from a fragment_set.
+    fragment_index(const fragment_set& set, const device_executor& dev)
+        : fragment_index(std::string_view(set.concat()), std::span<const std::uint32_t>(set.starts()), dev) {}
+#endif
     fragment_index(const fragment_index&) = delete;
     fragment_index& operator=(const fragment_index&) = delete;
     ~fragment_index() { reseq_cuda_index_destroy(ix_); }
+
+    std::uint32_t length(std::uint32_t id) const {   // fragment_set::length, sequence.hpp:78-83
+        const std::size_t end = (id + 1 < starts_.size() ? starts_[id + 1] : concat_.size()) - 1;
+        return static_cast<std::uint32_t>(end - starts_[id]);
+    }
+
+    /// prefix_related(residual), fragment_index.hpp:72-80: the batched device query with q = 1.
+    prefix_relation prefix_related(residual r) const {
+        if (r.frag >= starts_.size() || r.offset >= length(r.frag)) throw offset_out_of_range_error(r.frag, r.offset);
+        return prefix_related_batch(std::span<const residual>(&r, 1)).front();
+    }
+    /// The assembler's batch (find_fir_pairs, assembler.hpp:74-78: one independent query per fragment).
+    std::vector<prefix_relation> prefix_related_batch(std::span<const residual> rs) const {
+        std::vector<std::uint32_t> frag(rs.size()), off(rs.size());
+        for (std::size_t i = 0; i < rs.size(); ++i) {
+            frag[i] = rs[i].frag;
+            off[i] = rs[i].offset;
+        }
+        reseq_prefix_relations rel{};
+        const int st = reseq_cuda_index_prefix_related_batch(ix_, frag.data(), off.data(), rs.size(), &rel);
+        if (st != RESEQ_OK) {
+            reseq_cuda_prefix_relations_free(&rel);
+            detail::check(st);
+        }
+        std::vector<prefix_relation> out(rs.size());
+        for (std::size_t i = 0; i < rs.size(); ++i) {
+            out[i].prefixes_of.assign(rel.prefixes + rel.prefixes_off[i], rel.prefixes + rel.prefixes_off[i + 1]);
+            out[i].extensions_of.assign(rel.extensions + rel.extensions_off[i], rel.extensions + rel.extensions_off[i + 1]);
+            out[i].exact_matches.assign(rel.exact + rel.exact_off[i], rel.exact + rel.exact_off[i + 1]);
+        }
+        reseq_cuda_prefix_relations_free(&rel);
+        return out;
+    }
+    /// prefix_related(std::string_view), fragment_index.hpp:82-109, for arbitrary byte patterns: the
+    /// interval searches -- one per distinct fragment length below |bytes| plus one for the whole pattern
+    /// (at each length the reference's narrowed interval equals locate_prefix_range of that prefix, :75-80)
+    /// -- run on the device as ONE batch; the classification over start_rank_list is the reference's, on
+    /// the host.  Like the reference (:91), a pattern whose interval empties at an intermediate length
+    /// returns at once with prefixes_of in (length, rank) order.
+    prefix_relation prefix_related(std::string_view bytes) const {
+        load_start_tables();
+        prefix_relation rel;
+        const std::size_t m = bytes.size();
+        std::vector<std::uint32_t> cuts;
+        for (std::uint32_t len : lengths_) {
+            if (len >= m) break;
+            cuts.push_back(len);
+        }
+        std::string blob;
+        std::vector<std::uint64_t> offs{0};
+        for (std::uint32_t c : cuts) {
+            blob.append(bytes.substr(0, c));
+            offs.push_back(blob.size());
+        }
+        blob.append(bytes);
+        offs.push_back(blob.size());
+        std::vector<std::uint32_t> lo(offs.size() - 1), hi(offs.size() - 1);
+        detail::check(reseq_cuda_index_locate_batch(ix_, reinterpret_cast<const std::uint8_t*>(blob.data()), offs.data(),
+                                                    lo.size(), lo.data(), hi.data()));
+        auto range = [&](std::size_t q) {
+            return std::pair(std::lower_bound(start_rank_.begin(), start_rank_.end(), lo[q]) - start_rank_.begin(),
+                             std::lower_bound(start_rank_.begin(), start_rank_.end(), hi[q]) - start_rank_.begin());
+        };
+        for (std::size_t t = 0; t < cuts.size(); ++t) {
+            if (lo[t] == hi[t]) return rel;                                  // :91
+            const auto [a, b] = range(t);
+            for (auto u = a; u < b; ++u)                                     // collect_starts_of_length, :150-158
+                if (length(start_frag_[u]) == cuts[t]) rel.prefixes_of.push_back(start_frag_[u]);
+        }
+        const auto [a, b] = range(cuts.size());
+        for (auto u = a; u < b; ++u) {
+            const std::uint32_t id = start_frag_[u], len = length(id);
+            if (len > m) rel.extensions_of.push_back(id);
+            else if (len == m) rel.exact_matches.push_back(id);
+        }
+        std::sort(rel.prefixes_of.begin(), rel.prefixes_of.end());
+        std::sort(rel.extensions_of.begin(), rel.extensions_of.end());
+        std::sort(rel.exact_matches.begin(), rel.exact_matches.end());
+        return rel;
+    }
 
     suffix_array sa() const {
         suffix_array out;
@@ -225,9 +333,21 @@ public:
     }
 
 private:
+    void load_start_tables() const {   // start_rank_list_, frag_at_start_ along it, lengths_ (fragment_index.hpp:40-55)
+        if (!start_rank_.empty() || starts_.empty()) return;
+        start_rank_.resize(starts_.size());
+        start_frag_.resize(starts_.size());
+        detail::check(reseq_cuda_index_get(ix_, nullptr, nullptr, start_rank_.data()));
+        detail::check(reseq_cuda_index_start_fragments(ix_, start_frag_.data()));
+        for (std::uint32_t id = 0; id < starts_.size(); ++id) lengths_.push_back(length(id));
+        std::sort(lengths_.begin(), lengths_.end());
+        lengths_.erase(std::unique(lengths_.begin(), lengths_.end()), lengths_.end());
+    }
+
     std::string concat_;
     std::vector<std::uint32_t> starts_;
     reseq_cuda_index* ix_ = nullptr;
+    mutable std::vector<std::uint32_t> start_rank_, start_frag_, lengths_;
 };
 
 }  // namespace reseq::cuda

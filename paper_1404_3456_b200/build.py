@@ -105,6 +105,11 @@ def build_oracle() -> None:
                        stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"oracle build failed:\n{r.stdout}")
+    # the reference's own classes over libreseq_cuda.so (oracle/_ref/dropin_test; needs /root/reference)
+    r = subprocess.run([sys.executable, str(ROOT / "oracle" / "make_dropin.py")], stdout=subprocess.PIPE,
+                       stderr=subprocess.STDOUT, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"drop-in test build failed:\n{r.stdout}")
 
 
 if __name__ == "__main__":

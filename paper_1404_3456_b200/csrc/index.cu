@@ -54,6 +54,7 @@ struct reseq_cuda_index {
     u32 max_len = 0;
     u32* d_lengths = nullptr;     // distinct fragment lengths, ascending (lengths_, fragment_index.hpp:52-55)
     u32 n_lengths = 0;
+    std::vector<u32> h_lens;      // fragment lengths, host copy (query-offset tables, argument checks)
     std::vector<void*> owned;
 };
 
@@ -241,26 +242,39 @@ struct IndexView {
 };
 
 // SA interval of the pattern text[ppos .. ppos+m) (a residual).
+// narrow()'s continuation (fragment_index.hpp:114-148, used by the sweep of :87-93): on entry (*lo, *hi) is
+// an interval whose suffixes are known to share the pattern's first `depth` symbols and (*s_first, *s_last)
+// the start-list range inside it -- (0, n, 0, k) and depth 0 for a fresh search.  The search stays inside
+// them and compares symbols depth.. only.
 __device__ __forceinline__ void locate_residual(const IndexView& iv, u64 ppos, u32 m, u32* lo, u32* hi,
-                                                u32* s_first, u32* s_last) {
-    u32 l0 = 0, r0 = static_cast<u32>(iv.tv.n), f0 = 0, f1 = iv.k;
+                                                u32* s_first, u32* s_last, u32 depth = 0) {
+    u32 l0 = *lo, r0 = *hi, f0 = *s_first, f1 = *s_last;
     if (iv.tv.packed) {
         if (iv.dir && m >= static_cast<u32>(iv.D)) {
             const u32 x = static_cast<u32>(base_window(iv.tv.packed, ppos) >> (64 - 2 * iv.D));
-            l0 = iv.dir[x];
-            r0 = iv.dir[x + 1];
+            l0 = max(l0, iv.dir[x]);
+            r0 = max(l0, min(r0, iv.dir[x + 1]));
             const u32 xs = x >> (2 * (iv.D - iv.sD));
-            f0 = iv.sdir[xs];
-            f1 = iv.sdir[xs + 1];
+            f0 = max(f0, iv.sdir[xs]);
+            f1 = max(f0, min(f1, iv.sdir[xs + 1]));
         }
-        bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_packed(iv.tv, spos, ppos, m); }, lo, hi);
+        bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_packed(iv.tv, static_cast<u64>(spos) + depth, ppos + depth, m - depth); }, lo, hi);
     } else {
-        const u8* pat = iv.tv.text + ppos;
-        bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_bytes(iv.tv, spos, pat, m); }, lo, hi);
+        const u8* pat = iv.tv.text + ppos + depth;
+        bounds(iv.sa, l0, r0, [&](u32 spos) { return cmp_bytes(iv.tv, static_cast<u64>(spos) + depth, pat, m - depth); }, lo, hi);
     }
     // fragment_index.hpp:95-96
     *s_first = lower_bound_u32(iv.start_rank, f0, f1, *lo);
     *s_last = lower_bound_u32(iv.start_rank, *s_first, f1, *hi);
+}
+// A fresh search over the whole array.
+__device__ __forceinline__ void locate_residual_fresh(const IndexView& iv, u64 ppos, u32 m, u32* lo, u32* hi,
+                                                      u32* s_first, u32* s_last) {
+    *lo = 0;
+    *hi = static_cast<u32>(iv.tv.n);
+    *s_first = 0;
+    *s_last = iv.k;
+    locate_residual(iv, ppos, m, lo, hi, s_first, s_last, 0);
 }
 
 // The fragment-start suffixes inside the SA interval of the residual text[ppos .. ppos+m), without
@@ -345,7 +359,7 @@ locate_residuals_kernel(IndexView iv, const u32* __restrict__ frag, const u32* _
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < q; i += stride) {
         const u32 f = frag[i], o = off[i];
         u32 l, h, sf, sl;
-        locate_residual(iv, static_cast<u64>(iv.starts[f]) + o, iv.lens[f] - o, &l, &h, &sf, &sl);
+        locate_residual_fresh(iv, static_cast<u64>(iv.starts[f]) + o, iv.lens[f] - o, &l, &h, &sf, &sl);
         lo[i] = l;
         hi[i] = h;
     }
@@ -487,7 +501,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
         for (u32 o = lane; o < steps; o += 32) {
             const u32 m = len - o;
             u32 lo = 0, hi = 0, sf, sl;
-            locate_residual(iv, start + o, m, &lo, &hi, &sf, &sl);
+            locate_residual_fresh(iv, start + o, m, &lo, &hi, &sf, &sl);
             // f_i's own start suffix lies in the interval at o = 0, and at o > 0 whenever f_i
             // overlaps itself; the diagonal is zero by convention (overlap.hpp:26,41)
             const u32 self_in = (self >= sf && self < sl) ? 1u : 0u;
@@ -524,7 +538,7 @@ contained_kernel(IndexView iv, u64 f0, u64 f1, u8* __restrict__ contained) {
     for (u64 i = f0 + static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < f1; i += stride) {
         const u32 m = iv.lens[i];
         u32 lo, hi, sf, sl;
-        locate_residual(iv, iv.starts[i], m, &lo, &hi, &sf, &sl);
+        locate_residual_fresh(iv, iv.starts[i], m, &lo, &hi, &sf, &sl);
         u32 exact = 0, min_id = 0xFFFFFFFFu;
         for (u32 t = sf; t < sl; ++t) {
             const u32 id = iv.start_frag[t];
@@ -573,7 +587,8 @@ overlap_fill_kernel(IndexView iv, u64 f0, u64 f1, const u64* __restrict__ qoff, 
 // interval of the pattern's prefix); the final interval yields extensions and exact
 // matches.  MODE 0 counts, MODE 1 fills the CSR arrays at the scanned offsets.  For a
 // residual every prefix of the pattern occurs in the text, so the early return of
-// fragment_index.hpp:91 cannot trigger.  Lists leave in start-rank order; the host sorts
+// fragment_index.hpp:91 cannot trigger.  Each length resumes from the previous interval and
+// depth (narrow's continuation, :87-93).  Lists leave in start-rank order; the host sorts
 // each by id (fragment_index.hpp:105-107).
 template <int MODE>
 __global__ void __launch_bounds__(256)
@@ -590,11 +605,14 @@ prefix_related_kernel(IndexView iv, const u32* __restrict__ lengths, u32 n_lengt
         const u32 m = iv.lens[f] - o;
         u32 np = 0, ne = 0, nx = 0;
         u32 wp = MODE ? off_pre[i] : 0, we = MODE ? off_ext[i] : 0, wx = MODE ? off_exact[i] : 0;
-        u32 lo, hi, sf, sl;
+        // one narrowing sweep (fragment_index.hpp:84-93): every length resumes from the previous interval
+        // and depth, as narrow() does
+        u32 lo = 0, hi = static_cast<u32>(iv.tv.n), sf = 0, sl = iv.k, depth = 0;
         for (u32 t = 0; t < n_lengths; ++t) {
             const u32 len = lengths[t];
             if (len >= m) break;
-            locate_residual(iv, ppos, len, &lo, &hi, &sf, &sl);
+            locate_residual(iv, ppos, len, &lo, &hi, &sf, &sl, depth);
+            depth = len;
             for (u32 u = sf; u < sl; ++u) {
                 const u32 id = iv.start_frag[u];
                 if (iv.lens[id] == len) {
@@ -603,7 +621,7 @@ prefix_related_kernel(IndexView iv, const u32* __restrict__ lengths, u32 n_lengt
                 }
             }
         }
-        locate_residual(iv, ppos, m, &lo, &hi, &sf, &sl);
+        locate_residual(iv, ppos, m, &lo, &hi, &sf, &sl, depth);
         for (u32 u = sf; u < sl; ++u) {
             const u32 id = iv.start_frag[u];
             const u32 len = iv.lens[id];
@@ -844,6 +862,21 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     }
     if (static_cast<uint64_t>(starts[k - 1]) + 2 > n)
         return fail(RESEQ_INVALID_ARGUMENT, "the last fragment is empty (sequence.hpp:110)");
+    // fragment lengths (sequence.hpp:78-83) and the sorted distinct lengths (lengths_, fragment_index.hpp:52-55)
+    // come out of the same pass over `starts`: nothing is read back from the device for them
+    std::vector<u32> h_lens(k);
+    u32 max_len = 0;
+    for (size_t i = 0; i < k; ++i) {
+        h_lens[i] = static_cast<u32>((i + 1 < k ? starts[i + 1] : n) - 1 - starts[i]);
+        max_len = std::max(max_len, h_lens[i]);
+    }
+    std::vector<u32> distinct;
+    {
+        std::vector<bool> seen(static_cast<size_t>(max_len) + 1, false);
+        for (u32 v : h_lens) seen[v] = true;
+        for (size_t v = 0; v < seen.size(); ++v)
+            if (seen[v]) distinct.push_back(static_cast<u32>(v));
+    }
 
     auto* ix = new reseq_cuda_index();
     ix->ctx = ctx;
@@ -878,12 +911,20 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     IX_TRY(dev_alloc(ix, &ix->d_sent, n / 64 + 8));
     IX_CUDA(cudaMemcpyAsync(ix->d_text, concat, n, cudaMemcpyHostToDevice, s));
     IX_CUDA(cudaMemcpyAsync(ix->d_starts, starts, sizeof(u32) * k, cudaMemcpyHostToDevice, s));
+    ix->h_lens = std::move(h_lens);
+    ix->max_len = max_len;
+    ix->n_lengths = static_cast<u32>(distinct.size());
+    ix->min_len = distinct.front();
+    IX_TRY(dev_alloc(ix, &ix->d_lengths, distinct.size()));
+    IX_CUDA(cudaMemcpyAsync(ix->d_lens, ix->h_lens.data(), sizeof(u32) * k, cudaMemcpyHostToDevice, s));
+    IX_CUDA(cudaMemcpyAsync(ix->d_lengths, distinct.data(), sizeof(u32) * distinct.size(), cudaMemcpyHostToDevice, s));
+    IX_CUDA(cudaStreamSynchronize(s));   // `distinct` is a local: its copy must be done before it goes (the text copy is the long one)
 
     // suffix array (fragment_index.hpp:37)
     IX_TRY(ctx->reserve(sa_workspace_bytes(n)));
     ctx->begin();
     reseq_sa_stats st{};
-    IX_TRY(build_sa_device(ctx, ix->d_text, n, ix->d_sa, ix->d_rank, &st));
+    IX_TRY(build_sa_device(ctx, ix->d_text, n, ix->d_sa, ix->d_rank, &st, ix->d_packed, ix->d_sent));   // packs once, for both
     ix->dna = st.alphabet == 0;
 
     // lengths, start ranks (fragment_index.hpp:40-48), directories
@@ -926,28 +967,7 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     invert_kernel<<<grid_1d(ctx, k, 256), 256, 0, s>>>(ix->d_start_frag, k, ix->d_start_inv);
     RSQ_LAUNCH_END(ctx);
     IX_CUDA(cudaGetLastError());
-    IX_CUDA(cudaMemcpyAsync(ctx->pinned, counters, sizeof(u32), cudaMemcpyDeviceToHost, s));
-    IX_CUDA(cudaStreamSynchronize(s));
-    ix->max_len = *reinterpret_cast<volatile u32*>(ctx->pinned);
-    {
-        std::vector<u32> lens(k);
-        IX_CUDA(cudaMemcpy(lens.data(), ix->d_lens, sizeof(u32) * k, cudaMemcpyDeviceToHost));
-        {   // sorted distinct lengths by marking (k log k sort of 10^6 lengths cost more than the whole SA build)
-            std::vector<bool> seen(static_cast<size_t>(ix->max_len) + 1, false);
-            for (u32 v : lens) seen[v] = true;
-            lens.clear();
-            for (size_t v = 0; v < seen.size(); ++v)
-                if (seen[v]) lens.push_back(static_cast<u32>(v));
-        }
-        ix->n_lengths = static_cast<u32>(lens.size());
-        ix->min_len = lens.empty() ? 0u : lens.front();
-        IX_TRY(dev_alloc(ix, &ix->d_lengths, lens.size()));
-        IX_CUDA(cudaMemcpy(ix->d_lengths, lens.data(), sizeof(u32) * lens.size(), cudaMemcpyHostToDevice));
-    }
-
     if (ix->dna) {
-        bool is_dna = true;
-        IX_TRY(pack_dna_device(ctx, ix->d_text, n, ix->d_packed, ix->d_sent, counters + 8, &is_dna, nullptr));
         ix->dir_bases = D;
         ix->sdir_bases = D < 11 ? D : 11;   // 4^11 entries = 16 MB: L2-resident, and k start suffixes still land ~1 per bucket
         const size_t sdir_entries = (size_t{1} << (2 * ix->sdir_bases)) + 2;
@@ -1056,10 +1076,8 @@ int reseq_cuda_index_locate_residuals(reseq_cuda_index* ix, const uint32_t* frag
     reseq_cuda_ctx* ctx = ix->ctx;
     RSQ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    // residual_view's bounds check (sequence.hpp:127-131) needs the lengths on the host
-    std::vector<u32> lens(ix->k);
-    RSQ_CUDA(cudaMemcpyAsync(lens.data(), ix->d_lens, sizeof(u32) * ix->k, cudaMemcpyDeviceToHost, s));
-    RSQ_CUDA(cudaStreamSynchronize(s));
+    // residual_view's bounds check (sequence.hpp:127-131) on the host copy of the lengths
+    const std::vector<u32>& lens = ix->h_lens;
     for (size_t i = 0; i < q; ++i)
         if (frag[i] >= ix->k || off[i] >= lens[frag[i]])
             return fail(RESEQ_INVALID_ARGUMENT, "residual offset out of range (sequence.hpp:128-129)");
@@ -1109,9 +1127,7 @@ int reseq_cuda_index_prefix_related_batch(reseq_cuda_index* ix, const uint32_t* 
     }
     if (q == 0) return RESEQ_OK;
     if (!frag || !off) return fail(RESEQ_INVALID_ARGUMENT, "null buffer");
-    std::vector<u32> lens(ix->k);
-    RSQ_CUDA(cudaMemcpyAsync(lens.data(), ix->d_lens, sizeof(u32) * ix->k, cudaMemcpyDeviceToHost, s));
-    RSQ_CUDA(cudaStreamSynchronize(s));
+    const std::vector<u32>& lens = ix->h_lens;
     for (size_t i = 0; i < q; ++i)
         if (frag[i] >= ix->k || off[i] >= lens[frag[i]])
             return fail(RESEQ_INVALID_ARGUMENT, "residual offset out of range (sequence.hpp:128-129)");
@@ -1207,9 +1223,7 @@ static int overlaps_impl(reseq_cuda_index* ix, uint32_t min_overlap, size_t frag
     auto pad = reseq_cuda_ctx::padded;
 
     // -- per-fragment query counts -> query offsets (host prefix sum; k entries) -----------
-    std::vector<u32> lens(k);
-    RSQ_CUDA(cudaMemcpyAsync(lens.data(), ix->d_lens, sizeof(u32) * k, cudaMemcpyDeviceToHost, s));
-    RSQ_CUDA(cudaStreamSynchronize(s));
+    const std::vector<u32>& lens = ix->h_lens;
     std::vector<u64> qoff(kr + 1, 0);
     for (size_t i = 0; i < kr; ++i)
         qoff[i + 1] = qoff[i] + (lens[f0 + i] >= min_overlap ? lens[f0 + i] - min_overlap + 1 : 0);

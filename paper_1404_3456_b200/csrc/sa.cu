@@ -2248,7 +2248,7 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
 }  // namespace
 
 int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, u32* d_rank,
-                    reseq_sa_stats* stats) {
+                    reseq_sa_stats* stats, u64* packed_out, u64* sent_out) {
     reseq_sa_stats st{};
     const uint64_t launches0 = ctx->launches;
     if (n > RESEQ_CUDA_MAX_TEXT)
@@ -2259,8 +2259,8 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     }
     cudaStream_t s = ctx->stream;
 
-    u64* packed = ctx->alloc<u64>(n / 32 + 8);
-    u64* sent = ctx->alloc<u64>(n / 64 + 8);
+    u64* packed = packed_out ? packed_out : ctx->alloc<u64>(n / 32 + 8);
+    u64* sent = sent_out ? sent_out : ctx->alloc<u64>(n / 64 + 8);
     u64* keys_a = ctx->alloc<u64>(n);
     u64* keys_b = ctx->alloc<u64>(n);
     u32* vals_b = ctx->alloc<u32>(n);

@@ -109,7 +109,58 @@ int main() {
         REQUIRE((pos == u32v{0, 13} || pos == u32v{13, 0}));
         auto [l2, h2] = ix.locate_prefix_range("QQ");
         REQUIRE(l2 == h2);
+        // prefix_related, test_fragment_index.cpp:82-94
+        auto rel = ix.prefix_related(residual{0, 2});   // "TT"
+        REQUIRE(rel.prefixes_of.empty() && rel.exact_matches.empty());
+        REQUIRE(rel.extensions_of == (u32v{4}));
+        REQUIRE(ix.prefix_related(std::string_view("GGT")).exact_matches == (u32v{2}));
+        REQUIRE(ix.prefix_related(std::string_view("GATTA")).prefixes_of == (u32v{0, 3}));   // GA and GATT
+        REQUIRE(throws<offset_out_of_range_error>([&] { ix.prefix_related(residual{0, 4}); }));   // sequence.hpp:128-129
+        REQUIRE(throws<offset_out_of_range_error>([&] { ix.prefix_related(residual{6, 0}); }));
     }
+    {
+        // test_fragment_index.cpp:96-104
+        const std::string concat("ab\0cd\0efgh\0abcdef\0gh\0", 21);
+        const u32v starts{0, 3, 6, 11, 18};
+        fragment_index ix(concat, starts, dev);
+        auto rel = ix.prefix_related(std::string_view("cdef"));
+        REQUIRE(rel.prefixes_of == (u32v{1}) && rel.extensions_of.empty() && rel.exact_matches.empty());
+        // the early return of fragment_index.hpp:91: the interval empties at length 2 ("zz" is absent)
+        auto none = ix.prefix_related(std::string_view("zzzzzzz"));
+        REQUIRE(none.prefixes_of.empty() && none.extensions_of.empty() && none.exact_matches.empty());
+    }
+#ifdef RESEQ_B200_WITH_REFERENCE
+    {
+        // the reference's constructor shape (fragment_index.hpp:34) and 600 random queries against the
+        // reference's own prefix_related, residual and string_view forms (test_fragment_index.cpp:106-127)
+        std::mt19937_64 rng(53);
+        for (int it = 0; it < 60; ++it) {
+            std::vector<std::string> frags;
+            const int k = 2 + rng() % 12;
+            for (int f = 0; f < k; ++f) {
+                std::string s;
+                const int len = 1 + rng() % 9;
+                for (int i = 0; i < len; ++i) s.push_back("AC"[rng() % 2]);
+                frags.push_back(s);
+            }
+            auto set = reseq::make_fragment_set(frags, reseq::alphabet::dna);
+            fragment_index ix(set, dev);
+            reseq::fragment_index ref_ix(set);
+            for (int q = 0; q < 10; ++q) {
+                const std::uint32_t id = rng() % set.size(), off = rng() % set.length(id);
+                const auto a = ix.prefix_related(residual{id, off});
+                const auto b = ref_ix.prefix_related(reseq::residual{id, off});
+                REQUIRE(a.prefixes_of == b.prefixes_of && a.extensions_of == b.extensions_of && a.exact_matches == b.exact_matches);
+                std::string pat;
+                const int plen = 1 + rng() % 11;
+                for (int i = 0; i < plen; ++i) pat.push_back("ACG"[rng() % 3]);
+                const auto c = ix.prefix_related(std::string_view(pat));
+                const auto d = ref_ix.prefix_related(std::string_view(pat));
+                REQUIRE(c.prefixes_of == d.prefixes_of && c.extensions_of == d.extensions_of && c.exact_matches == d.exact_matches);
+            }
+        }
+    }
+#endif
     {
         // the paper's five fragments: SPEC.md:300
         const std::string concat("abthatb\0hatbpaab\0tbabhhatbpaa\0paabtabh\0bhaabtpb\0", 48);
