@@ -173,6 +173,8 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     if (const char* e = std::getenv("RESEQ_INVERSE_LO_BITS")) ctx->opt_inverse_lo_bits = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_INVERSE_MODE")) ctx->opt_inverse_mode = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_LOOKBACK_PACK")) ctx->opt_lookback_pack = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_SORT_TMA")) ctx->opt_sort_tma = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_OVERLAP_STAGE")) ctx->opt_overlap_stage = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_LOOKAHEAD")) {
         const int v = std::atoi(e);
         if (v >= 1 && v <= 8) ctx->opt_lookahead = v;
@@ -229,6 +231,14 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     }
     if (std::strcmp(name, "sa_uniform") == 0) {
         ctx->opt_uniform = value != 0;
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "overlap_stage") == 0) {
+        ctx->opt_overlap_stage = value != 0;
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "sort_tma") == 0) {
+        ctx->opt_sort_tma = value != 0;
         return RESEQ_OK;
     }
     if (std::strcmp(name, "sa_doubling_local") == 0) {

@@ -55,6 +55,7 @@ struct reseq_cuda_index {
     u32* d_lengths = nullptr;     // distinct fragment lengths, ascending (lengths_, fragment_index.hpp:52-55)
     u32 n_lengths = 0;
     std::vector<u32> h_lens;      // fragment lengths, host copy (query-offset tables, argument checks)
+    std::vector<u32> h_lengths;   // sorted distinct lengths, host copy
     std::vector<void*> owned;
 };
 
@@ -404,7 +405,10 @@ locate_patterns_kernel(IndexView iv, const u8* __restrict__ pats, const u64* __r
 // CONTAINED: also derive the containment verdict from the o = 0 query (needs the whole interval: a
 // full search by one lane while 31 wait) -- used only where the rank-anchored search does not apply;
 // otherwise contained_kernel does that with one thread per fragment.
-template <bool CONTAINED>
+constexpr int kStageRank = 272;   // rank entries staged per fragment: <= 255 + alignment slack, a multiple of 4
+constexpr int kStageText = 12;    // packed words staged per fragment
+
+template <bool CONTAINED, bool STAGE = false>
 __global__ void __launch_bounds__(256)
 overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __restrict__ qoff,
                      u32* __restrict__ q_first, u32* __restrict__ q_count, u8* __restrict__ contained,
@@ -426,12 +430,70 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
         u32* qr = s_qr[threadIdx.x >> 5];
         u32* qf0 = s_qf0[threadIdx.x >> 5];
         u32* qf1o = s_qf1o[threadIdx.x >> 5];
-        for (u64 i = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < f1; i += warps) {
-            const u32 len = iv.lens[i];
-            const u64 start = iv.starts[i];
+        // Staging (the north star's "SA blocks in shared memory or via TMA"): everything a fragment's
+        // queries read at consecutive addresses -- its block of the inverse suffix array, rank[start ..
+        // start + len), and its packed text -- is brought into shared memory by TWO bulk copies (TMA,
+        // cp.async.bulk) issued by the warp's first lane, double buffered: the copies for the warp's NEXT
+        // fragment are in flight while the current one is searched, so the queries start from shared
+        // memory instead of behind a chain of global loads (starts/lens -> rank, text).
+        __shared__ __align__(16) u32 s_rk[8][2][kStageRank];
+        __shared__ __align__(16) u64 s_tx[8][2][kStageText];
+        __shared__ __align__(8) u64 s_sbar[8][2];
+        const int wib = threadIdx.x >> 5;
+        if (lane == 0) {
+            mbar_init(&s_sbar[wib][0], 1);
+            mbar_init(&s_sbar[wib][1], 1);
+        }
+        __syncwarp();
+        auto stageable = [&](u64 st, u32 ln) {   // both copies 16-byte aligned and inside their arrays
+            return ln <= 255u && ((st & ~3ull) + (((st & 3ull) + ln + 3u) & ~3ull)) <= iv.tv.n;
+        };
+        auto issue = [&](u64 st, u32 ln, int b) {   // lane 0
+            const u64 r0 = st & ~3ull;
+            const u32 cnt = static_cast<u32>(((st - r0) + ln + 3u) & ~3ull);
+            const u64 w0 = (st >> 5) & ~1ull;
+            const u32 nw = static_cast<u32>((((st + ln + 31) >> 5) - w0 + 3u) & ~1ull);
+            mbar_expect_tx(&s_sbar[wib][b], cnt * 4u + nw * 8u);
+            tma_load_1d(s_rk[wib][b], iv.rank + r0, cnt * 4u, &s_sbar[wib][b]);
+            tma_load_1d(s_tx[wib][b], iv.tv.packed + w0, nw * 8u, &s_sbar[wib][b]);
+        };
+        const u64 i_first = f0 + ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+        // fragment descriptors one iteration ahead (registers), copies one iteration ahead (shared memory)
+        u64 start_n = 0;
+        u32 len_n = 0;
+        bool staged_n = false;
+        if (i_first < f1) {
+            start_n = iv.starts[i_first];
+            len_n = iv.lens[i_first];
+            staged_n = STAGE && stageable(start_n, len_n);
+            if (staged_n && lane == 0) issue(start_n, len_n, 0);
+        }
+        u32 uses[2] = {0u, 0u};   // completed phases of each buffer's barrier
+        int buf = 0;
+        for (u64 i = i_first; i < f1; i += warps, buf ^= 1) {
+            const u32 len = len_n;
+            const u64 start = start_n;
+            const bool staged = staged_n;
+            if (i + warps < f1) {   // next fragment: descriptor now, copies into the other buffer
+                start_n = iv.starts[i + warps];
+                len_n = iv.lens[i + warps];
+                staged_n = STAGE && stageable(start_n, len_n);
+                __syncwarp();       // (every lane is done with the other buffer: it was the fragment before this one)
+                if (staged_n && lane == 0) issue(start_n, len_n, buf ^ 1);
+            }
             const u64 qbase = qoff[i - f0];
             const u32 nq = static_cast<u32>(qoff[i - f0 + 1] - qbase);
             const u32 self = iv.start_inv[i];
+            const u32* rk = nullptr;
+            const u64* tx = nullptr;
+            u32 tx_bit0 = 0;
+            if (staged) {
+                mbar_wait(&s_sbar[wib][buf], uses[buf] & 1u);
+                ++uses[buf];
+                rk = s_rk[wib][buf] + (start & 3ull);
+                tx = s_tx[wib][buf];
+                tx_bit0 = 2u * static_cast<u32>(start - (((start >> 5) & ~1ull) << 5));
+            }
             u32 queued = 0, mine = 0;
             auto work_off = [&](u32 count) {   // the first `count` (<= 32) queue entries
                 if (lane < count) {
@@ -457,7 +519,21 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
                 bool has = false;
                 u32 r = 0, b0 = 0, b1 = 0;
                 if (o < nq) {
-                    residual_bracket(iv, start + o, len - o, &r, &b0, &b1);
+                    if (staged) {   // the query's own rank and its first sD bases, from shared memory
+                        r = rk[o];
+                        b0 = 0;
+                        b1 = iv.k;
+                        if (iv.sdir && len - o >= static_cast<u32>(iv.sD)) {
+                            const u32 bit = tx_bit0 + 2u * o, wi = bit >> 6, sh = bit & 63u;
+                            const u64 hi = tx[wi], lo = tx[wi + 1];
+                            const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+                            const u32 x = static_cast<u32>(win >> (64 - 2 * iv.sD));
+                            b0 = iv.sdir[x];
+                            b1 = iv.sdir[x + 1];
+                        }
+                    } else {
+                        residual_bracket(iv, start + o, len - o, &r, &b0, &b1);
+                    }
                     has = b0 < b1;
                     if (!has) {   // the diagonal cannot be inside an empty bracket either
                         q_first[qbase + o] = b0;
@@ -818,8 +894,13 @@ int launch_overlap_count(reseq_cuda_ctx* ctx, const IndexView& iv, u32 min_overl
     cudaStream_t s = ctx->stream;
     if (iv.tv.packed && iv.sdir) {
         RSQ_LAUNCH_BEGIN(ctx, "overlap_count_kernel");
-        overlap_count_kernel<false><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained,
-                                                         rawcount);
+        if (ctx->opt_overlap_stage != 0 && (reinterpret_cast<uintptr_t>(iv.rank) & 15) == 0 &&
+            (reinterpret_cast<uintptr_t>(iv.tv.packed) & 15) == 0)
+            overlap_count_kernel<false, true><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained,
+                                                                   rawcount);
+        else
+            overlap_count_kernel<false, false><<<grid, 256, 0, s>>>(iv, min_overlap, f0, f1, d_qoff, q_first, q_count, d_contained,
+                                                                    rawcount);
         RSQ_LAUNCH_END(ctx);
         RSQ_LAUNCH_BEGIN(ctx, "contained_kernel");
         contained_kernel<<<grid_1d(ctx, f1 - f0, 256), 256, 0, s>>>(iv, f0, f1, d_contained);
@@ -853,31 +934,8 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     // The reference can only build a fragment_set through make_fragment_set (sequence.hpp:103-124),
     // which guarantees this layout; the C ABI takes raw arrays, so it is checked here, O(k) on the host:
     // starts[0] == 0, strictly ascending, inside the text, every fragment non-empty and preceded by a
-    // separator.  (Separators INSIDE a fragment are not looked for: that is O(n).)
-    if (starts[0] != 0) return fail(RESEQ_INVALID_ARGUMENT, "starts[0] must be 0 (sequence.hpp:119)");
-    for (size_t i = 1; i < k; ++i) {
-        const uint64_t a = starts[i - 1], b = starts[i];
-        if (b >= n || b < a + 2 || concat[b - 1] != 0)
-            return fail(RESEQ_INVALID_ARGUMENT, "starts[" + std::to_string(i) + "] does not follow a separator-terminated, non-empty fragment (sequence.hpp:60-62,110)");
-    }
-    if (static_cast<uint64_t>(starts[k - 1]) + 2 > n)
-        return fail(RESEQ_INVALID_ARGUMENT, "the last fragment is empty (sequence.hpp:110)");
-    // fragment lengths (sequence.hpp:78-83) and the sorted distinct lengths (lengths_, fragment_index.hpp:52-55)
-    // come out of the same pass over `starts`: nothing is read back from the device for them
-    std::vector<u32> h_lens(k);
-    u32 max_len = 0;
-    for (size_t i = 0; i < k; ++i) {
-        h_lens[i] = static_cast<u32>((i + 1 < k ? starts[i + 1] : n) - 1 - starts[i]);
-        max_len = std::max(max_len, h_lens[i]);
-    }
-    std::vector<u32> distinct;
-    {
-        std::vector<bool> seen(static_cast<size_t>(max_len) + 1, false);
-        for (u32 v : h_lens) seen[v] = true;
-        for (size_t v = 0; v < seen.size(); ++v)
-            if (seen[v]) distinct.push_back(static_cast<u32>(v));
-    }
-
+    // separator.  (Separators INSIDE a fragment are not looked for: that is O(n).)  The check runs below, under the
+    // host-to-device copy of the text.
     auto* ix = new reseq_cuda_index();
     ix->ctx = ctx;
     ix->n = n;
@@ -909,16 +967,39 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     IX_TRY(dev_alloc(ix, &ix->d_start_inv, k));
     IX_TRY(dev_alloc(ix, &ix->d_packed, n / 32 + 8));
     IX_TRY(dev_alloc(ix, &ix->d_sent, n / 64 + 8));
-    IX_CUDA(cudaMemcpyAsync(ix->d_text, concat, n, cudaMemcpyHostToDevice, s));
-    IX_CUDA(cudaMemcpyAsync(ix->d_starts, starts, sizeof(u32) * k, cudaMemcpyHostToDevice, s));
-    ix->h_lens = std::move(h_lens);
+    IX_CUDA(cudaMemcpyAsync(ix->d_text, concat, n, cudaMemcpyHostToDevice, s));   // (page-locked text: the DMA runs under the host loop below)
+    if (starts[0] != 0) return bail(fail(RESEQ_INVALID_ARGUMENT, "starts[0] must be 0 (sequence.hpp:119)"));
+    for (size_t i = 1; i < k; ++i) {
+        const uint64_t a = starts[i - 1], b = starts[i];
+        if (b >= n || b < a + 2 || concat[b - 1] != 0)
+            return bail(fail(RESEQ_INVALID_ARGUMENT, "starts[" + std::to_string(i) + "] does not follow a separator-terminated, non-empty fragment (sequence.hpp:60-62,110)"));
+    }
+    if (static_cast<uint64_t>(starts[k - 1]) + 2 > n)
+        return bail(fail(RESEQ_INVALID_ARGUMENT, "the last fragment is empty (sequence.hpp:110)"));
+    // fragment lengths (sequence.hpp:78-83) and the sorted distinct lengths (lengths_, fragment_index.hpp:52-55)
+    // come out of the same pass over `starts`: nothing is read back from the device for them
+    std::vector<u32>& h_lens = ix->h_lens;
+    h_lens.resize(k);
+    u32 max_len = 0;
+    for (size_t i = 0; i < k; ++i) {
+        h_lens[i] = static_cast<u32>((i + 1 < k ? starts[i + 1] : n) - 1 - starts[i]);
+        max_len = std::max(max_len, h_lens[i]);
+    }
+    std::vector<u32>& distinct = ix->h_lengths;
+    {
+        std::vector<bool> seen(static_cast<size_t>(max_len) + 1, false);
+        for (u32 v : h_lens) seen[v] = true;
+        for (size_t v = 0; v < seen.size(); ++v)
+            if (seen[v]) distinct.push_back(static_cast<u32>(v));
+    }
+
     ix->max_len = max_len;
     ix->n_lengths = static_cast<u32>(distinct.size());
     ix->min_len = distinct.front();
     IX_TRY(dev_alloc(ix, &ix->d_lengths, distinct.size()));
-    IX_CUDA(cudaMemcpyAsync(ix->d_lens, ix->h_lens.data(), sizeof(u32) * k, cudaMemcpyHostToDevice, s));
+    IX_CUDA(cudaMemcpyAsync(ix->d_starts, starts, sizeof(u32) * k, cudaMemcpyHostToDevice, s));
+    IX_CUDA(cudaMemcpyAsync(ix->d_lens, h_lens.data(), sizeof(u32) * k, cudaMemcpyHostToDevice, s));        // (both vectors live in the index)
     IX_CUDA(cudaMemcpyAsync(ix->d_lengths, distinct.data(), sizeof(u32) * distinct.size(), cudaMemcpyHostToDevice, s));
-    IX_CUDA(cudaStreamSynchronize(s));   // `distinct` is a local: its copy must be done before it goes (the text copy is the long one)
 
     // suffix array (fragment_index.hpp:37)
     IX_TRY(ctx->reserve(sa_workspace_bytes(n)));

@@ -70,8 +70,11 @@ static int launch_pass_dpw(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, con
     // only the descriptor words of the tiles this pass really has need clearing
     RSQ_CUDA(cudaMemsetAsync(lookback, 0, sizeof(u64) * tiles * (kRadix / DPW), ctx->stream));
     RSQ_LAUNCH_BEGIN(ctx, (pass_name<KeyT, HAS_VAL>()));
+    // bulk tile loads need 16-byte aligned sources (the arena's are; a caller's arrays may not be)
+    const int use_tma = ctx->opt_sort_tma != 0 && (reinterpret_cast<uintptr_t>(kin) & 15) == 0 &&
+                        (!HAS_VAL || (reinterpret_cast<uintptr_t>(vin) & 15) == 0);
     kern<<<static_cast<unsigned>(tiles), BLOCK, smem, ctx->stream>>>(
-        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, emit);
+        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, emit, use_tma);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;

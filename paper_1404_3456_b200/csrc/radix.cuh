@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? (ITEMS <= 8 ? 6 : 4) : 
 onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,
                 u32 mask, const u32* __restrict__ digit_base, u64* __restrict__ lookback,
-                u32* __restrict__ ticket, EMIT emit) {
+                u32* __restrict__ ticket, EMIT emit, int use_tma) {
     static_assert(BLOCK >= kRadix && BLOCK % 32 == 0, "one thread per digit is assumed");
     static_assert(!EMIT::kActive || sizeof(KeyT) == 8, "emit hooks look at 64-bit records");
     using Cfg = OnesweepCfg<KeyT, HAS_VAL, BLOCK, ITEMS>;
@@ -203,9 +203,11 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     const int warp = tid >> 5;
     const unsigned lane = lane_id();
 
+    __shared__ __align__(8) u64 s_bar;   // completion of the tile's bulk load
     if (tid == 0) {
         *s_tile = atomicAdd(ticket, 1u);
         if (EMIT::kActive) s_emit[0] = 0;
+        if (use_tma) mbar_init(&s_bar, 1);
     }
     {
         uint4* z = reinterpret_cast<uint4*>(s_whist);
@@ -222,7 +224,24 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     u32 val[ITEMS];
     const u32 wbase = warp * (ITEMS * 32) + lane;
     auto load_key = [&](u64 i) -> KeyT { return static_cast<const KeyT*>(keys_in_raw)[i]; };
-    if (full) {
+    if (full && use_tma) {
+        // The tile is one contiguous stretch of HBM: a single elected thread has the TMA engine move it
+        // into the exchange buffer (cp.async.bulk, completion counted in bytes on an mbarrier) instead of
+        // ITEMS global loads per thread; the threads then pick their keys up from shared memory.  (The
+        // buffer is rewritten by the exchange only after the two barriers below.)
+        if (tid == 0) {
+            mbar_expect_tx(&s_bar, static_cast<u32>(TILE * (sizeof(KeyT) + (HAS_VAL ? sizeof(u32) : 0))));
+            tma_load_1d(s_keys, static_cast<const KeyT*>(keys_in_raw) + tile_base, static_cast<u32>(TILE * sizeof(KeyT)), &s_bar);
+            if (HAS_VAL) tma_load_1d(s_vals, vals_in + tile_base, static_cast<u32>(TILE * sizeof(u32)), &s_bar);
+        }
+        mbar_wait(&s_bar, 0);
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) key[j] = s_keys[wbase + j * 32];
+        if (HAS_VAL) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) val[j] = s_vals[wbase + j * 32];
+        }
+    } else if (full) {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) key[j] = load_key(tile_base + wbase + j * 32);
         if (HAS_VAL) {

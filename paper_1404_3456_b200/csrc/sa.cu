@@ -963,6 +963,25 @@ refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent
 // 4^16 = 4.3 G keys, so a group is one locus but for chance repeats; the fourth digit pass buys
 // groups that need no sorting at all.
 
+// Stages the packed words of reads [r0, r0 + nr) of a uniform read set; returns the bit offset of
+// read r0's first base inside the staged words.
+// One bulk copy (TMA) per CTA: the stretch is contiguous; the caller's __syncthreads() follows.  The copy
+// starts at an even word (16-byte aligned) and covers an even number of words.
+__device__ __forceinline__ u32 stage_reads(const u64* __restrict__ packed, u64* __restrict__ s_w, u64 r0, u32 nr, u32 period) {
+    __shared__ __align__(8) u64 s_bar;
+    const u64 base0 = r0 * period;
+    const u64 w0 = (base0 >> 5) & ~1ull;
+    const u32 nw = (static_cast<u32>(((base0 + static_cast<u64>(nr) * period + 31) >> 5) - w0) + 3u) & ~1u;   // the packed array is padded
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        mbar_expect_tx(&s_bar, nw * 8u);
+        tma_load_1d(s_w, packed + w0, nw * 8u, &s_bar);
+    }
+    __syncthreads();          // the barrier object is initialised for everybody ...
+    mbar_wait(&s_bar, 0);     // ... and the words have landed
+    return 2 * static_cast<u32>(base0 - (w0 << 5));
+}
+
 // Speculative route (build_sa_device): the pack kernel's verdict -- flags[0] != 0: a byte outside
 // {A,C,G,T,0}; flags[1]: number of separators -- against what the route was launched on.
 __global__ void route_check_kernel(const u32* __restrict__ flags, u32 reads, u32* __restrict__ bad) {
@@ -980,23 +999,18 @@ __global__ void __launch_bounds__(256)
 gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0, u64 k, u64* __restrict__ elems,
                    u32* __restrict__ g_hist) {
     // reads [read0, read0 + k) of the set (the whole set: read0 = 0); record t * k + (read - read0)
-    __shared__ u64 s_w[kUniReads * kUniMaxPeriod / 32 + 4];
+    __shared__ __align__(16) u64 s_w[kUniReads * kUniMaxPeriod / 32 + 8];
     __shared__ u32 s_hist[4 * kRadix];
     for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
     const u64 r0 = static_cast<u64>(blockIdx.x) * kUniReads;   // within the slice
     const u32 nr = static_cast<u32>(k - r0 < kUniReads ? k - r0 : kUniReads);
-    const u64 base0 = (read0 + r0) * period;
-    const u64 w0 = base0 >> 5;
-    const u32 off0 = static_cast<u32>(base0 & 31);
-    const u32 nw = static_cast<u32>(((base0 + static_cast<u64>(nr) * period + 31) >> 5) - w0) + 2;   // the packed array is padded
-    for (u32 i = threadIdx.x; i < nw; i += blockDim.x) s_w[i] = packed[w0 + i];
-    __syncthreads();
+    const u32 bit0 = stage_reads(packed, s_w, read0 + r0, nr, period);   // one TMA bulk load + the block barrier
     const u32 total = kUniReads * period;
     for (u32 idx = threadIdx.x; idx < total; idx += blockDim.x) {
         const u32 rl = idx & (kUniReads - 1), t = idx / kUniReads;    // lanes = consecutive reads: coalesced stores
         if (rl >= nr) continue;
         const u32 pl = rl * period + (period - 1 - t);
-        const u32 bit = 2 * (off0 + pl);
+        const u32 bit = bit0 + 2 * pl;
         const u32 wi = bit >> 6, sh = bit & 63;
         const u64 hi = s_w[wi], lo = s_w[wi + 1];
         const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
@@ -1216,6 +1230,10 @@ window_scatter_kernel(const u64* __restrict__ rec, u64 n, int win_bits, u32* __r
         const u64 r = rec[base + size - 1];
         s_win[static_cast<u32>(r >> 32) & mask] = static_cast<u32>(r);
     }
+    // (Measured and dropped: the window leaving as ONE TMA bulk store issued by an elected thread --
+    //  cp.async.bulk.global.shared::cta, 32 KB -- ran at 0.269 ms against 0.242 for the 128-bit stores
+    //  of all 512 threads below: the CTA ends on the copy engine's read of the window instead of
+    //  overlapping its stores with the next CTA's loads.  profiles/r2_negative_results.md.)
     __syncthreads();
     if ((reinterpret_cast<uintptr_t>(rank) & 15) == 0) {   // the caller's array may be aligned to 4 bytes only
         uint4* out4 = reinterpret_cast<uint4*>(rank + base);
@@ -1601,20 +1619,10 @@ __device__ __forceinline__ void for_each_suffix_of_read(const u64* __restrict__ 
     }
 }
 
-// Stages the packed words of reads [r0, r0 + nr) of a uniform read set; returns the bit offset of
-// read r0's first base inside the staged words.
-__device__ __forceinline__ u32 stage_reads(const u64* __restrict__ packed, u64* __restrict__ s_w, u64 r0, u32 nr, u32 period) {
-    const u64 base0 = r0 * period;
-    const u64 w0 = base0 >> 5;
-    const u32 nw = static_cast<u32>(((base0 + static_cast<u64>(nr) * period + 31) >> 5) - w0) + 2;   // the packed array is padded
-    for (u32 i = threadIdx.x; i < nw; i += blockDim.x) s_w[i] = packed[w0 + i];
-    return 2 * static_cast<u32>(base0 & 31);
-}
-
 // Histogram of the 12-bit key prefix over the suffixes of reads [read0, read0 + count).
 __global__ void __launch_bounds__(kShReads)
 shard_hist_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0, u64 count, u32* __restrict__ g_hist) {
-    __shared__ u64 s_w[kShReads * kUniMaxPeriod / 32 + 4];
+    __shared__ __align__(16) u64 s_w[kShReads * kUniMaxPeriod / 32 + 8];
     __shared__ u32 s_hist[1 << kShPrefixBits];
     for (int i = threadIdx.x; i < (1 << kShPrefixBits); i += blockDim.x) s_hist[i] = 0;
     const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
@@ -1635,7 +1643,7 @@ shard_hist_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0,
 __global__ void __launch_bounds__(kShReads)
 shard_count_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 plo, u32 phi, u32 tiles,
                            u32* __restrict__ counts) {
-    __shared__ u64 s_w[kShReads * kUniMaxPeriod / 32 + 4];
+    __shared__ __align__(16) u64 s_w[kShReads * kUniMaxPeriod / 32 + 8];
     __shared__ u32 s_cnt[kUniMaxPeriod + 1];
     for (int i = threadIdx.x; i <= static_cast<int>(kUniMaxPeriod); i += blockDim.x) s_cnt[i] = 0;
     const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
@@ -1657,7 +1665,7 @@ shard_count_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u3
 __global__ void __launch_bounds__(kShReads)
 shard_write_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 plo, u32 phi, u32 tiles,
                            const u32* __restrict__ offsets, u64* __restrict__ out, u32* __restrict__ g_hist) {
-    __shared__ u64 s_w[kShReads * kUniMaxPeriod / 32 + 4];
+    __shared__ __align__(16) u64 s_w[kShReads * kUniMaxPeriod / 32 + 8];
     __shared__ unsigned short s_wcnt[kShReads / 32][kUniMaxPeriod + 1];   // kept per (warp, t), then exclusive over warps
     __shared__ u32 s_hist[4 * kRadix];                                    // digit histograms of the bucket's four sort passes
     for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;

@@ -142,6 +142,38 @@ def test_overlap_lists_on_read_sets(rq, ex, oracle):
     _check_overlaps(rq, ex, oracle, [g[s:s + 50] for s in rng2.integers(0, 250, 2000)], "dna", 10)   # 400x coverage
 
 
+def test_overlap_search_without_staging_and_with_ragged_long_reads(rq, oracle):
+    """The unstaged form of the count kernel (overlap_stage = 0), and read sets whose fragments are
+    too long (> 255) or too ragged for the staged one: same lists."""
+    e = rq.Executor(0)
+    try:
+        e.set_option("overlap_stage", 0)
+        rng = np.random.default_rng(58)
+        _check_overlaps(rq, e, oracle, shotgun(rng, 20_000, 3_000, 100, 100), "dna", 20)
+    finally:
+        e.close()
+    e = rq.Executor(0)
+    try:
+        rng = np.random.default_rng(59)
+        _check_overlaps(rq, e, oracle, shotgun(rng, 30_000, 800, 200, 400), "dna", 25)     # mostly longer than 255
+        _check_overlaps(rq, e, oracle, shotgun(rng, 10_000, 2_000, 1, 300), "dna", 3)      # every alignment of start and length
+    finally:
+        e.close()
+
+
+def test_index_rejects_a_layout_that_is_not_a_fragment_set(rq, ex):
+    """The C ABI takes raw (concat, starts) arrays: what make_fragment_set guarantees (sequence.hpp:103-124)
+    is checked before anything is indexed with them."""
+    text, starts = rq.synth_read_text(5_000, 50, 100)
+    for bad in (starts[::-1].copy(),                                   # not ascending
+                np.concatenate([starts[:50], starts[49:50], starts[50:]]),   # duplicate start (an empty fragment)
+                np.concatenate([starts[:-1], [text.size + 10]]).astype(np.uint32),   # beyond the text
+                (starts + 1).astype(np.uint32)):                        # starts[0] != 0, not behind separators
+        with pytest.raises(ValueError):
+            rq.FragmentIndex(rq.fragment_set_from_text(text, bad), ex)
+    rq.FragmentIndex(rq.fragment_set_from_text(text, starts), ex).close()
+
+
 def test_greedy_reconstruction_matches_the_oracle(rq, ex, oracle):
     """overlap.hpp:80-113 end to end: device overlaps + host merge == the reference loop."""
     # the paper's example: SPEC.md:300, PAPER.md:146-147
