@@ -67,7 +67,7 @@ struct reseq_cuda_ctx {
     int opt_shortcut = 1;      // sentinel-distance shortcut in the refine kernel (tuning / tests)
     int opt_lookahead = 8;     // onesweep look-back descriptors in flight per digit (1..8)
     int opt_sort_cfg = 0;      // onesweep tile shape (0 = default tuning)
-    int opt_overlap_stage = 1; // overlap search: a fragment's rank block + packed text staged in shared memory by TMA, double buffered
+    int opt_overlap_stage = 0; // overlap search: a fragment's rank block + packed text staged in shared memory by TMA, double buffered (measured slower: off)
     int opt_sort_tma = 0;      // onesweep: full tiles loaded by one TMA bulk copy (measured 4 % slower than per-thread loads: off)
     int opt_lookback_pack = 1; // two digits per look-back descriptor word when n < 2^30 (0: always one)
     int opt_uniform = 1;       // transposed-record path for uniform read sets (0: general paths only)

@@ -22,6 +22,8 @@
 // positions and one exclusive scan.  sdir is the same table counted over fragment-start
 // suffixes only, indexing start_rank_list.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -178,12 +180,13 @@ __device__ __forceinline__ u32 lower_bound_u32(const u32* __restrict__ v, u32 l,
 
 __global__ void lens_kernel(const u32* __restrict__ starts, u64 k, u64 n, u32* __restrict__ lens,
                             const u32* __restrict__ rank, u32* __restrict__ keys, u32* __restrict__ ids,
-                            u32* __restrict__ max_len) {
+                            u32* __restrict__ max_len, const u8* __restrict__ text) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     u32 local_max = 0;
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
         const u64 end = (i + 1 < k ? starts[i + 1] : n) - 1;  // sequence.hpp:78-83
         const u32 len = static_cast<u32>(end - starts[i]);
+        if (text[end] != 0) atomicOr(max_len + 1, 1u);        // every fragment ends at a separator (sequence.hpp:60-62)
         lens[i] = len;
         keys[i] = rank[starts[i]];
         ids[i] = static_cast<u32>(i);
@@ -436,11 +439,14 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
         // cp.async.bulk) issued by the warp's first lane, double buffered: the copies for the warp's NEXT
         // fragment are in flight while the current one is searched, so the queries start from shared
         // memory instead of behind a chain of global loads (starts/lens -> rank, text).
-        __shared__ __align__(16) u32 s_rk[8][2][kStageRank];
-        __shared__ __align__(16) u64 s_tx[8][2][kStageText];
-        __shared__ __align__(8) u64 s_sbar[8][2];
-        const int wib = threadIdx.x >> 5;
-        if (lane == 0) {
+        // (measured: 3.20 ms against 2.88 for the unstaged form at config 2 -- the per-lane loads of ~50
+        //  resident warps hide the chain better than one elected lane's copies; kept as an option,
+        //  "overlap_stage", off by default.  profiles/r2_negative_results.md.)
+        __shared__ __align__(16) u32 s_rk[STAGE ? 8 : 1][2][STAGE ? kStageRank : 4];
+        __shared__ __align__(16) u64 s_tx[STAGE ? 8 : 1][2][STAGE ? kStageText : 2];
+        __shared__ __align__(8) u64 s_sbar[STAGE ? 8 : 1][2];
+        const int wib = STAGE ? threadIdx.x >> 5 : 0;
+        if (STAGE && lane == 0) {
             mbar_init(&s_sbar[wib][0], 1);
             mbar_init(&s_sbar[wib][1], 1);
         }
@@ -957,6 +963,15 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     } while (0)
 
     cudaStream_t s = ctx->stream;
+    const bool dbg = std::getenv("RESEQ_DEBUG") != nullptr;   // phase timestamps (synchronising: for diagnosis only)
+    auto t_prev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!dbg) return;
+        cudaStreamSynchronize(s);
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[reseq] index_create %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_prev).count());
+        t_prev = t;
+    };
     IX_TRY(dev_alloc(ix, &ix->d_text, n));
     IX_TRY(dev_alloc(ix, &ix->d_sa, n));
     IX_TRY(dev_alloc(ix, &ix->d_rank, n));
@@ -967,31 +982,30 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     IX_TRY(dev_alloc(ix, &ix->d_start_inv, k));
     IX_TRY(dev_alloc(ix, &ix->d_packed, n / 32 + 8));
     IX_TRY(dev_alloc(ix, &ix->d_sent, n / 64 + 8));
+    lap("allocations");
     IX_CUDA(cudaMemcpyAsync(ix->d_text, concat, n, cudaMemcpyHostToDevice, s));   // (page-locked text: the DMA runs under the host loop below)
     if (starts[0] != 0) return bail(fail(RESEQ_INVALID_ARGUMENT, "starts[0] must be 0 (sequence.hpp:119)"));
-    for (size_t i = 1; i < k; ++i) {
-        const uint64_t a = starts[i - 1], b = starts[i];
-        if (b >= n || b < a + 2 || concat[b - 1] != 0)
-            return bail(fail(RESEQ_INVALID_ARGUMENT, "starts[" + std::to_string(i) + "] does not follow a separator-terminated, non-empty fragment (sequence.hpp:60-62,110)"));
-    }
-    if (static_cast<uint64_t>(starts[k - 1]) + 2 > n)
-        return bail(fail(RESEQ_INVALID_ARGUMENT, "the last fragment is empty (sequence.hpp:110)"));
-    // fragment lengths (sequence.hpp:78-83) and the sorted distinct lengths (lengths_, fragment_index.hpp:52-55)
-    // come out of the same pass over `starts`: nothing is read back from the device for them
+    // ONE pass over `starts` (it runs under the text's DMA): order and bounds, the fragment lengths
+    // (sequence.hpp:78-83) and which lengths occur (lengths_, fragment_index.hpp:52-55).  That every start
+    // follows a separator byte is checked on the device (lens_kernel), next to the text.
     std::vector<u32>& h_lens = ix->h_lens;
     h_lens.resize(k);
+    std::vector<unsigned char> seen(1024, 0);
     u32 max_len = 0;
     for (size_t i = 0; i < k; ++i) {
-        h_lens[i] = static_cast<u32>((i + 1 < k ? starts[i + 1] : n) - 1 - starts[i]);
-        max_len = std::max(max_len, h_lens[i]);
+        const uint64_t a0 = starts[i], b0 = i + 1 < k ? starts[i + 1] : n;
+        if (b0 > n || b0 < a0 + 2)
+            return bail(fail(RESEQ_INVALID_ARGUMENT, "starts[" + std::to_string(i + 1 < k ? i + 1 : i) +
+                                                         "] does not follow a non-empty fragment inside the text (sequence.hpp:60-62,110)"));
+        const u32 len = static_cast<u32>(b0 - 1 - a0);
+        h_lens[i] = len;
+        if (len >= seen.size()) seen.resize(std::max<size_t>(2 * seen.size(), static_cast<size_t>(len) + 1), 0);
+        seen[len] = 1;
+        max_len = std::max(max_len, len);
     }
     std::vector<u32>& distinct = ix->h_lengths;
-    {
-        std::vector<bool> seen(static_cast<size_t>(max_len) + 1, false);
-        for (u32 v : h_lens) seen[v] = true;
-        for (size_t v = 0; v < seen.size(); ++v)
-            if (seen[v]) distinct.push_back(static_cast<u32>(v));
-    }
+    for (size_t v = 0; v <= max_len; ++v)
+        if (seen[v]) distinct.push_back(static_cast<u32>(v));
 
     ix->max_len = max_len;
     ix->n_lengths = static_cast<u32>(distinct.size());
@@ -1001,12 +1015,14 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     IX_CUDA(cudaMemcpyAsync(ix->d_lens, h_lens.data(), sizeof(u32) * k, cudaMemcpyHostToDevice, s));        // (both vectors live in the index)
     IX_CUDA(cudaMemcpyAsync(ix->d_lengths, distinct.data(), sizeof(u32) * distinct.size(), cudaMemcpyHostToDevice, s));
 
+    lap("host pass + H2D");
     // suffix array (fragment_index.hpp:37)
     IX_TRY(ctx->reserve(sa_workspace_bytes(n)));
     ctx->begin();
     reseq_sa_stats st{};
     IX_TRY(build_sa_device(ctx, ix->d_text, n, ix->d_sa, ix->d_rank, &st, ix->d_packed, ix->d_sent));   // packs once, for both
     ix->dna = st.alphabet == 0;
+    lap("suffix array");
 
     // lengths, start ranks (fragment_index.hpp:40-48), directories
     const int D = choose_dir_bases(n);
@@ -1027,7 +1043,8 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     IX_CUDA(cudaMemsetAsync(counters, 0, 256, s));
     RSQ_LAUNCH_BEGIN(ctx, "lens_kernel");
     lens_kernel<<<grid_1d(ctx, k, 256), 256, 0, s>>>(ix->d_starts, k, n, ix->d_lens, ix->d_rank, keys_a,
-                                                     ids_a, counters);
+                                                     ids_a, counters, ix->d_text);
+    IX_CUDA(cudaMemcpyAsync(ctx->pinned + 64, counters + 1, sizeof(u32), cudaMemcpyDeviceToHost, s));   // layout verdict, read at the end
     RSQ_LAUNCH_END(ctx);
     IX_CUDA(cudaGetLastError());
     if (k > 1) {
@@ -1048,6 +1065,7 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
     invert_kernel<<<grid_1d(ctx, k, 256), 256, 0, s>>>(ix->d_start_frag, k, ix->d_start_inv);
     RSQ_LAUNCH_END(ctx);
     IX_CUDA(cudaGetLastError());
+    lap("start ranks");
     if (ix->dna) {
         ix->dir_bases = D;
         ix->sdir_bases = D < 11 ? D : 11;   // 4^11 entries = 16 MB: L2-resident, and k start suffixes still land ~1 per bucket
@@ -1068,6 +1086,9 @@ int reseq_cuda_index_create(reseq_cuda_ctx* ctx, const uint8_t* concat, size_t n
         }
     }
     IX_CUDA(cudaStreamSynchronize(s));
+    lap("directories");
+    if (*reinterpret_cast<volatile u32*>(ctx->pinned + 64) != 0)
+        return bail(fail(RESEQ_INVALID_ARGUMENT, "a fragment does not end at a separator byte: starts does not describe concat (sequence.hpp:60-62)"));
 #undef IX_TRY
 #undef IX_CUDA
     *out = ix;

@@ -142,18 +142,15 @@ def test_overlap_lists_on_read_sets(rq, ex, oracle):
     _check_overlaps(rq, ex, oracle, [g[s:s + 50] for s in rng2.integers(0, 250, 2000)], "dna", 10)   # 400x coverage
 
 
-def test_overlap_search_without_staging_and_with_ragged_long_reads(rq, oracle):
-    """The unstaged form of the count kernel (overlap_stage = 0), and read sets whose fragments are
-    too long (> 255) or too ragged for the staged one: same lists."""
+def test_overlap_search_with_tma_staging_and_with_ragged_long_reads(rq, oracle):
+    """The TMA-staged form of the count kernel (overlap_stage = 1: a fragment's rank block and packed text
+    brought into shared memory by double-buffered bulk copies) on a uniform read set, and on read sets
+    whose fragments are too long (> 255) or too ragged for staging: same lists as the default form."""
     e = rq.Executor(0)
     try:
-        e.set_option("overlap_stage", 0)
+        e.set_option("overlap_stage", 1)
         rng = np.random.default_rng(58)
         _check_overlaps(rq, e, oracle, shotgun(rng, 20_000, 3_000, 100, 100), "dna", 20)
-    finally:
-        e.close()
-    e = rq.Executor(0)
-    try:
         rng = np.random.default_rng(59)
         _check_overlaps(rq, e, oracle, shotgun(rng, 30_000, 800, 200, 400), "dna", 25)     # mostly longer than 255
         _check_overlaps(rq, e, oracle, shotgun(rng, 10_000, 2_000, 1, 300), "dna", 3)      # every alignment of start and length
@@ -168,7 +165,8 @@ def test_index_rejects_a_layout_that_is_not_a_fragment_set(rq, ex):
     for bad in (starts[::-1].copy(),                                   # not ascending
                 np.concatenate([starts[:50], starts[49:50], starts[50:]]),   # duplicate start (an empty fragment)
                 np.concatenate([starts[:-1], [text.size + 10]]).astype(np.uint32),   # beyond the text
-                (starts + 1).astype(np.uint32)):                        # starts[0] != 0, not behind separators
+                (starts + 1).astype(np.uint32),                         # starts[0] != 0
+                np.concatenate([[0], starts[1:] + 1]).astype(np.uint32)):   # fragments that do not end at a separator (checked on the device)
         with pytest.raises(ValueError):
             rq.FragmentIndex(rq.fragment_set_from_text(text, bad), ex)
     rq.FragmentIndex(rq.fragment_set_from_text(text, starts), ex).close()
