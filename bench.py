@@ -526,6 +526,31 @@ def main():
                             "sort_passes": int(st_r.sort_passes), "init_symbols": int(st_r.init_symbols),
                             "frac_of_8d_model": peak_frac(per_suffix * n, ms_r)}
 
+        # a ragged read set of the same genome and read count (lengths 100 .. L: trimmed reads), default options
+        if G >= 2 * L:
+            rng = np.random.default_rng(7)
+            genome = rq.synth_random_dna(G, 1)
+            lens = rng.integers(max(16, L - 50), L + 1, k)
+            st0 = rng.integers(0, G - L, k)
+            total = int(lens.sum()) + k
+            offs = np.concatenate(([0], np.cumsum(lens + 1)[:-1]))
+            idx = np.minimum(np.repeat(st0 - offs, lens + 1) + np.arange(total), G - 1)
+            rag = genome[idx]
+            rag[offs + lens] = 0
+            del idx
+            d_rag = torch.from_numpy(rag).cuda()
+            e2 = rq.Executor(local_rank)
+            e2.set_stream(stream.cuda_stream)
+            ms_r, st_r = timed_builds(e2, d_rag, total, 3)
+            e2.close()
+            b_r, _, _ = bytes_alg_per_suffix(total, L)
+            routes["ragged_reads"] = {"option": f"default options; read lengths uniform in {max(16, L - 50)}..{L}", "suffixes": total,
+                                      "ms_per_build": ms_r, "msuffixes_per_s": total / (ms_r * 1e-3) / 1e6,
+                                      "vs_default_route_per_suffix": (ms_r / total) / (ms_per_step / n), "rounds": int(st_r.rounds),
+                                      "sort_passes": int(st_r.sort_passes), "init_symbols": int(st_r.init_symbols),
+                                      "frac_of_8d_model": peak_frac(b_r * total, ms_r)}
+            del d_rag, rag
+
     # ---- BASELINE config 3: throughput sweep over n by truncating k ---------------------------------
     sweep = None
     if args.sweep or workload == "c3":

@@ -83,6 +83,9 @@ size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
 /* Tuning / test knobs; results never depend on them.  Unknown names are RESEQ_INVALID_ARGUMENT.
  *   "sa_uniform"      0 switches off the path for uniform read sets (k reads of one length:
  *                     transposed 16-base records, one verified overlap per read); default 1
+ *   "sa_ragged"       0 switches off the path for ragged read sets (reads of mixed lengths <= 254 bases: the
+ *                     uniform path's flow with looked-up terminator distances); default 1.  "sa_uniform" = 0
+ *                     switches off both and leaves the general DNA records
  *   "sa_text_rounds"  maximum number of shared-memory group-refinement rounds (keys fetched from
  *                     the packed text) the DNA paths run before handing over to prefix doubling;
  *                     0 forces pure prefix doubling; default 16

@@ -180,6 +180,7 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
         if (v >= 1 && v <= 8) ctx->opt_lookahead = v;
     }
     if (const char* e = std::getenv("RESEQ_SA_UNIFORM")) ctx->opt_uniform = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_SA_RAGGED")) ctx->opt_ragged = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SPECULATE")) ctx->opt_speculate = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_DOUBLING_LOCAL")) ctx->opt_doubling_local = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SHORTCUT")) ctx->opt_shortcut = std::atoi(e);
@@ -231,6 +232,10 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     }
     if (std::strcmp(name, "sa_uniform") == 0) {
         ctx->opt_uniform = value != 0;
+        return RESEQ_OK;
+    }
+    if (std::strcmp(name, "sa_ragged") == 0) {
+        ctx->opt_ragged = value != 0;
         return RESEQ_OK;
     }
     if (std::strcmp(name, "overlap_stage") == 0) {

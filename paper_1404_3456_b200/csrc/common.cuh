@@ -71,6 +71,7 @@ struct reseq_cuda_ctx {
     int opt_sort_tma = 0;      // onesweep: full tiles loaded by one TMA bulk copy (measured 4 % slower than per-thread loads: off)
     int opt_lookback_pack = 1; // two digits per look-back descriptor word when n < 2^30 (0: always one)
     int opt_uniform = 1;       // transposed-record path for uniform read sets (0: general paths only)
+    int opt_ragged = 1;        // ragged read sets (mixed read lengths <= 254) on the uniform route's flow (0: general records)
     int opt_text_rounds = 16;  // max text-window refinement rounds before prefix doubling takes over
     int opt_doubling_local = 1;  // doubling rounds: groups ordered in shared memory (0: always the global digit passes)
     int opt_speculate = 1;     // start on the previous build's route when the text length matches (verified on device)

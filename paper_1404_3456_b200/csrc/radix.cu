@@ -132,7 +132,7 @@ static int launch_pass(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u
 template <typename KeyT>
 int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, u32* vals_b,
                   size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
-                  u32 skip_mask, bool* in_b, const EmitMultiples* emit_last) {
+                  u32 skip_mask, bool* in_b, const EmitMultiples* emit_last, const EmitStarts* emit_starts_last) {
     *in_b = false;
     if (n == 0 || pt.count == 0) return RESEQ_OK;
     const bool has_val = vals_a != nullptr;
@@ -172,6 +172,14 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
                 flipped = !flipped;
                 continue;
             }
+            if (emit_starts_last && !has_val && p == last_pass) {
+                RSQ_TRY((launch_pass<KeyT, false, EmitStarts>(ctx, kin, kout, nullptr, nullptr, n, pt.shift[p], pt.mask(p),
+                                                              ws.base + p * kRadix, ws.lookback, ws.tickets + p,
+                                                              *emit_starts_last)));
+                KeyT* tk = kin; kin = kout; kout = tk;
+                flipped = !flipped;
+                continue;
+            }
         }
         if (has_val)
             RSQ_TRY((launch_pass<KeyT, true>(ctx, kin, kout, vin, vout, n, pt.shift[p], pt.mask(p),
@@ -189,8 +197,8 @@ int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, 
 }
 
 template int onesweep_sort<u32>(reseq_cuda_ctx*, u32*, u32*, u32*, u32*, size_t, const PassTable&,
-                                const SortWorkspace&, bool, u32, bool*, const EmitMultiples*);
+                                const SortWorkspace&, bool, u32, bool*, const EmitMultiples*, const EmitStarts*);
 template int onesweep_sort<u64>(reseq_cuda_ctx*, u64*, u64*, u32*, u32*, size_t, const PassTable&,
-                                const SortWorkspace&, bool, u32, bool*, const EmitMultiples*);
+                                const SortWorkspace&, bool, u32, bool*, const EmitMultiples*, const EmitStarts*);
 
 }  // namespace rsq

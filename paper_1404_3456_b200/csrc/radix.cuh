@@ -158,6 +158,20 @@ struct EmitMultiples {
         return p == static_cast<u32>(__umul64hi(p, magic)) * period;
     }
 };
+// EmitStarts: the same for ragged read sets -- a record is reported when its position starts a read
+// (position 0, or a separator right before it in the sentinel bitmap: bit 63 - (p % 64) of word p / 64).
+struct EmitStarts {
+    static constexpr bool kActive = true;
+    const u64* sent;
+    u32* list;
+    u32* count;
+    __device__ __forceinline__ bool hit(u64 k) const {
+        const u32 p = static_cast<u32>(k);
+        if (p == 0) return true;
+        const u32 q = p - 1;
+        return (sent[q >> 6] >> (63 - (q & 63))) & 1ull;
+    }
+};
 constexpr int kEmitCap = 510;   // hits staged per tile; the overflow goes out one atomic each
 
 // Digit of a key.  HI (u64 keys, shift >= 32): the digit lies in the upper word, one 32-bit
@@ -456,6 +470,7 @@ int sort_workspace_carve(reseq_cuda_ctx* ctx, size_t n, SortWorkspace* ws);
 template <typename KeyT>
 int onesweep_sort(reseq_cuda_ctx* ctx, KeyT* keys_a, KeyT* keys_b, u32* vals_a, u32* vals_b,
                   size_t n, const PassTable& pt, const SortWorkspace& ws, bool hist_ready,
-                  u32 skip_mask, bool* in_b, const EmitMultiples* emit_last = nullptr);
+                  u32 skip_mask, bool* in_b, const EmitMultiples* emit_last = nullptr,
+                  const EmitStarts* emit_starts_last = nullptr);
 
 }  // namespace rsq

@@ -498,24 +498,42 @@ __device__ __forceinline__ u32 bases16(const u64* __restrict__ packed, u64 q) {
 // ends in the last member, so all members are prefixes of it and (distance, position) is their
 // order -- and never enters the step loop; in the loop the same proof replaces the base-by-base
 // comparison.  The terminator distance is arithmetic there: period - 1 - pos mod period.
-template <bool UNI>
+// MODE: kRefGeneral (the records above), kRefUniform (UNI), kRefRagged (UNI's flow for read sets of mixed
+// lengths: terminator distances from the sentinel bitmap's rank structure -- read id = separators before
+// the position, t = ends[id] - position -- and proofs as one bit per POSITION, see the ragged kernels below).
+enum : int { kRefGeneral = 0, kRefUniform = 1, kRefRagged = 2 };
+constexpr int kRagK = 15;   // ragged records: 15 bases + a 2-bit tag that is 0 for suffixes shorter than that
+
+template <int MODE>
 __global__ void __launch_bounds__(kRefBlock)
 refine_elems_kernel(const u64* __restrict__ packed, const u64* __restrict__ sent, u64 n_text,
                     const u64* __restrict__ elems, u64 m, u32* __restrict__ sa_out,
                     int max_rounds, bool use_shortcut, u32* __restrict__ counters,
                     const u8* __restrict__ cov, u32 period, u64 period_magic,
                     const u32* __restrict__ g_headbits, const u32* __restrict__ g_uncbits,
-                    const u8* __restrict__ g_tileflags) {
-    constexpr int KSYM = UNI ? kUniK : kElemK;             // symbols every member of a group shares
+                    const u8* __restrict__ g_tileflags, const u32* __restrict__ cum = nullptr,
+                    const u32* __restrict__ ends = nullptr) {
+    constexpr bool UNI = MODE != kRefGeneral;
+    constexpr int KSYM = MODE == kRefUniform ? kUniK : (MODE == kRefRagged ? kRagK : kElemK);   // symbols every member of a group shares
     constexpr int KEYSHIFT = kElemKeyShift;                // general records: bits above this are the group key
     constexpr u32 ESCBIT = kElemEscBit;                    // (the uniform path reads its group heads from a bitmap)
     auto term_dist = [&](u32 pos) -> u32 {   // UNI only: symbols before the read's sentinel
-        const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
-        return period - 1u - (pos - q * period);
+        if constexpr (MODE == kRefRagged) {
+            const u32 w = pos >> 6, b = pos & 63u;
+            const u32 q = cum[w] + (b ? static_cast<u32>(__popcll(sent[w] >> (64 - b))) : 0u);   // separators before pos = read id
+            return ends[q] - pos;
+        } else {
+            const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
+            return period - 1u - (pos - q * period);
+        }
     };
     auto covered = [&](u32 pos) -> bool {    // UNI only: proven a prefix of a later member of its group
-        const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
-        return period - 1u - (pos - q * period) <= __ldg(cov + q);
+        if constexpr (MODE == kRefRagged) {
+            return (reinterpret_cast<const u32*>(cov)[pos >> 5] >> (pos & 31u)) & 1u;
+        } else {
+            const u32 q = static_cast<u32>(__umul64hi(pos, period_magic));
+            return period - 1u - (pos - q * period) <= __ldg(cov + q);
+        }
     };
     // n_text: length of the text the positions refer to; m: number of records (equal for a
     // whole-text build, a bucket of it for a multi-GPU rank)
@@ -1181,6 +1199,278 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict
                 hbytes[i >> 3] = static_cast<u8>(x);
                 ubytes[i >> 3] = static_cast<u8>(x >> 8);
                 if (x >> 8) {   // the group of an uncovered member starts in this refine tile or the one before
+                    const u64 tile = i / kRefTile;
+                    tileflags[tile] = 1;
+                    if (tile) tileflags[tile - 1] = 1;
+                }
+            }
+        }
+    }
+}
+
+// ---- ragged read sets: route (i) for reads of mixed lengths ------------------------------------------
+//
+// A read set whose reads differ in length (trimmed reads) has no period to do arithmetic with, but the
+// idea of the uniform path carries over once two things are looked up instead of computed:
+//   * which read a position belongs to and how far its sentinel is: the sentinel bitmap with a count
+//     of separators before every 64-position word (`cum`) gives the read id, `ends[id]` the sentinel;
+//   * the order the records are born in: (terminator distance t, position) is a TRANSPOSITION WITH
+//     RAGGED ROWS -- record slot = (suffixes with a smaller t) + (reads before this one that are at least
+//     t long) -- made by the count / scan / write compaction of the multi-GPU bucket generator, keeping
+//     "t <= length of the read".
+// Records: key32 << 32 | position, key32 = first 15 bases (zero padded from the sentinel on) << 2 | tag,
+// tag = 0 for a suffix of fewer than 15 symbols (final after the sort, like the uniform path's t < 16),
+// 1 otherwise: the accept pass needs no terminator distance at all.  Proofs are one bit per POSITION
+// (n/8 bytes, L2-resident at config 2) set by link_ragged_kernel for the suffixes of a read from the
+// verified offset on.  Reads longer than 254 bases, texts that do not end in a separator: route (ii).
+constexpr u32 kRagMaxLen = 254;
+constexpr int kRagReads = 256;      // reads per CTA of the record generator; thread = read
+
+__global__ void __launch_bounds__(256)
+sent_popc_kernel(const u64* __restrict__ sent, u64 words, u32* __restrict__ out) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 w = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) out[w] = __popcll(sent[w]);
+}
+
+// ends[r] = position of the r-th separator; maxgap = longest read.
+__global__ void __launch_bounds__(256)
+ends_kernel(const u64* __restrict__ sent, const u32* __restrict__ cum, u64 words, u32* __restrict__ ends) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 w = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) {
+        u64 bits = sent[w];
+        u32 at = cum[w];
+        while (bits) {
+            const int lz = __clzll(bits);              // position w * 64 + lz
+            ends[at++] = static_cast<u32>((w << 6) + lz);
+            bits &= ~(1ull << (63 - lz));
+        }
+    }
+}
+__global__ void __launch_bounds__(256)
+maxlen_kernel(const u32* __restrict__ ends, u64 k, u32* __restrict__ out) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    u32 mx = 0;
+    for (u64 r = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; r < k; r += stride)
+        mx = max(mx, ends[r] - (r ? ends[r - 1] + 1u : 0u));
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane_id() == 0 && mx) atomicMax(out, mx);
+}
+
+// Calls f(t, key32, active) for t = tmax down to 0; active: the read has a suffix with t symbols before
+// its sentinel (t <= len).  The trip count is the same for every lane (f may vote).
+template <class F>
+__device__ __forceinline__ void for_each_suffix_ragged(const u64* __restrict__ s_w, u32 bit0, u32 len, u32 tmax, F f) {
+    for (int t = static_cast<int>(tmax); t >= 0; --t) {
+        const bool active = static_cast<u32>(t) <= len;
+        u32 key = 0;
+        if (active) {
+            const u32 bit = bit0 + 2 * (len - t);
+            const u32 wi = bit >> 6, sh = bit & 63;
+            const u64 hi = s_w[wi], lo = s_w[wi + 1];
+            const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+            u32 b15 = static_cast<u32>(win >> 34);                                        // 15 bases
+            if (t < kRagK) b15 = t ? b15 & ~((1u << (2 * (kRagK - t))) - 1u) : 0u;        // zero padded from the sentinel on
+            key = (b15 << 2) | (t >= kRagK ? 1u : 0u);
+        }
+        f(static_cast<u32>(t), key, active);
+    }
+}
+
+// Stages the packed text of reads [r0, r0 + nr) (contiguous: from the first read's start to the last
+// read's sentinel); per thread: bit offset of its read in the staged words and its length.
+__device__ __forceinline__ void stage_ragged(const u64* __restrict__ packed, const u32* __restrict__ ends, u64* __restrict__ s_w,
+                                             u64 r0, u32 nr, u32* my_bit0, u32* my_len, u64* my_start) {
+    __shared__ __align__(8) u64 s_bar;
+    const u64 base0 = r0 ? static_cast<u64>(ends[r0 - 1]) + 1 : 0;
+    const u64 end0 = static_cast<u64>(ends[r0 + nr - 1]) + 1;
+    const u64 w0 = (base0 >> 5) & ~1ull;
+    const u32 nw = (static_cast<u32>(((end0 + 31) >> 5) - w0) + 3u) & ~1u;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        mbar_expect_tx(&s_bar, nw * 8u);
+        tma_load_1d(s_w, packed + w0, nw * 8u, &s_bar);
+    }
+    const bool in = threadIdx.x < nr;
+    const u64 r = r0 + (in ? threadIdx.x : 0u);
+    const u64 st = r ? static_cast<u64>(ends[r - 1]) + 1 : 0;
+    *my_start = st;
+    *my_len = in ? ends[r] - static_cast<u32>(st) : 0u;
+    *my_bit0 = 2 * static_cast<u32>(st - (w0 << 5));
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+}
+
+__global__ void __launch_bounds__(kRagReads)
+ragged_count_kernel(const u64* __restrict__ packed, const u32* __restrict__ ends, u64 k, u32 tiles, u32 tmax,
+                    u32* __restrict__ counts) {
+    __shared__ __align__(16) u64 s_w[kRagReads * (kRagMaxLen + 1) / 32 + 8];
+    __shared__ u32 s_cnt[kRagMaxLen + 2];
+    for (int i = threadIdx.x; i < static_cast<int>(kRagMaxLen) + 2; i += blockDim.x) s_cnt[i] = 0;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kRagReads;
+    const u32 nr = static_cast<u32>(k - r0 < kRagReads ? k - r0 : kRagReads);
+    u32 bit0, len;
+    u64 st;
+    stage_ragged(packed, ends, s_w, r0, nr, &bit0, &len, &st);
+    const bool in = threadIdx.x < nr;
+    // no key is needed to count: a read of length len has one suffix for every t <= len
+    for (int t = static_cast<int>(tmax); t >= 0; --t) {
+        const unsigned b = __ballot_sync(0xffffffffu, in && static_cast<u32>(t) <= len);
+        if (b && lane_id() == 0) atomicAdd(&s_cnt[t], __popc(b));
+    }
+    __syncthreads();
+    for (u32 t = threadIdx.x; t <= tmax; t += blockDim.x) counts[static_cast<u64>(t) * tiles + blockIdx.x] = s_cnt[t];
+}
+
+__global__ void __launch_bounds__(kRagReads)
+ragged_write_kernel(const u64* __restrict__ packed, const u32* __restrict__ ends, u64 k, u32 tiles, u32 tmax,
+                    const u32* __restrict__ offsets, u64* __restrict__ out, u32* __restrict__ g_hist) {
+    __shared__ __align__(16) u64 s_w[kRagReads * (kRagMaxLen + 1) / 32 + 8];
+    __shared__ unsigned short s_wcnt[kRagReads / 32][kRagMaxLen + 2];
+    __shared__ u32 s_hist[4 * kRadix];
+    for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kRagReads;
+    const u32 nr = static_cast<u32>(k - r0 < kRagReads ? k - r0 : kRagReads);
+    u32 bit0, len;
+    u64 st;
+    stage_ragged(packed, ends, s_w, r0, nr, &bit0, &len, &st);
+    const bool in = threadIdx.x < nr;
+    const int warp = threadIdx.x >> 5;
+    for (int t = static_cast<int>(tmax); t >= 0; --t) {
+        const unsigned b = __ballot_sync(0xffffffffu, in && static_cast<u32>(t) <= len);
+        if (lane_id() == 0) s_wcnt[warp][t] = static_cast<unsigned short>(__popc(b));
+    }
+    __syncthreads();
+    for (u32 t = threadIdx.x; t <= tmax; t += blockDim.x) {
+        u32 run = 0;
+        for (int w = 0; w < kRagReads / 32; ++w) {
+            const u32 c = s_wcnt[w][t];
+            s_wcnt[w][t] = static_cast<unsigned short>(run);
+            run += c;
+        }
+    }
+    __syncthreads();
+    for_each_suffix_ragged(s_w, bit0, in ? len : 0u, tmax, [&](u32 t, u32 key, bool active) {
+        const bool keep = in && active;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const u64 slot = static_cast<u64>(offsets[static_cast<u64>(t) * tiles + blockIdx.x]) + s_wcnt[warp][t] +
+                             __popc(b & lanemask_lt());
+            out[slot] = (static_cast<u64>(key) << 32) | (st + (len - t));
+            atomicAdd(&s_hist[key & 0xffu], 1u);
+            atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
+            atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
+            atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
+        }
+    });
+    __syncthreads();
+    hist_flush(s_hist, g_hist, 4);
+}
+
+// One thread per whole read (their sorted indices come from the last digit pass, EmitStarts): the nearest
+// predecessor a of the read's first suffix b in its group is compared with b over its whole length t_a;
+// if equal, every suffix of a's read from a on is a prefix of the suffix the same distance into b -- a
+// later member of its own group -- and gets its bit in `covbits`.
+__global__ void __launch_bounds__(256)
+link_ragged_kernel(const u64* __restrict__ elems, const u32* __restrict__ list, const u32* __restrict__ count,
+                   const u64* __restrict__ packed, const u64* __restrict__ sent, const u32* __restrict__ cum,
+                   const u32* __restrict__ ends, u32* __restrict__ covbits) {
+    const u64 k = *count;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 x = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; x < k; x += stride) {
+        const u64 i = list[x];
+        const u64 e = elems[i];
+        if ((static_cast<u32>(e >> 32) & 3u) == 0) continue;      // a read shorter than the key: final after the sort
+        const u32 pos_b = static_cast<u32>(e);
+        for (u64 s = 1; s <= 16 && s <= i; ++s) {
+            const u64 ea = elems[i - s];
+            if ((ea >> 32) != (e >> 32)) break;
+            const u32 pos_a = static_cast<u32>(ea);
+            const u32 w = pos_a >> 6, bb = pos_a & 63u;
+            const u32 q = cum[w] + (bb ? static_cast<u32>(__popcll(sent[w] >> (64 - bb))) : 0u);
+            const u32 t_a = ends[q] - pos_a;                       // >= 15 (same tag), <= t_b (the run is in (t, pos) order)
+            bool ok = true;
+            for (u32 c = 0; c < t_a && ok; c += 32) {
+                const u64 wa = base_window(packed, static_cast<u64>(pos_a) + c);
+                const u64 wb = base_window(packed, static_cast<u64>(pos_b) + c);
+                const u32 nb = t_a - c < 32 ? t_a - c : 32;
+                ok = ((wa ^ wb) >> (64 - 2 * nb)) == 0;
+            }
+            if (!ok) continue;
+            // positions [pos_a, pos_a + t_a): a handful of words
+            const u32 first = pos_a, last = pos_a + t_a - 1;
+            for (u32 ww = first >> 5; ww <= (last >> 5); ++ww) {
+                u32 mk = 0xffffffffu;
+                if (ww == (first >> 5)) mk &= 0xffffffffu << (first & 31u);
+                if (ww == (last >> 5)) mk &= 0xffffffffu >> (31u - (last & 31u));
+                atomicOr(covbits + ww, mk);
+            }
+            break;
+        }
+    }
+}
+
+// accept_uniform_kernel for ragged records: "shorter than the key" is the record's tag, the proof a bit
+// per position.  Same pair layout, same outputs.
+__global__ void __launch_bounds__(256)
+accept_ragged_kernel(const u64* __restrict__ elems, u64 m, const u32* __restrict__ covbits, u32* __restrict__ sa_out,
+                     u32* __restrict__ headbits, u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
+    const unsigned lane = lane_id();
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    u8* hbytes = reinterpret_cast<u8*>(headbits);
+    u8* ubytes = reinterpret_cast<u8*>(uncbits);
+    for (u64 i0 = ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kAccSpan; i0 < m; i0 += warps * kAccSpan) {
+        u32 ka[kAccRows], kb[kAccRows], pa[kAccRows], pb[kAccRows];
+#pragma unroll
+        for (int c = 0; c < kAccRows; ++c) {
+            const u64 i = i0 + c * 64 + 2 * lane;
+            ulonglong2 v = make_ulonglong2(0, 0);
+            if (i + 1 < m) v = *reinterpret_cast<const ulonglong2*>(elems + i);
+            else if (i < m) v.x = elems[i];
+            ka[c] = static_cast<u32>(v.x >> 32); pa[c] = static_cast<u32>(v.x);
+            kb[c] = static_cast<u32>(v.y >> 32); pb[c] = static_cast<u32>(v.y);
+        }
+        u32 k_before = 0, k_after = 0;
+        if (lane == 0 && i0 > 0) k_before = static_cast<u32>(elems[i0 - 1] >> 32);
+        if (lane == 31 && i0 + kAccSpan < m) k_after = static_cast<u32>(elems[i0 + kAccSpan] >> 32);
+        u32 ca[kAccRows], cb[kAccRows];   // the proof bits, gathered up front
+#pragma unroll
+        for (int c = 0; c < kAccRows; ++c) {
+            const u64 i = i0 + c * 64 + 2 * lane;
+            ca[c] = i < m ? (__ldg(covbits + (pa[c] >> 5)) >> (pa[c] & 31u)) & 1u : 0u;
+            cb[c] = i + 1 < m ? (__ldg(covbits + (pb[c] >> 5)) >> (pb[c] & 31u)) & 1u : 0u;
+        }
+#pragma unroll
+        for (int c = 0; c < kAccRows; ++c) {
+            const u64 i = i0 + c * 64 + 2 * lane;
+            u32 kp = __shfl_up_sync(0xffffffffu, kb[c], 1);
+            u32 kn = __shfl_down_sync(0xffffffffu, ka[c], 1);
+            if (c > 0) {
+                const u32 k31 = __shfl_sync(0xffffffffu, kb[c > 0 ? c - 1 : 0], 31);
+                if (lane == 0) kp = k31;
+            } else if (lane == 0) kp = k_before;
+            if (c + 1 < kAccRows) {
+                const u32 k0 = __shfl_sync(0xffffffffu, ka[c + 1 < kAccRows ? c + 1 : c], 0);
+                if (lane == 31) kn = k0;
+            } else if (lane == 31) kn = k_after;
+            const bool in_a = i < m, in_b = i + 1 < m;
+            const bool short_a = (ka[c] & 3u) == 0, short_b = (kb[c] & 3u) == 0;
+            // (equal keys carry equal tags: "the neighbour is short" needs no test of its own)
+            const bool head_a = in_a && (i == 0 || ka[c] != kp || short_a);
+            const bool head_b = in_b && (kb[c] != ka[c] || short_b);
+            const bool last_a = !in_b || kb[c] != ka[c] || short_b;
+            const bool last_b = i + 2 >= m || kn != kb[c] || short_b;
+            const bool unc_a = in_a && !last_a && !short_a && !ca[c];
+            const bool unc_b = in_b && !last_b && !short_b && !cb[c];
+            if (in_b) *reinterpret_cast<uint2*>(sa_out + i) = make_uint2(pa[c], pb[c]);
+            else if (in_a) sa_out[i] = pa[c];
+            u32 x = (static_cast<u32>(head_a) | (static_cast<u32>(head_b) << 1) | (static_cast<u32>(unc_a) << 8) |
+                     (static_cast<u32>(unc_b) << 9)) << (2 * (lane & 3));
+            x |= __shfl_xor_sync(0xffffffffu, x, 1);
+            x |= __shfl_xor_sync(0xffffffffu, x, 2);
+            if ((lane & 3) == 0 && i < m) {
+                hbytes[i >> 3] = static_cast<u8>(x);
+                ubytes[i >> 3] = static_cast<u8>(x >> 8);
+                if (x >> 8) {
                     const u64 tile = i / kRefTile;
                     tileflags[tile] = 1;
                     if (tile) tileflags[tile - 1] = 1;
@@ -1938,6 +2228,16 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
 // claim counters of both partition passes
 static size_t inverse_scratch_words(size_t n) { return kIpMaxBins + (n >> 13) + 64; }
 
+// Ragged read sets are taken on when there are at most n / kRagMinAvg reads (mean length >= 15: below
+// that the 15-base key sorts nothing) -- which also bounds the tables below.
+constexpr size_t kRagMinAvg = 16;
+static size_t ragged_cells(size_t n) { return ((n / kRagMinAvg) / kRagReads + 2) * (kRagMaxLen + 1) + 1; }
+static size_t ragged_workspace_bytes(size_t n) {
+    auto pad = reseq_cuda_ctx::padded;
+    return pad(sizeof(u32) * (n / 64 + 2)) * 2 + pad(sizeof(u32) * (n / kRagMinAvg + 2)) + pad(sizeof(u32) * (n / 32 + 2)) +
+           2 * pad(sizeof(u32) * ragged_cells(n)) + scan_workspace_bytes(n / 64 + 2) + scan_workspace_bytes(ragged_cells(n)) + 8192;
+}
+
 size_t sa_workspace_bytes(size_t n) {
     auto pad = reseq_cuda_ctx::padded;
     size_t total = 0;
@@ -1949,6 +2249,7 @@ size_t sa_workspace_bytes(size_t n) {
     total += pad(sizeof(u64) * (n / kRankTile + 4)); // rerank descriptors
     total += pad(1024);                              // counters
     total += pad(n / kUniMinPeriod + 2);             // uniform read-set path: proof table, one byte per read
+    total += ragged_workspace_bytes(n);              // ragged read-set path: rank structure of the bitmap, proof bits, slot tables
     total += 2 * pad(sizeof(u32) * (n / 32 + 2 + n / kRefTile / 4 + 2));   // head / uncovered bitmaps, tile flags
     total += pad(sizeof(u32) * inverse_scratch_words(n));
     total += sort_workspace_bytes(n);
@@ -2129,11 +2430,11 @@ int sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, siz
     bool in_b = false;
     RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, m, pt, ws, hist_ready, 0, &in_b));
     st->sort_passes += pt.count;
-    RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<false>, kRefSmem);
+    RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<kRefGeneral>, kRefSmem);
     RSQ_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(u32), s));
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_elems_kernel");
-    refine_elems_kernel<false><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m,
+    refine_elems_kernel<kRefGeneral><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, in_b ? elems_b : elems_a, m,
                                                                   sa_out, max_rounds, use_shortcut, counters, nullptr, 0, 0, nullptr, nullptr, nullptr);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
@@ -2189,10 +2490,10 @@ int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sen
     accept_uniform_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
                                                                        uncbits, tileflags);
     RSQ_LAUNCH_END(ctx);
-    RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<true>, kRefSmem);
+    RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<kRefUniform>, kRefSmem);
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
     RSQ_LAUNCH_BEGIN(ctx, "refine_uniform_kernel");
-    refine_elems_kernel<true><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, sorted, m, sa_out, max_rounds, true,
+    refine_elems_kernel<kRefUniform><<<tiles, kRefBlock, kRefSmem, s>>>(packed, sent, n_text, sorted, m, sa_out, max_rounds, true,
                                                                  counters, cov, period, magic, headbits, uncbits,
                                                                  tileflags);
     RSQ_LAUNCH_END(ctx);
@@ -2251,6 +2552,103 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     RSQ_TRY(uniform_sort_link(ctx, packed, period, elems_a, elems_b, n, true, whole, cov, counters, ws, st, &sorted));
     return uniform_accept_refine(ctx, packed, sent, n, period, sorted, n, cov, headbits, uncbits, sa_out, max_rounds,
                                  counters, st, unfinished, defer_verdict);
+}
+
+// The ragged read-set route on one device.  *applicable = false: not this kind of text (a read longer
+// than 254 bases, too many short reads, no final separator) -- nothing was done; otherwise *unfinished as
+// for the uniform route.
+int ragged_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n, u64 k, u64* elems_a, u64* elems_b,
+                           u32* headbits, u32* uncbits, u32* whole, u32* sa_out, int max_rounds, u32* counters,
+                           const SortWorkspace& ws, reseq_sa_stats* st, bool* applicable, u64* unfinished) {
+    cudaStream_t s = ctx->stream;
+    *applicable = false;
+    *unfinished = 0;
+    if (k == 0 || k > n / kRagMinAvg || n >= (1ull << 32) - 64) return RESEQ_OK;
+    const u64 words = (n + 63) >> 6;
+    u32* cum = ctx->alloc<u32>(n / 64 + 2);
+    u32* popc = ctx->alloc<u32>(n / 64 + 2);
+    u32* ends = ctx->alloc<u32>(n / kRagMinAvg + 2);
+    u32* covbits = ctx->alloc<u32>(n / 32 + 2);
+    u32* counts = ctx->alloc<u32>(ragged_cells(n));
+    u32* offsets = ctx->alloc<u32>(ragged_cells(n));
+    u64* d_total = ctx->alloc<u64>(1);
+    if (!cum || !popc || !ends || !covbits || !counts || !offsets || !d_total)
+        return fail(RESEQ_OUT_OF_MEMORY, "ragged read-set workspace does not fit the reserved arena");
+    // -- rank structure of the sentinel bitmap, separator positions, the longest read ----------------
+    RSQ_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(u32), s));
+    RSQ_LAUNCH_BEGIN(ctx, "sent_popc_kernel");
+    sent_popc_kernel<<<grid_for(ctx, words, 256, 4, 8), 256, 0, s>>>(sent, words, popc);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_TRY(exclusive_scan_device(ctx, popc, cum, words, d_total));
+    RSQ_LAUNCH_BEGIN(ctx, "ends_kernel");
+    ends_kernel<<<grid_for(ctx, words, 256, 4, 8), 256, 0, s>>>(sent, cum, words, ends);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_LAUNCH_BEGIN(ctx, "maxlen_kernel");
+    maxlen_kernel<<<grid_for(ctx, k, 256, 4, 8), 256, 0, s>>>(ends, k, counters + 5);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters + 5, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned + 1, ends + (k - 1), sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    const u32 tmax = *reinterpret_cast<volatile u32*>(ctx->pinned);
+    const u32 last_sep = *reinterpret_cast<volatile u32*>(ctx->pinned + 1);
+    if (tmax > kRagMaxLen || static_cast<u64>(last_sep) + 1 != n) return RESEQ_OK;   // a long read, or text behind the last separator
+    *applicable = true;
+    // -- records in (terminator distance, position) order: count, scan, write ---------------------------
+    const u32 tiles = static_cast<u32>((k + kRagReads - 1) / kRagReads);
+    const size_t cells = static_cast<size_t>(tiles) * (tmax + 1);
+    RSQ_CUDA(cudaMemsetAsync(counts + cells, 0, sizeof(u32), s));
+    RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * 4 * kRadix, s));
+    RSQ_CUDA(cudaMemsetAsync(covbits, 0, sizeof(u32) * (n / 32 + 2), s));
+    RSQ_LAUNCH_BEGIN(ctx, "ragged_count_kernel");
+    ragged_count_kernel<<<tiles, kRagReads, 0, s>>>(packed, ends, k, tiles, tmax, counts);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_TRY(exclusive_scan_device(ctx, counts, offsets, cells + 1, d_total));
+    RSQ_LAUNCH_BEGIN(ctx, "ragged_write_kernel");
+    ragged_write_kernel<<<tiles, kRagReads, 0, s>>>(packed, ends, k, tiles, tmax, offsets, elems_a, ws.hist);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    // -- four digit passes; the last reports where the whole reads landed; one verified overlap per read --
+    const PassTable pt = make_passes(32, 64);
+    bool in_b = false;
+    const EmitStarts emit{sent, whole, counters + 4};
+    RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, n, pt, ws, true, 0, &in_b, nullptr, &emit));
+    st->sort_passes += pt.count;
+    const u64* sorted = in_b ? elems_b : elems_a;
+    RSQ_LAUNCH_BEGIN(ctx, "link_ragged_kernel");
+    link_ragged_kernel<<<grid_for(ctx, k, 256, 1, 16), 256, 0, s>>>(sorted, whole, counters + 4, packed, sent, cum, ends, covbits);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    // -- accept / refine under the proof bits -----------------------------------------------------------------
+    u8* tileflags = reinterpret_cast<u8*>(uncbits + n / 32 + 2);
+    RSQ_CUDA(cudaMemsetAsync(tileflags, 0, n / kRefTile + 2, s));
+    if ((reinterpret_cast<uintptr_t>(sorted) & 15) || (reinterpret_cast<uintptr_t>(sa_out) & 7))
+        return fail(RESEQ_INVALID_ARGUMENT, "record and suffix-array buffers must be 16- / 8-byte aligned");
+    RSQ_LAUNCH_BEGIN(ctx, "accept_ragged_kernel");
+    accept_ragged_kernel<<<grid_for(ctx, n, 256, 8, 8), 256, 0, s>>>(sorted, n, covbits, sa_out, headbits, uncbits, tileflags);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<kRefRagged>, kRefSmem);
+    const unsigned rtiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
+    RSQ_LAUNCH_BEGIN(ctx, "refine_ragged_kernel");
+    refine_elems_kernel<kRefRagged><<<rtiles, kRefBlock, kRefSmem, s>>>(packed, sent, n, sorted, n, sa_out, max_rounds, true, counters,
+                                                                       reinterpret_cast<const u8*>(covbits), 0, 0, headbits, uncbits,
+                                                                       tileflags, cum, ends);
+    RSQ_LAUNCH_END(ctx);
+    RSQ_CUDA(cudaGetLastError());
+    RSQ_CUDA(cudaMemcpyAsync(ctx->pinned, counters, 4 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    RSQ_CUDA(cudaStreamSynchronize(s));
+    const volatile u32* c = reinterpret_cast<volatile u32*>(ctx->pinned);
+    *unfinished = static_cast<u64>(c[0]) + (c[1] ? 1u : 0u);
+    if (std::getenv("RESEQ_DEBUG"))
+        std::fprintf(stderr, "[reseq] ragged refine: records=%zu reads=%llu longest=%u tied_left=%u oversize=%u steps=%u\n", n,
+                     static_cast<unsigned long long>(k), tmax, c[0], c[1], c[2]);
+    if (*unfinished == 0) {
+        st->rounds += c[2];
+        st->refined_tile += n;
+    }
+    return RESEQ_OK;
 }
 
 }  // namespace
@@ -2344,6 +2742,24 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
             return RESEQ_OK;
         }
         st.sort_passes = 0;   // not uniform after all, or a group the window cannot hold: the general paths
+    }
+
+    // -- ragged read sets (reads of mixed lengths <= 254): the uniform route's flow with looked-up
+    //    terminator distances, records born transposed with ragged rows ---------------------------------
+    if (dna && ctx->opt_text_rounds > 0 && ctx->opt_uniform != 0 && ctx->opt_ragged != 0 && n_separators > 0) {
+        bool applicable = false;
+        u64 unfinished = 0;
+        RSQ_TRY(ragged_sort_and_refine(ctx, packed, sent, n, n_separators, keys_a, keys_b, headbits, uncbits, vals_b, d_sa,
+                                       ctx->opt_text_rounds, counters + 4, ws, &st, &applicable, &unfinished));
+        if (applicable && unfinished == 0) {
+            st.init_symbols = kRagK;
+            RSQ_TRY(ctx->sa_ready(d_sa, n));
+            RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, inv_scratch));
+            st.kernel_launches = ctx->launches - launches0;
+            if (stats) *stats = st;
+            return RESEQ_OK;
+        }
+        st.sort_passes = 0;
     }
 
     // -- DNA fast path: 12-base records, 3 digit passes, groups finished from the L2-resident text --

@@ -69,7 +69,7 @@ def check(rq, ex, oracle, text):
         assert np.array_equal(alt.sa, wsa), f"text-round sa differs for text of length {len(text)}"
         assert np.array_equal(alt.rank, wrank)
         alt = rq.build_parallel(text, no_uniform_executor(rq))
-        assert alt.stats.init_symbols != 16
+        assert alt.stats.init_symbols not in (15, 16)
         assert np.array_equal(alt.sa, wsa), f"general-record sa differs for text of length {len(text)}"
         assert np.array_equal(alt.rank, wrank)
     return got
@@ -268,6 +268,65 @@ def test_speculative_route_is_verified_on_the_device(rq, oracle):
             wsa, wrank = oracle.build_sa(t)
             assert np.array_equal(got.sa, wsa) and np.array_equal(got.rank, wrank)
         assert got.stats.init_symbols == 16
+    finally:
+        e.close()
+
+
+def _ragged_reads(rng, genome, k, lo, hi):
+    out = []
+    for _ in range(k):
+        ln = int(rng.integers(lo, hi + 1))
+        st = int(rng.integers(0, len(genome) - ln + 1))
+        out.append(bytes(genome[st:st + ln]) + b"\0")
+    return b"".join(out)
+
+
+def test_ragged_read_sets_take_the_read_set_route(rq, ex, oracle):
+    """Reads of mixed lengths (trimmed reads): records born transposed with ragged rows, 15-base keys with
+    a short-suffix tag, proofs as one bit per position (sa.cu, ragged read sets).  Lengths from 1 to 254,
+    repeats (groups that mix loci), duplicates, reads contained in others, reads shorter than the key."""
+    rng = np.random.default_rng(81)
+    genome = rng.choice([65, 67, 71, 84], 40_000).astype(np.uint8)
+    for lo, hi, k in ((60, 150, 6000), (16, 254, 3000), (1, 40, 5000), (100, 101, 4000), (254, 254, 40), (15, 17, 6000)):
+        text = _ragged_reads(rng, genome, k, lo, hi)
+        got = check(rq, ex, oracle, text)
+        if len(text) // k >= 16 and lo != hi:
+            assert got.stats.init_symbols == 15, (lo, hi)          # the ragged route took it
+    unit = bytes(rng.choice([65, 67, 71, 84], 3000).astype(np.uint8))
+    rep = np.frombuffer(unit + unit[:1500] + unit[500:2500] + unit, np.uint8)     # repeats: groups mix loci
+    text = _ragged_reads(rng, rep, 5000, 40, 120)
+    text += text[: text.index(b"\0", 4000) + 1]                                   # duplicated reads
+    got = check(rq, ex, oracle, text)
+    assert got.stats.init_symbols == 15
+    low = rng.choice([65, 67], 5000).astype(np.uint8)                             # two-letter genome: long ties
+    check(rq, ex, oracle, _ragged_reads(rng, low, 3000, 20, 90))
+    # not this route: a read of 255 bases, text behind the last separator, mostly tiny reads
+    assert check(rq, ex, oracle, _ragged_reads(rng, genome, 300, 255, 255) + _ragged_reads(rng, genome, 300, 50, 60)).stats.init_symbols != 15
+    assert check(rq, ex, oracle, _ragged_reads(rng, genome, 2000, 30, 80) + b"ACGT").stats.init_symbols != 15
+    assert check(rq, ex, oracle, _ragged_reads(rng, genome, 4000, 1, 12)).stats.init_symbols != 15
+
+
+def test_ragged_read_set_at_config2_size(rq, oracle):
+    """BASELINE config 2's genome and coverage with read lengths drawn from 100..150: n ~ 116 M suffixes on
+    the ragged route, proved equal to the reference order."""
+    rng = np.random.default_rng(82)
+    genome = rq.synth_random_dna(4_600_000, 1)
+    k = 920_000
+    lens = rng.integers(100, 151, k)
+    starts = rng.integers(0, genome.size - 150, k)
+    total = int(lens.sum()) + k
+    text = np.zeros(total, np.uint8)
+    offs = np.concatenate(([0], np.cumsum(lens + 1)[:-1]))
+    idx = np.repeat(starts - offs, lens + 1) + np.arange(total)        # genome index of every text byte (sentinels: garbage)
+    idx = np.minimum(idx, genome.size - 1)
+    text[:] = genome[idx]
+    text[offs + lens] = 0
+    e = rq.Executor(0)
+    try:
+        got = rq.build_parallel(text, e)
+        assert got.stats.init_symbols == 15 and got.stats.refined_global == 0
+        assert oracle.verify_sa(text, got.sa, threads=32) == 0
+        assert np.array_equal(got.rank[got.sa], np.arange(text.size, dtype=np.uint32))
     finally:
         e.close()
 
