@@ -1366,16 +1366,33 @@ ragged_write_kernel(const u64* __restrict__ packed, const u32* __restrict__ ends
     hist_flush(s_hist, g_hist, 4);
 }
 
-// One thread per whole read (their sorted indices come from the last digit pass, EmitStarts): the nearest
-// predecessor a of the read's first suffix b in its group is compared with b over its whole length t_a;
-// if equal, every suffix of a's read from a on is a prefix of the suffix the same distance into b -- a
-// later member of its own group -- and gets its bit in `covbits`.
+// One thread per whole read (their sorted indices come from the last digit pass, EmitStarts).  Two links:
+//   * backward, as in the uniform path: the nearest predecessor a of the read's first suffix b in its group
+//     is compared with b over its whole length t_a; if equal, every suffix of a's read from a on is a prefix
+//     of the suffix the same distance into b -- a later member of its own group;
+//   * forward, which only ragged sets need: a whole read is the LAST of its group when all reads are equally
+//     long, but a longer read that started earlier and ends later comes after it.  b is compared over its
+//     whole length with its successor s; if equal, every suffix of b is a prefix of the suffix the same
+//     distance further into s.
+// Together they reach every member that has a successor from the same locus: take (read q, locus g) and its
+// successor s in the group of g.  No read covering g ends between them, so if s starts at or after q's
+// start, q is the predecessor of whole s in the group of s's start (backward link of s); if s starts before,
+// s is the successor of whole q in the group of q's start (forward link of q).
 __global__ void __launch_bounds__(256)
-link_ragged_kernel(const u64* __restrict__ elems, const u32* __restrict__ list, const u32* __restrict__ count,
+link_ragged_kernel(const u64* __restrict__ elems, u64 m, const u32* __restrict__ list, const u32* __restrict__ count,
                    const u64* __restrict__ packed, const u64* __restrict__ sent, const u32* __restrict__ cum,
                    const u32* __restrict__ ends, u32* __restrict__ covbits) {
     const u64 k = *count;
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    auto mark = [&](u32 first, u32 len) {   // positions [first, first + len): a handful of words
+        const u32 last = first + len - 1;
+        for (u32 ww = first >> 5; ww <= (last >> 5); ++ww) {
+            u32 mk = 0xffffffffu;
+            if (ww == (first >> 5)) mk &= 0xffffffffu << (first & 31u);
+            if (ww == (last >> 5)) mk &= 0xffffffffu >> (31u - (last & 31u));
+            atomicOr(covbits + ww, mk);
+        }
+    };
     for (u64 x = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; x < k; x += stride) {
         const u64 i = list[x];
         const u64 e = elems[i];
@@ -1396,14 +1413,28 @@ link_ragged_kernel(const u64* __restrict__ elems, const u32* __restrict__ list, 
                 ok = ((wa ^ wb) >> (64 - 2 * nb)) == 0;
             }
             if (!ok) continue;
-            // positions [pos_a, pos_a + t_a): a handful of words
-            const u32 first = pos_a, last = pos_a + t_a - 1;
-            for (u32 ww = first >> 5; ww <= (last >> 5); ++ww) {
-                u32 mk = 0xffffffffu;
-                if (ww == (first >> 5)) mk &= 0xffffffffu << (first & 31u);
-                if (ww == (last >> 5)) mk &= 0xffffffffu >> (31u - (last & 31u));
-                atomicOr(covbits + ww, mk);
+            mark(pos_a, t_a);
+            break;
+        }
+        // forward link
+        const u32 wb0 = pos_b >> 6, bb0 = pos_b & 63u;
+        const u32 q_b = cum[wb0] + (bb0 ? static_cast<u32>(__popcll(sent[wb0] >> (64 - bb0))) : 0u);
+        const u32 t_b = ends[q_b] - pos_b;
+        for (u64 s = 1; s <= 16 && i + s < m; ++s) {
+            const u64 es = elems[i + s];
+            if ((es >> 32) != (e >> 32)) break;
+            const u32 pos_s = static_cast<u32>(es);
+            bool ok = true;
+            for (u32 c = 0; c < t_b && ok; c += 32) {
+                const u64 wa = base_window(packed, static_cast<u64>(pos_b) + c);
+                const u64 ws = base_window(packed, static_cast<u64>(pos_s) + c);
+                const u32 nb = t_b - c < 32 ? t_b - c : 32;
+                ok = ((wa ^ ws) >> (64 - 2 * nb)) == 0;
             }
+            // (a successor shorter than t_b symbols cannot pass: its sentinel packs as a base code, but the
+            //  records are in (t, position) order, so every successor has at least t_b symbols)
+            if (!ok) continue;
+            mark(pos_b, t_b);
             break;
         }
     }
@@ -2618,7 +2649,7 @@ int ragged_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* se
     st->sort_passes += pt.count;
     const u64* sorted = in_b ? elems_b : elems_a;
     RSQ_LAUNCH_BEGIN(ctx, "link_ragged_kernel");
-    link_ragged_kernel<<<grid_for(ctx, k, 256, 1, 16), 256, 0, s>>>(sorted, whole, counters + 4, packed, sent, cum, ends, covbits);
+    link_ragged_kernel<<<grid_for(ctx, k, 256, 1, 16), 256, 0, s>>>(sorted, n, whole, counters + 4, packed, sent, cum, ends, covbits);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     // -- accept / refine under the proof bits -----------------------------------------------------------------

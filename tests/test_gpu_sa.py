@@ -230,11 +230,11 @@ def test_texts_that_only_look_uniform(rq, ex, oracle):
         s = int(rng.integers(0, 3900))
         reads.append(g[s:s + L] + b"\0")
     got = check(rq, ex, oracle, b"".join(reads))
-    assert got.stats.init_symbols == 11
+    assert got.stats.init_symbols in (11, 15)   # general records, or the ragged read-set route
     text = bytearray(b"".join(g[int(s):int(s) + 40] + b"\0" for s in rng.integers(0, 3900, 300)))
     text[100], text[40] = 0, 65          # one sentinel moved
     got = check(rq, ex, oracle, bytes(text))
-    assert got.stats.init_symbols == 11
+    assert got.stats.init_symbols in (11, 15)   # general records, or the ragged read-set route
 
 
 def test_speculative_route_is_verified_on_the_device(rq, oracle):
