@@ -1961,72 +1961,99 @@ shard_hist_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0,
 
 // counts[t * tiles + tile] = suffixes with t symbols before their sentinel, of the reads of `tile`,
 // whose key prefix lies in [plo, phi): the flattened array scans into slot bases in (t, read) order.
+// This is the only sweep that looks at every suffix key, so it also leaves the write sweep everything it
+// found: keep[(tile * period + t) * 8 + warp] = the warp's ballot of kept reads at t, wbase[...] = kept
+// reads of the tile's lower warps at t.  The write sweep then touches text only for what it keeps
+// (1/G of the suffixes).  (The first form recomputed every key in all three sweeps: 4.4 ms of a 13.6 ms
+// modelled 8-GPU build at 1 G suffixes, and the one part that does not shrink with G.)
+// The 6-base prefix of the suffix at offset o comes from a window that slides along the read (one
+// shared-memory word per 32 offsets), not from a fresh two-word extraction per offset.
 __global__ void __launch_bounds__(kShReads)
 shard_count_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 plo, u32 phi, u32 tiles,
-                           u32* __restrict__ counts) {
+                           u32* __restrict__ counts, u32* __restrict__ keep, unsigned short* __restrict__ wbase) {
     __shared__ __align__(16) u64 s_w[kShReads * kUniMaxPeriod / 32 + 8];
-    __shared__ u32 s_cnt[kUniMaxPeriod + 1];
-    for (int i = threadIdx.x; i <= static_cast<int>(kUniMaxPeriod); i += blockDim.x) s_cnt[i] = 0;
+    __shared__ unsigned short s_wcnt[kShReads / 32][kUniMaxPeriod + 1];
     const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
     const u32 nr = static_cast<u32>(k - r0 < kShReads ? k - r0 : kShReads);
     const u32 bit0 = stage_reads(packed, s_w, r0, nr, period);
-    __syncthreads();
     const bool in = threadIdx.x < nr;
-    for_each_suffix_of_read(s_w, bit0 + (in ? 2 * threadIdx.x * period : 0u), period, [&](u32 t, u32 key) {
-        const u32 pre = key >> (32 - kShPrefixBits);
-        const unsigned b = __ballot_sync(0xffffffffu, in && pre >= plo && pre < phi);
-        if (b && lane_id() == 0) atomicAdd(&s_cnt[t], __popc(b));
-    });
+    const int warp = threadIdx.x >> 5;
+    const u32 my_bit0 = bit0 + (in ? 2 * threadIdx.x * period : 0u);
+    // window = the next 32+ bases from offset o on, refilled every 16 offsets
+    u32 wi = my_bit0 >> 6, sh = my_bit0 & 63u;
+    u64 hi = s_w[wi], lo = s_w[wi + 1];
+    u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+    for (u32 o = 0; o < period; ++o) {
+        if ((o & 15u) == 0 && o) {
+            const u32 bit = my_bit0 + 2 * o;
+            wi = bit >> 6;
+            sh = bit & 63u;
+            hi = s_w[wi];
+            lo = s_w[wi + 1];
+            win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+        }
+        const u32 t = period - 1 - o;
+        u32 pre = static_cast<u32>(win >> (64 - kShPrefixBits));
+        if (t < 6u) pre = t ? pre & ~((1u << (2 * (6 - t))) - 1u) : 0u;    // zero padded from the sentinel on
+        win <<= 2;
+        const unsigned bm = __ballot_sync(0xffffffffu, in && pre >= plo && pre < phi);
+        if (lane_id() == 0) {
+            s_wcnt[warp][t] = static_cast<unsigned short>(__popc(bm));
+            keep[(static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period + t] = bm;
+        }
+    }
     __syncthreads();
-    for (u32 t = threadIdx.x; t < period; t += blockDim.x) counts[static_cast<u64>(t) * tiles + blockIdx.x] = s_cnt[t];
+    for (u32 t = threadIdx.x; t < period; t += blockDim.x) {
+        u32 run = 0;
+        for (int w = 0; w < kShReads / 32; ++w) {
+            wbase[(static_cast<u64>(blockIdx.x) * (kShReads / 32) + w) * period + t] = static_cast<unsigned short>(run);
+            run += s_wcnt[w][t];
+        }
+        counts[static_cast<u64>(t) * tiles + blockIdx.x] = run;
+    }
 }
 
 // Writes the kept records key32 << 32 | position at offsets[t * tiles + tile] + (rank of the read
 // among the tile's kept reads at this t): the bucket comes out in (t, position) order.
 __global__ void __launch_bounds__(kShReads)
-shard_write_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 plo, u32 phi, u32 tiles,
-                           const u32* __restrict__ offsets, u64* __restrict__ out, u32* __restrict__ g_hist) {
+shard_write_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 tiles, const u32* __restrict__ offsets,
+                           const u32* __restrict__ keep, const unsigned short* __restrict__ wbase,
+                           u64* __restrict__ out, u32* __restrict__ g_hist) {
     __shared__ __align__(16) u64 s_w[kShReads * kUniMaxPeriod / 32 + 8];
-    __shared__ unsigned short s_wcnt[kShReads / 32][kUniMaxPeriod + 1];   // kept per (warp, t), then exclusive over warps
     __shared__ u32 s_hist[4 * kRadix];                                    // digit histograms of the bucket's four sort passes
     for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
     const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
     const u32 nr = static_cast<u32>(k - r0 < kShReads ? k - r0 : kShReads);
     const u32 bit0 = stage_reads(packed, s_w, r0, nr, period);
-    __syncthreads();
-    const bool in = threadIdx.x < nr;
     const int warp = threadIdx.x >> 5;
-    const u32 my_bit0 = bit0 + (in ? 2 * threadIdx.x * period : 0u);   // (idle threads walk read 0: staged words only)
-    for_each_suffix_of_read(s_w, my_bit0, period, [&](u32 t, u32 key) {
-        const u32 pre = key >> (32 - kShPrefixBits);
-        const unsigned b = __ballot_sync(0xffffffffu, in && pre >= plo && pre < phi);
-        if (lane_id() == 0) s_wcnt[warp][t] = static_cast<unsigned short>(__popc(b));
-    });
-    __syncthreads();
-    for (u32 t = threadIdx.x; t < period; t += blockDim.x) {
-        u32 run = 0;
-        for (int w = 0; w < kShReads / 32; ++w) {
-            const u32 c = s_wcnt[w][t];
-            s_wcnt[w][t] = static_cast<unsigned short>(run);
-            run += c;
-        }
-    }
-    __syncthreads();
+    const unsigned lane = lane_id();
+    const u32 my_bit0 = bit0 + (threadIdx.x < nr ? 2 * threadIdx.x * period : 0u);
     const u64 pos0 = (r0 + threadIdx.x) * period;
-    for_each_suffix_of_read(s_w, my_bit0, period, [&](u32 t, u32 key) {
-        const u32 pre = key >> (32 - kShPrefixBits);
-        const bool keep = in && pre >= plo && pre < phi;
-        const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-            const u64 slot = static_cast<u64>(offsets[static_cast<u64>(t) * tiles + blockIdx.x]) + s_wcnt[warp][t] +
-                             __popc(b & lanemask_lt());
-            out[slot] = (static_cast<u64>(key) << 32) | (pos0 + (period - 1 - t));
+    const u64 wcell = (static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period;   // this warp's masks, t-contiguous
+    for (u32 t0 = 0; t0 < period; t0 += 32) {
+        const u32 tt = t0 + lane;
+        const u32 kw = tt < period ? keep[wcell + tt] : 0u;          // 32 masks per coalesced load, handed round by shuffles
+        const u32 wb = tt < period ? wbase[wcell + tt] : 0u;
+        const u32 jn = period - t0 < 32u ? period - t0 : 32u;
+        for (u32 j = 0; j < jn; ++j) {
+            const unsigned bm = __shfl_sync(0xffffffffu, kw, j);
+            const u32 base_w = __shfl_sync(0xffffffffu, wb, j);
+            if (!((bm >> lane) & 1u)) continue;
+            const u32 t = t0 + j;
+            const u32 o = period - 1 - t;
+            const u32 bit = my_bit0 + 2 * o, wi = bit >> 6, sh = bit & 63u;
+            const u64 hi = s_w[wi], lo = s_w[wi + 1];
+            const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+            u32 key = static_cast<u32>(win >> 32);
+            if (t < static_cast<u32>(kUniK)) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;
+            const u64 slot = static_cast<u64>(offsets[static_cast<u64>(t) * tiles + blockIdx.x]) + base_w + __popc(bm & lanemask_lt());
+            out[slot] = (static_cast<u64>(key) << 32) | (pos0 + o);
             atomicAdd(&s_hist[key & 0xffu], 1u);
             atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
             atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
             atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
         }
-    });
+    }
     __syncthreads();
     hist_flush(s_hist, g_hist, 4);
 }
@@ -2120,7 +2147,7 @@ struct OwnerTable {
     u64 base[17];    // base[g] = floor(n g / G), base[G] = n
     u64 magic;       // floor(2^64 G / n): mulhi(p, magic) is floor(p G / n) or one less
     u32 G;
-    u32 sub_shift;   // (p - base) >> sub_shift < sub for every slice
+    u32 sub_shift;   // (unused by the low-bit rule below; kept for the layout)
     u32 sub;         // sub-bins per owner (a power of two; G * sub <= 1024)
 };
 constexpr int kOwnMaxBins = 1024;
@@ -2129,7 +2156,10 @@ __device__ __forceinline__ u32 owner_bin(const OwnerTable& tb, u64 p, u64* rel) 
     u32 g = static_cast<u32>(__umul64hi(p, tb.magic));          // the owner, or up to two below it
     while (g + 1 < tb.G && tb.base[g + 1] <= p) ++g;
     *rel = p - tb.base[g];
-    return g * tb.sub + static_cast<u32>(*rel >> tb.sub_shift);
+    // the sub-bin only spreads the shared-memory atomics: LOW position bits, so that an owner's group
+    // stays unordered in the high bits the receiver partitions on (top bits made every tile of its first
+    // pass hit one bin: 0.79 ms against 0.52)
+    return g * tb.sub + (static_cast<u32>(*rel >> 2) & (tb.sub - 1u));
 }
 
 __global__ void __launch_bounds__(256)
@@ -2945,6 +2975,8 @@ struct reseq_cuda_sa_shard {
     // bucket between reseq_cuda_sa_shard_bucket_size and _bucket_records (arrays in the context's arena)
     rsq::u32 b_plo = 0, b_phi = 0, b_tiles = 0;
     rsq::u32* b_offsets = nullptr;
+    rsq::u32* b_keep = nullptr;
+    unsigned short* b_wbase = nullptr;
     size_t b_m = 0;
     bool b_ready = false;
     rsq::u32* b_hist = nullptr;     // [4][256] digit histograms of the bucket written last (own allocation)
@@ -3178,17 +3210,22 @@ int reseq_cuda_sa_shard_bucket_size(reseq_cuda_sa_shard* sh, uint32_t prefix_lo,
     const u64 units = sh->period ? sh->reads : sh->n;
     const u32 tiles = static_cast<u32>(sh->period ? (units + kShReads - 1) / kShReads : (units + kShTile - 1) / kShTile);
     const size_t cells = sh->period ? static_cast<size_t>(tiles) * sh->period : tiles;
+    const size_t wcells = sh->period ? cells * (kShReads / 32) : 0;   // per-warp keep masks and bases (uniform read sets)
     auto pad = reseq_cuda_ctx::padded;
-    RSQ_TRY(ctx->reserve(2 * pad(sizeof(u32) * (cells + 1)) + scan_workspace_bytes(cells + 1) + 8192));
+    RSQ_TRY(ctx->reserve(2 * pad(sizeof(u32) * (cells + 1)) + pad(sizeof(u32) * (wcells + 1)) + pad(sizeof(unsigned short) * (wcells + 1)) +
+                         scan_workspace_bytes(cells + 1) + 8192));
     ctx->begin();
     u32* counts = ctx->alloc<u32>(cells + 1);
     u32* offsets = ctx->alloc<u32>(cells + 1);
+    u32* keep = ctx->alloc<u32>(wcells + 1);
+    unsigned short* wbase = ctx->alloc<unsigned short>(wcells + 1);
     u64* d_total = ctx->alloc<u64>(1);
-    if (!counts || !offsets || !d_total) return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
+    if (!counts || !offsets || !keep || !wbase || !d_total) return fail(RESEQ_OUT_OF_MEMORY, "shard workspace");
     RSQ_CUDA(cudaMemsetAsync(counts + cells, 0, sizeof(u32), s));
     if (sh->period) {
         RSQ_LAUNCH_BEGIN(ctx, "shard_count_uniform_kernel");
-        shard_count_uniform_kernel<<<tiles, kShReads, 0, s>>>(sh->packed, sh->period, sh->reads, prefix_lo, prefix_hi, tiles, counts);
+        shard_count_uniform_kernel<<<tiles, kShReads, 0, s>>>(sh->packed, sh->period, sh->reads, prefix_lo, prefix_hi, tiles, counts,
+                                                              keep, wbase);
         RSQ_LAUNCH_END(ctx);
     } else {
         RSQ_LAUNCH_BEGIN(ctx, "shard_count_general_kernel");
@@ -3204,6 +3241,8 @@ int reseq_cuda_sa_shard_bucket_size(reseq_cuda_sa_shard* sh, uint32_t prefix_lo,
     sh->b_phi = prefix_hi;
     sh->b_tiles = tiles;
     sh->b_offsets = offsets;
+    sh->b_keep = keep;
+    sh->b_wbase = wbase;
     sh->b_ready = true;
     *m = sh->b_m;
     return RESEQ_OK;
@@ -3220,8 +3259,8 @@ int reseq_cuda_sa_shard_bucket_records(reseq_cuda_sa_shard* sh, uint64_t* d_reco
     RSQ_CUDA(cudaMemsetAsync(sh->b_hist, 0, sizeof(u32) * 4 * kRadix, ctx->stream));
     if (sh->period) {
         RSQ_LAUNCH_BEGIN(ctx, "shard_write_uniform_kernel");
-        shard_write_uniform_kernel<<<sh->b_tiles, kShReads, 0, ctx->stream>>>(sh->packed, sh->period, sh->reads, sh->b_plo, sh->b_phi,
-                                                                             sh->b_tiles, sh->b_offsets, d_records, sh->b_hist);
+        shard_write_uniform_kernel<<<sh->b_tiles, kShReads, 0, ctx->stream>>>(sh->packed, sh->period, sh->reads, sh->b_tiles,
+                                                                             sh->b_offsets, sh->b_keep, sh->b_wbase, d_records, sh->b_hist);
         RSQ_LAUNCH_END(ctx);
     } else {
         RSQ_LAUNCH_BEGIN(ctx, "shard_write_general_kernel");
