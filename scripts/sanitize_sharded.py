@@ -19,5 +19,5 @@ th = [threading.Thread(target=work, args=(r,)) for r in range(3)]
 [t.start() for t in th]; [t.join() for t in th]
 want = rq.build_parallel(text, ex).sa
 for sa, st in outs:
-    assert st["records"] == "uniform" and np.array_equal(sa, want)
+    assert st["records"] == "uniform" and st["path"] == "sharded" and np.array_equal(sa, want)
 print("sanitize_sharded: parity ok")

@@ -26,11 +26,25 @@ check(np.frombuffer(reads, np.uint8))
 big, _ = rq.synth_read_text(400_000, 100, 42_000)          # n = 4.24 M >= 2^22: partition passes + window scatter
 got = rq.build_parallel(big, ex)
 assert np.array_equal(got.rank[got.sa], np.arange(big.size, dtype=np.uint32)) and ora.verify_sa(big, got.sa) == 0
-# general DNA records, text steps, prefix doubling, generic bytes
+# ragged read sets (mixed read lengths: transposed records with ragged rows, forward / backward links), with repeats
+g40 = rng.choice([65, 67, 71, 84], 40_000).astype(np.uint8)
+def ragged_reads(genome, k, lo, hi):
+    out = []
+    for _ in range(k):
+        ln = int(rng.integers(lo, hi + 1)); st = int(rng.integers(0, len(genome) - ln + 1))
+        out.append(bytes(genome[st:st + ln]) + b"\0")
+    return np.frombuffer(b"".join(out), np.uint8)
+assert check(ragged_reads(g40, 3000, 40, 150)).stats.init_symbols == 15
+assert check(ragged_reads(np.frombuffer(genome, np.uint8), 3000, 16, 254)).stats.init_symbols == 15
+# general DNA records, text steps, prefix doubling (local rounds, global rounds, oversize groups), generic bytes
 ragged = rng.choice([65, 67, 71, 84, 0], 60_000, p=[.24, .24, .24, .24, .04]).astype(np.uint8)
 check(ragged)
 e2 = rq.Executor(0); e2.set_option("sa_text_rounds", 0); check(ragged, e2); check(text, e2)
+check(np.frombuffer((b"ACGTACGTAC" * 12 + b"\0") * 3000, np.uint8), e2)       # groups of 3000 > the local window
+e4 = rq.Executor(0); e4.set_option("sa_text_rounds", 0); e4.set_option("sa_doubling_local", 0); check(text, e4)
 e3 = rq.Executor(0); e3.set_option("sa_uniform", 0); check(text, e3)
+e5 = rq.Executor(0); e5.set_option("sort_tma", 1); check(text, e5)             # TMA tile loads in the sort
+check(text); check(text)                                                       # speculative route (second and third build)
 check(np.frombuffer(b"abthatb\0hatbpaab\0tbabhhatbpaa\0paabtabh\0bhaabtpb\0" * 50, np.uint8))
 check(np.frombuffer(b"A" * 5000, np.uint8))
 # primitives
@@ -54,6 +68,11 @@ sup, order = rq.greedy_superstring_from_overlaps(fs, ov)
 assert len(sup) > 0
 ov2 = ix.overlaps(20, reuse_buffers=True)
 assert np.array_equal(ov2.i, wi) and np.array_equal(ov2.w, ww)
+e6 = rq.Executor(0); e6.set_option("overlap_stage", 1)                         # TMA-staged rank blocks in the overlap search
+ix6 = rq.FragmentIndex(fs, e6); ov6 = ix6.overlaps(20)
+assert np.array_equal(ov6.i, wi) and np.array_equal(ov6.w, ww)
+pr = ix.prefix_related_batch([0, 1, 2], [0, 5, 10])
+assert len(pr) == 3
 dup = rq.make_fragment_set([b"ACGT" * 10] * 120 + [b"CGTA" * 10] * 40, "dna")     # overflow route of the overlap fill
 ixd = rq.FragmentIndex(dup, ex)
 ovd = ixd.overlaps(4)
@@ -68,18 +87,22 @@ if os.environ.get("SANITIZE_NO_SHARDED"):
 # the sharded build of a uniform read set as three virtual ranks
 import threading, torch
 from paper_1404_3456_b200.sharded import GpuBackend, LocalComm, build_sa_sharded
-d_text = torch.from_numpy(np.array(text, copy=True)).cuda()
-comms, outs = LocalComm.make(3), [None] * 3
-def work(r):
-    e = rq.Executor(0)
-    st = {}
-    sa, rk = build_sa_sharded(d_text, comms[r], GpuBackend(e), st)
-    torch.cuda.synchronize()
-    outs[r] = (sa.cpu().numpy().view(np.uint32), st)
-    e.close()
-th = [threading.Thread(target=work, args=(r,)) for r in range(3)]
-[t.start() for t in th]; [t.join() for t in th]
-want = rq.build_parallel(text, ex).sa
-for sa, st in outs:
-    assert st["records"] == "uniform" and np.array_equal(sa, want)
+want = rq.build_parallel(text, ex)
+for uniform in (True, False):          # bucket generators of both record kinds, rank exchange, slice inverse
+    d_text = torch.from_numpy(np.array(text, copy=True)).cuda()
+    comms, outs = LocalComm.make(3), [None] * 3
+    def work(r):
+        e = rq.Executor(0)
+        if not uniform:
+            e.set_option("sa_uniform", 0)
+        st = {}
+        sa, rk = build_sa_sharded(d_text, comms[r], GpuBackend(e), st)
+        torch.cuda.synchronize()
+        outs[r] = (sa.cpu().numpy().view(np.uint32), rk.cpu().numpy().view(np.uint32), st)
+        e.close()
+    th = [threading.Thread(target=work, args=(r,)) for r in range(3)]
+    [t.start() for t in th]; [t.join() for t in th]
+    for sa, rk, st in outs:
+        assert st["path"] == "sharded" and st["records"] == ("uniform" if uniform else "general")
+        assert np.array_equal(sa, want.sa) and np.array_equal(rk, want.rank)
 print("sanitize_small: all parity checks passed")
