@@ -574,6 +574,13 @@ def main():
         ix = rq.FragmentIndex(fset, ex)
         torch.cuda.synchronize()
         t_index = time.perf_counter() - t0
+        # per-kernel table of one more index build (CUDA events around every launch add their own cost:
+        # this build is not the one timed above)
+        ex.profile(True)
+        rq.FragmentIndex(fset, ex).close()
+        ix_prof = ex.profile_read()
+        ex.profile(False)
+        index_kernels = {kname: {"ms": ms, "launches": cnt} for kname, (cnt, ms) in sorted(ix_prof.items(), key=lambda kv: -kv[1][1])}
         ix.overlaps(20, reuse_buffers=True)  # warm-up (arena growth, page-locked result arrays)
         ex.profile(True)
         t0 = time.perf_counter()
@@ -599,6 +606,7 @@ def main():
                            "note": "index resident; query offsets in, (i, j, w) triples + containment flags out to page-locked host arrays"},
                    "overlaps_found": int(ov.i.size),
                    "contained_reads": int(ov.contained.sum()), "index_build_ms": t_index * 1e3,
+                   "index_build_kernels": index_kernels, "index_build_kernel_ms": sum(v["ms"] for v in index_kernels.values()),
                    "roofline": {"bound": "hbm", "kernel": dom_ov, "peak": peak, "unit": "GB/s",
                                 "traffic": dom_rec.get("dram_bytes_ncu"), "achieved": dom_rec.get("dram_gbs"),
                                 "frac": dom_rec.get("dram_frac_of_peak"),

@@ -58,7 +58,7 @@ static const char* pass_name() {
                              : (HAS_VAL ? "onesweep_u32_pairs" : "onesweep_u32_keys");
 }
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT, bool HI, int DPW>
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT, int HI, int DPW>
 static int launch_pass_dpw(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
                            size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket,
                            const EMIT& emit) {
@@ -74,13 +74,14 @@ static int launch_pass_dpw(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, con
     const int use_tma = ctx->opt_sort_tma != 0 && (reinterpret_cast<uintptr_t>(kin) & 15) == 0 &&
                         (!HAS_VAL || (reinterpret_cast<uintptr_t>(vin) & 15) == 0);
     kern<<<static_cast<unsigned>(tiles), BLOCK, smem, ctx->stream>>>(
-        kin, kout, vin, vout, n, HI ? shift - 32 : shift, mask, base, lookback, ticket, emit, use_tma);
+        kin, kout, vin, vout, n, HI == 2 ? (0x4440 | ((shift - 32) >> 3)) : (HI == 1 ? shift - 32 : shift), mask, base, lookback, ticket,
+        emit, use_tma);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     return RESEQ_OK;
 }
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT, bool HI>
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT, int HI>
 static int launch_pass_kernel(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, const u32* vin, u32* vout,
                               size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket,
                               const EMIT& emit) {
@@ -97,11 +98,14 @@ static int launch_pass_cfg(reseq_cuda_ctx* ctx, const void* kin, KeyT* kout, con
                            size_t n, int shift, u32 mask, const u32* base, u64* lookback, u32* ticket,
                            const EMIT& emit) {
     if constexpr (sizeof(KeyT) == 8) {
+        if (shift >= 32 && (shift & 7) == 0 && mask == 0xffu && ctx->opt_sort_prmt != 0)   // a whole byte of the upper word
+            return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, 2>(ctx, kin, kout, vin, vout, n, shift, mask,
+                                                                            base, lookback, ticket, emit);
         if (shift >= 32)
-            return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, true>(ctx, kin, kout, vin, vout, n, shift, mask,
-                                                                               base, lookback, ticket, emit);
+            return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, 1>(ctx, kin, kout, vin, vout, n, shift, mask,
+                                                                            base, lookback, ticket, emit);
     }
-    return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, false>(ctx, kin, kout, vin, vout, n, shift, mask, base,
+    return launch_pass_kernel<KeyT, HAS_VAL, BLOCK, ITEMS, EMIT, 0>(ctx, kin, kout, vin, vout, n, shift, mask, base,
                                                                         lookback, ticket, emit);
 }
 

@@ -119,11 +119,15 @@ hist_kernel(const KeyT* __restrict__ keys, u64 n, PassTable pt, u32* __restrict_
 // instead of the 7.6 per bit the C++ form compiled to; MATCH.ANY is slower still (its issue rate
 // capped the ranking loop at 1.5 TB/s of key traffic).  Digit bits above a narrow pass's width
 // are zero in every lane, so their ballots leave `peers` unchanged: all passes run 8 ballots.
+__device__ __forceinline__ unsigned and3(unsigned a, unsigned b, unsigned c) {
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
 __device__ __forceinline__ unsigned warp_match_digit(u32 d) {
-    unsigned peers = 0xffffffffu;
+    unsigned m[kRadixBits];
 #pragma unroll
     for (int b = 0; b < kRadixBits; ++b) {
-        unsigned m;
         asm volatile(
             "{\n\t"
             ".reg .pred p;\n\t"
@@ -133,11 +137,12 @@ __device__ __forceinline__ unsigned warp_match_digit(u32 d) {
             "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
             "@!p not.b32 %0, %0;\n\t"
             "}"
-            : "=r"(m)
+            : "=r"(m[b])
             : "r"(d), "r"(1u << b));
-        peers &= m;
     }
-    return peers;
+    // the eight masks meet in four three-input LOP3s instead of a chain of seven ANDs
+    static_assert(kRadixBits == 8, "the AND tree is written for eight ballots");
+    return and3(m[3], m[4], m[5]) & and3(m[6], m[7], and3(m[0], m[1], m[2]));
 }
 
 // What a pass reports besides sorting.  EmitMultiples: the OUTPUT index of every record whose low
@@ -174,11 +179,15 @@ struct EmitStarts {
 };
 constexpr int kEmitCap = 510;   // hits staged per tile; the overflow goes out one atomic each
 
-// Digit of a key.  HI (u64 keys, shift >= 32): the digit lies in the upper word, one 32-bit
+// Digit of a key.  HI 1 (u64 keys, shift >= 32): the digit lies in the upper word, one 32-bit
 // shift instead of a 64-bit funnel sequence -- the digit is extracted four times per item.
-template <bool HI, typename KeyT>
+// HI 2: the digit is a whole BYTE of the upper word (8-bit digit at a byte boundary: every pass of the
+// suffix-array builder's 32-bit keys); `shift` then holds the PRMT selector 0x4440 | byte and the digit
+// costs one instruction, no mask.
+template <int HI, typename KeyT>
 __device__ __forceinline__ u32 pass_digit(KeyT k, int shift, u32 mask) {
-    if constexpr (HI) return (static_cast<u32>(static_cast<u64>(k) >> 32) >> shift) & mask;  // shift is already -32
+    if constexpr (HI == 2) return __byte_perm(static_cast<u32>(static_cast<u64>(k) >> 32), 0u, static_cast<u32>(shift));
+    else if constexpr (HI == 1) return (static_cast<u32>(static_cast<u64>(k) >> 32) >> shift) & mask;  // shift is already -32
     else return static_cast<u32>(k >> shift) & mask;
 }
 
@@ -190,7 +199,7 @@ struct OnesweepCfg {
                                     sizeof(u32) * (kWarps * kRadix + 3 * kRadix + 32 + 4);   // + s_gofs, s_total, s_bin
 };
 
-template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT = EmitNone, bool HI = false, int DPW = 1>
+template <typename KeyT, bool HAS_VAL, int BLOCK, int ITEMS, class EMIT = EmitNone, int HI = 0, int DPW = 1>
 __global__ void __launch_bounds__(BLOCK, (BLOCK <= 256 ? (ITEMS <= 8 ? 6 : 4) : (BLOCK <= 384 ? (ITEMS <= 8 ? 4 : 3) : (BLOCK <= 512 ? (ITEMS <= 8 ? 3 : 2) : 1))))
 onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_out,
                 const u32* __restrict__ vals_in, u32* __restrict__ vals_out, u64 n, int shift,

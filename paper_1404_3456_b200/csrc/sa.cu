@@ -1117,12 +1117,63 @@ link_reads_kernel(const u64* __restrict__ elems, const u32* __restrict__ list, c
 // issue slots at 0.41 of the HBM peak).  Bitmaps leave as bytes: four lanes hold eight records.
 constexpr int kAccRows = 4;                       // pairs per thread in flight
 constexpr int kAccSpan = 64 * kAccRows;           // records per warp iteration
-__global__ void __launch_bounds__(256)
+//
+// LOWBITS: the gather of one proof byte per suffix (a 32-sector request per warp: the pass ran at 0.40 of the HBM
+// peak on L1 wavefronts and L2 sectors) is replaced, for most suffixes, by one bit from SHARED memory: every CTA
+// first condenses the table into "cov[read] < thr" (thr = L - 24: a read whose successor starts more than 24
+// bases on is rare), one bit per read (115 KB for the 920 000 reads of config 2).  A suffix with t <= thr of a
+// read whose bit is clear is proven (t <= thr <= cov[read]) without looking the byte up; only the suffixes with
+// t > thr (24 in L) and those of the rare reads still gather.  Bit layout: four words per 128 reads, word c of a
+// block holds reads 4 * lane + c (what one ballot per byte of a 32-bit load per lane produces).
+constexpr u32 kCovLowMargin = 24;
+template <bool LOWBITS>
+__global__ void __launch_bounds__(LOWBITS ? 1024 : 256)
 accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict__ cov, u32 period,
                       u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
-                      u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
+                      u32* __restrict__ uncbits, u8* __restrict__ tileflags, u32 reads, u32 thr) {
     constexpr u32 K = kUniK;
     const unsigned lane = lane_id();
+    extern __shared__ u32 s_low[];
+    if constexpr (LOWBITS) {
+        const u32 blocks = (reads + 127u) >> 7;
+        const u32 wstep = blockDim.x >> 5;
+        constexpr int kInFlight = 8;                       // loads in flight per warp: the table is read at L2 speed, not latency
+        for (u32 b0 = threadIdx.x >> 5; b0 < blocks; b0 += wstep * kInFlight) {
+            u32 v[kInFlight];
+#pragma unroll
+            for (int u = 0; u < kInFlight; ++u) {
+                const u32 b = b0 + u * wstep;
+                const u32 r = (b << 7) + 4u * lane;
+                v[u] = 0xffffffffu;                        // pads: "not low"
+                if (b < blocks) {
+                    if (r + 3u < reads) v[u] = *reinterpret_cast<const u32*>(cov + r);
+                    else if (r < reads) {
+                        v[u] = 0;
+                        for (u32 c = 0; c < 4; ++c) v[u] |= static_cast<u32>(r + c < reads ? cov[r + c] : 0xffu) << (8 * c);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kInFlight; ++u) {
+                const u32 b = b0 + u * wstep;
+                if (b >= blocks) break;
+#pragma unroll
+                for (u32 c = 0; c < 4; ++c) {
+                    const unsigned w = __ballot_sync(0xffffffffu, ((v[u] >> (8 * c)) & 0xffu) < thr);
+                    if (lane == c) s_low[4 * b + c] = w;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    auto proof = [&](u32 q, u32 t, bool in) -> u8 {
+        if constexpr (LOWBITS) {
+            const bool low = (s_low[((q >> 5) & ~3u) | (q & 3u)] >> ((q >> 2) & 31u)) & 1u;
+            return in && (t > thr || low) ? __ldg(cov + q) : static_cast<u8>(in ? 255 : 0);
+        } else {
+            return in ? __ldg(cov + q) : 0;
+        }
+    };
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     u8* hbytes = reinterpret_cast<u8*>(headbits);
     u8* ubytes = reinterpret_cast<u8*>(uncbits);
@@ -1163,8 +1214,8 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict
 #pragma unroll
         for (int c = 0; c < kAccRows; ++c) {
             const u64 i = i0 + c * 64 + 2 * lane;
-            cva[c] = i < m ? __ldg(cov + qa[c]) : 0;
-            cvb[c] = i + 1 < m ? __ldg(cov + qb[c]) : 0;
+            cva[c] = proof(qa[c], ta[c], i < m);
+            cvb[c] = proof(qb[c], tb[c], i + 1 < m);
         }
 #pragma unroll
         for (int c = 0; c < kAccRows; ++c) {
@@ -1979,27 +2030,31 @@ shard_count_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u3
     const bool in = threadIdx.x < nr;
     const int warp = threadIdx.x >> 5;
     const u32 my_bit0 = bit0 + (in ? 2 * threadIdx.x * period : 0u);
-    // window = the next 32+ bases from offset o on, refilled every 16 offsets
-    u32 wi = my_bit0 >> 6, sh = my_bit0 & 63u;
-    u64 hi = s_w[wi], lo = s_w[wi + 1];
-    u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+    // window = the next 32+ bases from offset o on, refilled every 16 offsets.  The ballots of 32 values of t
+    // are collected in registers (lane j keeps the mask of t = 32 c + j) and leave as one coalesced store.
+    const u32 span = phi - plo;
+    const unsigned lane = lane_id();
+    u32 mine = 0;
+    u64 win = 0;
     for (u32 o = 0; o < period; ++o) {
-        if ((o & 15u) == 0 && o) {
+        if ((o & 15u) == 0) {
             const u32 bit = my_bit0 + 2 * o;
-            wi = bit >> 6;
-            sh = bit & 63u;
-            hi = s_w[wi];
-            lo = s_w[wi + 1];
+            const u32 wi = bit >> 6, sh = bit & 63u;
+            const u64 hi = s_w[wi], lo = s_w[wi + 1];
             win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
         }
         const u32 t = period - 1 - o;
         u32 pre = static_cast<u32>(win >> (64 - kShPrefixBits));
         if (t < 6u) pre = t ? pre & ~((1u << (2 * (6 - t))) - 1u) : 0u;    // zero padded from the sentinel on
         win <<= 2;
-        const unsigned bm = __ballot_sync(0xffffffffu, in && pre >= plo && pre < phi);
-        if (lane_id() == 0) {
-            s_wcnt[warp][t] = static_cast<unsigned short>(__popc(bm));
-            keep[(static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period + t] = bm;
+        const unsigned bm = __ballot_sync(0xffffffffu, in && pre - plo < span);
+        if (lane == (t & 31u)) mine = bm;
+        if ((t & 31u) == 0) {                                             // t .. t + 31 are complete (t = 0 ends the read)
+            if (t + lane < period) {
+                keep[(static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period + t + lane] = mine;
+                s_wcnt[warp][t + lane] = static_cast<unsigned short>(__popc(mine));
+            }
+            mine = 0;
         }
     }
     __syncthreads();
@@ -2015,44 +2070,70 @@ shard_count_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u3
 
 // Writes the kept records key32 << 32 | position at offsets[t * tiles + tile] + (rank of the read
 // among the tile's kept reads at this t): the bucket comes out in (t, position) order.
+// A rank keeps 1/G of the suffixes, so with lanes = reads only ~32/G lanes of a warp had work at any t and
+// the record body ran for nearly every t all the same (5.8 ms at 3 G suffixes, G = 8: the largest phase that
+// does not shrink with G).  Instead each warp turns the keep masks of 32 values of t into a compact work
+// list in shared memory ((t - t0) << 5 | read, in (t, read) order: entries of one t are neighbours, so are
+// their output slots) and all 32 lanes take entries from it.
 __global__ void __launch_bounds__(kShReads)
 shard_write_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 tiles, const u32* __restrict__ offsets,
                            const u32* __restrict__ keep, const unsigned short* __restrict__ wbase,
                            u64* __restrict__ out, u32* __restrict__ g_hist) {
     __shared__ __align__(16) u64 s_w[kShReads * kUniMaxPeriod / 32 + 8];
     __shared__ u32 s_hist[4 * kRadix];                                    // digit histograms of the bucket's four sort passes
+    __shared__ unsigned short s_list[kShReads / 32][1024];                // per warp: the kept (t, read) pairs of 32 values of t
     for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
     const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
     const u32 nr = static_cast<u32>(k - r0 < kShReads ? k - r0 : kShReads);
     const u32 bit0 = stage_reads(packed, s_w, r0, nr, period);
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
-    const u32 my_bit0 = bit0 + (threadIdx.x < nr ? 2 * threadIdx.x * period : 0u);
-    const u64 pos0 = (r0 + threadIdx.x) * period;
+    const u32 warp_read0 = static_cast<u32>(warp) * 32u;
     const u64 wcell = (static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period;   // this warp's masks, t-contiguous
+    unsigned short* list = s_list[warp];
     for (u32 t0 = 0; t0 < period; t0 += 32) {
         const u32 tt = t0 + lane;
-        const u32 kw = tt < period ? keep[wcell + tt] : 0u;          // 32 masks per coalesced load, handed round by shuffles
-        const u32 wb = tt < period ? wbase[wcell + tt] : 0u;
-        const u32 jn = period - t0 < 32u ? period - t0 : 32u;
-        for (u32 j = 0; j < jn; ++j) {
-            const unsigned bm = __shfl_sync(0xffffffffu, kw, j);
-            const u32 base_w = __shfl_sync(0xffffffffu, wb, j);
-            if (!((bm >> lane) & 1u)) continue;
+        const u32 kw = tt < period ? keep[wcell + tt] : 0u;          // lane j: the mask of t0 + j
+        const u32 base = tt < period ? offsets[static_cast<u64>(tt) * tiles + blockIdx.x] + wbase[wcell + tt] : 0u;
+        const u32 c = __popc(kw);
+        u32 inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (static_cast<int>(lane) >= o) inc += v;
+        }
+        const u32 first = inc - c;                                    // index of this t's first entry in the list
+        const u32 total = __shfl_sync(0xffffffffu, inc, 31);
+        {
+            u32 m = kw, q = first;
+            while (m) {
+                const u32 b = __ffs(m) - 1u;
+                m &= m - 1u;
+                list[q++] = static_cast<unsigned short>((lane << 5) | b);
+            }
+        }
+        __syncwarp();
+        for (u32 i0 = 0; i0 < total; i0 += 32) {
+            const u32 i = i0 + lane;
+            const bool on = i < total;
+            const u32 ent = on ? list[i] : 0u;
+            const u32 j = ent >> 5, rd = warp_read0 + (ent & 31u);
+            const u32 slot = __shfl_sync(0xffffffffu, base, j) + (i - __shfl_sync(0xffffffffu, first, j));
+            if (!on) continue;
             const u32 t = t0 + j;
             const u32 o = period - 1 - t;
-            const u32 bit = my_bit0 + 2 * o, wi = bit >> 6, sh = bit & 63u;
+            const u32 bit = bit0 + 2 * (rd * period + o), wi = bit >> 6, sh = bit & 63u;
             const u64 hi = s_w[wi], lo = s_w[wi + 1];
             const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
             u32 key = static_cast<u32>(win >> 32);
             if (t < static_cast<u32>(kUniK)) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;
-            const u64 slot = static_cast<u64>(offsets[static_cast<u64>(t) * tiles + blockIdx.x]) + base_w + __popc(bm & lanemask_lt());
-            out[slot] = (static_cast<u64>(key) << 32) | (pos0 + o);
+            out[slot] = (static_cast<u64>(key) << 32) | ((r0 + rd) * period + o);
             atomicAdd(&s_hist[key & 0xffu], 1u);
             atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
             atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
             atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
         }
+        __syncwarp();
     }
     __syncthreads();
     hist_flush(s_hist, g_hist, 4);
@@ -2169,10 +2250,32 @@ owner_count_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u32* __rest
     for (u32 b = threadIdx.x; b < bins; b += blockDim.x) s_cnt[b] = 0;
     __syncthreads();
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
-        u64 rel;
-        atomicAdd(&s_cnt[owner_bin(tb, sa[i], &rel)], 1u);
+    const u64 tid0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    u64 rel;
+    // four positions per 16-byte load, two loads in flight (one 4-byte load per trip left the sweep waiting on
+    // DRAM latency: 1.75 ms for 378 M positions, 0.9 TB/s)
+    const u64 quads = (reinterpret_cast<uintptr_t>(sa) & 15) == 0 ? m / 4 : 0;
+    const uint4* sa4 = reinterpret_cast<const uint4*>(sa);
+    u64 i = tid0;
+    for (; i + stride < quads; i += 2 * stride) {
+        const uint4 a = sa4[i], b = sa4[i + stride];
+        atomicAdd(&s_cnt[owner_bin(tb, a.x, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, a.y, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, a.z, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, a.w, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, b.x, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, b.y, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, b.z, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, b.w, &rel)], 1u);
     }
+    if (i < quads) {
+        const uint4 a = sa4[i];
+        atomicAdd(&s_cnt[owner_bin(tb, a.x, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, a.y, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, a.z, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, a.w, &rel)], 1u);
+    }
+    for (u64 x = 4 * quads + tid0; x < m; x += stride) atomicAdd(&s_cnt[owner_bin(tb, sa[x], &rel)], 1u);
     __syncthreads();
     for (u32 b = threadIdx.x; b < bins; b += blockDim.x)
         if (s_cnt[b]) atomicAdd(counts + b, s_cnt[b]);
@@ -2548,8 +2651,24 @@ int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sen
     RSQ_CUDA(cudaMemsetAsync(tileflags, 0, m / kRefTile + 2, s));
     if ((reinterpret_cast<uintptr_t>(sorted) & 15) || (reinterpret_cast<uintptr_t>(sa_out) & 7))
         return fail(RESEQ_INVALID_ARGUMENT, "record and suffix-array buffers must be 16- / 8-byte aligned");
-    accept_uniform_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
-                                                                       uncbits, tileflags);
+    {
+        // the per-read "proof is short" bitmap in shared memory when it fits one SM (see the kernel)
+        const u64 reads = n_text / period;
+        const size_t low_bytes = ((reads + 127) / 128) * 16;
+        const bool lowbits = ctx->opt_accept_lowbits != 0 && period > 2 * kCovLowMargin && low_bytes <= 200 * 1024 &&
+                             m >= (1u << 22) && (reinterpret_cast<uintptr_t>(cov) & 3) == 0;
+        if (lowbits) {
+            RSQ_OPT_IN_SMEM(ctx, accept_uniform_kernel<true>, 200 * 1024);   // the largest bitmap taken
+            const int threads = 2 * (low_bytes + 1024) <= 228 * 1024 ? 512 : 1024;   // two CTAs per SM while two bitmaps fit
+            const unsigned grid = static_cast<unsigned>(ctx->sm_count) * (threads == 512 ? 2u : 1u);
+            accept_uniform_kernel<true><<<grid, threads, low_bytes, s>>>(sorted, m, cov, period, magic, sa_out, headbits, uncbits,
+                                                                         tileflags, static_cast<u32>(reads),
+                                                                         period - 1u - kCovLowMargin);
+        } else {
+            accept_uniform_kernel<false><<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
+                                                                                  uncbits, tileflags, 0u, 0u);
+        }
+    }
     RSQ_LAUNCH_END(ctx);
     RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<kRefUniform>, kRefSmem);
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
@@ -3286,7 +3405,8 @@ int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bu
     RSQ_TRY(ctx->reserve(16384));
     ctx->begin();
     int sub_bits = 10;
-    while ((world << sub_bits) > kOwnMaxBins) --sub_bits;   // owner x sub-range bins, at most 1024: the sub-bins spread the
+    const int max_bins = ctx->opt_owner_bins >= world && ctx->opt_owner_bins <= kOwnMaxBins ? ctx->opt_owner_bins : kOwnMaxBins;
+    while ((world << sub_bits) > max_bins) --sub_bits;   // owner x sub-range bins, at most 1024: the sub-bins spread the
     const int bins = world << sub_bits;                     // shared-memory atomics; the exchange sends whole owners
     u32* counts = ctx->alloc<u32>(2 * kOwnMaxBins);
     if (!counts) return fail(RESEQ_OUT_OF_MEMORY, "rank shard workspace");

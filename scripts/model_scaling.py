@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c4")
 ap.add_argument("--gpus", default="1,2,4,8")
 ap.add_argument("--out", default=None)
+ap.add_argument("--profile", action="store_true", help="per-kernel table of rank 0's phases (CUDA events around every launch)")
 args = ap.parse_args()
 PEER_GBS, ALLREDUCE_BUS_GBS = 770.0, 725.0
 
@@ -28,9 +29,14 @@ n = int(text.size)
 d_text = torch.from_numpy(text).cuda()
 torch.cuda.synchronize()
 
-def timed(fn):
+def timed(fn, prof=None):
+    """prof = (executor, phase name): also print the per-kernel table of this call."""
+    if prof: prof[0].profile(True)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(); out = fn(); b.record(); torch.cuda.synchronize()
+    if prof:
+        tab = prof[0].profile_read(); prof[0].profile(False)
+        print(f"   [{prof[1]}] {a.elapsed_time(b):.2f} ms: " + ", ".join(f"{k} x{c} {ms:.3f}" for k, (c, ms) in sorted(tab.items(), key=lambda kv: -kv[1][1])), flush=True)
     return out, a.elapsed_time(b)
 
 # single-GPU reference time
@@ -44,8 +50,11 @@ rows = []
 for G in [int(x) for x in args.gpus.split(",")]:
     exs = [rq.Executor(0) for _ in range(G)]
     bes = [GpuBackend(e) for e in exs]
-    ph = {p: [0.0] * G for p in ("pack", "hist", "bucket", "sort_link", "finish", "rank_partition", "rank_finish")}
-    for rep in range(2):   # the first repetition warms the arenas; the second is kept
+    phases = ("pack", "hist", "bucket", "sort_link", "finish", "rank_partition", "rank_finish")
+    best = {p: [float("inf")] * G for p in phases}
+    for rep in range(3):   # the first repetition warms the arenas; of the other two the faster time of each (phase, rank) is kept
+        ph = {p: [0.0] * G for p in phases}   # (a phase's events also span the host's allocations: one slow cudaMalloc is not kernel time)
+        P = (lambda r, name: (exs[r], f"G={G} rank {r} {name}") if args.profile and rep == 2 and r == G - 1 else None)
         for r, be in enumerate(bes):
             _, ph["pack"][r] = timed(lambda: be.open(d_text))
         period, reads = bes[0].uniform_info()
@@ -57,16 +66,16 @@ for G in [int(x) for x in args.gpus.split(",")]:
         bounds = [0] + choose_bounds(hist, G) + [1 << PREFIX_BITS]
         recs, covs, buckets = [], None, []
         for r, be in enumerate(bes):
-            rec, ph["bucket"][r] = timed(lambda: be.bucket(bounds[r], bounds[r + 1]))
-            c, ph["sort_link"][r] = timed(lambda: be.uniform_sort_link(rec, reads))
+            rec, ph["bucket"][r] = timed(lambda: be.bucket(bounds[r], bounds[r + 1]), P(r, "bucket"))
+            c, ph["sort_link"][r] = timed(lambda: be.uniform_sort_link(rec, reads), P(r, "sort_link"))
             covs = c if covs is None else torch.maximum(covs, c)
             recs.append(rec)
         sizes = [int(x.numel()) for x in recs]
         sa_parts, rank_recs = [], []
         for r, be in enumerate(bes):
-            (sa_b, unf), ph["finish"][r] = timed(lambda: be.uniform_finish(covs))
+            (sa_b, unf), ph["finish"][r] = timed(lambda: be.uniform_finish(covs), P(r, "finish"))
             assert unf == 0
-            (rr, counts), ph["rank_partition"][r] = timed(lambda: be.rank_records(sa_b, sum(sizes[:r]), n, G))
+            (rr, counts), ph["rank_partition"][r] = timed(lambda: be.rank_records(sa_b, sum(sizes[:r]), n, G), P(r, "rank_partition"))
             sa_parts.append(sa_b); rank_recs.append((rr, counts))
         recs = None
         # the exchange, done by hand: owner g receives every rank's group g
@@ -78,8 +87,8 @@ for G in [int(x) for x in args.gpus.split(",")]:
             mine = torch.cat(parts)
             slice_len = (n * (g + 1)) // G - (n * g) // G
             assert mine.numel() == slice_len
-            rk, ph["rank_finish"][g] = timed(lambda: be.rank_finish(mine, slice_len))
-            if rep == 1 and g == 0:   # spot check: rank[sa[i]] == i for entries of every bucket that fall in the first slice
+            rk, ph["rank_finish"][g] = timed(lambda: be.rank_finish(mine, slice_len), P(g, "rank_finish"))
+            if rep == 2 and g == 0:   # spot check: rank[sa[i]] == i for entries of every bucket that fall in the first slice
                 off = 0
                 for part in sa_parts:
                     head = part[:400_000].to(torch.int64) & 0xFFFFFFFF
@@ -91,6 +100,9 @@ for G in [int(x) for x in args.gpus.split(",")]:
         rank_recs = None; sa_parts = None
         for be in bes: be.close()
         torch.cuda.synchronize()
+        if rep >= 1:
+            for p in phases: best[p] = [min(a, b) for a, b in zip(best[p], ph[p])]
+    ph = best
     for e in exs: e.close()
     torch.cuda.empty_cache()
     # modelled collectives
