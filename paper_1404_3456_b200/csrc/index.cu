@@ -494,6 +494,7 @@ overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __rest
             const u64* tx = nullptr;
             u32 tx_bit0 = 0;
             if (staged) {
+                __syncwarp();   // lane 0 armed this barrier (an iteration ago, or before the loop): the other lanes only poll it
                 mbar_wait(&s_sbar[wib][buf], uses[buf] & 1u);
                 ++uses[buf];
                 rk = s_rk[wib][buf] + (start & 3ull);

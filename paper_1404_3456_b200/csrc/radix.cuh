@@ -227,10 +227,22 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     const unsigned lane = lane_id();
 
     __shared__ __align__(8) u64 s_bar;   // completion of the tile's bulk load
+    if (use_tma && tid == 0) mbar_init(&s_bar, 1);
+    __syncwarp();   // (racecheck attributes the barrier's initialisation to the warp, not to its lane 0)
     if (tid == 0) {
-        *s_tile = atomicAdd(ticket, 1u);
+        const u32 t = atomicAdd(ticket, 1u);
+        *s_tile = t;
         if (EMIT::kActive) s_emit[0] = 0;
-        if (use_tma) mbar_init(&s_bar, 1);
+        if (use_tma && static_cast<u64>(t) * TILE + TILE <= n) {
+            // The tile is one contiguous stretch of HBM: the thread that drew the ticket has the TMA engine move
+            // it into the exchange buffer (cp.async.bulk, completion counted in bytes on an mbarrier) instead of
+            // ITEMS global loads per thread; the threads then pick their keys up from shared memory.  Barrier
+            // set-up, arming and the copy all precede the block barrier below: the waiters only ever poll it.
+            // (The buffer is rewritten by the exchange only after two more barriers.)
+            mbar_expect_tx(&s_bar, static_cast<u32>(TILE * (sizeof(KeyT) + (HAS_VAL ? sizeof(u32) : 0))));
+            tma_load_1d(s_keys, static_cast<const KeyT*>(keys_in_raw) + static_cast<u64>(t) * TILE, static_cast<u32>(TILE * sizeof(KeyT)), &s_bar);
+            if (HAS_VAL) tma_load_1d(s_vals, vals_in + static_cast<u64>(t) * TILE, static_cast<u32>(TILE * sizeof(u32)), &s_bar);
+        }
     }
     {
         uint4* z = reinterpret_cast<uint4*>(s_whist);
@@ -248,15 +260,6 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     const u32 wbase = warp * (ITEMS * 32) + lane;
     auto load_key = [&](u64 i) -> KeyT { return static_cast<const KeyT*>(keys_in_raw)[i]; };
     if (full && use_tma) {
-        // The tile is one contiguous stretch of HBM: a single elected thread has the TMA engine move it
-        // into the exchange buffer (cp.async.bulk, completion counted in bytes on an mbarrier) instead of
-        // ITEMS global loads per thread; the threads then pick their keys up from shared memory.  (The
-        // buffer is rewritten by the exchange only after the two barriers below.)
-        if (tid == 0) {
-            mbar_expect_tx(&s_bar, static_cast<u32>(TILE * (sizeof(KeyT) + (HAS_VAL ? sizeof(u32) : 0))));
-            tma_load_1d(s_keys, static_cast<const KeyT*>(keys_in_raw) + tile_base, static_cast<u32>(TILE * sizeof(KeyT)), &s_bar);
-            if (HAS_VAL) tma_load_1d(s_vals, vals_in + tile_base, static_cast<u32>(TILE * sizeof(u32)), &s_bar);
-        }
         mbar_wait(&s_bar, 0);
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) key[j] = s_keys[wbase + j * 32];

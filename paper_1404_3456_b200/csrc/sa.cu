@@ -990,8 +990,9 @@ __device__ __forceinline__ u32 stage_reads(const u64* __restrict__ packed, u64* 
     const u64 base0 = r0 * period;
     const u64 w0 = (base0 >> 5) & ~1ull;
     const u32 nw = (static_cast<u32>(((base0 + static_cast<u64>(nr) * period + 31) >> 5) - w0) + 3u) & ~1u;   // the packed array is padded
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    __syncwarp();   // (racecheck attributes the barrier's initialisation to the warp, not to its lane 0)
     if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
         mbar_expect_tx(&s_bar, nw * 8u);
         tma_load_1d(s_w, packed + w0, nw * 8u, &s_bar);
     }
@@ -1336,8 +1337,9 @@ __device__ __forceinline__ void stage_ragged(const u64* __restrict__ packed, con
     const u64 end0 = static_cast<u64>(ends[r0 + nr - 1]) + 1;
     const u64 w0 = (base0 >> 5) & ~1ull;
     const u32 nw = (static_cast<u32>(((end0 + 31) >> 5) - w0) + 3u) & ~1u;
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    __syncwarp();   // (racecheck attributes the barrier's initialisation to the warp, not to its lane 0)
     if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
         mbar_expect_tx(&s_bar, nw * 8u);
         tma_load_1d(s_w, packed + w0, nw * 8u, &s_bar);
     }
@@ -2032,31 +2034,60 @@ shard_count_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u3
     const u32 my_bit0 = bit0 + (in ? 2 * threadIdx.x * period : 0u);
     // window = the next 32+ bases from offset o on, refilled every 16 offsets.  The ballots of 32 values of t
     // are collected in registers (lane j keeps the mask of t = 32 c + j) and leave as one coalesced store.
+    // Offsets are walked in three stretches so that the bulk of them runs as straight-line blocks of 16
+    // (8 instructions per suffix: no bounds, no padding mask, the flush test once per block): a generic
+    // prologue down to t = 15 mod 16, aligned blocks while t > 15, a generic epilogue for t = 15 .. 0 (the
+    // suffixes shorter than the 6-base prefix are there).  (One generic loop: 25 instructions per suffix,
+    // 2.7 ms per sweep over 3 G suffixes -- the phase of the sharded build that does not shrink with G.)
     const u32 span = phi - plo;
     const unsigned lane = lane_id();
+    const u64 kcell = (static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period;
     u32 mine = 0;
     u64 win = 0;
-    for (u32 o = 0; o < period; ++o) {
-        if ((o & 15u) == 0) {
-            const u32 bit = my_bit0 + 2 * o;
-            const u32 wi = bit >> 6, sh = bit & 63u;
-            const u64 hi = s_w[wi], lo = s_w[wi + 1];
-            win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+    auto refill = [&](u32 o) {
+        const u32 bit = my_bit0 + 2 * o;
+        const u32 wi = bit >> 6, sh = bit & 63u;
+        const u64 hi = s_w[wi], lo = s_w[wi + 1];
+        win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+    };
+    auto flush = [&](u32 t) {                                  // t .. t + 31 are complete
+        if (t + lane < period) {
+            keep[kcell + t + lane] = mine;
+            s_wcnt[warp][t + lane] = static_cast<unsigned short>(__popc(mine));
         }
+        mine = 0;
+    };
+    auto generic = [&](u32 o) {
         const u32 t = period - 1 - o;
         u32 pre = static_cast<u32>(win >> (64 - kShPrefixBits));
         if (t < 6u) pre = t ? pre & ~((1u << (2 * (6 - t))) - 1u) : 0u;    // zero padded from the sentinel on
         win <<= 2;
         const unsigned bm = __ballot_sync(0xffffffffu, in && pre - plo < span);
         if (lane == (t & 31u)) mine = bm;
-        if ((t & 31u) == 0) {                                             // t .. t + 31 are complete (t = 0 ends the read)
-            if (t + lane < period) {
-                keep[(static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period + t + lane] = mine;
-                s_wcnt[warp][t + lane] = static_cast<unsigned short>(__popc(mine));
-            }
-            mine = 0;
-        }
+        if ((t & 31u) == 0) flush(t);
+    };
+    u32 o = 0;
+    refill(0);
+    for (u32 c = 0; o < period && ((period - 1 - o) & 15u) != 15u; ++o, ++c) {       // prologue: < 16 offsets
+        if (c == 16) refill(o);
+        generic(o);
     }
+    while (o < period && period - 1 - o > 15u) {                                     // t = T .. T - 15, T = 15 mod 16, T >= 31
+        refill(o);
+        const u32 T = period - 1 - o;
+        const u32 d = (T & 31u) - lane;                                              // lane keeps iteration j = d
+#pragma unroll
+        for (u32 j = 0; j < 16; ++j) {
+            const u32 pre = static_cast<u32>(win >> (64 - kShPrefixBits));
+            win <<= 2;
+            const unsigned bm = __ballot_sync(0xffffffffu, in && pre - plo < span);
+            if (d == j) mine = bm;
+        }
+        o += 16;
+        if (((T - 15u) & 31u) == 0) flush(T - 15u);
+    }
+    if (o < period) refill(o);
+    for (; o < period; ++o) generic(o);                                              // epilogue: t = 15 .. 0
     __syncthreads();
     for (u32 t = threadIdx.x; t < period; t += blockDim.x) {
         u32 run = 0;
@@ -2134,6 +2165,52 @@ shard_write_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 k, u3
             atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
         }
         __syncwarp();
+    }
+    __syncthreads();
+    hist_flush(s_hist, g_hist, 4);
+}
+
+// The same with lanes = reads and no work list: the form for a rank that keeps most suffixes (G <= 2), where
+// nearly every lane has a record to write at every t and the list would only add work (15.9 vs 11.1 ms at 3 G
+// suffixes, G = 1).
+__global__ void __launch_bounds__(kShReads)
+shard_write_uniform_direct_kernel(const u64* __restrict__ packed, u32 period, u64 k, u32 tiles, const u32* __restrict__ offsets,
+                           const u32* __restrict__ keep, const unsigned short* __restrict__ wbase,
+                           u64* __restrict__ out, u32* __restrict__ g_hist) {
+    __shared__ __align__(16) u64 s_w[kShReads * kUniMaxPeriod / 32 + 8];
+    __shared__ u32 s_hist[4 * kRadix];                                    // digit histograms of the bucket's four sort passes
+    for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) s_hist[i] = 0;
+    const u64 r0 = static_cast<u64>(blockIdx.x) * kShReads;
+    const u32 nr = static_cast<u32>(k - r0 < kShReads ? k - r0 : kShReads);
+    const u32 bit0 = stage_reads(packed, s_w, r0, nr, period);
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const u32 my_bit0 = bit0 + (threadIdx.x < nr ? 2 * threadIdx.x * period : 0u);
+    const u64 pos0 = (r0 + threadIdx.x) * period;
+    const u64 wcell = (static_cast<u64>(blockIdx.x) * (kShReads / 32) + warp) * period;   // this warp's masks, t-contiguous
+    for (u32 t0 = 0; t0 < period; t0 += 32) {
+        const u32 tt = t0 + lane;
+        const u32 kw = tt < period ? keep[wcell + tt] : 0u;          // 32 masks per coalesced load, handed round by shuffles
+        const u32 wb = tt < period ? wbase[wcell + tt] : 0u;
+        const u32 jn = period - t0 < 32u ? period - t0 : 32u;
+        for (u32 j = 0; j < jn; ++j) {
+            const unsigned bm = __shfl_sync(0xffffffffu, kw, j);
+            const u32 base_w = __shfl_sync(0xffffffffu, wb, j);
+            if (!((bm >> lane) & 1u)) continue;
+            const u32 t = t0 + j;
+            const u32 o = period - 1 - t;
+            const u32 bit = my_bit0 + 2 * o, wi = bit >> 6, sh = bit & 63u;
+            const u64 hi = s_w[wi], lo = s_w[wi + 1];
+            const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+            u32 key = static_cast<u32>(win >> 32);
+            if (t < static_cast<u32>(kUniK)) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;
+            const u64 slot = static_cast<u64>(offsets[static_cast<u64>(t) * tiles + blockIdx.x]) + base_w + __popc(bm & lanemask_lt());
+            out[slot] = (static_cast<u64>(key) << 32) | (pos0 + o);
+            atomicAdd(&s_hist[key & 0xffu], 1u);
+            atomicAdd(&s_hist[kRadix + ((key >> 8) & 0xffu)], 1u);
+            atomicAdd(&s_hist[2 * kRadix + ((key >> 16) & 0xffu)], 1u);
+            atomicAdd(&s_hist[3 * kRadix + (key >> 24)], 1u);
+        }
     }
     __syncthreads();
     hist_flush(s_hist, g_hist, 4);
@@ -3378,8 +3455,12 @@ int reseq_cuda_sa_shard_bucket_records(reseq_cuda_sa_shard* sh, uint64_t* d_reco
     RSQ_CUDA(cudaMemsetAsync(sh->b_hist, 0, sizeof(u32) * 4 * kRadix, ctx->stream));
     if (sh->period) {
         RSQ_LAUNCH_BEGIN(ctx, "shard_write_uniform_kernel");
-        shard_write_uniform_kernel<<<sh->b_tiles, kShReads, 0, ctx->stream>>>(sh->packed, sh->period, sh->reads, sh->b_tiles,
-                                                                             sh->b_offsets, sh->b_keep, sh->b_wbase, d_records, sh->b_hist);
+        if (sh->b_m * 3 > sh->n)     // most suffixes are kept: lanes = reads
+            shard_write_uniform_direct_kernel<<<sh->b_tiles, kShReads, 0, ctx->stream>>>(sh->packed, sh->period, sh->reads, sh->b_tiles,
+                                                                                        sh->b_offsets, sh->b_keep, sh->b_wbase, d_records, sh->b_hist);
+        else                         // a sparse selection: per-warp work lists
+            shard_write_uniform_kernel<<<sh->b_tiles, kShReads, 0, ctx->stream>>>(sh->packed, sh->period, sh->reads, sh->b_tiles,
+                                                                                 sh->b_offsets, sh->b_keep, sh->b_wbase, d_records, sh->b_hist);
         RSQ_LAUNCH_END(ctx);
     } else {
         RSQ_LAUNCH_BEGIN(ctx, "shard_write_general_kernel");
