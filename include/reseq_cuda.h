@@ -98,6 +98,10 @@ size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
  *                     has just built a uniform read set of n bytes queues the next n-byte build on the
  *                     same route without a host round trip; the route's premises are re-checked on the
  *                     device and a text of another kind is rebuilt the ordinary way)
+ *   "sa_graph"        0: never replay the speculative route as a CUDA graph (default 1: a device-resident
+ *                     build whose text, outputs, workspace, stream and options are those of the previous
+ *                     build is ONE cudaGraphLaunch; needs a stream of the caller's or the context's own --
+ *                     capture is not allowed on the legacy default stream -- and no per-kernel profiling)
  *   "inverse_mode"    how rank = sa^-1 is computed above 2^22 suffixes: 0 two partition passes + a
  *                     shared-memory window scatter, 1 one partition pass + an L2-window scatter */
 int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long value);

@@ -185,6 +185,7 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     if (const char* e = std::getenv("RESEQ_SA_UNIFORM")) ctx->opt_uniform = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_RAGGED")) ctx->opt_ragged = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SPECULATE")) ctx->opt_speculate = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_SA_GRAPH")) ctx->opt_graph = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_DOUBLING_LOCAL")) ctx->opt_doubling_local = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_SHORTCUT")) ctx->opt_shortcut = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SA_TEXT_ROUNDS")) ctx->opt_text_rounds = std::atoi(e);
@@ -196,6 +197,7 @@ void reseq_cuda_ctx_destroy(reseq_cuda_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    ctx->drop_spec_graph();
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto& r : ctx->profile) {
@@ -213,6 +215,7 @@ int reseq_cuda_ctx_set_stream(reseq_cuda_ctx* ctx, void* cuda_stream) {
     RSQ_TRY(check_ctx(ctx));
     RSQ_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    ++ctx->option_epoch;
     return RESEQ_OK;
 }
 
@@ -224,6 +227,11 @@ int reseq_cuda_ctx_synchronize(reseq_cuda_ctx* ctx) {
 
 int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long value) {
     if (!ctx || !name) return fail(RESEQ_INVALID_ARGUMENT, "null argument");
+    ++ctx->option_epoch;   // whatever changes: a captured build graph is rebuilt
+    if (std::strcmp(name, "sa_graph") == 0) {
+        ctx->opt_graph = value != 0;
+        return RESEQ_OK;
+    }
     if (std::strcmp(name, "sa_text_rounds") == 0) {
         if (value < 0 || value > 1024) return fail(RESEQ_INVALID_ARGUMENT, "sa_text_rounds must be in 0..1024");
         ctx->opt_text_rounds = static_cast<int>(value);

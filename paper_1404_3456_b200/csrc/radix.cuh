@@ -154,13 +154,29 @@ struct EmitNone {
 };
 struct EmitMultiples {
     static constexpr bool kActive = true;
-    u32 period;
-    u64 magic;    // ceil(2^64 / period)
+    // p % period == 0  <=>  rotr(p * inv, e) <= limit, with period = odd * 2^e, inv = odd^-1 mod 2^32,
+    // limit = floor((2^32 - 1) / period) (Granlund-Montgomery): three instructions per record instead of the
+    // 64-bit multiply-high of a reciprocal division (7.7 % of the last pass's instructions, ncu source page).
+    u32 inv;
+    u32 e;
+    u32 limit;
     u32* list;
     u32* count;
+    static EmitMultiples make(u32 period, u32* list, u32* count) {
+        EmitMultiples m{};
+        u32 odd = period;
+        while (odd && !(odd & 1u)) { odd >>= 1; ++m.e; }
+        u32 inv = odd;                                   // Newton: correct bits double each step
+        for (int i = 0; i < 5; ++i) inv *= 2u - odd * inv;
+        m.inv = inv;
+        m.limit = 0xffffffffu / period;
+        m.list = list;
+        m.count = count;
+        return m;
+    }
     __device__ __forceinline__ bool hit(u64 k) const {
-        const u32 p = static_cast<u32>(k);
-        return p == static_cast<u32>(__umul64hi(p, magic)) * period;
+        const u32 x = static_cast<u32>(k) * inv;
+        return __funnelshift_r(x, x, e) <= limit;
     }
 };
 // EmitStarts: the same for ragged read sets -- a record is reported when its position starts a read
@@ -368,7 +384,10 @@ onesweep_kernel(const void* __restrict__ keys_in_raw, KeyT* __restrict__ keys_ou
     }
 
     // -- decoupled look-back over earlier tiles, one thread per descriptor word.  It runs after the
-    //    exchange so that the predecessors have had the time of this tile's exchange to publish.  The
+    //    exchange so that the predecessors have had the time of this tile's exchange to publish.
+    //    (Measured and dropped: the 128 threads that own no digit walking WHILE the 256 digit threads scan,
+    //    kept apart by named barriers -- 0.796 against 0.690 ms per pass: walkers that start early only poll
+    //    longer, and their share of the exchange then starts late.  profiles/r2_negative_results.md.)  The
     //    walk meets the front of finished tiles about (L2 latency / tile issue interval) tiles back;
     //    kLookahead descriptors are in flight at once. -------------------------------------------------
     if (tid < WALKERS) {

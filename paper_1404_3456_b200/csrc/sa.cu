@@ -2310,10 +2310,12 @@ struct OwnerTable {
 };
 constexpr int kOwnMaxBins = 1024;
 constexpr int kOwnBlock = 512, kOwnItems = 8, kOwnTile = kOwnBlock * kOwnItems;
-__device__ __forceinline__ u32 owner_bin(const OwnerTable& tb, u64 p, u64* rel) {
+// `base` = the table's bases copied to SHARED memory by the caller: lanes look up different owners, and a
+// kernel parameter indexed per lane is a constant-bank load replayed once per distinct owner in the warp.
+__device__ __forceinline__ u32 owner_bin(const OwnerTable& tb, const u64* __restrict__ base, u64 p, u64* rel) {
     u32 g = static_cast<u32>(__umul64hi(p, tb.magic));          // the owner, or up to two below it
-    while (g + 1 < tb.G && tb.base[g + 1] <= p) ++g;
-    *rel = p - tb.base[g];
+    while (g + 1 < tb.G && base[g + 1] <= p) ++g;
+    *rel = p - base[g];
     // the sub-bin only spreads the shared-memory atomics: LOW position bits, so that an owner's group
     // stays unordered in the high bits the receiver partitions on (top bits made every tile of its first
     // pass hit one bin: 0.79 ms against 0.52)
@@ -2323,8 +2325,10 @@ __device__ __forceinline__ u32 owner_bin(const OwnerTable& tb, u64 p, u64* rel) 
 __global__ void __launch_bounds__(256)
 owner_count_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u32* __restrict__ counts) {
     __shared__ u32 s_cnt[kOwnMaxBins];
+    __shared__ u64 s_base[17];
     const u32 bins = tb.G * tb.sub;
     for (u32 b = threadIdx.x; b < bins; b += blockDim.x) s_cnt[b] = 0;
+    if (threadIdx.x <= tb.G) s_base[threadIdx.x] = tb.base[threadIdx.x];
     __syncthreads();
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     const u64 tid0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -2336,23 +2340,23 @@ owner_count_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u32* __rest
     u64 i = tid0;
     for (; i + stride < quads; i += 2 * stride) {
         const uint4 a = sa4[i], b = sa4[i + stride];
-        atomicAdd(&s_cnt[owner_bin(tb, a.x, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, a.y, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, a.z, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, a.w, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, b.x, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, b.y, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, b.z, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, b.w, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.x, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.y, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.z, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.w, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, b.x, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, b.y, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, b.z, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, b.w, &rel)], 1u);
     }
     if (i < quads) {
         const uint4 a = sa4[i];
-        atomicAdd(&s_cnt[owner_bin(tb, a.x, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, a.y, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, a.z, &rel)], 1u);
-        atomicAdd(&s_cnt[owner_bin(tb, a.w, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.x, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.y, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.z, &rel)], 1u);
+        atomicAdd(&s_cnt[owner_bin(tb, s_base, a.w, &rel)], 1u);
     }
-    for (u64 x = 4 * quads + tid0; x < m; x += stride) atomicAdd(&s_cnt[owner_bin(tb, sa[x], &rel)], 1u);
+    for (u64 x = 4 * quads + tid0; x < m; x += stride) atomicAdd(&s_cnt[owner_bin(tb, s_base, sa[x], &rel)], 1u);
     __syncthreads();
     for (u32 b = threadIdx.x; b < bins; b += blockDim.x)
         if (s_cnt[b]) atomicAdd(counts + b, s_cnt[b]);
@@ -2374,7 +2378,9 @@ owner_partition_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u64 off
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     const int bins = static_cast<int>(tb.G * tb.sub);
+    __shared__ u64 s_base[17];
     for (int b = tid; b < bins; b += kOwnBlock) s_cnt[b] = 0;
+    if (tid <= static_cast<int>(tb.G)) s_base[tid] = tb.base[tid];
     __syncthreads();
     const u64 tile0 = static_cast<u64>(blockIdx.x) * kOwnTile;
     const u32 valid = static_cast<u32>(m - tile0 < static_cast<u64>(kOwnTile) ? m - tile0 : kOwnTile);
@@ -2388,7 +2394,7 @@ owner_partition_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u64 off
         rec[j] = 0;
         if (li < valid) {
             u64 rel;
-            bin[j] = owner_bin(tb, sa[tile0 + li], &rel);
+            bin[j] = owner_bin(tb, s_base, sa[tile0 + li], &rel);
             rec[j] = (rel << 32) | ((offset + tile0 + li) & 0xffffffffu);
             slot[j] = atomicAdd(&s_cnt[bin[j]], 1u);
         }
@@ -2701,7 +2707,7 @@ int uniform_sort_link(reseq_cuda_ctx* ctx, const u64* packed, u32 period, u64* e
     const u64 magic = ~0ull / period + 1;   // ceil(2^64 / period): floor(pos / period) = mulhi(pos, magic) for pos < 2^32
     const PassTable pt = make_passes(32, 64);
     bool in_b = false;
-    const EmitMultiples emit{period, magic, whole, counters + 4};
+    const EmitMultiples emit = EmitMultiples::make(period, whole, counters + 4);
     RSQ_TRY(onesweep_sort<u64>(ctx, elems_a, elems_b, nullptr, nullptr, m, pt, ws, hist_ready, 0, &in_b, &emit));
     st->sort_passes += pt.count;
     const u64* sorted = in_b ? elems_b : elems_a;
@@ -2955,12 +2961,53 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
     if (ctx->hint_n == n && ctx->hint_period != 0 && ctx->opt_text_rounds > 0 && ctx->opt_uniform != 0 && ctx->opt_speculate != 0) {
         const u32 period = ctx->hint_period;
         const u64 k = n / period;
-        RSQ_TRY(pack_dna_device(ctx, d_text, n, packed, sent, counters + 16, nullptr, nullptr));
         u64 unfinished = 0;
-        RSQ_TRY(uniform_sort_and_refine(ctx, packed, sent, n, period, k, keys_a, keys_b, cov, headbits, uncbits, vals_b, d_sa,
-                                        ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished, true, counters + 16));
-        RSQ_TRY(ctx->sa_ready(d_sa, n));
-        RSQ_TRY(inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, inv_scratch));
+        auto enqueue = [&]() -> int {   // everything up to the verdict: no host round trip, fixed launch shapes
+            RSQ_TRY(pack_dna_device(ctx, d_text, n, packed, sent, counters + 16, nullptr, nullptr));
+            RSQ_TRY(uniform_sort_and_refine(ctx, packed, sent, n, period, k, keys_a, keys_b, cov, headbits, uncbits, vals_b, d_sa,
+                                            ctx->opt_text_rounds, counters + 4, ws, &st, &unfinished, true, counters + 16));
+            RSQ_TRY(ctx->sa_ready(d_sa, n));
+            return inverse_device(ctx, d_sa, n, rank, keys_a, keys_b, inv_scratch);
+        };
+        // One CUDA graph per (text, outputs, arena, stream, options): device-resident builds on a stream of the
+        // caller's (capture is not allowed on the legacy default stream), no profiling events, no copy-out stream.
+        auto& g = ctx->spec_graph;
+        const bool graphable = ctx->opt_graph != 0 && !ctx->profiling && ctx->sa_host_dst == nullptr && packed_out == nullptr &&
+                               sent_out == nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread && s != nullptr;
+        const bool same = g.exec && g.n == n && g.period == period && g.text == d_text && g.sa == d_sa && g.rank == rank &&
+                          g.arena == ctx->arena && g.arena_cap == ctx->arena_cap && g.stream == s && g.epoch == ctx->option_epoch;
+        bool done = false;
+        if (graphable && same) {
+            RSQ_CUDA(cudaGraphLaunch(g.exec, s));
+            st = g.stats;
+            ctx->launches += g.launches;
+            done = true;
+        } else if (graphable) {
+            ctx->drop_spec_graph();
+            const uint64_t l0 = ctx->launches;
+            if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                (void)cudaMemsetAsync(counters, 0, 1024, s);   // the counters' reset belongs to the graph: it is replayed with it
+                const int rc = enqueue();
+                cudaGraph_t graph = nullptr;
+                const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+                if (rc == RESEQ_OK && ce == cudaSuccess && graph &&
+                    cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess) {
+                    g.n = n; g.period = period; g.text = d_text; g.sa = d_sa; g.rank = rank;
+                    g.arena = ctx->arena; g.arena_cap = ctx->arena_cap; g.stream = s; g.epoch = ctx->option_epoch;
+                    g.launches = ctx->launches - l0;
+                    g.stats = st;
+                    RSQ_CUDA(cudaGraphLaunch(g.exec, s));
+                    done = true;
+                } else {
+                    g.exec = nullptr;
+                    ctx->launches = l0;
+                    st = reseq_sa_stats{};
+                }
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();   // a failed capture leaves nothing enqueued: the plain launches below take over
+            }
+        }
+        if (!done) RSQ_TRY(enqueue());
         RSQ_TRY(uniform_verdict(ctx, counters + 4, n, period, &st, &unfinished));
         if (unfinished == 0) {
             st.alphabet = 0;
@@ -2970,6 +3017,7 @@ int build_sa_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u32* d_sa, 
             return RESEQ_OK;
         }
         ctx->hint_n = 0;          // not that kind of text (any more): decide afresh
+        ctx->drop_spec_graph();
         st = reseq_sa_stats{};
         if (ctx->sa_host_dst == nullptr && ctx->sa_host_saved != nullptr) ctx->sa_host_dst = ctx->sa_host_saved;   // the early copy-out took the wrong array
         RSQ_CUDA(cudaMemsetAsync(counters, 0, 1024, s));

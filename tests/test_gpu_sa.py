@@ -272,6 +272,51 @@ def test_speculative_route_is_verified_on_the_device(rq, oracle):
         e.close()
 
 
+def test_repeated_device_builds_replay_one_cuda_graph(rq, oracle):
+    """A device-resident build whose text buffer, outputs, workspace, stream and options are those of the
+    previous one is replayed as one CUDA graph (sa.cu build_sa_device, option "sa_graph").  The graph reads the
+    text through its pointer: new contents in the same buffer must give the new text's order; a text of another
+    kind must fail the device-side check, fall back and drop the graph; the launch count must keep counting
+    the kernels a replay runs; switching the option off must give the same arrays."""
+    import ctypes as C
+    import torch
+    lib = rq._lib.load()
+    L, k = 60, 3000
+    def uniform(seed):
+        g = np.random.default_rng(seed).choice([65, 67, 71, 84], 20_000).astype(np.uint8)
+        st = np.random.default_rng(seed + 1).integers(0, 20_000 - L, k)
+        return np.frombuffer(b"".join(bytes(g[x:x + L]) + b"\0" for x in st), np.uint8)
+    n = k * (L + 1)
+    e = rq.Executor(0)
+    stream = torch.cuda.Stream()
+    try:
+        e.set_stream(stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            d_text = torch.empty(n, dtype=torch.uint8, device="cuda")
+            d_sa = torch.empty(n, dtype=torch.int32, device="cuda")
+            d_rank = torch.empty(n, dtype=torch.int32, device="cuda")
+            texts = [uniform(1), uniform(1), uniform(3), uniform(5)]
+            ragged = uniform(9).copy(); ragged[L] = 65; ragged[L - 7] = 0      # same length, not uniform any more
+            texts += [ragged, uniform(7), uniform(11), uniform(13)]
+            per_build = []
+            for i, t in enumerate(texts):
+                if i == 6: e.set_option("sa_graph", 0)
+                d_text.copy_(torch.from_numpy(t.copy()), non_blocking=False)
+                st = rq.SaStats()
+                l0 = e.launch_count
+                rq._lib.check(lib.reseq_cuda_build_sa_device(e.handle, C.c_void_p(d_text.data_ptr()), n, C.c_void_p(d_sa.data_ptr()),
+                                                             C.c_void_p(d_rank.data_ptr()), C.byref(st)))
+                e.synchronize()
+                per_build.append(e.launch_count - l0)
+                wsa, wrank = oracle.build_sa(t.tobytes())
+                assert np.array_equal(d_sa.cpu().numpy().view(np.uint32), wsa), f"build {i}"
+                assert np.array_equal(d_rank.cpu().numpy().view(np.uint32), wrank), f"build {i}"
+            # builds 2 and 3 replay the graph captured by build 1, build 7 launches kernel by kernel: same kernels
+            assert per_build[2] == per_build[3] == per_build[7] > 10
+    finally:
+        e.close()
+
+
 def _ragged_reads(rng, genome, k, lo, hi):
     out = []
     for _ in range(k):
