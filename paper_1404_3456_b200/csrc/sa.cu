@@ -1118,63 +1118,12 @@ link_reads_kernel(const u64* __restrict__ elems, const u32* __restrict__ list, c
 // issue slots at 0.41 of the HBM peak).  Bitmaps leave as bytes: four lanes hold eight records.
 constexpr int kAccRows = 4;                       // pairs per thread in flight
 constexpr int kAccSpan = 64 * kAccRows;           // records per warp iteration
-//
-// LOWBITS: the gather of one proof byte per suffix (a 32-sector request per warp: the pass ran at 0.40 of the HBM
-// peak on L1 wavefronts and L2 sectors) is replaced, for most suffixes, by one bit from SHARED memory: every CTA
-// first condenses the table into "cov[read] < thr" (thr = L - 24: a read whose successor starts more than 24
-// bases on is rare), one bit per read (115 KB for the 920 000 reads of config 2).  A suffix with t <= thr of a
-// read whose bit is clear is proven (t <= thr <= cov[read]) without looking the byte up; only the suffixes with
-// t > thr (24 in L) and those of the rare reads still gather.  Bit layout: four words per 128 reads, word c of a
-// block holds reads 4 * lane + c (what one ballot per byte of a 32-bit load per lane produces).
-constexpr u32 kCovLowMargin = 24;
-template <bool LOWBITS>
-__global__ void __launch_bounds__(LOWBITS ? 1024 : 256)
+__global__ void __launch_bounds__(256)
 accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict__ cov, u32 period,
                       u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
-                      u32* __restrict__ uncbits, u8* __restrict__ tileflags, u32 reads, u32 thr) {
+                      u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
     constexpr u32 K = kUniK;
     const unsigned lane = lane_id();
-    extern __shared__ u32 s_low[];
-    if constexpr (LOWBITS) {
-        const u32 blocks = (reads + 127u) >> 7;
-        const u32 wstep = blockDim.x >> 5;
-        constexpr int kInFlight = 8;                       // loads in flight per warp: the table is read at L2 speed, not latency
-        for (u32 b0 = threadIdx.x >> 5; b0 < blocks; b0 += wstep * kInFlight) {
-            u32 v[kInFlight];
-#pragma unroll
-            for (int u = 0; u < kInFlight; ++u) {
-                const u32 b = b0 + u * wstep;
-                const u32 r = (b << 7) + 4u * lane;
-                v[u] = 0xffffffffu;                        // pads: "not low"
-                if (b < blocks) {
-                    if (r + 3u < reads) v[u] = *reinterpret_cast<const u32*>(cov + r);
-                    else if (r < reads) {
-                        v[u] = 0;
-                        for (u32 c = 0; c < 4; ++c) v[u] |= static_cast<u32>(r + c < reads ? cov[r + c] : 0xffu) << (8 * c);
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kInFlight; ++u) {
-                const u32 b = b0 + u * wstep;
-                if (b >= blocks) break;
-#pragma unroll
-                for (u32 c = 0; c < 4; ++c) {
-                    const unsigned w = __ballot_sync(0xffffffffu, ((v[u] >> (8 * c)) & 0xffu) < thr);
-                    if (lane == c) s_low[4 * b + c] = w;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    auto proof = [&](u32 q, u32 t, bool in) -> u8 {
-        if constexpr (LOWBITS) {
-            const bool low = (s_low[((q >> 5) & ~3u) | (q & 3u)] >> ((q >> 2) & 31u)) & 1u;
-            return in && (t > thr || low) ? __ldg(cov + q) : static_cast<u8>(in ? 255 : 0);
-        } else {
-            return in ? __ldg(cov + q) : 0;
-        }
-    };
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     u8* hbytes = reinterpret_cast<u8*>(headbits);
     u8* ubytes = reinterpret_cast<u8*>(uncbits);
@@ -1215,8 +1164,8 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict
 #pragma unroll
         for (int c = 0; c < kAccRows; ++c) {
             const u64 i = i0 + c * 64 + 2 * lane;
-            cva[c] = proof(qa[c], ta[c], i < m);
-            cvb[c] = proof(qb[c], tb[c], i + 1 < m);
+            cva[c] = i < m ? __ldg(cov + qa[c]) : 0;
+            cvb[c] = i + 1 < m ? __ldg(cov + qb[c]) : 0;
         }
 #pragma unroll
         for (int c = 0; c < kAccRows; ++c) {
@@ -1251,6 +1200,102 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict
                 hbytes[i >> 3] = static_cast<u8>(x);
                 ubytes[i >> 3] = static_cast<u8>(x >> 8);
                 if (x >> 8) {   // the group of an uncovered member starts in this refine tile or the one before
+                    const u64 tile = i / kRefTile;
+                    tileflags[tile] = 1;
+                    if (tile) tileflags[tile - 1] = 1;
+                }
+            }
+        }
+    }
+}
+
+// The same pass with a thread owning FOUR consecutive records (two 128-bit loads, one 128-bit store of sa): three of
+// every four neighbour relations stay inside the thread, a quad's neighbours cost four shuffles, its four head bits and
+// four uncovered bits one more (two lanes make a byte), and the record before lane 0 / after lane 31 is re-read from
+// memory by that lane instead of being passed between rows.  1.25 shuffles per record instead of 5: the pairs form spent
+// 34 % of its stall samples on the shuffle queue (mio_throttle + short scoreboard, profiles/r2_ncu_full_accept.txt).
+constexpr int kAccQuadRows = 2;                    // quads per thread in flight
+__global__ void __launch_bounds__(256, 4)
+accept_uniform_quads_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict__ cov, u32 period,
+                            u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
+                            u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
+    constexpr u32 K = kUniK;
+    constexpr u64 kSpan = 128 * kAccQuadRows;       // records per warp iteration
+    const unsigned lane = lane_id();
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    u8* hbytes = reinterpret_cast<u8*>(headbits);
+    u8* ubytes = reinterpret_cast<u8*>(uncbits);
+    auto term = [&](u32 p, u32* q) {
+        *q = static_cast<u32>(__umul64hi(p, period_magic));
+        return period - 1u - (p - *q * period);
+    };
+    for (u64 i0 = ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kSpan; i0 < m; i0 += warps * kSpan) {
+        u32 k[kAccQuadRows][4], p[kAccQuadRows][4], t[kAccQuadRows][4], q[kAccQuadRows][4];
+        u32 kp[kAccQuadRows], tp[kAccQuadRows], kn[kAccQuadRows], tn[kAccQuadRows];   // the records around the quad
+#pragma unroll
+        for (int c = 0; c < kAccQuadRows; ++c) {
+            const u64 i = i0 + c * 128 + 4 * lane;
+            ulonglong2 v0 = make_ulonglong2(0, 0), v1 = make_ulonglong2(0, 0);
+            if (i + 3 < m) {
+                v0 = *reinterpret_cast<const ulonglong2*>(elems + i);
+                v1 = *reinterpret_cast<const ulonglong2*>(elems + i + 2);
+            } else {
+                if (i < m) v0.x = elems[i];
+                if (i + 1 < m) v0.y = elems[i + 1];
+                if (i + 2 < m) v1.x = elems[i + 2];
+            }
+            k[c][0] = static_cast<u32>(v0.x >> 32); p[c][0] = static_cast<u32>(v0.x);
+            k[c][1] = static_cast<u32>(v0.y >> 32); p[c][1] = static_cast<u32>(v0.y);
+            k[c][2] = static_cast<u32>(v1.x >> 32); p[c][2] = static_cast<u32>(v1.x);
+            k[c][3] = static_cast<u32>(v1.y >> 32); p[c][3] = static_cast<u32>(v1.y);
+            // lane 0 / lane 31: the record before / after this row of 128, straight from memory (a cache hit)
+            u64 eb = 0, ea = 0;
+            if (lane == 0 && i > 0 && i < m) eb = elems[i - 1];
+            if (lane == 31 && i + 4 < m) ea = elems[i + 4];
+            u32 qx;
+            kp[c] = static_cast<u32>(eb >> 32); tp[c] = term(static_cast<u32>(eb), &qx);
+            kn[c] = static_cast<u32>(ea >> 32); tn[c] = term(static_cast<u32>(ea), &qx);
+        }
+#pragma unroll
+        for (int c = 0; c < kAccQuadRows; ++c)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) t[c][j] = term(p[c][j], &q[c][j]);
+        u8 cv[kAccQuadRows][4];   // the proof bytes, gathered up front (L2-resident table)
+#pragma unroll
+        for (int c = 0; c < kAccQuadRows; ++c)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cv[c][j] = i0 + c * 128 + 4 * lane + j < m ? __ldg(cov + q[c][j]) : 0;
+#pragma unroll
+        for (int c = 0; c < kAccQuadRows; ++c) {
+            const u64 i = i0 + c * 128 + 4 * lane;
+            const u32 ku = __shfl_up_sync(0xffffffffu, k[c][3], 1), tu = __shfl_up_sync(0xffffffffu, t[c][3], 1);
+            const u32 kd = __shfl_down_sync(0xffffffffu, k[c][0], 1), td = __shfl_down_sync(0xffffffffu, t[c][0], 1);
+            if (lane != 0) { kp[c] = ku; tp[c] = tu; }
+            if (lane != 31) { kn[c] = kd; tn[c] = td; }
+            u32 hn = 0, un = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool in = i + j < m;
+                const u32 kprev = j ? k[c][j - 1] : kp[c], tprev = j ? t[c][j - 1] : tp[c];
+                const u32 knext = j < 3 ? k[c][j + 1] : kn[c], tnext = j < 3 ? t[c][j + 1] : tn[c];
+                // a suffix shorter than the key is final after the sort; a group starts where the key
+                // changes or right behind such a suffix
+                const bool head = in && (i + j == 0 || k[c][j] != kprev || t[c][j] < K || tprev < K);
+                const bool last = i + j + 1 >= m || knext != k[c][j] || tnext < K;   // (t < K: the next record is a head then, too)
+                const bool unc = in && !last && t[c][j] >= K && t[c][j] > cv[c][j];
+                hn |= static_cast<u32>(head) << j;
+                un |= static_cast<u32>(unc) << j;
+            }
+            if (i + 3 < m) *reinterpret_cast<uint4*>(sa_out + i) = make_uint4(p[c][0], p[c][1], p[c][2], p[c][3]);
+            else
+                for (int j = 0; j < 4; ++j)
+                    if (i + j < m) sa_out[i + j] = p[c][j];
+            u32 x = (hn | (un << 8)) << (4 * (lane & 1));
+            x |= __shfl_xor_sync(0xffffffffu, x, 1);
+            if ((lane & 1) == 0 && i < m) {
+                hbytes[i >> 3] = static_cast<u8>(x);
+                ubytes[i >> 3] = static_cast<u8>(x >> 8);
+                if ((x >> 8) & 0xffu) {   // the group of an uncovered member starts in this refine tile or the one before
                     const u64 tile = i / kRefTile;
                     tileflags[tile] = 1;
                     if (tile) tileflags[tile - 1] = 1;
@@ -2734,24 +2779,12 @@ int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sen
     RSQ_CUDA(cudaMemsetAsync(tileflags, 0, m / kRefTile + 2, s));
     if ((reinterpret_cast<uintptr_t>(sorted) & 15) || (reinterpret_cast<uintptr_t>(sa_out) & 7))
         return fail(RESEQ_INVALID_ARGUMENT, "record and suffix-array buffers must be 16- / 8-byte aligned");
-    {
-        // the per-read "proof is short" bitmap in shared memory when it fits one SM (see the kernel)
-        const u64 reads = n_text / period;
-        const size_t low_bytes = ((reads + 127) / 128) * 16;
-        const bool lowbits = ctx->opt_accept_lowbits != 0 && period > 2 * kCovLowMargin && low_bytes <= 200 * 1024 &&
-                             m >= (1u << 22) && (reinterpret_cast<uintptr_t>(cov) & 3) == 0;
-        if (lowbits) {
-            RSQ_OPT_IN_SMEM(ctx, accept_uniform_kernel<true>, 200 * 1024);   // the largest bitmap taken
-            const int threads = 2 * (low_bytes + 1024) <= 228 * 1024 ? 512 : 1024;   // two CTAs per SM while two bitmaps fit
-            const unsigned grid = static_cast<unsigned>(ctx->sm_count) * (threads == 512 ? 2u : 1u);
-            accept_uniform_kernel<true><<<grid, threads, low_bytes, s>>>(sorted, m, cov, period, magic, sa_out, headbits, uncbits,
-                                                                         tileflags, static_cast<u32>(reads),
-                                                                         period - 1u - kCovLowMargin);
-        } else {
-            accept_uniform_kernel<false><<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
-                                                                                  uncbits, tileflags, 0u, 0u);
-        }
-    }
+    if (ctx->opt_accept_quads != 0 && (reinterpret_cast<uintptr_t>(sa_out) & 15) == 0)
+        accept_uniform_quads_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
+                                                                               uncbits, tileflags);
+    else
+        accept_uniform_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
+                                                                         uncbits, tileflags);
     RSQ_LAUNCH_END(ctx);
     RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<kRefUniform>, kRefSmem);
     const unsigned tiles = static_cast<unsigned>((m + kRefTile - 1) / kRefTile);
