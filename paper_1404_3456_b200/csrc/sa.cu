@@ -1214,13 +1214,18 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict
 // four uncovered bits one more (two lanes make a byte), and the record before lane 0 / after lane 31 is re-read from
 // memory by that lane instead of being passed between rows.  1.25 shuffles per record instead of 5: the pairs form spent
 // 34 % of its stall samples on the shuffle queue (mio_throttle + short scoreboard, profiles/r2_ncu_full_accept.txt).
-constexpr int kAccQuadRows = 2;                    // quads per thread in flight
+// Measured [B200, config 2]: pairs 0.657 ms, quads (W = 4) 0.613 ms, W = 8 (a whole bitmap byte per thread, no byte
+// shuffle, but 128-bit loads 64 bytes apart within a warp) 0.697 ms.
+template <int W>
 __global__ void __launch_bounds__(256, 4)
 accept_uniform_quads_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict__ cov, u32 period,
                             u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
                             u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
+    static_assert(W == 4 || W == 8, "four or eight consecutive records per thread");
     constexpr u32 K = kUniK;
-    constexpr u64 kSpan = 128 * kAccQuadRows;       // records per warp iteration
+    constexpr int R = 8 / W;                        // rows per thread in flight
+    constexpr u64 kRow = 32 * W;                    // records per warp row
+    constexpr u64 kSpan = kRow * R;                 // records per warp iteration
     const unsigned lane = lane_id();
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     u8* hbytes = reinterpret_cast<u8*>(headbits);
@@ -1230,54 +1235,49 @@ accept_uniform_quads_kernel(const u64* __restrict__ elems, u64 m, const u8* __re
         return period - 1u - (p - *q * period);
     };
     for (u64 i0 = ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kSpan; i0 < m; i0 += warps * kSpan) {
-        u32 k[kAccQuadRows][4], p[kAccQuadRows][4], t[kAccQuadRows][4], q[kAccQuadRows][4];
-        u32 kp[kAccQuadRows], tp[kAccQuadRows], kn[kAccQuadRows], tn[kAccQuadRows];   // the records around the quad
+        u32 k[R][W], p[R][W], t[R][W], q[R][W];
+        u32 kp[R], tp[R], kn[R], tn[R];             // the records around the thread's stretch
 #pragma unroll
-        for (int c = 0; c < kAccQuadRows; ++c) {
-            const u64 i = i0 + c * 128 + 4 * lane;
-            ulonglong2 v0 = make_ulonglong2(0, 0), v1 = make_ulonglong2(0, 0);
-            if (i + 3 < m) {
-                v0 = *reinterpret_cast<const ulonglong2*>(elems + i);
-                v1 = *reinterpret_cast<const ulonglong2*>(elems + i + 2);
-            } else {
-                if (i < m) v0.x = elems[i];
-                if (i + 1 < m) v0.y = elems[i + 1];
-                if (i + 2 < m) v1.x = elems[i + 2];
+        for (int c = 0; c < R; ++c) {
+            const u64 i = i0 + c * kRow + W * lane;
+#pragma unroll
+            for (int h = 0; h < W / 2; ++h) {
+                ulonglong2 v = make_ulonglong2(0, 0);
+                if (i + 2 * h + 1 < m) v = *reinterpret_cast<const ulonglong2*>(elems + i + 2 * h);
+                else if (i + 2 * h < m) v.x = elems[i + 2 * h];
+                k[c][2 * h] = static_cast<u32>(v.x >> 32); p[c][2 * h] = static_cast<u32>(v.x);
+                k[c][2 * h + 1] = static_cast<u32>(v.y >> 32); p[c][2 * h + 1] = static_cast<u32>(v.y);
             }
-            k[c][0] = static_cast<u32>(v0.x >> 32); p[c][0] = static_cast<u32>(v0.x);
-            k[c][1] = static_cast<u32>(v0.y >> 32); p[c][1] = static_cast<u32>(v0.y);
-            k[c][2] = static_cast<u32>(v1.x >> 32); p[c][2] = static_cast<u32>(v1.x);
-            k[c][3] = static_cast<u32>(v1.y >> 32); p[c][3] = static_cast<u32>(v1.y);
-            // lane 0 / lane 31: the record before / after this row of 128, straight from memory (a cache hit)
+            // lane 0 / lane 31: the record before / after this row, straight from memory (a cache hit)
             u64 eb = 0, ea = 0;
             if (lane == 0 && i > 0 && i < m) eb = elems[i - 1];
-            if (lane == 31 && i + 4 < m) ea = elems[i + 4];
+            if (lane == 31 && i + W < m) ea = elems[i + W];
             u32 qx;
             kp[c] = static_cast<u32>(eb >> 32); tp[c] = term(static_cast<u32>(eb), &qx);
             kn[c] = static_cast<u32>(ea >> 32); tn[c] = term(static_cast<u32>(ea), &qx);
         }
 #pragma unroll
-        for (int c = 0; c < kAccQuadRows; ++c)
+        for (int c = 0; c < R; ++c)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) t[c][j] = term(p[c][j], &q[c][j]);
-        u8 cv[kAccQuadRows][4];   // the proof bytes, gathered up front (L2-resident table)
+            for (int j = 0; j < W; ++j) t[c][j] = term(p[c][j], &q[c][j]);
+        u8 cv[R][W];   // the proof bytes, gathered up front (L2-resident table)
 #pragma unroll
-        for (int c = 0; c < kAccQuadRows; ++c)
+        for (int c = 0; c < R; ++c)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) cv[c][j] = i0 + c * 128 + 4 * lane + j < m ? __ldg(cov + q[c][j]) : 0;
+            for (int j = 0; j < W; ++j) cv[c][j] = i0 + c * kRow + W * lane + j < m ? __ldg(cov + q[c][j]) : 0;
 #pragma unroll
-        for (int c = 0; c < kAccQuadRows; ++c) {
-            const u64 i = i0 + c * 128 + 4 * lane;
-            const u32 ku = __shfl_up_sync(0xffffffffu, k[c][3], 1), tu = __shfl_up_sync(0xffffffffu, t[c][3], 1);
+        for (int c = 0; c < R; ++c) {
+            const u64 i = i0 + c * kRow + W * lane;
+            const u32 ku = __shfl_up_sync(0xffffffffu, k[c][W - 1], 1), tu = __shfl_up_sync(0xffffffffu, t[c][W - 1], 1);
             const u32 kd = __shfl_down_sync(0xffffffffu, k[c][0], 1), td = __shfl_down_sync(0xffffffffu, t[c][0], 1);
             if (lane != 0) { kp[c] = ku; tp[c] = tu; }
             if (lane != 31) { kn[c] = kd; tn[c] = td; }
             u32 hn = 0, un = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < W; ++j) {
                 const bool in = i + j < m;
-                const u32 kprev = j ? k[c][j - 1] : kp[c], tprev = j ? t[c][j - 1] : tp[c];
-                const u32 knext = j < 3 ? k[c][j + 1] : kn[c], tnext = j < 3 ? t[c][j + 1] : tn[c];
+                const u32 kprev = j ? k[c][j ? j - 1 : 0] : kp[c], tprev = j ? t[c][j ? j - 1 : 0] : tp[c];
+                const u32 knext = j < W - 1 ? k[c][j < W - 1 ? j + 1 : j] : kn[c], tnext = j < W - 1 ? t[c][j < W - 1 ? j + 1 : j] : tn[c];
                 // a suffix shorter than the key is final after the sort; a group starts where the key
                 // changes or right behind such a suffix
                 const bool head = in && (i + j == 0 || k[c][j] != kprev || t[c][j] < K || tprev < K);
@@ -1286,13 +1286,22 @@ accept_uniform_quads_kernel(const u64* __restrict__ elems, u64 m, const u8* __re
                 hn |= static_cast<u32>(head) << j;
                 un |= static_cast<u32>(unc) << j;
             }
-            if (i + 3 < m) *reinterpret_cast<uint4*>(sa_out + i) = make_uint4(p[c][0], p[c][1], p[c][2], p[c][3]);
-            else
-                for (int j = 0; j < 4; ++j)
-                    if (i + j < m) sa_out[i + j] = p[c][j];
-            u32 x = (hn | (un << 8)) << (4 * (lane & 1));
-            x |= __shfl_xor_sync(0xffffffffu, x, 1);
-            if ((lane & 1) == 0 && i < m) {
+#pragma unroll
+            for (int h = 0; h < W / 4; ++h) {
+                if (i + 4 * h + 3 < m)
+                    *reinterpret_cast<uint4*>(sa_out + i + 4 * h) = make_uint4(p[c][4 * h], p[c][4 * h + 1], p[c][4 * h + 2], p[c][4 * h + 3]);
+                else
+                    for (int j = 4 * h; j < 4 * h + 4; ++j)
+                        if (i + j < m) sa_out[i + j] = p[c][j];
+            }
+            u32 x = hn | (un << 8);
+            bool writer = true;
+            if constexpr (W == 4) {   // two lanes make a byte
+                x <<= 4 * (lane & 1);
+                x |= __shfl_xor_sync(0xffffffffu, x, 1);
+                writer = (lane & 1) == 0;
+            }
+            if (writer && i < m) {
                 hbytes[i >> 3] = static_cast<u8>(x);
                 ubytes[i >> 3] = static_cast<u8>(x >> 8);
                 if ((x >> 8) & 0xffu) {   // the group of an uncovered member starts in this refine tile or the one before
@@ -2780,8 +2789,8 @@ int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sen
     if ((reinterpret_cast<uintptr_t>(sorted) & 15) || (reinterpret_cast<uintptr_t>(sa_out) & 7))
         return fail(RESEQ_INVALID_ARGUMENT, "record and suffix-array buffers must be 16- / 8-byte aligned");
     if (ctx->opt_accept_quads != 0 && (reinterpret_cast<uintptr_t>(sa_out) & 15) == 0)
-        accept_uniform_quads_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
-                                                                               uncbits, tileflags);
+        accept_uniform_quads_kernel<4><<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
+                                                                                  uncbits, tileflags);
     else
         accept_uniform_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
                                                                          uncbits, tileflags);
