@@ -412,7 +412,7 @@ constexpr int kStageRank = 272;   // rank entries staged per fragment: <= 255 + 
 constexpr int kStageText = 12;    // packed words staged per fragment
 
 template <bool CONTAINED, bool STAGE = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (STAGE || CONTAINED) ? 4 : 6)
 overlap_count_kernel(IndexView iv, u32 min_ov, u64 f0, u64 f1, const u64* __restrict__ qoff,
                      u32* __restrict__ q_first, u32* __restrict__ q_count, u8* __restrict__ contained,
                      u32* __restrict__ rawcount) {

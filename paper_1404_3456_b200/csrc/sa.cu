@@ -2356,37 +2356,38 @@ shard_general_kernel(const u64* __restrict__ packed, const u64* __restrict__ sen
 // sit next to: the owner comes from one multiply-high by a host-made reciprocal and a fix-up against the
 // table of bases; the sub-bin from a shift.)
 struct OwnerTable {
-    u64 base[17];    // base[g] = floor(n g / G), base[G] = n
-    u64 magic;       // floor(2^64 G / n): mulhi(p, magic) is floor(p G / n) or one less
+    u64 base[17];    // base[g] = floor(n g / G), base[G] = n  (n <= 2^32 - 2: every base but base[G] fits 32 bits, and so does base[G])
+    u32 magic;       // floor(2^32 G / n): mulhi32(p, magic) is floor(p G / n) or up to two less
     u32 G;
-    u32 sub_shift;   // (unused by the low-bit rule below; kept for the layout)
     u32 sub;         // sub-bins per owner (a power of two; G * sub <= 1024)
 };
 constexpr int kOwnMaxBins = 1024;
 constexpr int kOwnBlock = 512, kOwnItems = 8, kOwnTile = kOwnBlock * kOwnItems;
-// `base` = the table's bases copied to SHARED memory by the caller: lanes look up different owners, and a
-// kernel parameter indexed per lane is a constant-bank load replayed once per distinct owner in the warp.
-__device__ __forceinline__ u32 owner_bin(const OwnerTable& tb, const u64* __restrict__ base, u64 p, u64* rel) {
-    u32 g = static_cast<u32>(__umul64hi(p, tb.magic));          // the owner, or up to two below it
+// `base` = the table's bases copied to SHARED memory by the caller as 32-bit words: lanes look up different owners,
+// and a kernel parameter indexed per lane is a constant-bank load replayed once per distinct owner in the warp.
+// Positions are 32-bit, so the owner estimate is ONE 32 x 32 multiply-high (the 64-bit reciprocal of the first
+// form cost ten instructions) and the fix-up compares words.
+__device__ __forceinline__ u32 owner_bin(const OwnerTable& tb, const u32* __restrict__ base, u32 p, u32* rel) {
+    u32 g = __umulhi(p, tb.magic);                              // the owner, or up to two below it
     while (g + 1 < tb.G && base[g + 1] <= p) ++g;
     *rel = p - base[g];
     // the sub-bin only spreads the shared-memory atomics: LOW position bits, so that an owner's group
     // stays unordered in the high bits the receiver partitions on (top bits made every tile of its first
     // pass hit one bin: 0.79 ms against 0.52)
-    return g * tb.sub + (static_cast<u32>(*rel >> 2) & (tb.sub - 1u));
+    return g * tb.sub + ((*rel >> 2) & (tb.sub - 1u));
 }
 
 __global__ void __launch_bounds__(256)
 owner_count_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u32* __restrict__ counts) {
     __shared__ u32 s_cnt[kOwnMaxBins];
-    __shared__ u64 s_base[17];
+    __shared__ u32 s_base[17];
     const u32 bins = tb.G * tb.sub;
     for (u32 b = threadIdx.x; b < bins; b += blockDim.x) s_cnt[b] = 0;
-    if (threadIdx.x <= tb.G) s_base[threadIdx.x] = tb.base[threadIdx.x];
+    if (threadIdx.x <= tb.G) s_base[threadIdx.x] = static_cast<u32>(tb.base[threadIdx.x]);
     __syncthreads();
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     const u64 tid0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
-    u64 rel;
+    u32 rel;
     // four positions per 16-byte load, two loads in flight (one 4-byte load per trip left the sweep waiting on
     // DRAM latency: 1.75 ms for 378 M positions, 0.9 TB/s)
     const u64 quads = (reinterpret_cast<uintptr_t>(sa) & 15) == 0 ? m / 4 : 0;
@@ -2421,7 +2422,7 @@ owner_count_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u32* __rest
 // starts at the bin's base, the tile leaves through shared memory as one contiguous run per bin.
 __global__ void __launch_bounds__(kOwnBlock, 2)
 owner_partition_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u64 offset, u32* __restrict__ claim,
-                       u64* __restrict__ out) {
+                       u64* __restrict__ out, u32 num_tiles) {
     extern __shared__ __align__(16) unsigned char own_smem[];
     u64* s_rec = reinterpret_cast<u64*>(own_smem);                                  // [tile] records, bin-sorted
     u32* s_cnt = reinterpret_cast<u32*>(s_rec + kOwnTile);                          // [1024]
@@ -2432,63 +2433,82 @@ owner_partition_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u64 off
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     const int bins = static_cast<int>(tb.G * tb.sub);
-    __shared__ u64 s_base[17];
+    __shared__ u32 s_base[17];
+    // Persistent, like inv_partition_persistent_kernel: two CTAs per SM walk the tiles round-robin and issue the next
+    // tile's loads before the current one is scanned, exchanged and stored (one tile per CTA: 3.2 ms for 378 M
+    // positions against 1.3 ms for the receiver's pass over the same records).
+    auto load_tile = [&](u32 tile, u32 (&p)[kOwnItems]) {
+        const u64 t0 = static_cast<u64>(tile) * kOwnTile;
+#pragma unroll
+        for (int j = 0; j < kOwnItems; ++j) {
+            const u64 i = t0 + static_cast<u64>(j) * kOwnBlock + tid;
+            p[j] = i < m ? sa[i] : 0u;
+        }
+    };
+    u32 pos[kOwnItems], nxt[kOwnItems];
+    if (blockIdx.x < num_tiles) load_tile(blockIdx.x, pos);
     for (int b = tid; b < bins; b += kOwnBlock) s_cnt[b] = 0;
-    if (tid <= static_cast<int>(tb.G)) s_base[tid] = tb.base[tid];
+    if (tid <= static_cast<int>(tb.G)) s_base[tid] = static_cast<u32>(tb.base[tid]);
     __syncthreads();
-    const u64 tile0 = static_cast<u64>(blockIdx.x) * kOwnTile;
-    const u32 valid = static_cast<u32>(m - tile0 < static_cast<u64>(kOwnTile) ? m - tile0 : kOwnTile);
-    u64 rec[kOwnItems];
-    u32 slot[kOwnItems], bin[kOwnItems];
+    for (u32 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const u64 tile0 = static_cast<u64>(tile) * kOwnTile;
+        const u32 valid = static_cast<u32>(m - tile0 < static_cast<u64>(kOwnTile) ? m - tile0 : kOwnTile);
+        u64 rec[kOwnItems];
+        u32 slot[kOwnItems], bin[kOwnItems];
 #pragma unroll
-    for (int j = 0; j < kOwnItems; ++j) {
-        const u32 li = static_cast<u32>(j) * kOwnBlock + tid;
-        slot[j] = 0;
-        bin[j] = 0;
-        rec[j] = 0;
-        if (li < valid) {
-            u64 rel;
-            bin[j] = owner_bin(tb, s_base, sa[tile0 + li], &rel);
-            rec[j] = (rel << 32) | ((offset + tile0 + li) & 0xffffffffu);
-            slot[j] = atomicAdd(&s_cnt[bin[j]], 1u);
+        for (int j = 0; j < kOwnItems; ++j) {
+            const u32 li = static_cast<u32>(j) * kOwnBlock + tid;
+            slot[j] = 0;
+            bin[j] = 0;
+            rec[j] = 0;
+            if (li < valid) {
+                u32 rel;
+                bin[j] = owner_bin(tb, s_base, pos[j], &rel);
+                rec[j] = (static_cast<u64>(rel) << 32) | ((offset + tile0 + li) & 0xffffffffu);
+                slot[j] = atomicAdd(&s_cnt[bin[j]], 1u);
+            }
         }
-    }
-    __syncthreads();
-    // two bins per thread (bins <= 1024 = 2 * block): counts, claims, exclusive scan
-    const int b0 = 2 * tid, b1 = 2 * tid + 1;
-    const u32 c0 = b0 < bins ? s_cnt[b0] : 0u, c1 = b1 < bins ? s_cnt[b1] : 0u;
-    u32 g0 = 0, g1 = 0;
-    if (c0) g0 = atomicAdd(claim + b0, c0);
-    if (c1) g1 = atomicAdd(claim + b1, c1);
-    u32 inc = c0 + c1;
+        if (tile + gridDim.x < num_tiles) load_tile(tile + gridDim.x, nxt);   // in flight until the end of this tile
+        __syncthreads();
+        // two bins per thread (bins <= 1024 = 2 * block): counts, claims, exclusive scan
+        const int b0 = 2 * tid, b1 = 2 * tid + 1;
+        const u32 c0 = b0 < bins ? s_cnt[b0] : 0u, c1 = b1 < bins ? s_cnt[b1] : 0u;
+        u32 g0 = 0, g1 = 0;
+        if (c0) g0 = atomicAdd(claim + b0, c0);
+        if (c1) g1 = atomicAdd(claim + b1, c1);
+        u32 inc = c0 + c1;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (static_cast<int>(lane) >= o) inc += t;
-    }
-    if (lane == 31) s_warp[tid >> 5] = inc;
-    __syncthreads();
-    u32 before = 0;
-#pragma unroll
-    for (int w = 0; w < kOwnBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
-    const u32 excl = before + inc - (c0 + c1);
-    if (b0 < bins) { s_ofs[b0] = excl; s_gdst[b0] = g0 - excl; }
-    if (b1 < bins) { s_ofs[b1] = excl + c0; s_gdst[b1] = g1 - (excl + c0); }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kOwnItems; ++j) {
-        const u32 li = static_cast<u32>(j) * kOwnBlock + tid;
-        if (li < valid) {
-            const u32 at = s_ofs[bin[j]] + slot[j];
-            s_rec[at] = rec[j];
-            s_binof[at] = static_cast<unsigned short>(bin[j]);
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (static_cast<int>(lane) >= o) inc += t;
         }
-    }
-    __syncthreads();
+        if (lane == 31) s_warp[tid >> 5] = inc;
+        __syncthreads();
+        u32 before = 0;
 #pragma unroll
-    for (int j = 0; j < kOwnItems; ++j) {
-        const u32 pidx = static_cast<u32>(j) * kOwnBlock + tid;
-        if (pidx < valid) out[static_cast<u64>(s_gdst[s_binof[pidx]]) + pidx] = s_rec[pidx];
+        for (int w = 0; w < kOwnBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
+        const u32 excl = before + inc - (c0 + c1);
+        if (b0 < bins) { s_ofs[b0] = excl; s_gdst[b0] = g0 - excl; s_cnt[b0] = 0; }
+        if (b1 < bins) { s_ofs[b1] = excl + c0; s_gdst[b1] = g1 - (excl + c0); s_cnt[b1] = 0; }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kOwnItems; ++j) {
+            const u32 li = static_cast<u32>(j) * kOwnBlock + tid;
+            if (li < valid) {
+                const u32 at = s_ofs[bin[j]] + slot[j];
+                s_rec[at] = rec[j];
+                s_binof[at] = static_cast<unsigned short>(bin[j]);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kOwnItems; ++j) {
+            const u32 pidx = static_cast<u32>(j) * kOwnBlock + tid;
+            if (pidx < valid) out[static_cast<u64>(s_gdst[s_binof[pidx]]) + pidx] = s_rec[pidx];
+        }
+#pragma unroll
+        for (int j = 0; j < kOwnItems; ++j) pos[j] = nxt[j];
+        __syncthreads();   // s_rec / s_gdst / s_binof are rewritten by the next tile
     }
 }
 constexpr size_t kOwnSmem = sizeof(u64) * kOwnTile + sizeof(u32) * (3 * kOwnMaxBins + kOwnBlock / 32) + sizeof(unsigned short) * kOwnTile;
@@ -3567,7 +3587,8 @@ int reseq_cuda_sa_shard_bucket_records(reseq_cuda_sa_shard* sh, uint64_t* d_reco
 int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bucket, size_t m, uint64_t global_offset,
                                     uint64_t n, int world, uint64_t* d_records_out, uint64_t* counts_out) {
     using namespace rsq;
-    if (!ctx || !counts_out || world < 1 || world > 16 || n == 0 || static_cast<uint64_t>(world) >= n) return fail(RESEQ_INVALID_ARGUMENT, "bad argument (1 <= world <= 16)");
+    if (!ctx || !counts_out || world < 1 || world > 16 || n == 0 || static_cast<uint64_t>(world) >= n || n > RESEQ_CUDA_MAX_TEXT)
+        return fail(RESEQ_INVALID_ARGUMENT, "bad argument (1 <= world <= 16, world < n <= 2^32 - 2)");
     for (int g = 0; g < world; ++g) counts_out[g] = 0;
     if (m == 0) return RESEQ_OK;
     if (!d_sa_bucket || !d_records_out) return fail(RESEQ_INVALID_ARGUMENT, "null device buffer");
@@ -3586,13 +3607,9 @@ int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bu
     RSQ_LAUNCH_BEGIN(ctx, "owner_count_kernel");
     OwnerTable tb{};
     tb.G = static_cast<u32>(world);
-    u64 max_len = 1;
     for (int g = 0; g <= world; ++g) tb.base[g] = static_cast<u64>((static_cast<unsigned __int128>(n) * g) / world);
-    for (int g = 0; g < world; ++g) max_len = std::max<u64>(max_len, tb.base[g + 1] - tb.base[g]);
-    tb.magic = static_cast<u64>((static_cast<unsigned __int128>(world) << 64) / n);   // world < n: fits 64 bits
-    const unsigned width = bit_width_u64(max_len - 1);
+    tb.magic = static_cast<u32>((static_cast<u64>(world) << 32) / n);   // world < n: fits 32 bits
     tb.sub = 1u << sub_bits;
-    tb.sub_shift = width > static_cast<unsigned>(sub_bits) ? width - sub_bits : 0;
     owner_count_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(d_sa_bucket, m, tb, counts);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
@@ -3609,8 +3626,11 @@ int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bu
     RSQ_CUDA(cudaMemcpyAsync(claim, h, sizeof(u32) * bins, cudaMemcpyHostToDevice, s));
     RSQ_LAUNCH_BEGIN(ctx, "owner_partition_kernel");
     RSQ_OPT_IN_SMEM(ctx, owner_partition_kernel, kOwnSmem);
-    owner_partition_kernel<<<static_cast<unsigned>((m + kOwnTile - 1) / kOwnTile), kOwnBlock, kOwnSmem, s>>>(
-        d_sa_bucket, m, tb, global_offset, claim, d_records_out);
+    {
+        const u32 num_tiles = static_cast<u32>((m + kOwnTile - 1) / kOwnTile);
+        const unsigned grid = num_tiles < 2u * static_cast<unsigned>(ctx->sm_count) ? num_tiles : 2u * static_cast<unsigned>(ctx->sm_count);
+        owner_partition_kernel<<<grid, kOwnBlock, kOwnSmem, s>>>(d_sa_bucket, m, tb, global_offset, claim, d_records_out, num_tiles);
+    }
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
     RSQ_CUDA(cudaStreamSynchronize(s));   // the pinned staging words are reused by the next call
