@@ -14,7 +14,7 @@ python bench.py --workload c3 --sweep --steps 10 --warmup 3 --no-overlap --no-cp
 python bench.py --workload c4 --steps 5 --warmup 3 --no-overlap --no-cpu --no-routes > gpurun_out/bench_${tag}_c4.json 2>> gpurun_out/bench_${tag}.err
 python bench.py --workload c5 --steps 3 --warmup 3 --no-overlap --no-cpu --no-routes > gpurun_out/bench_${tag}_c5.json 2>> gpurun_out/bench_${tag}.err
 head -c 300 gpurun_out/bench_${tag}.json; echo
-bash scripts/gpu_ncu.sh ${tag} onesweep:sa:onesweep_kernel accept:sa:accept_uniform gen:sa:gen_uniform invpart:sa:inv_partition
+bash scripts/gpu_ncu.sh ${tag} onesweep:sa:onesweep_kernel accept:sa:accept_uniform gen:sa:gen_uniform invpart:sa:inv_partition ov_count:ov:overlap_count_kernel ov_fill:ov:overlap_fill_sorted ov_contained:ov:contained_kernel
 timeout 900 python scripts/model_scaling.py --workload c4 --gpus 1,2,4,8 --out gpurun_out/scaling_model_${tag}_c4.json 2>&1 | grep "^G="
 timeout 1200 python scripts/model_scaling.py --workload c5 --gpus 1,2,4,8 --out gpurun_out/scaling_model_${tag}_c5.json 2>&1 | grep "^G="
 bash scripts/gpu_shard.sh ${tag} c4 2>&1 | grep "plain\|forced" | head -4
