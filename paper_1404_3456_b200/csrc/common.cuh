@@ -63,6 +63,7 @@ struct reseq_cuda_ctx {
     int sm_count = rsq::kSmCount;
     uint64_t launches = 0;
     int opt_inverse_lo_bits = -1;  // extra partition bits before the inverse scatter (-1 = auto)
+    int opt_inverse_repl = -1;     // replicated claim counters in the first inverse partition pass (-1 = from 2^28 records on)
     int opt_inverse_mode = 0;      // 0: two partition passes + shared-memory window; 1: one pass + L2-window scatter
     int opt_shortcut = 1;      // sentinel-distance shortcut in the refine kernel (tuning / tests)
     int opt_lookahead = 8;     // onesweep look-back descriptors in flight per digit (1..8)

@@ -1694,16 +1694,31 @@ constexpr int kIpMaxBins = 1024;
 // scanned, exchanged and stored, and the claims before the exchange, so the HBM latency of the
 // load and the L2 latency of the atomics are covered by the tile's own work (one tile per CTA:
 // 0.68 ms per pass at n = 139 M, 55 % of stalls on those two scoreboards; this form: 0.48 ms).
-template <int MODE>
+// REPLICATED CLAIMS (repl = kIpRepl, first passes of large arrays).  In a first pass every tile claims from the SAME
+// `nbins` counters: at 1 G records that is 246 000 tiles x 120 bins on 120 addresses, and the pass ran at 0.33 of the
+// HBM peak against 0.60 for the second pass over the same records, whose claims spread over bucket x bin counters.  A
+// bucket is therefore cut into `repl` stretches of known size, each with its own counter; a tile starts at stretch
+// (tile + bin) mod repl and takes [old, old + count) from it -- or, where the stretch runs out, what is left of it and
+// the rest from the next ones (a bucket's stretches hold exactly its records, so one round over them always
+// finds room).  Almost every run of a tile lands in one stretch; a second piece is carried through the scatter as a
+// threshold, and anything beyond two pieces (the last tiles of a bucket) is stored by the bin's own thread.
+constexpr int kIpRepl = 8;
+template <int MODE, bool REPL = false>
 __global__ void __launch_bounds__(kIpBlock, 2)
 inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shift, int prev_shift, int nbins,
                                 u32* __restrict__ claim, u64* __restrict__ out, u32 num_tiles,
                                 const u32* __restrict__ vals = nullptr) {
+    static_assert(!REPL || MODE != kIpRec, "replicated claims are for first passes (bin0 = 0)");
+    constexpr u32 repl_bits = REPL ? 3 : 0;
+    constexpr u32 repl = 1u << repl_bits;     // claim counters per bin
+    static_assert(repl == 1 || repl == static_cast<u32>(kIpRepl), "kIpRepl counters per bin");
     __shared__ __align__(16) u64 s_rec[kIpTile];
-    __shared__ u32 s_cnt[kIpMaxBins];
-    __shared__ u32 s_ofs[kIpMaxBins];
+    __shared__ u32 s_cnt[kIpMaxBins];     // counts of the tile; (replicated claims) destination of a run's second piece
+    __shared__ std::conditional_t<REPL, unsigned short, u32> s_ofs[kIpMaxBins];   // first tile slot of the bin (16 bits where the static 48 KB are tight)
     __shared__ u32 s_gdst[kIpMaxBins];
+    __shared__ u32 s_thr[REPL ? kIpMaxBins : 1];   // (replicated claims) tile slot where a run's second piece starts | end of it << 16
     __shared__ u32 s_warp[kIpBlock / 32];
+    __shared__ u32 s_more;                // (replicated claims) some run of this tile needs a third piece
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     auto load_tile = [&](u32 tile, u64 (&r)[kIpItems]) {
@@ -1719,9 +1734,18 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
                 r[j] = i < n ? static_cast<const u64*>(in_raw)[i] : 0;
         }
     };
+    // stretch r of bucket b (replicated claims; first passes: bucket b = positions [b << shift, (b + 1) << shift) of n)
+    auto stretch = [&](u32 b, u32 r, u32* lo) -> u32 {
+        const u64 base = static_cast<u64>(b) << shift;
+        const u32 sz = static_cast<u32>(n - base < (1ull << shift) ? n - base : (1ull << shift));
+        const u32 l = static_cast<u32>((static_cast<u64>(sz) * r) >> repl_bits), h = static_cast<u32>((static_cast<u64>(sz) * (r + 1)) >> repl_bits);
+        *lo = l;
+        return h - l;
+    };
     u64 rec[kIpItems], nxt[kIpItems];
     if (blockIdx.x < num_tiles) load_tile(blockIdx.x, rec);
     for (int b = tid; b < nbins; b += kIpBlock) s_cnt[b] = 0;
+    if (tid == 0) s_more = 0;
     __syncthreads();
     for (u32 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const u64 tile_base = static_cast<u64>(tile) * kIpTile;
@@ -1739,8 +1763,9 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
         const int b0 = 2 * tid, b1 = 2 * tid + 1;
         const u32 c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
         u32 g0 = 0, g1 = 0;   // claims are issued now, consumed after the exchange
-        if (c0) g0 = atomicAdd(claim + bin0 + b0, c0);
-        if (c1) g1 = atomicAdd(claim + bin0 + b1, c1);
+        const u32 r0 = (tile + b0) & (repl - 1u), r1 = (tile + b1) & (repl - 1u);   // repl is a power of two (1: one counter per bin)
+        if (c0) g0 = atomicAdd(claim + r0 * kIpMaxBins + bin0 + b0, c0);
+        if (c1) g1 = atomicAdd(claim + r1 * kIpMaxBins + bin0 + b1, c1);
         u32 inc = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1753,24 +1778,94 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
 #pragma unroll
         for (int w = 0; w < kIpBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
         const u32 excl = before + inc - (c0 + c1);
-        if (b0 < nbins) { s_ofs[b0] = excl; s_cnt[b0] = 0; }
-        if (b1 < nbins) { s_ofs[b1] = excl + c0; s_cnt[b1] = 0; }
+        if (b0 < nbins) { s_ofs[b0] = static_cast<std::remove_reference_t<decltype(s_ofs[0])>>(excl); s_cnt[b0] = 0; }
+        if (b1 < nbins) { s_ofs[b1] = static_cast<std::remove_reference_t<decltype(s_ofs[0])>>(excl + c0); s_cnt[b1] = 0; }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kIpItems; ++j) {
             const u32 li = static_cast<u32>(j) * kIpBlock + tid;
             if (li < valid) s_rec[s_ofs[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0] + slot[j]] = rec[j];
         }
-        if (c0) s_gdst[b0] = ((bin0 + b0) << shift) + g0 - excl;
-        if (c1) s_gdst[b1] = ((bin0 + b1) << shift) + g1 - (excl + c0);
+        // what is still to place of each of this thread's two runs after the pieces the scatter knows about
+        u32 left0 = 0, left1 = 0, at0 = 0, at1 = 0, rr0 = r0, rr1 = r1;
+        if constexpr (!REPL) {
+            if (c0) s_gdst[b0] = ((bin0 + b0) << shift) + g0 - excl;
+            if (c1) s_gdst[b1] = ((bin0 + b1) << shift) + g1 - (excl + c0);
+        } else {
+            // a run of c records starting at tile slot e: first piece from stretch r (claimed above: `old`), a second
+            // piece from the next stretch with room; more is left to the thread itself (left / at / rr)
+            auto place = [&](u32 b, u32 c, u32 e, u32 old, u32& r, u32& left, u32& at) {
+                const u32 bucket = static_cast<u32>(b) << shift;   // (first passes: bin0 = 0)
+                u32 lo, cap = stretch(b, r, &lo);
+                u32 take = old < cap ? (c < cap - old ? c : cap - old) : 0u;
+                s_gdst[b] = bucket + lo + old - e;                 // valid for slots [e, e + take)
+                u32 thr = e + take, end2 = e + take;
+                left = c - take;
+                at = e + take;
+                while (left && end2 == thr) {                      // second piece: the next stretch with room
+                    r = (r + 1u) & (repl - 1u);
+                    const u32 o2 = atomicAdd(claim + r * kIpMaxBins + b, left);
+                    cap = stretch(b, r, &lo);
+                    if (o2 < cap) {
+                        const u32 t2 = left < cap - o2 ? left : cap - o2;
+                        s_cnt[b] = bucket + lo + o2 - thr;         // (s_cnt is re-zeroed at the end of the tile)
+                        end2 = thr + t2;
+                        left -= t2;
+                        at = end2;
+                    }
+                    if (r == ((tile + b) & (repl - 1u))) break;    // (cannot happen: a bucket's stretches hold all its records)
+                }
+                s_thr[b] = thr | (end2 << 16);
+                if (left) s_more = 1;
+            };
+            if (c0) place(b0, c0, excl, g0, rr0, left0, at0);
+            if (c1) place(b1, c1, excl + c0, g1, rr1, left1, at1);
+        }
         __syncthreads();
+        if constexpr (!REPL) {
 #pragma unroll
-        for (int j = 0; j < kIpItems; ++j) {
-            const u32 p = static_cast<u32>(j) * kIpBlock + tid;
-            if (p < valid) {
-                const u64 r = s_rec[p];
-                out[s_gdst[(static_cast<u32>(r >> 32) >> shift) - bin0] + p] = r;
+            for (int j = 0; j < kIpItems; ++j) {
+                const u32 p = static_cast<u32>(j) * kIpBlock + tid;
+                if (p < valid) {
+                    const u64 r = s_rec[p];
+                    out[s_gdst[(static_cast<u32>(r >> 32) >> shift) - bin0] + p] = r;
+                }
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kIpItems; ++j) {
+                const u32 p = static_cast<u32>(j) * kIpBlock + tid;
+                if (p < valid) {
+                    const u64 r = s_rec[p];
+                    const u32 b = static_cast<u32>(r >> 32) >> shift;
+                    const u32 th = s_thr[b], thr = th & 0xffffu, end2 = th >> 16;
+                    if (p < thr) out[s_gdst[b] + p] = r;
+                    else if (p < end2) out[s_cnt[b] + p] = r;
+                }
+            }
+            if (s_more) {   // block-uniform: read after the barrier above, reset behind the one below
+                auto rest = [&](u32 b, u32 left, u32 at, u32 r) {
+                    const u32 bucket = static_cast<u32>(b) << shift;
+                    for (u32 k = 0; left && k < repl; ++k) {
+                        r = (r + 1u) & (repl - 1u);
+                        const u32 o = atomicAdd(claim + r * kIpMaxBins + b, left);
+                        u32 lo;
+                        const u32 cap = stretch(b, r, &lo);
+                        if (o < cap) {
+                            const u32 t = left < cap - o ? left : cap - o;
+                            for (u32 x = 0; x < t; ++x) out[static_cast<u64>(bucket) + lo + o + x] = s_rec[at + x];
+                            at += t;
+                            left -= t;
+                        }
+                    }
+                };
+                if (left0) rest(b0, left0, at0, rr0);
+                if (left1) rest(b1, left1, at1, rr1);
+            }
+            __syncthreads();                       // every reader of s_cnt (second pieces) and s_more is done
+            if (b0 < nbins) s_cnt[b0] = 0;
+            if (b1 < nbins) s_cnt[b1] = 0;
+            if (tid == 0) s_more = 0;
         }
 #pragma unroll
         for (int j = 0; j < kIpItems; ++j) rec[j] = nxt[j];
@@ -2547,7 +2642,7 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
 }
 
 // claim counters of both partition passes
-static size_t inverse_scratch_words(size_t n) { return kIpMaxBins + (n >> 13) + 64; }
+static size_t inverse_scratch_words(size_t n) { return 8 * 1024 + (n >> 13) + 64; }   // kIpRepl x kIpMaxBins first-pass counters + the second pass's
 
 // Ragged read sets are taken on when there are at most n / kRagMinAvg reads (mean length >= 15: below
 // that the 15-base key sorts nothing) -- which also bounds the tables below.
@@ -2589,6 +2684,14 @@ struct InversePlan {
     u32 buckets2;       // buckets after the second pass (= windows)
     unsigned tiles;
 };
+
+// Replicated first-pass claim counters (see inv_partition_persistent_kernel) from 2^28 records on: below that the
+// tiles are too few for their claims to queue up on one counter (no gain measured at 139 M records; 5.43 -> 3.98 ms for
+// the pass at 1 G).  "inverse_repl": -1 automatic, 0 never, 1 always.
+static_assert(kIpRepl == 8, "inverse_scratch_words() reserves 8 x 1024 first-pass counters");
+bool first_pass_repl(const reseq_cuda_ctx* ctx, size_t n) {
+    return ctx->opt_inverse_repl < 0 ? n >= (size_t{1} << 28) : ctx->opt_inverse_repl != 0;
+}
 
 InversePlan make_inverse_plan(size_t n, int mode) {
     InversePlan p{};
@@ -2641,12 +2744,14 @@ int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64*
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpMaxBins;
-    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpMaxBins + plan.buckets2 + 32), s));
+    u32* claim2 = scratch + kIpRepl * kIpMaxBins;
+    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpRepl * kIpMaxBins + plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_sa");
-    inv_partition_persistent_kernel<kIpSa><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a,
-                                                                    plan.tiles);
+    if (first_pass_repl(ctx, n))
+        inv_partition_persistent_kernel<kIpSa, true><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles);
+    else
+        inv_partition_persistent_kernel<kIpSa><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles);
     RSQ_LAUNCH_END(ctx);
     const u64* rec = rec_a;
     if (plan.win_bits == 0) {
@@ -2688,12 +2793,14 @@ int inverse_from_records(reseq_cuda_ctx* ctx, u64* rec_a, size_t len, u32* rank,
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpMaxBins;
-    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpMaxBins + plan.buckets2 + 32), s));
+    u32* claim2 = scratch + kIpRepl * kIpMaxBins;
+    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpRepl * kIpMaxBins + plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec0");
-    inv_partition_persistent_kernel<kIpRec0><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b,
-                                                                      plan.tiles);
+    if (first_pass_repl(ctx, len))
+        inv_partition_persistent_kernel<kIpRec0, true><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b, plan.tiles);
+    else
+        inv_partition_persistent_kernel<kIpRec0><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b, plan.tiles);
     RSQ_LAUNCH_END(ctx);
     const u64* rec = rec_b;
     if (plan.lo_bits > 0) {
@@ -2721,12 +2828,14 @@ int rank_update_device(reseq_cuda_ctx* ctx, const u32* sa, const u32* vals, size
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpMaxBins;
-    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpMaxBins + plan.buckets2 + 32), s));
+    u32* claim2 = scratch + kIpRepl * kIpMaxBins;
+    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpRepl * kIpMaxBins + plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_sa_val");
-    inv_partition_persistent_kernel<kIpSaVal><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a,
-                                                                       plan.tiles, vals);
+    if (first_pass_repl(ctx, n))
+        inv_partition_persistent_kernel<kIpSaVal, true><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles, vals);
+    else
+        inv_partition_persistent_kernel<kIpSaVal><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles, vals);
     RSQ_LAUNCH_END(ctx);
     const u64* rec = rec_a;
     if (plan.lo_bits > 0) {
