@@ -2693,7 +2693,7 @@ bool first_pass_repl(const reseq_cuda_ctx* ctx, size_t n) {
     return ctx->opt_inverse_repl < 0 ? n >= (size_t{1} << 28) : ctx->opt_inverse_repl != 0;
 }
 
-InversePlan make_inverse_plan(size_t n, int mode) {
+InversePlan make_inverse_plan(size_t n, int mode, int top_bits = -1) {
     InversePlan p{};
     p.partitioned = n >= (size_t{1} << 22);
     if (!p.partitioned) return p;
@@ -2710,6 +2710,7 @@ InversePlan make_inverse_plan(size_t n, int mode) {
     p.win_bits = 13;
     int rest = nb - p.win_bits;                               // bits the passes must consume
     int top = rest < 8 ? rest : 8;
+    if (top_bits > 0 && top_bits <= rest && top_bits <= 10 && rest - top_bits <= 9) top = top_bits;   // tuning knob ("inverse_lo_bits" carries it)
     int lo = rest - top;
     if (lo > 9) { p.win_bits = 14; --lo; }                    // n >= 2^31
     if (lo > 9) { top += lo - 9; lo = 9; }                    // n > 2^31: wider first pass (<= 10 bits)
@@ -2735,7 +2736,7 @@ int window_scatter_device(reseq_cuda_ctx* ctx, const u64* rec, size_t n, int win
 // inverse_scratch_words(n) claim counters).
 int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64* rec_a, u64* rec_b, u32* scratch) {
     cudaStream_t s = ctx->stream;
-    const InversePlan plan = make_inverse_plan(n, ctx->opt_inverse_mode);
+    const InversePlan plan = make_inverse_plan(n, ctx->opt_inverse_mode, ctx->opt_inverse_lo_bits);
     if (!plan.partitioned) {  // the whole rank array is L2-resident: scatter directly
         RSQ_LAUNCH_BEGIN(ctx, "inverse_kernel");
         inverse_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa, n, rank);
@@ -2784,7 +2785,7 @@ __global__ void inverse_records_kernel(const u64* __restrict__ rec, u64 m, u32* 
 // scratch of the same size), then scattered window by window.
 int inverse_from_records(reseq_cuda_ctx* ctx, u64* rec_a, size_t len, u32* rank, u64* rec_b, u32* scratch) {
     cudaStream_t s = ctx->stream;
-    const InversePlan plan = make_inverse_plan(len, 0);
+    const InversePlan plan = make_inverse_plan(len, 0, ctx->opt_inverse_lo_bits);
     if (!plan.partitioned) {
         RSQ_LAUNCH_BEGIN(ctx, "inverse_records_kernel");
         inverse_records_kernel<<<grid_for(ctx, len, 256, 4, 16), 256, 0, s>>>(rec_a, len, rank);
@@ -2819,7 +2820,7 @@ int inverse_from_records(reseq_cuda_ctx* ctx, u64* rec_a, size_t len, u32* rank,
 int rank_update_device(reseq_cuda_ctx* ctx, const u32* sa, const u32* vals, size_t n, u32* rank, u64* rec_a, u64* rec_b,
                        u32* scratch) {
     cudaStream_t s = ctx->stream;
-    const InversePlan plan = make_inverse_plan(n, 0);
+    const InversePlan plan = make_inverse_plan(n, 0, ctx->opt_inverse_lo_bits);
     if (!plan.partitioned) {
         RSQ_LAUNCH_BEGIN(ctx, "scatter_vals_kernel");
         scatter_vals_kernel<<<grid_for(ctx, n, 256, 4, 16), 256, 0, s>>>(sa, vals, n, rank);
