@@ -62,8 +62,8 @@ struct reseq_cuda_ctx {
     cudaStream_t stream = nullptr;
     int sm_count = rsq::kSmCount;
     uint64_t launches = 0;
-    int opt_inverse_lo_bits = -1;  // extra partition bits before the inverse scatter (-1 = auto)
-    int opt_inverse_repl = -1;     // replicated claim counters in the first inverse partition pass (-1 = from 2^28 records on)
+    int opt_inverse_lo_bits = -1;  // bits of the first inverse partition pass (-1 = auto: at most 7; tuning)
+    int opt_inverse_repl = -1;     // replicated claim counters in the first inverse partition pass (-1 = when that pass has more than 128 bins)
     int opt_inverse_mode = 0;      // 0: two partition passes + shared-memory window; 1: one pass + L2-window scatter
     int opt_shortcut = 1;      // sentinel-distance shortcut in the refine kernel (tuning / tests)
     int opt_lookahead = 8;     // onesweep look-back descriptors in flight per digit (1..8)
@@ -72,7 +72,7 @@ struct reseq_cuda_ctx {
     int opt_sort_tma = 0;      // onesweep: full tiles loaded by one TMA bulk copy (measured 4 % slower than per-thread loads: off)
     int opt_sort_prmt = 1;     // onesweep: byte-aligned 8-bit digits of the upper key word extracted by one PRMT (0: shift + mask)
     int opt_accept_quads = 1;  // uniform route, accept pass: a thread owns four consecutive records (0: pairs)
-    int opt_owner_bins = 1024;  // rank exchange: owner x sub-range bins of the sender's partition pass (tuning)
+    int opt_owner_bins = 128;   // rank exchange: owner x sub-range bins of the sender's partition pass (378 M positions, 8 owners: 1024 bins 2.58 ms, 256 2.33, 128 1.88, 32 1.80)
     int opt_lookback_pack = 1; // two digits per look-back descriptor word when n < 2^30 (0: always one)
     int opt_uniform = 1;       // transposed-record path for uniform read sets (0: general paths only)
     int opt_ragged = 1;        // ragged read sets (mixed read lengths <= 254) on the uniform route's flow (0: general records)

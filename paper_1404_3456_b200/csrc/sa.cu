@@ -1703,12 +1703,17 @@ constexpr int kIpMaxBins = 1024;
 // finds room).  Almost every run of a tile lands in one stretch; a second piece is carried through the scatter as a
 // threshold, and anything beyond two pieces (the last tiles of a bucket) is stored by the bin's own thread.
 constexpr int kIpRepl = 8;
+constexpr int kIpClaimStride = 32;   // words between first-pass claim counters: one per 128-byte line
 template <int MODE, bool REPL = false>
 __global__ void __launch_bounds__(kIpBlock, 2)
 inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shift, int prev_shift, int nbins,
                                 u32* __restrict__ claim, u64* __restrict__ out, u32 num_tiles,
                                 const u32* __restrict__ vals = nullptr) {
     static_assert(!REPL || MODE != kIpRec, "replicated claims are for first passes (bin0 = 0)");
+    // First passes: every tile claims from the same `nbins` counters; packed, they sit in a handful of cache lines -- a
+    // handful of L2 slices -- whose atomic units then bound the pass (~8 G claims/s).  One counter per 128-byte line
+    // spreads them over the slices.  (Second passes claim from bucket x bin counters: already spread.)
+    constexpr u32 CS = MODE == kIpRec ? 1u : static_cast<u32>(kIpClaimStride);
     constexpr u32 repl_bits = REPL ? 3 : 0;
     constexpr u32 repl = 1u << repl_bits;     // claim counters per bin
     static_assert(repl == 1 || repl == static_cast<u32>(kIpRepl), "kIpRepl counters per bin");
@@ -1764,8 +1769,8 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
         const u32 c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
         u32 g0 = 0, g1 = 0;   // claims are issued now, consumed after the exchange
         const u32 r0 = (tile + b0) & (repl - 1u), r1 = (tile + b1) & (repl - 1u);   // repl is a power of two (1: one counter per bin)
-        if (c0) g0 = atomicAdd(claim + r0 * kIpMaxBins + bin0 + b0, c0);
-        if (c1) g1 = atomicAdd(claim + r1 * kIpMaxBins + bin0 + b1, c1);
+        if (c0) g0 = atomicAdd(claim + (r0 * kIpMaxBins + bin0 + b0) * CS, c0);
+        if (c1) g1 = atomicAdd(claim + (r1 * kIpMaxBins + bin0 + b1) * CS, c1);
         u32 inc = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1804,7 +1809,7 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
                 at = e + take;
                 while (left && end2 == thr) {                      // second piece: the next stretch with room
                     r = (r + 1u) & (repl - 1u);
-                    const u32 o2 = atomicAdd(claim + r * kIpMaxBins + b, left);
+                    const u32 o2 = atomicAdd(claim + (r * kIpMaxBins + b) * CS, left);
                     cap = stretch(b, r, &lo);
                     if (o2 < cap) {
                         const u32 t2 = left < cap - o2 ? left : cap - o2;
@@ -1848,7 +1853,7 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
                     const u32 bucket = static_cast<u32>(b) << shift;
                     for (u32 k = 0; left && k < repl; ++k) {
                         r = (r + 1u) & (repl - 1u);
-                        const u32 o = atomicAdd(claim + r * kIpMaxBins + b, left);
+                        const u32 o = atomicAdd(claim + (r * kIpMaxBins + b) * CS, left);
                         u32 lo;
                         const u32 cap = stretch(b, r, &lo);
                         if (o < cap) {
@@ -2642,7 +2647,7 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
 }
 
 // claim counters of both partition passes
-static size_t inverse_scratch_words(size_t n) { return 8 * 1024 + (n >> 13) + 64; }   // kIpRepl x kIpMaxBins first-pass counters + the second pass's
+static size_t inverse_scratch_words(size_t n) { return 8 * 1024 * 32 + (n >> 13) + 64; }   // kIpRepl x kIpMaxBins first-pass counters, one per 128-byte line, + the second pass's
 
 // Ragged read sets are taken on when there are at most n / kRagMinAvg reads (mean length >= 15: below
 // that the 15-base key sorts nothing) -- which also bounds the tables below.
@@ -2685,12 +2690,13 @@ struct InversePlan {
     unsigned tiles;
 };
 
-// Replicated first-pass claim counters (see inv_partition_persistent_kernel) from 2^28 records on: below that the
-// tiles are too few for their claims to queue up on one counter (no gain measured at 139 M records; 5.43 -> 3.98 ms for
-// the pass at 1 G).  "inverse_repl": -1 automatic, 0 never, 1 always.
-static_assert(kIpRepl == 8, "inverse_scratch_words() reserves 8 x 1024 first-pass counters");
-bool first_pass_repl(const reseq_cuda_ctx* ctx, size_t n) {
-    return ctx->opt_inverse_repl < 0 ? n >= (size_t{1} << 28) : ctx->opt_inverse_repl != 0;
+// Replicated first-pass claim counters (see inv_partition_persistent_kernel) where the first pass still has more than
+// 128 bins (n > 2^31: 360 bins at 3 G records, 18.3 -> 13.1 ms); with the <= 128 bins every smaller array gets from
+// make_inverse_plan the single counter per bin is faster (1 G records, 121 bins: 3.27 ms against 4.05 replicated).
+// "inverse_repl": -1 automatic, 0 never, 1 always.
+static_assert(kIpRepl == 8 && kIpClaimStride == 32, "inverse_scratch_words() reserves 8 x 1024 first-pass counters of 32 words");
+bool first_pass_repl(const reseq_cuda_ctx* ctx, int bins1) {
+    return ctx->opt_inverse_repl < 0 ? bins1 > 128 : ctx->opt_inverse_repl != 0;
 }
 
 InversePlan make_inverse_plan(size_t n, int mode, int top_bits = -1) {
@@ -2707,13 +2713,21 @@ InversePlan make_inverse_plan(size_t n, int mode, int top_bits = -1) {
         p.tiles = static_cast<unsigned>((n + kIpTile - 1) / kIpTile);
         return p;
     }
+    // The first pass gets at most 7 bits: its tiles all claim from the same `bins1` counters, and with 133 - 240 bins
+    // it ran at 0.31 - 0.47 of the HBM peak against 0.57 with 67 - 97 (config 3: 0.60 -> 0.33 ms); the bits go to the
+    // second pass, whose claims spread over bucket x bin counters (<= 1024 bins), and to a 2^14-entry window.
     p.win_bits = 13;
     int rest = nb - p.win_bits;                               // bits the passes must consume
-    int top = rest < 8 ? rest : 8;
-    if (top_bits > 0 && top_bits <= rest && top_bits <= 10 && rest - top_bits <= 9) top = top_bits;   // tuning knob ("inverse_lo_bits" carries it)
+    const int top_max = top_bits > 0 && top_bits <= 10 ? top_bits : 7;   // tuning knob ("inverse_lo_bits" carries it)
+    int top = rest < top_max ? rest : top_max;
     int lo = rest - top;
-    if (lo > 9) { p.win_bits = 14; --lo; }                    // n >= 2^31
-    if (lo > 9) { top += lo - 9; lo = 9; }                    // n > 2^31: wider first pass (<= 10 bits)
+    if (lo > 9) {                                             // n >= 2^30: 64 KB windows
+        p.win_bits = 14;
+        rest = nb - p.win_bits;
+        top = rest < top_max ? rest : top_max;
+        lo = rest - top;
+    }
+    if (lo > 9) { top += lo - 9; lo = 9; }                    // n > 2^31: wider first pass (<= 9 bits; replicated counters)
     p.lo_bits = lo;
     p.shift1 = p.win_bits + lo;
     p.bins1 = static_cast<int>(((n - 1) >> p.shift1) + 1);
@@ -2745,11 +2759,12 @@ int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64*
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpRepl * kIpMaxBins;
-    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpRepl * kIpMaxBins + plan.buckets2 + 32), s));
+    u32* claim2 = scratch + kIpRepl * kIpMaxBins * kIpClaimStride;
+    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * ((first_pass_repl(ctx, plan.bins1) ? (kIpRepl - 1) * kIpMaxBins : 0) + plan.bins1) * kIpClaimStride, s));
+    RSQ_CUDA(cudaMemsetAsync(claim2, 0, sizeof(u32) * (plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_sa");
-    if (first_pass_repl(ctx, n))
+    if (first_pass_repl(ctx, plan.bins1))
         inv_partition_persistent_kernel<kIpSa, true><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles);
     else
         inv_partition_persistent_kernel<kIpSa><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles);
@@ -2785,7 +2800,10 @@ __global__ void inverse_records_kernel(const u64* __restrict__ rec, u64 m, u32* 
 // scratch of the same size), then scattered window by window.
 int inverse_from_records(reseq_cuda_ctx* ctx, u64* rec_a, size_t len, u32* rank, u64* rec_b, u32* scratch) {
     cudaStream_t s = ctx->stream;
-    const InversePlan plan = make_inverse_plan(len, 0, ctx->opt_inverse_lo_bits);
+    // (records arriving from the exchange: measured at a 378 M-position slice, 8 first-pass bits -- 181 bins, then 512 --
+    //  cost 1.31 + 1.34 ms, 7 bits -- 91 bins, then 1024 -- 1.30 + 1.53: this input does not show the first-pass
+    //  slowdown the suffix-array order does, so the second pass keeps the fewer bins)
+    const InversePlan plan = make_inverse_plan(len, 0, ctx->opt_inverse_lo_bits > 0 ? ctx->opt_inverse_lo_bits : 8);
     if (!plan.partitioned) {
         RSQ_LAUNCH_BEGIN(ctx, "inverse_records_kernel");
         inverse_records_kernel<<<grid_for(ctx, len, 256, 4, 16), 256, 0, s>>>(rec_a, len, rank);
@@ -2794,11 +2812,12 @@ int inverse_from_records(reseq_cuda_ctx* ctx, u64* rec_a, size_t len, u32* rank,
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpRepl * kIpMaxBins;
-    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpRepl * kIpMaxBins + plan.buckets2 + 32), s));
+    u32* claim2 = scratch + kIpRepl * kIpMaxBins * kIpClaimStride;
+    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * ((first_pass_repl(ctx, plan.bins1) ? (kIpRepl - 1) * kIpMaxBins : 0) + plan.bins1) * kIpClaimStride, s));
+    RSQ_CUDA(cudaMemsetAsync(claim2, 0, sizeof(u32) * (plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec0");
-    if (first_pass_repl(ctx, len))
+    if (first_pass_repl(ctx, plan.bins1))
         inv_partition_persistent_kernel<kIpRec0, true><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b, plan.tiles);
     else
         inv_partition_persistent_kernel<kIpRec0><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b, plan.tiles);
@@ -2829,11 +2848,12 @@ int rank_update_device(reseq_cuda_ctx* ctx, const u32* sa, const u32* vals, size
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpRepl * kIpMaxBins;
-    RSQ_CUDA(cudaMemsetAsync(scratch, 0, sizeof(u32) * (kIpRepl * kIpMaxBins + plan.buckets2 + 32), s));
+    u32* claim2 = scratch + kIpRepl * kIpMaxBins * kIpClaimStride;
+    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * ((first_pass_repl(ctx, plan.bins1) ? (kIpRepl - 1) * kIpMaxBins : 0) + plan.bins1) * kIpClaimStride, s));
+    RSQ_CUDA(cudaMemsetAsync(claim2, 0, sizeof(u32) * (plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_sa_val");
-    if (first_pass_repl(ctx, n))
+    if (first_pass_repl(ctx, plan.bins1))
         inv_partition_persistent_kernel<kIpSaVal, true><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles, vals);
     else
         inv_partition_persistent_kernel<kIpSaVal><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles, vals);
