@@ -102,8 +102,6 @@ size_t reseq_cuda_ctx_workspace_bytes(const reseq_cuda_ctx* ctx);
  *                     build whose text, outputs, workspace, stream and options are those of the previous
  *                     build is ONE cudaGraphLaunch; needs a stream of the caller's or the context's own --
  *                     capture is not allowed on the legacy default stream -- and no per-kernel profiling)
- *   "inverse_repl"    replicated claim counters in the first partition pass of the inverse: -1 (default) when
- *                     that pass has more than 128 bins (n > 2^31), 0 never, 1 always
  *   "inverse_mode"    how rank = sa^-1 is computed above 2^22 suffixes: 0 two partition passes + a
  *                     shared-memory window scatter, 1 one partition pass + an L2-window scatter */
 int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long value);

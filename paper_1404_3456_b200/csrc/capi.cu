@@ -172,7 +172,6 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     if (const char* e = std::getenv("RESEQ_SORT_CFG")) ctx->opt_sort_cfg = std::atoi(e);      // tuning only
     if (const char* e = std::getenv("RESEQ_INVERSE_LO_BITS")) ctx->opt_inverse_lo_bits = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_INVERSE_MODE")) ctx->opt_inverse_mode = std::atoi(e);
-    if (const char* e = std::getenv("RESEQ_INVERSE_REPL")) ctx->opt_inverse_repl = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_LOOKBACK_PACK")) ctx->opt_lookback_pack = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SORT_TMA")) ctx->opt_sort_tma = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_SORT_PRMT")) ctx->opt_sort_prmt = std::atoi(e);
@@ -264,11 +263,6 @@ int reseq_cuda_ctx_set_option(reseq_cuda_ctx* ctx, const char* name, long long v
     }
     if (std::strcmp(name, "sa_speculate") == 0) {
         ctx->opt_speculate = value != 0;
-        return RESEQ_OK;
-    }
-    if (std::strcmp(name, "inverse_repl") == 0) {
-        if (value < -1 || value > 1) return fail(RESEQ_INVALID_ARGUMENT, "inverse_repl must be -1, 0 or 1");
-        ctx->opt_inverse_repl = static_cast<int>(value);
         return RESEQ_OK;
     }
     if (std::strcmp(name, "inverse_mode") == 0) {

@@ -63,7 +63,6 @@ struct reseq_cuda_ctx {
     int sm_count = rsq::kSmCount;
     uint64_t launches = 0;
     int opt_inverse_lo_bits = -1;  // bits of the first inverse partition pass (-1 = auto: at most 7; tuning)
-    int opt_inverse_repl = -1;     // replicated claim counters in the first inverse partition pass (-1 = when that pass has more than 128 bins)
     int opt_inverse_mode = 0;      // 0: two partition passes + shared-memory window; 1: one pass + L2-window scatter
     int opt_shortcut = 1;      // sentinel-distance shortcut in the refine kernel (tuning / tests)
     int opt_lookahead = 8;     // onesweep look-back descriptors in flight per digit (1..8)

@@ -1694,36 +1694,23 @@ constexpr int kIpMaxBins = 1024;
 // scanned, exchanged and stored, and the claims before the exchange, so the HBM latency of the
 // load and the L2 latency of the atomics are covered by the tile's own work (one tile per CTA:
 // 0.68 ms per pass at n = 139 M, 55 % of stalls on those two scoreboards; this form: 0.48 ms).
-// REPLICATED CLAIMS (repl = kIpRepl, first passes of large arrays).  In a first pass every tile claims from the SAME
-// `nbins` counters: at 1 G records that is 246 000 tiles x 120 bins on 120 addresses, and the pass ran at 0.33 of the
-// HBM peak against 0.60 for the second pass over the same records, whose claims spread over bucket x bin counters.  A
-// bucket is therefore cut into `repl` stretches of known size, each with its own counter; a tile starts at stretch
-// (tile + bin) mod repl and takes [old, old + count) from it -- or, where the stretch runs out, what is left of it and
-// the rest from the next ones (a bucket's stretches hold exactly its records, so one round over them always
-// finds room).  Almost every run of a tile lands in one stretch; a second piece is carried through the scatter as a
-// threshold, and anything beyond two pieces (the last tiles of a bucket) is stored by the bin's own thread.
-constexpr int kIpRepl = 8;
 constexpr int kIpClaimStride = 32;   // words between first-pass claim counters: one per 128-byte line
-template <int MODE, bool REPL = false>
+template <int MODE>
 __global__ void __launch_bounds__(kIpBlock, 2)
 inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shift, int prev_shift, int nbins,
                                 u32* __restrict__ claim, u64* __restrict__ out, u32 num_tiles,
                                 const u32* __restrict__ vals = nullptr) {
-    static_assert(!REPL || MODE != kIpRec, "replicated claims are for first passes (bin0 = 0)");
     // First passes: every tile claims from the same `nbins` counters; packed, they sit in a handful of cache lines -- a
-    // handful of L2 slices -- whose atomic units then bound the pass (~8 G claims/s).  One counter per 128-byte line
-    // spreads them over the slices.  (Second passes claim from bucket x bin counters: already spread.)
+    // handful of L2 slices -- whose atomic units then bound the pass (~8 G claims/s: 0.31 of the HBM peak with 193 - 360
+    // bins).  One counter per 128-byte line spreads them over the slices.  (Second passes claim from bucket x bin
+    // counters: already spread.)  Measured and dropped in favour of this: counters replicated eight times per bin with
+    // sized stretches of each bucket (13.1 ms against 12.0 at 3 G records; profiles/r2_negative_results.md).
     constexpr u32 CS = MODE == kIpRec ? 1u : static_cast<u32>(kIpClaimStride);
-    constexpr u32 repl_bits = REPL ? 3 : 0;
-    constexpr u32 repl = 1u << repl_bits;     // claim counters per bin
-    static_assert(repl == 1 || repl == static_cast<u32>(kIpRepl), "kIpRepl counters per bin");
     __shared__ __align__(16) u64 s_rec[kIpTile];
-    __shared__ u32 s_cnt[kIpMaxBins];     // counts of the tile; (replicated claims) destination of a run's second piece
-    __shared__ std::conditional_t<REPL, unsigned short, u32> s_ofs[kIpMaxBins];   // first tile slot of the bin (16 bits where the static 48 KB are tight)
+    __shared__ u32 s_cnt[kIpMaxBins];
+    __shared__ u32 s_ofs[kIpMaxBins];
     __shared__ u32 s_gdst[kIpMaxBins];
-    __shared__ u32 s_thr[REPL ? kIpMaxBins : 1];   // (replicated claims) tile slot where a run's second piece starts | end of it << 16
     __shared__ u32 s_warp[kIpBlock / 32];
-    __shared__ u32 s_more;                // (replicated claims) some run of this tile needs a third piece
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     auto load_tile = [&](u32 tile, u64 (&r)[kIpItems]) {
@@ -1739,18 +1726,9 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
                 r[j] = i < n ? static_cast<const u64*>(in_raw)[i] : 0;
         }
     };
-    // stretch r of bucket b (replicated claims; first passes: bucket b = positions [b << shift, (b + 1) << shift) of n)
-    auto stretch = [&](u32 b, u32 r, u32* lo) -> u32 {
-        const u64 base = static_cast<u64>(b) << shift;
-        const u32 sz = static_cast<u32>(n - base < (1ull << shift) ? n - base : (1ull << shift));
-        const u32 l = static_cast<u32>((static_cast<u64>(sz) * r) >> repl_bits), h = static_cast<u32>((static_cast<u64>(sz) * (r + 1)) >> repl_bits);
-        *lo = l;
-        return h - l;
-    };
     u64 rec[kIpItems], nxt[kIpItems];
     if (blockIdx.x < num_tiles) load_tile(blockIdx.x, rec);
     for (int b = tid; b < nbins; b += kIpBlock) s_cnt[b] = 0;
-    if (tid == 0) s_more = 0;
     __syncthreads();
     for (u32 tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const u64 tile_base = static_cast<u64>(tile) * kIpTile;
@@ -1768,9 +1746,8 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
         const int b0 = 2 * tid, b1 = 2 * tid + 1;
         const u32 c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
         u32 g0 = 0, g1 = 0;   // claims are issued now, consumed after the exchange
-        const u32 r0 = (tile + b0) & (repl - 1u), r1 = (tile + b1) & (repl - 1u);   // repl is a power of two (1: one counter per bin)
-        if (c0) g0 = atomicAdd(claim + (r0 * kIpMaxBins + bin0 + b0) * CS, c0);
-        if (c1) g1 = atomicAdd(claim + (r1 * kIpMaxBins + bin0 + b1) * CS, c1);
+        if (c0) g0 = atomicAdd(claim + (bin0 + b0) * CS, c0);
+        if (c1) g1 = atomicAdd(claim + (bin0 + b1) * CS, c1);
         u32 inc = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1783,94 +1760,24 @@ inv_partition_persistent_kernel(const void* __restrict__ in_raw, u64 n, int shif
 #pragma unroll
         for (int w = 0; w < kIpBlock / 32; ++w) before += w < (tid >> 5) ? s_warp[w] : 0u;
         const u32 excl = before + inc - (c0 + c1);
-        if (b0 < nbins) { s_ofs[b0] = static_cast<std::remove_reference_t<decltype(s_ofs[0])>>(excl); s_cnt[b0] = 0; }
-        if (b1 < nbins) { s_ofs[b1] = static_cast<std::remove_reference_t<decltype(s_ofs[0])>>(excl + c0); s_cnt[b1] = 0; }
+        if (b0 < nbins) { s_ofs[b0] = excl; s_cnt[b0] = 0; }
+        if (b1 < nbins) { s_ofs[b1] = excl + c0; s_cnt[b1] = 0; }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kIpItems; ++j) {
             const u32 li = static_cast<u32>(j) * kIpBlock + tid;
             if (li < valid) s_rec[s_ofs[(static_cast<u32>(rec[j] >> 32) >> shift) - bin0] + slot[j]] = rec[j];
         }
-        // what is still to place of each of this thread's two runs after the pieces the scatter knows about
-        u32 left0 = 0, left1 = 0, at0 = 0, at1 = 0, rr0 = r0, rr1 = r1;
-        if constexpr (!REPL) {
-            if (c0) s_gdst[b0] = ((bin0 + b0) << shift) + g0 - excl;
-            if (c1) s_gdst[b1] = ((bin0 + b1) << shift) + g1 - (excl + c0);
-        } else {
-            // a run of c records starting at tile slot e: first piece from stretch r (claimed above: `old`), a second
-            // piece from the next stretch with room; more is left to the thread itself (left / at / rr)
-            auto place = [&](u32 b, u32 c, u32 e, u32 old, u32& r, u32& left, u32& at) {
-                const u32 bucket = static_cast<u32>(b) << shift;   // (first passes: bin0 = 0)
-                u32 lo, cap = stretch(b, r, &lo);
-                u32 take = old < cap ? (c < cap - old ? c : cap - old) : 0u;
-                s_gdst[b] = bucket + lo + old - e;                 // valid for slots [e, e + take)
-                u32 thr = e + take, end2 = e + take;
-                left = c - take;
-                at = e + take;
-                while (left && end2 == thr) {                      // second piece: the next stretch with room
-                    r = (r + 1u) & (repl - 1u);
-                    const u32 o2 = atomicAdd(claim + (r * kIpMaxBins + b) * CS, left);
-                    cap = stretch(b, r, &lo);
-                    if (o2 < cap) {
-                        const u32 t2 = left < cap - o2 ? left : cap - o2;
-                        s_cnt[b] = bucket + lo + o2 - thr;         // (s_cnt is re-zeroed at the end of the tile)
-                        end2 = thr + t2;
-                        left -= t2;
-                        at = end2;
-                    }
-                    if (r == ((tile + b) & (repl - 1u))) break;    // (cannot happen: a bucket's stretches hold all its records)
-                }
-                s_thr[b] = thr | (end2 << 16);
-                if (left) s_more = 1;
-            };
-            if (c0) place(b0, c0, excl, g0, rr0, left0, at0);
-            if (c1) place(b1, c1, excl + c0, g1, rr1, left1, at1);
-        }
+        if (c0) s_gdst[b0] = ((bin0 + b0) << shift) + g0 - excl;
+        if (c1) s_gdst[b1] = ((bin0 + b1) << shift) + g1 - (excl + c0);
         __syncthreads();
-        if constexpr (!REPL) {
 #pragma unroll
-            for (int j = 0; j < kIpItems; ++j) {
-                const u32 p = static_cast<u32>(j) * kIpBlock + tid;
-                if (p < valid) {
-                    const u64 r = s_rec[p];
-                    out[s_gdst[(static_cast<u32>(r >> 32) >> shift) - bin0] + p] = r;
-                }
+        for (int j = 0; j < kIpItems; ++j) {
+            const u32 p = static_cast<u32>(j) * kIpBlock + tid;
+            if (p < valid) {
+                const u64 r = s_rec[p];
+                out[s_gdst[(static_cast<u32>(r >> 32) >> shift) - bin0] + p] = r;
             }
-        } else {
-#pragma unroll
-            for (int j = 0; j < kIpItems; ++j) {
-                const u32 p = static_cast<u32>(j) * kIpBlock + tid;
-                if (p < valid) {
-                    const u64 r = s_rec[p];
-                    const u32 b = static_cast<u32>(r >> 32) >> shift;
-                    const u32 th = s_thr[b], thr = th & 0xffffu, end2 = th >> 16;
-                    if (p < thr) out[s_gdst[b] + p] = r;
-                    else if (p < end2) out[s_cnt[b] + p] = r;
-                }
-            }
-            if (s_more) {   // block-uniform: read after the barrier above, reset behind the one below
-                auto rest = [&](u32 b, u32 left, u32 at, u32 r) {
-                    const u32 bucket = static_cast<u32>(b) << shift;
-                    for (u32 k = 0; left && k < repl; ++k) {
-                        r = (r + 1u) & (repl - 1u);
-                        const u32 o = atomicAdd(claim + (r * kIpMaxBins + b) * CS, left);
-                        u32 lo;
-                        const u32 cap = stretch(b, r, &lo);
-                        if (o < cap) {
-                            const u32 t = left < cap - o ? left : cap - o;
-                            for (u32 x = 0; x < t; ++x) out[static_cast<u64>(bucket) + lo + o + x] = s_rec[at + x];
-                            at += t;
-                            left -= t;
-                        }
-                    }
-                };
-                if (left0) rest(b0, left0, at0, rr0);
-                if (left1) rest(b1, left1, at1, rr1);
-            }
-            __syncthreads();                       // every reader of s_cnt (second pieces) and s_more is done
-            if (b0 < nbins) s_cnt[b0] = 0;
-            if (b1 < nbins) s_cnt[b1] = 0;
-            if (tid == 0) s_more = 0;
         }
 #pragma unroll
         for (int j = 0; j < kIpItems; ++j) rec[j] = nxt[j];
@@ -2520,6 +2427,26 @@ owner_count_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u32* __rest
 // One lean partition pass (see inv_partition_persistent_kernel): a record takes its slot in the tile's bin
 // from one shared-memory atomicAdd, a bin claims its stretch with one global atomicAdd on a counter that
 // starts at the bin's base, the tile leaves through shared memory as one contiguous run per bin.
+// Exclusive bases of the owner x sub-range bins, one claim counter per 128-byte line (all tiles claim from these
+// few counters: packed they shared four cache lines).  One block; bins <= 1024.
+__global__ void __launch_bounds__(kOwnMaxBins)
+owner_bases_kernel(const u32* __restrict__ counts, int bins, u32* __restrict__ claim) {
+    __shared__ u32 s_warp[kOwnMaxBins / 32];
+    const int b = threadIdx.x;
+    const u32 c = b < bins ? counts[b] : 0u;
+    u32 inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (static_cast<int>(lane_id()) >= o) inc += t;
+    }
+    if (lane_id() == 31) s_warp[b >> 5] = inc;
+    __syncthreads();
+    u32 before = 0;
+    for (int w = 0; w < (b >> 5); ++w) before += s_warp[w];
+    if (b < bins) claim[static_cast<size_t>(b) * kIpClaimStride] = before + inc - c;
+}
+
 __global__ void __launch_bounds__(kOwnBlock, 2)
 owner_partition_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u64 offset, u32* __restrict__ claim,
                        u64* __restrict__ out, u32 num_tiles) {
@@ -2574,8 +2501,8 @@ owner_partition_kernel(const u32* __restrict__ sa, u64 m, OwnerTable tb, u64 off
         const int b0 = 2 * tid, b1 = 2 * tid + 1;
         const u32 c0 = b0 < bins ? s_cnt[b0] : 0u, c1 = b1 < bins ? s_cnt[b1] : 0u;
         u32 g0 = 0, g1 = 0;
-        if (c0) g0 = atomicAdd(claim + b0, c0);
-        if (c1) g1 = atomicAdd(claim + b1, c1);
+        if (c0) g0 = atomicAdd(claim + b0 * kIpClaimStride, c0);
+        if (c1) g1 = atomicAdd(claim + b1 * kIpClaimStride, c1);
         u32 inc = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -2647,7 +2574,7 @@ int pack_dna_device(reseq_cuda_ctx* ctx, const u8* d_text, size_t n, u64* packed
 }
 
 // claim counters of both partition passes
-static size_t inverse_scratch_words(size_t n) { return 8 * 1024 * 32 + (n >> 13) + 64; }   // kIpRepl x kIpMaxBins first-pass counters, one per 128-byte line, + the second pass's
+static size_t inverse_scratch_words(size_t n) { return 1024 * 32 + (n >> 13) + 64; }   // kIpMaxBins first-pass counters, one per 128-byte line, + the second pass's
 
 // Ragged read sets are taken on when there are at most n / kRagMinAvg reads (mean length >= 15: below
 // that the 15-base key sorts nothing) -- which also bounds the tables below.
@@ -2690,15 +2617,6 @@ struct InversePlan {
     unsigned tiles;
 };
 
-// Replicated first-pass claim counters (see inv_partition_persistent_kernel) where the first pass still has more than
-// 128 bins (n > 2^31: 360 bins at 3 G records, 18.3 -> 13.1 ms); with the <= 128 bins every smaller array gets from
-// make_inverse_plan the single counter per bin is faster (1 G records, 121 bins: 3.27 ms against 4.05 replicated).
-// "inverse_repl": -1 automatic, 0 never, 1 always.
-static_assert(kIpRepl == 8 && kIpClaimStride == 32, "inverse_scratch_words() reserves 8 x 1024 first-pass counters of 32 words");
-bool first_pass_repl(const reseq_cuda_ctx* ctx, int bins1) {
-    return ctx->opt_inverse_repl < 0 ? bins1 > 128 : ctx->opt_inverse_repl != 0;
-}
-
 InversePlan make_inverse_plan(size_t n, int mode, int top_bits = -1) {
     InversePlan p{};
     p.partitioned = n >= (size_t{1} << 22);
@@ -2727,7 +2645,7 @@ InversePlan make_inverse_plan(size_t n, int mode, int top_bits = -1) {
         top = rest < top_max ? rest : top_max;
         lo = rest - top;
     }
-    if (lo > 9) { top += lo - 9; lo = 9; }                    // n > 2^31: wider first pass (<= 9 bits; replicated counters)
+    if (lo > 9) { top += lo - 9; lo = 9; }                    // n > 2^31: wider first pass (<= 9 bits)
     p.lo_bits = lo;
     p.shift1 = p.win_bits + lo;
     p.bins1 = static_cast<int>(((n - 1) >> p.shift1) + 1);
@@ -2759,15 +2677,12 @@ int inverse_device(reseq_cuda_ctx* ctx, const u32* sa, size_t n, u32* rank, u64*
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpRepl * kIpMaxBins * kIpClaimStride;
-    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * ((first_pass_repl(ctx, plan.bins1) ? (kIpRepl - 1) * kIpMaxBins : 0) + plan.bins1) * kIpClaimStride, s));
+    u32* claim2 = scratch + kIpMaxBins * kIpClaimStride;
+    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * plan.bins1 * kIpClaimStride, s));
     RSQ_CUDA(cudaMemsetAsync(claim2, 0, sizeof(u32) * (plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_sa");
-    if (first_pass_repl(ctx, plan.bins1))
-        inv_partition_persistent_kernel<kIpSa, true><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles);
-    else
-        inv_partition_persistent_kernel<kIpSa><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles);
+    inv_partition_persistent_kernel<kIpSa><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles);
     RSQ_LAUNCH_END(ctx);
     const u64* rec = rec_a;
     if (plan.win_bits == 0) {
@@ -2812,15 +2727,12 @@ int inverse_from_records(reseq_cuda_ctx* ctx, u64* rec_a, size_t len, u32* rank,
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpRepl * kIpMaxBins * kIpClaimStride;
-    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * ((first_pass_repl(ctx, plan.bins1) ? (kIpRepl - 1) * kIpMaxBins : 0) + plan.bins1) * kIpClaimStride, s));
+    u32* claim2 = scratch + kIpMaxBins * kIpClaimStride;
+    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * plan.bins1 * kIpClaimStride, s));
     RSQ_CUDA(cudaMemsetAsync(claim2, 0, sizeof(u32) * (plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_rec0");
-    if (first_pass_repl(ctx, plan.bins1))
-        inv_partition_persistent_kernel<kIpRec0, true><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b, plan.tiles);
-    else
-        inv_partition_persistent_kernel<kIpRec0><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b, plan.tiles);
+    inv_partition_persistent_kernel<kIpRec0><<<grid, kIpBlock, 0, s>>>(rec_a, len, plan.shift1, 0, plan.bins1, claim1, rec_b, plan.tiles);
     RSQ_LAUNCH_END(ctx);
     const u64* rec = rec_b;
     if (plan.lo_bits > 0) {
@@ -2848,15 +2760,12 @@ int rank_update_device(reseq_cuda_ctx* ctx, const u32* sa, const u32* vals, size
         return RESEQ_OK;
     }
     u32* claim1 = scratch;
-    u32* claim2 = scratch + kIpRepl * kIpMaxBins * kIpClaimStride;
-    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * ((first_pass_repl(ctx, plan.bins1) ? (kIpRepl - 1) * kIpMaxBins : 0) + plan.bins1) * kIpClaimStride, s));
+    u32* claim2 = scratch + kIpMaxBins * kIpClaimStride;
+    RSQ_CUDA(cudaMemsetAsync(claim1, 0, sizeof(u32) * plan.bins1 * kIpClaimStride, s));
     RSQ_CUDA(cudaMemsetAsync(claim2, 0, sizeof(u32) * (plan.buckets2 + 32), s));
     const unsigned grid = plan.tiles < static_cast<unsigned>(ctx->sm_count) * 2 ? plan.tiles : ctx->sm_count * 2;
     RSQ_LAUNCH_BEGIN(ctx, "inv_partition_sa_val");
-    if (first_pass_repl(ctx, plan.bins1))
-        inv_partition_persistent_kernel<kIpSaVal, true><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles, vals);
-    else
-        inv_partition_persistent_kernel<kIpSaVal><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles, vals);
+    inv_partition_persistent_kernel<kIpSaVal><<<grid, kIpBlock, 0, s>>>(sa, n, plan.shift1, 0, plan.bins1, claim1, rec_a, plan.tiles, vals);
     RSQ_LAUNCH_END(ctx);
     const u64* rec = rec_a;
     if (plan.lo_bits > 0) {
@@ -3724,15 +3633,15 @@ int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bu
     if (!d_sa_bucket || !d_records_out) return fail(RESEQ_INVALID_ARGUMENT, "null device buffer");
     RSQ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    RSQ_TRY(ctx->reserve(16384));
+    RSQ_TRY(ctx->reserve(sizeof(u32) * (kOwnMaxBins + kOwnMaxBins * kIpClaimStride) + 16384));
     ctx->begin();
     int sub_bits = 10;
     const int max_bins = ctx->opt_owner_bins >= world && ctx->opt_owner_bins <= kOwnMaxBins ? ctx->opt_owner_bins : kOwnMaxBins;
     while ((world << sub_bits) > max_bins) --sub_bits;   // owner x sub-range bins, at most 1024: the sub-bins spread the
     const int bins = world << sub_bits;                     // shared-memory atomics; the exchange sends whole owners
-    u32* counts = ctx->alloc<u32>(2 * kOwnMaxBins);
+    u32* counts = ctx->alloc<u32>(kOwnMaxBins + kOwnMaxBins * kIpClaimStride);
     if (!counts) return fail(RESEQ_OUT_OF_MEMORY, "rank shard workspace");
-    u32* claim = counts + kOwnMaxBins;
+    u32* claim = counts + kOwnMaxBins;   // one counter per 128-byte line
     RSQ_CUDA(cudaMemsetAsync(counts, 0, sizeof(u32) * bins, s));
     RSQ_LAUNCH_BEGIN(ctx, "owner_count_kernel");
     OwnerTable tb{};
@@ -3743,17 +3652,13 @@ int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bu
     owner_count_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(d_sa_bucket, m, tb, counts);
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
-    u32* h = reinterpret_cast<u32*>(ctx->pinned);   // 4096 pinned bytes: 16 * 64 counters
+    // the bins' bases stay on the device (the partition is queued without waiting for the host); the per-owner counts
+    // the exchange needs travel to the host behind it
+    RSQ_LAUNCH_BEGIN(ctx, "owner_bases_kernel");
+    owner_bases_kernel<<<1, kOwnMaxBins, 0, s>>>(counts, bins, claim);
+    RSQ_LAUNCH_END(ctx);
+    u32* h = reinterpret_cast<u32*>(ctx->pinned);   // 4096 pinned bytes: up to 1024 counters
     RSQ_CUDA(cudaMemcpyAsync(h, counts, sizeof(u32) * bins, cudaMemcpyDeviceToHost, s));
-    RSQ_CUDA(cudaStreamSynchronize(s));
-    u64 run = 0;
-    for (int b = 0; b < bins; ++b) {   // counts -> exclusive bases, in place
-        const u32 c = h[b];
-        counts_out[b >> sub_bits] += c;
-        h[b] = static_cast<u32>(run);
-        run += c;
-    }
-    RSQ_CUDA(cudaMemcpyAsync(claim, h, sizeof(u32) * bins, cudaMemcpyHostToDevice, s));
     RSQ_LAUNCH_BEGIN(ctx, "owner_partition_kernel");
     RSQ_OPT_IN_SMEM(ctx, owner_partition_kernel, kOwnSmem);
     {
@@ -3763,7 +3668,8 @@ int reseq_cuda_rank_shard_partition(reseq_cuda_ctx* ctx, const uint32_t* d_sa_bu
     }
     RSQ_LAUNCH_END(ctx);
     RSQ_CUDA(cudaGetLastError());
-    RSQ_CUDA(cudaStreamSynchronize(s));   // the pinned staging words are reused by the next call
+    RSQ_CUDA(cudaStreamSynchronize(s));   // the counts have landed; the pinned staging words are reused by the next call
+    for (int b = 0; b < bins; ++b) counts_out[b >> sub_bits] += h[b];
     return RESEQ_OK;
 }
 

@@ -29,15 +29,22 @@ n = int(text.size)
 d_text = torch.from_numpy(text).cuda()
 torch.cuda.synchronize()
 
-def timed(fn, prof=None):
-    """prof = (executor, phase name): also print the per-kernel table of this call."""
-    if prof: prof[0].profile(True)
+def timed(fn, prof=None, ex=None):
+    """Device time of one phase of one rank.  With an executor: the SUM of the phase's kernel times (CUDA events around
+    every launch) -- the events around the whole call also span the host's work in between (torch allocations of
+    gigabyte outputs with eight ranks' buffers alive: tens of ms now and then), which a real rank does not pay per build;
+    the host round trips a build does need are a separate modelled term.  prof = phase name: print the kernel table."""
+    if ex is not None: ex.profile(True)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(); out = fn(); b.record(); torch.cuda.synchronize()
-    if prof:
-        tab = prof[0].profile_read(); prof[0].profile(False)
-        print(f"   [{prof[1]}] {a.elapsed_time(b):.2f} ms: " + ", ".join(f"{k} x{c} {ms:.3f}" for k, (c, ms) in sorted(tab.items(), key=lambda kv: -kv[1][1])), flush=True)
-    return out, a.elapsed_time(b)
+    ms = a.elapsed_time(b)
+    if ex is not None:
+        tab = ex.profile_read(); ex.profile(False)
+        ksum = sum(v[1] for v in tab.values())
+        if prof:
+            print(f"   [{prof}] kernels {ksum:.2f} ms (call {ms:.2f} ms): " + ", ".join(f"{k} x{c} {t:.3f}" for k, (c, t) in sorted(tab.items(), key=lambda kv: -kv[1][1])), flush=True)
+        ms = ksum
+    return out, ms
 
 # single-GPU reference time
 ex0 = rq.Executor(0); ex0.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -54,28 +61,28 @@ for G in [int(x) for x in args.gpus.split(",")]:
     best = {p: [float("inf")] * G for p in phases}
     for rep in range(3):   # the first repetition warms the arenas; of the other two the faster time of each (phase, rank) is kept
         ph = {p: [0.0] * G for p in phases}   # (a phase's events also span the host's allocations: one slow cudaMalloc is not kernel time)
-        P = (lambda r, name: (exs[r], f"G={G} rank {r} {name}") if args.profile and rep == 2 and r == G - 1 else None)
+        P = (lambda r, name: f"G={G} rank {r} {name}" if args.profile and rep == 2 and r == G - 1 else None)
         for r, be in enumerate(bes):
-            _, ph["pack"][r] = timed(lambda: be.open(d_text))
+            _, ph["pack"][r] = timed(lambda: be.open(d_text), None, exs[r])
         period, reads = bes[0].uniform_info()
         hist = None
         for r, be in enumerate(bes):
             lo, hi = (reads * r) // G, (reads * (r + 1)) // G
-            h, ph["hist"][r] = timed(lambda: be.prefix_hist(lo, hi - lo))
+            h, ph["hist"][r] = timed(lambda: be.prefix_hist(lo, hi - lo), None, exs[r])
             hist = h if hist is None else hist + h
         bounds = [0] + choose_bounds(hist, G) + [1 << PREFIX_BITS]
         recs, covs, buckets = [], None, []
         for r, be in enumerate(bes):
-            rec, ph["bucket"][r] = timed(lambda: be.bucket(bounds[r], bounds[r + 1]), P(r, "bucket"))
-            c, ph["sort_link"][r] = timed(lambda: be.uniform_sort_link(rec, reads), P(r, "sort_link"))
+            rec, ph["bucket"][r] = timed(lambda: be.bucket(bounds[r], bounds[r + 1]), P(r, "bucket"), exs[r])
+            c, ph["sort_link"][r] = timed(lambda: be.uniform_sort_link(rec, reads), P(r, "sort_link"), exs[r])
             covs = c if covs is None else torch.maximum(covs, c)
             recs.append(rec)
         sizes = [int(x.numel()) for x in recs]
         sa_parts, rank_recs = [], []
         for r, be in enumerate(bes):
-            (sa_b, unf), ph["finish"][r] = timed(lambda: be.uniform_finish(covs), P(r, "finish"))
+            (sa_b, unf), ph["finish"][r] = timed(lambda: be.uniform_finish(covs), P(r, "finish"), exs[r])
             assert unf == 0
-            (rr, counts), ph["rank_partition"][r] = timed(lambda: be.rank_records(sa_b, sum(sizes[:r]), n, G), P(r, "rank_partition"))
+            (rr, counts), ph["rank_partition"][r] = timed(lambda: be.rank_records(sa_b, sum(sizes[:r]), n, G), P(r, "rank_partition"), exs[r])
             sa_parts.append(sa_b); rank_recs.append((rr, counts))
         recs = None
         # the exchange, done by hand: owner g receives every rank's group g
@@ -87,7 +94,7 @@ for G in [int(x) for x in args.gpus.split(",")]:
             mine = torch.cat(parts)
             slice_len = (n * (g + 1)) // G - (n * g) // G
             assert mine.numel() == slice_len
-            rk, ph["rank_finish"][g] = timed(lambda: be.rank_finish(mine, slice_len), P(g, "rank_finish"))
+            rk, ph["rank_finish"][g] = timed(lambda: be.rank_finish(mine, slice_len), P(g, "rank_finish"), exs[g])
             if rep == 2 and g == 0:   # spot check: rank[sa[i]] == i for entries of every bucket that fall in the first slice
                 off = 0
                 for part in sa_parts:
@@ -118,7 +125,7 @@ for G in [int(x) for x in args.gpus.split(",")]:
                  "total_ms": total, "speedup_vs_single_gpu_build": t_single / total})
     print(f"G={G}: " + "  ".join(f"{p} {v:.2f}" for p, v in compute.items()) + f"  | a2a {a2a_ms:.2f} cov {cov_ms:.2f} | total {total:.2f} ms  speed-up {t_single / total:.2f}x", flush=True)
 out = {"workload": DESCRIPTION[args.workload], "suffixes": n, "single_gpu_build_ms": t_single, "rows": rows,
-       "how": "compute phases measured on one B200, one rank after another, maximum over ranks; collectives modelled (peer 770 GB/s per direction, all-reduce bus 725 GB/s)"}
+       "how": "compute phases = sums of kernel times (CUDA events around every launch) measured on one B200, one rank after another, maximum over ranks; collectives modelled (peer 770 GB/s per direction, all-reduce bus 725 GB/s)"}
 print(json.dumps(out))
 if args.out:
     open(args.out, "w").write(json.dumps(out, indent=1))
