@@ -1024,30 +1024,45 @@ gen_uniform_kernel(const u64* __restrict__ packed, u32 period, u64 read0, u64 k,
     const u64 r0 = static_cast<u64>(blockIdx.x) * kUniReads;   // within the slice
     const u32 nr = static_cast<u32>(k - r0 < kUniReads ? k - r0 : kUniReads);
     const u32 bit0 = stage_reads(packed, s_w, read0 + r0, nr, period);   // one TMA bulk load + the block barrier
-    const u32 total = kUniReads * period;
-    for (u32 idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const u32 rl = idx & (kUniReads - 1), t = idx / kUniReads;    // lanes = consecutive reads: coalesced stores
-        if (rl >= nr) continue;
-        const u32 pl = rl * period + (period - 1 - t);
-        const u32 bit = bit0 + 2 * pl;
-        const u32 wi = bit >> 6, sh = bit & 63;
-        const u64 hi = s_w[wi], lo = s_w[wi + 1];
-        const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
-        u32 key = static_cast<u32>(win >> 32);                          // 16 bases
-        if (t < kUniK) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;   // zero padded from the sentinel on
-        const u64 pos = (read0 + r0 + rl) * period + (period - 1 - t);
-        elems[static_cast<u64>(t) * k + r0 + rl] = (static_cast<u64>(key) << 32) | pos;
-        // One histogram serves all four passes: digit j of a suffix (bases 4j..4j+3 of its window,
-        // zero padded) is the TOP digit of the suffix 4j positions further into the same read, and 0
-        // if there is none.  So H_j = A - B_j + [0] * 4jk, A = top-digit histogram of all suffixes,
-        // B_j = that of the suffixes at the first 4j offsets of a read (8 % of them); see
-        // uniform_hist_kernel.  Rows here: [3] = A, [2] = B_1, [1] = B_2, [0] = B_3.
-        const u32 top = key >> 24, o = period - 1 - t;
-        atomicAdd(&s_hist[3 * kRadix + top], 1u);
-        if (o < 12) {
-            atomicAdd(&s_hist[top], 1u);
-            if (o < 8) atomicAdd(&s_hist[kRadix + top], 1u);
-            if (o < 4) atomicAdd(&s_hist[2 * kRadix + top], 1u);
+    // Thread = (read rl, quarter q of its offsets): consecutive offsets of one read, so the 16-base key comes from a
+    // window that slides two bits per suffix (refilled from shared memory every 16 offsets) instead of a fresh
+    // two-word extraction per suffix; at a given step the lanes of a warp are consecutive reads at one offset: the
+    // stores stay coalesced.  (One strided (read, t) item per trip: 45 instructions per suffix, the kernel was bound
+    // by issue slots at 0.63 of the HBM peak.)
+    const u32 rl = threadIdx.x & (kUniReads - 1), q = threadIdx.x / kUniReads;
+    constexpr u32 kQuarters = 256 / kUniReads;
+    static_assert(kQuarters * kUniReads == 256, "gen_uniform_kernel runs 256 threads");
+    const u32 per = (period + kQuarters - 1) / kQuarters;
+    const u32 o_begin = q * per, o_end = o_begin + per < period ? o_begin + per : period;
+    if (rl < nr) {
+        const u32 read_bit0 = bit0 + 2 * rl * period;
+        const u64 pos0 = (read0 + r0 + rl) * period;
+        u64* dst = elems + r0 + rl;
+        u64 win = 0;
+        for (u32 o = o_begin; o < o_end; ++o) {
+            if (((o - o_begin) & 15u) == 0) {
+                const u32 bit = read_bit0 + 2 * o;
+                const u32 wi = bit >> 6, sh = bit & 63;
+                const u64 hi = s_w[wi], lo = s_w[wi + 1];
+                win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+            }
+            const u32 t = period - 1 - o;
+            u32 key = static_cast<u32>(win >> 32);                          // 16 bases
+            win <<= 2;
+            if (t < kUniK) key = t ? key & ~((1u << (2 * (kUniK - t))) - 1u) : 0u;   // zero padded from the sentinel on
+            dst[static_cast<u64>(t) * k] = (static_cast<u64>(key) << 32) | (pos0 + o);
+            // One histogram serves all four passes: digit j of a suffix (bases 4j..4j+3 of its window,
+            // zero padded) is the TOP digit of the suffix 4j positions further into the same read, and 0
+            // if there is none.  So H_j = A - B_j + [0] * 4jk, A = top-digit histogram of all suffixes,
+            // B_j = that of the suffixes at the first 4j offsets of a read (8 % of them); see
+            // uniform_hist_kernel.  Rows here: [3] = A, [2] = B_1, [1] = B_2, [0] = B_3.
+            const u32 top = key >> 24;
+            atomicAdd(&s_hist[3 * kRadix + top], 1u);
+            if (o < 12) {
+                atomicAdd(&s_hist[top], 1u);
+                if (o < 8) atomicAdd(&s_hist[kRadix + top], 1u);
+                if (o < 4) atomicAdd(&s_hist[2 * kRadix + top], 1u);
+            }
         }
     }
     __syncthreads();
