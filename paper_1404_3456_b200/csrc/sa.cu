@@ -2648,13 +2648,14 @@ InversePlan make_inverse_plan(size_t n, int mode, int top_bits = -1) {
     }
     // The first pass gets at most 7 bits: its tiles all claim from the same `bins1` counters, and with 133 - 240 bins
     // it ran at 0.31 - 0.47 of the HBM peak against 0.57 with 67 - 97 (config 3: 0.60 -> 0.33 ms); the bits go to the
-    // second pass, whose claims spread over bucket x bin counters (<= 1024 bins), and to a 2^14-entry window.
+    // second pass, whose claims spread over bucket x bin counters (<= 1024 bins), and, above 2^27 records, to a
+    // 2^14-entry window.
     p.win_bits = 13;
     int rest = nb - p.win_bits;                               // bits the passes must consume
     const int top_max = top_bits > 0 && top_bits <= 10 ? top_bits : 7;   // tuning knob ("inverse_lo_bits" carries it)
     int top = rest < top_max ? rest : top_max;
     int lo = rest - top;
-    if (lo > 9) {                                             // n >= 2^30: 64 KB windows
+    if (lo > 7) {                                             // n > 2^27: 64 KB windows rather than 512+ second-pass bins (0.506 -> 0.479 ms at config 2)
         p.win_bits = 14;
         rest = nb - p.win_bits;
         top = rest < top_max ? rest : top_max;
