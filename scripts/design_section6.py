@@ -42,8 +42,9 @@ Other configurations, device-resident on one B200 (`profiles/r2_bench_c1.json`, 
 {row('C5 (3 Gbp read set, beyond the reference’s 2³¹−1 cap)', c5)}
 
 C1 also runs the query half: {ov1['queries'] / 1e6:.1f} M queries in {ov1['device_ms']:.2f} ms = {ov1['value'] / 1e3:.1f} Gq/s, index build {ov1['index_build_ms']:.1f} ms wall. End to end every
-configuration sits at the PCIe rate (n bytes in, 8n bytes out: ≈ 5 Gsuffix/s), the suffix array leaving on a second
-stream while its inverse is computed. At 1–3 G suffixes the refine kernel's share grows (2–8 % of the groups mix loci
+configuration sits at the PCIe rate (n bytes in, 8n bytes out: ≈ 5 Gsuffix/s; one of seven visits to the pool measured
+33 ms instead of 26–27 ms for config 2 with the same device time: the host side of the box), the suffix array leaving
+on a second stream while its inverse is computed. At 1–3 G suffixes the refine kernel's share grows (2–8 % of the groups mix loci
 once the genome has 10⁸ loci against 4.3 G keys, and the packed text — 755 MB at C5 — no longer sits in L2:
 {c5['roofline']['kernels']['refine_uniform_kernel']['ms_per_step']:.0f} of the {c5['ms_per_step']:.0f} ms; ncu: half of its stall samples are block barriers around steps that only a few dozen of a tile's
 2 048 suffixes take part in).
