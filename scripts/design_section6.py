@@ -12,7 +12,8 @@ per_kernel = tables[tables.index("| kernel | launches"):tables.index("CPU baseli
 sweep = tables[tables.index("Sweep ("):tables.index("config[3]: 1 Gbp")]
 scaling = tables[tables.index("config[3]: 1 Gbp"):]
 cb = b["cpu_baseline"]
-row = lambda name, d: f"| {name} | {d['config']['suffixes'] / 1e6:.2f} M | {d['ms_per_step']:.3g} | {d['value'] / 1e3:.1f} | {d['e2e']['ms_per_step']:.3g} ({d['e2e']['value'] / 1e3:.1f}) |"
+ms = lambda x: f"{x:.3f}" if x < 1 else (f"{x:.2f}" if x < 10 else (f"{x:.1f}" if x < 100 else f"{x:.0f}"))
+row = lambda name, d: f"| {name} | {d['config']['suffixes'] / 1e6:.2f} M | {ms(d['ms_per_step'])} | {d['value'] / 1e3:.1f} | {ms(d['e2e']['ms_per_step'])} ({d['e2e']['value'] / 1e3:.1f}) |"
 g8 = lambda m: next(r for r in m["rows"] if r["G"] == 8)
 r8 = g8(m5)
 ph = r8["phase_ms_max_over_ranks"]
