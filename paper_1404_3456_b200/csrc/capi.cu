@@ -177,6 +177,7 @@ int reseq_cuda_ctx_create(int device, reseq_cuda_ctx** out) {
     if (const char* e = std::getenv("RESEQ_SORT_PRMT")) ctx->opt_sort_prmt = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_OWNER_BINS")) ctx->opt_owner_bins = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_ACCEPT_QUADS")) ctx->opt_accept_quads = std::atoi(e);
+    if (const char* e = std::getenv("RESEQ_ACCEPT_EXC")) ctx->opt_accept_exc = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_OVERLAP_STAGE")) ctx->opt_overlap_stage = std::atoi(e);
     if (const char* e = std::getenv("RESEQ_LOOKAHEAD")) {
         const int v = std::atoi(e);

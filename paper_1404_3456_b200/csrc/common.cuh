@@ -70,6 +70,7 @@ struct reseq_cuda_ctx {
     int opt_overlap_stage = 0; // overlap search: a fragment's rank block + packed text staged in shared memory by TMA, double buffered (measured slower: off)
     int opt_sort_tma = 0;      // onesweep: full tiles loaded by one TMA bulk copy (measured 4 % slower than per-thread loads: off)
     int opt_sort_prmt = 1;     // onesweep: byte-aligned 8-bit digits of the upper key word extracted by one PRMT (0: shift + mask)
+    int opt_accept_exc = 1;    // uniform route, accept pass: no proof-byte gather for t <= L - 64 when the reads with shorter proofs fit a 16-entry list
     int opt_accept_quads = 1;  // uniform route, accept pass: a thread owns four consecutive records (0: pairs)
     int opt_owner_bins = 128;   // rank exchange: owner x sub-range bins of the sender's partition pass (378 M positions, 8 owners: 1024 bins 2.58 ms, 256 2.33, 128 1.88, 32 1.80)
     int opt_lookback_pack = 1; // two digits per look-back descriptor word when n < 2^30 (0: always one)

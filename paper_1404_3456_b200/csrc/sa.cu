@@ -1231,11 +1231,26 @@ accept_uniform_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict
 // 34 % of its stall samples on the shuffle queue (mio_throttle + short scoreboard, profiles/r2_ncu_full_accept.txt).
 // Measured [B200, config 2]: pairs 0.657 ms, quads (W = 4) 0.613 ms, W = 8 (a whole bitmap byte per thread, no byte
 // shuffle, but 128-bit loads 64 bytes apart within a warp) 0.697 ms.
-template <int W>
+// Reads whose proof is SHORT (cov[read] < thr), as a 64-bit Bloom word: bit (read mod 64) of exc[0 .. 1].  At 30x
+// coverage a read's successor starts 5 bases on average, so with thr = L - 64 there are a handful of such reads (the
+// last ones of the genome) among a million; a suffix with t <= thr of a read whose bit is clear is proven
+// (t <= thr <= cov[read]) without looking its byte up -- 57 % of the gathers the accept pass is bound by; a set bit
+// (one read in ~20 shares it by chance) only means "look it up".  With many short proofs (low coverage) every bit is
+// set and every suffix gathers, as before.
+constexpr u32 kCovExcMargin = 64;
+__global__ void __launch_bounds__(256)
+cov_exceptions_kernel(const u8* __restrict__ cov, u64 reads, u32 thr, u32* __restrict__ exc) {
+    const u64 r = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r < reads && cov[r] < thr) atomicOr(exc + ((r >> 5) & 1u), 1u << (r & 31u));
+}
+
+template <int W, bool EXC>
 __global__ void __launch_bounds__(256, 4)
 accept_uniform_quads_kernel(const u64* __restrict__ elems, u64 m, const u8* __restrict__ cov, u32 period,
                             u64 period_magic, u32* __restrict__ sa_out, u32* __restrict__ headbits,
-                            u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
+                            u32* __restrict__ uncbits, u8* __restrict__ tileflags, const u32* __restrict__ exc, u32 thr) {
+    u32 bloom0 = 0xffffffffu, bloom1 = 0xffffffffu;
+    if constexpr (EXC) { bloom0 = exc[0]; bloom1 = exc[1]; }
     static_assert(W == 4 || W == 8, "four or eight consecutive records per thread");
     constexpr u32 K = kUniK;
     constexpr int R = 8 / W;                        // rows per thread in flight
@@ -1279,7 +1294,13 @@ accept_uniform_quads_kernel(const u64* __restrict__ elems, u64 m, const u8* __re
 #pragma unroll
         for (int c = 0; c < R; ++c)
 #pragma unroll
-            for (int j = 0; j < W; ++j) cv[c][j] = i0 + c * kRow + W * lane + j < m ? __ldg(cov + q[c][j]) : 0;
+            for (int j = 0; j < W; ++j) {
+                const bool in = i0 + c * kRow + W * lane + j < m;
+                const u32 qq = q[c][j];
+                bool need = true;
+                if constexpr (EXC) need = t[c][j] > thr || ((((qq & 32u) ? bloom1 : bloom0) >> (qq & 31u)) & 1u);
+                cv[c][j] = in ? (need ? __ldg(cov + qq) : static_cast<u8>(255)) : 0;
+            }
 #pragma unroll
         for (int c = 0; c < R; ++c) {
             const u64 i = i0 + c * kRow + W * lane;
@@ -2855,7 +2876,8 @@ int uniform_verdict(reseq_cuda_ctx* ctx, const u32* counters, size_t m, u32 peri
 // group is proven, the others are re-sorted; *unfinished != 0 sends the caller to the general paths.
 int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sent, size_t n_text, u32 period,
                           const u64* sorted, size_t m, const u8* cov, u32* headbits, u32* uncbits, u32* sa_out,
-                          int max_rounds, u32* counters, reseq_sa_stats* st, u64* unfinished, bool defer_verdict = false) {
+                          int max_rounds, u32* counters, reseq_sa_stats* st, u64* unfinished, bool defer_verdict = false,
+                          u32* exc = nullptr) {
     cudaStream_t s = ctx->stream;
     const u64 magic = ~0ull / period + 1;
     RSQ_LAUNCH_BEGIN(ctx, "accept_uniform_kernel");
@@ -2863,9 +2885,20 @@ int uniform_accept_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* sen
     RSQ_CUDA(cudaMemsetAsync(tileflags, 0, m / kRefTile + 2, s));
     if ((reinterpret_cast<uintptr_t>(sorted) & 15) || (reinterpret_cast<uintptr_t>(sa_out) & 7))
         return fail(RESEQ_INVALID_ARGUMENT, "record and suffix-array buffers must be 16- / 8-byte aligned");
-    if (ctx->opt_accept_quads != 0 && (reinterpret_cast<uintptr_t>(sa_out) & 15) == 0)
-        accept_uniform_quads_kernel<4><<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
-                                                                                  uncbits, tileflags);
+    if (ctx->opt_accept_quads != 0 && (reinterpret_cast<uintptr_t>(sa_out) & 15) == 0) {
+        const bool use_exc = exc != nullptr && ctx->opt_accept_exc != 0 && period - 1u >= 2 * kCovExcMargin;
+        const u32 thr = use_exc ? period - 1u - kCovExcMargin : 0u;
+        if (use_exc) {
+            const u64 reads = n_text / period;
+            cov_exceptions_kernel<<<static_cast<unsigned>((reads + 255) / 256), 256, 0, s>>>(cov, reads, thr, exc);
+        }
+        if (use_exc)
+            accept_uniform_quads_kernel<4, true><<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
+                                                                                            uncbits, tileflags, exc, thr);
+        else
+            accept_uniform_quads_kernel<4, false><<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
+                                                                                             uncbits, tileflags, nullptr, 0u);
+    }
     else
         accept_uniform_kernel<<<grid_for(ctx, m, 256, 8, 8), 256, 0, s>>>(sorted, m, cov, period, magic, sa_out, headbits,
                                                                          uncbits, tileflags);
@@ -2916,6 +2949,7 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
         RSQ_LAUNCH_END(ctx);
     }
     RSQ_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(u32) * 4 * kRadix, s));
+    RSQ_CUDA(cudaMemsetAsync(counters + 60, 0, sizeof(u32) * 2, s));   // the accept pass's Bloom word of short proofs
     RSQ_CUDA(cudaMemsetAsync(cov, 0, k, s));
     RSQ_LAUNCH_BEGIN(ctx, "uniform_check_kernel");
     uniform_check_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, s>>>(sent, period, k, counters + 3);
@@ -2930,8 +2964,9 @@ int uniform_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* s
     RSQ_CUDA(cudaGetLastError());
     const u64* sorted = nullptr;
     RSQ_TRY(uniform_sort_link(ctx, packed, period, elems_a, elems_b, n, true, whole, cov, counters, ws, st, &sorted));
+    // (counters + 60, + 61: the Bloom word of short proofs; the whole table `cov` is this device's)
     return uniform_accept_refine(ctx, packed, sent, n, period, sorted, n, cov, headbits, uncbits, sa_out, max_rounds,
-                                 counters, st, unfinished, defer_verdict);
+                                 counters, st, unfinished, defer_verdict, counters + 60);
 }
 
 // The ragged read-set route on one device.  *applicable = false: not this kind of text (a read longer
