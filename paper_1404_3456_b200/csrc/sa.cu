@@ -1402,15 +1402,22 @@ maxlen_kernel(const u32* __restrict__ ends, u64 k, u32* __restrict__ out) {
 // its sentinel (t <= len).  The trip count is the same for every lane (f may vote).
 template <class F>
 __device__ __forceinline__ void for_each_suffix_ragged(const u64* __restrict__ s_w, u32 bit0, u32 len, u32 tmax, F f) {
+    // The read's suffixes come in offset order (t falls, the offset len - t rises), so the 15-base key comes from a
+    // window that slides two bits per suffix; it is refilled at the read's first suffix and wherever t = 15 mod 16 (the
+    // same trips for every lane), instead of two shared-memory words and a funnel shift per suffix.
+    u64 win = 0;
     for (int t = static_cast<int>(tmax); t >= 0; --t) {
         const bool active = static_cast<u32>(t) <= len;
         u32 key = 0;
         if (active) {
-            const u32 bit = bit0 + 2 * (len - t);
-            const u32 wi = bit >> 6, sh = bit & 63;
-            const u64 hi = s_w[wi], lo = s_w[wi + 1];
-            const u64 win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+            if ((t & 15) == 15 || static_cast<u32>(t) == len) {
+                const u32 bit = bit0 + 2 * (len - t);
+                const u32 wi = bit >> 6, sh = bit & 63;
+                const u64 hi = s_w[wi], lo = s_w[wi + 1];
+                win = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+            }
             u32 b15 = static_cast<u32>(win >> 34);                                        // 15 bases
+            win <<= 2;
             if (t < kRagK) b15 = t ? b15 & ~((1u << (2 * (kRagK - t))) - 1u) : 0u;        // zero padded from the sentinel on
             key = (b15 << 2) | (t >= kRagK ? 1u : 0u);
         }
