@@ -74,6 +74,6 @@ overhead when there is nobody to exchange with.
 
 """
 s = open("DESIGN.md").read()
-a, z = s.index("Per kernel (CUDA events around every launch"), s.index("## 7. Install note for the reference arm")
+a, z = s.index("Per kernel (CUDA events around every launch"), s.index("### Tuning knobs")
 open("DESIGN.md", "w").write(s[:a] + head + per_kernel + other + s[z:])
 print("section 6 rewritten:", b["ms_per_step"], c1["ms_per_step"], c4["ms_per_step"], c5["ms_per_step"], r8["speedup_vs_single_gpu_build"])
