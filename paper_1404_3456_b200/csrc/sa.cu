@@ -1661,6 +1661,78 @@ accept_ragged_kernel(const u64* __restrict__ elems, u64 m, const u32* __restrict
     }
 }
 
+// The same pass with a thread owning four consecutive records (see accept_uniform_quads_kernel): three of four
+// neighbour relations stay in registers, a quad's outer neighbours cost two shuffles, its eight flag bits one.
+__global__ void __launch_bounds__(256)
+accept_ragged_quads_kernel(const u64* __restrict__ elems, u64 m, const u32* __restrict__ covbits, u32* __restrict__ sa_out,
+                           u32* __restrict__ headbits, u32* __restrict__ uncbits, u8* __restrict__ tileflags) {
+    constexpr int R = 2;
+    constexpr u64 kRow = 128, kSpan = kRow * R;
+    const unsigned lane = lane_id();
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    u8* hbytes = reinterpret_cast<u8*>(headbits);
+    u8* ubytes = reinterpret_cast<u8*>(uncbits);
+    for (u64 i0 = ((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kSpan; i0 < m; i0 += warps * kSpan) {
+        u32 k[R][4], p[R][4], kp[R], kn[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            const u64 i = i0 + c * kRow + 4 * lane;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                ulonglong2 v = make_ulonglong2(0, 0);
+                if (i + 2 * h + 1 < m) v = *reinterpret_cast<const ulonglong2*>(elems + i + 2 * h);
+                else if (i + 2 * h < m) v.x = elems[i + 2 * h];
+                k[c][2 * h] = static_cast<u32>(v.x >> 32); p[c][2 * h] = static_cast<u32>(v.x);
+                k[c][2 * h + 1] = static_cast<u32>(v.y >> 32); p[c][2 * h + 1] = static_cast<u32>(v.y);
+            }
+            kp[c] = 0; kn[c] = 0;
+            if (lane == 0 && i > 0 && i < m) kp[c] = static_cast<u32>(elems[i - 1] >> 32);
+            if (lane == 31 && i + 4 < m) kn[c] = static_cast<u32>(elems[i + 4] >> 32);
+        }
+        u32 cb[R][4];   // the proof bits, gathered up front
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                cb[c][j] = i0 + c * kRow + 4 * lane + j < m ? (__ldg(covbits + (p[c][j] >> 5)) >> (p[c][j] & 31u)) & 1u : 0u;
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            const u64 i = i0 + c * kRow + 4 * lane;
+            const u32 ku = __shfl_up_sync(0xffffffffu, k[c][3], 1), kd = __shfl_down_sync(0xffffffffu, k[c][0], 1);
+            if (lane != 0) kp[c] = ku;
+            if (lane != 31) kn[c] = kd;
+            u32 hn = 0, un = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool in = i + j < m;
+                const u32 kprev = j ? k[c][j ? j - 1 : 0] : kp[c], knext = j < 3 ? k[c][j < 3 ? j + 1 : j] : kn[c];
+                const bool shrt = (k[c][j] & 3u) == 0;
+                // (equal keys carry equal tags: "the neighbour is short" needs no test of its own)
+                const bool head = in && (i + j == 0 || k[c][j] != kprev || shrt);
+                const bool last = i + j + 1 >= m || knext != k[c][j] || shrt;
+                const bool unc = in && !last && !shrt && !cb[c][j];
+                hn |= static_cast<u32>(head) << j;
+                un |= static_cast<u32>(unc) << j;
+            }
+            if (i + 3 < m) *reinterpret_cast<uint4*>(sa_out + i) = make_uint4(p[c][0], p[c][1], p[c][2], p[c][3]);
+            else
+                for (int j = 0; j < 4; ++j)
+                    if (i + j < m) sa_out[i + j] = p[c][j];
+            u32 x = (hn | (un << 8)) << (4 * (lane & 1));
+            x |= __shfl_xor_sync(0xffffffffu, x, 1);
+            if ((lane & 1) == 0 && i < m) {
+                hbytes[i >> 3] = static_cast<u8>(x);
+                ubytes[i >> 3] = static_cast<u8>(x >> 8);
+                if ((x >> 8) & 0xffu) {
+                    const u64 tile = i / kRefTile;
+                    tileflags[tile] = 1;
+                    if (tile) tileflags[tile - 1] = 1;
+                }
+            }
+        }
+    }
+}
+
 // rank = inverse permutation of sa.  A direct scatter rank[sa[i]] = i is n random 4-byte
 // writes, each a DRAM read-modify-write of a whole sector (measured 5.9 ms at n = 139 M).
 // Instead the (sa[i] << 32 | i) records are first partitioned by the top bits of sa[i] -- two
@@ -3049,7 +3121,10 @@ int ragged_sort_and_refine(reseq_cuda_ctx* ctx, const u64* packed, const u64* se
     if ((reinterpret_cast<uintptr_t>(sorted) & 15) || (reinterpret_cast<uintptr_t>(sa_out) & 7))
         return fail(RESEQ_INVALID_ARGUMENT, "record and suffix-array buffers must be 16- / 8-byte aligned");
     RSQ_LAUNCH_BEGIN(ctx, "accept_ragged_kernel");
-    accept_ragged_kernel<<<grid_for(ctx, n, 256, 8, 8), 256, 0, s>>>(sorted, n, covbits, sa_out, headbits, uncbits, tileflags);
+    if (ctx->opt_accept_quads != 0 && (reinterpret_cast<uintptr_t>(sa_out) & 15) == 0)
+        accept_ragged_quads_kernel<<<grid_for(ctx, n, 256, 8, 8), 256, 0, s>>>(sorted, n, covbits, sa_out, headbits, uncbits, tileflags);
+    else
+        accept_ragged_kernel<<<grid_for(ctx, n, 256, 8, 8), 256, 0, s>>>(sorted, n, covbits, sa_out, headbits, uncbits, tileflags);
     RSQ_LAUNCH_END(ctx);
     RSQ_OPT_IN_SMEM(ctx, refine_elems_kernel<kRefRagged>, kRefSmem);
     const unsigned rtiles = static_cast<unsigned>((n + kRefTile - 1) / kRefTile);
